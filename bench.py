@@ -1,0 +1,369 @@
+#!/usr/bin/env python
+"""Decode throughput of the B200 MoE-Gen engine (BASELINE.json metric: decode tokens/sec at
+prompt 512 / gen 256; expert GEMM tensor-pipe utilisation) on the Mixtral-8x7B shape, 1 B200
+resident (BASELINE.json configs[1]).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference] [--batch B]
+
+A step = one full decode phase of one batch: B sequences x 256 greedy decode forwards at
+positions 512..767 (the reference's accounting: B tokens per decode forward,
+plan_search.py:62-65), replayed as CUDA graphs.  Prefill is excluded from the metric; its KV state
+is synthetic (counter-based values in every page).  Weights are random-init (counter-based, in
+HBM).  Under torchrun each rank runs an independent replica (Mixtral-8x7B fits one GPU:
+"replicas only"); value = all ranks' tokens / max-over-ranks time.
+
+--impl reference times the CPU restatement of the same path (oracle/, the reference ships no
+numeric implementation) on the host cores: one Mixtral-8x7B decoder layer decode step of B
+sequences at mid-decode context, scaled by the layer count.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "decode tokens/sec at prompt 512/gen 256"
+UNIT = "tokens/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), float(p.get("bf16_tflops_sustained", p["bf16_tflops"])), "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows: list[list[str]] = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                for line in out.stdout.strip().splitlines():
+                    self.rows.append([c.strip() for c in line.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self) -> dict:
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[5:9]) if v.strip().lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws > 1:
+        import torch.distributed as dist
+
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        dist.init_process_group(backend)
+        return dist, dist.get_rank(), ws, int(os.environ.get("LOCAL_RANK", "0"))
+    return None, 0, 1, 0
+
+
+def _max_over_ranks(dist, v: float) -> float:
+    if dist is None:
+        return v
+    t = torch.tensor([v], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------------------------------------
+# CPU arm (oracle port): one decoder layer decode step of B sequences, x L layers
+# ------------------------------------------------------------------------------------------
+def cpu_layer_sample(arch, B: int, ctx: int, reps: int, threads: int) -> tuple[float, str]:
+    from oracle import moe_ref as R
+
+    torch.set_num_threads(threads)
+    a = arch
+    d, hd = a.hidden, a.head_dim
+    g = torch.Generator().manual_seed(0)
+    bf = torch.bfloat16
+
+    def U(*shape, std=0.02):
+        return (torch.rand(*shape, generator=g) * 2 - 1).mul_(std * math.sqrt(3)).to(bf)
+
+    W = dict(ln1=torch.ones(d, dtype=bf), wq=U(a.n_heads * hd, d), wk=U(a.n_kv_heads * hd, d),
+             wv=U(a.n_kv_heads * hd, d), wo=U(d, a.n_heads * hd), ln2=torch.ones(d, dtype=bf),
+             router=U(a.n_experts, d), w_gate_up=U(a.n_experts, 2 * a.moe_ffn, d),
+             w_down=U(a.n_experts, d, a.moe_ffn))
+
+    class _W:
+        layers = [W]
+    orc = R.MixtralOracle.__new__(R.MixtralOracle)
+    orc.a, orc.w = a, _W()
+    kc = U(B, a.n_kv_heads, ctx - 1, hd, std=1.0)
+    vc = U(B, a.n_kv_heads, ctx - 1, hd, std=1.0)
+    x = U(B, d, std=1.0)
+    times = []
+    for r in range(reps + 1):
+        orc.k_cache, orc.v_cache = [kc], [vc]
+        t0 = time.perf_counter()
+        orc.layer_forward(0, x, ctx - 1)
+        times.append(time.perf_counter() - t0)
+    t_layer = statistics.median(times[1:])
+    sample = (f"oracle/moe_ref.py MixtralOracle.layer_forward: one {a.name} decoder layer, B={B} sequences, "
+              f"context {ctx}, bf16 torch-CPU, median of {reps}; tokens/s = B / (t_layer x {a.layers} layers)")
+    return B / (t_layer * a.layers), sample
+
+
+def run_reference(args, dist, rank, world) -> None:
+    from paper_2503_09716_b200.configs import get_arch
+
+    if rank != 0:
+        return
+    arch = get_arch(args.config)
+    threads = os.cpu_count() or 1
+    B = args.cpu_batch
+    ctx = args.prompt_len + args.decode_len // 2
+    vals = []
+    sample = ""
+    for _ in range(args.warmup):
+        cpu_layer_sample(arch, B, ctx, 1, threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        v, sample = cpu_layer_sample(arch, B, ctx, 1, threads)
+        vals.append(v)
+    wall = time.perf_counter() - t0
+    value = statistics.median(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / max(1, args.steps),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic", "config": {"workload": f"{arch.name} decode, prompt {args.prompt_len} / gen "
+                                                        f"{args.decode_len}", "batch": B, "context": ctx},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------
+# GPU arm
+# ------------------------------------------------------------------------------------------
+def kernel_breakdown(eng, reps: int = 2) -> dict:
+    """Eager pass with CUDA events around every launch of one decode step (same stream as the
+    graph); returns {name: avg ms per launch, count per step}."""
+    from paper_2503_09716_b200 import ops
+
+    st = eng.stream
+    recs: dict[str, list[float]] = {}
+    orig = {n: getattr(ops, n) for n in ("moe_gemm_gate_up", "moe_gemm_down", "decode_attn_gqa", "router_topk",
+                                         "permute", "unpermute_combine", "add_rmsnorm", "rope_append_gqa",
+                                         "embed", "argmax", "decode_advance")}
+    pend: list[tuple[str, torch.cuda.Event, torch.cuda.Event]] = []
+
+    def wrap(name, fn):
+        def inner(*a, **k):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            fn(*a, **k)
+            e1.record(st)
+            pend.append((name, e0, e1))
+        return inner
+
+    mm = torch.mm
+
+    def mm_wrap(*a, **k):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        r = mm(*a, **k)
+        e1.record(st)
+        pend.append(("cublas_gemm", e0, e1))
+        return r
+
+    import paper_2503_09716_b200.engine as E
+    try:
+        for n, f in orig.items():
+            setattr(ops, n, wrap(n, f))
+        torch.mm = mm_wrap
+        saved = [t.clone() for t in (eng.buf.positions, eng.buf.step, eng.buf.next_ids, eng.buf.seq_lens)]
+        for _ in range(reps):
+            with torch.cuda.stream(st):
+                # park the stream so the host enqueues the whole step before the GPU starts:
+                # event gaps then measure kernels, not Python launch latency
+                torch.cuda._sleep(int(2e8))
+                pend.clear() if _ == 0 and False else None
+                eng._step(record=False)
+            torch.cuda.synchronize()
+        for t, s in zip((eng.buf.positions, eng.buf.step, eng.buf.next_ids, eng.buf.seq_lens), saved):
+            t.copy_(s)
+    finally:
+        for n, f in orig.items():
+            setattr(ops, n, f)
+        torch.mm = mm
+    for name, e0, e1 in pend:
+        recs.setdefault(name, []).append(e0.elapsed_time(e1))
+    return {n: {"avg_ms": sum(v) / len(v), "per_step": len(v) // reps, "ms_per_step": sum(v) / reps}
+            for n, v in recs.items()}
+
+
+def run_ours(args, dist, rank, world) -> None:
+    from paper_2503_09716_b200.configs import get_arch
+    from paper_2503_09716_b200.engine import Engine, resident_plan
+
+    torch.cuda.set_device(rank % torch.cuda.device_count())
+    arch = get_arch(args.config)
+    plan = resident_plan(arch, args.prompt_len, args.decode_len, B=args.batch, reserve_bytes=args.reserve_gb << 30)
+    eng = Engine(arch, plan, prompt_len=args.prompt_len, decode_len=args.decode_len, seed=0, use_graph=True)
+    B = eng.B
+    N = args.decode_len
+    eng.synthetic_prefill(seed=1)
+    first = torch.randint(0, arch.vocab, (B,), generator=torch.Generator().manual_seed(7))
+    first_pinned = first.to(torch.int32).pin_memory()
+    eng.capture()
+
+    def one_step():
+        eng.reset(args.prompt_len)
+        eng.buf.next_ids.copy_(first_pinned, non_blocking=True)
+        for _ in range(N):
+            eng.graph.replay()
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(args.steps):
+            one_step()
+        e1.record()
+        torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    t = _max_over_ranks(dist, e0.elapsed_time(e1) / 1e3)
+    tokens = B * N * args.steps * world
+    value = tokens / t
+
+    # ---- end-to-end through the public API (host tokens in, host tokens out) ----
+    e2e_times = []
+    for _ in range(args.e2e_steps):
+        eng.reset(args.prompt_len)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        out = eng.decode(first_pinned, N)
+        torch.cuda.synchronize()
+        e2e_times.append(time.perf_counter() - t0)
+    t_e2e = _max_over_ranks(dist, statistics.median(e2e_times))
+    e2e_value = B * N * world / t_e2e
+
+    # ---- per-kernel breakdown and roofline of the dominant kernel ----
+    eng.reset(args.prompt_len + args.decode_len // 2)
+    bd = kernel_breakdown(eng)
+    hbm, tf_burst, tf_sust, src = _peaks()
+    a = arch
+    rows = B * a.top_k
+    k_active = a.n_experts  # every expert is hit at these batch sizes
+    gu = bd.get("moe_gemm_gate_up", {"avg_ms": float("nan")})
+    dn = bd.get("moe_gemm_down", {"avg_ms": float("nan")})
+    gu_bytes = k_active * 2 * a.moe_ffn * a.hidden * 2 + rows * a.hidden * 2 + rows * a.moe_ffn * 2
+    dn_bytes = k_active * a.hidden * a.moe_ffn * 2 + rows * a.moe_ffn * 2 + rows * a.hidden * 2
+    gu_flops = 2.0 * rows * a.hidden * 2 * a.moe_ffn
+    dn_flops = 2.0 * rows * a.hidden * a.moe_ffn
+    gu_gbs = gu_bytes / (gu["avg_ms"] * 1e-3) / 1e9
+    step_ms_eager = sum(v["ms_per_step"] for v in bd.values())
+    ffn_ms = gu["avg_ms"] + dn["avg_ms"]
+    expert_tflops = (gu_flops + dn_flops) / (ffn_ms * 1e-3) / 1e12
+    roofline = {"kernel": "mgb_moe_gemm_gate_up (tcgen05 grouped GEMM + SiLU*up)", "bound": "hbm",
+                "achieved": gu_gbs, "peak": hbm, "unit": "GB/s", "frac": gu_gbs / hbm, "traffic": None,
+                "algorithmic_bytes_per_launch": gu_bytes, "avg_launch_ms": gu["avg_ms"], "peak_source": src,
+                "share_of_step": gu["ms_per_step"] / step_ms_eager}
+    launches_per_step = eng.kernel_launches_per_step * N
+    ctx_avg = args.prompt_len + args.decode_len / 2
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic (random-init counter-based weights, synthetic prefill KV)",
+        "config": {"workload": f"{arch.name} decode phase, prompt {args.prompt_len} / gen {N}, 1 B200 resident "
+                               f"(BASELINE configs[1]); step = {N} decode forwards of B={B} sequences",
+                   "batch": B, "b_a": plan.b_a, "b_e": plan.b_e, "kv_policy": "resident (paged, HBM)",
+                   "parallelism": f"replicas x{world}", "l2": "inputs larger than L2 (93 GB weights streamed/forward)"},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(first_pinned.numel() * 4),
+                "d2h_bytes_per_step": int(out.numel() * out.element_size())},
+        "roofline": roofline,
+        "expert_gemm": {"tflops": expert_tflops, "tensor_util_of_bf16_peak": expert_tflops / tf_burst,
+                        "tokens_per_expert": rows / a.n_experts, "gate_up_ms": gu["avg_ms"], "down_ms": dn["avg_ms"],
+                        "gate_up_gbs": gu_gbs, "down_gbs": dn_bytes / (dn["avg_ms"] * 1e-3) / 1e9},
+        "kernel_ms_per_forward": {k: round(v["ms_per_step"], 4) for k, v in sorted(bd.items())},
+        "forward_ms": 1e3 * t / args.steps / N, "context_avg": ctx_avg,
+        "clocks": clk.summary(), "gpu_launches": launches_per_step * args.steps,
+    }
+    if rank == 0:
+        if args.cpu_baseline:
+            v, sample = cpu_layer_sample(arch, args.cpu_batch, int(ctx_avg), 2, os.cpu_count() or 1)
+            line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                                    "sample": sample}
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="mixtral-8x7b")
+    ap.add_argument("--batch", type=int, default=None, help="sequences per GPU (default: planner's largest)")
+    ap.add_argument("--prompt-len", type=int, default=512)
+    ap.add_argument("--decode-len", type=int, default=256)
+    ap.add_argument("--reserve-gb", type=int, default=14)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--cpu-batch", type=int, default=64)
+    ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    args = ap.parse_args()
+    dist, rank, world, local = _dist()
+    if args.impl == "reference":
+        run_reference(args, dist, rank, world)
+    else:
+        run_ours(args, dist, rank, world)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

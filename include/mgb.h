@@ -1,0 +1,86 @@
+/*
+ * mgb.h — C-ABI of libmgb.so, the B200 (sm_100a) kernels behind the MoE-Gen module-based
+ * batching hot path.  Plain pointers + sizes + a cudaStream_t passed as void*; no torch types.
+ *
+ * The reference (arxiv 2503.09716, /root/reference/pkg) has no operator FFI: its engine-facing
+ * interface is the job DAG whose node kinds name the modules the engine launches
+ * (pkg/src/moe_planner/offload_dag.py:62-86) and the profiling boundary that names the kernels
+ * (pkg/src/moe_planner/hw_profile.py:52-58 ModuleKind).  Each entry point below cites the DAG
+ * node / module kind it executes.  Numerics follow HF transformers 5.5.0 (the model definition
+ * the paper's engine integrates with).
+ *
+ * Conventions
+ *  - every function returns int: 0 ok, -1 invalid argument, -2 capacity exceeded, -3 CUDA error;
+ *  - the caller owns every buffer (device memory unless stated); nothing here allocates HBM;
+ *  - all functions are asynchronous on `stream` and reentrant per stream;
+ *  - bf16 tensors are row-major, 16-byte aligned rows.
+ */
+#ifndef MGB_H_
+#define MGB_H_
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- introspection ---------------------------------------------------------------------- */
+int mgb_abi_version(void);
+int mgb_num_sms(void);
+const char* mgb_last_error(void);
+int mgb_kv_page_size(void);                /* tokens per KV page (64) */
+int mgb_router_num_blocks(int T);          /* rows of the router block_hist workspace */
+int mgb_router_tokens_per_block(void);
+
+/* ---- ROUTER (offload_dag.py:418-425, ModuleKind.ROUTER hw_profile.py:58) -----------------
+ * x[T,d] bf16, w_gate[E,d] bf16 (or logits_in[T,E] fp32 to route given logits).
+ * mode 0 Mixtral softmax->topk->renorm; 1 DeepSeek greedy (x scaling); 2 group-limited greedy.
+ * Outputs topk_idx[T,k] int32, topk_w[T,k] fp32, counts[E], offsets[E+1]; workspace
+ * local_rank[T*k], block_hist[router_num_blocks(T)*E], ticket[1] (zeroed once, self-resetting). */
+int mgb_router_topk(const void* x, const void* w_gate, const float* logits_in, int T, int d, int E, int k,
+                    int mode, float scaling, int n_group, int topk_group, float* logits_out, int* topk_idx,
+                    float* topk_w, int* local_rank, int* block_hist, int* counts, int* offsets, int* ticket,
+                    void* stream);
+
+/* ---- token grouping in front of EXPERT_COMPUTE (offload_dag.py:427-463) ------------------
+ * Stable expert-major permutation; x_perm[rows_cap,d], src_token[rows_cap], dst_pos[T*k]. */
+int mgb_permute(const void* x, const int* topk_idx, const int* local_rank, const int* block_base,
+                const int* offsets, int T, int d, int k, int E, void* x_perm, int* src_token, int* dst_pos,
+                void* stream);
+
+/* ---- EXPERT_COMPUTE (offload_dag.py:449-463, ModuleKind.EXPERT hw_profile.py:57) ---------
+ * tcgen05/TMEM/TMA grouped GEMMs over the expert-major rows; w_gate_up[E,2f,d], w_down[E,d,f]. */
+int mgb_moe_gemm_gate_up(const void* w_gate_up, const void* x_perm, const int* offsets, int E, int d, int f,
+                         int rows_cap, void* h_out, void* stream);
+int mgb_moe_gemm_down(const void* w_down, const void* h, const int* offsets, int E, int d, int f, int rows_cap,
+                      void* y_out, void* stream);
+int mgb_grouped_ffn(const void* w_gate_up, const void* w_down, const void* x_perm, const int* offsets, int E, int d,
+                    int f, int rows_cap, void* h_scratch, void* y_out, void* stream);
+
+/* ---- combine back to token order (end of the MoE layer, offload_dag.py:465-472) ---------- */
+int mgb_unpermute_combine(const void* y_perm, const int* dst_pos, const float* topk_w, const void* shared_out,
+                          const void* residual, int T, int d, int k, void* out, void* stream);
+
+/* ---- ATTN_MECH_GPU (offload_dag.py:393-402, ModuleKind.ATTN_MECH_GPU hw_profile.py:54) ---
+ * Paged GQA decode attention; K pages chunk-major, V pages row-major (see attn_gqa.cu). */
+int mgb_decode_attn_gqa(const void* q, const void* k_cache, const void* v_cache, const int* block_table,
+                        int max_pages, const int* seq_lens, int B, int Hq, int Hkv, int head_dim, float scale,
+                        void* out, void* stream);
+
+/* ---- PRE_ATTENTION / POST_ATTENTION helpers (offload_dag.py:359-416) --------------------- */
+int mgb_add_rmsnorm(const void* x, const void* delta, const void* weight, float eps, int T, int d, void* x_out,
+                    void* y, void* stream);
+int mgb_rope_append_gqa(const void* qkv, int T, int seq0, const int* positions, const float* cos_t,
+                        const float* sin_t, int Hq, int Hkv, int head_dim, const int* block_table, int max_pages,
+                        void* k_cache, void* v_cache, void* q_out, int* seq_lens, void* stream);
+int mgb_embed(const int* ids, const void* table, int T, int d, void* out, void* stream);
+int mgb_argmax(const void* logits, int T, int V, int* out, void* stream);
+int mgb_decode_advance(const int* next, int B, long long* out_tokens, int ld, int* step, int* positions,
+                       void* stream);
+
+/* ---- synthetic random-init weights (counter-based, mirrored by oracle/rng.py) ------------ */
+int mgb_fill_uniform_bf16(void* out, long long n, unsigned long long seed, unsigned long long tensor_id, float std,
+                          float constant, int mode, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MGB_H_ */

@@ -1,0 +1,108 @@
+"""ctypes binding of libmgb.so — the C-ABI declared in include/mgb.h.
+
+This is the only bridge between Python and the sm_100a kernels.  There is deliberately no CPU
+or PyTorch fallback: if the library is missing or a call fails, we raise.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+from . import build as _build
+
+P = ctypes.c_void_p
+I = ctypes.c_int
+F = ctypes.c_float
+L = ctypes.c_int64
+
+# name -> argument types (every entry point returns int status, 0 = ok)
+SIGNATURES: dict[str, list] = {
+    # introspection
+    "mgb_abi_version": [],
+    "mgb_num_sms": [],
+    "mgb_kv_page_size": [],
+    "mgb_router_num_blocks": [I],
+    "mgb_router_tokens_per_block": [],
+    # router / permutation / combine (routing.cu)
+    "mgb_router_topk": [P, P, P, I, I, I, I, I, F, I, I, P, P, P, P, P, P, P, P, P],
+    "mgb_permute": [P, P, P, P, P, I, I, I, I, P, P, P, P],
+    "mgb_unpermute_combine": [P, P, P, P, P, I, I, I, P, P],
+    # grouped expert FFN (moe_gemm.cu)
+    "mgb_moe_gemm_gate_up": [P, P, P, I, I, I, I, P, P],
+    "mgb_moe_gemm_down": [P, P, P, I, I, I, I, P, P],
+    "mgb_grouped_ffn": [P, P, P, P, I, I, I, I, P, P, P],
+    # attention (attn_gqa.cu)
+    "mgb_decode_attn_gqa": [P, P, P, P, I, P, I, I, I, I, F, P, P],
+    # elementwise.cu
+    "mgb_add_rmsnorm": [P, P, P, F, I, I, P, P, P],
+    "mgb_rope_append_gqa": [P, I, I, P, P, P, I, I, I, P, I, P, P, P, P, P],
+    "mgb_embed": [P, P, I, I, P, P],
+    "mgb_argmax": [P, I, I, P, P],
+    "mgb_decode_advance": [P, I, P, I, P, P, P],
+    "mgb_fill_uniform_bf16": [P, L, ctypes.c_uint64, ctypes.c_uint64, F, F, I, P],
+}
+
+# entry points that return a value rather than a status
+VALUE_FNS = {"mgb_abi_version", "mgb_num_sms", "mgb_kv_page_size", "mgb_router_num_blocks",
+             "mgb_router_tokens_per_block"}
+
+STATUS = {0: "ok", -1: "invalid argument", -2: "capacity exceeded", -3: "CUDA error"}
+
+
+class NativeError(RuntimeError):
+    pass
+
+
+class _Lib:
+    def __init__(self) -> None:
+        self._lib = None
+
+    def load(self) -> ctypes.CDLL:
+        if self._lib is not None:
+            return self._lib
+        path = Path(os.environ.get("MGB_LIB", str(_build.LIB_PATH)))
+        if not path.exists():
+            if os.environ.get("MGB_NO_BUILD"):
+                raise NativeError(f"libmgb.so not found at {path}; run __graft_entry__.build()")
+            _build.build(verbose=False)
+        lib = ctypes.CDLL(str(path), mode=ctypes.RTLD_GLOBAL)
+        for name, args in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = ctypes.c_int
+        lib.mgb_last_error.restype = ctypes.c_char_p
+        lib.mgb_last_error.argtypes = []
+        self._lib = lib
+        return lib
+
+    def value(self, name: str, *args) -> int:
+        assert name in VALUE_FNS
+        return int(getattr(self.load(), name)(*args))
+
+    def call(self, name: str, *args) -> None:
+        lib = self.load()
+        rc = getattr(lib, name)(*args)
+        if rc != 0:
+            err = lib.mgb_last_error().decode()
+            raise NativeError(f"{name} failed: {STATUS.get(rc, rc)} (cuda: {err})")
+
+    @property
+    def path(self) -> str:
+        return str(_build.LIB_PATH)
+
+
+LIB = _Lib()
+
+
+def call(name: str, *args) -> None:
+    LIB.call(name, *args)
+
+
+def value(name: str, *args) -> int:
+    return LIB.value(name, *args)
+
+
+def exported_symbols() -> list[str]:
+    return list(SIGNATURES) + ["mgb_last_error"]

@@ -1,0 +1,255 @@
+// Small HBM-bound kernels around the hot path: fused residual-add + RMSNorm, RoPE + paged KV
+// append, embedding gather, greedy argmax + decode-step bookkeeping, and the counter-based weight
+// generator.  Numerics follow HF transformers 5.5.0 (MixtralRMSNorm, apply_rotary_pos_emb),
+// including every intermediate bf16 rounding, so these match the CPU oracle bit-exactly except
+// for the RMS reduction order.
+#include "common.cuh"
+
+namespace mgb {
+
+constexpr int kPageTok = 64;  // must equal attn_gqa.cu kPage
+
+MGB_DEVINL float block_sum(float v, float* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float t = 0.f;
+  const int nw = blockDim.x >> 5;
+  for (int i = 0; i < nw; ++i) t += red[i];
+  __syncthreads();
+  return t;
+}
+
+// x' = delta ? bf16(x + delta) : x; x_out = x'; y = bf16(w * bf16(x' * rsqrt(mean(x'^2) + eps)))
+__global__ void add_rmsnorm_kernel(const __nv_bfloat16* x, const __nv_bfloat16* __restrict__ delta,
+                                   const __nv_bfloat16* __restrict__ w, float eps, int d,
+                                   __nv_bfloat16* x_out, __nv_bfloat16* __restrict__ y) {
+  __shared__ float red[32];
+  const size_t row = blockIdx.x;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + row * d);
+  const uint4* dr = delta ? reinterpret_cast<const uint4*>(delta + row * d) : nullptr;
+  float ss = 0.f;
+  for (int c = threadIdx.x; c < d / 8; c += blockDim.x) {
+    uint4 v = xr[c];
+    if (dr) {
+      const uint4 dv = dr[c];
+      v.x = pack_bf16x2(bf16lo(v.x) + bf16lo(dv.x), bf16hi(v.x) + bf16hi(dv.x));
+      v.y = pack_bf16x2(bf16lo(v.y) + bf16lo(dv.y), bf16hi(v.y) + bf16hi(dv.y));
+      v.z = pack_bf16x2(bf16lo(v.z) + bf16lo(dv.z), bf16hi(v.z) + bf16hi(dv.z));
+      v.w = pack_bf16x2(bf16lo(v.w) + bf16lo(dv.w), bf16hi(v.w) + bf16hi(dv.w));
+    }
+    if (x_out) reinterpret_cast<uint4*>(x_out + row * d)[c] = v;
+    const float f[8] = {bf16lo(v.x), bf16hi(v.x), bf16lo(v.y), bf16hi(v.y),
+                        bf16lo(v.z), bf16hi(v.z), bf16lo(v.w), bf16hi(v.w)};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ss = fmaf(f[i], f[i], ss);
+  }
+  const float inv = 1.0f / sqrtf(block_sum(ss, red) / (float)d + eps);
+  const uint4* wr = reinterpret_cast<const uint4*>(w);
+  for (int c = threadIdx.x; c < d / 8; c += blockDim.x) {
+    uint4 v;
+    if (x_out) {
+      v = reinterpret_cast<const uint4*>(x_out + row * d)[c];  // x' written by this thread above
+    } else {
+      v = xr[c];
+      if (dr) {  // recompute x' (same rounding as above)
+        const uint4 dv = dr[c];
+        v.x = pack_bf16x2(bf16lo(v.x) + bf16lo(dv.x), bf16hi(v.x) + bf16hi(dv.x));
+        v.y = pack_bf16x2(bf16lo(v.y) + bf16lo(dv.y), bf16hi(v.y) + bf16hi(dv.y));
+        v.z = pack_bf16x2(bf16lo(v.z) + bf16lo(dv.z), bf16hi(v.z) + bf16hi(dv.z));
+        v.w = pack_bf16x2(bf16lo(v.w) + bf16lo(dv.w), bf16hi(v.w) + bf16hi(dv.w));
+      }
+    }
+    const uint4 wv = wr[c];
+    uint4 o;
+    o.x = pack_bf16x2(bf16lo(wv.x) * bf16_round(bf16lo(v.x) * inv), bf16hi(wv.x) * bf16_round(bf16hi(v.x) * inv));
+    o.y = pack_bf16x2(bf16lo(wv.y) * bf16_round(bf16lo(v.y) * inv), bf16hi(wv.y) * bf16_round(bf16hi(v.y) * inv));
+    o.z = pack_bf16x2(bf16lo(wv.z) * bf16_round(bf16lo(v.z) * inv), bf16hi(wv.z) * bf16_round(bf16hi(v.z) * inv));
+    o.w = pack_bf16x2(bf16lo(wv.w) * bf16_round(bf16lo(v.w) * inv), bf16hi(wv.w) * bf16_round(bf16hi(v.w) * inv));
+    reinterpret_cast<uint4*>(y + row * d)[c] = o;
+  }
+}
+
+// One warp per (token, head) of the fused qkv row [Hq | Hkv | Hkv] x hd.  q heads are rotated
+// into q_out; k heads rotated and written into the chunk-major K page; v heads copied into the
+// row-major V page.  Rotation = HF rotate_half with bf16 products and sum.
+__global__ void rope_append_gqa_kernel(const __nv_bfloat16* __restrict__ qkv, int T, int seq0,
+                                       const int* __restrict__ positions, const float* __restrict__ cos_t,
+                                       const float* __restrict__ sin_t, int Hq, int Hkv, int hd,
+                                       const int* __restrict__ block_table, int max_pages,
+                                       __nv_bfloat16* __restrict__ k_cache, __nv_bfloat16* __restrict__ v_cache,
+                                       __nv_bfloat16* __restrict__ q_out, int* __restrict__ seq_lens) {
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int H = Hq + 2 * Hkv;
+  if (gw >= T * H) return;
+  const int t = gw / H, hh = gw - t * H;
+  const int seq = seq0 + t;
+  const int pos = positions[seq];
+  const __nv_bfloat16* src = qkv + ((size_t)t * H + hh) * hd;
+  const int half = hd / 2;
+  const int page = block_table[(size_t)seq * max_pages + pos / kPageTok];
+  const int slot = pos % kPageTok;
+  if (seq_lens && hh == 0 && lane == 0) seq_lens[seq] = pos + 1;  // cache length after the append
+  for (int i = lane; i < hd; i += 32) {
+    float v = __bfloat162float(src[i]);
+    if (hh < Hq + Hkv) {
+      const int fi = i < half ? i : i - half;
+      const float c = cos_t[(size_t)pos * half + fi], s = sin_t[(size_t)pos * half + fi];
+      const float rh = i < half ? -__bfloat162float(src[i + half]) : __bfloat162float(src[i - half]);
+      v = bf16_round(v * c) + bf16_round(rh * s);
+    }
+    const __nv_bfloat16 bv = __float2bfloat16_rn(v);
+    if (hh < Hq) {
+      q_out[((size_t)t * Hq + hh) * hd + i] = bv;
+    } else if (hh < Hq + Hkv) {
+      const int kh = hh - Hq;
+      const size_t blk = ((size_t)page * Hkv + kh) * hd * kPageTok;
+      k_cache[blk + ((size_t)(i / 8) * kPageTok + slot) * 8 + (i % 8)] = bv;
+    } else {
+      const int vh = hh - Hq - Hkv;
+      const size_t blk = ((size_t)page * Hkv + vh) * hd * kPageTok;
+      v_cache[blk + (size_t)slot * hd + i] = bv;
+    }
+  }
+}
+
+__global__ void embed_kernel(const int* __restrict__ ids, const __nv_bfloat16* __restrict__ table, int d,
+                             __nv_bfloat16* __restrict__ out) {
+  const size_t t = blockIdx.x;
+  const uint4* src = reinterpret_cast<const uint4*>(table + (size_t)ids[t] * d);
+  uint4* dst = reinterpret_cast<uint4*>(out + t * d);
+  for (int c = threadIdx.x; c < d / 8; c += blockDim.x) dst[c] = src[c];
+}
+
+// Greedy argmax over a bf16 logits row (first maximal index wins, like torch.argmax).
+__global__ void argmax_kernel(const __nv_bfloat16* __restrict__ logits, int V, int* __restrict__ out) {
+  const size_t row = blockIdx.x;
+  const __nv_bfloat16* lr = logits + row * V;
+  float bv = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int i = threadIdx.x; i < V; i += blockDim.x) {
+    const float v = __bfloat162float(lr[i]);
+    if (v > bv || (v == bv && i < bi)) { bv = v; bi = i; }
+  }
+  __shared__ float sv[32];
+  __shared__ int si[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) { sv[w] = bv; si[w] = bi; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < (int)(blockDim.x >> 5); ++i)
+      if (sv[i] > bv || (sv[i] == bv && si[i] < bi)) { bv = sv[i]; bi = si[i]; }
+    out[row] = bi;
+  }
+}
+
+// out_tokens[b * ld + *step] = next[b]; positions[b] += 1; then ++*step.
+__global__ void decode_advance_kernel(const int* __restrict__ next, int B, long long* __restrict__ out_tokens,
+                                      int ld, int* __restrict__ step, int* __restrict__ positions) {
+  const int s = *step;
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    if (out_tokens && s < ld) out_tokens[(size_t)b * ld + s] = next[b];
+    positions[b] += 1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *step = s + 1;
+}
+
+// Counter-based weight generator (mirrored bit-exactly by oracle/rng.py):
+//   x = (seed * K1 + tensor_id) * K2 + i;  z = splitmix64_mix(x);
+//   u = int(z >> 40) - 2^23  (uniform over [-2^23, 2^23));  value = bf16(float(u) * scale)
+// with scale = fp32(std * sqrt(3) / 2^23): a uniform distribution with standard deviation `std`.
+MGB_DEVINL uint64_t splitmix64_mix(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__global__ void fill_uniform_kernel(__nv_bfloat16* __restrict__ out, size_t n, uint64_t seed, uint64_t tensor_id,
+                                    float scale, float constant, int mode) {
+  const uint64_t base = (seed * 0x9E3779B97F4A7C15ull + tensor_id) * 0xD1B54A32D192ED03ull;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    if (mode == 1) {
+      out[i] = __float2bfloat16_rn(constant);
+    } else {
+      const uint64_t z = splitmix64_mix(base + i);
+      const int u = (int)(z >> 40) - (1 << 23);
+      out[i] = __float2bfloat16_rn(__fmul_rn((float)u, scale));
+    }
+  }
+}
+
+}  // namespace mgb
+
+extern "C" {
+
+int mgb_add_rmsnorm(const void* x, const void* delta, const void* weight, float eps, int T, int d, void* x_out,
+                    void* y, void* stream) {
+  if (T < 1 || d % 8) return MGB_EINVAL;
+  const int threads = d / 8 >= 256 ? 256 : ((d / 8 + 31) / 32) * 32;
+  mgb::add_rmsnorm_kernel<<<T, threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const __nv_bfloat16*>(x), reinterpret_cast<const __nv_bfloat16*>(delta),
+      reinterpret_cast<const __nv_bfloat16*>(weight), eps, d, reinterpret_cast<__nv_bfloat16*>(x_out),
+      reinterpret_cast<__nv_bfloat16*>(y));
+  return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
+}
+
+int mgb_rope_append_gqa(const void* qkv, int T, int seq0, const int* positions, const float* cos_t,
+                        const float* sin_t, int Hq, int Hkv, int head_dim, const int* block_table, int max_pages,
+                        void* k_cache, void* v_cache, void* q_out, int* seq_lens, void* stream) {
+  if (T < 1 || head_dim % 8 || Hq % Hkv) return MGB_EINVAL;
+  const int warps = T * (Hq + 2 * Hkv);
+  const int threads = 256;
+  mgb::rope_append_gqa_kernel<<<(warps * 32 + threads - 1) / threads, threads, 0,
+                                reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const __nv_bfloat16*>(qkv), T, seq0, positions, cos_t, sin_t, Hq, Hkv, head_dim, block_table,
+      max_pages, reinterpret_cast<__nv_bfloat16*>(k_cache), reinterpret_cast<__nv_bfloat16*>(v_cache),
+      reinterpret_cast<__nv_bfloat16*>(q_out), seq_lens);
+  return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
+}
+
+int mgb_embed(const int* ids, const void* table, int T, int d, void* out, void* stream) {
+  if (T < 1 || d % 8) return MGB_EINVAL;
+  mgb::embed_kernel<<<T, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      ids, reinterpret_cast<const __nv_bfloat16*>(table), d, reinterpret_cast<__nv_bfloat16*>(out));
+  return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
+}
+
+int mgb_argmax(const void* logits, int T, int V, int* out, void* stream) {
+  if (T < 1 || V < 1) return MGB_EINVAL;
+  mgb::argmax_kernel<<<T, 512, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const __nv_bfloat16*>(logits), V, out);
+  return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
+}
+
+int mgb_decode_advance(const int* next, int B, long long* out_tokens, int ld, int* step, int* positions,
+                       void* stream) {
+  if (B < 1) return MGB_EINVAL;
+  mgb::decode_advance_kernel<<<1, 1024, 0, reinterpret_cast<cudaStream_t>(stream)>>>(next, B, out_tokens, ld, step,
+                                                                                     positions);
+  return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
+}
+
+// mode 0: counter-based uniform with standard deviation `std`; mode 1: constant fill.
+int mgb_fill_uniform_bf16(void* out, long long n, unsigned long long seed, unsigned long long tensor_id, float std,
+                          float constant, int mode, void* stream) {
+  if (n < 0) return MGB_EINVAL;
+  if (n == 0) return MGB_OK;
+  const float scale = (float)((double)std * 1.7320508075688772 / 8388608.0);
+  const int threads = 256;
+  long long blocks = (n + threads - 1) / threads;
+  if (blocks > 148 * 64) blocks = 148 * 64;
+  mgb::fill_uniform_kernel<<<(int)blocks, threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<__nv_bfloat16*>(out), (size_t)n, seed, tensor_id, scale, constant, mode);
+  return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
+}
+
+}  // extern "C"

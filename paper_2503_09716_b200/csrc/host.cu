@@ -1,0 +1,58 @@
+// Host-side utilities shared by every launcher in libmgb: tensor-map encoding (through the
+// runtime's driver entry point, so the library does not link libcuda directly), SM count, and the
+// C-ABI introspection entry points.
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "common.cuh"
+
+namespace mgb_host {
+
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+static std::once_flag g_encode_once;
+
+CUresult encode_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                             uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer) {
+  std::call_once(g_encode_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  if (!g_encode) return CUDA_ERROR_NOT_FOUND;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_stride_bytes};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  return g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+}
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = mgb::kNumSMsB200;
+  }
+  return n;
+}
+
+}  // namespace mgb_host
+
+extern "C" {
+
+// ABI version of include/mgb.h; bumped whenever a signature changes.
+int mgb_abi_version(void) { return 1; }
+
+// Name of the last CUDA error seen by the runtime in this library (for loud failures).
+const char* mgb_last_error(void) { return cudaGetErrorString(cudaPeekAtLastError()); }
+
+// Number of SMs of the current device (148 on B200).
+int mgb_num_sms(void) { return mgb_host::num_sms(); }
+
+}  // extern "C"

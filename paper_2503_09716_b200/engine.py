@@ -1,0 +1,302 @@
+"""MoE-Gen engine on one B200: executes the module-based batching job list with the sm_100a
+kernels of libmgb.so.
+
+The scheduler side follows the reference: the engine takes the planner's decision vector
+(`plan.json` / BatchingPlan, reference memory_model.py:66-89, cli.py:74-109), sizes its HBM
+buffers from it, builds the per-layer job list with `schedule.build_schedule` (the reference's
+`_build_graph`, offload_dag.py:240-492) and issues those jobs in submission order on CUDA
+streams.  Per layer (decode):
+    pre_attention(mb)  : RMSNorm -> fused QKV GEMM (cuBLAS) -> RoPE + paged-KV append   [b_a seqs]
+    attn_mech_gpu(mb)  : paged GQA decode attention (mgb_decode_attn_gqa)               [b_a seqs]
+    post_attention     : O GEMM (cuBLAS) -> residual add + RMSNorm                      [B seqs]
+    router             : fused gate GEMV + softmax + top-k + counts (mgb_router_topk) + stable permute
+    expert_compute     : tcgen05 grouped GEMM gate/up+SiLU, down (all experts' chunks in one
+                         persistent launch each) -> weighted combine + residual add
+The whole decode step (all layers + LM head + greedy argmax + bookkeeping) is captured once as a
+CUDA graph and replayed per generated token, so the host issues one launch per token.
+"""
+
+from __future__ import annotations
+
+import json
+import math
+import time
+from dataclasses import dataclass
+
+import torch
+
+from . import ops
+from .configs import ModelArch, get_arch
+from .planner import BatchingPlan, Hardware, ModelSpec, WorkloadSpec, largest_batch, load_plan
+from .schedule import Schedule, build_schedule
+from .weights import MixtralDeviceWeights
+
+BF16 = torch.bfloat16
+
+
+def b200_hardware(host_bytes: int = 2_000_000_000_000, hbm_bytes: int | None = None) -> Hardware:
+    """B200 machine description for the planner (capacities; rates only seed the estimate)."""
+    if hbm_bytes is None:
+        hbm_bytes = torch.cuda.get_device_properties(0).total_memory if torch.cuda.is_available() else 183_359 << 20
+    return Hardware(m_g=int(hbm_bytes), m_c=int(host_bytes), bw_htod=55e9, bw_dtoh=55e9, gpu_peak_flops=1.63e15,
+                    gpu_mem_bw=6.54e12, gpu_launch_overhead=5e-6, cpu_attn_flops=0.0)
+
+
+def _unit_latency(kind: str, tokens: int, ctx: int) -> float:
+    return 1e-6 * tokens
+
+
+def resident_plan(arch: ModelArch, prompt_len: int, decode_len: int, B: int | None = None,
+                  b_a: int | None = None, b_e: int = 4096, reserve_bytes: int = 12 << 30,
+                  hbm_bytes: int | None = None) -> BatchingPlan:
+    """Plan for an HBM-resident model (s_params = whole model, no expert slots): B is the largest
+    batch whose paged KV fits next to the weights (reference max_feasible_B with the resident KV
+    policy), capped by `B` if given."""
+    spec = ModelSpec.from_document(arch.model_spec_document())
+    hw = b200_hardware(hbm_bytes=hbm_bytes)
+    hw = Hardware(**{**hw.__dict__, "m_g": hw.m_g - reserve_bytes})
+    wl = WorkloadSpec(prompt_len, decode_len, 1, "decode")
+    tmpl = BatchingPlan(1, 1, b_e, 0.0, 0, spec.model_bytes)
+    bmax = largest_batch(spec, hw, wl, tmpl, kv_policy="resident")
+    B = bmax if B is None else min(B, bmax)
+    return BatchingPlan(B, B if b_a is None else min(b_a, B), b_e, 0.0, 0, spec.model_bytes)
+
+
+@dataclass
+class StepBuffers:
+    x: torch.Tensor
+    h: torch.Tensor
+    qkv: torch.Tensor
+    q: torch.Tensor
+    attn: torch.Tensor
+    o: torch.Tensor
+    x_perm: torch.Tensor
+    h_ffn: torch.Tensor
+    y_perm: torch.Tensor
+    logits: torch.Tensor
+    next_ids: torch.Tensor
+    positions: torch.Tensor
+    seq_lens: torch.Tensor
+    step: torch.Tensor
+
+
+class Engine:
+    """Greedy MoE decoding engine (Mixtral family, HBM-resident weights + paged KV)."""
+
+    def __init__(self, arch: ModelArch | str, plan=None, *, prompt_len: int, decode_len: int, seed: int = 0,
+                 kv_policy: str = "resident", use_graph: bool = True, device: str = "cuda"):
+        if not torch.cuda.is_available():
+            raise RuntimeError("the B200 engine needs a CUDA device (there is no CPU fallback)")
+        self.arch = get_arch(arch) if isinstance(arch, str) else arch
+        if self.arch.family != "mixtral":
+            raise NotImplementedError("this engine build runs the Mixtral family (GQA)")
+        if kv_policy != "resident":
+            raise NotImplementedError("kv_policy='offload' is planned; this build keeps KV in HBM")
+        a = self.arch
+        self.kv_policy = kv_policy
+        self.prompt_len, self.decode_len = prompt_len, decode_len
+        self.max_ctx = prompt_len + decode_len
+        self.plan = load_plan(plan) if plan is not None else resident_plan(a, prompt_len, decode_len)
+        self.spec = ModelSpec.from_document(a.model_spec_document())
+        self.workload = WorkloadSpec(prompt_len, decode_len, self.plan.B, "decode")
+        self.B = B = self.plan.B
+        self.device = device
+        self.use_graph = use_graph
+        # ---- job list (structure only; durations are measured, not modelled) ----
+        self.schedule: Schedule = build_schedule(self.spec, b200_hardware(), _unit_latency, self.workload, self.plan,
+                                                 kv_policy=kv_policy)
+        self.layer_jobs = [[] for _ in range(a.layers)]
+        for j in self.schedule.jobs:
+            if j.resource is not None and j.layer >= 0:
+                self.layer_jobs[j.layer].append(j)
+        # ---- weights ----
+        self.w = MixtralDeviceWeights(a, seed=seed, device=device)
+        # ---- paged KV cache (identity block table: sequence b owns pages [b*pps, (b+1)*pps)) ----
+        self.page = ops.kv_page_size()
+        self.pps = math.ceil(self.max_ctx / self.page)
+        n_pages = B * self.pps
+        blk = a.n_kv_heads * a.head_dim * self.page
+        self.k_cache = [torch.empty(n_pages * blk, dtype=BF16, device=device) for _ in range(a.layers)]
+        self.v_cache = [torch.empty(n_pages * blk, dtype=BF16, device=device) for _ in range(a.layers)]
+        self.block_table = torch.arange(n_pages, dtype=torch.int32, device=device).view(B, self.pps)
+        # ---- RoPE tables (HF MixtralRotaryEmbedding, bf16-rounded, modeling_mixtral.py:210-220) ----
+        hd = a.head_dim
+        inv_freq = 1.0 / (a.rope_theta ** (torch.arange(0, hd, 2, dtype=torch.int64).float() / hd))
+        freqs = torch.arange(self.max_ctx).float()[:, None] * inv_freq[None, :]
+        self.cos_t = freqs.cos().to(BF16).float().contiguous().to(device)
+        self.sin_t = freqs.sin().to(BF16).float().contiguous().to(device)
+        # ---- step buffers ----
+        d, k, f = a.hidden, a.top_k, a.moe_ffn
+        qd, kvd = a.n_heads * hd, a.n_kv_heads * hd
+        rows = B * k
+        bf = dict(dtype=BF16, device=device)
+        i32 = dict(dtype=torch.int32, device=device)
+        self.buf = StepBuffers(
+            x=torch.zeros(B, d, **bf), h=torch.zeros(B, d, **bf), qkv=torch.zeros(B, qd + 2 * kvd, **bf),
+            q=torch.zeros(B, qd, **bf), attn=torch.zeros(B, qd, **bf), o=torch.zeros(B, d, **bf),
+            x_perm=torch.zeros(rows, d, **bf), h_ffn=torch.zeros(rows, f, **bf), y_perm=torch.zeros(rows, d, **bf),
+            logits=torch.zeros(B, a.vocab, **bf), next_ids=torch.zeros(B, **i32), positions=torch.zeros(B, **i32),
+            seq_lens=torch.zeros(B, **i32), step=torch.zeros(1, **i32))
+        self.rws = ops.RouterWorkspace(B, a.n_experts, k, device=device)
+        self.out_tokens = torch.zeros(B, max(1, self.max_ctx), dtype=torch.int64, device=device)
+        self.graph: torch.cuda.CUDAGraph | None = None
+        self.stream = torch.cuda.Stream(device=device)
+        self.kernel_launches_per_step = self._count_launches()
+
+    # ------------------------------------------------------------------------------------
+    # job issue
+    # ------------------------------------------------------------------------------------
+    def _issue_layer(self, l: int) -> None:
+        a, b, W = self.arch, self.buf, self.w.layers[l]
+        hd, Hq, Hkv = a.head_dim, a.n_heads, a.n_kv_heads
+        experts_done = False
+        for j in self.layer_jobs[l]:
+            if j.kind == "pre_attention":
+                s0, s1 = self._mb_range(j)
+                ops.add_rmsnorm(b.x[s0:s1], W["ln1"], a.rms_eps, b.h[s0:s1])
+                torch.mm(b.h[s0:s1], W["wqkv"].t(), out=b.qkv[s0:s1])
+                ops.rope_append_gqa(b.qkv[s0:s1], s0, b.positions, self.cos_t, self.sin_t, Hq, Hkv, hd,
+                                    self.block_table, self.k_cache[l], self.v_cache[l], b.q[s0:s1], b.seq_lens)
+            elif j.kind == "attn_mech_gpu":
+                s0, s1 = self._mb_range(j)
+                ops.decode_attn_gqa(b.q[s0:s1], self.k_cache[l], self.v_cache[l], self.block_table[s0:s1],
+                                    b.seq_lens[s0:s1], Hq, Hkv, hd, b.attn[s0:s1])
+            elif j.kind == "post_attention":
+                torch.mm(b.attn, W["wo"].t(), out=b.o)
+                ops.add_rmsnorm(b.x, W["ln2"], a.rms_eps, b.h, delta=b.o, x_out=b.x)
+            elif j.kind == "router":
+                ops.router_topk(b.h, W["router"], self.rws, a.top_k, a.router_mode, a.routed_scaling, a.n_group,
+                                a.topk_group)
+                ops.permute(b.h, self.rws, b.x_perm)
+            elif j.kind == "expert_compute":
+                # all experts' b_e chunks of this layer execute inside one persistent grouped
+                # launch per GEMM (the kernel's token tiles are the chunks)
+                if not experts_done:
+                    ops.moe_gemm_gate_up(W["w_gate_up"], b.x_perm, self.rws.offsets, b.h_ffn)
+                    ops.moe_gemm_down(W["w_down"], b.h_ffn, self.rws.offsets, b.y_perm)
+                    ops.unpermute_combine(b.y_perm, self.rws, b.x, self.B, residual=b.x)
+                    experts_done = True
+            else:
+                raise RuntimeError(f"job kind {j.kind!r} is not executable under kv_policy={self.kv_policy!r}")
+
+    def _mb_range(self, j) -> tuple[int, int]:
+        mb = int(j.label.rsplit("mb", 1)[1])
+        s0 = mb * self.plan.b_a
+        return s0, s0 + j.seqs
+
+    def _count_launches(self) -> int:
+        n = 2  # embed, and final norm
+        for l in range(self.arch.layers):
+            for j in self.layer_jobs[l]:
+                n += {"pre_attention": 2, "attn_mech_gpu": 1, "post_attention": 1, "router": 2}.get(j.kind, 0)
+            n += 3  # gate_up, down, combine
+        return n + 2  # argmax, advance  (cuBLAS GEMMs are library launches, not counted)
+
+    def _step(self, record: bool = True) -> None:
+        """One decode forward of all B sequences (one token each)."""
+        a, b = self.arch, self.buf
+        ops.embed(b.next_ids, self.w.embed, b.x)
+        for l in range(a.layers):
+            self._issue_layer(l)
+        ops.add_rmsnorm(b.x, self.w.final_norm, a.rms_eps, b.h)
+        torch.mm(b.h, self.w.lm_head.t(), out=b.logits)
+        ops.argmax(b.logits, b.next_ids)
+        ops.decode_advance(b.next_ids, self.out_tokens if record else None, b.step, b.positions)
+
+    # ------------------------------------------------------------------------------------
+    # graph capture / replay
+    # ------------------------------------------------------------------------------------
+    def capture(self) -> None:
+        if self.graph is not None or not self.use_graph:
+            return
+        # snapshot mutable state: the eager warm-up step must not advance it
+        snap = [t.clone() for t in (self.buf.positions, self.buf.step, self.buf.next_ids, self.buf.seq_lens)]
+        with torch.cuda.stream(self.stream):
+            self._step()
+        torch.cuda.current_stream().wait_stream(self.stream)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=self.stream):
+            self._step()
+        torch.cuda.synchronize()
+        for t, s in zip((self.buf.positions, self.buf.step, self.buf.next_ids, self.buf.seq_lens), snap):
+            t.copy_(s)
+        torch.cuda.synchronize()
+        self.graph = g
+
+    def run_step(self) -> None:
+        if self.use_graph:
+            if self.graph is None:
+                self.capture()
+            self.graph.replay()
+        else:
+            with torch.cuda.stream(self.stream):
+                self._step()
+            torch.cuda.current_stream().wait_stream(self.stream)
+
+    # ------------------------------------------------------------------------------------
+    # public API
+    # ------------------------------------------------------------------------------------
+    def reset(self, start_pos: int = 0) -> None:
+        self.buf.positions.fill_(start_pos)
+        self.buf.seq_lens.fill_(start_pos)
+        self.buf.step.zero_()
+        self.out_tokens.zero_()
+
+    def synthetic_prefill(self, seed: int = 1, std: float = 1.0) -> None:
+        """Stand-in for the prefill phase (excluded from the decode metric): fill every KV page
+        with counter-based values (std ~ real K/V scale) and position all sequences at
+        prompt_len, so decode steps attend over prompt_len..prompt_len+decode_len keys."""
+        from .weights import fill_uniform_
+        for l in range(self.arch.layers):
+            fill_uniform_(self.k_cache[l], seed, 10_000_000 + 2 * l, std)
+            fill_uniform_(self.v_cache[l], seed, 10_000_001 + 2 * l, std)
+        self.reset(self.prompt_len)
+
+    def decode(self, first_tokens: torch.Tensor, n_steps: int) -> torch.Tensor:
+        """Decode phase through the public API: host `first_tokens` [B] (pinned H2D), n_steps
+        greedy forwards from the current positions; returns host int64 [B, n_steps]."""
+        assert first_tokens.shape == (self.B,)
+        self.buf.next_ids.copy_(first_tokens.to(torch.int32), non_blocking=True)
+        self.buf.step.zero_()
+        for _ in range(n_steps):
+            self.run_step()
+        return self.out_tokens[:, :n_steps].to("cpu", non_blocking=False)
+
+    @torch.no_grad()
+    def generate(self, input_ids: torch.Tensor, max_new_tokens: int) -> torch.Tensor:
+        """Greedy generation (HF generate semantics: no EOS stop, equal-length prompts).  The
+        prompt is consumed through the same decode step, one position per step."""
+        B, P = input_ids.shape
+        assert B == self.B, f"engine was planned for B={self.B}"
+        assert P + max_new_tokens <= self.max_ctx
+        self.reset(0)
+        prompt = input_ids.to(self.device, torch.int32)
+        for p in range(P):
+            self.buf.next_ids.copy_(prompt[:, p])
+            self.run_step()
+        # step P-1 predicted the first new token; it is already in next_ids
+        for _ in range(max_new_tokens - 1):
+            self.run_step()
+        gen = self.out_tokens[:, P - 1:P - 1 + max_new_tokens].cpu()
+        return torch.cat([input_ids.cpu().to(torch.int64), gen], dim=1)
+
+    def debug_forward(self, tokens: torch.Tensor, pos: int) -> dict:
+        """One eager step at absolute position `pos` (all sequences), returning intermediate
+        tensors of layer 0 and the logits (parity tests)."""
+        self.buf.positions.fill_(pos)
+        self.buf.next_ids.copy_(tokens.to(torch.int32))
+        with torch.cuda.stream(self.stream):
+            self._step(record=False)
+        torch.cuda.current_stream().wait_stream(self.stream)
+        torch.cuda.synchronize()
+        return dict(logits=self.buf.logits.clone(), next_ids=self.buf.next_ids.clone())
+
+    def job_trace(self) -> list[dict]:
+        """The issued job list (kinds/labels/shapes), in submission order."""
+        return [dict(id=j.id, kind=j.kind, resource=j.resource, label=j.label, layer=j.layer, tokens=j.tokens,
+                     seqs=j.seqs, nbytes=j.nbytes) for j in self.schedule.jobs]
+
+    def plan_document(self) -> str:
+        return json.dumps({"plan": self.plan.to_document(), "phase": "decode", "kv_policy": self.kv_policy},
+                          sort_keys=True)

@@ -1,0 +1,122 @@
+"""Torch-tensor front end of the C-ABI (include/mgb.h).  Every op launches on the current CUDA
+stream (so it is CUDA-graph capturable), writes into caller-provided outputs where given, and
+raises if the native library is missing or returns an error.  No CPU fallback exists.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _native as nat
+
+BF16 = torch.bfloat16
+
+
+def _s() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _p(t: torch.Tensor | None) -> int | None:
+    if t is None:
+        return None
+    assert t.is_cuda, "device tensor expected"
+    return t.data_ptr()
+
+
+class RouterWorkspace:
+    """Router/permutation scratch for up to T tokens and E experts with top-k."""
+
+    def __init__(self, T: int, E: int, k: int, device="cuda"):
+        nblk = nat.value("mgb_router_num_blocks", T)
+        i32 = dict(dtype=torch.int32, device=device)
+        self.T, self.E, self.k = T, E, k
+        self.topk_idx = torch.zeros(T, k, **i32)
+        self.topk_w = torch.zeros(T, k, dtype=torch.float32, device=device)
+        self.local_rank = torch.zeros(T * k, **i32)
+        self.block_hist = torch.zeros(nblk, E, **i32)
+        self.counts = torch.zeros(E, **i32)
+        self.offsets = torch.zeros(E + 1, **i32)
+        self.ticket = torch.zeros(1, **i32)
+        self.src_token = torch.zeros(T * k, **i32)
+        self.dst_pos = torch.zeros(T * k, **i32)
+
+
+def router_topk(x: torch.Tensor | None, w_gate: torch.Tensor | None, ws: RouterWorkspace, k: int, mode: int,
+                scaling: float = 1.0, n_group: int = 1, topk_group: int = 1,
+                logits_in: torch.Tensor | None = None, logits_out: torch.Tensor | None = None,
+                T: int | None = None, E: int | None = None) -> None:
+    if logits_in is not None:
+        T, E = logits_in.shape
+        d = 0
+    else:
+        T, d = x.shape
+        E = w_gate.shape[0]
+    nat.call("mgb_router_topk", _p(x), _p(w_gate), _p(logits_in), T, d, E, k, mode, scaling, n_group, topk_group,
+             _p(logits_out), _p(ws.topk_idx), _p(ws.topk_w), _p(ws.local_rank), _p(ws.block_hist), _p(ws.counts),
+             _p(ws.offsets), _p(ws.ticket), _s())
+
+
+def permute(x: torch.Tensor, ws: RouterWorkspace, x_perm: torch.Tensor, T: int | None = None) -> None:
+    T = x.shape[0] if T is None else T
+    nat.call("mgb_permute", _p(x), _p(ws.topk_idx), _p(ws.local_rank), _p(ws.block_hist), _p(ws.offsets), T,
+             x.shape[1], ws.k, ws.E, _p(x_perm), _p(ws.src_token), _p(ws.dst_pos), _s())
+
+
+def moe_gemm_gate_up(w_gate_up: torch.Tensor, x_perm: torch.Tensor, offsets: torch.Tensor, h_out: torch.Tensor) -> None:
+    E, two_f, d = w_gate_up.shape
+    nat.call("mgb_moe_gemm_gate_up", _p(w_gate_up), _p(x_perm), _p(offsets), E, d, two_f // 2, x_perm.shape[0],
+             _p(h_out), _s())
+
+
+def moe_gemm_down(w_down: torch.Tensor, h: torch.Tensor, offsets: torch.Tensor, y_out: torch.Tensor) -> None:
+    E, d, f = w_down.shape
+    nat.call("mgb_moe_gemm_down", _p(w_down), _p(h), _p(offsets), E, d, f, h.shape[0], _p(y_out), _s())
+
+
+def unpermute_combine(y_perm: torch.Tensor, ws: RouterWorkspace, out: torch.Tensor, T: int,
+                      residual: torch.Tensor | None = None, shared_out: torch.Tensor | None = None) -> None:
+    nat.call("mgb_unpermute_combine", _p(y_perm), _p(ws.dst_pos), _p(ws.topk_w), _p(shared_out), _p(residual), T,
+             out.shape[1], ws.k, _p(out), _s())
+
+
+def add_rmsnorm(x: torch.Tensor, weight: torch.Tensor, eps: float, y: torch.Tensor,
+                delta: torch.Tensor | None = None, x_out: torch.Tensor | None = None) -> None:
+    T, d = x.shape
+    nat.call("mgb_add_rmsnorm", _p(x), _p(delta), _p(weight), eps, T, d, _p(x_out), _p(y), _s())
+
+
+def rope_append_gqa(qkv: torch.Tensor, seq0: int, positions: torch.Tensor, cos_t: torch.Tensor, sin_t: torch.Tensor,
+                    Hq: int, Hkv: int, hd: int, block_table: torch.Tensor, k_cache: torch.Tensor,
+                    v_cache: torch.Tensor, q_out: torch.Tensor, seq_lens: torch.Tensor | None = None) -> None:
+    T = qkv.shape[0]
+    nat.call("mgb_rope_append_gqa", _p(qkv), T, seq0, _p(positions), _p(cos_t), _p(sin_t), Hq, Hkv, hd,
+             _p(block_table), block_table.shape[1], _p(k_cache), _p(v_cache), _p(q_out), _p(seq_lens), _s())
+
+
+def decode_attn_gqa(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor, block_table: torch.Tensor,
+                    seq_lens: torch.Tensor, Hq: int, Hkv: int, hd: int, out: torch.Tensor,
+                    scale: float | None = None) -> None:
+    B = q.shape[0]
+    scale = hd ** -0.5 if scale is None else scale
+    nat.call("mgb_decode_attn_gqa", _p(q), _p(k_cache), _p(v_cache), _p(block_table), block_table.shape[1],
+             _p(seq_lens), B, Hq, Hkv, hd, scale, _p(out), _s())
+
+
+def embed(ids: torch.Tensor, table: torch.Tensor, out: torch.Tensor) -> None:
+    nat.call("mgb_embed", _p(ids), _p(table), ids.shape[0], table.shape[1], _p(out), _s())
+
+
+def argmax(logits: torch.Tensor, out: torch.Tensor) -> None:
+    T, V = logits.shape
+    nat.call("mgb_argmax", _p(logits), T, V, _p(out), _s())
+
+
+def decode_advance(next_ids: torch.Tensor, out_tokens: torch.Tensor | None, step: torch.Tensor,
+                   positions: torch.Tensor) -> None:
+    B = next_ids.shape[0]
+    ld = out_tokens.shape[1] if out_tokens is not None else 0
+    nat.call("mgb_decode_advance", _p(next_ids), B, _p(out_tokens), ld, _p(step), _p(positions), _s())
+
+
+def kv_page_size() -> int:
+    return nat.value("mgb_kv_page_size")

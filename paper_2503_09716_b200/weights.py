@@ -1,0 +1,75 @@
+"""Device-resident random-init weights, generated in HBM by the counter-based kernel
+(mgb_fill_uniform_bf16) so 93-471 GB models need no host files and are bit-identical to the
+CPU oracle's copy (oracle/rng.py) at small sizes.
+
+Tensor-id scheme (must match oracle/moe_ref.py): globals 1 embed, 2 final norm, 3 lm_head;
+layer l uses 1000 + 100*l + slot.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _native as nat
+from .configs import ModelArch
+
+TID_EMBED, TID_FINAL_NORM, TID_LM_HEAD = 1, 2, 3
+LAYER_BASE, LAYER_STRIDE = 1000, 100
+SLOT = dict(ln1=0, wq=1, wk=2, wv=3, wo=4, ln2=5, router=6, w_gate_up=7, w_down=8)
+
+
+def tid(layer: int, name: str) -> int:
+    return LAYER_BASE + LAYER_STRIDE * layer + SLOT[name]
+
+
+def fill_uniform_(t: torch.Tensor, seed: int, tensor_id: int, std: float) -> torch.Tensor:
+    assert t.dtype == torch.bfloat16 and t.is_cuda and t.is_contiguous()
+    nat.call("mgb_fill_uniform_bf16", t.data_ptr(), t.numel(), seed, tensor_id, std, 0.0, 0,
+             torch.cuda.current_stream().cuda_stream)
+    return t
+
+
+def fill_const_(t: torch.Tensor, value: float) -> torch.Tensor:
+    assert t.dtype == torch.bfloat16 and t.is_cuda and t.is_contiguous()
+    nat.call("mgb_fill_uniform_bf16", t.data_ptr(), t.numel(), 0, 0, 0.0, value, 1,
+             torch.cuda.current_stream().cuda_stream)
+    return t
+
+
+class MixtralDeviceWeights:
+    """Mixtral-family weights in the engine's layout.  q/k/v projections are stored fused as
+    one [Hq*hd + 2*Hkv*hd, d] matrix (rows = wq | wk | wv), each part generated with its own
+    tensor id so it equals the oracle's separate wq/wk/wv."""
+
+    def __init__(self, arch: ModelArch, seed: int = 0, device: str = "cuda"):
+        a = arch
+        d, hd = a.hidden, a.head_dim
+        qd, kvd = a.n_heads * hd, a.n_kv_heads * hd
+        std = a.init_std
+        bf = dict(dtype=torch.bfloat16, device=device)
+        self.arch = a
+        self.embed = fill_uniform_(torch.empty(a.vocab, d, **bf), seed, TID_EMBED, std)
+        self.final_norm = fill_const_(torch.empty(d, **bf), 1.0)
+        self.lm_head = fill_uniform_(torch.empty(a.vocab, d, **bf), seed, TID_LM_HEAD, std)
+        self.layers = []
+        for l in range(a.layers):
+            wqkv = torch.empty(qd + 2 * kvd, d, **bf)
+            fill_uniform_(wqkv[:qd], seed, tid(l, "wq"), std)
+            fill_uniform_(wqkv[qd:qd + kvd], seed, tid(l, "wk"), std)
+            fill_uniform_(wqkv[qd + kvd:], seed, tid(l, "wv"), std)
+            self.layers.append(dict(
+                ln1=fill_const_(torch.empty(d, **bf), 1.0),
+                wqkv=wqkv,
+                wo=fill_uniform_(torch.empty(d, qd, **bf), seed, tid(l, "wo"), std),
+                ln2=fill_const_(torch.empty(d, **bf), 1.0),
+                router=fill_uniform_(torch.empty(a.n_experts, d, **bf), seed, tid(l, "router"), std),
+                w_gate_up=fill_uniform_(torch.empty(a.n_experts, 2 * a.moe_ffn, d, **bf), seed,
+                                        tid(l, "w_gate_up"), std),
+                w_down=fill_uniform_(torch.empty(a.n_experts, d, a.moe_ffn, **bf), seed, tid(l, "w_down"), std),
+            ))
+
+    def nbytes(self) -> int:
+        n = self.embed.nbytes + self.final_norm.nbytes + self.lm_head.nbytes
+        for L in self.layers:
+            n += sum(t.nbytes for t in L.values())
+        return n
