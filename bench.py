@@ -223,7 +223,6 @@ def kernel_breakdown(eng, reps: int = 2) -> dict:
                 # park the stream so the host enqueues the whole step before the GPU starts:
                 # event gaps then measure kernels, not Python launch latency
                 torch.cuda._sleep(int(2e8))
-                pend.clear() if _ == 0 and False else None
                 eng._step(record=False)
             torch.cuda.synchronize()
         for t, s in zip((eng.buf.positions, eng.buf.step, eng.buf.next_ids, eng.buf.seq_lens), saved):

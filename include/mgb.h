@@ -55,9 +55,12 @@ int mgb_moe_gemm_down(const void* w_down, const void* h, const int* offsets, int
 int mgb_grouped_ffn(const void* w_gate_up, const void* w_down, const void* x_perm, const int* offsets, int E, int d,
                     int f, int rows_cap, void* h_scratch, void* y_out, void* stream);
 
-/* ---- combine back to token order (end of the MoE layer, offload_dag.py:465-472) ---------- */
+/* ---- combine back to token order (end of the MoE layer, offload_dag.py:465-472) ----------
+ * out = residual + bf16(sum_j w*y) (+ shared); optionally norm_out = RMSNorm(out)*norm_w, the
+ * next layer's input norm fused in (norm_w/norm_out may be NULL). */
 int mgb_unpermute_combine(const void* y_perm, const int* dst_pos, const float* topk_w, const void* shared_out,
-                          const void* residual, int T, int d, int k, void* out, void* stream);
+                          const void* residual, int T, int d, int k, void* out, const void* norm_w, float eps,
+                          void* norm_out, void* stream);
 
 /* ---- ATTN_MECH_GPU (offload_dag.py:393-402, ModuleKind.ATTN_MECH_GPU hw_profile.py:54) ---
  * Paged GQA decode attention; K pages chunk-major, V pages row-major (see attn_gqa.cu). */

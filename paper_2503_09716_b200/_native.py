@@ -28,7 +28,7 @@ SIGNATURES: dict[str, list] = {
     # router / permutation / combine (routing.cu)
     "mgb_router_topk": [P, P, P, I, I, I, I, I, F, I, I, P, P, P, P, P, P, P, P, P],
     "mgb_permute": [P, P, P, P, P, I, I, I, I, P, P, P, P],
-    "mgb_unpermute_combine": [P, P, P, P, P, I, I, I, P, P],
+    "mgb_unpermute_combine": [P, P, P, P, P, I, I, I, P, P, F, P, P],
     # grouped expert FFN (moe_gemm.cu)
     "mgb_moe_gemm_gate_up": [P, P, P, I, I, I, I, P, P],
     "mgb_moe_gemm_down": [P, P, P, I, I, I, I, P, P],

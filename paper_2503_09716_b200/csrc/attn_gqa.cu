@@ -1,211 +1,234 @@
 // Paged GQA decode attention (Mixtral) on sm_100a — the ATTN_MECH_GPU job of the module-based
 // batching schedule (reference: pkg/src/moe_planner/offload_dag.py:393-402; cost model
-// hw_profile.py:269-270,285-287).  Semantics: HF transformers 5.5.0 eager_attention_forward
-// (modeling_mixtral.py:269-291): softmax(q k^T / sqrt(hd)) v with key/value head i // G for query
-// head i; this kernel keeps scores and the softmax in fp32 (online softmax), so it matches HF's
-// bf16-rounded scores within tolerance, not bit-exactly.
+// hw_profile.py:269-270,285-287).  Semantics: softmax(q k^T / sqrt(hd)) v with key/value head
+// i // G for query head i (HF transformers 5.5.0 attention with repeat_kv,
+// modeling_mixtral.py:257-291), computed with fp32 scores / softmax / accumulation and one bf16
+// rounding of the output (HF's default sdpa path), so it matches the oracle within tolerance.
 //
 // KV layout (owned by this framework, chosen for the decode access pattern): pages of
-// kPage = 64 tokens; per (page, kv-head) one contiguous 16 KB block for K and one for V:
-//   K: [page][kvh][hd/8 chunks][64 tokens][8]  (chunk-major -> lane = token reads are coalesced)
-//   V: [page][kvh][64 tokens][hd]              (row-major   -> lane = dim-pair reads are coalesced)
-// Each CTA owns one (sequence, kv-head) and streams its pages through shared memory with
-// double-buffered cp.async.bulk copies (TMA bulk engine), so the kernel is HBM-bound.
+// kPage = 64 tokens; per (page, kv-head) one contiguous block for K and one for V, both
+// "chunk-major": [hd/8 chunks][64 tokens][8 dims].  Eight consecutive tokens of one 8-dim chunk
+// are 128 contiguous bytes, so every ldmatrix (K) / ldmatrix.trans (V) is bank-conflict free.
+//
+// Persistent kernel, 2 CTAs per SM: warp 4 is a bulk-copy producer streaming the pages of the
+// CTA's (sequence, kv-head) work items through a 3-stage shared-memory ring (cp.async.bulk +
+// mbarrier), running ahead across work-item boundaries; warps 0-3 consume, each owning 16 tokens
+// of every page: S = Q K^T and O += P V on the tensor cores (mma.sync m16n8k16, the G query heads
+// of the group are rows 0..G-1 of the 16-row tile), online softmax per warp, then a 4-way merge
+// per work item.  HBM-bound by construction: ~1 MMA per 128 B of KV.
 #include "common.cuh"
 
 namespace mgb {
 
 constexpr int kPage = 64;
-constexpr int kAttnThreads = 128;
+constexpr int kAttnStages = 3;
+constexpr int kConsumerWarps = 4;
+constexpr int kAttnThreads = (kConsumerWarps + 1) * 32;
 
 template <int HD, int G>
-struct AttnSmem {
-  static constexpr int kTileElems = HD * kPage;                 // per K (or V) page-head block
-  static constexpr int kTileBytes = kTileElems * 2;
-  static constexpr int kGP = (G + 3) & ~3;                      // padded G for vector reads
-  static constexpr size_t kBytes = 2 * 2 * (size_t)kTileBytes   // {K,V} x 2 stages
-                                   + sizeof(float) * G * HD       // q
-                                   + sizeof(float) * 2 * G * kPage  // partial scores (2 halves)
-                                   + sizeof(float) * kPage * kGP    // p
-                                   + sizeof(float) * 4 * G          // m, l, alpha, pad
-                                   + 64;                            // mbarriers
+struct GqaSmem {
+  static constexpr int kTileElems = HD * kPage;
+  static constexpr int kTileBytes = kTileElems * 2;                 // one K (or V) page-head block
+  static constexpr int kStageBytes = 2 * kTileBytes;
+  static constexpr int kMergeStride = G * HD + 16;                  // per warp: O (G rows) + m[8] + l[8]
+  static constexpr int kMergeBytes = kConsumerWarps * kMergeStride * 4;
+  static constexpr size_t kBytes = (size_t)kAttnStages * kStageBytes + kMergeBytes + 128;
 };
 
+MGB_DEVINL void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+MGB_DEVINL void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+// D(16x8 f32) += A(16x16 bf16, row) * B(16x8 bf16, col)
+MGB_DEVINL void mma_bf16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                               uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+MGB_DEVINL void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
 template <int HD, int G>
-__global__ void __launch_bounds__(kAttnThreads)
+__global__ void __launch_bounds__(kAttnThreads, 2)
 decode_attn_gqa_kernel(const __nv_bfloat16* __restrict__ q,       // [B, Hkv*G, HD]
-                       const __nv_bfloat16* __restrict__ k_cache,  // pages
+                       const __nv_bfloat16* __restrict__ k_cache,  // pages, chunk-major
                        const __nv_bfloat16* __restrict__ v_cache,
                        const int* __restrict__ block_table, int max_pages,
-                       const int* __restrict__ seq_lens, int Hkv, float scale_log2,
+                       const int* __restrict__ seq_lens, int B, int Hkv, float scale_log2,
                        __nv_bfloat16* __restrict__ out) {          // [B, Hkv*G*HD]
-  using S = AttnSmem<HD, G>;
-  constexpr int kGP = S::kGP;
-  constexpr int NCH = HD / 8;            // 16 B chunks per head row
-  constexpr int NPAIR = HD / 2;          // dim pairs
-  constexpr int TGROUPS = kAttnThreads / NPAIR;
-  constexpr int TPG = kPage / TGROUPS;   // tokens per PV group
-  static_assert(kAttnThreads % NPAIR == 0 && kPage % TGROUPS == 0, "shape");
-
+  static_assert(G <= 8 && HD % 16 == 0, "GQA tile: G <= 8 query heads per kv head");
+  using S = GqaSmem<HD, G>;
+  constexpr int KSTEPS = HD / 16;   // k-steps of QK^T
+  constexpr int NT = HD / 8;        // n-tiles of PV (8 dims each)
   extern __shared__ __align__(128) uint8_t smem[];
-  __nv_bfloat16* kv_s = reinterpret_cast<__nv_bfloat16*>(smem);   // [stage][K|V][tile]
-  float* q_s = reinterpret_cast<float*>(smem + 4 * S::kTileBytes);  // [G][HD]
-  float* sp_s = q_s + G * HD;                                       // [2][G][kPage]
-  float* p_s = sp_s + 2 * G * kPage;                                // [kPage][kGP]
-  float* m_s = p_s + kPage * kGP;                                   // [G]
-  float* l_s = m_s + G;
-  float* a_s = l_s + G;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(
-      (reinterpret_cast<uintptr_t>(a_s + 2 * G) + 15) & ~uintptr_t(15));  // [2]
+  uint8_t* ring = smem;
+  float* merge = reinterpret_cast<float*>(smem + kAttnStages * S::kStageBytes);  // [warp][8][HD] + m,l
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kAttnStages * S::kStageBytes + S::kMergeBytes);
+  uint64_t* empty = full + kAttnStages;
 
-  const int b = blockIdx.x / Hkv;
-  const int h = blockIdx.x - b * Hkv;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int len = seq_lens[b];
-  const int npages = (len + kPage - 1) / kPage;
-  const int* bt = block_table + (size_t)b * max_pages;
-
-  if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_items = B * Hkv;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kAttnStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
     fence_mbar_init();
   }
-  for (int i = tid; i < G * HD; i += kAttnThreads)
-    q_s[i] = __bfloat162float(q[((size_t)b * Hkv * G + (size_t)h * G) * HD + i]) * scale_log2;
-  if (tid < G) {
-    m_s[tid] = -INFINITY;
-    l_s[tid] = 0.f;
-  }
   __syncthreads();
 
-  const uint64_t pol = policy_evict_first();
-  auto issue = [&](int i) {
-    const int stage = i & 1;
-    const size_t blk = ((size_t)bt[i] * Hkv + h) * S::kTileElems;
-    mbar_arrive_expect_tx(&bar[stage], 2 * S::kTileBytes);
-    bulk_load(kv_s + (size_t)stage * 2 * S::kTileElems, k_cache + blk, S::kTileBytes, &bar[stage], pol);
-    bulk_load(kv_s + (size_t)stage * 2 * S::kTileElems + S::kTileElems, v_cache + blk, S::kTileBytes, &bar[stage],
-              pol);
-  };
-  if (tid == 0 && npages > 0) issue(0);
-
-  float o[G][2];
-#pragma unroll
-  for (int g = 0; g < G; ++g) o[g][0] = o[g][1] = 0.f;
-
-  for (int i = 0; i < npages; ++i) {
-    if (tid == 0 && i + 1 < npages) issue(i + 1);
-    mbar_wait(&bar[i & 1], (i >> 1) & 1);
-    const __nv_bfloat16* k_t = kv_s + (size_t)(i & 1) * 2 * S::kTileElems;
-    const __nv_bfloat16* v_t = k_t + S::kTileElems;
-    const int n = min(kPage, len - i * kPage);
-
-    // ---- scores: thread = (token, half of the head dims) ----
-    {
-      const int tok = tid & (kPage - 1);
-      const int half = tid / kPage;  // 0 or 1
-      float s[G];
-#pragma unroll
-      for (int g = 0; g < G; ++g) s[g] = 0.f;
-#pragma unroll
-      for (int cc = 0; cc < NCH / 2; ++cc) {
-        const int c = half * (NCH / 2) + cc;
-        const uint4 kv = *reinterpret_cast<const uint4*>(k_t + ((size_t)c * kPage + tok) * 8);
-        const float k0 = bf16lo(kv.x), k1 = bf16hi(kv.x), k2 = bf16lo(kv.y), k3 = bf16hi(kv.y);
-        const float k4 = bf16lo(kv.z), k5 = bf16hi(kv.z), k6 = bf16lo(kv.w), k7 = bf16hi(kv.w);
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-          const float4 qa = *reinterpret_cast<const float4*>(q_s + g * HD + c * 8);
-          const float4 qb = *reinterpret_cast<const float4*>(q_s + g * HD + c * 8 + 4);
-          float acc = s[g];
-          acc = fmaf(qa.x, k0, acc); acc = fmaf(qa.y, k1, acc); acc = fmaf(qa.z, k2, acc); acc = fmaf(qa.w, k3, acc);
-          acc = fmaf(qb.x, k4, acc); acc = fmaf(qb.y, k5, acc); acc = fmaf(qb.z, k6, acc); acc = fmaf(qb.w, k7, acc);
-          s[g] = acc;
+  if (warp == kConsumerWarps) {
+    // ------------------------------ producer ------------------------------
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const int b = it / Hkv, h = it - b * Hkv;
+        const int np = (seq_lens[b] + kPage - 1) / kPage;
+        const int* bt = block_table + (size_t)b * max_pages;
+        for (int p = 0; p < np; ++p) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          const size_t blk = ((size_t)bt[p] * Hkv + h) * S::kTileElems;
+          uint8_t* dst = ring + stage * S::kStageBytes;
+          mbar_arrive_expect_tx(&full[stage], S::kStageBytes);
+          bulk_load(dst, k_cache + blk, S::kTileBytes, &full[stage], pol);
+          bulk_load(dst + S::kTileBytes, v_cache + blk, S::kTileBytes, &full[stage], pol);
+          if (++stage == kAttnStages) { stage = 0; phase ^= 1; }
         }
       }
-#pragma unroll
-      for (int g = 0; g < G; ++g) sp_s[(half * G + g) * kPage + tok] = s[g];
     }
-    __syncthreads();
+    return;
+  }
 
-    // ---- online softmax: one warp per head ----
-    for (int g = warp; g < G; g += kAttnThreads / 32) {
-      const int t0 = lane, t1 = lane + 32;
-      const float s0 = t0 < n ? sp_s[g * kPage + t0] + sp_s[(G + g) * kPage + t0] : -INFINITY;
-      const float s1 = t1 < n ? sp_s[g * kPage + t1] + sp_s[(G + g) * kPage + t1] : -INFINITY;
-      float mt = fmaxf(s0, s1);
+  // ------------------------------ consumers (warps 0..3) ------------------------------
+  const int g = lane >> 2, t = lane & 3;   // mma fragment coordinates
+  const bool row_ok = g < G;
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    const int b = it / Hkv, h = it - b * Hkv;
+    const int len = seq_lens[b];
+    const int np = (len + kPage - 1) / kPage;
+    // Q A-fragments (rows = the G query heads of this kv head; rows >= G are zero)
+    uint32_t qa[KSTEPS][2];
+    const __nv_bfloat16* qrow = q + ((size_t)b * Hkv * G + (size_t)h * G + (row_ok ? g : 0)) * HD;
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, off));
-      const float m_old = m_s[g];
-      const float m_new = fmaxf(m_old, mt);
-      const float alpha = exp2f(m_old - m_new);
-      const float p0 = exp2f(s0 - m_new), p1 = exp2f(s1 - m_new);
-      float ps = p0 + p1;
+    for (int ks = 0; ks < KSTEPS; ++ks) {
+      qa[ks][0] = row_ok ? *reinterpret_cast<const uint32_t*>(qrow + ks * 16 + 2 * t) : 0u;
+      qa[ks][1] = row_ok ? *reinterpret_cast<const uint32_t*>(qrow + ks * 16 + 8 + 2 * t) : 0u;
+    }
+    float o[NT][4];
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, off);
-      p_s[t0 * kGP + g] = p0;
-      p_s[t1 * kGP + g] = p1;
+    for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+    float m_run = -INFINITY, l_run = 0.f;
+
+    for (int p = 0; p < np; ++p) {
+      mbar_wait(&full[stage], phase);
+      const uint32_t kbase = smem_u32(ring + stage * S::kStageBytes);
+      const uint32_t vbase = kbase + S::kTileBytes;
+      const int tok0 = warp * 16;  // this warp's 16 tokens of the page
+      // ---- S = Q K^T for 16 tokens (two n-tiles of 8) ----
+      float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int ks = 0; ks < KSTEPS; ++ks) {
+        // matrices: (chunk 2ks, tok0..+7), (chunk 2ks+1, tok0..+7), (chunk 2ks, tok0+8..), (chunk 2ks+1, tok0+8..)
+        const int mi = lane >> 3, r = lane & 7;
+        const int chunk = 2 * ks + (mi & 1);
+        const int tok = tok0 + ((mi >> 1) << 3) + r;
+        uint32_t b00, b01, b10, b11;
+        ldsm_x4(kbase + (uint32_t)((chunk * kPage + tok) * 16), b00, b01, b10, b11);
+        mma_bf16_16816(s0, qa[ks][0], 0u, qa[ks][1], 0u, b00, b01);
+        mma_bf16_16816(s1, qa[ks][0], 0u, qa[ks][1], 0u, b10, b11);
+      }
+      // ---- online softmax over this warp's tokens (row g; columns 2t,2t+1 and 8+2t,8+2t+1) ----
+      const int n_valid = len - p * kPage - tok0;  // tokens of this warp that exist
+      float x0 = (2 * t < n_valid) ? s0[0] * scale_log2 : -INFINITY;
+      float x1 = (2 * t + 1 < n_valid) ? s0[1] * scale_log2 : -INFINITY;
+      float x2 = (8 + 2 * t < n_valid) ? s1[0] * scale_log2 : -INFINITY;
+      float x3 = (8 + 2 * t + 1 < n_valid) ? s1[1] * scale_log2 : -INFINITY;
+      float mt = fmaxf(fmaxf(x0, x1), fmaxf(x2, x3));
+      mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, 1));
+      mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, 2));
+      const float m_new = fmaxf(m_run, mt);
+      const float m_use = (m_new == -INFINITY) ? 0.f : m_new;
+      const float alpha = exp2f(m_run - m_use);
+      const float p0 = exp2f(x0 - m_use), p1 = exp2f(x1 - m_use), p2 = exp2f(x2 - m_use), p3 = exp2f(x3 - m_use);
+      l_run = l_run * alpha + (p0 + p1 + p2 + p3);
+      m_run = m_new;
+#pragma unroll
+      for (int n = 0; n < NT; ++n) {
+        o[n][0] *= alpha;
+        o[n][1] *= alpha;
+      }
+      // P as the A operand (k = 16 tokens): rows >= G are zero
+      const uint32_t pa0 = row_ok ? pack_bf16x2(p0, p1) : 0u;
+      const uint32_t pa2 = row_ok ? pack_bf16x2(p2, p3) : 0u;
+      // ---- O += P V : two dim-chunks (n-tiles) per ldmatrix.x4.trans ----
+#pragma unroll
+      for (int n2 = 0; n2 < NT / 2; ++n2) {
+        const int mi = lane >> 3, r = lane & 7;
+        const int chunk = 2 * n2 + (mi >> 1);
+        const int tok = tok0 + ((mi & 1) << 3) + r;
+        uint32_t v0a, v0b, v1a, v1b;
+        ldsm_x4_t(vbase + (uint32_t)((chunk * kPage + tok) * 16), v0a, v0b, v1a, v1b);
+        mma_bf16_16816(o[2 * n2], pa0, 0u, pa2, 0u, v0a, v0b);
+        mma_bf16_16816(o[2 * n2 + 1], pa0, 0u, pa2, 0u, v1a, v1b);
+      }
       __syncwarp();
-      if (lane == 0) {
-        m_s[g] = m_new;
-        l_s[g] = l_s[g] * alpha + ps;
-        a_s[g] = alpha;
-      }
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == kAttnStages) { stage = 0; phase ^= 1; }
     }
-    __syncthreads();
 
-    // ---- P V: thread = (dim pair, token group) ----
-    {
-      const int dp = tid % NPAIR;
-      const int tg = tid / NPAIR;
+    // ---- merge the 4 warps' partial (m, l, O) and store ----
+    l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
+    l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
+    constexpr int MS = S::kMergeStride;
+    float* mo = merge + warp * MS;
+    if (row_ok) {
 #pragma unroll
-      for (int g = 0; g < G; ++g) {
-        const float al = a_s[g];
-        o[g][0] *= al;
-        o[g][1] *= al;
+      for (int n = 0; n < NT; ++n) {
+        mo[g * HD + n * 8 + 2 * t] = o[n][0];
+        mo[g * HD + n * 8 + 2 * t + 1] = o[n][1];
       }
-      const int tb = tg * TPG;
-      const int te = min(tb + TPG, n);
-      for (int t = tb; t < te; ++t) {
-        const uint32_t v2 = *reinterpret_cast<const uint32_t*>(v_t + (size_t)t * HD + 2 * dp);
-        const float v0 = bf16lo(v2), v1 = bf16hi(v2);
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-          const float p = p_s[t * kGP + g];
-          o[g][0] = fmaf(p, v0, o[g][0]);
-          o[g][1] = fmaf(p, v1, o[g][1]);
-        }
+      if (t == 0) {
+        mo[G * HD + g] = m_run;
+        mo[G * HD + 8 + g] = l_run;
       }
     }
-    __syncthreads();  // stage (i & 1) fully consumed before it is refilled at iteration i + 1
-  }
-
-  // ---- reduce the token groups, normalise, store ----
-  float* red = reinterpret_cast<float*>(smem);  // reuse the KV stages: [TGROUPS][G][HD]
-  {
-    const int dp = tid % NPAIR;
-    const int tg = tid / NPAIR;
+    named_bar_sync(1, kConsumerWarps * 32);
+    for (int i = threadIdx.x; i < G * HD; i += kConsumerWarps * 32) {
+      const int row = i / HD, col = i - row * HD;
+      float M = -INFINITY;
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-      red[((size_t)tg * G + g) * HD + 2 * dp] = o[g][0];
-      red[((size_t)tg * G + g) * HD + 2 * dp + 1] = o[g][1];
+      for (int w = 0; w < kConsumerWarps; ++w) M = fmaxf(M, merge[w * MS + G * HD + row]);
+      float num = 0.f, den = 0.f;
+#pragma unroll
+      for (int w = 0; w < kConsumerWarps; ++w) {
+        const float* mw = merge + w * MS;
+        const float mw_row = mw[G * HD + row];
+        const float sc = (mw_row == -INFINITY) ? 0.f : exp2f(mw_row - M);
+        num += sc * mw[row * HD + col];
+        den += sc * mw[G * HD + 8 + row];
+      }
+      out[((size_t)b * Hkv * G + (size_t)h * G + row) * HD + col] = __float2bfloat16_rn(den > 0.f ? num / den : 0.f);
     }
-  }
-  __syncthreads();
-  for (int i = tid; i < G * HD; i += kAttnThreads) {
-    const int g = i / HD;
-    float acc = 0.f;
-#pragma unroll
-    for (int tg = 0; tg < TGROUPS; ++tg) acc += red[(size_t)tg * G * HD + i];
-    const float l = l_s[g];
-    out[((size_t)b * Hkv * G + (size_t)h * G) * HD + i] = __float2bfloat16_rn(l > 0.f ? acc / l : 0.f);
+    named_bar_sync(1, kConsumerWarps * 32);  // merge buffer reused by the next item
   }
 }
 
 template <int HD, int G>
 int launch_gqa(const void* q, const void* kc, const void* vc, const int* bt, int max_pages, const int* lens, int B,
                int Hkv, float scale, void* out, cudaStream_t st) {
-  using S = AttnSmem<HD, G>;
+  using S = GqaSmem<HD, G>;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(decode_attn_gqa_kernel<HD, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -213,9 +236,12 @@ int launch_gqa(const void* q, const void* kc, const void* vc, const int* bt, int
       return MGB_ECUDA;
     attr = true;
   }
-  decode_attn_gqa_kernel<HD, G><<<B * Hkv, kAttnThreads, S::kBytes, st>>>(
+  const int items = B * Hkv;
+  int grid = 2 * mgb_host::num_sms();
+  if (grid > items) grid = items;
+  decode_attn_gqa_kernel<HD, G><<<grid, kAttnThreads, S::kBytes, st>>>(
       reinterpret_cast<const __nv_bfloat16*>(q), reinterpret_cast<const __nv_bfloat16*>(kc),
-      reinterpret_cast<const __nv_bfloat16*>(vc), bt, max_pages, lens, Hkv, scale * 1.4426950408889634f,
+      reinterpret_cast<const __nv_bfloat16*>(vc), bt, max_pages, lens, B, Hkv, scale * 1.4426950408889634f,
       reinterpret_cast<__nv_bfloat16*>(out));
   return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
 }

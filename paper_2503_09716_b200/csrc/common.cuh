@@ -92,6 +92,13 @@ MGB_DEVINL void tma_load_2d(void* smem_dst, const CUtensorMap* m, uint64_t* bar,
       "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
       : "memory");
 }
+// Warm L2 with a tile that a later TMA load will fetch (turns its DRAM latency into L2 latency).
+MGB_DEVINL void tma_prefetch_2d(const CUtensorMap* m, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
 // 1-D bulk copy global -> shared (no tensor map; 16 B aligned, size multiple of 16)
 MGB_DEVINL void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar,
                           uint64_t policy) {

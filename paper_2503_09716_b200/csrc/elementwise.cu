@@ -23,51 +23,56 @@ MGB_DEVINL float block_sum(float v, float* red) {
 }
 
 // x' = delta ? bf16(x + delta) : x; x_out = x'; y = bf16(w * bf16(x' * rsqrt(mean(x'^2) + eps)))
-__global__ void add_rmsnorm_kernel(const __nv_bfloat16* x, const __nv_bfloat16* __restrict__ delta,
-                                   const __nv_bfloat16* __restrict__ w, float eps, int d,
-                                   __nv_bfloat16* x_out, __nv_bfloat16* __restrict__ y) {
+// One CTA per row; the row stays in registers between the reduction and the normalisation.
+constexpr int kNormThreads = 256;
+constexpr int kNormVec = 4;  // d <= 8192
+__global__ void __launch_bounds__(kNormThreads)
+add_rmsnorm_kernel(const __nv_bfloat16* x, const __nv_bfloat16* __restrict__ delta,
+                   const __nv_bfloat16* __restrict__ w, float eps, int d, __nv_bfloat16* x_out,
+                   __nv_bfloat16* __restrict__ y) {
   __shared__ float red[32];
   const size_t row = blockIdx.x;
+  const int nvec = d / 8;
   const uint4* xr = reinterpret_cast<const uint4*>(x + row * d);
   const uint4* dr = delta ? reinterpret_cast<const uint4*>(delta + row * d) : nullptr;
-  float ss = 0.f;
-  for (int c = threadIdx.x; c < d / 8; c += blockDim.x) {
-    uint4 v = xr[c];
-    if (dr) {
-      const uint4 dv = dr[c];
-      v.x = pack_bf16x2(bf16lo(v.x) + bf16lo(dv.x), bf16hi(v.x) + bf16hi(dv.x));
-      v.y = pack_bf16x2(bf16lo(v.y) + bf16lo(dv.y), bf16hi(v.y) + bf16hi(dv.y));
-      v.z = pack_bf16x2(bf16lo(v.z) + bf16lo(dv.z), bf16hi(v.z) + bf16hi(dv.z));
-      v.w = pack_bf16x2(bf16lo(v.w) + bf16lo(dv.w), bf16hi(v.w) + bf16hi(dv.w));
+  uint4 v[kNormVec], dv[kNormVec];
+#pragma unroll
+  for (int u = 0; u < kNormVec; ++u) {
+    const int c = threadIdx.x + u * kNormThreads;
+    if (c < nvec) {
+      v[u] = xr[c];
+      if (dr) dv[u] = dr[c];
     }
-    if (x_out) reinterpret_cast<uint4*>(x_out + row * d)[c] = v;
-    const float f[8] = {bf16lo(v.x), bf16hi(v.x), bf16lo(v.y), bf16hi(v.y),
-                        bf16lo(v.z), bf16hi(v.z), bf16lo(v.w), bf16hi(v.w)};
+  }
+  float ss = 0.f;
+#pragma unroll
+  for (int u = 0; u < kNormVec; ++u) {
+    const int c = threadIdx.x + u * kNormThreads;
+    if (c >= nvec) continue;
+    if (dr) {
+      v[u].x = pack_bf16x2(bf16lo(v[u].x) + bf16lo(dv[u].x), bf16hi(v[u].x) + bf16hi(dv[u].x));
+      v[u].y = pack_bf16x2(bf16lo(v[u].y) + bf16lo(dv[u].y), bf16hi(v[u].y) + bf16hi(dv[u].y));
+      v[u].z = pack_bf16x2(bf16lo(v[u].z) + bf16lo(dv[u].z), bf16hi(v[u].z) + bf16hi(dv[u].z));
+      v[u].w = pack_bf16x2(bf16lo(v[u].w) + bf16lo(dv[u].w), bf16hi(v[u].w) + bf16hi(dv[u].w));
+    }
+    if (x_out) reinterpret_cast<uint4*>(x_out + row * d)[c] = v[u];
+    const float f[8] = {bf16lo(v[u].x), bf16hi(v[u].x), bf16lo(v[u].y), bf16hi(v[u].y),
+                        bf16lo(v[u].z), bf16hi(v[u].z), bf16lo(v[u].w), bf16hi(v[u].w)};
 #pragma unroll
     for (int i = 0; i < 8; ++i) ss = fmaf(f[i], f[i], ss);
   }
   const float inv = 1.0f / sqrtf(block_sum(ss, red) / (float)d + eps);
   const uint4* wr = reinterpret_cast<const uint4*>(w);
-  for (int c = threadIdx.x; c < d / 8; c += blockDim.x) {
-    uint4 v;
-    if (x_out) {
-      v = reinterpret_cast<const uint4*>(x_out + row * d)[c];  // x' written by this thread above
-    } else {
-      v = xr[c];
-      if (dr) {  // recompute x' (same rounding as above)
-        const uint4 dv = dr[c];
-        v.x = pack_bf16x2(bf16lo(v.x) + bf16lo(dv.x), bf16hi(v.x) + bf16hi(dv.x));
-        v.y = pack_bf16x2(bf16lo(v.y) + bf16lo(dv.y), bf16hi(v.y) + bf16hi(dv.y));
-        v.z = pack_bf16x2(bf16lo(v.z) + bf16lo(dv.z), bf16hi(v.z) + bf16hi(dv.z));
-        v.w = pack_bf16x2(bf16lo(v.w) + bf16lo(dv.w), bf16hi(v.w) + bf16hi(dv.w));
-      }
-    }
+#pragma unroll
+  for (int u = 0; u < kNormVec; ++u) {
+    const int c = threadIdx.x + u * kNormThreads;
+    if (c >= nvec) continue;
     const uint4 wv = wr[c];
     uint4 o;
-    o.x = pack_bf16x2(bf16lo(wv.x) * bf16_round(bf16lo(v.x) * inv), bf16hi(wv.x) * bf16_round(bf16hi(v.x) * inv));
-    o.y = pack_bf16x2(bf16lo(wv.y) * bf16_round(bf16lo(v.y) * inv), bf16hi(wv.y) * bf16_round(bf16hi(v.y) * inv));
-    o.z = pack_bf16x2(bf16lo(wv.z) * bf16_round(bf16lo(v.z) * inv), bf16hi(wv.z) * bf16_round(bf16hi(v.z) * inv));
-    o.w = pack_bf16x2(bf16lo(wv.w) * bf16_round(bf16lo(v.w) * inv), bf16hi(wv.w) * bf16_round(bf16hi(v.w) * inv));
+    o.x = pack_bf16x2(bf16lo(wv.x) * bf16_round(bf16lo(v[u].x) * inv), bf16hi(wv.x) * bf16_round(bf16hi(v[u].x) * inv));
+    o.y = pack_bf16x2(bf16lo(wv.y) * bf16_round(bf16lo(v[u].y) * inv), bf16hi(wv.y) * bf16_round(bf16hi(v[u].y) * inv));
+    o.z = pack_bf16x2(bf16lo(wv.z) * bf16_round(bf16lo(v[u].z) * inv), bf16hi(wv.z) * bf16_round(bf16hi(v[u].z) * inv));
+    o.w = pack_bf16x2(bf16lo(wv.w) * bf16_round(bf16lo(v[u].w) * inv), bf16hi(wv.w) * bf16_round(bf16hi(v[u].w) * inv));
     reinterpret_cast<uint4*>(y + row * d)[c] = o;
   }
 }
@@ -81,38 +86,50 @@ __global__ void rope_append_gqa_kernel(const __nv_bfloat16* __restrict__ qkv, in
                                        const int* __restrict__ block_table, int max_pages,
                                        __nv_bfloat16* __restrict__ k_cache, __nv_bfloat16* __restrict__ v_cache,
                                        __nv_bfloat16* __restrict__ q_out, int* __restrict__ seq_lens) {
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
+  // one thread per (token, head, 8-dim chunk): 16 B in, 16 B out
+  const int nch = hd / 8;
   const int H = Hq + 2 * Hkv;
-  if (gw >= T * H) return;
-  const int t = gw / H, hh = gw - t * H;
+  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (long long)T * H * nch) return;
+  const int c = (int)(gid % nch);
+  const long long th = gid / nch;
+  const int t = (int)(th / H), hh = (int)(th - (long long)t * H);
   const int seq = seq0 + t;
   const int pos = positions[seq];
   const __nv_bfloat16* src = qkv + ((size_t)t * H + hh) * hd;
-  const int half = hd / 2;
   const int page = block_table[(size_t)seq * max_pages + pos / kPageTok];
   const int slot = pos % kPageTok;
-  if (seq_lens && hh == 0 && lane == 0) seq_lens[seq] = pos + 1;  // cache length after the append
-  for (int i = lane; i < hd; i += 32) {
-    float v = __bfloat162float(src[i]);
-    if (hh < Hq + Hkv) {
-      const int fi = i < half ? i : i - half;
-      const float c = cos_t[(size_t)pos * half + fi], s = sin_t[(size_t)pos * half + fi];
-      const float rh = i < half ? -__bfloat162float(src[i + half]) : __bfloat162float(src[i - half]);
-      v = bf16_round(v * c) + bf16_round(rh * s);
+  if (seq_lens && hh == 0 && c == 0) seq_lens[seq] = pos + 1;  // cache length after the append
+  const uint4 xv = reinterpret_cast<const uint4*>(src)[c];
+  uint4 ov = xv;
+  if (hh < Hq + Hkv) {
+    const int half_ch = nch / 2;
+    const bool lo = c < half_ch;
+    const uint4 pv = reinterpret_cast<const uint4*>(src)[lo ? c + half_ch : c - half_ch];
+    const float x[8] = {bf16lo(xv.x), bf16hi(xv.x), bf16lo(xv.y), bf16hi(xv.y),
+                        bf16lo(xv.z), bf16hi(xv.z), bf16lo(xv.w), bf16hi(xv.w)};
+    const float pr[8] = {bf16lo(pv.x), bf16hi(pv.x), bf16lo(pv.y), bf16hi(pv.y),
+                         bf16lo(pv.z), bf16hi(pv.z), bf16lo(pv.w), bf16hi(pv.w)};
+    const int fi0 = (lo ? c : c - half_ch) * 8;
+    const float* cs = cos_t + (size_t)pos * (hd / 2) + fi0;
+    const float* sn = sin_t + (size_t)pos * (hd / 2) + fi0;
+    float r[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float rh = lo ? -pr[i] : pr[i];  // rotate_half
+      r[i] = bf16_round(x[i] * cs[i]) + bf16_round(rh * sn[i]);
     }
-    const __nv_bfloat16 bv = __float2bfloat16_rn(v);
-    if (hh < Hq) {
-      q_out[((size_t)t * Hq + hh) * hd + i] = bv;
-    } else if (hh < Hq + Hkv) {
-      const int kh = hh - Hq;
-      const size_t blk = ((size_t)page * Hkv + kh) * hd * kPageTok;
-      k_cache[blk + ((size_t)(i / 8) * kPageTok + slot) * 8 + (i % 8)] = bv;
-    } else {
-      const int vh = hh - Hq - Hkv;
-      const size_t blk = ((size_t)page * Hkv + vh) * hd * kPageTok;
-      v_cache[blk + (size_t)slot * hd + i] = bv;
-    }
+    ov.x = pack_bf16x2(r[0], r[1]); ov.y = pack_bf16x2(r[2], r[3]);
+    ov.z = pack_bf16x2(r[4], r[5]); ov.w = pack_bf16x2(r[6], r[7]);
+  }
+  if (hh < Hq) {
+    reinterpret_cast<uint4*>(q_out + ((size_t)t * Hq + hh) * hd)[c] = ov;
+  } else {
+    const bool is_k = hh < Hq + Hkv;
+    const int kh = is_k ? hh - Hq : hh - Hq - Hkv;
+    const size_t blk = ((size_t)page * Hkv + kh) * hd * kPageTok;
+    __nv_bfloat16* dst = (is_k ? k_cache : v_cache) + blk + ((size_t)c * kPageTok + slot) * 8;
+    *reinterpret_cast<uint4*>(dst) = ov;
   }
 }
 
@@ -193,9 +210,8 @@ extern "C" {
 
 int mgb_add_rmsnorm(const void* x, const void* delta, const void* weight, float eps, int T, int d, void* x_out,
                     void* y, void* stream) {
-  if (T < 1 || d % 8) return MGB_EINVAL;
-  const int threads = d / 8 >= 256 ? 256 : ((d / 8 + 31) / 32) * 32;
-  mgb::add_rmsnorm_kernel<<<T, threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+  if (T < 1 || d % 8 || d > 8 * mgb::kNormThreads * mgb::kNormVec) return MGB_EINVAL;
+  mgb::add_rmsnorm_kernel<<<T, mgb::kNormThreads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<const __nv_bfloat16*>(x), reinterpret_cast<const __nv_bfloat16*>(delta),
       reinterpret_cast<const __nv_bfloat16*>(weight), eps, d, reinterpret_cast<__nv_bfloat16*>(x_out),
       reinterpret_cast<__nv_bfloat16*>(y));
@@ -205,10 +221,10 @@ int mgb_add_rmsnorm(const void* x, const void* delta, const void* weight, float 
 int mgb_rope_append_gqa(const void* qkv, int T, int seq0, const int* positions, const float* cos_t,
                         const float* sin_t, int Hq, int Hkv, int head_dim, const int* block_table, int max_pages,
                         void* k_cache, void* v_cache, void* q_out, int* seq_lens, void* stream) {
-  if (T < 1 || head_dim % 8 || Hq % Hkv) return MGB_EINVAL;
-  const int warps = T * (Hq + 2 * Hkv);
+  if (T < 1 || head_dim % 16 || Hq % Hkv) return MGB_EINVAL;
+  const long long items = (long long)T * (Hq + 2 * Hkv) * (head_dim / 8);
   const int threads = 256;
-  mgb::rope_append_gqa_kernel<<<(warps * 32 + threads - 1) / threads, threads, 0,
+  mgb::rope_append_gqa_kernel<<<(int)((items + threads - 1) / threads), threads, 0,
                                 reinterpret_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<const __nv_bfloat16*>(qkv), T, seq0, positions, cos_t, sin_t, Hq, Hkv, head_dim, block_table,
       max_pages, reinterpret_cast<__nv_bfloat16*>(k_cache), reinterpret_cast<__nv_bfloat16*>(v_cache),

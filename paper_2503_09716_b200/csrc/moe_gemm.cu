@@ -15,6 +15,8 @@
 // Persistent grid (one CTA per SM), static round-robin over (expert, token-tile, row-tile) units
 // ordered row-tile-fastest so concurrently running CTAs share the same token tile in L2.
 // Warp roles: w0 = TMA producer, w1 = MMA issuer (+TMEM owner), w2..w5 = epilogue.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace mgb {
@@ -60,7 +62,7 @@ template <int NA>
 __global__ void __launch_bounds__(192, 1)
 moe_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const int* __restrict__ offsets, int E, int MT, int K, int rows_per_expert,
-                int half_rows, __nv_bfloat16* __restrict__ out, int ldo) {
+                int half_rows, __nv_bfloat16* __restrict__ out, int ldo, int prefetch) {
   using Cfg = GemmCfg<NA>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -114,13 +116,30 @@ moe_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       const uint64_t pol_x = policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
+      // optional L2 prefetch of the weight tiles `prefetch` k-blocks ahead of the TMA loads
+      // (crossing into the CTA's next unit); measured slower on B200 at decode shapes -> off.
+      auto prefetch_a = [&](int u, int kb) {
+        int e2, nt2, mt2, tok2, n2;
+        sched.decode(u, offsets, e2, nt2, mt2, tok2, n2);
+        const int r0 = e2 * rows_per_expert + mt2 * kBM;
+        tma_prefetch_2d(&tmA, kb * kBK, r0);
+        if (NA == 2) tma_prefetch_2d(&tmA, kb * kBK, r0 + half_rows);
+      };
+      if (blockIdx.x < total)
+        for (int kb = 0; kb < prefetch && kb < KB; ++kb) prefetch_a(blockIdx.x, kb);
       for (int u = blockIdx.x; u < total; u += gridDim.x) {
         int e, nt, mt, tok0, n;
         sched.decode(u, offsets, e, nt, mt, tok0, n);
         const int nb = (n + kBRows - 1) / kBRows;
         const uint32_t bytes = NA * kATileBytes + nb * kBBoxBytes;
         const int arow0 = e * rows_per_expert + mt * kBM;
+        const int u_next = u + gridDim.x;
         for (int kb = 0; kb < KB; ++kb) {
+          if (prefetch > 0) {
+            const int pf = kb + prefetch;
+            if (pf < KB) prefetch_a(u, pf);
+            else if (u_next < total && pf - KB < KB) prefetch_a(u_next, pf - KB);
+          }
           mbar_wait(&empty_bar[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full_bar[stage], bytes);
           uint8_t* st = tiles + stage * Cfg::kStageBytes;
@@ -221,6 +240,14 @@ moe_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 // Host side
 // ------------------------------------------------------------------------------------------
 namespace {
+int gemm_prefetch_distance() {
+  static int v = [] {
+    const char* e = getenv("MGB_GEMM_PREFETCH");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
 template <int NA>
 int launch_moe_gemm(const void* w, int w_rows_total, const void* act, int act_rows, const int* offsets,
                     int E, int MT, int K, int rows_per_expert, int half_rows, void* out, int ldo,
@@ -241,7 +268,7 @@ int launch_moe_gemm(const void* w, int w_rows_total, const void* act, int act_ro
   const int grid = mgb_host::num_sms();
   mgb::moe_gemm_kernel<NA><<<grid, 192, Cfg::kSmemBytes, stream>>>(
       tmA, tmB, offsets, E, MT, K, rows_per_expert, half_rows,
-      reinterpret_cast<__nv_bfloat16*>(out), ldo);
+      reinterpret_cast<__nv_bfloat16*>(out), ldo, gemm_prefetch_distance());
   return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
 }
 }  // namespace

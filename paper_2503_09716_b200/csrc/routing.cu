@@ -79,21 +79,34 @@ __global__ void __launch_bounds__(kRouterThreads) router_topk_kernel(RouterArgs 
     for (int i = threadIdx.x; i < ntok * E; i += blockDim.x)
       s_logit[(i / E) * kMaxE + (i % E)] = a.logits_in[(size_t)(t0 + i / E) * E + (i % E)];
   } else {
-    // stage the CTA's token rows in smem (16 B vectors)
+    // stage the CTA's (contiguous) token rows in smem with one bulk copy (TMA engine)
     const int vec_per_row = d / 8;
-    for (int i = threadIdx.x; i < ntok * vec_per_row; i += blockDim.x) {
-      const int r = i / vec_per_row, c = i - r * vec_per_row;
-      reinterpret_cast<uint4*>(s_x)[r * vec_per_row + c] =
-          ld_nc_v4(reinterpret_cast<const uint4*>(a.x + (size_t)(t0 + r) * d) + c);
+    __shared__ __align__(8) uint64_t s_bar;
+    if (threadIdx.x == 0) {
+      mbar_init(&s_bar, 1);
+      fence_mbar_init();
+      const uint32_t bytes = (uint32_t)ntok * d * 2;
+      mbar_arrive_expect_tx(&s_bar, bytes);
+      bulk_load(s_x, a.x + (size_t)t0 * d, bytes, &s_bar, policy_evict_first());
     }
     __syncthreads();
+    mbar_wait(&s_bar, 0);
     for (int e = warp; e < E; e += kRouterThreads / 32) {
       float acc[kRouterTPB];
 #pragma unroll
       for (int t = 0; t < kRouterTPB; ++t) acc[t] = 0.f;
       const uint4* wrow = reinterpret_cast<const uint4*>(a.wg + (size_t)e * d);
-      for (int c = lane; c < vec_per_row; c += 32) {
-        const uint4 w = __ldg(wrow + c);
+      // the warp's whole gate row (<= 24 x 16 B per lane) is requested before any use
+      constexpr int kWV = 24;
+      uint4 wreg[kWV];
+#pragma unroll
+      for (int i = 0; i < kWV; ++i)
+        if (lane + 32 * i < vec_per_row) wreg[i] = __ldg(wrow + lane + 32 * i);
+#pragma unroll
+      for (int i = 0; i < kWV; ++i) {
+        const int c = lane + 32 * i;
+        if (c >= vec_per_row) break;
+        const uint4 w = wreg[i];
         const float w0 = bf16lo(w.x), w1 = bf16hi(w.x), w2 = bf16lo(w.y), w3 = bf16hi(w.y);
         const float w4 = bf16lo(w.z), w5 = bf16hi(w.z), w6 = bf16lo(w.w), w7 = bf16hi(w.w);
 #pragma unroll
@@ -204,16 +217,43 @@ __global__ void __launch_bounds__(kRouterThreads) router_topk_kernel(RouterArgs 
   // ---------------- last CTA: per-block bases, counts, offsets ----------------
   __threadfence();
   int* s_cnt = reinterpret_cast<int*>(smem);  // reuse
-  for (int e = threadIdx.x; e < E; e += blockDim.x) {
-    int run = 0;
-    for (int b = 0; b < (int)gridDim.x; ++b) {
-      int* p = a.block_hist + (size_t)b * E + e;
-      const int c = __ldcg(p);
-      *p = run;
-      run += c;
+  // Exclusive scan of block_hist down each expert column.  A warp owns 4 experts at a time and
+  // 32 blocks per chunk (all loads of a chunk in flight together, warp shuffles for the scan),
+  // so the serial depth is nblk/32 L2 round trips instead of nblk.
+  {
+    const int NB = gridDim.x;
+    for (int eg = warp; eg * 4 < E; eg += kRouterThreads / 32) {
+      int carry[4] = {0, 0, 0, 0};
+      for (int b0 = 0; b0 < NB; b0 += 32) {
+        const int b = b0 + lane;
+        int v[4];
+#pragma unroll
+        for (int qd = 0; qd < 4; ++qd) {
+          const int e = eg * 4 + qd;
+          v[qd] = (e < E && b < NB) ? __ldcg(a.block_hist + (size_t)b * E + e) : 0;
+        }
+#pragma unroll
+        for (int qd = 0; qd < 4; ++qd) {
+          int incl = v[qd];
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+          }
+          const int e = eg * 4 + qd;
+          if (e < E && b < NB) a.block_hist[(size_t)b * E + e] = carry[qd] + incl - v[qd];
+          carry[qd] += __shfl_sync(0xffffffffu, incl, 31);
+        }
+      }
+      if (lane == 0)
+        for (int qd = 0; qd < 4; ++qd) {
+          const int e = eg * 4 + qd;
+          if (e < E) {
+            a.counts[e] = carry[qd];
+            s_cnt[e] = carry[qd];
+          }
+        }
     }
-    a.counts[e] = run;
-    s_cnt[e] = run;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -245,52 +285,120 @@ __global__ void permute_kernel(const __nv_bfloat16* __restrict__ x, const int* _
   }
   const uint4* src = reinterpret_cast<const uint4*>(x + (size_t)t * d);
   uint4* dst = reinterpret_cast<uint4*>(x_perm + (size_t)pos * d);
-  for (int c = lane; c < d / 8; c += 32) dst[c] = ld_nc_v4(src + c);
+  // all of the lane's 16 B vectors in flight before any store (row <= 8 KB -> <= 24 vectors/lane)
+  constexpr int U = 8;
+  const int nvec = d / 8;
+  for (int c0 = lane; c0 < nvec; c0 += 32 * U) {
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (c0 + 32 * u < nvec) v[u] = ld_nc_v4(src + c0 + 32 * u);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (c0 + 32 * u < nvec) dst[c0 + 32 * u] = v[u];
+  }
 }
 
 // out[t] = bf16( sum_j w[t,j] * y[dst[t,j]] ) (fp32, j ascending), then optional
-//          moe = bf16(moe + shared[t]), then optional out = bf16(residual[t] + moe).
-// One CTA per token, 8 dims (16 B) per thread per iteration.
-__global__ void combine_kernel(const __nv_bfloat16* __restrict__ y_perm, const int* __restrict__ dst_pos,
-                               const float* __restrict__ topk_w, const __nv_bfloat16* __restrict__ shared_out,
-                               const __nv_bfloat16* residual, int T, int d, int k,
-                               __nv_bfloat16* out) {  // out may alias residual (in-place residual add)
+//          moe = bf16(moe + shared[t]), then optional out = bf16(residual[t] + moe),
+//          then optional norm_out[t] = RMSNorm(out[t]) * norm_w (HF MixtralRMSNorm rounding) --
+//          the next layer's input norm fused into the row this CTA just produced.
+// One CTA per token; the whole row lives in registers (<= kCombineVec 16 B vectors / thread).
+constexpr int kCombineThreads = 256;
+constexpr int kCombineVec = 4;  // d <= 8192
+__global__ void __launch_bounds__(kCombineThreads)
+combine_kernel(const __nv_bfloat16* __restrict__ y_perm, const int* __restrict__ dst_pos,
+               const float* __restrict__ topk_w, const __nv_bfloat16* __restrict__ shared_out,
+               const __nv_bfloat16* residual, int T, int d, int k,
+               __nv_bfloat16* out,  // may alias residual (in-place residual add)
+               const __nv_bfloat16* __restrict__ norm_w, float eps, __nv_bfloat16* __restrict__ norm_out) {
   const int t = blockIdx.x;
   __shared__ int s_pos[kMaxK];
   __shared__ float s_w[kMaxK];
+  __shared__ float s_red[kCombineThreads / 32];
   if (threadIdx.x < k) {
     s_pos[threadIdx.x] = dst_pos[(size_t)t * k + threadIdx.x];
     s_w[threadIdx.x] = topk_w[(size_t)t * k + threadIdx.x];
   }
   __syncthreads();
-  for (int c = threadIdx.x; c < d / 8; c += blockDim.x) {
-    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int j = 0; j < k; ++j) {
-      const uint4 v = ld_nc_v4(reinterpret_cast<const uint4*>(y_perm + (size_t)s_pos[j] * d) + c);
-      const float w = s_w[j];
-      acc[0] += w * bf16lo(v.x); acc[1] += w * bf16hi(v.x);
-      acc[2] += w * bf16lo(v.y); acc[3] += w * bf16hi(v.y);
-      acc[4] += w * bf16lo(v.z); acc[5] += w * bf16hi(v.z);
-      acc[6] += w * bf16lo(v.w); acc[7] += w * bf16hi(v.w);
+  const int nvec = d / 8;
+  float acc[kCombineVec][8];
+#pragma unroll
+  for (int u = 0; u < kCombineVec; ++u)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[u][i] = 0.f;
+  for (int j = 0; j < k; ++j) {
+    const uint4* yrow = reinterpret_cast<const uint4*>(y_perm + (size_t)s_pos[j] * d);
+    const float w = s_w[j];
+    uint4 v[kCombineVec];
+#pragma unroll
+    for (int u = 0; u < kCombineVec; ++u) {
+      const int c = threadIdx.x + u * kCombineThreads;
+      if (c < nvec) v[u] = ld_nc_v4(yrow + c);
     }
 #pragma unroll
-    for (int i = 0; i < 8; ++i) acc[i] = bf16_round(acc[i]);
+    for (int u = 0; u < kCombineVec; ++u) {
+      const int c = threadIdx.x + u * kCombineThreads;
+      if (c < nvec) {
+        acc[u][0] += w * bf16lo(v[u].x); acc[u][1] += w * bf16hi(v[u].x);
+        acc[u][2] += w * bf16lo(v[u].y); acc[u][3] += w * bf16hi(v[u].y);
+        acc[u][4] += w * bf16lo(v[u].z); acc[u][5] += w * bf16hi(v[u].z);
+        acc[u][6] += w * bf16lo(v[u].w); acc[u][7] += w * bf16hi(v[u].w);
+      }
+    }
+  }
+  float ss = 0.f;
+#pragma unroll
+  for (int u = 0; u < kCombineVec; ++u) {
+    const int c = threadIdx.x + u * kCombineThreads;
+    if (c >= nvec) continue;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[u][i] = bf16_round(acc[u][i]);
     if (shared_out) {
-      const uint4 s = ld_nc_v4(reinterpret_cast<const uint4*>(shared_out + (size_t)t * d) + c);
-      acc[0] = bf16_round(acc[0] + bf16lo(s.x)); acc[1] = bf16_round(acc[1] + bf16hi(s.x));
-      acc[2] = bf16_round(acc[2] + bf16lo(s.y)); acc[3] = bf16_round(acc[3] + bf16hi(s.y));
-      acc[4] = bf16_round(acc[4] + bf16lo(s.z)); acc[5] = bf16_round(acc[5] + bf16hi(s.z));
-      acc[6] = bf16_round(acc[6] + bf16lo(s.w)); acc[7] = bf16_round(acc[7] + bf16hi(s.w));
+      const uint4 sv = ld_nc_v4(reinterpret_cast<const uint4*>(shared_out + (size_t)t * d) + c);
+      const float f[8] = {bf16lo(sv.x), bf16hi(sv.x), bf16lo(sv.y), bf16hi(sv.y),
+                          bf16lo(sv.z), bf16hi(sv.z), bf16lo(sv.w), bf16hi(sv.w)};
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[u][i] = bf16_round(acc[u][i] + f[i]);
     }
     if (residual) {
       const uint4 r = reinterpret_cast<const uint4*>(residual + (size_t)t * d)[c];
-      acc[0] += bf16lo(r.x); acc[1] += bf16hi(r.x); acc[2] += bf16lo(r.y); acc[3] += bf16hi(r.y);
-      acc[4] += bf16lo(r.z); acc[5] += bf16hi(r.z); acc[6] += bf16lo(r.w); acc[7] += bf16hi(r.w);
+      const float f[8] = {bf16lo(r.x), bf16hi(r.x), bf16lo(r.y), bf16hi(r.y),
+                          bf16lo(r.z), bf16hi(r.z), bf16lo(r.w), bf16hi(r.w)};
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[u][i] = bf16_round(acc[u][i] + f[i]);
     }
     uint4 o;
-    o.x = pack_bf16x2(acc[0], acc[1]); o.y = pack_bf16x2(acc[2], acc[3]);
-    o.z = pack_bf16x2(acc[4], acc[5]); o.w = pack_bf16x2(acc[6], acc[7]);
+    o.x = pack_bf16x2(acc[u][0], acc[u][1]); o.y = pack_bf16x2(acc[u][2], acc[u][3]);
+    o.z = pack_bf16x2(acc[u][4], acc[u][5]); o.w = pack_bf16x2(acc[u][6], acc[u][7]);
     reinterpret_cast<uint4*>(out + (size_t)t * d)[c] = o;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ss = fmaf(acc[u][i], acc[u][i], ss);
+  }
+  if (!norm_out) return;
+  // fused RMSNorm of the row just written (block reduction of the sum of squares)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  float tot = 0.f;
+#pragma unroll
+  for (int i = 0; i < kCombineThreads / 32; ++i) tot += s_red[i];
+  const float inv = 1.0f / sqrtf(tot / (float)d + eps);
+#pragma unroll
+  for (int u = 0; u < kCombineVec; ++u) {
+    const int c = threadIdx.x + u * kCombineThreads;
+    if (c >= nvec) continue;
+    const uint4 wv = reinterpret_cast<const uint4*>(norm_w)[c];
+    const float wf[8] = {bf16lo(wv.x), bf16hi(wv.x), bf16lo(wv.y), bf16hi(wv.y),
+                         bf16lo(wv.z), bf16hi(wv.z), bf16lo(wv.w), bf16hi(wv.w)};
+    float r[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r[i] = wf[i] * bf16_round(acc[u][i] * inv);
+    uint4 o;
+    o.x = pack_bf16x2(r[0], r[1]); o.y = pack_bf16x2(r[2], r[3]);
+    o.z = pack_bf16x2(r[4], r[5]); o.w = pack_bf16x2(r[6], r[7]);
+    reinterpret_cast<uint4*>(norm_out + (size_t)t * d)[c] = o;
   }
 }
 
@@ -310,7 +418,7 @@ int mgb_router_topk(const void* x, const void* w_gate, const float* logits_in, i
                     void* stream) {
   if (T < 1 || E < 1 || E > mgb::kMaxE || k < 1 || k > mgb::kMaxK || k > E || mode < 0 || mode > 2)
     return MGB_EINVAL;
-  if (!logits_in && (d % 8 || d < 8)) return MGB_EINVAL;
+  if (!logits_in && (d % 8 || d < 8 || d > 8 * 32 * 24)) return MGB_EINVAL;  // d <= 6144
   if (mode == 2 && (n_group < 1 || n_group > 32 || E % n_group || topk_group < 1 || topk_group > n_group ||
                     topk_group * (E / n_group) < k))
     return MGB_EINVAL;
@@ -345,15 +453,19 @@ int mgb_permute(const void* x, const int* topk_idx, const int* local_rank, const
 }
 
 // Weighted un-permute + combine (fp32, j ascending, one bf16 rounding), optional shared-expert
-// add and residual add (HF grouped_mm semantics, integrations/moe.py:417-429).
+// add and residual add (HF grouped_mm semantics, integrations/moe.py:417-429), optionally fused
+// with the following RMSNorm (norm_w != NULL: norm_out = RMSNorm(out) * norm_w).
 int mgb_unpermute_combine(const void* y_perm, const int* dst_pos, const float* topk_w, const void* shared_out,
-                          const void* residual, int T, int d, int k, void* out, void* stream) {
-  if (T < 1 || d % 8 || k < 1 || k > mgb::kMaxK) return MGB_EINVAL;
-  const int threads = (d / 8) >= 256 ? 256 : ((d / 8 + 31) / 32) * 32;
-  mgb::combine_kernel<<<T, threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+                          const void* residual, int T, int d, int k, void* out, const void* norm_w, float eps,
+                          void* norm_out, void* stream) {
+  if (T < 1 || d % 8 || d > 8 * mgb::kCombineThreads * mgb::kCombineVec || k < 1 || k > mgb::kMaxK ||
+      (norm_out && !norm_w))
+    return MGB_EINVAL;
+  mgb::combine_kernel<<<T, mgb::kCombineThreads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<const __nv_bfloat16*>(y_perm), dst_pos, topk_w,
       reinterpret_cast<const __nv_bfloat16*>(shared_out), reinterpret_cast<const __nv_bfloat16*>(residual), T, d,
-      k, reinterpret_cast<__nv_bfloat16*>(out));
+      k, reinterpret_cast<__nv_bfloat16*>(out), reinterpret_cast<const __nv_bfloat16*>(norm_w), eps,
+      reinterpret_cast<__nv_bfloat16*>(norm_out));
   return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
 }
 

@@ -116,8 +116,8 @@ class Engine:
         self.pps = math.ceil(self.max_ctx / self.page)
         n_pages = B * self.pps
         blk = a.n_kv_heads * a.head_dim * self.page
-        self.k_cache = [torch.empty(n_pages * blk, dtype=BF16, device=device) for _ in range(a.layers)]
-        self.v_cache = [torch.empty(n_pages * blk, dtype=BF16, device=device) for _ in range(a.layers)]
+        self.k_cache = [torch.zeros(n_pages * blk, dtype=BF16, device=device) for _ in range(a.layers)]
+        self.v_cache = [torch.zeros(n_pages * blk, dtype=BF16, device=device) for _ in range(a.layers)]
         self.block_table = torch.arange(n_pages, dtype=torch.int32, device=device).view(B, self.pps)
         # ---- RoPE tables (HF MixtralRotaryEmbedding, bf16-rounded, modeling_mixtral.py:210-220) ----
         hd = a.head_dim
@@ -140,6 +140,7 @@ class Engine:
         self.rws = ops.RouterWorkspace(B, a.n_experts, k, device=device)
         self.out_tokens = torch.zeros(B, max(1, self.max_ctx), dtype=torch.int64, device=device)
         self.graph: torch.cuda.CUDAGraph | None = None
+        self.debug_taps: dict | None = None
         self.stream = torch.cuda.Stream(device=device)
         self.kernel_launches_per_step = self._count_launches()
 
@@ -153,7 +154,8 @@ class Engine:
         for j in self.layer_jobs[l]:
             if j.kind == "pre_attention":
                 s0, s1 = self._mb_range(j)
-                ops.add_rmsnorm(b.x[s0:s1], W["ln1"], a.rms_eps, b.h[s0:s1])
+                if l == 0:  # later layers get h from the previous layer's fused combine+norm
+                    ops.add_rmsnorm(b.x[s0:s1], W["ln1"], a.rms_eps, b.h[s0:s1])
                 torch.mm(b.h[s0:s1], W["wqkv"].t(), out=b.qkv[s0:s1])
                 ops.rope_append_gqa(b.qkv[s0:s1], s0, b.positions, self.cos_t, self.sin_t, Hq, Hkv, hd,
                                     self.block_table, self.k_cache[l], self.v_cache[l], b.q[s0:s1], b.seq_lens)
@@ -168,13 +170,17 @@ class Engine:
                 ops.router_topk(b.h, W["router"], self.rws, a.top_k, a.router_mode, a.routed_scaling, a.n_group,
                                 a.topk_group)
                 ops.permute(b.h, self.rws, b.x_perm)
+                if self.debug_taps is not None:  # eager-only parity hook
+                    self.debug_taps.update(h2=b.h.clone(), topk_idx=self.rws.topk_idx.clone(), attn=b.attn.clone())
             elif j.kind == "expert_compute":
                 # all experts' b_e chunks of this layer execute inside one persistent grouped
                 # launch per GEMM (the kernel's token tiles are the chunks)
                 if not experts_done:
                     ops.moe_gemm_gate_up(W["w_gate_up"], b.x_perm, self.rws.offsets, b.h_ffn)
                     ops.moe_gemm_down(W["w_down"], b.h_ffn, self.rws.offsets, b.y_perm)
-                    ops.unpermute_combine(b.y_perm, self.rws, b.x, self.B, residual=b.x)
+                    nxt = self.w.layers[l + 1]["ln1"] if l + 1 < a.layers else self.w.final_norm
+                    ops.unpermute_combine(b.y_perm, self.rws, b.x, self.B, residual=b.x, norm_w=nxt, eps=a.rms_eps,
+                                          norm_out=b.h)
                     experts_done = True
             else:
                 raise RuntimeError(f"job kind {j.kind!r} is not executable under kv_policy={self.kv_policy!r}")
@@ -185,10 +191,11 @@ class Engine:
         return s0, s0 + j.seqs
 
     def _count_launches(self) -> int:
-        n = 2  # embed, and final norm
+        n = 1  # embed (the final norm is fused into the last combine)
         for l in range(self.arch.layers):
             for j in self.layer_jobs[l]:
-                n += {"pre_attention": 2, "attn_mech_gpu": 1, "post_attention": 1, "router": 2}.get(j.kind, 0)
+                n += {"pre_attention": 2 if l == 0 else 1, "attn_mech_gpu": 1, "post_attention": 1,
+                      "router": 2}.get(j.kind, 0)
             n += 3  # gate_up, down, combine
         return n + 2  # argmax, advance  (cuBLAS GEMMs are library launches, not counted)
 
@@ -198,7 +205,6 @@ class Engine:
         ops.embed(b.next_ids, self.w.embed, b.x)
         for l in range(a.layers):
             self._issue_layer(l)
-        ops.add_rmsnorm(b.x, self.w.final_norm, a.rms_eps, b.h)
         torch.mm(b.h, self.w.lm_head.t(), out=b.logits)
         ops.argmax(b.logits, b.next_ids)
         ops.decode_advance(b.next_ids, self.out_tokens if record else None, b.step, b.positions)

@@ -74,9 +74,11 @@ def moe_gemm_down(w_down: torch.Tensor, h: torch.Tensor, offsets: torch.Tensor, 
 
 
 def unpermute_combine(y_perm: torch.Tensor, ws: RouterWorkspace, out: torch.Tensor, T: int,
-                      residual: torch.Tensor | None = None, shared_out: torch.Tensor | None = None) -> None:
+                      residual: torch.Tensor | None = None, shared_out: torch.Tensor | None = None,
+                      norm_w: torch.Tensor | None = None, eps: float = 0.0,
+                      norm_out: torch.Tensor | None = None) -> None:
     nat.call("mgb_unpermute_combine", _p(y_perm), _p(ws.dst_pos), _p(ws.topk_w), _p(shared_out), _p(residual), T,
-             out.shape[1], ws.k, _p(out), _s())
+             out.shape[1], ws.k, _p(out), _p(norm_w), eps, _p(norm_out), _s())
 
 
 def add_rmsnorm(x: torch.Tensor, weight: torch.Tensor, eps: float, y: torch.Tensor,

@@ -156,14 +156,14 @@ def test_add_rmsnorm():
 
 
 def _paged_kv(kc, vc, B, Hkv, hd, ctx, page, pps):
-    """dense [B,Hkv,ctx,hd] -> engine page layout (K chunk-major, V row-major)."""
+    """dense [B,Hkv,ctx,hd] -> engine page layout (K and V chunk-major [hd/8][page][8])."""
     kp = torch.zeros(B * pps, Hkv, hd // 8, page, 8, dtype=BF16)
-    vp = torch.zeros(B * pps, Hkv, page, hd, dtype=BF16)
+    vp = torch.zeros(B * pps, Hkv, hd // 8, page, 8, dtype=BF16)
     for b in range(B):
         for t in range(ctx):
             pg, s = b * pps + t // page, t % page
             kp[pg, :, :, s, :] = kc[b, :, t, :].view(Hkv, hd // 8, 8)
-            vp[pg, :, s, :] = vc[b, :, t, :]
+            vp[pg, :, :, s, :] = vc[b, :, t, :].view(Hkv, hd // 8, 8)
     return kp.reshape(-1), vp.reshape(-1)
 
 
@@ -211,11 +211,11 @@ def test_rope_append_matches_oracle():
     assert torch.equal(qo.cpu().view(B, Hq, hd), R.apply_rope(q, cos, sin))
     kref = R.apply_rope(k, cos, sin)
     kp = kc.cpu().view(B * pps, Hkv, hd // 8, page, 8)
-    vp = vc.cpu().view(B * pps, Hkv, page, hd)
+    vp = vc.cpu().view(B * pps, Hkv, hd // 8, page, 8)
     for b in range(B):
         pg, s = b * pps + pos // page, pos % page
         assert torch.equal(kp[pg, :, :, s, :].reshape(Hkv, hd), kref[b])
-        assert torch.equal(vp[pg, :, s, :], v[b])
+        assert torch.equal(vp[pg, :, :, s, :].reshape(Hkv, hd), v[b])
     assert torch.equal(lens.cpu(), torch.full((B,), pos + 1, dtype=torch.int32))
 
 
