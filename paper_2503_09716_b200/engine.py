@@ -109,8 +109,15 @@ class Engine:
         for j in self.schedule.jobs:
             if j.resource is not None and j.layer >= 0:
                 self.layer_jobs[j.layer].append(j)
+        self.offload = self.plan.s_params < self.spec.model_bytes
+        self._plan_streams()
         # ---- weights ----
-        self.w = MixtralDeviceWeights(a, seed=seed, device=device)
+        if self.offload:
+            from .offload import OffloadedMixtralWeights
+            self.w = OffloadedMixtralWeights(a, self.spec, self.plan.s_params, self.plan.s_expert, seed=seed,
+                                             device=device)
+        else:
+            self.w = MixtralDeviceWeights(a, seed=seed, device=device)
         # ---- paged KV cache (identity block table: sequence b owns pages [b*pps, (b+1)*pps)) ----
         self.page = ops.kv_page_size()
         self.pps = math.ceil(self.max_ctx / self.page)
@@ -142,17 +149,103 @@ class Engine:
         self.graph: torch.cuda.CUDAGraph | None = None
         self.debug_taps: dict | None = None
         self.stream = torch.cuda.Stream(device=device)
+        self.h2d = torch.cuda.Stream(device=device) if self.offload else None
+        self._fork, self._join = torch.cuda.Event(), torch.cuda.Event()
+        self.events = {i: torch.cuda.Event() for i in self.need_event}
+        self.trace_events: dict | None = None  # job id -> (start, end) timing events (eager trace mode)
         self.kernel_launches_per_step = self._count_launches()
 
     # ------------------------------------------------------------------------------------
     # job issue
     # ------------------------------------------------------------------------------------
+    def _plan_streams(self) -> None:
+        """Cross-resource edges of the serialized schedule become cudaEvent waits; same-resource
+        chains are plain in-order stream semantics.  Barriers are expanded into their producers."""
+        jobs = self.schedule.jobs
+        preds = self.schedule.preds()
+        eff: dict[int, list[int]] = {}
+
+        def producers(i: int) -> list[int]:
+            if jobs[i].resource is not None:
+                return [i]
+            if i not in eff:
+                out: list[int] = []
+                for p in preds[i]:
+                    out += producers(p)
+                eff[i] = sorted(set(out))
+            return eff[i]
+
+        self.xwait: dict[int, list[int]] = {}
+        self.need_event: set[int] = set()
+        for j in jobs:
+            if j.resource is None:
+                continue
+            w = []
+            for p in preds[j.id]:
+                for q in producers(p):
+                    if jobs[q].resource != j.resource:
+                        w.append(q)
+            self.xwait[j.id] = sorted(set(w))
+            self.need_event.update(w)
+        # expert slot of every uncached expert copy: copy k reuses slot k % slots
+        # (the schedule's recycle edge, offload_dag.py:446-448)
+        self.slot_of: dict[tuple[int, int], int] = {}
+        slots = max(1, self.plan.s_expert // self.spec.expert_bytes) if self.spec.expert_bytes else 1
+        k = 0
+        for j in jobs:
+            if j.kind == "weight_copy" and "/expert" in j.label:
+                e = int(j.label.split("/expert")[1].split("_")[0])
+                self.slot_of[(j.layer, e)] = k % slots
+                k += 1
+        # first / last expert_compute job of each layer (resident group launch / combine)
+        self.first_expert_job, self.last_expert_job = {}, {}
+        for j in jobs:
+            if j.kind == "expert_compute":
+                self.first_expert_job.setdefault(j.layer, j.id)
+                self.last_expert_job[j.layer] = j.id
+        if self.plan.B * self.arch.top_k < self.arch.n_experts:
+            raise ValueError("B * top_k < experts: some experts would have no scheduled expert_compute job")
+
+    def _stream_of(self, j) -> torch.cuda.Stream:
+        return self.h2d if j.resource == "htod_link" else self.stream
+
     def _issue_layer(self, l: int) -> None:
-        a, b, W = self.arch, self.buf, self.w.layers[l]
-        hd, Hq, Hkv = a.head_dim, a.n_heads, a.n_kv_heads
-        experts_done = False
         for j in self.layer_jobs[l]:
-            if j.kind == "pre_attention":
+            st = self._stream_of(j)
+            for p in self.xwait.get(j.id, ()):
+                st.wait_event(self.events[p])
+            with torch.cuda.stream(st):
+                te = self.trace_events
+                if te is not None:
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(st)
+                self._issue_job(l, j)
+                if te is not None:
+                    e1.record(st)
+                    te[j.id] = (e0, e1)
+                if j.id in self.need_event:
+                    self.events[j.id].record(st)
+
+    def _layer_weights(self, l: int) -> dict:
+        W = self.w.layers[l]
+        if self.offload and l >= self.w.place.dense_layers:
+            wqkv, wo = self.w.dense_views()
+            W = dict(W, wqkv=wqkv, wo=wo)
+        return W
+
+    def _issue_job(self, l: int, j) -> None:
+        a, b = self.arch, self.buf
+        W = self._layer_weights(l)
+        hd, Hq, Hkv = a.head_dim, a.n_heads, a.n_kv_heads
+        if True:
+            if j.kind == "weight_copy":
+                if j.label.endswith("dense_copy"):
+                    self.w.dense_buf.copy_(self.w.host_dense[l], non_blocking=True)
+                else:
+                    e = int(j.label.split("/expert")[1].split("_")[0])
+                    n_c = self.w.place.experts_per_layer[l]
+                    self.w.slots[self.slot_of[(l, e)]].copy_(self.w.host_experts[l][e - n_c], non_blocking=True)
+            elif j.kind == "pre_attention":
                 s0, s1 = self._mb_range(j)
                 if l == 0:  # later layers get h from the previous layer's fused combine+norm
                     ops.add_rmsnorm(b.x[s0:s1], W["ln1"], a.rms_eps, b.h[s0:s1])
@@ -173,15 +266,24 @@ class Engine:
                 if self.debug_taps is not None:  # eager-only parity hook
                     self.debug_taps.update(h2=b.h.clone(), topk_idx=self.rws.topk_idx.clone(), attn=b.attn.clone())
             elif j.kind == "expert_compute":
-                # all experts' b_e chunks of this layer execute inside one persistent grouped
-                # launch per GEMM (the kernel's token tiles are the chunks)
-                if not experts_done:
+                # b_e chunks of one expert run inside one persistent grouped launch (the kernel's
+                # token tiles are the chunks); all HBM-resident experts of the layer share one
+                # launch, each streamed expert runs from its slot once its copy has landed
+                e = int(j.label.split("/expert")[1].split("/")[0])
+                first_chunk = j.label.endswith("/chunk0")
+                n_c = self.w.place.experts_per_layer[l] if self.offload else a.n_experts
+                if j.id == self.first_expert_job[l] and n_c > 0:
                     ops.moe_gemm_gate_up(W["w_gate_up"], b.x_perm, self.rws.offsets, b.h_ffn)
                     ops.moe_gemm_down(W["w_down"], b.h_ffn, self.rws.offsets, b.y_perm)
+                elif first_chunk and e >= n_c:
+                    gu, dn = self.w.slot_views(self.slot_of[(l, e)])
+                    offs = self.rws.offsets[e:e + 2]
+                    ops.moe_gemm_gate_up(gu, b.x_perm, offs, b.h_ffn)
+                    ops.moe_gemm_down(dn, b.h_ffn, offs, b.y_perm)
+                if j.id == self.last_expert_job[l]:
                     nxt = self.w.layers[l + 1]["ln1"] if l + 1 < a.layers else self.w.final_norm
                     ops.unpermute_combine(b.y_perm, self.rws, b.x, self.B, residual=b.x, norm_w=nxt, eps=a.rms_eps,
                                           norm_out=b.h)
-                    experts_done = True
             else:
                 raise RuntimeError(f"job kind {j.kind!r} is not executable under kv_policy={self.kv_policy!r}")
 
@@ -202,9 +304,15 @@ class Engine:
     def _step(self, record: bool = True) -> None:
         """One decode forward of all B sequences (one token each)."""
         a, b = self.arch, self.buf
+        if self.offload:  # fork the H2D copy stream off the compute stream
+            self._fork.record(self.stream)
+            self.h2d.wait_event(self._fork)
         ops.embed(b.next_ids, self.w.embed, b.x)
         for l in range(a.layers):
             self._issue_layer(l)
+        if self.offload:  # join: the step ends when every copy has landed
+            self._join.record(self.h2d)
+            self.stream.wait_event(self._join)
         torch.mm(b.h, self.w.lm_head.t(), out=b.logits)
         ops.argmax(b.logits, b.next_ids)
         ops.decode_advance(b.next_ids, self.out_tokens if record else None, b.step, b.positions)
@@ -297,6 +405,47 @@ class Engine:
         torch.cuda.current_stream().wait_stream(self.stream)
         torch.cuda.synchronize()
         return dict(logits=self.buf.logits.clone(), next_ids=self.buf.next_ids.clone())
+
+    def trace_step(self) -> tuple[list[dict], dict]:
+        """One eager decode step with timing events around every job on its own stream.
+        Returns (records, report): records use the reference simulator's JSONL trace schema
+        {time, node, kind, resource, action} (exec_sim.py:113-136) with measured times, and the
+        report carries SimReport-style busy / idle / bytes / makespan (exec_sim.py:84-110) plus the
+        transfer/compute overlap 1 - (makespan - max(busy)) / min(busy)."""
+        self.trace_events = {}
+        t0 = torch.cuda.Event(enable_timing=True)
+        saved = [t.clone() for t in (self.buf.positions, self.buf.step, self.buf.next_ids, self.buf.seq_lens)]
+        with torch.cuda.stream(self.stream):
+            torch.cuda._sleep(int(5e7))  # host enqueues the whole step before the GPU starts
+            t0.record(self.stream)
+            self._step(record=False)
+            t1 = torch.cuda.Event(enable_timing=True)
+            t1.record(self.stream)
+        torch.cuda.synchronize()
+        for t, s in zip((self.buf.positions, self.buf.step, self.buf.next_ids, self.buf.seq_lens), saved):
+            t.copy_(s)
+        jobs = self.schedule.jobs
+        recs, busy = [], {}
+        nbytes = {"htod_link": 0.0, "dtoh_link": 0.0}
+        for jid, (e0, e1) in self.trace_events.items():
+            j = jobs[jid]
+            s, e = t0.elapsed_time(e0) * 1e-3, t0.elapsed_time(e1) * 1e-3
+            recs.append({"time": s, "node": jid, "kind": j.kind, "resource": j.resource, "action": "start"})
+            recs.append({"time": e, "node": jid, "kind": j.kind, "resource": j.resource, "action": "finish"})
+            busy[j.resource] = busy.get(j.resource, 0.0) + (e - s)
+            if j.resource in nbytes:
+                nbytes[j.resource] += j.nbytes
+        self.trace_events = None
+        recs.sort(key=lambda r: (r["time"], r["node"], r["action"] != "start"))
+        makespan = t0.elapsed_time(t1) * 1e-3
+        g, h = busy.get("gpu_compute", 0.0), busy.get("htod_link", 0.0)
+        overlap = 1.0 - (makespan - max(g, h)) / min(g, h) if min(g, h) > 0 else None
+        report = {"makespan": makespan, "busy": busy,
+                  "idle_fraction": {r: 1.0 - v / makespan for r, v in busy.items()},
+                  "bytes_htod": nbytes["htod_link"], "bytes_dtoh": nbytes["dtoh_link"],
+                  "htod_gbs": nbytes["htod_link"] / h / 1e9 if h > 0 else None,
+                  "throughput": self.B / makespan, "overlap": overlap}
+        return recs, report
 
     def job_trace(self) -> list[dict]:
         """The issued job list (kinds/labels/shapes), in submission order."""

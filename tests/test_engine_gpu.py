@@ -156,3 +156,32 @@ def test_per_layer_hidden_states(oracle_weights):
             ops.add_rmsnorm(b.x, nxt, TINY.rms_eps, b.h)
     # end-to-end (not re-synchronised) routing may flip on bf16 near-ties
     assert route_equal >= 0.9 * total
+
+
+def test_offloaded_weights_match_resident_bit_exact():
+    """Module-based batching with weights partly in pinned host memory (prefetch subsystem):
+    uncached dense layers / experts (reference cache_placement) are streamed on the H2D copy
+    stream into the dense buffer / expert slots; outputs must equal the fully resident engine bit
+    for bit, eagerly and under CUDA-graph replay, and the trace's H2D bytes = uncached bytes."""
+    from paper_2503_09716_b200.configs import TINY
+    from paper_2503_09716_b200.engine import Engine
+    from paper_2503_09716_b200.planner import BatchingPlan, ModelSpec, placement
+
+    spec = ModelSpec.from_document(TINY.model_spec_document())
+    dense, ex = spec.dense_bytes_per_layer, spec.expert_bytes
+    B, P, N = 8, 4, 5
+    res_plan = BatchingPlan(B, 4, 16, 0.0, 0, spec.model_bytes)
+    ids = torch.randint(0, TINY.vocab, (B, P), generator=torch.Generator().manual_seed(11))
+    ref = Engine(TINY, res_plan, prompt_len=P, decode_len=N, use_graph=False).generate(ids, N)
+    for s_params, slots in ((2 * dense + dense // 2, 2), (4 * dense + 10 * ex, 3)):
+        off_plan = BatchingPlan(B, 4, 16, 0.0, slots * ex, s_params)
+        pl = placement(spec, s_params)  # reference cache_placement (memory_model.py:147-164)
+        assert pl.uncached_expert_count > 0
+        for graph in (False, True):
+            eng = Engine(TINY, off_plan, prompt_len=P, decode_len=N, use_graph=graph)
+            assert eng.offload and eng.w.n_slots == slots
+            assert torch.equal(eng.generate(ids, N), ref)
+        recs, rep = eng.trace_step()
+        uncached = (TINY.layers - pl.dense_layers) * dense + pl.uncached_expert_count * ex
+        assert rep["bytes_htod"] == uncached
+        assert {r["kind"] for r in recs} >= {"weight_copy", "expert_compute", "router"}
