@@ -296,3 +296,150 @@ def softmax_margin(logits: torch.Tensor) -> torch.Tensor:
 
 
 __all__ = [n for n in dir() if not n.startswith("_")] + ["math"]
+
+
+# ------------------------------------------------------------------------------------------
+# DeepSeek-V2 family (MLA attention, shared experts, dense first layers)
+# HF transformers 5.5.0 modeling_deepseek_v2.py: DeepseekV2Attention.forward :337-396,
+# apply_rotary_emb :305-318, DeepseekV2Moe :85-131, DeepseekV2MLP :134-146, decoder layer :399-430
+# ------------------------------------------------------------------------------------------
+DS_SLOT = dict(ln1=0, ln2=5, router=6, w_gate_up=7, w_down=8, q_proj=10, q_a_norm=11, q_b=12, kv_a=13,
+               kv_a_norm=14, kv_b=15, wo=16, sh_gate_up=17, sh_down=18, dense_gate_up=19, dense_down=20)
+
+
+def ds_tid(layer: int, name: str) -> int:
+    return LAYER_BASE + LAYER_STRIDE * layer + DS_SLOT[name]
+
+
+def make_dsv2_weights(arch, seed: int = 0) -> MixtralWeights:
+    a = arch
+    d, H = a.hidden, a.n_heads
+    qk = a.qk_nope_dim + a.qk_rope_dim
+    std = a.init_std
+    U = lambda shape, t: uniform_bf16(shape, seed, t, std)  # noqa: E731
+    ones = lambda n: torch.ones(n, dtype=BF16)  # noqa: E731
+    layers = []
+    for l in range(a.layers):
+        L = dict(ln1=ones(d), ln2=ones(d),
+                 kv_a=U((a.kv_lora_rank + a.qk_rope_dim, d), ds_tid(l, "kv_a")), kv_a_norm=ones(a.kv_lora_rank),
+                 kv_b=U((H * (a.qk_nope_dim + a.v_head_dim), a.kv_lora_rank), ds_tid(l, "kv_b")),
+                 wo=U((d, H * a.v_head_dim), ds_tid(l, "wo")))
+        if a.q_lora_rank:
+            L.update(q_a=U((a.q_lora_rank, d), ds_tid(l, "q_proj")), q_a_norm=ones(a.q_lora_rank),
+                     q_b=U((H * qk, a.q_lora_rank), ds_tid(l, "q_b")))
+        else:
+            L.update(q_proj=U((H * qk, d), ds_tid(l, "q_proj")))
+        if l < a.first_k_dense:
+            L.update(dense_gate_up=U((2 * a.dense_ffn, d), ds_tid(l, "dense_gate_up")),
+                     dense_down=U((d, a.dense_ffn), ds_tid(l, "dense_down")))
+        else:
+            fs = a.moe_ffn * a.n_shared
+            L.update(router=U((a.n_experts, d), ds_tid(l, "router")),
+                     w_gate_up=U((a.n_experts, 2 * a.moe_ffn, d), ds_tid(l, "w_gate_up")),
+                     w_down=U((a.n_experts, d, a.moe_ffn), ds_tid(l, "w_down")),
+                     sh_gate_up=U((2 * fs, d), ds_tid(l, "sh_gate_up")), sh_down=U((d, fs), ds_tid(l, "sh_down")))
+        layers.append(L)
+    return MixtralWeights(embed=U((a.vocab, d), TID_EMBED), final_norm=ones(d), lm_head=U((a.vocab, d), TID_LM_HEAD),
+                          layers=layers)
+
+
+def rope_interleaved(x: torch.Tensor, pos: torch.Tensor, theta: float) -> torch.Tensor:
+    """apply_rotary_emb (modeling_deepseek_v2.py:305-318): complex rotation of (2i, 2i+1) pairs in
+    fp32, one cast back.  x [T, H, r], pos [T]."""
+    r = x.shape[-1]
+    inv_freq = 1.0 / (theta ** (torch.arange(0, r, 2, dtype=torch.int64).float() / r))
+    freqs = pos.float()[:, None] * inv_freq[None, :]
+    cis = torch.polar(torch.ones_like(freqs), freqs)  # [T, r/2]
+    xc = torch.view_as_complex(x.float().reshape(*x.shape[:-1], -1, 2))
+    return torch.view_as_real(xc * cis[:, None, :]).flatten(-2).type_as(x)
+
+
+def mla_absorbed_attention(q_lat: torch.Tensor, q_pe: torch.Tensor, c_cache: torch.Tensor, pe_cache: torch.Tensor,
+                           scale: float) -> torch.Tensor:
+    """Absorbed MLA decode attention in fp32 (what mgb_decode_attn_mla computes):
+    q_lat [B,H,R], q_pe [B,H,r]; c_cache [B,ctx,R], pe_cache [B,ctx,r] -> o_lat [B,H,R] (bf16)."""
+    s = (torch.einsum("bhr,btr->bht", q_lat.float(), c_cache.float())
+         + torch.einsum("bhr,btr->bht", q_pe.float(), pe_cache.float())) * scale
+    p = torch.softmax(s, dim=-1)
+    return torch.einsum("bht,btr->bhr", p, c_cache.float()).to(q_lat.dtype)
+
+
+class DeepseekV2Oracle:
+    """Token-by-token greedy decoding (HF DeepseekV2 semantics, non-absorbed attention with
+    per-head K/V caches, sdpa-style fp32 attention)."""
+
+    def __init__(self, arch, weights: MixtralWeights):
+        self.a, self.w = arch, weights
+        self.kc = [None] * arch.layers
+        self.vc = [None] * arch.layers
+
+    def attention(self, l: int, h: torch.Tensor, pos: int, trace: dict | None = None) -> torch.Tensor:
+        a, W = self.a, self.w.layers[l]
+        B, H = h.shape[0], a.n_heads
+        nope, rope, vd = a.qk_nope_dim, a.qk_rope_dim, a.v_head_dim
+        if a.q_lora_rank:
+            q = F.linear(rmsnorm(F.linear(h, W["q_a"]), W["q_a_norm"], a.rms_eps), W["q_b"])
+        else:
+            q = F.linear(h, W["q_proj"])
+        q = q.view(B, H, nope + rope)
+        q_nope, q_pe = q[..., :nope], q[..., nope:]
+        ckv = F.linear(h, W["kv_a"])
+        c, k_pe = ckv[:, :a.kv_lora_rank], ckv[:, a.kv_lora_rank:]
+        c = rmsnorm(c, W["kv_a_norm"], a.rms_eps)
+        kvb = F.linear(c, W["kv_b"]).view(B, H, nope + vd)
+        k_nope, v = kvb[..., :nope], kvb[..., nope:]
+        posv = torch.full((B,), pos)
+        q_pe = rope_interleaved(q_pe, posv, a.rope_theta)
+        k_pe = rope_interleaved(k_pe.view(B, 1, rope), posv, a.rope_theta)
+        key = torch.cat([k_nope, k_pe.expand(B, H, rope)], dim=-1)
+        query = torch.cat([q_nope, q_pe], dim=-1)
+        if self.kc[l] is None:
+            self.kc[l], self.vc[l] = key[:, :, None], v[:, :, None]
+        else:
+            self.kc[l] = torch.cat([self.kc[l], key[:, :, None]], 2)
+            self.vc[l] = torch.cat([self.vc[l], v[:, :, None]], 2)
+        scale = (nope + rope) ** -0.5
+        s = torch.matmul(query[:, :, None, :].float(), self.kc[l].float().transpose(2, 3)) * scale
+        p = torch.softmax(s, dim=-1)
+        o = torch.matmul(p, self.vc[l].float()).reshape(B, H * vd).to(h.dtype)
+        if trace is not None:
+            trace.update(c=c, k_pe=k_pe.view(B, rope), q_nope=q_nope, q_pe=q_pe, attn=o)
+        return F.linear(o, W["wo"])
+
+    def layer_forward(self, l: int, x: torch.Tensor, pos: int, trace: dict | None = None) -> torch.Tensor:
+        a, W = self.a, self.w.layers[l]
+        h = rmsnorm(x, W["ln1"], a.rms_eps)
+        x = x + self.attention(l, h, pos, trace)
+        h2 = rmsnorm(x, W["ln2"], a.rms_eps)
+        if l < a.first_k_dense:
+            y = expert_ffn(h2, W["dense_gate_up"], W["dense_down"])
+        else:
+            routed = moe_block(h2, W["router"], W["w_gate_up"], W["w_down"], a.top_k, a.router_mode, a.routed_scaling,
+                               a.n_group, a.topk_group, fp32_router=True, trace=trace)
+            y = routed + expert_ffn(h2, W["sh_gate_up"], W["sh_down"])
+        if trace is not None:
+            trace.update(h2=h2)
+        return x + y
+
+    def step(self, tokens: torch.Tensor, pos: int, traces: list | None = None) -> torch.Tensor:
+        x = self.w.embed[tokens]
+        for l in range(self.a.layers):
+            tr = {} if traces is not None else None
+            x = self.layer_forward(l, x, pos, tr)
+            if traces is not None:
+                tr["x_out"] = x
+                traces.append(tr)
+        return F.linear(rmsnorm(x, self.w.final_norm, self.a.rms_eps), self.w.lm_head)
+
+    def generate(self, input_ids: torch.Tensor, max_new_tokens: int):
+        B, P = input_ids.shape
+        ids = input_ids.clone()
+        cur = None
+        for p in range(P):
+            cur = self.step(ids[:, p], p)
+        for n in range(max_new_tokens):
+            nxt = torch.argmax(cur.float(), dim=-1)
+            ids = torch.cat([ids, nxt[:, None]], dim=1)
+            if n + 1 < max_new_tokens:
+                cur = self.step(nxt, P + n)
+        return ids

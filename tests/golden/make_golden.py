@@ -207,7 +207,68 @@ def hf_tiny():
     return gen
 
 
+def hf_tiny_dsv2():
+    """HF DeepseekV2ForCausalLM (MLA, group-limited routing, shared experts, dense layer 0) on the
+    counter-based weights of configs.TINY_DSV2 (default rope: the YaRN scaling of the released
+    checkpoints is a checkpoint property, not part of the path)."""
+    from transformers import DeepseekV2Config, DeepseekV2ForCausalLM
+
+    from oracle import moe_ref as R
+    from paper_2503_09716_b200.configs import TINY_DSV2
+
+    a = TINY_DSV2
+    cfg = DeepseekV2Config(vocab_size=a.vocab, hidden_size=a.hidden, intermediate_size=a.dense_ffn,
+                           moe_intermediate_size=a.moe_ffn, num_hidden_layers=a.layers, num_attention_heads=a.n_heads,
+                           num_key_value_heads=a.n_heads, n_shared_experts=a.n_shared, n_routed_experts=a.n_experts,
+                           routed_scaling_factor=a.routed_scaling, kv_lora_rank=a.kv_lora_rank, q_lora_rank=None,
+                           qk_rope_head_dim=a.qk_rope_dim, v_head_dim=a.v_head_dim, qk_nope_head_dim=a.qk_nope_dim,
+                           topk_method=a.topk_method, n_group=a.n_group, topk_group=a.topk_group,
+                           num_experts_per_tok=a.top_k, first_k_dense_replace=a.first_k_dense, rms_norm_eps=a.rms_eps,
+                           max_position_embeddings=4096, tie_word_embeddings=False,
+                           rope_parameters={"rope_type": "default", "rope_theta": a.rope_theta})
+    cfg._attn_implementation = "sdpa"
+    model = DeepseekV2ForCausalLM._from_config(cfg, dtype=torch.bfloat16, experts_implementation="grouped_mm").eval()
+    W = R.make_dsv2_weights(a, seed=0)
+    sd = {"model.embed_tokens.weight": W.embed, "model.norm.weight": W.final_norm, "lm_head.weight": W.lm_head}
+    for l, L in enumerate(W.layers):
+        p = f"model.layers.{l}."
+        sd.update({p + "input_layernorm.weight": L["ln1"], p + "post_attention_layernorm.weight": L["ln2"],
+                   p + "self_attn.q_proj.weight": L["q_proj"], p + "self_attn.kv_a_proj_with_mqa.weight": L["kv_a"],
+                   p + "self_attn.kv_a_layernorm.weight": L["kv_a_norm"], p + "self_attn.kv_b_proj.weight": L["kv_b"],
+                   p + "self_attn.o_proj.weight": L["wo"]})
+        if l < a.first_k_dense:
+            f = a.dense_ffn
+            sd.update({p + "mlp.gate_proj.weight": L["dense_gate_up"][:f], p + "mlp.up_proj.weight": L["dense_gate_up"][f:],
+                       p + "mlp.down_proj.weight": L["dense_down"]})
+        else:
+            fs = a.moe_ffn * a.n_shared
+            sd.update({p + "mlp.gate.weight": L["router"], p + "mlp.experts.gate_up_proj": L["w_gate_up"],
+                       p + "mlp.experts.down_proj": L["w_down"],
+                       p + "mlp.shared_experts.gate_proj.weight": L["sh_gate_up"][:fs],
+                       p + "mlp.shared_experts.up_proj.weight": L["sh_gate_up"][fs:],
+                       p + "mlp.shared_experts.down_proj.weight": L["sh_down"]})
+    missing, unexpected = model.load_state_dict(sd, strict=False)
+    assert not unexpected, unexpected
+    assert all("rotary" in m for m in missing), missing
+    # HF 5.5.0 DeepseekV2Moe.route_tokens_to_experts reads self.num_experts for
+    # group_limited_greedy (modeling_deepseek_v2.py:112) but never sets it: supply the attribute.
+    for layer in model.model.layers:
+        if hasattr(layer.mlp, "experts"):
+            layer.mlp.num_experts = a.n_experts
+    B, P, N = 4, 6, 6
+    ids = torch.randint(0, a.vocab, (B, P), generator=torch.Generator().manual_seed(2))
+    with torch.no_grad():
+        out = model(ids, output_hidden_states=True, use_cache=False)
+        gen = model.generate(ids, max_new_tokens=N, min_new_tokens=N, do_sample=False, pad_token_id=0)
+    doc = {"input_ids": ids, "hidden_states": [h[:, -1, :].clone() for h in out.hidden_states],
+           "last_logits": out.logits[:, -1, :].clone(), "generated": gen,
+           "meta": {"transformers": __import__("transformers").__version__, "attn": "sdpa", "B": B, "P": P, "N": N}}
+    torch.save(doc, os.path.join(HERE, "hf_tiny_dsv2.pt"))
+    return gen
+
+
 if __name__ == "__main__":
     print("schedules", schedules())
     print("memory rows", memory_model())
     print("hf generate", hf_tiny().tolist())
+    print("hf dsv2 generate", hf_tiny_dsv2().tolist())

@@ -140,3 +140,22 @@ def test_group_limited_routing_respects_groups():
         assert set(groups[t].tolist()) <= set(best3[t].tolist())
     probs = torch.softmax(lg, -1)
     torch.testing.assert_close(w, torch.gather(probs, 1, idx) * 16.0)
+
+
+def test_dsv2_oracle_matches_hf():
+    """DeepSeek-V2 family (MLA, fp32 group-limited router, shared experts, dense layer 0): the
+    oracle vs HF DeepseekV2ForCausalLM on the same counter-based weights."""
+    from paper_2503_09716_b200.configs import TINY_DSV2 as A
+
+    G = torch.load(os.path.join(os.path.dirname(__file__), "golden", "hf_tiny_dsv2.pt"), weights_only=False)
+    w = R.make_dsv2_weights(A, seed=0)
+    orc = R.DeepseekV2Oracle(A, w)
+    ids = G["input_ids"]
+    for p in range(ids.shape[1]):
+        tr = []
+        lg = orc.step(ids[:, p], p, traces=tr)
+    for l in range(A.layers - 1):
+        assert R.rel_err(tr[l]["x_out"], G["hidden_states"][l + 1]) <= 2e-2
+    assert R.rel_err(lg, G["last_logits"]) <= 2e-2
+    gen = R.DeepseekV2Oracle(A, w).generate(ids, G["meta"]["N"])
+    assert (gen == G["generated"]).all(1).float().mean() >= 0.75
