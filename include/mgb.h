@@ -68,6 +68,17 @@ int mgb_decode_attn_gqa(const void* q, const void* k_cache, const void* v_cache,
                         int max_pages, const int* seq_lens, int B, int Hq, int Hkv, int head_dim, float scale,
                         void* out, void* stream);
 
+/* ---- ATTN_MECH_GPU for MLA models (DeepSeek-V2; model_catalog.py:242-295 prices it) -------
+ * Absorbed latent attention: q_lat [H,B,R], q_pe [B,H,RP], latent pages of mgb_mla_page_size()
+ * tokens, chunk-major [(R+RP)/8][page][8] -> o_lat [H,B,R].  mgb_mla_append writes the new
+ * token's normed latent + RoPE'd k_pe, RoPE's q_pe and re-lays q_nope as [H,B,NOPE]. */
+int mgb_mla_page_size(void);
+int mgb_decode_attn_mla(const void* q_lat, const void* q_pe, const void* cache, const int* block_table, int max_pages,
+                        const int* seq_lens, int B, int H, int R, int RP, float scale, void* o_lat, void* stream);
+int mgb_mla_append(const void* q, const void* ckv, const void* norm_w, float eps, int B, int H, int R, int RP, int NOPE,
+                   const int* positions, const float* cos_t, const float* sin_t, const int* block_table, int max_pages,
+                   void* cache, void* q_nope_out, void* q_pe_out, int* seq_lens, void* stream);
+
 /* ---- PRE_ATTENTION / POST_ATTENTION helpers (offload_dag.py:359-416) --------------------- */
 int mgb_add_rmsnorm(const void* x, const void* delta, const void* weight, float eps, int T, int d, void* x_out,
                     void* y, void* stream);

@@ -42,10 +42,14 @@ SIGNATURES: dict[str, list] = {
     "mgb_argmax": [P, I, I, P, P],
     "mgb_decode_advance": [P, I, P, I, P, P, P],
     "mgb_fill_uniform_bf16": [P, L, ctypes.c_uint64, ctypes.c_uint64, F, F, I, P],
+    # attn_mla.cu
+    "mgb_mla_page_size": [],
+    "mgb_decode_attn_mla": [P, P, P, P, I, P, I, I, I, I, F, P, P],
+    "mgb_mla_append": [P, P, P, F, I, I, I, I, I, P, P, P, P, I, P, P, P, P, P],
 }
 
 # entry points that return a value rather than a status
-VALUE_FNS = {"mgb_abi_version", "mgb_num_sms", "mgb_kv_page_size", "mgb_router_num_blocks",
+VALUE_FNS = {"mgb_abi_version", "mgb_num_sms", "mgb_kv_page_size", "mgb_mla_page_size", "mgb_router_num_blocks",
              "mgb_router_tokens_per_block"}
 
 STATUS = {0: "ok", -1: "invalid argument", -2: "capacity exceeded", -3: "CUDA error"}
@@ -58,6 +62,7 @@ class NativeError(RuntimeError):
 class _Lib:
     def __init__(self) -> None:
         self._lib = None
+        self.calls = 0  # libmgb entry-point calls (each launches exactly one kernel)
 
     def load(self) -> ctypes.CDLL:
         if self._lib is not None:
@@ -83,6 +88,7 @@ class _Lib:
 
     def call(self, name: str, *args) -> None:
         lib = self.load()
+        self.calls += 1
         rc = getattr(lib, name)(*args)
         if rc != 0:
             err = lib.mgb_last_error().decode()

@@ -25,11 +25,12 @@ from dataclasses import dataclass
 
 import torch
 
+from . import _native as nat
 from . import ops
 from .configs import ModelArch, get_arch
 from .planner import BatchingPlan, Hardware, ModelSpec, WorkloadSpec, largest_batch, load_plan
 from .schedule import Schedule, build_schedule
-from .weights import MixtralDeviceWeights
+from .weights import DeepseekDeviceWeights, MixtralDeviceWeights
 
 BF16 = torch.bfloat16
 
@@ -88,11 +89,12 @@ class Engine:
         if not torch.cuda.is_available():
             raise RuntimeError("the B200 engine needs a CUDA device (there is no CPU fallback)")
         self.arch = get_arch(arch) if isinstance(arch, str) else arch
-        if self.arch.family != "mixtral":
-            raise NotImplementedError("this engine build runs the Mixtral family (GQA)")
+        if self.arch.family not in ("mixtral", "deepseek_v2"):
+            raise NotImplementedError(f"unknown model family {self.arch.family!r}")
         if kv_policy != "resident":
-            raise NotImplementedError("kv_policy='offload' is planned; this build keeps KV in HBM")
+            raise NotImplementedError("kv_policy='offload' (KV streamed from host) is not built yet; KV is paged in HBM")
         a = self.arch
+        self.mla = a.family == "deepseek_v2"
         self.kv_policy = kv_policy
         self.prompt_len, self.decode_len = prompt_len, decode_len
         self.max_ctx = prompt_len + decode_len
@@ -110,37 +112,74 @@ class Engine:
             if j.resource is not None and j.layer >= 0:
                 self.layer_jobs[j.layer].append(j)
         self.offload = self.plan.s_params < self.spec.model_bytes
+        if self.offload and self.mla:
+            raise NotImplementedError("weight offload is built for the Mixtral family; DeepSeek-V2 runs resident")
         self._plan_streams()
         # ---- weights ----
         if self.offload:
             from .offload import OffloadedMixtralWeights
             self.w = OffloadedMixtralWeights(a, self.spec, self.plan.s_params, self.plan.s_expert, seed=seed,
                                              device=device)
+        elif self.mla:
+            self.w = DeepseekDeviceWeights(a, seed=seed, device=device)
         else:
             self.w = MixtralDeviceWeights(a, seed=seed, device=device)
-        # ---- paged KV cache (identity block table: sequence b owns pages [b*pps, (b+1)*pps)) ----
-        self.page = ops.kv_page_size()
-        self.pps = math.ceil(self.max_ctx / self.page)
-        n_pages = B * self.pps
-        blk = a.n_kv_heads * a.head_dim * self.page
-        self.k_cache = [torch.zeros(n_pages * blk, dtype=BF16, device=device) for _ in range(a.layers)]
-        self.v_cache = [torch.zeros(n_pages * blk, dtype=BF16, device=device) for _ in range(a.layers)]
-        self.block_table = torch.arange(n_pages, dtype=torch.int32, device=device).view(B, self.pps)
-        # ---- RoPE tables (HF MixtralRotaryEmbedding, bf16-rounded, modeling_mixtral.py:210-220) ----
-        hd = a.head_dim
-        inv_freq = 1.0 / (a.rope_theta ** (torch.arange(0, hd, 2, dtype=torch.int64).float() / hd))
-        freqs = torch.arange(self.max_ctx).float()[:, None] * inv_freq[None, :]
-        self.cos_t = freqs.cos().to(BF16).float().contiguous().to(device)
-        self.sin_t = freqs.sin().to(BF16).float().contiguous().to(device)
-        # ---- step buffers ----
         d, k, f = a.hidden, a.top_k, a.moe_ffn
-        qd, kvd = a.n_heads * hd, a.n_kv_heads * hd
-        rows = B * k
         bf = dict(dtype=BF16, device=device)
         i32 = dict(dtype=torch.int32, device=device)
+        # ---- paged KV cache (identity block table: sequence b owns pages [b*pps, (b+1)*pps)) ----
+        if self.mla:
+            # latent pages [(R + r)/8][32 tok][8] (attn_mla.cu)
+            self.page = nat.value("mgb_mla_page_size")
+            self.pps = math.ceil(self.max_ctx / self.page)
+            n_pages = B * self.pps
+            self.latent = [torch.zeros(n_pages * (a.kv_lora_rank + a.qk_rope_dim) * self.page, **bf)
+                           for _ in range(a.layers)]
+            r = a.qk_rope_dim
+            inv_freq = 1.0 / (a.rope_theta ** (torch.arange(0, r, 2, dtype=torch.int64).float() / r))
+            freqs = torch.arange(self.max_ctx).float()[:, None] * inv_freq[None, :]
+            cis = torch.polar(torch.ones_like(freqs), freqs)  # fp32, HF DeepseekV2RotaryEmbedding
+            self.cos_t = cis.real.contiguous().to(device)
+            self.sin_t = cis.imag.contiguous().to(device)
+        else:
+            self.page = ops.kv_page_size()
+            self.pps = math.ceil(self.max_ctx / self.page)
+            n_pages = B * self.pps
+            blk = a.n_kv_heads * a.head_dim * self.page
+            self.k_cache = [torch.zeros(n_pages * blk, **bf) for _ in range(a.layers)]
+            self.v_cache = [torch.zeros(n_pages * blk, **bf) for _ in range(a.layers)]
+            # RoPE tables (HF MixtralRotaryEmbedding, bf16-rounded, modeling_mixtral.py:210-220)
+            hd = a.head_dim
+            inv_freq = 1.0 / (a.rope_theta ** (torch.arange(0, hd, 2, dtype=torch.int64).float() / hd))
+            freqs = torch.arange(self.max_ctx).float()[:, None] * inv_freq[None, :]
+            self.cos_t = freqs.cos().to(BF16).float().contiguous().to(device)
+            self.sin_t = freqs.sin().to(BF16).float().contiguous().to(device)
+        self.block_table = torch.arange(n_pages, dtype=torch.int32, device=device).view(B, self.pps)
+        # ---- step buffers ----
+        rows = B * k
+        if self.mla:
+            H = a.n_heads
+            qd = H * (a.qk_nope_dim + a.qk_rope_dim)
+            self.mb = dict(q=torch.zeros(B, qd, **bf), ckv=torch.zeros(B, a.kv_lora_rank + a.qk_rope_dim, **bf),
+                           q_nope=torch.zeros(H * B * a.qk_nope_dim, **bf),
+                           q_pe=torch.zeros(B, H, a.qk_rope_dim, **bf),
+                           q_lat=torch.zeros(H * B * a.kv_lora_rank, **bf),
+                           o_lat=torch.zeros(H * B * a.kv_lora_rank, **bf),
+                           o_hb=torch.zeros(H * B * a.v_head_dim, **bf),
+                           o_cat=torch.zeros(B, H * a.v_head_dim, **bf),
+                           offsets_all=torch.tensor([0, B], dtype=torch.int32, device=device))
+            if a.q_lora_rank:
+                self.mb.update(q_a=torch.zeros(B, a.q_lora_rank, **bf), q_an=torch.zeros(B, a.q_lora_rank, **bf))
+            fs = a.moe_ffn * a.n_shared
+            self.mb.update(sh_h=torch.zeros(B, fs, **bf), de_h=torch.zeros(B, max(a.dense_ffn, 8), **bf),
+                           sh_out=torch.zeros(B, d, **bf))
+            qkv_cols, attn_cols = 8, 8  # unused for MLA
+        else:
+            hd = a.head_dim
+            qkv_cols, attn_cols = (a.n_heads + 2 * a.n_kv_heads) * hd, a.n_heads * hd
         self.buf = StepBuffers(
-            x=torch.zeros(B, d, **bf), h=torch.zeros(B, d, **bf), qkv=torch.zeros(B, qd + 2 * kvd, **bf),
-            q=torch.zeros(B, qd, **bf), attn=torch.zeros(B, qd, **bf), o=torch.zeros(B, d, **bf),
+            x=torch.zeros(B, d, **bf), h=torch.zeros(B, d, **bf), qkv=torch.zeros(B, qkv_cols, **bf),
+            q=torch.zeros(B, attn_cols, **bf), attn=torch.zeros(B, attn_cols, **bf), o=torch.zeros(B, d, **bf),
             x_perm=torch.zeros(rows, d, **bf), h_ffn=torch.zeros(rows, f, **bf), y_perm=torch.zeros(rows, d, **bf),
             logits=torch.zeros(B, a.vocab, **bf), next_ids=torch.zeros(B, **i32), positions=torch.zeros(B, **i32),
             seq_lens=torch.zeros(B, **i32), step=torch.zeros(1, **i32))
@@ -233,9 +272,88 @@ class Engine:
             W = dict(W, wqkv=wqkv, wo=wo)
         return W
 
+    # ---- DeepSeek-V2 (MLA) jobs ------------------------------------------------------------
+    def _ds_views(self, s0: int, s1: int):
+        """Per-micro-batch [H, Bmb, *] views of the head-major MLA scratch buffers."""
+        a, m = self.arch, self.mb
+        H, n = a.n_heads, s1 - s0
+        R, nope, v = a.kv_lora_rank, a.qk_nope_dim, a.v_head_dim
+        off = H * s0
+        return (m["q_nope"][off * nope:(off + H * n) * nope].view(H, n, nope),
+                m["q_lat"][off * R:(off + H * n) * R].view(H, n, R),
+                m["o_lat"][off * R:(off + H * n) * R].view(H, n, R),
+                m["o_hb"][off * v:(off + H * n) * v].view(H, n, v))
+
+    def _ds_job(self, l: int, j, W: dict) -> None:
+        """DeepseekV2DecoderLayer (modeling_deepseek_v2.py:399-430) as module jobs; attention in the
+        absorbed latent form (q_lat = W_UK^T q_nope, o = W_UV o_lat, attn_mla.cu)."""
+        a, b, m = self.arch, self.buf, self.mb
+        H, R, r, nope = a.n_heads, a.kv_lora_rank, a.qk_rope_dim, a.qk_nope_dim
+        if j.kind == "pre_attention":
+            s0, s1 = self._mb_range(j)
+            if l == 0:
+                ops.add_rmsnorm(b.x[s0:s1], W["ln1"], a.rms_eps, b.h[s0:s1])
+            h = b.h[s0:s1]
+            if a.q_lora_rank:
+                torch.mm(h, W["q_a"].t(), out=m["q_a"][s0:s1])
+                ops.add_rmsnorm(m["q_a"][s0:s1], W["q_a_norm"], a.rms_eps, m["q_an"][s0:s1])
+                torch.mm(m["q_an"][s0:s1], W["q_b"].t(), out=m["q"][s0:s1])
+            else:
+                torch.mm(h, W["q_proj"].t(), out=m["q"][s0:s1])
+            torch.mm(h, W["kv_a"].t(), out=m["ckv"][s0:s1])
+            q_nope, q_lat, _, _ = self._ds_views(s0, s1)
+            nat.call("mgb_mla_append", m["q"][s0:s1].data_ptr(), m["ckv"][s0:s1].data_ptr(),
+                     W["kv_a_norm"].data_ptr(), a.rms_eps, s1 - s0, H, R, r, nope, b.positions[s0:].data_ptr(),
+                     self.cos_t.data_ptr(), self.sin_t.data_ptr(), self.block_table[s0:].data_ptr(), self.pps,
+                     self.latent[l].data_ptr(), q_nope.data_ptr(), m["q_pe"][s0:s1].data_ptr(),
+                     b.seq_lens[s0:].data_ptr(), torch.cuda.current_stream().cuda_stream)
+            torch.bmm(q_nope, W["w_uk"], out=q_lat)
+        elif j.kind == "attn_mech_gpu":
+            s0, s1 = self._mb_range(j)
+            _, q_lat, o_lat, o_hb = self._ds_views(s0, s1)
+            scale = (a.qk_nope_dim + a.qk_rope_dim) ** -0.5
+            nat.call("mgb_decode_attn_mla", q_lat.data_ptr(), m["q_pe"][s0:s1].data_ptr(), self.latent[l].data_ptr(),
+                     self.block_table[s0:].data_ptr(), self.pps, b.seq_lens[s0:].data_ptr(), s1 - s0, H, R, r, scale,
+                     o_lat.data_ptr(), torch.cuda.current_stream().cuda_stream)
+            torch.bmm(o_lat, W["w_uv_t"], out=o_hb)
+            m["o_cat"][s0:s1].view(s1 - s0, H, a.v_head_dim).copy_(o_hb.transpose(0, 1))
+        elif j.kind == "post_attention":
+            torch.mm(m["o_cat"], W["wo"].t(), out=b.o)
+            ops.add_rmsnorm(b.x, W["ln2"], a.rms_eps, b.h, delta=b.o, x_out=b.x)
+        elif j.kind == "router":
+            if l >= a.first_k_dense:
+                ops.router_topk(b.h, W["router"], self.rws, a.top_k, a.router_mode, a.routed_scaling, a.n_group,
+                                a.topk_group)
+                ops.permute(b.h, self.rws, b.x_perm)
+                if self.debug_taps is not None:
+                    self.debug_taps.update(h2=b.h.clone(), topk_idx=self.rws.topk_idx.clone())
+        elif j.kind == "expert_compute":
+            nxt = self.w.layers[l + 1]["ln1"] if l + 1 < a.layers else self.w.final_norm
+            first, last = j.id == self.first_expert_job[l], j.id == self.last_expert_job[l]
+            if l < a.first_k_dense:
+                # dense MLP of the first layers (DeepseekV2MLP) on the same grouped kernel, E = 1
+                if first:
+                    ops.moe_gemm_gate_up(W["dense_gate_up"], b.h, m["offsets_all"], m["de_h"])
+                    ops.moe_gemm_down(W["dense_down"], m["de_h"], m["offsets_all"], b.o)
+                    ops.add_rmsnorm(b.x, nxt, a.rms_eps, b.h, delta=b.o, x_out=b.x)
+                return
+            if first:
+                ops.moe_gemm_gate_up(W["w_gate_up"], b.x_perm, self.rws.offsets, b.h_ffn)
+                ops.moe_gemm_down(W["w_down"], b.h_ffn, self.rws.offsets, b.y_perm)
+                # shared experts on every token (DeepseekV2Moe.shared_experts)
+                ops.moe_gemm_gate_up(W["sh_gate_up"], b.h, m["offsets_all"], m["sh_h"])
+                ops.moe_gemm_down(W["sh_down"], m["sh_h"], m["offsets_all"], m["sh_out"])
+            if last:
+                ops.unpermute_combine(b.y_perm, self.rws, b.x, self.B, residual=b.x, shared_out=m["sh_out"],
+                                      norm_w=nxt, eps=a.rms_eps, norm_out=b.h)
+        else:
+            raise RuntimeError(f"job kind {j.kind!r} is not executable under kv_policy={self.kv_policy!r}")
+
     def _issue_job(self, l: int, j) -> None:
         a, b = self.arch, self.buf
         W = self._layer_weights(l)
+        if self.mla:
+            return self._ds_job(l, j, W)
         hd, Hq, Hkv = a.head_dim, a.n_heads, a.n_kv_heads
         if True:
             if j.kind == "weight_copy":
@@ -330,8 +448,10 @@ class Engine:
         torch.cuda.current_stream().wait_stream(self.stream)
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
+        n0 = nat.LIB.calls
         with torch.cuda.graph(g, stream=self.stream):
             self._step()
+        self.kernel_launches_per_step = nat.LIB.calls - n0  # libmgb launches captured per step
         torch.cuda.synchronize()
         for t, s in zip((self.buf.positions, self.buf.step, self.buf.next_ids, self.buf.seq_lens), snap):
             t.copy_(s)
@@ -363,8 +483,11 @@ class Engine:
         prompt_len, so decode steps attend over prompt_len..prompt_len+decode_len keys."""
         from .weights import fill_uniform_
         for l in range(self.arch.layers):
-            fill_uniform_(self.k_cache[l], seed, 10_000_000 + 2 * l, std)
-            fill_uniform_(self.v_cache[l], seed, 10_000_001 + 2 * l, std)
+            if self.mla:
+                fill_uniform_(self.latent[l], seed, 10_000_000 + 2 * l, std)
+            else:
+                fill_uniform_(self.k_cache[l], seed, 10_000_000 + 2 * l, std)
+                fill_uniform_(self.v_cache[l], seed, 10_000_001 + 2 * l, std)
         self.reset(self.prompt_len)
 
     def decode(self, first_tokens: torch.Tensor, n_steps: int) -> torch.Tensor:

@@ -73,3 +73,55 @@ class MixtralDeviceWeights:
         for L in self.layers:
             n += sum(t.nbytes for t in L.values())
         return n
+
+
+DS_SLOT = dict(ln1=0, ln2=5, router=6, w_gate_up=7, w_down=8, q_proj=10, q_a_norm=11, q_b=12, kv_a=13,
+               kv_a_norm=14, kv_b=15, wo=16, sh_gate_up=17, sh_down=18, dense_gate_up=19, dense_down=20)
+
+
+def ds_tid(layer: int, name: str) -> int:
+    return LAYER_BASE + LAYER_STRIDE * layer + DS_SLOT[name]
+
+
+class DeepseekDeviceWeights:
+    """DeepSeek-V2 family weights in HF layouts (q_proj or q_a/q_b, kv_a_proj_with_mqa, kv_b_proj,
+    o_proj; routed experts [E,2f,d]/[E,d,f]; shared experts and the dense first layers as fused
+    gate|up [2f,d] + down [d,f]).  Tensor ids mirror oracle/moe_ref.py DS_SLOT."""
+
+    def __init__(self, arch: ModelArch, seed: int = 0, device: str = "cuda"):
+        a = arch
+        d, H = a.hidden, a.n_heads
+        qk = a.qk_nope_dim + a.qk_rope_dim
+        std = a.init_std
+        bf = dict(dtype=torch.bfloat16, device=device)
+        U = lambda shape, name, l: fill_uniform_(torch.empty(*shape, **bf), seed, ds_tid(l, name), std)  # noqa: E731
+        ones = lambda n: fill_const_(torch.empty(n, **bf), 1.0)  # noqa: E731
+        self.arch = a
+        self.embed = fill_uniform_(torch.empty(a.vocab, d, **bf), seed, TID_EMBED, std)
+        self.final_norm = ones(d)
+        self.lm_head = fill_uniform_(torch.empty(a.vocab, d, **bf), seed, TID_LM_HEAD, std)
+        self.layers = []
+        for l in range(a.layers):
+            L = dict(ln1=ones(d), ln2=ones(d), kv_a=U((a.kv_lora_rank + a.qk_rope_dim, d), "kv_a", l),
+                     kv_a_norm=ones(a.kv_lora_rank),
+                     kv_b=U((H * (a.qk_nope_dim + a.v_head_dim), a.kv_lora_rank), "kv_b", l),
+                     wo=U((d, H * a.v_head_dim), "wo", l))
+            if a.q_lora_rank:
+                L.update(q_a=U((a.q_lora_rank, d), "q_proj", l), q_a_norm=ones(a.q_lora_rank),
+                         q_b=U((H * qk, a.q_lora_rank), "q_b", l))
+            else:
+                L["q_proj"] = U((H * qk, d), "q_proj", l)
+            if l < a.first_k_dense:
+                L.update(dense_gate_up=U((1, 2 * a.dense_ffn, d), "dense_gate_up", l),
+                         dense_down=U((1, d, a.dense_ffn), "dense_down", l))
+            else:
+                fs = a.moe_ffn * a.n_shared
+                L.update(router=U((a.n_experts, d), "router", l),
+                         w_gate_up=U((a.n_experts, 2 * a.moe_ffn, d), "w_gate_up", l),
+                         w_down=U((a.n_experts, d, a.moe_ffn), "w_down", l),
+                         sh_gate_up=U((1, 2 * fs, d), "sh_gate_up", l), sh_down=U((1, d, fs), "sh_down", l))
+            # absorption views of kv_b_proj: rows [h*(nope+v), h*(nope+v)+nope) = W_UK_h, rest = W_UV_h
+            kvb = L["kv_b"].view(H, a.qk_nope_dim + a.v_head_dim, a.kv_lora_rank)
+            L["w_uk"] = kvb[:, :a.qk_nope_dim, :]          # [H, nope, R]
+            L["w_uv_t"] = kvb[:, a.qk_nope_dim:, :].transpose(1, 2)  # [H, R, v]
+            self.layers.append(L)
