@@ -114,38 +114,68 @@ def _max_over_ranks(dist, v: float) -> float:
 # CPU arm (oracle port): one decoder layer decode step of B sequences, x L layers
 # ------------------------------------------------------------------------------------------
 def cpu_layer_sample(arch, B: int, ctx: int, reps: int, threads: int) -> tuple[float, str]:
+    """The oracle port (oracle/moe_ref.py) timed on the host: one MoE decoder layer of B sequences
+    at context `ctx`, scaled by the layer count (a full 93-471 GB model is impractical on CPU)."""
     from oracle import moe_ref as R
 
     torch.set_num_threads(threads)
     a = arch
-    d, hd = a.hidden, a.head_dim
+    d = a.hidden
     g = torch.Generator().manual_seed(0)
     bf = torch.bfloat16
 
     def U(*shape, std=0.02):
         return (torch.rand(*shape, generator=g) * 2 - 1).mul_(std * math.sqrt(3)).to(bf)
 
-    W = dict(ln1=torch.ones(d, dtype=bf), wq=U(a.n_heads * hd, d), wk=U(a.n_kv_heads * hd, d),
-             wv=U(a.n_kv_heads * hd, d), wo=U(d, a.n_heads * hd), ln2=torch.ones(d, dtype=bf),
-             router=U(a.n_experts, d), w_gate_up=U(a.n_experts, 2 * a.moe_ffn, d),
-             w_down=U(a.n_experts, d, a.moe_ffn))
-
     class _W:
-        layers = [W]
-    orc = R.MixtralOracle.__new__(R.MixtralOracle)
-    orc.a, orc.w = a, _W()
-    kc = U(B, a.n_kv_heads, ctx - 1, hd, std=1.0)
-    vc = U(B, a.n_kv_heads, ctx - 1, hd, std=1.0)
+        layers = []
+    if a.family == "deepseek_v2":
+        H, qk = a.n_heads, a.qk_nope_dim + a.qk_rope_dim
+        fs = a.moe_ffn * a.n_shared
+        W = dict(ln1=torch.ones(d, dtype=bf), ln2=torch.ones(d, dtype=bf),
+                 kv_a=U(a.kv_lora_rank + a.qk_rope_dim, d), kv_a_norm=torch.ones(a.kv_lora_rank, dtype=bf),
+                 kv_b=U(H * (a.qk_nope_dim + a.v_head_dim), a.kv_lora_rank), wo=U(d, H * a.v_head_dim),
+                 router=U(a.n_experts, d), w_gate_up=U(a.n_experts, 2 * a.moe_ffn, d),
+                 w_down=U(a.n_experts, d, a.moe_ffn), sh_gate_up=U(2 * fs, d), sh_down=U(d, fs))
+        if a.q_lora_rank:
+            W.update(q_a=U(a.q_lora_rank, d), q_a_norm=torch.ones(a.q_lora_rank, dtype=bf), q_b=U(H * qk, a.q_lora_rank))
+        else:
+            W["q_proj"] = U(H * qk, d)
+        _W.layers = [None] * a.first_k_dense + [W]
+        orc = R.DeepseekV2Oracle.__new__(R.DeepseekV2Oracle)
+        orc.a, orc.w = a, _W()
+        li = a.first_k_dense
+        kc = U(B, H, ctx - 1, qk, std=1.0)
+        vc = U(B, H, ctx - 1, a.v_head_dim, std=1.0)
+        caches = lambda: ([None] * li + [kc], [None] * li + [vc])  # noqa: E731
+        name = "DeepseekV2Oracle.layer_forward"
+    else:
+        hd = a.head_dim
+        W = dict(ln1=torch.ones(d, dtype=bf), wq=U(a.n_heads * hd, d), wk=U(a.n_kv_heads * hd, d),
+                 wv=U(a.n_kv_heads * hd, d), wo=U(d, a.n_heads * hd), ln2=torch.ones(d, dtype=bf),
+                 router=U(a.n_experts, d), w_gate_up=U(a.n_experts, 2 * a.moe_ffn, d),
+                 w_down=U(a.n_experts, d, a.moe_ffn))
+        _W.layers = [W]
+        orc = R.MixtralOracle.__new__(R.MixtralOracle)
+        orc.a, orc.w = a, _W()
+        li = 0
+        kc = U(B, a.n_kv_heads, ctx - 1, hd, std=1.0)
+        vc = U(B, a.n_kv_heads, ctx - 1, hd, std=1.0)
+        caches = lambda: ([kc], [vc])  # noqa: E731
+        name = "MixtralOracle.layer_forward"
     x = U(B, d, std=1.0)
     times = []
     for r in range(reps + 1):
-        orc.k_cache, orc.v_cache = [kc], [vc]
+        if a.family == "deepseek_v2":
+            orc.kc, orc.vc = caches()
+        else:
+            orc.k_cache, orc.v_cache = caches()
         t0 = time.perf_counter()
-        orc.layer_forward(0, x, ctx - 1)
+        orc.layer_forward(li, x, ctx - 1)
         times.append(time.perf_counter() - t0)
     t_layer = statistics.median(times[1:])
-    sample = (f"oracle/moe_ref.py MixtralOracle.layer_forward: one {a.name} decoder layer, B={B} sequences, "
-              f"context {ctx}, bf16 torch-CPU, median of {reps}; tokens/s = B / (t_layer x {a.layers} layers)")
+    sample = (f"oracle/moe_ref.py {name}: one {a.name} MoE decoder layer, B={B} sequences, context {ctx}, "
+              f"bf16 torch-CPU, median of {reps}; tokens/s = B / (t_layer x {a.layers} layers)")
     return B / (t_layer * a.layers), sample
 
 
@@ -306,10 +336,18 @@ def run_ours(args, dist, rank, world) -> None:
     step_ms_eager = sum(v["ms_per_step"] for v in bd.values())
     ffn_ms = gu["avg_ms"] + dn["avg_ms"]
     expert_tflops = (gu_flops + dn_flops) / (ffn_ms * 1e-3) / 1e12
-    roofline = {"kernel": "mgb_moe_gemm_gate_up (tcgen05 grouped GEMM + SiLU*up)", "bound": "hbm",
-                "achieved": gu_gbs, "peak": hbm, "unit": "GB/s", "frac": gu_gbs / hbm, "traffic": None,
-                "algorithmic_bytes_per_launch": gu_bytes, "avg_launch_ms": gu["avg_ms"], "peak_source": src,
-                "share_of_step": gu["ms_per_step"] / step_ms_eager}
+    tok_per_expert = rows / a.n_experts
+    ridge = tf_burst * 1e12 / (hbm * 1e9)  # flop/B; expert GEMM intensity = tokens/expert flop/B
+    if tok_per_expert < ridge:
+        roofline = {"kernel": "mgb_moe_gemm_gate_up (tcgen05 grouped GEMM + SiLU*up)", "bound": "hbm",
+                    "achieved": gu_gbs, "peak": hbm, "unit": "GB/s", "frac": gu_gbs / hbm}
+    else:
+        gu_tf = gu_flops / (gu["avg_ms"] * 1e-3) / 1e12
+        roofline = {"kernel": "mgb_moe_gemm_gate_up (tcgen05 grouped GEMM + SiLU*up)", "bound": "tensor",
+                    "achieved": gu_tf, "peak": tf_burst, "unit": "TFLOP/s", "frac": gu_tf / tf_burst}
+    roofline.update({"traffic": None, "algorithmic_bytes_per_launch": gu_bytes, "algorithmic_flops_per_launch": gu_flops,
+                     "avg_launch_ms": gu["avg_ms"], "peak_source": src, "tokens_per_expert": tok_per_expert,
+                     "share_of_step": gu["ms_per_step"] / step_ms_eager})
     launches_per_step = eng.kernel_launches_per_step * N
     ctx_avg = args.prompt_len + args.decode_len / 2
 
@@ -318,7 +356,8 @@ def run_ours(args, dist, rank, world) -> None:
         "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (random-init counter-based weights, synthetic prefill KV)",
         "config": {"workload": f"{arch.name} decode phase, prompt {args.prompt_len} / gen {N}, 1 B200 resident "
-                               f"(BASELINE configs[1]); step = {N} decode forwards of B={B} sequences",
+                               f"({'BASELINE configs[1]' if arch.name == 'mixtral-8x7b' else 'BASELINE configs[2] shape'});"
+                               f" step = {N} decode forwards of B={B} sequences",
                    "batch": B, "b_a": plan.b_a, "b_e": plan.b_e, "kv_policy": "resident (paged, HBM)",
                    "parallelism": f"replicas x{world}", "l2": "inputs larger than L2 (93 GB weights streamed/forward)"},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(first_pinned.numel() * 4),
