@@ -113,8 +113,11 @@ class ModelArch:
             doc["attn_flops_per_context"] = float(
                 2 * self.kv_lora_rank * H * self.qk_nope_dim + 2 * self.kv_lora_rank * H * self.v_head_dim
                 + 2 * H * (self.qk_nope_dim + self.qk_rope_dim) + 2 * H * self.v_head_dim)
-            up = H * ((self.qk_nope_dim + self.qk_rope_dim) + self.v_head_dim) * BYTES
-            doc["attn_activation_bytes_per_ctx_token"] = float(6 * up)
+            # The reference's DSV2 preset charges the up-projected per-head K/V working set
+            # (6 x H x 320 x 2 B per context token, model_catalog.py:248-254).  This engine runs
+            # absorbed MLA (attn_mla.cu) straight off the 576-wide latent cache, so no per-context
+            # activation exists and the term is 0.
+            doc["attn_activation_bytes_per_ctx_token"] = 0.0
         else:
             doc["attn_flops_per_context"] = float(4 * self.n_heads * self.head_dim)
         return doc

@@ -58,9 +58,18 @@ def resident_plan(arch: ModelArch, prompt_len: int, decode_len: int, B: int | No
     hw = Hardware(**{**hw.__dict__, "m_g": hw.m_g - reserve_bytes})
     wl = WorkloadSpec(prompt_len, decode_len, 1, "decode")
     tmpl = BatchingPlan(1, 1, b_e, 0.0, 0, spec.model_bytes)
+    from .planner import footprint
+
     bmax = largest_batch(spec, hw, wl, tmpl, kv_policy="resident")
+    if b_a is None:  # one attention micro-batch: re-size B with b_a = B charged (Eq. 3)
+        bmax = largest_batch(spec, hw, wl, BatchingPlan(1, bmax, b_e, 0.0, 0, spec.model_bytes), kv_policy="resident")
     B = bmax if B is None else min(B, bmax)
-    return BatchingPlan(B, B if b_a is None else min(b_a, B), b_e, 0.0, 0, spec.model_bytes)
+    b_a = B if b_a is None else min(b_a, B)
+    # largest attention micro-batch the GPU constraint admits (Eq. 3 charges b_a's activations)
+    while b_a > 1 and not footprint(spec, hw, wl, BatchingPlan(B, b_a, b_e, 0.0, 0, spec.model_bytes),
+                                    "resident").feasible:
+        b_a = (b_a + 1) // 2
+    return BatchingPlan(B, b_a, b_e, 0.0, 0, spec.model_bytes)
 
 
 @dataclass
