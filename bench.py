@@ -212,57 +212,44 @@ def run_reference(args, dist, rank, world) -> None:
 # GPU arm
 # ------------------------------------------------------------------------------------------
 def kernel_breakdown(eng, reps: int = 2) -> dict:
-    """Eager pass with CUDA events around every launch of one decode step (same stream as the
-    graph); returns {name: avg ms per launch, count per step}."""
-    from paper_2503_09716_b200 import ops
+    """Eager pass with CUDA events around every launch of one decode step on the engine stream
+    (the stream the graph replays on): every libmgb entry point (by C-ABI name) and every cuBLAS
+    call.  The stream is parked first so the host enqueues the whole step before the GPU starts;
+    event gaps then time kernels, not Python launch latency."""
+    from paper_2503_09716_b200 import _native as nat
 
     st = eng.stream
-    recs: dict[str, list[float]] = {}
-    orig = {n: getattr(ops, n) for n in ("moe_gemm_gate_up", "moe_gemm_down", "decode_attn_gqa", "router_topk",
-                                         "permute", "unpermute_combine", "add_rmsnorm", "rope_append_gqa",
-                                         "embed", "argmax", "decode_advance")}
     pend: list[tuple[str, torch.cuda.Event, torch.cuda.Event]] = []
 
-    def wrap(name, fn):
+    def timed(name, fn):
         def inner(*a, **k):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(st)
-            fn(*a, **k)
+            r = fn(*a, **k)
             e1.record(st)
-            pend.append((name, e0, e1))
+            pend.append((name if isinstance(name, str) else name(a), e0, e1))
+            return r
         return inner
 
-    mm = torch.mm
-
-    def mm_wrap(*a, **k):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(st)
-        r = mm(*a, **k)
-        e1.record(st)
-        pend.append(("cublas_gemm", e0, e1))
-        return r
-
-    import paper_2503_09716_b200.engine as E
+    orig_call, mm, bmm = nat.call, torch.mm, torch.bmm
     try:
-        for n, f in orig.items():
-            setattr(ops, n, wrap(n, f))
-        torch.mm = mm_wrap
+        # grouped GEMM launches are keyed by expert count (routed E vs shared / dense E = 1)
+        nat.call = timed(lambda a: f"{a[0]}[E={a[4]}]" if a[0].startswith("mgb_moe_gemm") else a[0], orig_call)
+        torch.mm = timed("cublas_gemm", mm)
+        torch.bmm = timed("cublas_bmm", bmm)
         saved = [t.clone() for t in (eng.buf.positions, eng.buf.step, eng.buf.next_ids, eng.buf.seq_lens)]
         for _ in range(reps):
             with torch.cuda.stream(st):
-                # park the stream so the host enqueues the whole step before the GPU starts:
-                # event gaps then measure kernels, not Python launch latency
                 torch.cuda._sleep(int(2e8))
                 eng._step(record=False)
             torch.cuda.synchronize()
         for t, s in zip((eng.buf.positions, eng.buf.step, eng.buf.next_ids, eng.buf.seq_lens), saved):
             t.copy_(s)
     finally:
-        for n, f in orig.items():
-            setattr(ops, n, f)
-        torch.mm = mm
+        nat.call, torch.mm, torch.bmm = orig_call, mm, bmm
+    recs: dict[str, list[float]] = {}
     for name, e0, e1 in pend:
-        recs.setdefault(name, []).append(e0.elapsed_time(e1))
+        recs.setdefault(name.replace("mgb_", ""), []).append(e0.elapsed_time(e1))
     return {n: {"avg_ms": sum(v) / len(v), "per_step": len(v) // reps, "ms_per_step": sum(v) / reps}
             for n, v in recs.items()}
 
@@ -326,8 +313,9 @@ def run_ours(args, dist, rank, world) -> None:
     a = arch
     rows = B * a.top_k
     k_active = a.n_experts  # every expert is hit at these batch sizes
-    gu = bd.get("moe_gemm_gate_up", {"avg_ms": float("nan")})
-    dn = bd.get("moe_gemm_down", {"avg_ms": float("nan")})
+    nan = {"avg_ms": float("nan"), "ms_per_step": float("nan")}
+    gu = bd.get(f"moe_gemm_gate_up[E={arch.n_experts}]", nan)  # the routed-expert launches
+    dn = bd.get(f"moe_gemm_down[E={arch.n_experts}]", nan)
     gu_bytes = k_active * 2 * a.moe_ffn * a.hidden * 2 + rows * a.hidden * 2 + rows * a.moe_ffn * 2
     dn_bytes = k_active * a.hidden * a.moe_ffn * 2 + rows * a.moe_ffn * 2 + rows * a.hidden * 2
     gu_flops = 2.0 * rows * a.hidden * 2 * a.moe_ffn

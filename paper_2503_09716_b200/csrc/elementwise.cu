@@ -147,9 +147,31 @@ __global__ void argmax_kernel(const __nv_bfloat16* __restrict__ logits, int V, i
   const __nv_bfloat16* lr = logits + row * V;
   float bv = -INFINITY;
   int bi = 0x7fffffff;
-  for (int i = threadIdx.x; i < V; i += blockDim.x) {
-    const float v = __bfloat162float(lr[i]);
-    if (v > bv || (v == bv && i < bi)) { bv = v; bi = i; }
+  if ((V & 7) == 0) {  // 16 B vectors; all of a thread's loads issued before the compares
+    const uint4* lv = reinterpret_cast<const uint4*>(lr);
+    const int nv = V / 8;
+    constexpr int U = 4;
+    for (int c0 = threadIdx.x; c0 < nv; c0 += blockDim.x * U) {
+      uint4 w[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (c0 + u * (int)blockDim.x < nv) w[u] = ld_nc_v4(lv + c0 + u * blockDim.x);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int c = c0 + u * blockDim.x;
+        if (c >= nv) break;
+        const float f[8] = {bf16lo(w[u].x), bf16hi(w[u].x), bf16lo(w[u].y), bf16hi(w[u].y),
+                            bf16lo(w[u].z), bf16hi(w[u].z), bf16lo(w[u].w), bf16hi(w[u].w)};
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          if (f[i] > bv) { bv = f[i]; bi = c * 8 + i; }  // ascending index within a thread: first max kept
+      }
+    }
+  } else {
+    for (int i = threadIdx.x; i < V; i += blockDim.x) {
+      const float v = __bfloat162float(lr[i]);
+      if (v > bv || (v == bv && i < bi)) { bv = v; bi = i; }
+    }
   }
   __shared__ float sv[32];
   __shared__ int si[32];

@@ -22,6 +22,7 @@ constexpr int kRouterTPB = 8;        // tokens per CTA
 constexpr int kRouterThreads = 256;  // 8 warps: one token per warp in the selection phase
 constexpr int kMaxE = 256;
 constexpr int kMaxK = 8;
+constexpr int kFusedScanMaxBlocks = 128;  // above this the column scan runs as its own E-CTA kernel
 
 struct RouterArgs {
   const __nv_bfloat16* x;  // [T, d]
@@ -208,6 +209,7 @@ __global__ void __launch_bounds__(kRouterThreads) router_topk_kernel(RouterArgs 
     for (int j = 0; j < nent; ++j) c += (s_exp[j] == e);
     a.block_hist[(size_t)blockIdx.x * E + e] = c;
   }
+  if ((int)gridDim.x > kFusedScanMaxBlocks) return;  // many blocks: router_scan_kernel finishes the job
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) s_last = (atomicAdd(a.ticket, 1) == (int)gridDim.x - 1);
@@ -264,6 +266,63 @@ __global__ void __launch_bounds__(kRouterThreads) router_topk_kernel(RouterArgs 
     }
     a.offsets[E] = run;
     *a.ticket = 0;
+  }
+}
+
+// Column scan of the per-CTA expert histograms for large T: one CTA per expert turns its column
+// into exclusive per-block bases (4 blocks per thread, warp shuffles + one smem pass per chunk of
+// 1024 blocks) and writes counts[e]; the last CTA to finish derives offsets[E+1] from counts.
+__global__ void __launch_bounds__(256) router_scan_kernel(int* __restrict__ block_hist, int nblk, int E,
+                                                          int* __restrict__ counts, int* __restrict__ offsets,
+                                                          int* __restrict__ ticket) {
+  const int e = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ int s_warp[8];
+  __shared__ int s_carry;
+  __shared__ bool s_last;
+  if (tid == 0) s_carry = 0;
+  __syncthreads();
+  for (int base = 0; base < nblk; base += 256 * 4) {
+    int v[4];
+    const int b0 = base + tid * 4;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = (b0 + i < nblk) ? __ldcg(block_hist + (size_t)(b0 + i) * E + e) : 0;
+    const int s = v[0] + v[1] + v[2] + v[3];
+    int incl = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    int wpre = 0;
+    for (int w = 0; w < warp; ++w) wpre += s_warp[w];
+    int run = s_carry + wpre + incl - s;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (b0 + i < nblk) block_hist[(size_t)(b0 + i) * E + e] = run;
+      run += v[i];
+    }
+    __syncthreads();
+    if (tid == 255) s_carry = run;  // thread 255 holds the chunk's inclusive total
+    __syncthreads();
+  }
+  if (tid == 0) counts[e] = s_carry;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = (atomicAdd(ticket, 1) == (int)gridDim.x - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (tid == 0) {
+    int run = 0;
+    for (int i = 0; i < E; ++i) {
+      offsets[i] = run;
+      run += __ldcg(counts + i);
+    }
+    offsets[E] = run;
+    *ticket = 0;
   }
 }
 
@@ -434,6 +493,9 @@ int mgb_router_topk(const void* x, const void* w_gate, const float* logits_in, i
       return MGB_ECUDA;
   }
   mgb::router_topk_kernel<<<nblk, mgb::kRouterThreads, smem, reinterpret_cast<cudaStream_t>(stream)>>>(a);
+  if (nblk > mgb::kFusedScanMaxBlocks)
+    mgb::router_scan_kernel<<<E, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(block_hist, nblk, E, counts, offsets,
+                                                                                   ticket);
   return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
 }
 

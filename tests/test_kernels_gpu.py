@@ -24,7 +24,8 @@ def _ops():
 
 @pytest.mark.parametrize("T,E,k,mode,ng,tg", [
     (1, 8, 2, 0, 1, 1), (64, 8, 2, 0, 1, 1), (777, 8, 2, 0, 1, 1), (300, 64, 6, 1, 1, 1),
-    (257, 160, 6, 2, 8, 3), (40, 16, 4, 2, 4, 2), (1024, 64, 6, 1, 1, 1)])
+    (257, 160, 6, 2, 8, 3), (40, 16, 4, 2, 4, 2), (1024, 64, 6, 1, 1, 1), (6058, 64, 6, 1, 1, 1),
+    (3001, 160, 6, 2, 8, 3), (9000, 8, 2, 0, 1, 1)])
 def test_router_topk_bitexact_given_logits(T, E, k, mode, ng, tg):
     ops = _ops()
     g = torch.Generator().manual_seed(T * 31 + E)
