@@ -86,6 +86,8 @@ int mgb_rope_append_gqa(const void* qkv, int T, int seq0, const int* positions, 
                         const float* sin_t, int Hq, int Hkv, int head_dim, const int* block_table, int max_pages,
                         void* k_cache, void* v_cache, void* q_out, int* seq_lens, void* stream);
 int mgb_embed(const int* ids, const void* table, int T, int d, void* out, void* stream);
+/* h[T,F] = bf16(bf16(silu(g)) * u) for gate_up[T, 2F] = [g | u] (dense/shared-expert MLP epilogue) */
+int mgb_silu_mul(const void* gate_up, int T, int F, void* h, void* stream);
 int mgb_argmax(const void* logits, int T, int V, int* out, void* stream);
 int mgb_decode_advance(const int* next, int B, long long* out_tokens, int ld, int* step, int* positions,
                        void* stream);

@@ -39,6 +39,7 @@ SIGNATURES: dict[str, list] = {
     "mgb_add_rmsnorm": [P, P, P, F, I, I, P, P, P],
     "mgb_rope_append_gqa": [P, I, I, P, P, P, I, I, I, P, I, P, P, P, P, P],
     "mgb_embed": [P, P, I, I, P, P],
+    "mgb_silu_mul": [P, I, I, P, P],
     "mgb_argmax": [P, I, I, P, P],
     "mgb_decode_advance": [P, I, P, I, P, P, P],
     "mgb_fill_uniform_bf16": [P, L, ctypes.c_uint64, ctypes.c_uint64, F, F, I, P],

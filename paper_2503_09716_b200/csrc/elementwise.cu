@@ -133,6 +133,25 @@ __global__ void rope_append_gqa_kernel(const __nv_bfloat16* __restrict__ qkv, in
   }
 }
 
+// h = bf16(bf16(silu(g)) * u) for gu = [g | u] rows (HF DeepseekV2MLP / MixtralExperts act-mul on the
+// bf16 outputs of a cuBLAS gate|up GEMM).  8 features per thread, 16 B in/out.
+__global__ void silu_mul_kernel(const __nv_bfloat16* __restrict__ gu, int T, int F, __nv_bfloat16* __restrict__ h) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int nv = F / 8;
+  if (i >= (long long)T * nv) return;
+  const int t = (int)(i / nv), c = (int)(i - (long long)t * nv);
+  const uint4 g = reinterpret_cast<const uint4*>(gu + (size_t)t * 2 * F)[c];
+  const uint4 u = reinterpret_cast<const uint4*>(gu + (size_t)t * 2 * F + F)[c];
+  const float gf[8] = {bf16lo(g.x), bf16hi(g.x), bf16lo(g.y), bf16hi(g.y), bf16lo(g.z), bf16hi(g.z), bf16lo(g.w), bf16hi(g.w)};
+  const float uf[8] = {bf16lo(u.x), bf16hi(u.x), bf16lo(u.y), bf16hi(u.y), bf16lo(u.z), bf16hi(u.z), bf16lo(u.w), bf16hi(u.w)};
+  float r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = bf16_round(gf[j] / (1.0f + expf(-gf[j]))) * uf[j];
+  uint4 o;
+  o.x = pack_bf16x2(r[0], r[1]); o.y = pack_bf16x2(r[2], r[3]); o.z = pack_bf16x2(r[4], r[5]); o.w = pack_bf16x2(r[6], r[7]);
+  reinterpret_cast<uint4*>(h + (size_t)t * F)[c] = o;
+}
+
 __global__ void embed_kernel(const int* __restrict__ ids, const __nv_bfloat16* __restrict__ table, int d,
                              __nv_bfloat16* __restrict__ out) {
   const size_t t = blockIdx.x;
@@ -251,6 +270,14 @@ int mgb_rope_append_gqa(const void* qkv, int T, int seq0, const int* positions, 
       reinterpret_cast<const __nv_bfloat16*>(qkv), T, seq0, positions, cos_t, sin_t, Hq, Hkv, head_dim, block_table,
       max_pages, reinterpret_cast<__nv_bfloat16*>(k_cache), reinterpret_cast<__nv_bfloat16*>(v_cache),
       reinterpret_cast<__nv_bfloat16*>(q_out), seq_lens);
+  return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
+}
+
+int mgb_silu_mul(const void* gate_up, int T, int F, void* h, void* stream) {
+  if (T < 1 || F % 8) return MGB_EINVAL;
+  const long long n = (long long)T * (F / 8);
+  mgb::silu_mul_kernel<<<(int)((n + 255) / 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const __nv_bfloat16*>(gate_up), T, F, reinterpret_cast<__nv_bfloat16*>(h));
   return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
 }
 

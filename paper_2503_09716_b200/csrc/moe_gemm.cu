@@ -18,6 +18,8 @@
 // ordered row-tile-fastest so concurrently running CTAs share the same token tile in L2.  4-stage
 // TMA ring, double-buffered TMEM accumulators (epilogue of unit i overlaps the MMAs of unit i+1).
 // Warp roles: w0 = TMA producer, w1 = MMA issuer (+TMEM owner), w2..w5 = epilogue.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace mgb {
@@ -230,21 +232,240 @@ moe_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   if (warp == 1) tmem_dealloc<512>(tmem_base);
 }
 
+// ------------------------------------------------------------------------------------------
+// CTA-pair variant (cluster of 2, tcgen05 cta_group::2, UMMA M = 256).  Each CTA holds its own
+// 128 weight rows (A) and HALF of the token tile (B rows), so per SM the token-operand smem and
+// L2 traffic halve and the ring deepens to 6 stages; the leader CTA issues the pair MMAs and
+// multicasts its commits to both CTAs' barriers; both CTAs' TMA loads complete on the leader's
+// full barrier; both epilogues drain their own TMEM half and arrive on the leader's TMEM-empty
+// barrier.  Unit = (expert, token tile, 256-row pair tile).
+// ------------------------------------------------------------------------------------------
+constexpr int kPStages = 6;
+constexpr int kPBRows = 16;                                   // token rows per TMA box (2 KB)
+constexpr int kPBBoxBytes = kPBRows * kBK * 2;
+constexpr int kPStageBytes = kATileBytes + (kBNMax / 2) * kBK * 2;  // 16 KB A + <= 16 KB half-B
+constexpr int kPairSmem = kPStages * kPStageBytes + 64 * kXStride * 4 + 1024 + 256;
+
+template <bool GATED>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const int* __restrict__ offsets, int E, int MT, int K, int rows_per_expert, int half_rows,
+                     __nv_bfloat16* __restrict__ out, int ldo) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* tiles = smem;
+  float* xbuf = reinterpret_cast<float*>(smem + kPStages * kPStageBytes);
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(xbuf + 64 * kXStride);
+  uint64_t* empty_bar = full_bar + kPStages;
+  uint64_t* tfull_bar = empty_bar + kPStages;
+  uint64_t* tempty_bar = tfull_bar + kAccStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + kAccStages);
+  __shared__ int s_prefix[kMaxExperts + 1];
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  constexpr int kRowsPerCta = GATED ? kBM / 2 : kBM;  // output features per CTA per unit
+
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int e = 0; e < E; ++e) {
+      s_prefix[e] = acc;
+      const int cnt = offsets[e + 1] - offsets[e];
+      acc += ((cnt + kBNMax - 1) / kBNMax) * MT;
+    }
+    s_prefix[E] = acc;
+  }
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+    for (int s = 0; s < kPStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < kAccStages; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 2 * 128);  // both CTAs' epilogue threads (used on the leader)
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc_pair<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int total = s_prefix[E];
+  UnitSched sched{s_prefix, E, MT};
+  const int KB = K / kBK;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+
+  if (warp == 0) {
+    // ------------------------------ TMA producer (both CTAs) ------------------------------
+    if (elect_one()) {
+      const uint64_t pol_w = policy_evict_first();
+      const uint64_t pol_x = policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = pair; u < total; u += npairs) {
+        int e, nt, mt, tok0, n;
+        sched.decode(u, offsets, e, nt, mt, tok0, n);
+        const int N = (n + 31) & ~31;
+        const int half = N / 2;
+        const int nb = half / kPBRows;
+        const uint32_t bytes = 2u * (kATileBytes + nb * kPBBoxBytes);
+        const int arow0 = e * rows_per_expert + mt * 2 * kRowsPerCta + rank * kRowsPerCta;
+        const int trow0 = tok0 + rank * half;
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          if (leader) mbar_arrive_expect_tx(&full_bar[stage], bytes);
+          uint8_t* st = tiles + stage * kPStageBytes;
+          if (GATED) {
+            tma_load_2d_pair(st, &tmA, &full_bar[stage], kb * kBK, arow0, pol_w);
+            tma_load_2d_pair(st + kAHalfBytes, &tmA, &full_bar[stage], kb * kBK, arow0 + half_rows, pol_w);
+          } else {
+            tma_load_2d_pair(st, &tmA, &full_bar[stage], kb * kBK, arow0, pol_w);
+          }
+          uint8_t* bt = st + kATileBytes;
+          for (int j = 0; j < nb; ++j)
+            tma_load_2d_pair(bt + j * kPBBoxBytes, &tmB, &full_bar[stage], kb * kBK, trow0 + j * kPBRows, pol_x);
+          if (++stage == kPStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------ MMA issuer (leader only) ------------------------------
+    if (leader && elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int u = pair; u < total; u += npairs) {
+        int e, nt, mt, tok0, n;
+        sched.decode(u, offsets, e, nt, mt, tok0, n);
+        const uint32_t N = (uint32_t)((n + 31) & ~31);
+        const uint32_t idesc = make_idesc_bf16(2 * kBM, N);
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d0 = tmem_base + acc * kBNMax;
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t st = smem_u32(tiles + stage * kPStageBytes);
+          const uint64_t a0 = make_sdesc_sw128(st);
+          const uint64_t b0 = make_sdesc_sw128(st + kATileBytes);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k)
+            umma_bf16_pair(d0, a0 + 2 * k, b0 + 2 * k, idesc, (kb | k) ? 1u : 0u);
+          umma_commit_pair(&empty_bar[stage], 0x3);
+          if (++stage == kPStages) { stage = 0; phase ^= 1; }
+        }
+        umma_commit_pair(&tfull_bar[acc], 0x3);
+        if (++acc == kAccStages) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else {
+    // ------------------------------ epilogue (warps 2..5, both CTAs) ------------------------------
+    const uint32_t q = warp & 3;
+    const int row = q * 32 + lane;
+    const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty_bar[0]), 0);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int u = pair; u < total; u += npairs) {
+      int e, nt, mt, tok0, n;
+      sched.decode(u, offsets, e, nt, mt, tok0, n);
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t tl = tmem_base + ((q * 32) << 16) + acc * kBNMax;
+      const int col0 = mt * 2 * kRowsPerCta + rank * kRowsPerCta;
+      if (GATED) {
+        const bool is_up = q >= 2;
+        const int f = row & 63;
+        __nv_bfloat16* ocol = out + (size_t)tok0 * ldo + col0 + f;
+        for (int c0 = 0; c0 < n; c0 += 32) {
+          uint32_t v[32];
+          tmem_ld32(tl + c0, v);
+          tmem_ld_wait();
+          if (is_up) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) xbuf[f * kXStride + j] = bf16_round(__uint_as_float(v[j]));
+          }
+          epi_bar();
+          if (!is_up) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              if (c0 + j < n) {
+                const float gv = bf16_round(__uint_as_float(v[j]));
+                const float sv = bf16_round(gv / (1.0f + expf(-gv)));
+                ocol[(size_t)(c0 + j) * ldo] = __float2bfloat16_rn(sv * xbuf[f * kXStride + j]);
+              }
+            }
+          }
+          epi_bar();
+        }
+      } else {
+        __nv_bfloat16* ocol = out + (size_t)tok0 * ldo + col0 + row;
+        for (int c0 = 0; c0 < n; c0 += 32) {
+          uint32_t v[32];
+          tmem_ld32(tl + c0, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (c0 + j < n) ocol[(size_t)(c0 + j) * ldo] = __float2bfloat16_rn(__uint_as_float(v[j]));
+        }
+      }
+      tc_fence_before();
+      mbar_arrive_cluster(tempty_leader0 + acc * 8);
+      if (++acc == kAccStages) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 1) tmem_dealloc_pair<512>(tmem_base);
+}
+
 }  // namespace mgb
 
 // ------------------------------------------------------------------------------------------
 // Host side
 // ------------------------------------------------------------------------------------------
 namespace {
+bool use_pair_kernel() {
+  static const bool v = [] {
+    const char* e = getenv("MGB_GEMM_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
+// rows_per_unit: weight rows one CTA covers per unit (64 gated / 128 down); the pair kernel
+// covers twice that per unit, so MT is given for the single-CTA tiling and halved here.
 template <bool GATED>
 int launch_moe_gemm(const void* w, int w_rows_total, const void* act, int act_rows, const int* offsets, int E,
                     int MT, int K, int rows_per_expert, int half_rows, void* out, int ldo, cudaStream_t stream) {
+  const bool pair = use_pair_kernel() && MT % 2 == 0 && (mgb_host::num_sms() & ~1) >= 2;
   CUtensorMap tmA, tmB;
   if (mgb_host::encode_tmap_2d_bf16(&tmA, w, K, w_rows_total, (uint64_t)K * 2, mgb::kBK,
                                     GATED ? mgb::kBM / 2 : mgb::kBM) != CUDA_SUCCESS)
     return MGB_ECUDA;
-  if (mgb_host::encode_tmap_2d_bf16(&tmB, act, K, act_rows, (uint64_t)K * 2, mgb::kBK, mgb::kBRows) != CUDA_SUCCESS)
+  if (mgb_host::encode_tmap_2d_bf16(&tmB, act, K, act_rows, (uint64_t)K * 2, mgb::kBK,
+                                    pair ? mgb::kPBRows : mgb::kBRows) != CUDA_SUCCESS)
     return MGB_ECUDA;
+  if (pair) {
+    static bool attr_p = false;
+    if (!attr_p) {
+      if (cudaFuncSetAttribute(mgb::moe_gemm_pair_kernel<GATED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               mgb::kPairSmem) != cudaSuccess)
+        return MGB_ECUDA;
+      attr_p = true;
+    }
+    const int grid = mgb_host::num_sms() & ~1;
+    mgb::moe_gemm_pair_kernel<GATED><<<grid, 192, mgb::kPairSmem, stream>>>(
+        tmA, tmB, offsets, E, MT / 2, K, rows_per_expert, half_rows, reinterpret_cast<__nv_bfloat16*>(out), ldo);
+    return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
+  }
   static bool attr_set = false;
   if (!attr_set) {
     if (cudaFuncSetAttribute(mgb::moe_gemm_kernel<GATED>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -77,8 +77,13 @@ __global__ void __launch_bounds__(kRouterThreads) router_topk_kernel(RouterArgs 
 
   // ---------------- phase 1: logits ----------------
   if (a.logits_in) {
-    for (int i = threadIdx.x; i < ntok * E; i += blockDim.x)
-      s_logit[(i / E) * kMaxE + (i % E)] = a.logits_in[(size_t)(t0 + i / E) * E + (i % E)];
+    // given fp32 logits (e.g. a cuBLAS bf16 GEMM with fp32 output); Mixtral's router linear is a
+    // bf16 GEMM (modeling_mixtral.py:111), i.e. the fp32 accumulator rounded once to bf16
+    for (int t = warp; t < ntok; t += kRouterThreads / 32)
+      for (int e = lane; e < E; e += 32) {
+        const float v = a.logits_in[(size_t)(t0 + t) * E + e];
+        s_logit[t * kMaxE + e] = (a.mode == 0) ? bf16_round(v) : v;
+      }
   } else {
     // stage the CTA's (contiguous) token rows in smem with one bulk copy (TMA engine)
     const int vec_per_row = d / 8;
@@ -97,15 +102,18 @@ __global__ void __launch_bounds__(kRouterThreads) router_topk_kernel(RouterArgs 
 #pragma unroll
       for (int t = 0; t < kRouterTPB; ++t) acc[t] = 0.f;
       const uint4* wrow = reinterpret_cast<const uint4*>(a.wg + (size_t)e * d);
-      // the warp's whole gate row (<= 24 x 16 B per lane) is requested before any use
-      constexpr int kWV = 24;
+      // gate row in groups of 8 x 16 B per lane, all loads of a group in flight together; the
+      // outer loop stays rolled to keep the kernel's code small (I-cache)
+      constexpr int kWV = 8;
+#pragma unroll 1
+      for (int i0 = 0; i0 < vec_per_row; i0 += 32 * kWV) {
       uint4 wreg[kWV];
 #pragma unroll
       for (int i = 0; i < kWV; ++i)
-        if (lane + 32 * i < vec_per_row) wreg[i] = __ldg(wrow + lane + 32 * i);
+        if (i0 + lane + 32 * i < vec_per_row) wreg[i] = __ldg(wrow + i0 + lane + 32 * i);
 #pragma unroll
       for (int i = 0; i < kWV; ++i) {
-        const int c = lane + 32 * i;
+        const int c = i0 + lane + 32 * i;
         if (c >= vec_per_row) break;
         const uint4 w = wreg[i];
         const float w0 = bf16lo(w.x), w1 = bf16hi(w.x), w2 = bf16lo(w.y), w3 = bf16hi(w.y);
@@ -122,6 +130,7 @@ __global__ void __launch_bounds__(kRouterThreads) router_topk_kernel(RouterArgs 
             acc[t] = s;
           }
         }
+      }
       }
 #pragma unroll
       for (int t = 0; t < kRouterTPB; ++t) {
@@ -477,7 +486,7 @@ int mgb_router_topk(const void* x, const void* w_gate, const float* logits_in, i
                     void* stream) {
   if (T < 1 || E < 1 || E > mgb::kMaxE || k < 1 || k > mgb::kMaxK || k > E || mode < 0 || mode > 2)
     return MGB_EINVAL;
-  if (!logits_in && (d % 8 || d < 8 || d > 8 * 32 * 24)) return MGB_EINVAL;  // d <= 6144
+  if (!logits_in && (d % 8 || d < 8)) return MGB_EINVAL;
   if (mode == 2 && (n_group < 1 || n_group > 32 || E % n_group || topk_group < 1 || topk_group > n_group ||
                     topk_group * (E / n_group) < k))
     return MGB_EINVAL;

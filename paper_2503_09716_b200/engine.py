@@ -180,8 +180,10 @@ class Engine:
             if a.q_lora_rank:
                 self.mb.update(q_a=torch.zeros(B, a.q_lora_rank, **bf), q_an=torch.zeros(B, a.q_lora_rank, **bf))
             fs = a.moe_ffn * a.n_shared
-            self.mb.update(sh_h=torch.zeros(B, fs, **bf), de_h=torch.zeros(B, max(a.dense_ffn, 8), **bf),
-                           sh_out=torch.zeros(B, d, **bf))
+            self.mb.update(sh_h=torch.zeros(B, fs, **bf), sh_gu=torch.zeros(B, 2 * fs, **bf),
+                           de_h=torch.zeros(B, max(a.dense_ffn, 8), **bf),
+                           de_gu=torch.zeros(B, 2 * max(a.dense_ffn, 8), **bf), sh_out=torch.zeros(B, d, **bf),
+                           logits_r=torch.zeros(B, a.n_experts, dtype=torch.float32, device=device))
             qkv_cols, attn_cols = 8, 8  # unused for MLA
         else:
             hd = a.head_dim
@@ -196,6 +198,8 @@ class Engine:
         self.out_tokens = torch.zeros(B, max(1, self.max_ctx), dtype=torch.int64, device=device)
         self.graph: torch.cuda.CUDAGraph | None = None
         self.debug_taps: dict | None = None
+        self.router_logits = "cublas"  # or "fused": gate GEMV inside mgb_router_topk
+        self.logits_r = torch.zeros(B, a.n_experts, dtype=torch.float32, device=device)
         self.stream = torch.cuda.Stream(device=device)
         self.h2d = torch.cuda.Stream(device=device) if self.offload else None
         self._fork, self._join = torch.cuda.Event(), torch.cuda.Event()
@@ -331,8 +335,11 @@ class Engine:
             ops.add_rmsnorm(b.x, W["ln2"], a.rms_eps, b.h, delta=b.o, x_out=b.x)
         elif j.kind == "router":
             if l >= a.first_k_dense:
-                ops.router_topk(b.h, W["router"], self.rws, a.top_k, a.router_mode, a.routed_scaling, a.n_group,
-                                a.topk_group)
+                # fp32 router logits (HF: F.linear(x.float(), W.float()), modeling_deepseek_v2.py:125) as a
+                # bf16 tensor-core GEMM with fp32 output (exact products, fp32 accumulation)
+                m["logits_r"].copy_(torch.mm(b.h, W["router"].t(), out_dtype=torch.float32))
+                ops.router_topk(None, None, self.rws, a.top_k, a.router_mode, a.routed_scaling, a.n_group,
+                                a.topk_group, logits_in=m["logits_r"])
                 ops.permute(b.h, self.rws, b.x_perm)
                 if self.debug_taps is not None:
                     self.debug_taps.update(h2=b.h.clone(), topk_idx=self.rws.topk_idx.clone())
@@ -341,17 +348,20 @@ class Engine:
             first, last = j.id == self.first_expert_job[l], j.id == self.last_expert_job[l]
             if l < a.first_k_dense:
                 # dense MLP of the first layers (DeepseekV2MLP) on the same grouped kernel, E = 1
-                if first:
-                    ops.moe_gemm_gate_up(W["dense_gate_up"], b.h, m["offsets_all"], m["de_h"])
-                    ops.moe_gemm_down(W["dense_down"], m["de_h"], m["offsets_all"], b.o)
+                if first:  # dense GEMMs over all tokens: cuBLAS + fused SiLU*up
+                    F = a.dense_ffn
+                    torch.mm(b.h, W["dense_gate_up"][0].t(), out=m["de_gu"][:, :2 * F])
+                    ops.silu_mul(m["de_gu"][:, :2 * F], m["de_h"][:, :F])
+                    torch.mm(m["de_h"][:, :F], W["dense_down"][0].t(), out=b.o)
                     ops.add_rmsnorm(b.x, nxt, a.rms_eps, b.h, delta=b.o, x_out=b.x)
                 return
             if first:
                 ops.moe_gemm_gate_up(W["w_gate_up"], b.x_perm, self.rws.offsets, b.h_ffn)
                 ops.moe_gemm_down(W["w_down"], b.h_ffn, self.rws.offsets, b.y_perm)
-                # shared experts on every token (DeepseekV2Moe.shared_experts)
-                ops.moe_gemm_gate_up(W["sh_gate_up"], b.h, m["offsets_all"], m["sh_h"])
-                ops.moe_gemm_down(W["sh_down"], m["sh_h"], m["offsets_all"], m["sh_out"])
+                # shared experts on every token (DeepseekV2Moe.shared_experts): dense -> cuBLAS
+                torch.mm(b.h, W["sh_gate_up"][0].t(), out=m["sh_gu"])
+                ops.silu_mul(m["sh_gu"], m["sh_h"])
+                torch.mm(m["sh_h"], W["sh_down"][0].t(), out=m["sh_out"])
             if last:
                 ops.unpermute_combine(b.y_perm, self.rws, b.x, self.B, residual=b.x, shared_out=m["sh_out"],
                                       norm_w=nxt, eps=a.rms_eps, norm_out=b.h)
@@ -387,8 +397,15 @@ class Engine:
                 torch.mm(b.attn, W["wo"].t(), out=b.o)
                 ops.add_rmsnorm(b.x, W["ln2"], a.rms_eps, b.h, delta=b.o, x_out=b.x)
             elif j.kind == "router":
-                ops.router_topk(b.h, W["router"], self.rws, a.top_k, a.router_mode, a.routed_scaling, a.n_group,
-                                a.topk_group)
+                if self.router_logits == "cublas":
+                    # gate GEMM on the tensor cores with fp32 output; the router kernel rounds it to
+                    # bf16 exactly as HF's bf16 F.linear does (modeling_mixtral.py:111)
+                    self.logits_r.copy_(torch.mm(b.h, W["router"].t(), out_dtype=torch.float32))
+                    ops.router_topk(None, None, self.rws, a.top_k, a.router_mode, a.routed_scaling, a.n_group,
+                                    a.topk_group, logits_in=self.logits_r)
+                else:
+                    ops.router_topk(b.h, W["router"], self.rws, a.top_k, a.router_mode, a.routed_scaling,
+                                    a.n_group, a.topk_group)
                 ops.permute(b.h, self.rws, b.x_perm)
                 if self.debug_taps is not None:  # eager-only parity hook
                     self.debug_taps.update(h2=b.h.clone(), topk_idx=self.rws.topk_idx.clone(), attn=b.attn.clone())

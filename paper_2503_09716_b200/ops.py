@@ -104,6 +104,12 @@ def decode_attn_gqa(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tenso
              _p(seq_lens), B, Hq, Hkv, hd, scale, _p(out), _s())
 
 
+def silu_mul(gate_up: torch.Tensor, h: torch.Tensor) -> None:
+    T, F = h.shape
+    assert gate_up.shape == (T, 2 * F) and gate_up.is_contiguous() and h.is_contiguous()
+    nat.call("mgb_silu_mul", _p(gate_up), T, F, _p(h), _s())
+
+
 def embed(ids: torch.Tensor, table: torch.Tensor, out: torch.Tensor) -> None:
     nat.call("mgb_embed", _p(ids), _p(table), ids.shape[0], table.shape[1], _p(out), _s())
 
