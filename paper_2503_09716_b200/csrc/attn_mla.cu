@@ -54,8 +54,10 @@ struct MlaCfg {
   static constexpr int kPStride = kMlaPage * 2 + 16;   // padded P row (bytes)
   static constexpr int DPW = R / kMlaConsumers;         // latent dims of O per warp
   static constexpr int NT = DPW / 8;                    // PV n-tiles per warp
-  static constexpr size_t kSmem = (size_t)kMlaStages * kPageBytes + 16 * kQStride + 2 * 16 * kMlaPage * 4 +
-                                  2 * 16 * kPStride + 16 * 4 * 4 + 64;
+  static constexpr int KST = D / 16;                   // k-steps of S = Q C^T
+  static constexpr int KPW = (KST + kMlaConsumers - 1) / kMlaConsumers;  // k-steps per warp (K split)
+  static constexpr size_t kSmem = (size_t)kMlaStages * kPageBytes + 16 * kQStride +
+                                  kMlaConsumers * 16 * kMlaPage * 4 + 2 * 16 * kPStride + 16 * 4 * 4 + 64;
   static_assert(R % (8 * kMlaConsumers * 2) == 0 && D % 32 == 0, "MLA shape");
 };
 
@@ -70,8 +72,8 @@ decode_attn_mla_kernel(const __nv_bfloat16* __restrict__ q_lat,  // [H, B, R]
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* ring = smem;
   uint8_t* q_s = smem + kMlaStages * C::kPageBytes;                                   // [16][kQStride]
-  float* s_s = reinterpret_cast<float*>(q_s + 16 * C::kQStride);                      // [2][16][32]
-  uint8_t* p_s = reinterpret_cast<uint8_t*>(s_s + 2 * 16 * kMlaPage);                 // [2][16][kPStride]
+  float* s_s = reinterpret_cast<float*>(q_s + 16 * C::kQStride);                      // [warp][16][32] partial S
+  uint8_t* p_s = reinterpret_cast<uint8_t*>(s_s + kMlaConsumers * 16 * kMlaPage);     // [2][16][kPStride]
   float* m_s = reinterpret_cast<float*>(p_s + 2 * 16 * C::kPStride);                 // [16]
   float* l_s = m_s + 16;
   float* a_s = l_s + 16;                                                               // alpha [16]
@@ -141,33 +143,51 @@ decode_attn_mla_kernel(const __nv_bfloat16* __restrict__ q_lat,  // [H, B, R]
     cons_bar();
 
     const uint32_t qbase = smem_u32(q_s);
+    // this warp's K-split share of Q (k-steps warp, warp+4, ...) lives in registers for the item
+    uint32_t qa[C::KPW][4];
+    {
+      const int mi = lane >> 3, r = lane & 7;
+#pragma unroll
+      for (int kk = 0; kk < C::KPW; ++kk) {
+        const int ks = warp + kMlaConsumers * kk;
+        if (ks < C::KST)
+          ldsm4(qbase + (uint32_t)(((mi & 1) * 8 + r) * C::kQStride + (ks * 16 + (mi >> 1) * 8) * 2), qa[kk][0],
+                qa[kk][1], qa[kk][2], qa[kk][3]);
+      }
+    }
     for (int p = 0; p < np; ++p) {
       mbar_wait(&full[stage], phase);
       const uint32_t cbase = smem_u32(ring + stage * C::kPageBytes);
-      float* S = s_s + sbuf * 16 * kMlaPage;
+      float* S = s_s;
       uint8_t* P = p_s + sbuf * 16 * C::kPStride;
-      // ---- S[16 x 8] for this warp's tokens 8w..8w+7 over all D dims ----
+      // ---- partial S[16 x 32] over this warp's k-steps (4 independent n-tile accumulators) ----
       {
-        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        float acc[4][4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
         const int mi = lane >> 3, r = lane & 7;
-#pragma unroll 4
-        for (int ks = 0; ks < C::D / 16; ks += 2) {
-          // B fragments for two k-steps: chunks 2ks .. 2ks+3, tokens 8w + r
-          uint32_t b0, b1, b2, b3;
-          ldsm4(cbase + (uint32_t)(((2 * ks + mi) * kMlaPage + warp * 8 + r) * 16), b0, b1, b2, b3);
-          // A fragments (Q rows 0-15) for k-steps ks, ks+1
-          uint32_t a0, a1, a2, a3, c0, c1, c2, c3;
-          const int qrow = (mi & 1) * 8 + r, qcol = ks * 16 + (mi >> 1) * 8;
-          ldsm4(qbase + (uint32_t)(qrow * C::kQStride + qcol * 2), a0, a1, a2, a3);
-          ldsm4(qbase + (uint32_t)(qrow * C::kQStride + (qcol + 16) * 2), c0, c1, c2, c3);
-          mma16816(acc, a0, a1, a2, a3, b0, b1);
-          mma16816(acc, c0, c1, c2, c3, b2, b3);
+#pragma unroll
+        for (int kk = 0; kk < C::KPW; ++kk) {
+          const int ks = warp + kMlaConsumers * kk;
+          if (ks < C::KST) {
+            // matrices (chunk 2ks, tok 0-7), (chunk 2ks+1, tok 0-7), (chunk 2ks, tok 8-15), (chunk 2ks+1, tok 8-15)
+            uint32_t b0, b1, b2, b3, b4, b5, b6, b7;
+            const uint32_t kaddr = cbase + (uint32_t)(((2 * ks + (mi & 1)) * kMlaPage + (mi >> 1) * 8 + r) * 16);
+            ldsm4(kaddr, b0, b1, b2, b3);
+            ldsm4(kaddr + 16 * 16, b4, b5, b6, b7);  // tokens 16..31
+            mma16816(acc[0], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b0, b1);
+            mma16816(acc[1], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b2, b3);
+            mma16816(acc[2], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b4, b5);
+            mma16816(acc[3], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b6, b7);
+          }
         }
-        const int col = warp * 8 + 2 * t;
-        S[g * kMlaPage + col] = acc[0] * scale_log2;
-        S[g * kMlaPage + col + 1] = acc[1] * scale_log2;
-        S[(g + 8) * kMlaPage + col] = acc[2] * scale_log2;
-        S[(g + 8) * kMlaPage + col + 1] = acc[3] * scale_log2;
+        float* Sw = S + warp * 16 * kMlaPage;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int col = j * 8 + 2 * t;
+          *reinterpret_cast<float2*>(Sw + g * kMlaPage + col) = make_float2(acc[j][0], acc[j][1]);
+          *reinterpret_cast<float2*>(Sw + (g + 8) * kMlaPage + col) = make_float2(acc[j][2], acc[j][3]);
+        }
       }
       cons_bar();
       // ---- online softmax: warp w owns rows 4w..4w+3, lane = token ----
@@ -176,7 +196,13 @@ decode_attn_mla_kernel(const __nv_bfloat16* __restrict__ q_lat,  // [H, B, R]
 #pragma unroll
         for (int rr = 0; rr < 4; ++rr) {
           const int row = warp * 4 + rr;
-          const float sv = lane < n ? S[row * kMlaPage + lane] : -INFINITY;
+          float sv = -INFINITY;
+          if (lane < n) {
+            sv = 0.f;
+#pragma unroll
+            for (int w = 0; w < kMlaConsumers; ++w) sv += S[(w * 16 + row) * kMlaPage + lane];
+            sv *= scale_log2;
+          }
           float mt = sv;
 #pragma unroll
           for (int off = 16; off > 0; off >>= 1) mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, off));
