@@ -91,10 +91,11 @@ class StepBuffers:
 
 
 class Engine:
-    """Greedy MoE decoding engine (Mixtral family, HBM-resident weights + paged KV)."""
+    """Greedy MoE decoding engine (Mixtral and DeepSeek-V2 families; HBM-resident or partly
+    host-offloaded weights, paged KV in HBM, optional expert parallelism)."""
 
     def __init__(self, arch: ModelArch | str, plan=None, *, prompt_len: int, decode_len: int, seed: int = 0,
-                 kv_policy: str = "resident", use_graph: bool = True, device: str = "cuda"):
+                 kv_policy: str = "resident", use_graph: bool = True, device: str = "cuda", ep=None):
         if not torch.cuda.is_available():
             raise RuntimeError("the B200 engine needs a CUDA device (there is no CPU fallback)")
         self.arch = get_arch(arch) if isinstance(arch, str) else arch
@@ -112,7 +113,11 @@ class Engine:
         self.workload = WorkloadSpec(prompt_len, decode_len, self.plan.B, "decode")
         self.B = B = self.plan.B
         self.device = device
-        self.use_graph = use_graph
+        # expert parallelism (ep.ExpertParallel): experts of this rank's range run locally, token
+        # rows are dispatched/combined over torch.distributed; the host-side split sizes make the
+        # EP step eager (no CUDA graph) in this build
+        self.ep = ep if (ep is not None and ep.world > 1) else None
+        self.use_graph = use_graph and self.ep is None
         # ---- job list (structure only; durations are measured, not modelled) ----
         self.schedule: Schedule = build_schedule(self.spec, b200_hardware(), _unit_latency, self.workload, self.plan,
                                                  kv_policy=kv_policy)
@@ -356,8 +361,7 @@ class Engine:
                     ops.add_rmsnorm(b.x, nxt, a.rms_eps, b.h, delta=b.o, x_out=b.x)
                 return
             if first:
-                ops.moe_gemm_gate_up(W["w_gate_up"], b.x_perm, self.rws.offsets, b.h_ffn)
-                ops.moe_gemm_down(W["w_down"], b.h_ffn, self.rws.offsets, b.y_perm)
+                self._routed_experts(W)
                 # shared experts on every token (DeepseekV2Moe.shared_experts): dense -> cuBLAS
                 torch.mm(b.h, W["sh_gate_up"][0].t(), out=m["sh_gu"])
                 ops.silu_mul(m["sh_gu"], m["sh_h"])
@@ -367,6 +371,26 @@ class Engine:
                                       norm_w=nxt, eps=a.rms_eps, norm_out=b.h)
         else:
             raise RuntimeError(f"job kind {j.kind!r} is not executable under kv_policy={self.kv_policy!r}")
+
+    def _routed_experts(self, W: dict) -> None:
+        """Grouped expert FFN over the permuted rows; with expert parallelism the rows go to the
+        experts' owner ranks and back around the local grouped GEMMs (ep.py)."""
+        b = self.buf
+        if self.ep is None:
+            ops.moe_gemm_gate_up(W["w_gate_up"], b.x_perm, self.rws.offsets, b.h_ffn)
+            ops.moe_gemm_down(W["w_down"], b.h_ffn, self.rws.offsets, b.y_perm)
+            return
+        a, ep = self.arch, self.ep
+        x_loc, offs, st = ep.dispatch(b.x_perm, self.rws.counts)
+        n = x_loc.shape[0]
+        y_loc = torch.empty(n, a.hidden, dtype=BF16, device=self.device)
+        if n > 0:
+            h = torch.empty(n, a.moe_ffn, dtype=BF16, device=self.device)
+            lo = ep.first
+            ops.moe_gemm_gate_up(W["w_gate_up"][lo:lo + ep.E_local], x_loc, offs, h)
+            ops.moe_gemm_down(W["w_down"][lo:lo + ep.E_local], h, offs, y_loc)
+        y = ep.combine(y_loc, st)
+        b.y_perm[:y.shape[0]].copy_(y)
 
     def _issue_job(self, l: int, j) -> None:
         a, b = self.arch, self.buf
@@ -417,8 +441,7 @@ class Engine:
                 first_chunk = j.label.endswith("/chunk0")
                 n_c = self.w.place.experts_per_layer[l] if self.offload else a.n_experts
                 if j.id == self.first_expert_job[l] and n_c > 0:
-                    ops.moe_gemm_gate_up(W["w_gate_up"], b.x_perm, self.rws.offsets, b.h_ffn)
-                    ops.moe_gemm_down(W["w_down"], b.h_ffn, self.rws.offsets, b.y_perm)
+                    self._routed_experts(W)
                 elif first_chunk and e >= n_c:
                     gu, dn = self.w.slot_views(self.slot_of[(l, e)])
                     offs = self.rws.offsets[e:e + 2]

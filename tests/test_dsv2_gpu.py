@@ -128,3 +128,21 @@ def test_dsv2_generate_vs_oracle(ds_weights):
     same = (o1 == ref).all(1).float().mean().item()
     print(f"DSV2 identical greedy rows: {same:.2f}")
     assert same >= 0.5
+
+
+def test_engine_expert_parallel_single_rank_path():
+    """The EP-aware engine path with a 1-rank ExpertParallel (identity exchange) equals the plain
+    engine; multi-rank dispatch/combine is covered on CPU by tests/test_ep_gloo.py."""
+    from paper_2503_09716_b200.ep import ExpertParallel
+    from paper_2503_09716_b200.configs import TINY_DSV2 as A
+    from paper_2503_09716_b200.engine import Engine
+    from paper_2503_09716_b200.planner import BatchingPlan, ModelSpec
+
+    mb = ModelSpec.from_document(A.model_spec_document()).model_bytes
+    ids = torch.randint(0, A.vocab, (8, 4), generator=torch.Generator().manual_seed(9))
+    plan = BatchingPlan(8, 4, 16, 0.0, 0, mb)
+    ref = Engine(A, plan, prompt_len=4, decode_len=3, use_graph=False).generate(ids, 3)
+    ep = ExpertParallel(A.n_experts)
+    eng = Engine(A, plan, prompt_len=4, decode_len=3, use_graph=False, ep=ep)
+    eng.ep = ep  # force the EP code path even at world size 1
+    assert torch.equal(eng.generate(ids, 3), ref)
