@@ -50,15 +50,47 @@ struct UnitSched {
     }
     e = lo;
     int local = u - s_prefix[e];
-    nt = local / MT;
-    mt = local - nt * MT;
     const int beg = offs[e], cnt = offs[e + 1] - beg;
+    // token tiles fastest: the (up to ceil(cnt/256)) units that share one weight tile run on
+    // neighbouring CTAs at the same time, so the tile is read from HBM once and hit in L2 after
+    const int NT = (cnt + kBNMax - 1) / kBNMax;
+    mt = local / NT;
+    nt = local - mt * NT;
     tok0 = beg + nt * kBNMax;
     n = min(kBNMax, cnt - nt * kBNMax);
   }
 };
 
 MGB_DEVINL void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+// One 32-token chunk of the gated epilogue.  TMEM lanes 0-63 hold gate, 64-127 up for the same 64
+// features; the gate warps finish tokens 0-15 of the chunk and the up warps tokens 16-31, each
+// taking the partner half through shared memory, so all four epilogue warps do the SiLU*up work.
+// h = bf16(bf16(silu(bf16(gate))) * bf16(up)) (HF MixtralExperts, modeling_mixtral.py:91-93).
+MGB_DEVINL void gated_chunk(uint32_t tl, int c0, int n, bool is_up, int f, float* xbuf, __nv_bfloat16* ocol,
+                            int ldo) {
+  uint32_t v[32];
+  tmem_ld32(tl + c0, v);
+  tmem_ld_wait();
+  float* xr = xbuf + f * kXStride;
+  if (is_up) {  // hand over up for tokens 0-15, finish tokens 16-31 (register indices stay static)
+#pragma unroll
+    for (int j = 0; j < 16; ++j) xr[j] = bf16_round(__uint_as_float(v[j]));
+  } else {      // hand over gate for tokens 16-31, finish tokens 0-15
+#pragma unroll
+    for (int j = 0; j < 16; ++j) xr[16 + j] = bf16_round(__uint_as_float(v[16 + j]));
+  }
+  epi_bar();
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int c = c0 + (is_up ? 16 : 0) + j;
+    const float mine = bf16_round(__uint_as_float(is_up ? v[16 + j] : v[j]));
+    const float other = is_up ? xr[16 + j] : xr[j];
+    const float gv = is_up ? other : mine, uv = is_up ? mine : other;
+    if (c < n) ocol[(size_t)c * ldo] = __float2bfloat16_rn(bf16_round(gv / (1.0f + expf(-gv))) * uv);
+  }
+  epi_bar();
+}
 
 template <bool GATED>
 __global__ void __launch_bounds__(192, 1)
@@ -190,27 +222,7 @@ moe_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const bool is_up = q >= 2;
         const int f = row & 63;
         __nv_bfloat16* ocol = out + (size_t)tok0 * ldo + mt * kRowsPerUnit + f;
-        for (int c0 = 0; c0 < n; c0 += 32) {
-          uint32_t v[32];
-          tmem_ld32(tl + c0, v);
-          tmem_ld_wait();
-          if (is_up) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) xbuf[f * kXStride + j] = bf16_round(__uint_as_float(v[j]));
-          }
-          epi_bar();
-          if (!is_up) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              if (c0 + j < n) {
-                const float gv = bf16_round(__uint_as_float(v[j]));
-                const float sv = bf16_round(gv / (1.0f + expf(-gv)));
-                ocol[(size_t)(c0 + j) * ldo] = __float2bfloat16_rn(sv * xbuf[f * kXStride + j]);
-              }
-            }
-          }
-          epi_bar();
-        }
+        for (int c0 = 0; c0 < n; c0 += 32) gated_chunk(tl, c0, n, is_up, f, xbuf, ocol, ldo);
       } else {
         __nv_bfloat16* ocol = out + (size_t)tok0 * ldo + mt * kRowsPerUnit + row;
         for (int c0 = 0; c0 < n; c0 += 32) {
@@ -383,27 +395,7 @@ moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
         const bool is_up = q >= 2;
         const int f = row & 63;
         __nv_bfloat16* ocol = out + (size_t)tok0 * ldo + col0 + f;
-        for (int c0 = 0; c0 < n; c0 += 32) {
-          uint32_t v[32];
-          tmem_ld32(tl + c0, v);
-          tmem_ld_wait();
-          if (is_up) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) xbuf[f * kXStride + j] = bf16_round(__uint_as_float(v[j]));
-          }
-          epi_bar();
-          if (!is_up) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              if (c0 + j < n) {
-                const float gv = bf16_round(__uint_as_float(v[j]));
-                const float sv = bf16_round(gv / (1.0f + expf(-gv)));
-                ocol[(size_t)(c0 + j) * ldo] = __float2bfloat16_rn(sv * xbuf[f * kXStride + j]);
-              }
-            }
-          }
-          epi_bar();
-        }
+        for (int c0 = 0; c0 < n; c0 += 32) gated_chunk(tl, c0, n, is_up, f, xbuf, ocol, ldo);
       } else {
         __nv_bfloat16* ocol = out + (size_t)tok0 * ldo + col0 + row;
         for (int c0 = 0; c0 < n; c0 += 32) {
