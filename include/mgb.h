@@ -70,9 +70,12 @@ int mgb_decode_attn_gqa(const void* q, const void* k_cache, const void* v_cache,
 
 /* ---- ATTN_MECH_GPU for MLA models (DeepSeek-V2; model_catalog.py:242-295 prices it) -------
  * Absorbed latent attention: q_lat [H,B,R], q_pe [B,H,RP], latent pages of mgb_mla_page_size()
- * tokens, chunk-major [(R+RP)/8][page][8] -> o_lat [H,B,R].  mgb_mla_append writes the new
- * token's normed latent + RoPE'd k_pe, RoPE's q_pe and re-lays q_nope as [H,B,NOPE]. */
+ * tokens and mgb_mla_page_elems(R, RP) bf16 elements, laid out as 64-dim blocks
+ * [ceil((R+RP)/64)][page][64] with the 16-byte chunks of each token row 128B-swizzled (chunk c
+ * of token t stored at c ^ (t & 7)) -> o_lat [H,B,R].  mgb_mla_append writes the new token's
+ * normed latent + RoPE'd k_pe, RoPE's q_pe and re-lays q_nope as [H,B,NOPE]. */
 int mgb_mla_page_size(void);
+int mgb_mla_page_elems(int R, int RP);
 int mgb_decode_attn_mla(const void* q_lat, const void* q_pe, const void* cache, const int* block_table, int max_pages,
                         const int* seq_lens, int B, int H, int R, int RP, float scale, void* o_lat, void* stream);
 int mgb_mla_append(const void* q, const void* ckv, const void* norm_w, float eps, int B, int H, int R, int RP, int NOPE,

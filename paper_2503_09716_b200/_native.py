@@ -45,13 +45,14 @@ SIGNATURES: dict[str, list] = {
     "mgb_fill_uniform_bf16": [P, L, ctypes.c_uint64, ctypes.c_uint64, F, F, I, P],
     # attn_mla.cu
     "mgb_mla_page_size": [],
+    "mgb_mla_page_elems": [I, I],
     "mgb_decode_attn_mla": [P, P, P, P, I, P, I, I, I, I, F, P, P],
     "mgb_mla_append": [P, P, P, F, I, I, I, I, I, P, P, P, P, I, P, P, P, P, P],
 }
 
 # entry points that return a value rather than a status
-VALUE_FNS = {"mgb_abi_version", "mgb_num_sms", "mgb_kv_page_size", "mgb_mla_page_size", "mgb_router_num_blocks",
-             "mgb_router_tokens_per_block"}
+VALUE_FNS = {"mgb_abi_version", "mgb_num_sms", "mgb_kv_page_size", "mgb_mla_page_size", "mgb_mla_page_elems",
+             "mgb_router_num_blocks", "mgb_router_tokens_per_block"}
 
 STATUS = {0: "ok", -1: "invalid argument", -2: "capacity exceeded", -3: "CUDA error"}
 

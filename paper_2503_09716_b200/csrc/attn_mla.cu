@@ -9,264 +9,384 @@
 // the cache holds only the 576-wide latent row per token (1,152 B instead of 2*H*... per head).
 // Equal to HF within bf16 tolerance, not bit-exact (different rounding points).
 //
-// Latent cache: pages of kMlaPage = 32 tokens, chunk-major [(R+r)/8][32 tok][8] bf16, so every
-// ldmatrix / ldmatrix.trans is conflict free and a page is one contiguous bulk copy.
-// Persistent kernel, 2 CTAs per SM: warp 4 streams pages through a 2-stage ring
-// (cp.async.bulk + mbarrier); warps 0-3 consume.  Per page: each warp computes S = Q C^T for 8
-// tokens x 16 heads on the tensor cores (Q in padded smem, ldmatrix A fragments), the four warps
-// run one online-softmax pass over the 32 tokens in smem, then each warp accumulates O for its
-// quarter of the latent dims with P V on the tensor cores.  A work item is (sequence, 16-head group).
+// Latent cache: pages of kMlaPage = 56 tokens stored exactly as the tensor cores read them from
+// shared memory: 64-dim blocks [(R+r)/64][56 tok][128 B], each 128-byte token row holding its 8
+// 16-byte chunks in 128B-swizzled order (chunk c of token t at position c ^ (t & 7)).  That one
+// layout is, without any re-staging, both operands a page is used as:
+//   S^T[64 tok, 16 heads] = C[64 tok, R+r] . Q^T          (A = page, K-major, SWIZZLE_128B)
+//   O^T[R, 16 heads]     += C[:, :R]^T [R, 64 tok] . P^T  (A = page, MN-major, SWIZZLE_128B)
+// The MMAs are 64 tokens tall; rows 56-63 are "phantom" rows that alias the next 64-dim block
+// (masked to P = 0).  56-token pages let three stages (189 KB) fit in shared memory, which keeps
+// enough bytes in flight per SM while a page is held for S^T -> softmax -> P.V.  The swizzle keeps
+// the tensor cores' shared-memory reads conflict free; R + r is padded to a multiple of 64 in the
+// page, and the padding is never read.
+// so a page is one contiguous cp.async.bulk and both GEMMs run on tcgen05 with fp32 accumulators in
+// TMEM ("swap-AB": tokens / latent dims fill the MMA M side, the 16 heads of a work item are N).
+//
+// Persistent kernel, one CTA per SM, 6 warps:
+//   warp 4  producer: streams the pages of every work item through a 3-stage smem ring, and Q
+//   warp 5  MMA issuer (one elected lane): S^T of each page and P.V of each softmaxed page, issued
+//           as each becomes ready (double-buffered TMEM accumulators)
+//   warps 0-3 softmax + correction: TMEM -> registers (lane = token), per-head online softmax with a
+//           warp transpose-reduction, P^T -> smem, O accumulated in registers (lane = latent dim)
+// A work item is (sequence, 16-head group); heads >= H are zero rows of Q and never stored.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace mgb {
 
-constexpr int kMlaPage = 32;
-constexpr int kMlaStages = 2;
-constexpr int kMlaConsumers = 4;
-constexpr int kMlaThreads = (kMlaConsumers + 1) * 32;
+constexpr int kMlaPage = 56;     // tokens per latent page (7 swizzle atoms of 8 tokens)
+constexpr int kMlaTile = 64;     // M of the S^T MMA / K of P.V: a page plus 8 phantom rows
+constexpr int kMlaStages = 3;    // pages in flight per SM (3 x 63 KB for R = 512)
+constexpr int kMlaHeads = 16;    // heads per work item = N of both MMAs
+constexpr int kMlaThreads = 192;
 
-MGB_DEVINL void ldsm4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-               : "r"(addr));
-}
-MGB_DEVINL void ldsm4t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-               : "r"(addr));
-}
-MGB_DEVINL void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
-                         uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
-}
 MGB_DEVINL void cons_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
 template <int R, int RP>  // latent width, rope width
 struct MlaCfg {
-  static constexpr int D = R + RP;                     // cached row width
-  static constexpr int NCH = D / 8;                    // 16 B chunks per row
-  static constexpr int kPageBytes = D * kMlaPage * 2;  // one page, contiguous
-  static constexpr int kQStride = D * 2 + 16;          // padded smem row (bytes) -> conflict-free ldmatrix
-  static constexpr int kPStride = kMlaPage * 2 + 16;   // padded P row (bytes)
-  static constexpr int DPW = R / kMlaConsumers;         // latent dims of O per warp
-  static constexpr int NT = DPW / 8;                    // PV n-tiles per warp
-  static constexpr int KST = D / 16;                   // k-steps of S = Q C^T
-  static constexpr int KPW = (KST + kMlaConsumers - 1) / kMlaConsumers;  // k-steps per warp (K split)
-  static constexpr size_t kSmem = (size_t)kMlaStages * kPageBytes + 16 * kQStride +
-                                  kMlaConsumers * 16 * kMlaPage * 4 + 2 * 16 * kPStride + 16 * 4 * 4 + 64;
-  static_assert(R % (8 * kMlaConsumers * 2) == 0 && D % 32 == 0, "MLA shape");
+  static constexpr int D = R + RP;                         // cached row width
+  static constexpr int NKB = (D + 63) / 64;                // 64-dim blocks per page (padded)
+  static constexpr int kBlockBytes = kMlaPage * 128;       // one 64-dim block of a page
+  static constexpr int kPageBytes = NKB * kBlockBytes;     // [NKB][56 tok][128 B swizzled]
+  static constexpr int kQBlockBytes = kMlaHeads * 128;     // one 64-dim block of Q
+  static constexpr int kQBytes = NKB * kQBlockBytes;       // [NKB][16 heads][128 B swizzled]
+  static constexpr int kChunkBytes = kMlaTile * 16;        // P^T: [2 head groups][64 tok][8 heads]
+  static constexpr int kPBytes = 2 * kMlaTile * 16;
+  static constexpr int MT = R / 128;                       // O^T M tiles of 128 latent dims
+  static constexpr int KS = D / 16;                        // k-steps of S^T
+  // Small MMAs accumulating into one TMEM tile serialise on their latency, so S^T is split over
+  // kSAcc independent partial accumulators (k-step k -> partial k % kSAcc, summed by the softmax
+  // warps) and the P.V MMAs interleave their MT independent M tiles.
+  static constexpr int kSAcc = KS % 2 == 0 ? 2 : 1;
+  static constexpr uint32_t kSCol = 0;                        // S^T: 2 buffers x kSAcc x 16 columns
+  static constexpr uint32_t kOCol = 2 * kSAcc * 16;           // O^T: 2 buffers x MT x 16 columns
+  static constexpr uint32_t kTmemCols = kOCol + 2 * MT * 16 <= 128 ? 128 : 256;
+  static_assert(kOCol + 2 * MT * 16 <= 256, "TMEM budget");
+  static constexpr int kOffQ = kMlaStages * kPageBytes;
+  static constexpr int kOffP = kOffQ + kQBytes;
+  static constexpr int kOffRed = kOffP + 2 * kPBytes;      // float [2][4][16] max + [4][16] sum
+  static constexpr int kOffBar = kOffRed + 3 * 4 * 16 * 4;
+  static constexpr size_t kSmem = kOffBar + 18 * 8 + 16;
+  static_assert(R % 128 == 0 && RP % 16 == 0 && kBlockBytes % 1024 == 0, "MLA shape");
+  static_assert(kSmem <= 227 * 1024, "MLA smem");
 };
 
+// Reduce 16 per-head values over the 16 lanes of each half-warp (max or sum); lane l ends with
+// head (l & 15).  15 shuffles instead of 64 by halving the vector at every step.
+template <bool kMax>
+MGB_DEVINL float xreduce16(float (&v)[16], int lane) {
+#pragma unroll
+  for (int o = 8; o >= 1; o >>= 1) {
+    const bool hi = lane & o;
+#pragma unroll
+    for (int i = 0; i < o; ++i) {
+      const float keep = hi ? v[i + o] : v[i];
+      const float send = hi ? v[i] : v[i + o];
+      const float got = __shfl_xor_sync(0xffffffffu, send, o);
+      v[i] = kMax ? fmaxf(keep, got) : keep + got;
+    }
+  }
+  return v[0];
+}
+
 template <int R, int RP>
-__global__ void __launch_bounds__(kMlaThreads, 2)
-decode_attn_mla_kernel(const __nv_bfloat16* __restrict__ q_lat,  // [H, B, R]
-                       const __nv_bfloat16* __restrict__ q_pe,   // [B, H, RP]
-                       const __nv_bfloat16* __restrict__ cache,  // latent pages
+__global__ void __launch_bounds__(kMlaThreads, 1)
+decode_attn_mla_kernel(const __grid_constant__ CUtensorMap tm_qlat,  // q_lat [H, B, R] as [64][H][R/64][B]
+                       const __grid_constant__ CUtensorMap tm_qpe,   // q_pe [B, H, RP] as [RP][H][B]
+                       const __nv_bfloat16* __restrict__ cache,      // latent pages
                        const int* __restrict__ block_table, int max_pages, const int* __restrict__ seq_lens,
-                       int B, int H, float scale_log2, __nv_bfloat16* __restrict__ o_lat) {  // [H, B, R]
+                       int B, int H, float scale_log2, __nv_bfloat16* __restrict__ o_lat,  // [H, B, R]
+                       int pf_dist) {
   using C = MlaCfg<R, RP>;
-  extern __shared__ __align__(128) uint8_t smem[];
-  uint8_t* ring = smem;
-  uint8_t* q_s = smem + kMlaStages * C::kPageBytes;                                   // [16][kQStride]
-  float* s_s = reinterpret_cast<float*>(q_s + 16 * C::kQStride);                      // [warp][16][32] partial S
-  uint8_t* p_s = reinterpret_cast<uint8_t*>(s_s + kMlaConsumers * 16 * kMlaPage);     // [2][16][kPStride]
-  float* m_s = reinterpret_cast<float*>(p_s + 2 * 16 * C::kPStride);                 // [16]
-  float* l_s = m_s + 16;
-  float* a_s = l_s + 16;                                                               // alpha [16]
-  uint64_t* full = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(a_s + 32) + 15) & ~uintptr_t(15));
-  uint64_t* empty = full + kMlaStages;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* pages = smem;
+  uint8_t* q_s = smem + C::kOffQ;
+  uint8_t* p_s = smem + C::kOffP;
+  float* red = reinterpret_cast<float*>(smem + C::kOffRed);  // [2][4][16]
+  float* lred = red + 2 * 4 * 16;                              // [4][16]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
+  uint64_t *full = bars, *empty = bars + 3, *qfull = bars + 6, *qempty = bars + 7, *sfull = bars + 8,
+           *sempty = bars + 10, *pfull = bars + 12, *ofull = bars + 14, *oempty = bars + 16;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_hg = (H + 15) / 16;
+  const int n_hg = (H + kMlaHeads - 1) / kMlaHeads;
   const int n_items = B * n_hg;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kMlaStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kMlaConsumers);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(qfull, 1);
+    mbar_init(qempty, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&sfull[s], 1);
+      mbar_init(&sempty[s], 4);
+      mbar_init(&pfull[s], 4);
+      mbar_init(&ofull[s], 1);
+      mbar_init(&oempty[s], 4);
     }
     fence_mbar_init();
   }
+  if (warp == 5) tmem_alloc<C::kTmemCols>(tmem_slot);
+  tc_fence_before();
   __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
 
-  if (warp == kMlaConsumers) {
+  if (warp == 4) {
+    // ------------------------------ producer ------------------------------
+    // lane 0 streams pages through the 3-stage ring; lane 1 refills the single Q buffer as soon as
+    // the previous item's last S^T has consumed it (the two lanes wait independently).
     if (lane == 0) {
-      const uint64_t pol = policy_evict_first();
-      int stage = 0;
-      uint32_t phase = 0;
+      // pages are read once per head group: stream them past L2 unless several groups share them
+      const uint64_t pol = n_hg == 1 ? policy_evict_first() : policy_evict_last();
+      // L2 prefetch cursor running pf_dist pages ahead of the smem ring
+      int pf_it = blockIdx.x, pf_p = 0;
+      auto prefetch_next = [&]() {
+        while (pf_it < n_items) {
+          const int pb = pf_it / n_hg;
+          if (pf_p < (seq_lens[pb] + kMlaPage - 1) / kMlaPage) {
+            bulk_prefetch_l2(cache + (size_t)block_table[(size_t)pb * max_pages + pf_p] * (C::kPageBytes / 2),
+                             C::kPageBytes);
+            ++pf_p;
+            return;
+          }
+          pf_it += gridDim.x;
+          pf_p = 0;
+        }
+      };
+      for (int i = 0; i < pf_dist; ++i) prefetch_next();
+      int g = 0;
       for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
         const int b = it / n_hg;
         const int np = (seq_lens[b] + kMlaPage - 1) / kMlaPage;
         const int* bt = block_table + (size_t)b * max_pages;
-        for (int p = 0; p < np; ++p) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], C::kPageBytes);
-          bulk_load(ring + stage * C::kPageBytes, cache + (size_t)bt[p] * (C::kPageBytes / 2), C::kPageBytes,
-                    &full[stage], pol);
-          if (++stage == kMlaStages) { stage = 0; phase ^= 1; }
+        for (int p = 0; p < np; ++p, ++g) {
+          const int s = g % kMlaStages;
+          mbar_wait(&empty[s], ((g / kMlaStages) & 1) ^ 1);
+          prefetch_next();
+          mbar_arrive_expect_tx(&full[s], C::kPageBytes);
+          bulk_load(pages + s * C::kPageBytes, cache + (size_t)bt[p] * (C::kPageBytes / 2), C::kPageBytes, &full[s],
+                    pol);
         }
       }
+    } else if (lane == 1) {
+      prefetch_tmap(&tm_qlat);
+      prefetch_tmap(&tm_qpe);
+      int qi = 0;
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const int b = it / n_hg, hg = it - b * n_hg;
+        if (seq_lens[b] <= 0) continue;
+        // Q of the group -> [block][16 heads][128 B swizzled] (heads >= H and rope dims past RP
+        // are zero-filled out of bounds)
+        mbar_wait(qempty, (qi & 1) ^ 1);
+        mbar_arrive_expect_tx(qfull, C::kQBytes);
+        tma_load_4d(q_s, &tm_qlat, qfull, 0, hg * kMlaHeads, 0, b);
+        for (int kb = R / 64; kb < C::NKB; ++kb)
+          tma_load_3d(q_s + kb * C::kQBlockBytes, &tm_qpe, qfull, (kb - R / 64) * 64, hg * kMlaHeads, b);
+        ++qi;
+      }
     }
-    return;
-  }
+  } else if (warp == 5) {
+    // ------------------------------ MMA issuer ------------------------------
+    // Two independent in-order streams: S^T of page g needs page g in smem; P.V of page t needs
+    // the softmax warps' P_t.  The warp polls both and issues whichever is ready, so a late page
+    // never holds back the P.V (and with it the stage release) of the page before it.  The whole
+    // warp runs this converged (warp-uniform conditions) so the MMAs issue back to back.
+    const uint32_t idesc_s = make_idesc_bf16(64, kMlaHeads);
+    const uint32_t idesc_o = make_idesc_bf16(128, kMlaHeads) | kIdescAMajorMN | kIdescBMajorMN;
+    const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+    const uint32_t pages_a = smem_u32(pages), q_a = smem_u32(q_s), p_a = smem_u32(p_s);
+    // descriptors of stage / buffer 0; other stages and k-steps are constant offsets added to the
+    // 14-bit start-address field (smem addresses < 256 KB never carry out of it)
+    const uint64_t dC_s = make_sdesc_sw128(pages_a);                          // page as K-major A
+    const uint64_t dC_o = make_sdesc_sw128_mn(pages_a, C::kBlockBytes, 1024);  // page as MN-major A
+    const uint64_t dQ = make_sdesc_sw128(q_a);
+    const uint64_t dP = make_sdesc_noswz(p_a, 128, C::kChunkBytes);
+    int gs = 0, gpv = 0;            // next page for S^T / for P.V (global page counters)
+    int it = blockIdx.x, p = 0, np = -1, qi = 0;  // S^T cursor: item, page in item
+    bool s_done = false;
+    while (true) {
+      if (!s_done && np < 0) {  // advance the S^T cursor to the next item with pages
+        while (it < n_items) {
+          np = __shfl_sync(0xffffffffu, (seq_lens[it / n_hg] + kMlaPage - 1) / kMlaPage, 0);
+          if (np > 0) break;
+          it += gridDim.x;
+        }
+        if (it >= n_items) s_done = true;
+        p = 0;
+      }
+      const int sb = gs & 1, pb = gpv & 1;                       // TMEM / P buffers
+      const int sst = gs % kMlaStages, pst = gpv % kMlaStages;  // smem stages
+      const bool can_s = !s_done && __all_sync(0xffffffffu, mbar_test(&full[sst], (gs / kMlaStages) & 1) &&
+                                                                mbar_test(&sempty[sb], ((gs >> 1) & 1) ^ 1) &&
+                                                                mbar_test(qfull, qi & 1));
+      const bool can_pv = gpv < gs && __all_sync(0xffffffffu, mbar_test(&pfull[pb], (gpv >> 1) & 1) &&
+                                                                   mbar_test(&oempty[pb], ((gpv >> 1) & 1) ^ 1));
+      if (can_pv) {  // O^T[pb] = C_gpv[:, :R]^T . P_gpv^T, then release the page's stage
+        tc_fence_after();
+        const uint64_t a0 = dC_o + ((uint32_t)(pst * C::kPageBytes) >> 4), b0 = dP + ((uint32_t)(pb * C::kPBytes) >> 4);
+        const uint32_t d0 = tm + C::kOCol + pb * C::MT * 16;
+#pragma unroll
+        for (int k = 0; k < kMlaTile / 16; ++k)
+#pragma unroll
+          for (int mt = 0; mt < C::MT; ++mt)
+            umma_bf16_warp(d0 + mt * 16, a0 + ((mt * 2 * C::kBlockBytes + k * 2048) >> 4), b0 + ((k * 256) >> 4),
+                           idesc_o, k > 0);
+        umma_commit_warp(&ofull[pb]);
+        umma_commit_warp(&empty[pst]);
+        ++gpv;
+      } else if (can_s) {  // S^T[sb] = C_gs . Q^T over kSAcc partial accumulators
+        tc_fence_after();
+        const uint64_t a0 = dC_s + ((uint32_t)(sst * C::kPageBytes) >> 4);
+        const uint64_t b0 = dQ;
+        const uint32_t d = tm + C::kSCol + sb * C::kSAcc * 16;
+#pragma unroll
+        for (int k = 0; k < C::KS; ++k)
+          umma_bf16_warp(d + (k % C::kSAcc) * 16, a0 + (((k >> 2) * C::kBlockBytes + (k & 3) * 32) >> 4),
+                         b0 + (((k >> 2) * C::kQBlockBytes + (k & 3) * 32) >> 4), idesc_s, k >= C::kSAcc);
+        umma_commit_warp(&sfull[sb]);
+        ++gs;
+        if (++p == np) {  // last page of the item: its Q buffer may be refilled
+          umma_commit_warp(qempty);
+          ++qi;
+          it += gridDim.x;
+          np = -1;
+        }
+      } else if (s_done && gpv == gs) {
+        break;
+      }
+    }
+  } else {
+    // ------------------------- softmax + correction -------------------------
+    const int tid = threadIdx.x;  // 0..127
+    const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+    int g = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const int b = it / n_hg, hg = it - b * n_hg;
+      const int len = seq_lens[b];
+      const int np = (len + kMlaPage - 1) / kMlaPage;
+      if (np == 0) {
+        for (int i = tid; i < kMlaHeads * R; i += 128) {
+          const int h = hg * kMlaHeads + i / R;
+          if (h < H) o_lat[((size_t)h * B + b) * R + i % R] = __float2bfloat16_rn(0.f);
+        }
+        continue;
+      }
+      float m_run[16], lpart[16], alpha_prev[16], O[C::MT][16];
+#pragma unroll
+      for (int h = 0; h < 16; ++h) {
+        m_run[h] = -INFINITY;
+        lpart[h] = 0.f;
+        alpha_prev[h] = 0.f;
+#pragma unroll
+        for (int mt = 0; mt < C::MT; ++mt) O[mt][h] = 0.f;
+      }
+      auto accumulate_o = [&](int t) {  // O = O * alpha(t) + O^T tile t (lane = latent dim)
+        const int s = t & 1;
+        mbar_wait(&ofull[s], (t >> 1) & 1);
+        tc_fence_after();
+        uint32_t v[C::MT][16];
+#pragma unroll
+        for (int mt = 0; mt < C::MT; ++mt) tmem_ld16(trow + C::kOCol + (s * C::MT + mt) * 16, v[mt]);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&oempty[s]);
+#pragma unroll
+        for (int mt = 0; mt < C::MT; ++mt)
+#pragma unroll
+          for (int h = 0; h < 16; ++h) O[mt][h] = fmaf(O[mt][h], alpha_prev[h], __uint_as_float(v[mt][h]));
+      };
 
-  const int g = lane >> 2, t = lane & 3;
-  const int tid = threadIdx.x;  // 0..127
-  int stage = 0;
-  uint32_t phase = 0;
-  int sbuf = 0;
-  for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-    const int b = it / n_hg, hg = it - b * n_hg;
-    const int len = seq_lens[b];
-    const int np = (len + kMlaPage - 1) / kMlaPage;
-    // ---- stage Q = [q_lat | q_pe] for the 16 heads of the group (rows >= H are zero) ----
-    for (int i = tid; i < 16 * C::NCH; i += 128) {
-      const int row = i / C::NCH, ch = i - row * C::NCH;
-      const int h = hg * 16 + row;
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (h < H) {
-        v = ch < R / 8 ? *reinterpret_cast<const uint4*>(q_lat + ((size_t)h * B + b) * R + ch * 8)
-                       : *reinterpret_cast<const uint4*>(q_pe + ((size_t)b * H + h) * RP + (ch - R / 8) * 8);
-      }
-      *reinterpret_cast<uint4*>(q_s + row * C::kQStride + ch * 16) = v;
-    }
-    if (tid < 16) {
-      m_s[tid] = -INFINITY;
-      l_s[tid] = 0.f;
-    }
-    float o[C::NT][4];
-#pragma unroll
-    for (int n = 0; n < C::NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
-    cons_bar();
-
-    const uint32_t qbase = smem_u32(q_s);
-    // this warp's K-split share of Q (k-steps warp, warp+4, ...) lives in registers for the item
-    uint32_t qa[C::KPW][4];
-    {
-      const int mi = lane >> 3, r = lane & 7;
-#pragma unroll
-      for (int kk = 0; kk < C::KPW; ++kk) {
-        const int ks = warp + kMlaConsumers * kk;
-        if (ks < C::KST)
-          ldsm4(qbase + (uint32_t)(((mi & 1) * 8 + r) * C::kQStride + (ks * 16 + (mi >> 1) * 8) * 2), qa[kk][0],
-                qa[kk][1], qa[kk][2], qa[kk][3]);
-      }
-    }
-    for (int p = 0; p < np; ++p) {
-      mbar_wait(&full[stage], phase);
-      const uint32_t cbase = smem_u32(ring + stage * C::kPageBytes);
-      float* S = s_s;
-      uint8_t* P = p_s + sbuf * 16 * C::kPStride;
-      // ---- partial S[16 x 32] over this warp's k-steps (4 independent n-tile accumulators) ----
-      {
-        float acc[4][4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
-        const int mi = lane >> 3, r = lane & 7;
-#pragma unroll
-        for (int kk = 0; kk < C::KPW; ++kk) {
-          const int ks = warp + kMlaConsumers * kk;
-          if (ks < C::KST) {
-            // matrices (chunk 2ks, tok 0-7), (chunk 2ks+1, tok 0-7), (chunk 2ks, tok 8-15), (chunk 2ks+1, tok 8-15)
-            uint32_t b0, b1, b2, b3, b4, b5, b6, b7;
-            const uint32_t kaddr = cbase + (uint32_t)(((2 * ks + (mi & 1)) * kMlaPage + (mi >> 1) * 8 + r) * 16);
-            ldsm4(kaddr, b0, b1, b2, b3);
-            ldsm4(kaddr + 16 * 16, b4, b5, b6, b7);  // tokens 16..31
-            mma16816(acc[0], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b0, b1);
-            mma16816(acc[1], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b2, b3);
-            mma16816(acc[2], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b4, b5);
-            mma16816(acc[3], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b6, b7);
-          }
-        }
-        float* Sw = S + warp * 16 * kMlaPage;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int col = j * 8 + 2 * t;
-          *reinterpret_cast<float2*>(Sw + g * kMlaPage + col) = make_float2(acc[j][0], acc[j][1]);
-          *reinterpret_cast<float2*>(Sw + (g + 8) * kMlaPage + col) = make_float2(acc[j][2], acc[j][3]);
-        }
-      }
-      cons_bar();
-      // ---- online softmax: warp w owns rows 4w..4w+3, lane = token ----
-      {
+      for (int p = 0; p < np; ++p, ++g) {
+        const int s = g & 1, st = g % kMlaStages;
         const int n = min(kMlaPage, len - p * kMlaPage);
+        mbar_wait(&sfull[s], (g >> 1) & 1);
+        tc_fence_after();
+        uint32_t sv[C::kSAcc][16];
 #pragma unroll
-        for (int rr = 0; rr < 4; ++rr) {
-          const int row = warp * 4 + rr;
-          float sv = -INFINITY;
-          if (lane < n) {
-            sv = 0.f;
+        for (int j = 0; j < C::kSAcc; ++j) tmem_ld16(trow + C::kSCol + (s * C::kSAcc + j) * 16, sv[j]);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sempty[s]);
+        // M = 64 accumulator: token 16*warp + lane sits in TMEM lane 32*warp + lane (lanes < 16)
+        const int tok = warp * 16 + lane;
+        const bool valid = lane < 16 && tok < n;
+        float x[16], r[16];
 #pragma unroll
-            for (int w = 0; w < kMlaConsumers; ++w) sv += S[(w * 16 + row) * kMlaPage + lane];
-            sv *= scale_log2;
-          }
-          float mt = sv;
+        for (int h = 0; h < 16; ++h) {
+          float acc = __uint_as_float(sv[0][h]);
 #pragma unroll
-          for (int off = 16; off > 0; off >>= 1) mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, off));
-          const float m_old = m_s[row];
-          const float m_new = fmaxf(m_old, mt);
-          const float pv = exp2f(sv - m_new);
-          float ps = pv;
+          for (int j = 1; j < C::kSAcc; ++j) acc += __uint_as_float(sv[j][h]);
+          x[h] = valid ? acc * scale_log2 : -INFINITY;
+          r[h] = x[h];
+        }
+        const float wmax = xreduce16<true>(r, lane);
+        if (lane < 16) red[(s * 4 + warp) * 16 + lane] = wmax;
+        cons_bar();
+        float alpha[16], pv[16];
 #pragma unroll
-          for (int off = 16; off > 0; off >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, off);
-          reinterpret_cast<__nv_bfloat16*>(P + row * C::kPStride)[lane] = __float2bfloat16_rn(pv);
-          __syncwarp();
-          if (lane == 0) {
-            const float alpha = exp2f(m_old - m_new);
-            a_s[row] = alpha;
-            l_s[row] = l_s[row] * alpha + ps;
-            m_s[row] = m_new;
+        for (int h = 0; h < 16; ++h) {
+          const float* rr = red + s * 64 + h;
+          const float m_new = fmaxf(fmaxf(m_run[h], fmaxf(rr[0], rr[16])), fmaxf(rr[32], rr[48]));
+          alpha[h] = exp2f(m_run[h] - m_new);
+          m_run[h] = m_new;
+          pv[h] = exp2f(x[h] - m_new);
+          lpart[h] = fmaf(lpart[h], alpha[h], pv[h]);
+        }
+        if (lane < 16) {
+          uint8_t* pd = p_s + s * C::kPBytes;
+          *reinterpret_cast<uint4*>(pd + tok * 16) = make_uint4(
+              pack_bf16x2(pv[0], pv[1]), pack_bf16x2(pv[2], pv[3]), pack_bf16x2(pv[4], pv[5]), pack_bf16x2(pv[6], pv[7]));
+          *reinterpret_cast<uint4*>(pd + (kMlaTile + tok) * 16) =
+              make_uint4(pack_bf16x2(pv[8], pv[9]), pack_bf16x2(pv[10], pv[11]), pack_bf16x2(pv[12], pv[13]),
+                         pack_bf16x2(pv[14], pv[15]));
+        }
+        if (n < kMlaPage) {  // rows past the sequence end: P = 0, and V must not hold NaN/Inf
+          const int tail = kMlaPage - n;
+          uint8_t* pg = pages + st * C::kPageBytes + n * 128;  // token rows are contiguous 128 B
+          for (int i = tid; i < tail * 8 * C::NKB; i += 128) {  // (P.V's phantom rows alias the next block)
+            const int kb = i / (tail * 8), r = i - kb * tail * 8;
+            *reinterpret_cast<uint4*>(pg + kb * C::kBlockBytes + r * 16) = make_uint4(0, 0, 0, 0);
           }
         }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&pfull[s]);
+        if (p > 0) accumulate_o(g - 1);
+#pragma unroll
+        for (int h = 0; h < 16; ++h) alpha_prev[h] = alpha[h];
       }
+      accumulate_o(g - 1);
+
+      // ---- normalise and store: lane = latent dim, 16 heads per thread ----
+      const float lsum = xreduce16<false>(lpart, lane);
+      if (lane < 16) lred[warp * 16 + lane] = lsum;
       cons_bar();
-      // ---- O[16 x DPW] = O * alpha + P[16 x 32] C[32 x DPW] ----
-      {
-        const float al0 = a_s[g], al1 = a_s[g + 8];
 #pragma unroll
-        for (int n = 0; n < C::NT; ++n) {
-          o[n][0] *= al0; o[n][1] *= al0; o[n][2] *= al1; o[n][3] *= al1;
-        }
-        const uint32_t pbase = smem_u32(P);
-        const int mi = lane >> 3, r = lane & 7;
+      for (int h = 0; h < 16; ++h) {
+        const int hh = hg * kMlaHeads + h;
+        const float l = lred[h] + lred[16 + h] + lred[32 + h] + lred[48 + h];
+        const float inv = l > 0.f ? 1.0f / l : 0.f;
+        if (hh < H) {
+          __nv_bfloat16* dst = o_lat + ((size_t)hh * B + b) * R + warp * 32 + lane;
 #pragma unroll
-        for (int ks = 0; ks < kMlaPage / 16; ++ks) {
-          uint32_t a0, a1, a2, a3;
-          ldsm4(pbase + (uint32_t)(((mi & 1) * 8 + r) * C::kPStride + (ks * 16 + (mi >> 1) * 8) * 2), a0, a1, a2, a3);
-#pragma unroll
-          for (int n2 = 0; n2 < C::NT / 2; ++n2) {
-            const int chunk = warp * (C::DPW / 8) + 2 * n2 + (mi >> 1);
-            const int tok = ks * 16 + ((mi & 1) << 3) + r;
-            uint32_t v0a, v0b, v1a, v1b;
-            ldsm4t(cbase + (uint32_t)((chunk * kMlaPage + tok) * 16), v0a, v0b, v1a, v1b);
-            mma16816(o[2 * n2], a0, a1, a2, a3, v0a, v0b);
-            mma16816(o[2 * n2 + 1], a0, a1, a2, a3, v1a, v1b);
-          }
+          for (int mt = 0; mt < C::MT; ++mt) dst[mt * 128] = __float2bfloat16_rn(O[mt][h] * inv);
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[stage]);
-      if (++stage == kMlaStages) { stage = 0; phase ^= 1; }
-      sbuf ^= 1;
+      cons_bar();  // lred reused by the next item
     }
-    // ---- normalise and store this warp's dims of the heads of the group ----
-    cons_bar();  // l_s final for every row
-    const float l0 = l_s[g], l1 = l_s[g + 8];
-    const int h0 = hg * 16 + g, h1 = h0 + 8;
-#pragma unroll
-    for (int n = 0; n < C::NT; ++n) {
-      const int dim = warp * C::DPW + n * 8 + 2 * t;
-      if (h0 < H)
-        *reinterpret_cast<uint32_t*>(o_lat + ((size_t)h0 * B + b) * R + dim) =
-            pack_bf16x2(l0 > 0.f ? o[n][0] / l0 : 0.f, l0 > 0.f ? o[n][1] / l0 : 0.f);
-      if (h1 < H)
-        *reinterpret_cast<uint32_t*>(o_lat + ((size_t)h1 * B + b) * R + dim) =
-            pack_bf16x2(l1 > 0.f ? o[n][2] / l1 : 0.f, l1 > 0.f ? o[n][3] / l1 : 0.f);
-    }
-    cons_bar();  // q_s / m_s / l_s reused by the next item
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) {
+    tc_fence_after();
+    tmem_dealloc<C::kTmemCols>(tmem);
   }
 }
 
@@ -281,13 +401,32 @@ int launch_mla(const void* q_lat, const void* q_pe, const void* cache, const int
       return MGB_ECUDA;
     attr = true;
   }
-  const int items = B * ((H + 15) / 16);
-  int grid = 2 * mgb_host::num_sms();
+  const int items = B * ((H + kMlaHeads - 1) / kMlaHeads);
+  int grid = mgb_host::num_sms();
   if (grid > items) grid = items;
+  static const int pf_dist = [] {
+    const char* e = getenv("MGB_MLA_PREFETCH");
+    return e ? atoi(e) : 4;
+  }();
+  // Q operands straight from q_lat [H,B,R] / q_pe [B,H,RP] into the swizzled K-major
+  // [block][head][64 dims] layout.  q_lat: dim0 = 64 dims of a block, dim1 = head, dim2 = block,
+  // dim3 = sequence (one TMA for all R/64 blocks); q_pe: dims, head, sequence (one per block).
+  CUtensorMap tq, tp;
+  {
+    const uint64_t d[4] = {64, (uint64_t)H, R / 64, (uint64_t)B};
+    const uint64_t s[3] = {(uint64_t)B * R * 2, 128, (uint64_t)R * 2};
+    const uint32_t box[4] = {64, kMlaHeads, R / 64, 1};
+    if (mgb_host::encode_tmap_bf16(&tq, q_lat, 4, d, s, box, true) != CUDA_SUCCESS) return MGB_ECUDA;
+  }
+  {
+    const uint64_t d[3] = {RP, (uint64_t)H, (uint64_t)B};
+    const uint64_t s[2] = {(uint64_t)RP * 2, (uint64_t)H * RP * 2};
+    const uint32_t box[3] = {64, kMlaHeads, 1};
+    if (mgb_host::encode_tmap_bf16(&tp, q_pe, 3, d, s, box, true) != CUDA_SUCCESS) return MGB_ECUDA;
+  }
   decode_attn_mla_kernel<R, RP><<<grid, kMlaThreads, C::kSmem, st>>>(
-      reinterpret_cast<const __nv_bfloat16*>(q_lat), reinterpret_cast<const __nv_bfloat16*>(q_pe),
-      reinterpret_cast<const __nv_bfloat16*>(cache), bt, max_pages, lens, B, H, scale * 1.4426950408889634f,
-      reinterpret_cast<__nv_bfloat16*>(out));
+      tq, tp, reinterpret_cast<const __nv_bfloat16*>(cache), bt, max_pages, lens, B, H, scale * 1.4426950408889634f,
+      reinterpret_cast<__nv_bfloat16*>(out), pf_dist);
   return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
 }
 
@@ -308,7 +447,10 @@ __global__ void mla_append_kernel(const __nv_bfloat16* __restrict__ q,    // [B,
   const __nv_bfloat16* row = ckv + (size_t)b * D;
   const int page = block_table[(size_t)b * max_pages + pos / kMlaPage];
   const int slot = pos % kMlaPage;
-  __nv_bfloat16* pg = cache + (size_t)page * D * kMlaPage;
+  const int DP = (D + 63) / 64 * 64;  // padded page row (see the page layout above)
+  __nv_bfloat16* pg = cache + (size_t)page * DP * kMlaPage;
+  // element offset of dim i of this token inside the swizzled page
+  auto at = [slot](int i) { return (i >> 6) * (kMlaPage * 64) + slot * 64 + ((((i >> 3) & 7) ^ (slot & 7)) << 3) + (i & 7); };
   if (seq_lens && threadIdx.x == 0) seq_lens[b] = pos + 1;
   // latent RMSNorm (HF DeepseekV2RMSNorm: fp32 variance, bf16 cast, times weight)
   float ss = 0.f;
@@ -325,7 +467,7 @@ __global__ void mla_append_kernel(const __nv_bfloat16* __restrict__ q,    // [B,
   const float inv = 1.0f / sqrtf(tot / (float)R + eps);
   for (int i = threadIdx.x; i < R; i += blockDim.x) {
     const float v = __bfloat162float(norm_w[i]) * bf16_round(__bfloat162float(row[i]) * inv);
-    pg[((size_t)(i / 8) * kMlaPage + slot) * 8 + (i % 8)] = __float2bfloat16_rn(v);
+    pg[at(i)] = __float2bfloat16_rn(v);
   }
   const float* cs = cos_t + (size_t)pos * (RP / 2);
   const float* sn = sin_t + (size_t)pos * (RP / 2);
@@ -333,8 +475,8 @@ __global__ void mla_append_kernel(const __nv_bfloat16* __restrict__ q,    // [B,
     const float x0 = __bfloat162float(row[R + 2 * i]), x1 = __bfloat162float(row[R + 2 * i + 1]);
     const float c = cs[i], s = sn[i];
     const int d0 = R + 2 * i;
-    pg[((size_t)(d0 / 8) * kMlaPage + slot) * 8 + (d0 % 8)] = __float2bfloat16_rn(x0 * c - x1 * s);
-    pg[((size_t)((d0 + 1) / 8) * kMlaPage + slot) * 8 + ((d0 + 1) % 8)] = __float2bfloat16_rn(x0 * s + x1 * c);
+    pg[at(d0)] = __float2bfloat16_rn(x0 * c - x1 * s);
+    pg[at(d0 + 1)] = __float2bfloat16_rn(x0 * s + x1 * c);
   }
   const int QD = NOPE + RP;
   for (int i = threadIdx.x; i < H * (RP / 2); i += blockDim.x) {  // per-head q_pe
@@ -358,6 +500,9 @@ __global__ void mla_append_kernel(const __nv_bfloat16* __restrict__ q,    // [B,
 extern "C" {
 
 int mgb_mla_page_size(void) { return mgb::kMlaPage; }
+
+// bf16 elements of one latent page for latent width R and rope width RP (rows padded to 64).
+int mgb_mla_page_elems(int R, int RP) { return (R + RP + 63) / 64 * 64 * mgb::kMlaPage; }
 
 // Absorbed MLA decode attention: q_lat [H,B,R], q_pe [B,H,RP], latent pages -> o_lat [H,B,R].
 int mgb_decode_attn_mla(const void* q_lat, const void* q_pe, const void* cache, const int* block_table, int max_pages,

@@ -62,6 +62,18 @@ MGB_DEVINL bool mbar_try_wait(uint32_t bar_addr, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// Non-blocking: has the phase with this parity completed?
+MGB_DEVINL bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 MGB_DEVINL void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   while (!mbar_try_wait(a, parity)) {
@@ -92,12 +104,30 @@ MGB_DEVINL void tma_load_2d(void* smem_dst, const CUtensorMap* m, uint64_t* bar,
       "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
       : "memory");
 }
+MGB_DEVINL void tma_load_4d(void* smem_dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+MGB_DEVINL void tma_load_3d(void* smem_dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
 // Warm L2 with a tile that a later TMA load will fetch (turns its DRAM latency into L2 latency).
 MGB_DEVINL void tma_prefetch_2d(const CUtensorMap* m, int c0, int c1) {
   asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
                    reinterpret_cast<uint64_t>(m)),
                "r"(c0), "r"(c1)
                : "memory");
+}
+// 1-D bulk prefetch global -> L2 (no smem, no completion tracking)
+MGB_DEVINL void bulk_prefetch_l2(const void* gsrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gsrc), "r"(bytes) : "memory");
 }
 // 1-D bulk copy global -> shared (no tensor map; 16 B aligned, size multiple of 16)
 MGB_DEVINL void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar,
@@ -139,6 +169,26 @@ MGB_DEVINL void umma_bf16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uin
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// Warp-converged variants: the whole warp executes them and elect.sync inside the asm picks the
+// issuing thread, which lets ptxas emit back-to-back UTCHMMA / UTCBAR without the per-instruction
+// ELECT / BRA.U.ANY loop it wraps around single-thread (lane == 0) tcgen05 code.
+MGB_DEVINL void umma_bf16_warp(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                               uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t"
+      "setp.ne.b32 q, %4, 0;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, q;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+MGB_DEVINL void umma_commit_warp(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "@p tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
 // Arrive on an mbarrier once all previously issued tcgen05 ops of this thread complete.
 MGB_DEVINL void umma_commit(uint64_t* bar) {
   asm volatile(
@@ -169,6 +219,48 @@ MGB_DEVINL uint64_t make_sdesc_sw128(uint32_t smem_addr) {
   d |= (uint64_t)1 << 46;                           // descriptor version (sm_100)
   d |= (uint64_t)2 << 61;                           // layout: SWIZZLE_128B
   return d;
+}
+
+// Shared-memory matrix descriptor for a non-swizzled ("interleaved") operand built from 8x16-byte
+// core matrices (each 128 contiguous bytes).  K-major: lbo = byte step between core matrices along
+// K, sbo = along M/N.  MN-major: sbo = step between 8-element groups along M/N, lbo = between
+// 8-row groups along K (CUTLASS cute/atom/mma_traits_sm100.hpp canonical layouts).
+MGB_DEVINL uint64_t make_sdesc_noswz(uint32_t smem_addr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3fff);
+  d |= (uint64_t)((lbo >> 4) & 0x3fff) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3fff) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (sm_100); layout bits 61-63 = 0: SWIZZLE_NONE
+  return d;
+}
+// Instruction-descriptor bits selecting MN-major (transposed) A / B operands.
+constexpr uint32_t kIdescAMajorMN = 1u << 15;
+constexpr uint32_t kIdescBMajorMN = 1u << 16;
+
+// Order this thread's generic-proxy shared-memory writes before later async-proxy (tensor core /
+// TMA) reads that are synchronised through an mbarrier.
+MGB_DEVINL void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// MN-major 128B-swizzled operand: 64-element (128 B) rows along M/N, one row per K index, 8-row
+// atoms of 1024 B; lbo = byte step between 64-wide M/N atom columns, sbo = between 8-row K groups.
+MGB_DEVINL uint64_t make_sdesc_sw128_mn(uint32_t smem_addr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3fff);
+  d |= (uint64_t)((lbo >> 4) & 0x3fff) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3fff) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+  return d;
+}
+
+// 32 lanes x 16 columns of fp32 from TMEM -> 16 registers per thread.
+MGB_DEVINL void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
 }
 
 // 32 lanes x 32 columns of fp32 from TMEM -> 32 registers per thread.
@@ -276,5 +368,8 @@ namespace mgb_host {
 // cuTensorMapEncodeTiled resolved through the runtime's driver entry point (no -lcuda).
 CUresult encode_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
                              uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer);
+// Rank-N (N <= 5) bf16 tensor map, unswizzled or 128B-swizzled; strides_bytes has rank-1 entries (dims 1..N-1).
+CUresult encode_tmap_bf16(CUtensorMap* map, const void* base, int rank, const uint64_t* dims,
+                          const uint64_t* strides_bytes, const uint32_t* box, bool swizzle128 = false);
 int num_sms();
 }  // namespace mgb_host

@@ -143,12 +143,12 @@ class Engine:
         i32 = dict(dtype=torch.int32, device=device)
         # ---- paged KV cache (identity block table: sequence b owns pages [b*pps, (b+1)*pps)) ----
         if self.mla:
-            # latent pages [(R + r)/8][32 tok][8] (attn_mla.cu)
+            # latent pages: swizzled 64-dim blocks [ceil((R + r)/64)][page tok][64] (attn_mla.cu)
             self.page = nat.value("mgb_mla_page_size")
             self.pps = math.ceil(self.max_ctx / self.page)
             n_pages = B * self.pps
-            self.latent = [torch.zeros(n_pages * (a.kv_lora_rank + a.qk_rope_dim) * self.page, **bf)
-                           for _ in range(a.layers)]
+            page_elems = nat.value("mgb_mla_page_elems", a.kv_lora_rank, a.qk_rope_dim)
+            self.latent = [torch.zeros(n_pages * page_elems, **bf) for _ in range(a.layers)]
             r = a.qk_rope_dim
             inv_freq = 1.0 / (a.rope_theta ** (torch.arange(0, r, 2, dtype=torch.int64).float() / r))
             freqs = torch.arange(self.max_ctx).float()[:, None] * inv_freq[None, :]

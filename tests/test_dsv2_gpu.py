@@ -16,14 +16,19 @@ TOL = 2e-2
 
 
 def _latent_pages(c, pe, B, ctx, page, pps):
-    """dense [B,ctx,R] + [B,ctx,r] -> chunk-major latent pages [B*pps][(R+r)/8][page][8]."""
+    """dense [B,ctx,R] + [B,ctx,r] -> latent pages [B*pps][ceil(D/64)][page][64] with the 16-byte
+    chunks of every token row 128B-swizzled (chunk j of token t stored at j ^ (t % 8)); attn_mla.cu."""
     D = c.shape[-1] + pe.shape[-1]
-    full = torch.cat([c, pe], -1)  # [B, ctx, D]
-    pages = torch.zeros(B * pps, D // 8, page, 8, dtype=BF16)
-    for b in range(B):
-        for t in range(ctx):
-            pages[b * pps + t // page, :, t % page, :] = full[b, t].view(D // 8, 8)
-    return pages.reshape(-1)
+    NKB = (D + 63) // 64
+    full = torch.zeros(B, pps * page, NKB * 64, dtype=BF16)
+    full[:, :ctx, :D] = torch.cat([c, pe], -1)
+    t = torch.arange(page)
+    j = torch.arange(8)
+    src = j[None, :] ^ (t[:, None] % 8)                        # stored chunk j holds logical chunk j ^ (t%8)
+    x = full.view(B, pps, page, NKB, 8, 8)                     # [b, page, tok, block, chunk, 8]
+    x = x[:, :, t[:, None], :, src, :]                         # gather -> [page_tok, 8, b, pps, block, 8]
+    x = x.permute(2, 3, 4, 0, 1, 5)                            # [b, pps, block, tok, chunk, 8]
+    return x.contiguous().reshape(-1)
 
 
 @pytest.mark.parametrize("B,H,RL,r,ctx", [(3, 16, 512, 64, 1), (4, 16, 512, 64, 100), (2, 128, 512, 64, 70),

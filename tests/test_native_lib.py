@@ -59,6 +59,9 @@ def test_sass_uses_tcgen05_and_tma():
     attn = subprocess.run(["cuobjdump", "-sass", os.path.join(ROOT, "paper_2503_09716_b200", "_lib", "attn_gqa.o")],
                           capture_output=True, text=True).stdout
     assert "UBLKCP" in attn and "HMMA" in attn
+    mla = subprocess.run(["cuobjdump", "-sass", os.path.join(ROOT, "paper_2503_09716_b200", "_lib", "attn_mla.o")],
+                         capture_output=True, text=True).stdout
+    assert "UTCHMMA" in mla and "UBLKCP" in mla and "LDTM" in mla
 
 
 def test_missing_library_fails_loudly(tmp_path):
