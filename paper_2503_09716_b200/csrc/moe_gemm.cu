@@ -39,9 +39,24 @@ constexpr int kAccStages = 2;                      // 2 x 256 TMEM columns
 constexpr int kXStride = 33;                       // padded row of the gate/up exchange buffer
 constexpr int kGemmSmem = kStages * kStageBytes + 64 * kXStride * 4 + 1024 /*align*/ + 256 /*barriers*/;
 
+// Token tiles of an expert: as few as fit N <= 256.  The gated GEMM (heavier per-token epilogue)
+// sizes them equally (multiple of 32) so no unit is a tiny remainder whose epilogue cannot hide
+// behind the next unit's main loop (568 tokens -> 3 x 192 rather than 256 + 256 + 56); the plain
+// GEMM keeps full 256-token tiles, which measured faster for it.
+MGB_DEVINL int token_tile(int cnt, bool balanced) {
+  if (!balanced) return kBNMax;
+  const int nt0 = (cnt + kBNMax - 1) / kBNMax;
+  return nt0 == 0 ? kBNMax : (((cnt + nt0 - 1) / nt0) + 31) & ~31;
+}
+MGB_DEVINL int token_tiles(int cnt, bool balanced) {
+  const int t = token_tile(cnt, balanced);
+  return (cnt + t - 1) / t;
+}
+
 struct UnitSched {
   const int* s_prefix;  // [E+1] units before expert e (smem)
   int E, MT;
+  bool balanced;
   __device__ void decode(int u, const int* offs, int& e, int& nt, int& mt, int& tok0, int& n) const {
     int lo = 0, hi = E - 1;  // last e with prefix[e] <= u
     while (lo < hi) {
@@ -53,11 +68,11 @@ struct UnitSched {
     const int beg = offs[e], cnt = offs[e + 1] - beg;
     // token tiles fastest: the (up to ceil(cnt/256)) units that share one weight tile run on
     // neighbouring CTAs at the same time, so the tile is read from HBM once and hit in L2 after
-    const int NT = (cnt + kBNMax - 1) / kBNMax;
+    const int tile = token_tile(cnt, balanced), NT = (cnt + tile - 1) / tile;
     mt = local / NT;
     nt = local - mt * NT;
-    tok0 = beg + nt * kBNMax;
-    n = min(kBNMax, cnt - nt * kBNMax);
+    tok0 = beg + nt * tile;
+    n = min(tile, cnt - nt * tile);
   }
 };
 
@@ -118,7 +133,7 @@ moe_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     for (int e = 0; e < E; ++e) {
       s_prefix[e] = acc;
       const int cnt = offsets[e + 1] - offsets[e];
-      acc += ((cnt + kBNMax - 1) / kBNMax) * MT;
+      acc += token_tiles(cnt, GATED) * MT;
     }
     s_prefix[E] = acc;
   }
@@ -141,7 +156,7 @@ moe_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int total = s_prefix[E];
-  UnitSched sched{s_prefix, E, MT};
+  UnitSched sched{s_prefix, E, MT, GATED};
   const int KB = K / kBK;
 
   if (warp == 0) {
@@ -285,7 +300,7 @@ moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
     for (int e = 0; e < E; ++e) {
       s_prefix[e] = acc;
       const int cnt = offsets[e + 1] - offsets[e];
-      acc += ((cnt + kBNMax - 1) / kBNMax) * MT;
+      acc += token_tiles(cnt, GATED) * MT;
     }
     s_prefix[E] = acc;
   }
@@ -298,7 +313,7 @@ moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
     }
     for (int s = 0; s < kAccStages; ++s) {
       mbar_init(&tfull_bar[s], 1);
-      mbar_init(&tempty_bar[s], 2 * 128);  // both CTAs' epilogue threads (used on the leader)
+      mbar_init(&tempty_bar[s], 2 * 4);  // both CTAs' epilogue warps (used on the leader)
     }
     fence_mbar_init();
   }
@@ -309,20 +324,23 @@ moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int total = s_prefix[E];
-  UnitSched sched{s_prefix, E, MT};
+  UnitSched sched{s_prefix, E, MT, GATED};
   const int KB = K / kBK;
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
 
   if (warp == 0) {
     // ------------------------------ TMA producer (both CTAs) ------------------------------
     if (elect_one()) {
-      const uint64_t pol_w = policy_evict_first();
+      // a weight tile read by several token tiles (neighbouring pairs, same time) stays in L2 for
+      // them; one read once streams past it
+      const uint64_t pol_once = policy_evict_first(), pol_shared = policy_evict_normal();
       const uint64_t pol_x = policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
       for (int u = pair; u < total; u += npairs) {
         int e, nt, mt, tok0, n;
         sched.decode(u, offsets, e, nt, mt, tok0, n);
+        const uint64_t pol_w = token_tiles(offsets[e + 1] - offsets[e], GATED) > 1 ? pol_shared : pol_once;
         const int N = (n + 31) & ~31;
         const int half = N / 2;
         const int nb = half / kPBRows;
@@ -408,7 +426,8 @@ moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
         }
       }
       tc_fence_before();
-      mbar_arrive_cluster(tempty_leader0 + acc * 8);
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_leader0 + acc * 8);
       if (++acc == kAccStages) { acc = 0; acc_phase ^= 1; }
     }
   }

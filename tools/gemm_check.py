@@ -77,7 +77,16 @@ def run(E, d, f, counts, check=True, iters=0):
         print(f"  gate_up {t1*1e3:.1f} us  {b1/t1/1e6:.0f} GB/s  {fl1/t1/1e9:.0f} TF/s | down {t2*1e3:.1f} us {b2/t2/1e6:.0f} GB/s {fl2/t2/1e9:.0f} TF/s")
 
 
+SHAPES = {  # bench shapes: tokens per expert at the planner's batch
+    "mixtral": (8, 4096, 14336, [208] * 8),
+    "dsv2": (64, 2048, 1408, [568] * 64),
+}
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1:
+        E, d, f, counts = SHAPES[sys.argv[1]]
+        run(E, d, f, counts, check=len(sys.argv) > 2, iters=10)
+        sys.exit(0)
     run(1, 256, 512, [40])
     run(8, 256, 512, [0, 1, 17, 33, 64, 100, 255, 300])
     run(4, 512, 384, [256, 257, 512, 3])
