@@ -82,6 +82,15 @@ int mgb_mla_append(const void* q, const void* ckv, const void* norm_w, float eps
                    const int* positions, const float* cos_t, const float* sin_t, const int* block_table, int max_pages,
                    void* cache, void* q_nope_out, void* q_pe_out, int* seq_lens, void* stream);
 
+/* ---- KV_COPY_OUT / new-token insert for kv_policy "offload" (offload_dag.py:372-392) --------
+ * Copies the token at positions[b] of sequence b from page src_table[b][pos/page_tokens] of src to
+ * page dst_table[b][pos/page_tokens] of dst (same in-page slot).  A token's bytes inside a page are
+ * n_units runs of unit_bytes, run u at u*unit_stride + slot*unit_bytes (GQA: 16 B / 16*page;
+ * MLA: 128 B / 128*page).  src/dst may be mapped pinned host memory (UVA). */
+int mgb_kv_token_copy(const void* src, const int* src_table, int src_max_pages, void* dst, const int* dst_table,
+                      int dst_max_pages, const int* positions, int B, int page_tokens, long long page_bytes,
+                      int unit_bytes, int n_units, long long unit_stride, void* stream);
+
 /* ---- PRE_ATTENTION / POST_ATTENTION helpers (offload_dag.py:359-416) --------------------- */
 int mgb_add_rmsnorm(const void* x, const void* delta, const void* weight, float eps, int T, int d, void* x_out,
                     void* y, void* stream);

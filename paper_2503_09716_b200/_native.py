@@ -48,6 +48,8 @@ SIGNATURES: dict[str, list] = {
     "mgb_mla_page_elems": [I, I],
     "mgb_decode_attn_mla": [P, P, P, P, I, P, I, I, I, I, F, P, P],
     "mgb_mla_append": [P, P, P, F, I, I, I, I, I, P, P, P, P, I, P, P, P, P, P],
+    # kv_stream.cu
+    "mgb_kv_token_copy": [P, P, I, P, P, I, P, I, I, L, I, I, L, P],
 }
 
 # entry points that return a value rather than a status

@@ -95,14 +95,15 @@ class Engine:
     host-offloaded weights, paged KV in HBM, optional expert parallelism)."""
 
     def __init__(self, arch: ModelArch | str, plan=None, *, prompt_len: int, decode_len: int, seed: int = 0,
-                 kv_policy: str = "resident", use_graph: bool = True, device: str = "cuda", ep=None):
+                 kv_policy: str = "resident", use_graph: bool = True, device: str = "cuda", ep=None,
+                 kv_ring_slots: int = 3):
         if not torch.cuda.is_available():
             raise RuntimeError("the B200 engine needs a CUDA device (there is no CPU fallback)")
         self.arch = get_arch(arch) if isinstance(arch, str) else arch
         if self.arch.family not in ("mixtral", "deepseek_v2"):
             raise NotImplementedError(f"unknown model family {self.arch.family!r}")
-        if kv_policy != "resident":
-            raise NotImplementedError("kv_policy='offload' (KV streamed from host) is not built yet; KV is paged in HBM")
+        if kv_policy not in ("resident", "offload"):
+            raise ValueError(f"kv_policy must be 'resident' or 'offload', got {kv_policy!r}")
         a = self.arch
         self.mla = a.family == "deepseek_v2"
         self.kv_policy = kv_policy
@@ -126,6 +127,7 @@ class Engine:
             if j.resource is not None and j.layer >= 0:
                 self.layer_jobs[j.layer].append(j)
         self.offload = self.plan.s_params < self.spec.model_bytes
+        self.kv_ring_cap = kv_ring_slots
         if self.offload and self.mla:
             raise NotImplementedError("weight offload is built for the Mixtral family; DeepSeek-V2 runs resident")
         self._plan_streams()
@@ -141,14 +143,13 @@ class Engine:
         d, k, f = a.hidden, a.top_k, a.moe_ffn
         bf = dict(dtype=BF16, device=device)
         i32 = dict(dtype=torch.int32, device=device)
-        # ---- paged KV cache (identity block table: sequence b owns pages [b*pps, (b+1)*pps)) ----
+        # ---- paged KV (identity block table: sequence b owns pages [b*pps, (b+1)*pps)) ----
         if self.mla:
             # latent pages: swizzled 64-dim blocks [ceil((R + r)/64)][page tok][64] (attn_mla.cu)
             self.page = nat.value("mgb_mla_page_size")
-            self.pps = math.ceil(self.max_ctx / self.page)
-            n_pages = B * self.pps
-            page_elems = nat.value("mgb_mla_page_elems", a.kv_lora_rank, a.qk_rope_dim)
-            self.latent = [torch.zeros(n_pages * page_elems, **bf) for _ in range(a.layers)]
+            self.page_elems = nat.value("mgb_mla_page_elems", a.kv_lora_rank, a.qk_rope_dim)
+            self.kv_unit = (128, self.page_elems // (64 * self.page), 128 * self.page)  # bytes, runs, run stride
+            n_stores = 1
             r = a.qk_rope_dim
             inv_freq = 1.0 / (a.rope_theta ** (torch.arange(0, r, 2, dtype=torch.int64).float() / r))
             freqs = torch.arange(self.max_ctx).float()[:, None] * inv_freq[None, :]
@@ -156,18 +157,31 @@ class Engine:
             self.cos_t = cis.real.contiguous().to(device)
             self.sin_t = cis.imag.contiguous().to(device)
         else:
+            # chunk-major K and V pages [Hkv][hd/8][page tok][8] (attn_gqa.cu)
             self.page = ops.kv_page_size()
-            self.pps = math.ceil(self.max_ctx / self.page)
-            n_pages = B * self.pps
-            blk = a.n_kv_heads * a.head_dim * self.page
-            self.k_cache = [torch.zeros(n_pages * blk, **bf) for _ in range(a.layers)]
-            self.v_cache = [torch.zeros(n_pages * blk, **bf) for _ in range(a.layers)]
+            self.page_elems = a.n_kv_heads * a.head_dim * self.page
+            self.kv_unit = (16, a.n_kv_heads * a.head_dim // 8, 16 * self.page)
+            n_stores = 2
             # RoPE tables (HF MixtralRotaryEmbedding, bf16-rounded, modeling_mixtral.py:210-220)
             hd = a.head_dim
             inv_freq = 1.0 / (a.rope_theta ** (torch.arange(0, hd, 2, dtype=torch.int64).float() / hd))
             freqs = torch.arange(self.max_ctx).float()[:, None] * inv_freq[None, :]
             self.cos_t = freqs.cos().to(BF16).float().contiguous().to(device)
             self.sin_t = freqs.sin().to(BF16).float().contiguous().to(device)
+        self.pps = math.ceil(self.max_ctx / self.page)
+        n_pages = B * self.pps
+        # kv[l][s] = the page store of layer l, store s (GQA: K, V; MLA: latent): HBM when resident,
+        # pinned host memory when offloaded (then see _init_kv_stream for the HBM ring and staging)
+        if kv_policy == "resident":
+            self.kv = [[torch.zeros(n_pages * self.page_elems, **bf) for _ in range(n_stores)]
+                       for _ in range(a.layers)]
+        else:
+            self._init_kv_stream(n_stores, n_pages)
+        if self.mla:
+            self.latent = [st[0] for st in self.kv]
+        else:
+            self.k_cache = [st[0] for st in self.kv]
+            self.v_cache = [st[1] for st in self.kv]
         self.block_table = torch.arange(n_pages, dtype=torch.int32, device=device).view(B, self.pps)
         # ---- step buffers ----
         rows = B * k
@@ -206,7 +220,10 @@ class Engine:
         self.router_logits = "cublas"  # or "fused": gate GEMV inside mgb_router_topk
         self.logits_r = torch.zeros(B, a.n_experts, dtype=torch.float32, device=device)
         self.stream = torch.cuda.Stream(device=device)
-        self.h2d = torch.cuda.Stream(device=device) if self.offload else None
+        self.streaming = self.offload or kv_policy == "offload"
+        self.h2d = torch.cuda.Stream(device=device) if self.streaming else None
+        self.d2h = torch.cuda.Stream(device=device) if kv_policy == "offload" else None
+        self._join2 = torch.cuda.Event()
         self._fork, self._join = torch.cuda.Event(), torch.cuda.Event()
         self.events = {i: torch.cuda.Event() for i in self.need_event}
         self.trace_events: dict | None = None  # job id -> (start, end) timing events (eager trace mode)
@@ -260,11 +277,92 @@ class Engine:
             if j.kind == "expert_compute":
                 self.first_expert_job.setdefault(j.layer, j.id)
                 self.last_expert_job[j.layer] = j.id
+        # KV streaming (kv_policy="offload"): copy-in k lands in ring slot k % n; its slot is free once
+        # the attention of copy k - n has run (the schedule's ring edge, offload_dag.py:383-386, when
+        # n equals the planner's ring).  The new-token staging pages are double-buffered by layer
+        # parity, so pre_attention(l, mb) also waits for kv_copy_out(l - 2, mb) to have read them.
+        kins = [j for j in jobs if j.kind == "kv_copy_in"]
+        self.kv_ring_n = min(len(kins), self.kv_ring_cap) if kins else 0
+        self.kv_slot_of: dict[int, int] = {}
+        mech_of_kin: dict[int, int] = {}
+        succ = self.schedule.succs()
+        for i, kj in enumerate(kins):
+            self.kv_slot_of[kj.id] = i % self.kv_ring_n
+            mech_of_kin[kj.id] = next(v for v in succ[kj.id] if jobs[v].kind == "attn_mech_gpu")
+        self.kin_of_mech = {m: k for k, m in mech_of_kin.items()}
+        for i, kj in enumerate(kins):
+            if i >= self.kv_ring_n:
+                m = mech_of_kin[kins[i - self.kv_ring_n].id]
+                self.xwait[kj.id] = sorted(set(self.xwait[kj.id]) | {m})
+                self.need_event.add(m)
+        kv_out = {(j.layer, j.label.rsplit("/", 1)[1]): j.id for j in jobs if j.kind == "kv_copy_out"}
+        for j in jobs:
+            if j.kind == "pre_attention" and (j.layer - 2, j.label.rsplit("/", 1)[1]) in kv_out:
+                o = kv_out[(j.layer - 2, j.label.rsplit("/", 1)[1])]
+                self.xwait[j.id] = sorted(set(self.xwait[j.id]) | {o})
+                self.need_event.add(o)
         if self.plan.B * self.arch.top_k < self.arch.n_experts:
             raise ValueError("B * top_k < experts: some experts would have no scheduled expert_compute job")
 
     def _stream_of(self, j) -> torch.cuda.Stream:
-        return self.h2d if j.resource == "htod_link" else self.stream
+        return {"htod_link": self.h2d, "dtoh_link": self.d2h}.get(j.resource, self.stream)
+
+    def _init_kv_stream(self, n_stores: int, n_pages: int) -> None:
+        """Full KV offload (reference memory_model.py:182-205): every sequence's pages live in pinned
+        host memory; HBM holds `kv_ring_n` micro-batch slices (the KV_COPY_IN ring) and one staging
+        page per sequence and store for the new token, double-buffered by layer parity."""
+        a, pe, bf = self.arch, self.page_elems, dict(dtype=BF16, device=self.device)
+        per_layer = n_pages * pe
+        host = torch.empty(a.layers * n_stores * per_layer, dtype=BF16).pin_memory()
+        self.kv_host = host
+        self.kv = [[host[(l * n_stores + s) * per_layer:(l * n_stores + s + 1) * per_layer] for s in range(n_stores)]
+                   for l in range(a.layers)]
+        slice_pages = self.plan.b_a * self.pps
+        self.kv_ring = [[torch.zeros(slice_pages * pe, **bf) for _ in range(n_stores)]
+                        for _ in range(max(1, self.kv_ring_n))]
+        self.kv_stage = [[torch.zeros(self.B * pe, **bf) for _ in range(n_stores)] for _ in range(2)]
+        i32 = dict(dtype=torch.int32, device=self.device)
+        # staging table: every page index of sequence b maps to staging page b
+        self.stage_table = torch.arange(self.B, **i32)[:, None].expand(self.B, self.pps).contiguous()
+        # ring-slot table: the micro-batch's sequence i owns slot pages [i*pps, (i+1)*pps)
+        self.slot_table = torch.arange(slice_pages, **i32).view(self.plan.b_a, self.pps)
+
+    def _kv_token_copy(self, src, src_table, dst, dst_table, s0: int, n: int) -> None:
+        ub, nu, us = self.kv_unit
+        nat.call("mgb_kv_token_copy", src.data_ptr(), src_table.data_ptr(), self.pps, dst.data_ptr(),
+                 dst_table.data_ptr(), self.pps, self.buf.positions[s0:].data_ptr(), n, self.page,
+                 self.page_elems * 2, ub, nu, us, torch.cuda.current_stream().cuda_stream)
+
+    def _kv_job(self, l: int, j) -> bool:
+        """KV_COPY_IN / KV_COPY_OUT jobs (offload_dag.py:372-392); returns False for other kinds."""
+        if j.kind == "kv_copy_in":
+            s0, s1 = self._mb_range(j)
+            r, pe, pps = self.kv_slot_of[j.id], self.page_elems, self.pps
+            for s, host in enumerate(self.kv[l]):
+                self.kv_ring[r][s][:(s1 - s0) * pps * pe].copy_(host[s0 * pps * pe:s1 * pps * pe], non_blocking=True)
+            return True
+        if j.kind == "kv_copy_out":
+            s0, s1 = self._mb_range(j)
+            for s, host in enumerate(self.kv[l]):
+                self._kv_token_copy(self.kv_stage[l % 2][s], self.stage_table[s0:], host, self.block_table[s0:],
+                                    s0, s1 - s0)
+            return True
+        return False
+
+    def _kv_views(self, l: int, j, s0: int, s1: int, phase: str):
+        """(stores, block_table rows from s0) the pre_attention append / attention of micro-batch
+        [s0, s1) of layer l work on.  Resident: the layer's page store.  Offloaded: the staging pages
+        for the append; for the attention the ring slot its copy-in filled, after the new token is
+        inserted into it."""
+        if self.kv_policy == "resident":
+            return self.kv[l], self.block_table[s0:]
+        if phase == "append":
+            return self.kv_stage[l % 2], self.stage_table[s0:]
+        kin = self.kin_of_mech[j.id]
+        slot = self.kv_ring[self.kv_slot_of[kin]]
+        for s in range(len(slot)):
+            self._kv_token_copy(self.kv_stage[l % 2][s], self.stage_table[s0:], slot[s], self.slot_table, s0, s1 - s0)
+        return slot, self.slot_table
 
     def _issue_layer(self, l: int) -> None:
         for j in self.layer_jobs[l]:
@@ -320,18 +418,20 @@ class Engine:
                 torch.mm(h, W["q_proj"].t(), out=m["q"][s0:s1])
             torch.mm(h, W["kv_a"].t(), out=m["ckv"][s0:s1])
             q_nope, q_lat, _, _ = self._ds_views(s0, s1)
+            (cache,), table = self._kv_views(l, j, s0, s1, "append")
             nat.call("mgb_mla_append", m["q"][s0:s1].data_ptr(), m["ckv"][s0:s1].data_ptr(),
                      W["kv_a_norm"].data_ptr(), a.rms_eps, s1 - s0, H, R, r, nope, b.positions[s0:].data_ptr(),
-                     self.cos_t.data_ptr(), self.sin_t.data_ptr(), self.block_table[s0:].data_ptr(), self.pps,
-                     self.latent[l].data_ptr(), q_nope.data_ptr(), m["q_pe"][s0:s1].data_ptr(),
+                     self.cos_t.data_ptr(), self.sin_t.data_ptr(), table.data_ptr(), self.pps,
+                     cache.data_ptr(), q_nope.data_ptr(), m["q_pe"][s0:s1].data_ptr(),
                      b.seq_lens[s0:].data_ptr(), torch.cuda.current_stream().cuda_stream)
             torch.bmm(q_nope, W["w_uk"], out=q_lat)
         elif j.kind == "attn_mech_gpu":
             s0, s1 = self._mb_range(j)
             _, q_lat, o_lat, o_hb = self._ds_views(s0, s1)
             scale = (a.qk_nope_dim + a.qk_rope_dim) ** -0.5
-            nat.call("mgb_decode_attn_mla", q_lat.data_ptr(), m["q_pe"][s0:s1].data_ptr(), self.latent[l].data_ptr(),
-                     self.block_table[s0:].data_ptr(), self.pps, b.seq_lens[s0:].data_ptr(), s1 - s0, H, R, r, scale,
+            (cache,), table = self._kv_views(l, j, s0, s1, "attend")
+            nat.call("mgb_decode_attn_mla", q_lat.data_ptr(), m["q_pe"][s0:s1].data_ptr(), cache.data_ptr(),
+                     table.data_ptr(), self.pps, b.seq_lens[s0:].data_ptr(), s1 - s0, H, R, r, scale,
                      o_lat.data_ptr(), torch.cuda.current_stream().cuda_stream)
             torch.bmm(o_lat, W["w_uv_t"], out=o_hb)
             m["o_cat"][s0:s1].view(s1 - s0, H, a.v_head_dim).copy_(o_hb.transpose(0, 1))
@@ -394,6 +494,8 @@ class Engine:
 
     def _issue_job(self, l: int, j) -> None:
         a, b = self.arch, self.buf
+        if self._kv_job(l, j):
+            return
         W = self._layer_weights(l)
         if self.mla:
             return self._ds_job(l, j, W)
@@ -411,12 +513,14 @@ class Engine:
                 if l == 0:  # later layers get h from the previous layer's fused combine+norm
                     ops.add_rmsnorm(b.x[s0:s1], W["ln1"], a.rms_eps, b.h[s0:s1])
                 torch.mm(b.h[s0:s1], W["wqkv"].t(), out=b.qkv[s0:s1])
+                (kc, vc), table = self._kv_views(l, j, 0, s1, "append")
                 ops.rope_append_gqa(b.qkv[s0:s1], s0, b.positions, self.cos_t, self.sin_t, Hq, Hkv, hd,
-                                    self.block_table, self.k_cache[l], self.v_cache[l], b.q[s0:s1], b.seq_lens)
+                                    table, kc, vc, b.q[s0:s1], b.seq_lens)
             elif j.kind == "attn_mech_gpu":
                 s0, s1 = self._mb_range(j)
-                ops.decode_attn_gqa(b.q[s0:s1], self.k_cache[l], self.v_cache[l], self.block_table[s0:s1],
-                                    b.seq_lens[s0:s1], Hq, Hkv, hd, b.attn[s0:s1])
+                (kc, vc), table = self._kv_views(l, j, s0, s1, "attend")
+                ops.decode_attn_gqa(b.q[s0:s1], kc, vc, table[:s1 - s0], b.seq_lens[s0:s1], Hq, Hkv, hd,
+                                    b.attn[s0:s1])
             elif j.kind == "post_attention":
                 torch.mm(b.attn, W["wo"].t(), out=b.o)
                 ops.add_rmsnorm(b.x, W["ln2"], a.rms_eps, b.h, delta=b.o, x_out=b.x)
@@ -457,6 +561,8 @@ class Engine:
     def _mb_range(self, j) -> tuple[int, int]:
         mb = int(j.label.rsplit("mb", 1)[1])
         s0 = mb * self.plan.b_a
+        if j.kind in ("kv_copy_in", "kv_copy_out"):  # copy jobs carry bytes, not seqs
+            return s0, min(s0 + self.plan.b_a, self.plan.gpu_sequences())
         return s0, s0 + j.seqs
 
     def _count_launches(self) -> int:
@@ -471,15 +577,20 @@ class Engine:
     def _step(self, record: bool = True) -> None:
         """One decode forward of all B sequences (one token each)."""
         a, b = self.arch, self.buf
-        if self.offload:  # fork the H2D copy stream off the compute stream
+        if self.streaming:  # fork the copy streams off the compute stream
             self._fork.record(self.stream)
             self.h2d.wait_event(self._fork)
+            if self.d2h is not None:
+                self.d2h.wait_event(self._fork)
         ops.embed(b.next_ids, self.w.embed, b.x)
         for l in range(a.layers):
             self._issue_layer(l)
-        if self.offload:  # join: the step ends when every copy has landed
+        if self.streaming:  # join: the step ends when every copy has landed
             self._join.record(self.h2d)
             self.stream.wait_event(self._join)
+            if self.d2h is not None:
+                self._join2.record(self.d2h)
+                self.stream.wait_event(self._join2)
         torch.mm(b.h, self.w.lm_head.t(), out=b.logits)
         ops.argmax(b.logits, b.next_ids)
         ops.decode_advance(b.next_ids, self.out_tokens if record else None, b.step, b.positions)
@@ -532,11 +643,13 @@ class Engine:
         prompt_len, so decode steps attend over prompt_len..prompt_len+decode_len keys."""
         from .weights import fill_uniform_
         for l in range(self.arch.layers):
-            if self.mla:
-                fill_uniform_(self.latent[l], seed, 10_000_000 + 2 * l, std)
-            else:
-                fill_uniform_(self.k_cache[l], seed, 10_000_000 + 2 * l, std)
-                fill_uniform_(self.v_cache[l], seed, 10_000_001 + 2 * l, std)
+            for s, store in enumerate(self.kv[l]):
+                tid = 10_000_000 + 2 * l + s  # MLA: one latent store per layer; GQA: K then V
+                if store.is_cuda:
+                    fill_uniform_(store, seed, tid, std)
+                else:  # host page store of the offloaded KV: generate on the device, then copy
+                    store.copy_(fill_uniform_(torch.empty_like(store, device=self.device), seed, tid, std))
+        torch.cuda.synchronize()
         self.reset(self.prompt_len)
 
     def decode(self, first_tokens: torch.Tensor, n_steps: int) -> torch.Tensor:
