@@ -30,6 +30,7 @@ from . import ops
 from .configs import ModelArch, get_arch
 from .planner import BatchingPlan, Hardware, ModelSpec, WorkloadSpec, largest_batch, load_plan
 from .schedule import Schedule, build_schedule
+from .hostmem import pinned_empty
 from .weights import DeepseekDeviceWeights, MixtralDeviceWeights
 
 BF16 = torch.bfloat16
@@ -128,13 +129,11 @@ class Engine:
                 self.layer_jobs[j.layer].append(j)
         self.offload = self.plan.s_params < self.spec.model_bytes
         self.kv_ring_cap = kv_ring_slots
-        if self.offload and self.mla:
-            raise NotImplementedError("weight offload is built for the Mixtral family; DeepSeek-V2 runs resident")
         self._plan_streams()
         # ---- weights ----
         if self.offload:
-            from .offload import OffloadedMixtralWeights
-            self.w = OffloadedMixtralWeights(a, self.spec, self.plan.s_params, self.plan.s_expert, seed=seed,
+            from .offload import OffloadedWeights
+            self.w = OffloadedWeights(a, self.spec, self.plan.s_params, self.plan.s_expert, seed=seed,
                                              device=device)
         elif self.mla:
             self.w = DeepseekDeviceWeights(a, seed=seed, device=device)
@@ -313,7 +312,7 @@ class Engine:
         page per sequence and store for the new token, double-buffered by layer parity."""
         a, pe, bf = self.arch, self.page_elems, dict(dtype=BF16, device=self.device)
         per_layer = n_pages * pe
-        host = torch.empty(a.layers * n_stores * per_layer, dtype=BF16).pin_memory()
+        host = pinned_empty(a.layers * n_stores * per_layer)
         self.kv_host = host
         self.kv = [[host[(l * n_stores + s) * per_layer:(l * n_stores + s + 1) * per_layer] for s in range(n_stores)]
                    for l in range(a.layers)]
@@ -332,6 +331,19 @@ class Engine:
         nat.call("mgb_kv_token_copy", src.data_ptr(), src_table.data_ptr(), self.pps, dst.data_ptr(),
                  dst_table.data_ptr(), self.pps, self.buf.positions[s0:].data_ptr(), n, self.page,
                  self.page_elems * 2, ub, nu, us, torch.cuda.current_stream().cuda_stream)
+
+    def _weight_copy_job(self, l: int, j) -> bool:
+        """WEIGHT_COPY (offload_dag.py:308-321,438-448): one DMA of a layer's dense blob into the single
+        dense buffer, or of one expert's [gate_up | down] blob into its slot."""
+        if j.kind != "weight_copy":
+            return False
+        if j.label.endswith("dense_copy"):
+            self.w.dense_buf.copy_(self.w.host_dense[l], non_blocking=True)
+        elif self.w.host_experts[l] is not None:  # (DeepSeek-V2's dense first layers have no experts)
+            e = int(j.label.split("/expert")[1].split("_")[0])
+            n_c = self.w.place.experts_per_layer[l]
+            self.w.slots[self.slot_of[(l, e)]].copy_(self.w.host_experts[l][e - n_c], non_blocking=True)
+        return True
 
     def _kv_job(self, l: int, j) -> bool:
         """KV_COPY_IN / KV_COPY_OUT jobs (offload_dag.py:372-392); returns False for other kinds."""
@@ -384,8 +396,7 @@ class Engine:
     def _layer_weights(self, l: int) -> dict:
         W = self.w.layers[l]
         if self.offload and l >= self.w.place.dense_layers:
-            wqkv, wo = self.w.dense_views()
-            W = dict(W, wqkv=wqkv, wo=wo)
+            W = dict(W, **self.w.dense_views())
         return W
 
     # ---- DeepSeek-V2 (MLA) jobs ------------------------------------------------------------
@@ -438,6 +449,13 @@ class Engine:
         elif j.kind == "post_attention":
             torch.mm(m["o_cat"], W["wo"].t(), out=b.o)
             ops.add_rmsnorm(b.x, W["ln2"], a.rms_eps, b.h, delta=b.o, x_out=b.x)
+            if l >= a.first_k_dense:
+                # shared experts on every token (DeepseekV2Moe.shared_experts): dense -> cuBLAS.  They are
+                # part of the layer's dense modules (dense_bytes_per_layer), so they run before the
+                # single dense buffer is handed to the next layer's copy (offload_dag.py:308-321)
+                torch.mm(b.h, W["sh_gate_up"][0].t(), out=m["sh_gu"])
+                ops.silu_mul(m["sh_gu"], m["sh_h"])
+                torch.mm(m["sh_h"], W["sh_down"][0].t(), out=m["sh_out"])
         elif j.kind == "router":
             if l >= a.first_k_dense:
                 # fp32 router logits (HF: F.linear(x.float(), W.float()), modeling_deepseek_v2.py:125) as a
@@ -449,28 +467,41 @@ class Engine:
                 if self.debug_taps is not None:
                     self.debug_taps.update(h2=b.h.clone(), topk_idx=self.rws.topk_idx.clone())
         elif j.kind == "expert_compute":
-            nxt = self.w.layers[l + 1]["ln1"] if l + 1 < a.layers else self.w.final_norm
-            first, last = j.id == self.first_expert_job[l], j.id == self.last_expert_job[l]
             if l < a.first_k_dense:
-                # dense MLP of the first layers (DeepseekV2MLP) on the same grouped kernel, E = 1
-                if first:  # dense GEMMs over all tokens: cuBLAS + fused SiLU*up
+                # dense MLP of the first layers (DeepseekV2MLP): cuBLAS + fused SiLU*up
+                if j.id == self.first_expert_job[l]:
+                    nxt = self.w.layers[l + 1]["ln1"] if l + 1 < a.layers else self.w.final_norm
                     F = a.dense_ffn
                     torch.mm(b.h, W["dense_gate_up"][0].t(), out=m["de_gu"][:, :2 * F])
                     ops.silu_mul(m["de_gu"][:, :2 * F], m["de_h"][:, :F])
                     torch.mm(m["de_h"][:, :F], W["dense_down"][0].t(), out=b.o)
                     ops.add_rmsnorm(b.x, nxt, a.rms_eps, b.h, delta=b.o, x_out=b.x)
                 return
-            if first:
-                self._routed_experts(W)
-                # shared experts on every token (DeepseekV2Moe.shared_experts): dense -> cuBLAS
-                torch.mm(b.h, W["sh_gate_up"][0].t(), out=m["sh_gu"])
-                ops.silu_mul(m["sh_gu"], m["sh_h"])
-                torch.mm(m["sh_h"], W["sh_down"][0].t(), out=m["sh_out"])
-            if last:
-                ops.unpermute_combine(b.y_perm, self.rws, b.x, self.B, residual=b.x, shared_out=m["sh_out"],
-                                      norm_w=nxt, eps=a.rms_eps, norm_out=b.h)
+            self._expert_job(l, j, W, shared_out=m["sh_out"])
         else:
             raise RuntimeError(f"job kind {j.kind!r} is not executable under kv_policy={self.kv_policy!r}")
+
+    def _expert_job(self, l: int, j, W: dict, shared_out=None) -> None:
+        """EXPERT_COMPUTE (offload_dag.py:449-463).  The b_e chunks of one expert run inside one
+        persistent grouped launch (the kernel's token tiles are the chunks); all HBM-resident experts
+        of the layer share one launch, each streamed expert runs from its slot once its copy has
+        landed; the layer's last job combines back to token order (+ shared experts, + residual) and
+        applies the next layer's input norm."""
+        a, b = self.arch, self.buf
+        e = int(j.label.split("/expert")[1].split("/")[0])
+        first_chunk = j.label.endswith("/chunk0")
+        n_c = self.w.place.experts_per_layer[l] if self.offload else a.n_experts
+        if j.id == self.first_expert_job[l] and n_c > 0:
+            self._routed_experts(W)
+        elif first_chunk and e >= n_c:
+            gu, dn = self.w.slot_views(self.slot_of[(l, e)])
+            offs = self.rws.offsets[e:e + 2]
+            ops.moe_gemm_gate_up(gu, b.x_perm, offs, b.h_ffn)
+            ops.moe_gemm_down(dn, b.h_ffn, offs, b.y_perm)
+        if j.id == self.last_expert_job[l]:
+            nxt = self.w.layers[l + 1]["ln1"] if l + 1 < a.layers else self.w.final_norm
+            ops.unpermute_combine(b.y_perm, self.rws, b.x, self.B, residual=b.x, shared_out=shared_out,
+                                  norm_w=nxt, eps=a.rms_eps, norm_out=b.h)
 
     def _routed_experts(self, W: dict) -> None:
         """Grouped expert FFN over the permuted rows; with expert parallelism the rows go to the
@@ -494,69 +525,45 @@ class Engine:
 
     def _issue_job(self, l: int, j) -> None:
         a, b = self.arch, self.buf
-        if self._kv_job(l, j):
+        if self._kv_job(l, j) or self._weight_copy_job(l, j):
             return
         W = self._layer_weights(l)
         if self.mla:
             return self._ds_job(l, j, W)
         hd, Hq, Hkv = a.head_dim, a.n_heads, a.n_kv_heads
-        if True:
-            if j.kind == "weight_copy":
-                if j.label.endswith("dense_copy"):
-                    self.w.dense_buf.copy_(self.w.host_dense[l], non_blocking=True)
-                else:
-                    e = int(j.label.split("/expert")[1].split("_")[0])
-                    n_c = self.w.place.experts_per_layer[l]
-                    self.w.slots[self.slot_of[(l, e)]].copy_(self.w.host_experts[l][e - n_c], non_blocking=True)
-            elif j.kind == "pre_attention":
-                s0, s1 = self._mb_range(j)
-                if l == 0:  # later layers get h from the previous layer's fused combine+norm
-                    ops.add_rmsnorm(b.x[s0:s1], W["ln1"], a.rms_eps, b.h[s0:s1])
-                torch.mm(b.h[s0:s1], W["wqkv"].t(), out=b.qkv[s0:s1])
-                (kc, vc), table = self._kv_views(l, j, 0, s1, "append")
-                ops.rope_append_gqa(b.qkv[s0:s1], s0, b.positions, self.cos_t, self.sin_t, Hq, Hkv, hd,
-                                    table, kc, vc, b.q[s0:s1], b.seq_lens)
-            elif j.kind == "attn_mech_gpu":
-                s0, s1 = self._mb_range(j)
-                (kc, vc), table = self._kv_views(l, j, s0, s1, "attend")
-                ops.decode_attn_gqa(b.q[s0:s1], kc, vc, table[:s1 - s0], b.seq_lens[s0:s1], Hq, Hkv, hd,
-                                    b.attn[s0:s1])
-            elif j.kind == "post_attention":
-                torch.mm(b.attn, W["wo"].t(), out=b.o)
-                ops.add_rmsnorm(b.x, W["ln2"], a.rms_eps, b.h, delta=b.o, x_out=b.x)
-            elif j.kind == "router":
-                if self.router_logits == "cublas":
-                    # gate GEMM on the tensor cores with fp32 output; the router kernel rounds it to
-                    # bf16 exactly as HF's bf16 F.linear does (modeling_mixtral.py:111)
-                    self.logits_r.copy_(torch.mm(b.h, W["router"].t(), out_dtype=torch.float32))
-                    ops.router_topk(None, None, self.rws, a.top_k, a.router_mode, a.routed_scaling, a.n_group,
-                                    a.topk_group, logits_in=self.logits_r)
-                else:
-                    ops.router_topk(b.h, W["router"], self.rws, a.top_k, a.router_mode, a.routed_scaling,
-                                    a.n_group, a.topk_group)
-                ops.permute(b.h, self.rws, b.x_perm)
-                if self.debug_taps is not None:  # eager-only parity hook
-                    self.debug_taps.update(h2=b.h.clone(), topk_idx=self.rws.topk_idx.clone(), attn=b.attn.clone())
-            elif j.kind == "expert_compute":
-                # b_e chunks of one expert run inside one persistent grouped launch (the kernel's
-                # token tiles are the chunks); all HBM-resident experts of the layer share one
-                # launch, each streamed expert runs from its slot once its copy has landed
-                e = int(j.label.split("/expert")[1].split("/")[0])
-                first_chunk = j.label.endswith("/chunk0")
-                n_c = self.w.place.experts_per_layer[l] if self.offload else a.n_experts
-                if j.id == self.first_expert_job[l] and n_c > 0:
-                    self._routed_experts(W)
-                elif first_chunk and e >= n_c:
-                    gu, dn = self.w.slot_views(self.slot_of[(l, e)])
-                    offs = self.rws.offsets[e:e + 2]
-                    ops.moe_gemm_gate_up(gu, b.x_perm, offs, b.h_ffn)
-                    ops.moe_gemm_down(dn, b.h_ffn, offs, b.y_perm)
-                if j.id == self.last_expert_job[l]:
-                    nxt = self.w.layers[l + 1]["ln1"] if l + 1 < a.layers else self.w.final_norm
-                    ops.unpermute_combine(b.y_perm, self.rws, b.x, self.B, residual=b.x, norm_w=nxt, eps=a.rms_eps,
-                                          norm_out=b.h)
+        if j.kind == "pre_attention":
+            s0, s1 = self._mb_range(j)
+            if l == 0:  # later layers get h from the previous layer's fused combine+norm
+                ops.add_rmsnorm(b.x[s0:s1], W["ln1"], a.rms_eps, b.h[s0:s1])
+            torch.mm(b.h[s0:s1], W["wqkv"].t(), out=b.qkv[s0:s1])
+            (kc, vc), table = self._kv_views(l, j, 0, s1, "append")
+            ops.rope_append_gqa(b.qkv[s0:s1], s0, b.positions, self.cos_t, self.sin_t, Hq, Hkv, hd,
+                                table, kc, vc, b.q[s0:s1], b.seq_lens)
+        elif j.kind == "attn_mech_gpu":
+            s0, s1 = self._mb_range(j)
+            (kc, vc), table = self._kv_views(l, j, s0, s1, "attend")
+            ops.decode_attn_gqa(b.q[s0:s1], kc, vc, table[:s1 - s0], b.seq_lens[s0:s1], Hq, Hkv, hd,
+                                b.attn[s0:s1])
+        elif j.kind == "post_attention":
+            torch.mm(b.attn, W["wo"].t(), out=b.o)
+            ops.add_rmsnorm(b.x, W["ln2"], a.rms_eps, b.h, delta=b.o, x_out=b.x)
+        elif j.kind == "router":
+            if self.router_logits == "cublas":
+                # gate GEMM on the tensor cores with fp32 output; the router kernel rounds it to
+                # bf16 exactly as HF's bf16 F.linear does (modeling_mixtral.py:111)
+                self.logits_r.copy_(torch.mm(b.h, W["router"].t(), out_dtype=torch.float32))
+                ops.router_topk(None, None, self.rws, a.top_k, a.router_mode, a.routed_scaling, a.n_group,
+                                a.topk_group, logits_in=self.logits_r)
             else:
-                raise RuntimeError(f"job kind {j.kind!r} is not executable under kv_policy={self.kv_policy!r}")
+                ops.router_topk(b.h, W["router"], self.rws, a.top_k, a.router_mode, a.routed_scaling,
+                                a.n_group, a.topk_group)
+            ops.permute(b.h, self.rws, b.x_perm)
+            if self.debug_taps is not None:  # eager-only parity hook
+                self.debug_taps.update(h2=b.h.clone(), topk_idx=self.rws.topk_idx.clone(), attn=b.attn.clone())
+        elif j.kind == "expert_compute":
+            self._expert_job(l, j, W)
+        else:
+            raise RuntimeError(f"job kind {j.kind!r} is not executable under kv_policy={self.kv_policy!r}")
 
     def _mb_range(self, j) -> tuple[int, int]:
         mb = int(j.label.rsplit("mb", 1)[1])
@@ -603,6 +610,7 @@ class Engine:
             return
         # snapshot mutable state: the eager warm-up step must not advance it
         snap = [t.clone() for t in (self.buf.positions, self.buf.step, self.buf.next_ids, self.buf.seq_lens)]
+        self.stream.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(self.stream):
             self._step()
         torch.cuda.current_stream().wait_stream(self.stream)
@@ -623,7 +631,8 @@ class Engine:
             if self.graph is None:
                 self.capture()
             self.graph.replay()
-        else:
+        else:  # eager issue on the engine stream, ordered after the caller's stream both ways
+            self.stream.wait_stream(torch.cuda.current_stream())
             with torch.cuda.stream(self.stream):
                 self._step()
             torch.cuda.current_stream().wait_stream(self.stream)
@@ -685,6 +694,7 @@ class Engine:
         tensors of layer 0 and the logits (parity tests)."""
         self.buf.positions.fill_(pos)
         self.buf.next_ids.copy_(tokens.to(torch.int32))
+        self.stream.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(self.stream):
             self._step(record=False)
         torch.cuda.current_stream().wait_stream(self.stream)
@@ -700,6 +710,7 @@ class Engine:
         self.trace_events = {}
         t0 = torch.cuda.Event(enable_timing=True)
         saved = [t.clone() for t in (self.buf.positions, self.buf.step, self.buf.next_ids, self.buf.seq_lens)]
+        self.stream.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(self.stream):
             torch.cuda._sleep(int(5e7))  # host enqueues the whole step before the GPU starts
             t0.record(self.stream)

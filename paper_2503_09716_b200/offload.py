@@ -18,77 +18,96 @@ from __future__ import annotations
 import torch
 
 from .configs import ModelArch
+from .hostmem import pinned_empty
 from .planner import placement, ModelSpec
-from .weights import TID_EMBED, TID_LM_HEAD, fill_const_, fill_uniform_, tid
+from .weights import (DERIVED, TID_EMBED, TID_LM_HEAD, deepseek_layer, dense_keys, derive_views, fill_const_,
+                      fill_uniform_, mixtral_layer)
 
 BF16 = torch.bfloat16
 
 
-class OffloadedMixtralWeights:
+class OffloadedWeights:
+    """Weights of either family (Mixtral, DeepSeek-V2) split between HBM and pinned host memory by
+    the reference's cache placement.  DeepSeek-V2's dense first layers (first_k_dense MLP) and all
+    norms / router gates are small and stay resident; the dense modules of a layer are its
+    attention projections plus its shared experts (the reference's dense_bytes_per_layer)."""
+
     def __init__(self, arch: ModelArch, spec: ModelSpec, s_params: int, s_expert: int, seed: int = 0,
                  device: str = "cuda"):
         a = arch
-        d, hd, f, E = a.hidden, a.head_dim, a.moe_ffn, a.n_experts
-        qd, kvd = a.n_heads * hd, a.n_kv_heads * hd
+        d, f, E = a.hidden, a.moe_ffn, a.n_experts
         std = a.init_std
         bf = dict(dtype=BF16, device=device)
         self.arch = a
         self.place = placement(spec, s_params)
+        if a.is_mla and self.place.dense_layers < a.first_k_dense:
+            raise ValueError("DeepSeek-V2 offload keeps the dense first layers resident: s_params too small")
         self.n_slots = s_expert // spec.expert_bytes if spec.expert_bytes else 0
         if self.place.uncached_expert_count > 0 and self.n_slots < 2:
             raise ValueError("offloaded experts need at least 2 expert slots (double buffering)")
         self.embed = fill_uniform_(torch.empty(a.vocab, d, **bf), seed, TID_EMBED, std)
         self.final_norm = fill_const_(torch.empty(d, **bf), 1.0)
         self.lm_head = fill_uniform_(torch.empty(a.vocab, d, **bf), seed, TID_LM_HEAD, std)
-        self.dense_elems = (qd + 2 * kvd) * d + d * qd
+        build = deepseek_layer if a.is_mla else mixtral_layer
+        self.dense_keys = dense_keys(a)
+        self.dense_shapes: dict[str, tuple] | None = None
+        self.dense_elems = 0
         self.expert_elems = 3 * d * f
-        self.dense_buf = torch.empty(self.dense_elems, **bf) if self.place.dense_layers < a.layers else None
+        self.dense_buf = None
         self.slots = torch.empty(max(self.n_slots, 0), self.expert_elems, **bf)
-        self.layers = []
+        self.layers: list[dict] = []
         self.host_dense: list[torch.Tensor | None] = []
         self.host_experts: list[torch.Tensor | None] = []
-        stage = torch.empty(max(self.dense_elems, self.expert_elems), **bf)
+        moe_first = a.first_k_dense if a.is_mla else 0
         for l in range(a.layers):
-            L = dict(ln1=fill_const_(torch.empty(d, **bf), 1.0), ln2=fill_const_(torch.empty(d, **bf), 1.0),
-                     router=fill_uniform_(torch.empty(E, d, **bf), seed, tid(l, "router"), std))
-            # dense (attention) weights: resident or one pinned blob [wqkv | wo]
-            dense = torch.empty(self.dense_elems, **bf) if l < self.place.dense_layers else stage[:self.dense_elems]
-            wqkv = dense[:(qd + 2 * kvd) * d].view(qd + 2 * kvd, d)
-            fill_uniform_(wqkv[:qd], seed, tid(l, "wq"), std)
-            fill_uniform_(wqkv[qd:qd + kvd], seed, tid(l, "wk"), std)
-            fill_uniform_(wqkv[qd + kvd:], seed, tid(l, "wv"), std)
-            fill_uniform_(dense[(qd + 2 * kvd) * d:].view(d, qd), seed, tid(l, "wo"), std)
+            L = build(a, l, seed, device)  # generated on the device (bit-identical to the resident build)
+            if l >= moe_first and self.dense_shapes is None:
+                self.dense_shapes = {k: tuple(L[k].shape) for k in self.dense_keys}
+                self.dense_elems = sum(L[k].numel() for k in self.dense_keys)
+                assert self.dense_elems * 2 == spec.dense_bytes_per_layer, "dense blob != reference dense bytes"
+                if self.place.dense_layers < a.layers:
+                    self.dense_buf = torch.empty(self.dense_elems, **bf)
+            # dense modules: resident, or one pinned blob (one DMA per layer, offload_dag.py:308-321)
             if l < self.place.dense_layers:
-                L["wqkv"], L["wo"] = wqkv, dense[(qd + 2 * kvd) * d:].view(d, qd)
                 self.host_dense.append(None)
             else:
-                self.host_dense.append(dense.cpu().pin_memory())
-            # experts: generate the full per-layer tensors (tensor-id indexing), keep the cached
-            # prefix in HBM, move the rest to one pinned blob per expert
+                blob = pinned_empty(self.dense_elems)
+                o = 0
+                for k in self.dense_keys:
+                    t = L.pop(k).reshape(-1)
+                    blob[o:o + t.numel()].copy_(t)
+                    o += t.numel()
+                self.host_dense.append(blob)
+                for k in DERIVED:
+                    L.pop(k, None)
+            # routed experts: keep the cached prefix in HBM, one pinned blob [gate_up | down] per other expert
             n_c = self.place.experts_per_layer[l]
-            gu = fill_uniform_(torch.empty(E, 2 * f, d, **bf), seed, tid(l, "w_gate_up"), std)
-            dn = fill_uniform_(torch.empty(E, d, f, **bf), seed, tid(l, "w_down"), std)
-            L["w_gate_up"] = gu[:n_c].clone() if n_c > 0 else None
-            L["w_down"] = dn[:n_c].clone() if n_c > 0 else None
-            if n_c < E:
-                blob = torch.empty(E - n_c, self.expert_elems, dtype=BF16).pin_memory()
-                for e in range(n_c, E):
-                    row = torch.cat([gu[e].reshape(-1), dn[e].reshape(-1)])
-                    blob[e - n_c].copy_(row)
+            if "w_gate_up" in L and n_c < E:
+                gu, dn = L["w_gate_up"], L["w_down"]
+                blob = pinned_empty((E - n_c) * self.expert_elems).view(E - n_c, self.expert_elems)
+                g = 2 * f * d
+                blob[:, :g].copy_(gu[n_c:].reshape(E - n_c, g))
+                blob[:, g:].copy_(dn[n_c:].reshape(E - n_c, d * f))
                 self.host_experts.append(blob)
+                L["w_gate_up"] = gu[:n_c].clone() if n_c > 0 else None
+                L["w_down"] = dn[:n_c].clone() if n_c > 0 else None
+                del gu, dn
             else:
                 self.host_experts.append(None)
-            del gu, dn
             self.layers.append(L)
         torch.cuda.synchronize()
 
-    # views into the streamed buffers
-    def dense_views(self):
-        a = self.arch
-        d, hd = a.hidden, a.head_dim
-        qd, kvd = a.n_heads * hd, a.n_kv_heads * hd
-        return (self.dense_buf[:(qd + 2 * kvd) * d].view(qd + 2 * kvd, d),
-                self.dense_buf[(qd + 2 * kvd) * d:].view(d, qd))
+    def dense_views(self) -> dict:
+        """The streamed dense modules as views into the single dense buffer."""
+        out, o = {}, 0
+        for k in self.dense_keys:
+            shape = self.dense_shapes[k]
+            n = 1
+            for x in shape:
+                n *= x
+            out[k] = self.dense_buf[o:o + n].view(shape)
+            o += n
+        return derive_views(self.arch, out)
 
     def slot_views(self, s: int):
         a = self.arch
@@ -99,3 +118,6 @@ class OffloadedMixtralWeights:
     def host_bytes(self) -> int:
         n = sum(t.nbytes for t in self.host_dense if t is not None)
         return n + sum(t.nbytes for t in self.host_experts if t is not None)
+
+
+OffloadedMixtralWeights = OffloadedWeights

@@ -36,43 +36,55 @@ def fill_const_(t: torch.Tensor, value: float) -> torch.Tensor:
     return t
 
 
-class MixtralDeviceWeights:
-    """Mixtral-family weights in the engine's layout.  q/k/v projections are stored fused as
-    one [Hq*hd + 2*Hkv*hd, d] matrix (rows = wq | wk | wv), each part generated with its own
-    tensor id so it equals the oracle's separate wq/wk/wv."""
+def mixtral_layer(a: ModelArch, l: int, seed: int, device: str = "cuda") -> dict:
+    """Layer l of a Mixtral-family model in the engine's layout.  q/k/v projections are stored
+    fused as one [Hq*hd + 2*Hkv*hd, d] matrix (rows = wq | wk | wv), each part generated with its
+    own tensor id so it equals the oracle's separate wq/wk/wv."""
+    d, hd = a.hidden, a.head_dim
+    qd, kvd = a.n_heads * hd, a.n_kv_heads * hd
+    std = a.init_std
+    bf = dict(dtype=torch.bfloat16, device=device)
+    wqkv = torch.empty(qd + 2 * kvd, d, **bf)
+    fill_uniform_(wqkv[:qd], seed, tid(l, "wq"), std)
+    fill_uniform_(wqkv[qd:qd + kvd], seed, tid(l, "wk"), std)
+    fill_uniform_(wqkv[qd + kvd:], seed, tid(l, "wv"), std)
+    return dict(
+        ln1=fill_const_(torch.empty(d, **bf), 1.0),
+        wqkv=wqkv,
+        wo=fill_uniform_(torch.empty(d, qd, **bf), seed, tid(l, "wo"), std),
+        ln2=fill_const_(torch.empty(d, **bf), 1.0),
+        router=fill_uniform_(torch.empty(a.n_experts, d, **bf), seed, tid(l, "router"), std),
+        w_gate_up=fill_uniform_(torch.empty(a.n_experts, 2 * a.moe_ffn, d, **bf), seed, tid(l, "w_gate_up"), std),
+        w_down=fill_uniform_(torch.empty(a.n_experts, d, a.moe_ffn, **bf), seed, tid(l, "w_down"), std),
+    )
+
+
+class _DeviceWeights:
+    """All weights HBM-resident, generated layer by layer by the family's layer builder."""
 
     def __init__(self, arch: ModelArch, seed: int = 0, device: str = "cuda"):
         a = arch
-        d, hd = a.hidden, a.head_dim
-        qd, kvd = a.n_heads * hd, a.n_kv_heads * hd
-        std = a.init_std
         bf = dict(dtype=torch.bfloat16, device=device)
         self.arch = a
-        self.embed = fill_uniform_(torch.empty(a.vocab, d, **bf), seed, TID_EMBED, std)
-        self.final_norm = fill_const_(torch.empty(d, **bf), 1.0)
-        self.lm_head = fill_uniform_(torch.empty(a.vocab, d, **bf), seed, TID_LM_HEAD, std)
-        self.layers = []
-        for l in range(a.layers):
-            wqkv = torch.empty(qd + 2 * kvd, d, **bf)
-            fill_uniform_(wqkv[:qd], seed, tid(l, "wq"), std)
-            fill_uniform_(wqkv[qd:qd + kvd], seed, tid(l, "wk"), std)
-            fill_uniform_(wqkv[qd + kvd:], seed, tid(l, "wv"), std)
-            self.layers.append(dict(
-                ln1=fill_const_(torch.empty(d, **bf), 1.0),
-                wqkv=wqkv,
-                wo=fill_uniform_(torch.empty(d, qd, **bf), seed, tid(l, "wo"), std),
-                ln2=fill_const_(torch.empty(d, **bf), 1.0),
-                router=fill_uniform_(torch.empty(a.n_experts, d, **bf), seed, tid(l, "router"), std),
-                w_gate_up=fill_uniform_(torch.empty(a.n_experts, 2 * a.moe_ffn, d, **bf), seed,
-                                        tid(l, "w_gate_up"), std),
-                w_down=fill_uniform_(torch.empty(a.n_experts, d, a.moe_ffn, **bf), seed, tid(l, "w_down"), std),
-            ))
+        self.embed = fill_uniform_(torch.empty(a.vocab, a.hidden, **bf), seed, TID_EMBED, a.init_std)
+        self.final_norm = fill_const_(torch.empty(a.hidden, **bf), 1.0)
+        self.lm_head = fill_uniform_(torch.empty(a.vocab, a.hidden, **bf), seed, TID_LM_HEAD, a.init_std)
+        build = deepseek_layer if a.is_mla else mixtral_layer
+        self.layers = [build(a, l, seed, device) for l in range(a.layers)]
 
     def nbytes(self) -> int:
         n = self.embed.nbytes + self.final_norm.nbytes + self.lm_head.nbytes
         for L in self.layers:
-            n += sum(t.nbytes for t in L.values())
+            n += sum(t.nbytes for k, t in L.items() if k not in DERIVED)
         return n
+
+
+class MixtralDeviceWeights(_DeviceWeights):
+    pass
+
+
+class DeepseekDeviceWeights(_DeviceWeights):
+    pass
 
 
 DS_SLOT = dict(ln1=0, ln2=5, router=6, w_gate_up=7, w_down=8, q_proj=10, q_a_norm=11, q_b=12, kv_a=13,
@@ -83,45 +95,52 @@ def ds_tid(layer: int, name: str) -> int:
     return LAYER_BASE + LAYER_STRIDE * layer + DS_SLOT[name]
 
 
-class DeepseekDeviceWeights:
-    """DeepSeek-V2 family weights in HF layouts (q_proj or q_a/q_b, kv_a_proj_with_mqa, kv_b_proj,
-    o_proj; routed experts [E,2f,d]/[E,d,f]; shared experts and the dense first layers as fused
-    gate|up [2f,d] + down [d,f]).  Tensor ids mirror oracle/moe_ref.py DS_SLOT."""
+def deepseek_layer(a: ModelArch, l: int, seed: int, device: str = "cuda") -> dict:
+    """Layer l of a DeepSeek-V2-family model in HF layouts (q_proj or q_a/q_b, kv_a_proj_with_mqa,
+    kv_b_proj, o_proj; routed experts [E,2f,d]/[E,d,f]; shared experts and the dense first layers
+    as fused gate|up [2f,d] + down [d,f]).  Tensor ids mirror oracle/moe_ref.py DS_SLOT."""
+    d, H = a.hidden, a.n_heads
+    qk = a.qk_nope_dim + a.qk_rope_dim
+    std = a.init_std
+    bf = dict(dtype=torch.bfloat16, device=device)
+    U = lambda shape, name: fill_uniform_(torch.empty(*shape, **bf), seed, ds_tid(l, name), std)  # noqa: E731
+    ones = lambda n: fill_const_(torch.empty(n, **bf), 1.0)  # noqa: E731
+    L = dict(ln1=ones(d), ln2=ones(d), kv_a=U((a.kv_lora_rank + a.qk_rope_dim, d), "kv_a"),
+             kv_a_norm=ones(a.kv_lora_rank), kv_b=U((H * (a.qk_nope_dim + a.v_head_dim), a.kv_lora_rank), "kv_b"),
+             wo=U((d, H * a.v_head_dim), "wo"))
+    if a.q_lora_rank:
+        L.update(q_a=U((a.q_lora_rank, d), "q_proj"), q_a_norm=ones(a.q_lora_rank), q_b=U((H * qk, a.q_lora_rank), "q_b"))
+    else:
+        L["q_proj"] = U((H * qk, d), "q_proj")
+    if l < a.first_k_dense:
+        L.update(dense_gate_up=U((1, 2 * a.dense_ffn, d), "dense_gate_up"),
+                 dense_down=U((1, d, a.dense_ffn), "dense_down"))
+    else:
+        fs = a.moe_ffn * a.n_shared
+        L.update(router=U((a.n_experts, d), "router"), w_gate_up=U((a.n_experts, 2 * a.moe_ffn, d), "w_gate_up"),
+                 w_down=U((a.n_experts, d, a.moe_ffn), "w_down"), sh_gate_up=U((1, 2 * fs, d), "sh_gate_up"),
+                 sh_down=U((1, d, fs), "sh_down"))
+    derive_views(a, L)
+    return L
 
-    def __init__(self, arch: ModelArch, seed: int = 0, device: str = "cuda"):
-        a = arch
-        d, H = a.hidden, a.n_heads
-        qk = a.qk_nope_dim + a.qk_rope_dim
-        std = a.init_std
-        bf = dict(dtype=torch.bfloat16, device=device)
-        U = lambda shape, name, l: fill_uniform_(torch.empty(*shape, **bf), seed, ds_tid(l, name), std)  # noqa: E731
-        ones = lambda n: fill_const_(torch.empty(n, **bf), 1.0)  # noqa: E731
-        self.arch = a
-        self.embed = fill_uniform_(torch.empty(a.vocab, d, **bf), seed, TID_EMBED, std)
-        self.final_norm = ones(d)
-        self.lm_head = fill_uniform_(torch.empty(a.vocab, d, **bf), seed, TID_LM_HEAD, std)
-        self.layers = []
-        for l in range(a.layers):
-            L = dict(ln1=ones(d), ln2=ones(d), kv_a=U((a.kv_lora_rank + a.qk_rope_dim, d), "kv_a", l),
-                     kv_a_norm=ones(a.kv_lora_rank),
-                     kv_b=U((H * (a.qk_nope_dim + a.v_head_dim), a.kv_lora_rank), "kv_b", l),
-                     wo=U((d, H * a.v_head_dim), "wo", l))
-            if a.q_lora_rank:
-                L.update(q_a=U((a.q_lora_rank, d), "q_proj", l), q_a_norm=ones(a.q_lora_rank),
-                         q_b=U((H * qk, a.q_lora_rank), "q_b", l))
-            else:
-                L["q_proj"] = U((H * qk, d), "q_proj", l)
-            if l < a.first_k_dense:
-                L.update(dense_gate_up=U((1, 2 * a.dense_ffn, d), "dense_gate_up", l),
-                         dense_down=U((1, d, a.dense_ffn), "dense_down", l))
-            else:
-                fs = a.moe_ffn * a.n_shared
-                L.update(router=U((a.n_experts, d), "router", l),
-                         w_gate_up=U((a.n_experts, 2 * a.moe_ffn, d), "w_gate_up", l),
-                         w_down=U((a.n_experts, d, a.moe_ffn), "w_down", l),
-                         sh_gate_up=U((1, 2 * fs, d), "sh_gate_up", l), sh_down=U((1, d, fs), "sh_down", l))
-            # absorption views of kv_b_proj: rows [h*(nope+v), h*(nope+v)+nope) = W_UK_h, rest = W_UV_h
-            kvb = L["kv_b"].view(H, a.qk_nope_dim + a.v_head_dim, a.kv_lora_rank)
-            L["w_uk"] = kvb[:, :a.qk_nope_dim, :]          # [H, nope, R]
-            L["w_uv_t"] = kvb[:, a.qk_nope_dim:, :].transpose(1, 2)  # [H, R, v]
-            self.layers.append(L)
+
+DERIVED = ("w_uk", "w_uv_t")
+
+
+def derive_views(a: ModelArch, L: dict) -> dict:
+    """Absorption views of kv_b_proj: rows [h*(nope+v), h*(nope+v)+nope) = W_UK_h, rest = W_UV_h."""
+    if a.is_mla:
+        kvb = L["kv_b"].view(a.n_heads, a.qk_nope_dim + a.v_head_dim, a.kv_lora_rank)
+        L["w_uk"] = kvb[:, :a.qk_nope_dim, :]                     # [H, nope, R]
+        L["w_uv_t"] = kvb[:, a.qk_nope_dim:, :].transpose(1, 2)   # [H, R, v]
+    return L
+
+
+def dense_keys(a: ModelArch) -> list[str]:
+    """The per-layer 'dense' modules of the reference's memory model (attention weights + shared
+    experts, model_catalog.py:55-88 dense_bytes_per_layer): streamed through the single dense
+    buffer when the layer is not cached."""
+    if not a.is_mla:
+        return ["wqkv", "wo"]
+    q = ["q_a", "q_b"] if a.q_lora_rank else ["q_proj"]
+    return q + ["kv_a", "kv_b", "wo", "sh_gate_up", "sh_down"]

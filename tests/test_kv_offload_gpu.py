@@ -30,7 +30,12 @@ def test_kv_token_copy(unit, n_units, page, host_dst):
     page_bytes = n_units * unit * page
     src = torch.randint(0, 255, (B * pps * page_bytes,), dtype=torch.uint8, device="cuda")
     dst = torch.zeros(B * pps * page_bytes, dtype=torch.uint8)
-    dst = dst.pin_memory() if host_dst else dst.cuda()
+    if host_dst:  # registered in place, as the engine's host stores are (hostmem.py)
+        from paper_2503_09716_b200.hostmem import pinned_empty
+
+        dst = pinned_empty(dst.numel(), torch.uint8).zero_()
+    else:
+        dst = dst.cuda()
     src_table = torch.randperm(B * pps, dtype=torch.int32).view(B, pps).cuda()
     dst_table = torch.randperm(B * pps, dtype=torch.int32).view(B, pps).cuda()
     pos = torch.tensor([0, page - 1, page, 2 * page + 7, 3 * page - 1], dtype=torch.int32, device="cuda")
@@ -88,3 +93,33 @@ def test_kv_offload_decode_across_pages(family):
     assert rep["bytes_htod"] == A.layers * B * (P + N) * kv
     assert rep["bytes_dtoh"] == A.layers * B * kv
     assert {r["kind"] for r in recs} >= {"kv_copy_in", "kv_copy_out", "attn_mech_gpu"}
+
+
+def test_dsv2_offloaded_weights_and_kv_match_resident():
+    """DeepSeek-V2 module-based batching with weights partly in pinned host memory (dense modules =
+    MLA projections + shared experts through the single dense buffer; routed experts through the
+    slots) and, on top, the KV store offloaded: bit-identical to the resident engine; the trace's
+    H2D bytes are the uncached weight bytes plus the KV_COPY_IN bytes."""
+    from paper_2503_09716_b200.configs import TINY_DSV2 as A
+    from paper_2503_09716_b200.engine import Engine
+    from paper_2503_09716_b200.planner import BatchingPlan, ModelSpec, placement
+
+    spec = ModelSpec.from_document(A.model_spec_document())
+    dense, ex = spec.dense_bytes_per_layer, spec.expert_bytes
+    B, P, N = 8, 4, 5
+    ids = torch.randint(0, A.vocab, (B, P), generator=torch.Generator().manual_seed(13))
+    ref = Engine(A, BatchingPlan(B, 4, 16, 0.0, 0, spec.model_bytes), prompt_len=P, decode_len=N,
+                 use_graph=False).generate(ids, N)
+    two_layers = 2 * dense + ((dense - 1) // ex) * ex  # 2 dense layers cached + a few experts
+    for s_params, slots, policy in ((dense + dense // 2, 2, "resident"), (two_layers, 3, "offload")):
+        plan = BatchingPlan(B, 4, 16, 0.0, slots * ex, s_params)
+        pl = placement(spec, s_params)
+        assert pl.uncached_expert_count > 0 and pl.dense_layers < A.layers
+        for graph in (False, True):
+            eng = Engine(A, plan, prompt_len=P, decode_len=N, use_graph=graph, kv_policy=policy)
+            assert eng.offload
+            assert torch.equal(eng.generate(ids, N), ref), (s_params, policy, graph)
+        recs, rep = eng.trace_step()
+        uncached = (A.layers - pl.dense_layers) * dense + pl.uncached_expert_count * ex
+        kv_in = A.layers * B * (P + N) * A.kv_bytes_per_token_layer if policy == "offload" else 0
+        assert rep["bytes_htod"] == uncached + kv_in  # schedule bytes (the reference's accounting)
