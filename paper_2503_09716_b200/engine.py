@@ -129,6 +129,9 @@ class Engine:
                 self.layer_jobs[j.layer].append(j)
         self.offload = self.plan.s_params < self.spec.model_bytes
         self.kv_ring_cap = kv_ring_slots
+        # measurement only: False issues every job except the host<->device copies (compute-only
+        # step time for the transfer/compute overlap figure; outputs are then meaningless)
+        self.copies_enabled = True
         self._plan_streams()
         # ---- weights ----
         if self.offload:
@@ -300,8 +303,80 @@ class Engine:
                 o = kv_out[(j.layer - 2, j.label.rsplit("/", 1)[1])]
                 self.xwait[j.id] = sorted(set(self.xwait[j.id]) | {o})
                 self.need_event.add(o)
+        self._plan_lookahead(jobs, preds, mech_of_kin)
         if self.plan.B * self.arch.top_k < self.arch.n_experts:
             raise ValueError("B * top_k < experts: some experts would have no scheduled expert_compute job")
+
+    def _plan_lookahead(self, jobs, preds, mech_of_kin) -> None:
+        """Cross-step copy lookahead.  The leading H2D copies of a step that wait on no compute of
+        their own step (the first dense copy, the first `slots` expert copies, the first `ring` KV
+        slices: the schedule gives them no recycle edge) are issued at the END of the previous step,
+        once that step's last user of the buffer they overwrite is done (and, for a KV slice, once
+        that step's KV_COPY_OUT of the same slice has landed on the host).  The host link then keeps
+        streaming through the step boundary instead of idling while the GPU drains the last layer
+        and starts the next.  The first step of a decode call gets them from an eager prologue."""
+        copies = [j for j in jobs if j.resource == "htod_link"]
+        self.lookahead: list = []
+        for c in copies:
+            if any(jobs[p].resource not in (None, "htod_link") for p in preds[c.id]):
+                break
+            self.lookahead.append(c)
+        ids = {c.id for c in self.lookahead}
+        self.lookahead_waits: dict[int, list[int]] = {}
+        succ = self.schedule.succs()
+        last_dense = [c for c in copies if c.label.endswith("dense_copy")]
+        kv_out = {(j.layer, j.label.rsplit("/", 1)[1]): j.id for j in jobs if j.kind == "kv_copy_out"}
+        for c in self.lookahead:
+            if c.label.endswith("dense_copy"):  # single dense buffer: post_attention of the last streamed layer
+                L = last_dense[-1].layer
+                w = [next(j.id for j in jobs if j.kind == "post_attention" and j.layer == L)]
+            elif c.kind == "weight_copy":  # expert slot: last consumer of the last copy into that slot
+                slot = self.slot_of[(c.layer, int(c.label.split("/expert")[1].split("_")[0]))]
+                last = [x for x in copies if x.kind == "weight_copy" and not x.label.endswith("dense_copy")
+                        and self.slot_of[(x.layer, int(x.label.split("/expert")[1].split("_")[0]))] == slot][-1]
+                w = [max(v for v in succ[last.id] if jobs[v].kind == "expert_compute")]
+            else:  # KV ring slot + the same slice's new-token write-back
+                r = self.kv_slot_of[c.id]
+                last = [x for x in copies if x.kind == "kv_copy_in" and self.kv_slot_of[x.id] == r][-1]
+                w = [mech_of_kin[last.id], kv_out[(c.layer, c.label.rsplit("/", 1)[1])]]
+            self.lookahead_waits[c.id] = w
+            self.need_event.update(w)
+        # consumers in the step no longer wait on the (previous-step) lookahead copies
+        for jid, ws in self.xwait.items():
+            self.xwait[jid] = [p for p in ws if p not in ids]
+        self.need_event -= ids
+        self._lookahead_ids = ids
+        self._primed = False
+
+    def _issue_lookahead(self, prologue: bool) -> None:
+        """Issue the lookahead copies on the H2D stream: as the eager prologue of a decode call, or
+        at the end of a step for the next one (after their buffers' last users in this step)."""
+        if not self.lookahead:
+            return
+        for c in self.lookahead:
+            if not prologue:
+                for p in self.lookahead_waits[c.id]:
+                    self.h2d.wait_event(self.events[p])
+            te = None if prologue else self.trace_events
+            with torch.cuda.stream(self.h2d):
+                if te is not None:
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(self.h2d)
+                self._kv_job(c.layer, c) or self._weight_copy_job(c.layer, c)
+                if te is not None:
+                    e1.record(self.h2d)
+                    te[c.id] = (e0, e1)
+        self._primed = True
+
+    def prime(self) -> None:
+        """Eager prologue: land the lookahead copies the first step of a decode call expects."""
+        if self._primed or not self.streaming:
+            return
+        self.h2d.wait_stream(self.stream)
+        self.h2d.wait_stream(torch.cuda.current_stream())
+        self._issue_lookahead(prologue=True)
+        self.stream.wait_stream(self.h2d)
+        torch.cuda.current_stream().wait_stream(self.h2d)
 
     def _stream_of(self, j) -> torch.cuda.Stream:
         return {"htod_link": self.h2d, "dtoh_link": self.d2h}.get(j.resource, self.stream)
@@ -337,6 +412,8 @@ class Engine:
         dense buffer, or of one expert's [gate_up | down] blob into its slot."""
         if j.kind != "weight_copy":
             return False
+        if not self.copies_enabled:
+            return True
         if j.label.endswith("dense_copy"):
             self.w.dense_buf.copy_(self.w.host_dense[l], non_blocking=True)
         elif self.w.host_experts[l] is not None:  # (DeepSeek-V2's dense first layers have no experts)
@@ -347,6 +424,8 @@ class Engine:
 
     def _kv_job(self, l: int, j) -> bool:
         """KV_COPY_IN / KV_COPY_OUT jobs (offload_dag.py:372-392); returns False for other kinds."""
+        if j.kind in ("kv_copy_in", "kv_copy_out") and not self.copies_enabled:
+            return True
         if j.kind == "kv_copy_in":
             s0, s1 = self._mb_range(j)
             r, pe, pps = self.kv_slot_of[j.id], self.page_elems, self.pps
@@ -377,7 +456,10 @@ class Engine:
         return slot, self.slot_table
 
     def _issue_layer(self, l: int) -> None:
+        skip = self._lookahead_ids
         for j in self.layer_jobs[l]:
+            if j.id in skip:  # landed at the end of the previous step (or by the prologue)
+                continue
             st = self._stream_of(j)
             for p in self.xwait.get(j.id, ()):
                 st.wait_event(self.events[p])
@@ -589,18 +671,23 @@ class Engine:
             self.h2d.wait_event(self._fork)
             if self.d2h is not None:
                 self.d2h.wait_event(self._fork)
+            if not self._primed:  # eager first step: land this step's lookahead copies now
+                self._issue_lookahead(prologue=True)
+                self.stream.wait_stream(self.h2d)
         ops.embed(b.next_ids, self.w.embed, b.x)
         for l in range(a.layers):
             self._issue_layer(l)
+        if self.streaming:  # next step's leading copies stream while the GPU finishes this one
+            self._issue_lookahead(prologue=False)
+        torch.mm(b.h, self.w.lm_head.t(), out=b.logits)
+        ops.argmax(b.logits, b.next_ids)
+        ops.decode_advance(b.next_ids, self.out_tokens if record else None, b.step, b.positions)
         if self.streaming:  # join: the step ends when every copy has landed
             self._join.record(self.h2d)
             self.stream.wait_event(self._join)
             if self.d2h is not None:
                 self._join2.record(self.d2h)
                 self.stream.wait_event(self._join2)
-        torch.mm(b.h, self.w.lm_head.t(), out=b.logits)
-        ops.argmax(b.logits, b.next_ids)
-        ops.decode_advance(b.next_ids, self.out_tokens if record else None, b.step, b.positions)
 
     # ------------------------------------------------------------------------------------
     # graph capture / replay
@@ -630,6 +717,7 @@ class Engine:
         if self.use_graph:
             if self.graph is None:
                 self.capture()
+            self.prime()
             self.graph.replay()
         else:  # eager issue on the engine stream, ordered after the caller's stream both ways
             self.stream.wait_stream(torch.cuda.current_stream())
@@ -641,6 +729,7 @@ class Engine:
     # public API
     # ------------------------------------------------------------------------------------
     def reset(self, start_pos: int = 0) -> None:
+        self._primed = False
         self.buf.positions.fill_(start_pos)
         self.buf.seq_lens.fill_(start_pos)
         self.buf.step.zero_()
@@ -659,6 +748,7 @@ class Engine:
                 else:  # host page store of the offloaded KV: generate on the device, then copy
                     store.copy_(fill_uniform_(torch.empty_like(store, device=self.device), seed, tid, std))
         torch.cuda.synchronize()
+        self._primed = False
         self.reset(self.prompt_len)
 
     def decode(self, first_tokens: torch.Tensor, n_steps: int) -> torch.Tensor:

@@ -131,9 +131,13 @@ class LatencyCurve:
     entries: list = field(default_factory=list)
 
     def _levels(self) -> dict[int, list[tuple[int, float]]]:
-        lv: dict[int, list[tuple[int, float]]] = {}
-        for t, c, s in sorted(self.entries, key=lambda e: (e[1], e[0])):
-            lv.setdefault(int(c), []).append((int(t), float(s)))
+        # derived once: a curve's samples are fixed after construction
+        lv = self.__dict__.get("_lv")
+        if lv is None or self.__dict__.get("_lv_n") != len(self.entries):
+            lv = {}
+            for t, c, s in sorted(self.entries, key=lambda e: (e[1], e[0])):
+                lv.setdefault(int(c), []).append((int(t), float(s)))
+            self.__dict__["_lv"], self.__dict__["_lv_n"] = lv, len(self.entries)
         return lv
 
     @staticmethod

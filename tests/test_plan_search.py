@@ -1,0 +1,79 @@
+"""The scheduler's plan search (paper_2503_09716_b200.plan_search) vs the reference planner.
+
+1. forward_time (streaming critical path) == the critical path of the materialized schedule
+   (schedule.build_schedule, itself golden-equal to the reference DAG) on every golden schedule and
+   on a sweep of plans;
+2. search / model_based_baseline winners, candidate counts and skip tallies == the reference's own
+   search (plan_search.py:169-314) on tests/golden/search_*.json (tests/golden/make_golden_search.py).
+"""
+
+import glob
+import json
+import math
+import os
+import time
+
+import pytest
+
+from paper_2503_09716_b200.plan_search import (SearchSpace, enumerate_candidates, forward_time,
+                                               model_based_baseline, search)
+from paper_2503_09716_b200.planner import BatchingPlan, ModelSpec, WorkloadSpec, load_profile_document
+from paper_2503_09716_b200.schedule import build_schedule, latency_from_curves
+
+HERE = os.path.join(os.path.dirname(__file__), "golden")
+SCHEDULES = sorted(glob.glob(os.path.join(HERE, "schedule_*.json")))
+SEARCHES = sorted(glob.glob(os.path.join(HERE, "search_*.json")))
+
+
+def _inputs(doc):
+    spec = ModelSpec.from_document(doc["model"])
+    hw, curves = load_profile_document(doc["profile"])
+    w = doc["workload"]
+    wl = WorkloadSpec(w["prompt_len"], w["decode_len"], w["num_sequences"], w["phase"])
+    return spec, hw, latency_from_curves(curves), wl
+
+
+@pytest.mark.parametrize("path", SCHEDULES, ids=[os.path.basename(p) for p in SCHEDULES])
+def test_forward_time_equals_schedule_critical_path(path):
+    doc = json.load(open(path))
+    if doc.get("layer_index") is not None:
+        pytest.skip("single-layer fixture")
+    spec, hw, lat, wl = _inputs(doc)
+    plan = BatchingPlan.from_document(doc["plan"])
+    t = forward_time(spec, hw, lat, wl, plan, expert_counts=doc["expert_tokens"])
+    assert math.isclose(t, doc["critical_path"], rel_tol=1e-12)
+
+
+def test_forward_time_sweep_matches_build_schedule():
+    doc = json.load(open(os.path.join(HERE, "search_tiny_decode.json")))
+    spec, hw, lat, wl = _inputs(doc)
+    n = 0
+    for phase in ("decode", "prefill"):
+        w = wl.with_phase(phase)
+        for plan in enumerate_candidates(spec, hw, w, SearchSpace(b_a_grid=(16, 64), b_e_grid=(256, 4096),
+                                                                  omega_grid=(0.0, 0.3, 0.5),
+                                                                  s_expert_slots_grid=(2, 8))):
+            ref = build_schedule(spec, hw, lat, w, plan).critical_path()
+            assert math.isclose(forward_time(spec, hw, lat, w, plan), ref, rel_tol=1e-12), plan
+            n += 1
+    assert n > 50
+
+
+@pytest.mark.parametrize("path", SEARCHES, ids=[os.path.basename(p) for p in SEARCHES])
+def test_search_matches_reference(path):
+    doc = json.load(open(path))
+    spec, hw, lat, wl = _inputs(doc)
+    wl = wl.with_phase(doc["phase"])
+    space = SearchSpace.from_document(doc["space"])
+    skips = {}
+    assert sum(1 for _ in enumerate_candidates(spec, hw, wl, space, skip_counts=skips)) == doc["candidates"]
+    assert skips == doc["skips"]
+    t0 = time.time()
+    best = search(spec, hw, lat, wl, space)
+    dt = time.time() - t0
+    assert best.plan == BatchingPlan.from_document(doc["best"]["plan"])
+    assert math.isclose(best.t_forward, doc["best"]["t_forward"], rel_tol=1e-12)
+    base = model_based_baseline(spec, hw, lat, wl)
+    assert base.plan == BatchingPlan.from_document(doc["baseline"]["plan"])
+    assert math.isclose(base.throughput, doc["baseline"]["throughput"], rel_tol=1e-12)
+    print(f"{doc['name']}: {dt:.2f} s here vs {doc['reference_search_seconds']:.2f} s in the reference")
