@@ -132,11 +132,13 @@ class Engine:
         # measurement only: False issues every job except the host<->device copies (compute-only
         # step time for the transfer/compute overlap figure; outputs are then meaningless)
         self.copies_enabled = True
+        self.compute_enabled = True  # False: copies only (the link-bound time of the same step)
         self._plan_streams()
         # ---- weights ----
         if self.offload:
             from .offload import OffloadedWeights
             self.w = OffloadedWeights(a, self.spec, self.plan.s_params, self.plan.s_expert, seed=seed,
+                                      extra_slots=self.lookahead_expert_slots, extra_dense=len(self.dense_buf_of),
                                              device=device)
         elif self.mla:
             self.w = DeepseekDeviceWeights(a, seed=seed, device=device)
@@ -309,38 +311,43 @@ class Engine:
 
     def _plan_lookahead(self, jobs, preds, mech_of_kin) -> None:
         """Cross-step copy lookahead.  The leading H2D copies of a step that wait on no compute of
-        their own step (the first dense copy, the first `slots` expert copies, the first `ring` KV
-        slices: the schedule gives them no recycle edge) are issued at the END of the previous step,
-        once that step's last user of the buffer they overwrite is done (and, for a KV slice, once
-        that step's KV_COPY_OUT of the same slice has landed on the host).  The host link then keeps
-        streaming through the step boundary instead of idling while the GPU drains the last layer
-        and starts the next.  The first step of a decode call gets them from an eager prologue."""
+        their own step (the first dense copy, the first `slots` expert copies, the first KV slices)
+        are issued at the END of the previous step, so the host link keeps streaming through the step
+        boundary instead of idling while the GPU drains the last layer and starts the next.  Each
+        lookahead copy lands in a buffer of its own (one extra dense buffer, expert slot or KV ring
+        slot per copy, beyond the plan's s_expert), which only that copy's consumers in the step read:
+        the next step's copy into it waits for those consumers alone (and, for a KV slice, for the
+        step's KV_COPY_OUT of the same slice), not for the last layer.  The first step of a decode
+        call gets them from an eager prologue."""
         copies = [j for j in jobs if j.resource == "htod_link"]
         self.lookahead: list = []
-        for c in copies:
-            if any(jobs[p].resource not in (None, "htod_link") for p in preds[c.id]):
+        for c in copies:  # leading copies with no recycle wait on this step's compute
+            if self.xwait[c.id]:
                 break
             self.lookahead.append(c)
         ids = {c.id for c in self.lookahead}
-        self.lookahead_waits: dict[int, list[int]] = {}
         succ = self.schedule.succs()
-        last_dense = [c for c in copies if c.label.endswith("dense_copy")]
         kv_out = {(j.layer, j.label.rsplit("/", 1)[1]): j.id for j in jobs if j.kind == "kv_copy_out"}
+        n_slots = max(1, self.plan.s_expert // self.spec.expert_bytes) if self.spec.expert_bytes else 1
+        self.dense_buf_of: dict[int, int] = {}
+        self.lookahead_waits: dict[int, list[int]] = {}
+        n_e = n_kv = 0
         for c in self.lookahead:
-            if c.label.endswith("dense_copy"):  # single dense buffer: post_attention of the last streamed layer
-                L = last_dense[-1].layer
-                w = [next(j.id for j in jobs if j.kind == "post_attention" and j.layer == L)]
-            elif c.kind == "weight_copy":  # expert slot: last consumer of the last copy into that slot
-                slot = self.slot_of[(c.layer, int(c.label.split("/expert")[1].split("_")[0]))]
-                last = [x for x in copies if x.kind == "weight_copy" and not x.label.endswith("dense_copy")
-                        and self.slot_of[(x.layer, int(x.label.split("/expert")[1].split("_")[0]))] == slot][-1]
-                w = [max(v for v in succ[last.id] if jobs[v].kind == "expert_compute")]
-            else:  # KV ring slot + the same slice's new-token write-back
-                r = self.kv_slot_of[c.id]
-                last = [x for x in copies if x.kind == "kv_copy_in" and self.kv_slot_of[x.id] == r][-1]
-                w = [mech_of_kin[last.id], kv_out[(c.layer, c.label.rsplit("/", 1)[1])]]
+            if c.label.endswith("dense_copy"):
+                self.dense_buf_of[c.layer] = 1
+                w = [next(j.id for j in jobs if j.kind == "post_attention" and j.layer == c.layer)]
+            elif c.kind == "weight_copy":
+                e = int(c.label.split("/expert")[1].split("_")[0])
+                self.slot_of[(c.layer, e)] = n_slots + n_e
+                n_e += 1
+                w = [max(v for v in succ[c.id] if jobs[v].kind == "expert_compute")]
+            else:
+                self.kv_slot_of[c.id] = self.kv_ring_n + n_kv
+                n_kv += 1
+                w = [mech_of_kin[c.id], kv_out[(c.layer, c.label.rsplit("/", 1)[1])]]
             self.lookahead_waits[c.id] = w
             self.need_event.update(w)
+        self.lookahead_expert_slots, self.lookahead_kv_slots = n_e, n_kv
         # consumers in the step no longer wait on the (previous-step) lookahead copies
         for jid, ws in self.xwait.items():
             self.xwait[jid] = [p for p in ws if p not in ids]
@@ -393,7 +400,7 @@ class Engine:
                    for l in range(a.layers)]
         slice_pages = self.plan.b_a * self.pps
         self.kv_ring = [[torch.zeros(slice_pages * pe, **bf) for _ in range(n_stores)]
-                        for _ in range(max(1, self.kv_ring_n))]
+                        for _ in range(max(1, self.kv_ring_n) + self.lookahead_kv_slots)]
         self.kv_stage = [[torch.zeros(self.B * pe, **bf) for _ in range(n_stores)] for _ in range(2)]
         i32 = dict(dtype=torch.int32, device=self.device)
         # staging table: every page index of sequence b maps to staging page b
@@ -415,12 +422,20 @@ class Engine:
         if not self.copies_enabled:
             return True
         if j.label.endswith("dense_copy"):
-            self.w.dense_buf.copy_(self.w.host_dense[l], non_blocking=True)
+            self.w.dense_bufs[self.dense_buf_of.get(l, 0)].copy_(self.w.host_dense[l], non_blocking=True)
         elif self.w.host_experts[l] is not None:  # (DeepSeek-V2's dense first layers have no experts)
             e = int(j.label.split("/expert")[1].split("_")[0])
             n_c = self.w.place.experts_per_layer[l]
             self.w.slots[self.slot_of[(l, e)]].copy_(self.w.host_experts[l][e - n_c], non_blocking=True)
         return True
+
+    def _moved_bytes(self, j) -> float:
+        """Bytes a copy job really moves: the schedule's bytes, except the expert copies the
+        reference's all-MoE model charges to DeepSeek-V2's dense first layers (no experts exist)."""
+        if (j.kind == "weight_copy" and not j.label.endswith("dense_copy") and self.offload
+                and self.w.host_experts[j.layer] is None):
+            return 0.0
+        return j.nbytes
 
     def _kv_job(self, l: int, j) -> bool:
         """KV_COPY_IN / KV_COPY_OUT jobs (offload_dag.py:372-392); returns False for other kinds."""
@@ -468,7 +483,8 @@ class Engine:
                 if te is not None:
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     e0.record(st)
-                self._issue_job(l, j)
+                if self.compute_enabled or j.resource in ("htod_link", "dtoh_link"):
+                    self._issue_job(l, j)
                 if te is not None:
                     e1.record(st)
                     te[j.id] = (e0, e1)
@@ -478,7 +494,7 @@ class Engine:
     def _layer_weights(self, l: int) -> dict:
         W = self.w.layers[l]
         if self.offload and l >= self.w.place.dense_layers:
-            W = dict(W, **self.w.dense_views())
+            W = dict(W, **self.w.dense_views(self.dense_buf_of.get(l, 0)))
         return W
 
     # ---- DeepSeek-V2 (MLA) jobs ------------------------------------------------------------
@@ -820,7 +836,7 @@ class Engine:
             recs.append({"time": e, "node": jid, "kind": j.kind, "resource": j.resource, "action": "finish"})
             busy[j.resource] = busy.get(j.resource, 0.0) + (e - s)
             if j.resource in nbytes:
-                nbytes[j.resource] += j.nbytes
+                nbytes[j.resource] += self._moved_bytes(j)
         self.trace_events = None
         recs.sort(key=lambda r: (r["time"], r["node"], r["action"] != "start"))
         makespan = t0.elapsed_time(t1) * 1e-3

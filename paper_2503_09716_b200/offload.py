@@ -33,7 +33,7 @@ class OffloadedWeights:
     attention projections plus its shared experts (the reference's dense_bytes_per_layer)."""
 
     def __init__(self, arch: ModelArch, spec: ModelSpec, s_params: int, s_expert: int, seed: int = 0,
-                 device: str = "cuda"):
+                 device: str = "cuda", extra_slots: int = 0, extra_dense: int = 0):
         a = arch
         d, f, E = a.hidden, a.moe_ffn, a.n_experts
         std = a.init_std
@@ -53,8 +53,9 @@ class OffloadedWeights:
         self.dense_shapes: dict[str, tuple] | None = None
         self.dense_elems = 0
         self.expert_elems = 3 * d * f
-        self.dense_buf = None
-        self.slots = torch.empty(max(self.n_slots, 0), self.expert_elems, **bf)
+        self.dense_bufs: list[torch.Tensor] = []
+        # the plan's s_expert slots, then one slot per cross-step lookahead expert copy (engine.py)
+        self.slots = torch.empty(max(self.n_slots, 0) + extra_slots, self.expert_elems, **bf)
         self.layers: list[dict] = []
         self.host_dense: list[torch.Tensor | None] = []
         self.host_experts: list[torch.Tensor | None] = []
@@ -65,8 +66,8 @@ class OffloadedWeights:
                 self.dense_shapes = {k: tuple(L[k].shape) for k in self.dense_keys}
                 self.dense_elems = sum(L[k].numel() for k in self.dense_keys)
                 assert self.dense_elems * 2 == spec.dense_bytes_per_layer, "dense blob != reference dense bytes"
-                if self.place.dense_layers < a.layers:
-                    self.dense_buf = torch.empty(self.dense_elems, **bf)
+                if self.place.dense_layers < a.layers:  # the single dense buffer (+ the lookahead one)
+                    self.dense_bufs = [torch.empty(self.dense_elems, **bf) for _ in range(1 + extra_dense)]
             # dense modules: resident, or one pinned blob (one DMA per layer, offload_dag.py:308-321)
             if l < self.place.dense_layers:
                 self.host_dense.append(None)
@@ -97,15 +98,15 @@ class OffloadedWeights:
             self.layers.append(L)
         torch.cuda.synchronize()
 
-    def dense_views(self) -> dict:
-        """The streamed dense modules as views into the single dense buffer."""
+    def dense_views(self, buf: int = 0) -> dict:
+        """The streamed dense modules as views into a dense buffer."""
         out, o = {}, 0
         for k in self.dense_keys:
             shape = self.dense_shapes[k]
             n = 1
             for x in shape:
                 n *= x
-            out[k] = self.dense_buf[o:o + n].view(shape)
+            out[k] = self.dense_bufs[buf][o:o + n].view(shape)
             o += n
         return derive_views(self.arch, out)
 

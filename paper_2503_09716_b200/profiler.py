@@ -1,0 +1,174 @@
+"""Measured B200 latency tables for the planner (the paper's profiling step).
+
+The reference prices every schedule job from per-module latency tables `(tokens, context) ->
+seconds` (hw_profile.py:52-149, LatencyTable) and otherwise synthesizes them from a roofline
+(hw_profile.py:260-354).  `profile_engine` measures them instead, on this engine's own kernels:
+each module kind is issued exactly as the engine issues that job, for a token count of the grid,
+on one decoder layer of the model, and timed with CUDA events (median of `reps` after warm-up).
+
+    pre_attention             QKV projection(s) + RoPE + KV append (+ MLA absorption bmm)
+    attention_mechanism_gpu   paged decode attention over `context` keys (ctx grid)
+    post_attention            O projection + residual add + RMSNorm (+ DeepSeek shared experts)
+    router                    gate logits GEMM + fused top-k/softmax/counts + stable permutation
+    expert                    grouped gate/up+SiLU and down GEMMs of ONE expert with `tokens` rows
+
+The result is a profile document in the reference's schema (hw_profile.py:156-249, ingestible by
+its `ingest_profile`), with the machine's capacities and measured link/HBM rates.
+"""
+
+from __future__ import annotations
+
+import dataclasses
+import json
+import os
+import statistics
+from typing import Sequence
+
+import torch
+
+from . import _native as nat
+from . import ops
+from .configs import ModelArch, get_arch
+from .planner import BatchingPlan, Hardware, LatencyCurve, ModelSpec, profile_document
+
+BF16 = torch.bfloat16
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _time(fn, reps: int) -> float:
+    for _ in range(2):
+        fn()
+    ts = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) * 1e-3)
+    return statistics.median(ts)
+
+
+def measure_links(nbytes: int = 1 << 30, reps: int = 5) -> tuple[float, float]:
+    """Pinned host<->device copy rates (bytes/s), the PAPER.md:701 procedure."""
+    h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    up = nbytes / _time(lambda: d.copy_(h, non_blocking=True), reps)
+    down = nbytes / _time(lambda: h.copy_(d, non_blocking=True), reps)
+    return up, down
+
+
+def measured_hardware(host_bytes: int | None = None) -> Hardware:
+    up, down = measure_links()
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except OSError:
+        pass
+    if host_bytes is None:
+        host_bytes = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+    return Hardware(m_g=torch.cuda.get_device_properties(0).total_memory, m_c=int(host_bytes), bw_htod=up,
+                    bw_dtoh=down, gpu_peak_flops=float(peaks.get("bf16_tflops_sustained", 1388.0)) * 1e12,
+                    gpu_mem_bw=float(peaks.get("hbm_gbs", 6550.0)) * 1e9, gpu_launch_overhead=5e-6,
+                    cpu_attn_flops=0.0)
+
+
+def profile_engine(arch: ModelArch | str, token_grid: Sequence[int] | None = None,
+                   ctx_grid: Sequence[int] = (128, 512, 768), reps: int = 5,
+                   hardware: Hardware | None = None) -> dict:
+    """Profile document with measured tables for every GPU module kind of `arch` (one decoder
+    layer of it is instantiated; the latency of a job does not depend on the layer index)."""
+    from .engine import Engine
+
+    full = get_arch(arch) if isinstance(arch, str) else arch
+    first_moe = full.first_k_dense if full.is_mla else 0
+    one = dataclasses.replace(full, layers=first_moe + 1, name=f"{full.name}[profile]")
+    token_grid = list(token_grid or [2 ** i for i in range(0, 14)])
+    Tmax = max(token_grid)
+    ctx_max = max(ctx_grid)
+    spec = ModelSpec.from_document(one.model_spec_document())
+    plan = BatchingPlan(Tmax, Tmax, 1 << 20, 0.0, 0, spec.model_bytes)
+    eng = Engine(one, plan, prompt_len=max(1, ctx_max - 1), decode_len=1, use_graph=False)
+    eng.synthetic_prefill()
+    a, b, l = eng.arch, eng.buf, first_moe
+    W = eng._layer_weights(l)
+    d = a.hidden
+    b.h.normal_(0.0, 1.0)
+    b.positions.fill_(ctx_max - 1)
+    g = torch.Generator(device="cuda").manual_seed(0)
+    tables: dict[str, list] = {k: [] for k in ("pre_attention", "attention_mechanism_gpu", "post_attention",
+                                               "router", "expert")}
+    from .schedule import Job
+
+    def job(kind: str, T: int):
+        return Job(0, kind, "gpu_compute", 0.0, f"L{l}/{kind}/mb0", layer=l, tokens=T, seqs=T)
+
+    for T in token_grid:
+        # pre-attention: exactly the engine's job on micro-batch [0, T)
+        tables["pre_attention"].append([T, 0, _time(lambda: eng._issue_job(l, job("pre_attention", T)), reps)])
+        # post-attention on T tokens (O projection + residual/norm [+ shared experts])
+        if eng.mla:
+            m = eng.mb
+
+            def post():
+                torch.mm(m["o_cat"][:T], W["wo"].t(), out=b.o[:T])
+                ops.add_rmsnorm(b.x[:T], W["ln2"], a.rms_eps, b.h[:T], delta=b.o[:T], x_out=b.x[:T])
+                torch.mm(b.h[:T], W["sh_gate_up"][0].t(), out=m["sh_gu"][:T])
+                ops.silu_mul(m["sh_gu"][:T], m["sh_h"][:T])
+                torch.mm(m["sh_h"][:T], W["sh_down"][0].t(), out=m["sh_out"][:T])
+        else:
+            def post():
+                torch.mm(b.attn[:T], W["wo"].t(), out=b.o[:T])
+                ops.add_rmsnorm(b.x[:T], W["ln2"], a.rms_eps, b.h[:T], delta=b.o[:T], x_out=b.x[:T])
+        tables["post_attention"].append([T, 0, _time(post, reps)])
+        # router on T tokens: logits GEMM + fused top-k + stable permutation
+        ws = ops.RouterWorkspace(T, a.n_experts, a.top_k)
+        logits = torch.empty(T, a.n_experts, dtype=torch.float32, device="cuda")
+        xp = torch.empty(T * a.top_k, d, dtype=BF16, device="cuda")
+
+        def route():
+            logits.copy_(torch.mm(b.h[:T], W["router"].t(), out_dtype=torch.float32))
+            ops.router_topk(None, None, ws, a.top_k, a.router_mode, a.routed_scaling, a.n_group, a.topk_group,
+                            logits_in=logits)
+            ops.permute(b.h[:T], ws, xp)
+        tables["router"].append([T, 0, _time(route, reps)])
+        # one expert with T rows (the EXPERT_COMPUTE chunk): gate/up+SiLU then down
+        rows = max(T, 1)
+        x = torch.randn(rows, d, generator=g, device="cuda").to(BF16)
+        h = torch.empty(rows, a.moe_ffn, dtype=BF16, device="cuda")
+        y = torch.empty(rows, d, dtype=BF16, device="cuda")
+        offs = torch.tensor([0, T], dtype=torch.int32, device="cuda")
+        gu, dn = W["w_gate_up"][:1], W["w_down"][:1]
+
+        def expert():
+            ops.moe_gemm_gate_up(gu, x, offs, h)
+            ops.moe_gemm_down(dn, h, offs, y)
+        tables["expert"].append([T, 0, _time(expert, reps)])
+        # attention over `ctx` keys for T sequences
+        for ctx in ctx_grid:
+            b.seq_lens[:T].fill_(ctx)
+            if eng.mla:
+                _, q_lat, o_lat, _ = eng._ds_views(0, T)
+                scale = (a.qk_nope_dim + a.qk_rope_dim) ** -0.5
+
+                def attn():
+                    nat.call("mgb_decode_attn_mla", q_lat.data_ptr(), eng.mb["q_pe"][:T].data_ptr(),
+                             eng.latent[l].data_ptr(), eng.block_table.data_ptr(), eng.pps, b.seq_lens.data_ptr(),
+                             T, a.n_heads, a.kv_lora_rank, a.qk_rope_dim, scale, o_lat.data_ptr(),
+                             torch.cuda.current_stream().cuda_stream)
+            else:
+                def attn():
+                    ops.decode_attn_gqa(b.q[:T], eng.k_cache[l], eng.v_cache[l], eng.block_table[:T],
+                                        b.seq_lens[:T], a.n_heads, a.n_kv_heads, a.head_dim, b.attn[:T])
+            tables["attention_mechanism_gpu"].append([T, ctx, _time(attn, reps)])
+    del eng
+    torch.cuda.empty_cache()
+    # the reference requires tables monotone in tokens (hw_profile.py:117-142): running max per context
+    for k, v in tables.items():
+        best: dict[int, float] = {}
+        for e in sorted(v, key=lambda e: (e[1], e[0])):
+            e[2] = best[e[1]] = max(e[2], best.get(e[1], 0.0))
+    curves = [LatencyCurve(k, [tuple(e) for e in v]) for k, v in tables.items()]
+    hw = hardware or measured_hardware()
+    return profile_document(hw, curves)

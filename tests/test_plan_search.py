@@ -77,3 +77,32 @@ def test_search_matches_reference(path):
     assert base.plan == BatchingPlan.from_document(doc["baseline"]["plan"])
     assert math.isclose(base.throughput, doc["baseline"]["throughput"], rel_tol=1e-12)
     print(f"{doc['name']}: {dt:.2f} s here vs {doc['reference_search_seconds']:.2f} s in the reference")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["tiny-mixtral", "tiny-deepseek-v2"])
+def test_measured_profile_feeds_search(name):
+    """profiler.profile_engine measures every GPU module kind on the engine's kernels and emits the
+    reference's profile schema (monotone tables, hw_profile.py:117-142); the search runs on it."""
+    from paper_2503_09716_b200.configs import get_arch
+    from paper_2503_09716_b200.profiler import profile_engine
+
+    arch = get_arch(name)
+    doc = profile_engine(arch, token_grid=[1, 2, 8, 32, 64], ctx_grid=(16, 64), reps=2)
+    kinds = {t["module_kind"] for t in doc["latency_tables"]}
+    assert kinds == {"pre_attention", "attention_mechanism_gpu", "post_attention", "router", "expert"}
+    for t in doc["latency_tables"]:
+        by_ctx = {}
+        for tok, ctx, sec in t["entries"]:
+            assert sec > 0
+            by_ctx.setdefault(ctx, []).append((tok, sec))
+        for pts in by_ctx.values():
+            pts.sort()
+            assert len(pts) >= 2 and all(a[1] <= b[1] for a, b in zip(pts, pts[1:]))
+    hw, curves = load_profile_document(doc)
+    assert hw.bw_htod > 1e9 and hw.m_g > 1e10
+    spec = ModelSpec.from_document(arch.model_spec_document())
+    space = SearchSpace(b_a_grid=(16, 64), b_e_grid=(256,), omega_grid=(0.0,), s_expert_slots_grid=(2,),
+                        s_params_fracs=(0.0, 1.0))
+    best = search(spec, hw, latency_from_curves(curves), WorkloadSpec(64, 32, 10_000), space)
+    assert best.throughput > 0

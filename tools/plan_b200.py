@@ -1,0 +1,78 @@
+"""Close the scheduler loop on a B200: measure the engine's module latency tables
+(profiler.profile_engine), search the batching plan with them (plan_search.search, the reference's
+search semantics), run the engine at the chosen plan and compare the measured forward time with the
+plan's critical-path estimate (SURVEY.md §8c engine target 2).
+
+  python tools/plan_b200.py --config mixtral-8x7b --kv-policy offload --out profiles/...json
+"""
+import argparse
+import dataclasses
+import json
+import os
+import sys
+import time
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2503_09716_b200.configs import get_arch  # noqa: E402
+from paper_2503_09716_b200.engine import Engine  # noqa: E402
+from paper_2503_09716_b200.plan_search import SearchSpace, evaluate_plan, search  # noqa: E402
+from paper_2503_09716_b200.planner import Hardware, ModelSpec, WorkloadSpec, load_profile_document  # noqa: E402
+from paper_2503_09716_b200.profiler import profile_engine  # noqa: E402
+from paper_2503_09716_b200.schedule import latency_from_curves  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="mixtral-8x7b")
+ap.add_argument("--layers", type=int, default=None)
+ap.add_argument("--kv-policy", default="offload", choices=["offload", "resident"])
+ap.add_argument("--host-gb", type=float, default=170.0)
+ap.add_argument("--reserve-gb", type=float, default=12.0)
+ap.add_argument("--steps", type=int, default=3)
+ap.add_argument("--profile-in", default=None)
+ap.add_argument("--out", default=None)
+args = ap.parse_args()
+
+full = get_arch(args.config)
+arch = full if args.layers is None else dataclasses.replace(full, layers=args.layers, name=f"{full.name}[{args.layers}L]")
+t0 = time.time()
+if args.profile_in:
+    prof = json.load(open(args.profile_in))
+else:
+    prof = profile_engine(arch, token_grid=[2 ** i for i in range(0, 14)])
+t_prof = time.time() - t0
+hw, curves = load_profile_document(prof)
+hw = Hardware(**{**hw.__dict__, "m_g": hw.m_g - int(args.reserve_gb * 2**30), "m_c": int(args.host_gb * 1e9)})
+lat = latency_from_curves(curves)
+spec = ModelSpec.from_document(arch.model_spec_document())
+wl = WorkloadSpec(512, 256, 1_000_000, "decode")
+space = SearchSpace(b_a_grid=(64, 128, 256, 512, 1024), b_e_grid=(1024, 4096, 16384), omega_grid=(0.0,),
+                    s_expert_slots_grid=(2, 4, 8), s_params_fracs=(0.0, 0.25, 0.5, 0.75, 1.0))
+t0 = time.time()
+best = search(spec, hw, lat, wl, space, kv_policy=args.kv_policy)
+t_search = time.time() - t0
+plan = best.plan
+eng = Engine(arch, plan, prompt_len=512, decode_len=256, use_graph=True, kv_policy=args.kv_policy)
+eng.synthetic_prefill()
+eng.reset(767)  # the planner prices attention at the full context (max_context, offload_dag.py:353)
+eng.buf.next_ids.random_(0, arch.vocab)
+eng.capture()
+eng.prime()
+eng.graph.replay()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+torch.cuda.synchronize()
+e0.record()
+for _ in range(args.steps):
+    eng.graph.replay()
+e1.record()
+torch.cuda.synchronize()
+t_meas = e0.elapsed_time(e1) * 1e-3 / args.steps
+out = {"config": arch.name, "kv_policy": args.kv_policy, "plan": plan.to_document(),
+       "predicted_forward_s": best.t_forward, "measured_forward_s": t_meas,
+       "predicted_tokens_per_s": best.throughput, "measured_tokens_per_s": plan.B / t_meas,
+       "rel_err": (t_meas - best.t_forward) / best.t_forward,
+       "profile_s": t_prof, "search_s": t_search, "hardware": prof["hardware"]}
+print(json.dumps(out))
+if args.out:
+    with open(args.out, "w") as f:
+        json.dump({"result": out, "profile": prof}, f)
