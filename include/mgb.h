@@ -91,6 +91,27 @@ int mgb_kv_token_copy(const void* src, const int* src_table, int src_max_pages, 
                       int dst_max_pages, const int* positions, int B, int page_tokens, long long page_bytes,
                       int unit_bytes, int n_units, long long unit_stride, void* stream);
 
+/* ---- ATTN_MECH_CPU (offload_dag.py:328-357; ModuleKind.ATTN_MECH_CPU hw_profile.py:55) -----
+ * GQA decode attention on the host cores over the host KV page store (GPU page layout), for the
+ * plan's CPU share of sequences (omega > 0).  AVX-512 BF16 when the host has it, scalar otherwise.
+ * mgb_cpu_attn_gqa runs synchronously; mgb_cpu_attn_gqa_enqueue adds it to `stream` as a host node
+ * (cudaLaunchHostFunc; CUDA-graph capturable) and reads `desc` when the node runs. */
+typedef struct MgbCpuAttnGqa {
+  const unsigned short* k_pages; /* host page store of the layer, K (bf16 bits) */
+  const unsigned short* v_pages; /* V */
+  const unsigned short* q;       /* [B, Hq, hd] bf16, RoPE applied (pinned host) */
+  const int* seq_lens;           /* [B] keys per sequence (pinned host) */
+  unsigned short* out;           /* [B, Hq * hd] bf16 (pinned host) */
+  long long first_page;          /* sequence b owns pages first_page + b * pps ... */
+  int pps, B, Hq, Hkv, hd, page_tokens;
+  float scale;
+  int status;                    /* written by the host node: 0 ok, -1 invalid */
+} MgbCpuAttnGqa;
+int mgb_cpu_attn_gqa(MgbCpuAttnGqa* desc);
+int mgb_cpu_attn_gqa_enqueue(MgbCpuAttnGqa* desc, void* stream);
+int mgb_cpu_threads(int n);        /* resize the host thread pool (n > 0); returns its size */
+int mgb_cpu_attn_simd(void);       /* 1 if the AVX-512 BF16 path is active */
+
 /* ---- PRE_ATTENTION / POST_ATTENTION helpers (offload_dag.py:359-416) --------------------- */
 int mgb_add_rmsnorm(const void* x, const void* delta, const void* weight, float eps, int T, int d, void* x_out,
                     void* y, void* stream);

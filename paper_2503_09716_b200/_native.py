@@ -50,10 +50,23 @@ SIGNATURES: dict[str, list] = {
     "mgb_mla_append": [P, P, P, F, I, I, I, I, I, P, P, P, P, I, P, P, P, P, P],
     # kv_stream.cu
     "mgb_kv_token_copy": [P, P, I, P, P, I, P, I, I, L, I, I, L, P],
+    # cpu_attn.cpp (host code: ATTN_MECH_CPU)
+    "mgb_cpu_attn_gqa": [P],
+    "mgb_cpu_attn_gqa_enqueue": [P, P],
+    "mgb_cpu_threads": [I],
+    "mgb_cpu_attn_simd": [],
 }
 
+
+class CpuAttnGqa(ctypes.Structure):
+    """struct MgbCpuAttnGqa (include/mgb.h): one layer's CPU-attention job description."""
+
+    _fields_ = [("k_pages", P), ("v_pages", P), ("q", P), ("seq_lens", P), ("out", P), ("first_page", L),
+                ("pps", ctypes.c_int32), ("B", ctypes.c_int32), ("Hq", ctypes.c_int32), ("Hkv", ctypes.c_int32),
+                ("hd", ctypes.c_int32), ("page_tokens", ctypes.c_int32), ("scale", F), ("status", ctypes.c_int32)]
+
 # entry points that return a value rather than a status
-VALUE_FNS = {"mgb_abi_version", "mgb_num_sms", "mgb_kv_page_size", "mgb_mla_page_size", "mgb_mla_page_elems",
+VALUE_FNS = {"mgb_cpu_threads", "mgb_cpu_attn_simd", "mgb_abi_version", "mgb_num_sms", "mgb_kv_page_size", "mgb_mla_page_size", "mgb_mla_page_elems",
              "mgb_router_num_blocks", "mgb_router_tokens_per_block"}
 
 STATUS = {0: "ok", -1: "invalid argument", -2: "capacity exceeded", -3: "CUDA error"}

@@ -36,8 +36,13 @@ NVCC_FLAGS = [
 ]
 
 
+CXX = os.environ.get("CXX", "g++")
+CXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-g", "-pthread", "-I/usr/local/cuda/include", f"-I{REPO / 'include'}"]
+
+
 def _sources() -> list[Path]:
-    return sorted(CSRC.glob("*.cu"))
+    # *.cu: device code for sm_100a; *.cpp: host code (the CPU attention path), compiled by g++
+    return sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cpp"))
 
 
 def _headers() -> list[Path]:
@@ -52,7 +57,10 @@ def _stale(obj: Path, src: Path, headers: list[Path]) -> bool:
 
 
 def _compile(src: Path, obj: Path, verbose: bool) -> str:
-    cmd = [NVCC, *ARCH_FLAGS, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+    if src.suffix == ".cpp":
+        cmd = [CXX, *CXX_FLAGS, "-c", str(src), "-o", str(obj)]
+    else:
+        cmd = [NVCC, *ARCH_FLAGS, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
     proc = subprocess.run(cmd, capture_output=True, text=True)
     log = proc.stdout + proc.stderr
     (obj.with_suffix(".ptxas.log")).write_text(log)
@@ -68,7 +76,7 @@ def build(force: bool = False, verbose: bool = True) -> Path:
     OUT_DIR.mkdir(parents=True, exist_ok=True)
     headers = _headers()
     srcs = _sources()
-    objs = [OUT_DIR / (s.stem + ".o") for s in srcs]
+    objs = [OUT_DIR / (s.name.replace(".", "_") + ".o") for s in srcs]
     todo = [(s, o) for s, o in zip(srcs, objs) if force or _stale(o, s, headers)]
     if todo:
         with cf.ThreadPoolExecutor(max_workers=min(8, len(todo))) as ex:

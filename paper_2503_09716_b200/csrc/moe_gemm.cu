@@ -111,7 +111,7 @@ template <bool GATED>
 __global__ void __launch_bounds__(192, 1)
 moe_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const int* __restrict__ offsets, int E, int MT, int K, int rows_per_expert, int half_rows,
-                __nv_bfloat16* __restrict__ out, int ldo) {
+                __nv_bfloat16* __restrict__ out, int ldo, bool balanced) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* tiles = smem;
@@ -133,7 +133,7 @@ moe_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     for (int e = 0; e < E; ++e) {
       s_prefix[e] = acc;
       const int cnt = offsets[e + 1] - offsets[e];
-      acc += token_tiles(cnt, GATED) * MT;
+      acc += token_tiles(cnt, balanced) * MT;
     }
     s_prefix[E] = acc;
   }
@@ -156,7 +156,7 @@ moe_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int total = s_prefix[E];
-  UnitSched sched{s_prefix, E, MT, GATED};
+  UnitSched sched{s_prefix, E, MT, balanced};
   const int KB = K / kBK;
 
   if (warp == 0) {
@@ -277,7 +277,7 @@ template <bool GATED>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
 moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const int* __restrict__ offsets, int E, int MT, int K, int rows_per_expert, int half_rows,
-                     __nv_bfloat16* __restrict__ out, int ldo) {
+                     __nv_bfloat16* __restrict__ out, int ldo, bool balanced) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* tiles = smem;
@@ -300,7 +300,7 @@ moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
     for (int e = 0; e < E; ++e) {
       s_prefix[e] = acc;
       const int cnt = offsets[e + 1] - offsets[e];
-      acc += token_tiles(cnt, GATED) * MT;
+      acc += token_tiles(cnt, balanced) * MT;
     }
     s_prefix[E] = acc;
   }
@@ -324,7 +324,7 @@ moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int total = s_prefix[E];
-  UnitSched sched{s_prefix, E, MT, GATED};
+  UnitSched sched{s_prefix, E, MT, balanced};
   const int KB = K / kBK;
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
 
@@ -340,7 +340,7 @@ moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
       for (int u = pair; u < total; u += npairs) {
         int e, nt, mt, tok0, n;
         sched.decode(u, offsets, e, nt, mt, tok0, n);
-        const uint64_t pol_w = token_tiles(offsets[e + 1] - offsets[e], GATED) > 1 ? pol_shared : pol_once;
+        const uint64_t pol_w = token_tiles(offsets[e + 1] - offsets[e], balanced) > 1 ? pol_shared : pol_once;
         const int N = (n + 31) & ~31;
         const int half = N / 2;
         const int nb = half / kPBRows;
@@ -457,6 +457,12 @@ template <bool GATED>
 int launch_moe_gemm(const void* w, int w_rows_total, const void* act, int act_rows, const int* offsets, int E,
                     int MT, int K, int rows_per_expert, int half_rows, void* out, int ldo, cudaStream_t stream) {
   const bool pair = use_pair_kernel() && MT % 2 == 0 && (mgb_host::num_sms() & ~1) >= 2;
+  // token tiling: the gated GEMM balances its tiles (see token_tile); MGB_GEMM_BALANCED=0/1 overrides
+  static const int bal_env = [] {
+    const char* e = getenv("MGB_GEMM_BALANCED");
+    return e ? (e[0] == '1' ? 1 : 0) : -1;
+  }();
+  const bool balanced = bal_env < 0 ? GATED : bal_env == 1;
   CUtensorMap tmA, tmB;
   if (mgb_host::encode_tmap_2d_bf16(&tmA, w, K, w_rows_total, (uint64_t)K * 2, mgb::kBK,
                                     GATED ? mgb::kBM / 2 : mgb::kBM) != CUDA_SUCCESS)
@@ -474,7 +480,8 @@ int launch_moe_gemm(const void* w, int w_rows_total, const void* act, int act_ro
     }
     const int grid = mgb_host::num_sms() & ~1;
     mgb::moe_gemm_pair_kernel<GATED><<<grid, 192, mgb::kPairSmem, stream>>>(
-        tmA, tmB, offsets, E, MT / 2, K, rows_per_expert, half_rows, reinterpret_cast<__nv_bfloat16*>(out), ldo);
+        tmA, tmB, offsets, E, MT / 2, K, rows_per_expert, half_rows, reinterpret_cast<__nv_bfloat16*>(out), ldo,
+        balanced);
     return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
   }
   static bool attr_set = false;
@@ -486,7 +493,7 @@ int launch_moe_gemm(const void* w, int w_rows_total, const void* act, int act_ro
   }
   const int grid = mgb_host::num_sms();
   mgb::moe_gemm_kernel<GATED><<<grid, 192, mgb::kGemmSmem, stream>>>(
-      tmA, tmB, offsets, E, MT, K, rows_per_expert, half_rows, reinterpret_cast<__nv_bfloat16*>(out), ldo);
+      tmA, tmB, offsets, E, MT, K, rows_per_expert, half_rows, reinterpret_cast<__nv_bfloat16*>(out), ldo, balanced);
   return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
 }
 }  // namespace

@@ -97,7 +97,7 @@ class Engine:
 
     def __init__(self, arch: ModelArch | str, plan=None, *, prompt_len: int, decode_len: int, seed: int = 0,
                  kv_policy: str = "resident", use_graph: bool = True, device: str = "cuda", ep=None,
-                 kv_ring_slots: int = 3):
+                 kv_ring_slots: int = 3, lookahead: bool = True):
         if not torch.cuda.is_available():
             raise RuntimeError("the B200 engine needs a CUDA device (there is no CPU fallback)")
         self.arch = get_arch(arch) if isinstance(arch, str) else arch
@@ -121,7 +121,15 @@ class Engine:
         self.ep = ep if (ep is not None and ep.world > 1) else None
         self.use_graph = use_graph and self.ep is None
         # ---- job list (structure only; durations are measured, not modelled) ----
-        self.schedule: Schedule = build_schedule(self.spec, b200_hardware(), _unit_latency, self.workload, self.plan,
+        # ---- CPU attention share (omega > 0): GQA over the host page store on the host cores ----
+        self.n_cpu = self.plan.cpu_sequences()
+        if self.n_cpu > 0 and (kv_policy != "offload" or self.mla_family() or ep is not None):
+            raise ValueError("a CPU attention share (omega > 0) needs kv_policy='offload', a GQA model and no EP "
+                             "(the paper runs DeepSeek with omega = 0, PAPER.md:509)")
+        hw_sched = b200_hardware()
+        if self.n_cpu > 0:  # the schedule only needs a nonzero CPU rate to admit CPU jobs
+            hw_sched = Hardware(**{**hw_sched.__dict__, "cpu_attn_flops": 1e11})
+        self.schedule: Schedule = build_schedule(self.spec, hw_sched, _unit_latency, self.workload, self.plan,
                                                  kv_policy=kv_policy)
         self.layer_jobs = [[] for _ in range(a.layers)]
         for j in self.schedule.jobs:
@@ -129,6 +137,7 @@ class Engine:
                 self.layer_jobs[j.layer].append(j)
         self.offload = self.plan.s_params < self.spec.model_bytes
         self.kv_ring_cap = kv_ring_slots
+        self.use_lookahead = lookahead
         # measurement only: False issues every job except the host<->device copies (compute-only
         # step time for the transfer/compute overlap figure; outputs are then meaningless)
         self.copies_enabled = True
@@ -228,14 +237,22 @@ class Engine:
         self.h2d = torch.cuda.Stream(device=device) if self.streaming else None
         self.d2h = torch.cuda.Stream(device=device) if kv_policy == "offload" else None
         self._join2 = torch.cuda.Event()
+        self.cpu_stream = torch.cuda.Stream(device=device) if self.n_cpu > 0 else None
+        self._join3 = torch.cuda.Event()
+        if self.n_cpu > 0:
+            self._init_cpu_attention()
         self._fork, self._join = torch.cuda.Event(), torch.cuda.Event()
         self.events = {i: torch.cuda.Event() for i in self.need_event}
         self.trace_events: dict | None = None  # job id -> (start, end) timing events (eager trace mode)
         self.kernel_launches_per_step = self._count_launches()
+        self.host_pos = 0
 
     # ------------------------------------------------------------------------------------
     # job issue
     # ------------------------------------------------------------------------------------
+    def mla_family(self) -> bool:
+        return self.arch.family == "deepseek_v2"
+
     def _plan_streams(self) -> None:
         """Cross-resource edges of the serialized schedule become cudaEvent waits; same-resource
         chains are plain in-order stream semantics.  Barriers are expanded into their producers."""
@@ -301,6 +318,10 @@ class Engine:
                 self.need_event.add(m)
         kv_out = {(j.layer, j.label.rsplit("/", 1)[1]): j.id for j in jobs if j.kind == "kv_copy_out"}
         for j in jobs:
+            if j.kind == "attn_mech_cpu":  # reads the host pages the share's KV_COPY_OUT writes
+                o = kv_out[(j.layer, "cpu")]
+                self.xwait[j.id] = sorted(set(self.xwait[j.id]) | {o})
+                self.need_event.add(o)
             if j.kind == "pre_attention" and (j.layer - 2, j.label.rsplit("/", 1)[1]) in kv_out:
                 o = kv_out[(j.layer - 2, j.label.rsplit("/", 1)[1])]
                 self.xwait[j.id] = sorted(set(self.xwait[j.id]) | {o})
@@ -322,7 +343,7 @@ class Engine:
         copies = [j for j in jobs if j.resource == "htod_link"]
         self.lookahead: list = []
         for c in copies:  # leading copies with no recycle wait on this step's compute
-            if self.xwait[c.id]:
+            if self.xwait[c.id] or not self.use_lookahead:
                 break
             self.lookahead.append(c)
         ids = {c.id for c in self.lookahead}
@@ -386,7 +407,8 @@ class Engine:
         torch.cuda.current_stream().wait_stream(self.h2d)
 
     def _stream_of(self, j) -> torch.cuda.Stream:
-        return {"htod_link": self.h2d, "dtoh_link": self.d2h}.get(j.resource, self.stream)
+        return {"htod_link": self.h2d, "dtoh_link": self.d2h, "cpu_compute": self.cpu_stream}.get(j.resource,
+                                                                                                    self.stream)
 
     def _init_kv_stream(self, n_stores: int, n_pages: int) -> None:
         """Full KV offload (reference memory_model.py:182-205): every sequence's pages live in pinned
@@ -428,6 +450,31 @@ class Engine:
             n_c = self.w.place.experts_per_layer[l]
             self.w.slots[self.slot_of[(l, e)]].copy_(self.w.host_experts[l][e - n_c], non_blocking=True)
         return True
+
+    def _init_cpu_attention(self) -> None:
+        """Pinned staging for the CPU share (q out, output back) and one job description per layer
+        for the host node (csrc/cpu_attn.cpp)."""
+        a, n = self.arch, self.n_cpu
+        width = a.n_heads * a.head_dim
+        self.cpu_q = torch.empty(n, width, dtype=BF16, pin_memory=True)
+        self.cpu_lens = torch.empty(n, dtype=torch.int32, pin_memory=True)
+        self.cpu_out = torch.empty(n, width, dtype=BF16, pin_memory=True)
+        self.cpu_desc = [nat.CpuAttnGqa(self.kv[l][0].data_ptr(), self.kv[l][1].data_ptr(), self.cpu_q.data_ptr(),
+                                        self.cpu_lens.data_ptr(), self.cpu_out.data_ptr(), 0, self.pps, n, a.n_heads,
+                                        a.n_kv_heads, a.head_dim, self.page, a.head_dim ** -0.5, 0)
+                         for l in range(a.layers)]
+
+    def _cpu_attention_job(self, l: int) -> None:
+        """ATTN_MECH_CPU (offload_dag.py:343-357): q and lengths of the CPU share go host-ward, the host
+        cores attend over the host page store (a host node of the step's graph), the output comes back
+        for post_attention.  All three on the CPU-attention stream, in order."""
+        import ctypes
+
+        b, n = self.buf, self.n_cpu
+        self.cpu_q.copy_(b.q[:n], non_blocking=True)
+        self.cpu_lens.copy_(b.seq_lens[:n], non_blocking=True)
+        nat.call("mgb_cpu_attn_gqa_enqueue", ctypes.byref(self.cpu_desc[l]), torch.cuda.current_stream().cuda_stream)
+        b.attn[:n].copy_(self.cpu_out, non_blocking=True)
 
     def _moved_bytes(self, j) -> float:
         """Bytes a copy job really moves: the schedule's bytes, except the expert copies the
@@ -625,6 +672,8 @@ class Engine:
         a, b = self.arch, self.buf
         if self._kv_job(l, j) or self._weight_copy_job(l, j):
             return
+        if j.kind == "attn_mech_cpu":
+            return self._cpu_attention_job(l)
         W = self._layer_weights(l)
         if self.mla:
             return self._ds_job(l, j, W)
@@ -664,10 +713,14 @@ class Engine:
             raise RuntimeError(f"job kind {j.kind!r} is not executable under kv_policy={self.kv_policy!r}")
 
     def _mb_range(self, j) -> tuple[int, int]:
+        """Sequences of a per-micro-batch job: the CPU share is [0, n_cpu), GPU micro-batch m is
+        [n_cpu + m*b_a, ...) (the schedule issues the CPU share first, offload_dag.py:328-357)."""
+        if j.label.endswith("/cpu"):
+            return 0, self.n_cpu
         mb = int(j.label.rsplit("mb", 1)[1])
-        s0 = mb * self.plan.b_a
+        s0 = self.n_cpu + mb * self.plan.b_a
         if j.kind in ("kv_copy_in", "kv_copy_out"):  # copy jobs carry bytes, not seqs
-            return s0, min(s0 + self.plan.b_a, self.plan.gpu_sequences())
+            return s0, min(s0 + self.plan.b_a, self.plan.B)
         return s0, s0 + j.seqs
 
     def _count_launches(self) -> int:
@@ -687,6 +740,8 @@ class Engine:
             self.h2d.wait_event(self._fork)
             if self.d2h is not None:
                 self.d2h.wait_event(self._fork)
+            if self.cpu_stream is not None:
+                self.cpu_stream.wait_event(self._fork)
             if not self._primed:  # eager first step: land this step's lookahead copies now
                 self._issue_lookahead(prologue=True)
                 self.stream.wait_stream(self.h2d)
@@ -704,6 +759,9 @@ class Engine:
             if self.d2h is not None:
                 self._join2.record(self.d2h)
                 self.stream.wait_event(self._join2)
+            if self.cpu_stream is not None:
+                self._join3.record(self.cpu_stream)
+                self.stream.wait_event(self._join3)
 
     # ------------------------------------------------------------------------------------
     # graph capture / replay
@@ -730,6 +788,11 @@ class Engine:
         self.graph = g
 
     def run_step(self) -> None:
+        # every sequence appends one token at `host_pos`: past the paged context the block table has
+        # no page for it, so refuse rather than let a kernel index outside the cache
+        if not 0 <= self.host_pos < self.max_ctx:
+            raise ValueError(f"decode position {self.host_pos} outside the planned context [0, {self.max_ctx})")
+        self.host_pos += 1
         if self.use_graph:
             if self.graph is None:
                 self.capture()
@@ -746,6 +809,7 @@ class Engine:
     # ------------------------------------------------------------------------------------
     def reset(self, start_pos: int = 0) -> None:
         self._primed = False
+        self.host_pos = start_pos  # host mirror of the (uniform) device positions
         self.buf.positions.fill_(start_pos)
         self.buf.seq_lens.fill_(start_pos)
         self.buf.step.zero_()
@@ -799,6 +863,7 @@ class Engine:
         """One eager step at absolute position `pos` (all sequences), returning intermediate
         tensors of layer 0 and the logits (parity tests)."""
         self.buf.positions.fill_(pos)
+        self.host_pos = pos + 1
         self.buf.next_ids.copy_(tokens.to(torch.int32))
         self.stream.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(self.stream):

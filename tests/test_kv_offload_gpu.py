@@ -125,3 +125,54 @@ def test_dsv2_offloaded_weights_and_kv_match_resident():
         phantom = sum(A.n_experts - pl.experts_per_layer[l] for l in range(A.first_k_dense)) * ex
         kv_in = A.layers * B * (P + N) * A.kv_bytes_per_token_layer if policy == "offload" else 0
         assert rep["bytes_htod"] == uncached - phantom + kv_in
+
+
+def test_cpu_attention_share_matches_gpu_engine():
+    """omega > 0 (MoE-Gen(H)): the first round(omega*B) sequences attend on the host cores over the
+    host page store (ATTN_MECH_CPU as a host node of the step graph), the rest on the GPU.
+    1. On a one-layer model (identical inputs, identical KV history) the attention outputs of the CPU
+       share match the all-GPU engine's within bf16 tolerance at every position, across a page.
+    2. End to end (4 layers, teacher forced) the logits keep the per-layer bar (median row error
+       <= 2e-2; a near-tied bf16 router logit may flip an expert).
+    3. Greedy decode runs eagerly and as a CUDA graph with identical results."""
+    import dataclasses
+
+    from paper_2503_09716_b200.configs import TINY as A
+    from paper_2503_09716_b200.engine import Engine
+    from paper_2503_09716_b200.planner import BatchingPlan, ModelSpec
+
+    def engines(arch, P, N):
+        mb = ModelSpec.from_document(arch.model_spec_document()).model_bytes
+        ref = Engine(arch, BatchingPlan(8, 4, 16, 0.0, 0, mb), prompt_len=P, decode_len=N, use_graph=False)
+        cpu = Engine(arch, BatchingPlan(8, 2, 16, 0.5, 0, mb), prompt_len=P, decode_len=N, use_graph=False,
+                     kv_policy="offload")
+        return ref, cpu
+
+    B, P, N = 8, 6, 70  # crosses a 64-token page
+    toks = torch.randint(0, A.vocab, (B, P + N), generator=torch.Generator().manual_seed(17))
+    ref, cpu = engines(dataclasses.replace(A, layers=1), P, N)
+    assert cpu.n_cpu == 4 and cpu.cpu_stream is not None
+    worst = 0.0
+    for pos in range(P + N):
+        outs = []
+        for e in (ref, cpu):
+            e.debug_taps = {}
+            e.debug_forward(toks[:, pos], pos)
+            outs.append(e.debug_taps["attn"][:4].float())
+        worst = max(worst, ((outs[0] - outs[1]).abs().max() / outs[0].abs().max()).item())
+    assert worst <= 1e-2, worst
+    ref, cpu = engines(A, P, N)
+    errs = []
+    for pos in range(P + N):
+        lr = ref.debug_forward(toks[:, pos], pos)["logits"].float()
+        lc = cpu.debug_forward(toks[:, pos], pos)["logits"].float()
+        errs += [((lr[i] - lc[i]).abs().max() / lr[i].abs().max()).item() for i in range(B)]
+    errs.sort()
+    assert errs[len(errs) // 2] <= 2e-2, errs[len(errs) // 2]
+    mb = ModelSpec.from_document(A.model_spec_document()).model_bytes
+    outs = [Engine(A, BatchingPlan(B, 2, 16, 0.5, 0, mb), prompt_len=P, decode_len=N, use_graph=g,
+                   kv_policy="offload").generate(toks[:, :P], 8) for g in (False, True)]
+    assert torch.equal(outs[0], outs[1])
+    cpu.reset(P)
+    recs, rep = cpu.trace_step()
+    assert rep["busy"].get("cpu_compute", 0.0) > 0 and {r["kind"] for r in recs} >= {"attn_mech_cpu", "kv_copy_out"}

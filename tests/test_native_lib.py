@@ -53,13 +53,13 @@ def test_sass_uses_tcgen05_and_tma():
     from paper_2503_09716_b200 import build
 
     build.build(verbose=False)
-    obj = os.path.join(ROOT, "paper_2503_09716_b200", "_lib", "moe_gemm.o")
+    obj = os.path.join(ROOT, "paper_2503_09716_b200", "_lib", "moe_gemm_cu.o")
     sass = subprocess.run(["cuobjdump", "-sass", obj], capture_output=True, text=True).stdout
     assert "UTCHMMA" in sass and "UTMALDG" in sass and "LDTM" in sass
-    attn = subprocess.run(["cuobjdump", "-sass", os.path.join(ROOT, "paper_2503_09716_b200", "_lib", "attn_gqa.o")],
+    attn = subprocess.run(["cuobjdump", "-sass", os.path.join(ROOT, "paper_2503_09716_b200", "_lib", "attn_gqa_cu.o")],
                           capture_output=True, text=True).stdout
     assert "UBLKCP" in attn and "HMMA" in attn
-    mla = subprocess.run(["cuobjdump", "-sass", os.path.join(ROOT, "paper_2503_09716_b200", "_lib", "attn_mla.o")],
+    mla = subprocess.run(["cuobjdump", "-sass", os.path.join(ROOT, "paper_2503_09716_b200", "_lib", "attn_mla_cu.o")],
                          capture_output=True, text=True).stdout
     assert "UTCHMMA" in mla and "UBLKCP" in mla and "LDTM" in mla
 

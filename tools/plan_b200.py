@@ -40,6 +40,9 @@ if args.profile_in:
     prof = json.load(open(args.profile_in))
 else:
     prof = profile_engine(arch, token_grid=[2 ** i for i in range(0, 14)])
+    if args.out:
+        with open(args.out + ".profile.json", "w") as f:
+            json.dump(prof, f)
 t_prof = time.time() - t0
 hw, curves = load_profile_document(prof)
 hw = Hardware(**{**hw.__dict__, "m_g": hw.m_g - int(args.reserve_gb * 2**30), "m_c": int(args.host_gb * 1e9)})
@@ -52,9 +55,12 @@ t0 = time.time()
 best = search(spec, hw, lat, wl, space, kv_policy=args.kv_policy)
 t_search = time.time() - t0
 plan = best.plan
+print("plan", plan, "predicted", best.t_forward, flush=True)
 eng = Engine(arch, plan, prompt_len=512, decode_len=256, use_graph=True, kv_policy=args.kv_policy)
 eng.synthetic_prefill()
-eng.reset(767)  # the planner prices attention at the full context (max_context, offload_dag.py:353)
+# the planner prices attention at the full context (max_context, offload_dag.py:353): time the last
+# steps of the decode phase
+eng.reset(768 - 2 - args.steps)
 eng.buf.next_ids.random_(0, arch.vocab)
 eng.capture()
 eng.prime()
