@@ -38,6 +38,18 @@ METRIC = "decode tokens/sec at prompt 512/gen 256"
 UNIT = "tokens/s"
 
 
+def _ncu_traffic(config: str, gemm: str):
+    """DRAM bytes (read + write) per launch of the dominant kernel from the committed ncu --set full
+    capture (profiles/ncu_traffic.json, written by tools/ncu_traffic.py), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            rows = json.load(f)
+        r = rows[config][gemm]
+        return r["dram_bytes"], r["source"]
+    except Exception:
+        return None, None
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -333,7 +345,8 @@ def run_ours(args, dist, rank, world) -> None:
         gu_tf = gu_flops / (gu["avg_ms"] * 1e-3) / 1e12
         roofline = {"kernel": "mgb_moe_gemm_gate_up (tcgen05 grouped GEMM + SiLU*up)", "bound": "tensor",
                     "achieved": gu_tf, "peak": tf_burst, "unit": "TFLOP/s", "frac": gu_tf / tf_burst}
-    roofline.update({"traffic": None, "algorithmic_bytes_per_launch": gu_bytes, "algorithmic_flops_per_launch": gu_flops,
+    traffic, traffic_src = _ncu_traffic(args.config, "gate_up")
+    roofline.update({"traffic": traffic, "traffic_source": traffic_src, "algorithmic_bytes_per_launch": gu_bytes, "algorithmic_flops_per_launch": gu_flops,
                      "avg_launch_ms": gu["avg_ms"], "peak_source": src, "tokens_per_expert": tok_per_expert,
                      "share_of_step": gu["ms_per_step"] / step_ms_eager})
     launches_per_step = eng.kernel_launches_per_step * N

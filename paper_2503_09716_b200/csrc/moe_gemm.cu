@@ -37,7 +37,10 @@ constexpr int kStages = 4;
 constexpr int kStageBytes = kATileBytes + kBTileBytes;
 constexpr int kAccStages = 2;                      // 2 x 256 TMEM columns
 constexpr int kXStride = 33;                       // padded row of the gate/up exchange buffer
-constexpr int kGemmSmem = kStages * kStageBytes + 64 * kXStride * 4 + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int kEpiGroups = 2;                      // epilogue warp groups (4 warps each, one per TMEM lane quarter)
+constexpr int kThreads = 64 + kEpiGroups * 128;    // TMA warp + MMA warp + epilogue warps
+constexpr int kXBytes = kEpiGroups * 64 * kXStride * 4;
+constexpr int kGemmSmem = kStages * kStageBytes + kXBytes + 1024 /*align*/ + 256 /*barriers*/;
 
 // Token tiles of an expert: as few as fit N <= 256.  The gated GEMM (heavier per-token epilogue)
 // sizes them equally (multiple of 32) so no unit is a tiny remainder whose epilogue cannot hide
@@ -76,14 +79,15 @@ struct UnitSched {
   }
 };
 
-MGB_DEVINL void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+// named barrier of one epilogue group (ids 1.., 128 threads); 0 is __syncthreads
+MGB_DEVINL void epi_bar(int group) { asm volatile("bar.sync %0, 128;" ::"r"(1 + group) : "memory"); }
 
 // One 32-token chunk of the gated epilogue.  TMEM lanes 0-63 hold gate, 64-127 up for the same 64
 // features; the gate warps finish tokens 0-15 of the chunk and the up warps tokens 16-31, each
 // taking the partner half through shared memory, so all four epilogue warps do the SiLU*up work.
 // h = bf16(bf16(silu(bf16(gate))) * bf16(up)) (HF MixtralExperts, modeling_mixtral.py:91-93).
 MGB_DEVINL void gated_chunk(uint32_t tl, int c0, int n, bool is_up, int f, float* xbuf, __nv_bfloat16* ocol,
-                            int ldo) {
+                            int ldo, int group) {
   uint32_t v[32];
   tmem_ld32(tl + c0, v);
   tmem_ld_wait();
@@ -95,28 +99,29 @@ MGB_DEVINL void gated_chunk(uint32_t tl, int c0, int n, bool is_up, int f, float
 #pragma unroll
     for (int j = 0; j < 16; ++j) xr[16 + j] = bf16_round(__uint_as_float(v[16 + j]));
   }
-  epi_bar();
+  epi_bar(group);
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
     const int c = c0 + (is_up ? 16 : 0) + j;
     const float mine = bf16_round(__uint_as_float(is_up ? v[16 + j] : v[j]));
     const float other = is_up ? xr[16 + j] : xr[j];
     const float gv = is_up ? other : mine, uv = is_up ? mine : other;
-    if (c < n) ocol[(size_t)c * ldo] = __float2bfloat16_rn(bf16_round(gv / (1.0f + expf(-gv))) * uv);
+    // silu in fp32 with the SFU exponential and a fast divide (within bf16 rounding of HF's silu)
+    if (c < n) ocol[(size_t)c * ldo] = __float2bfloat16_rn(bf16_round(__fdividef(gv, 1.0f + __expf(-gv))) * uv);
   }
-  epi_bar();
+  epi_bar(group);
 }
 
 template <bool GATED>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(kThreads, 1)
 moe_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const int* __restrict__ offsets, int E, int MT, int K, int rows_per_expert, int half_rows,
                 __nv_bfloat16* __restrict__ out, int ldo, bool balanced) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* tiles = smem;
-  float* xbuf = reinterpret_cast<float*>(smem + kStages * kStageBytes);  // [64][kXStride] up values
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(xbuf + 64 * kXStride);
+  float* xbuf = reinterpret_cast<float*>(smem + kStages * kStageBytes);  // [group][64][kXStride] exchange
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes + kXBytes);
   uint64_t* empty_bar = full_bar + kStages;
   uint64_t* tfull_bar = empty_bar + kStages;
   uint64_t* tempty_bar = tfull_bar + kAccStages;
@@ -146,7 +151,7 @@ moe_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     }
     for (int s = 0; s < kAccStages; ++s) {
       mbar_init(&tfull_bar[s], 1);
-      mbar_init(&tempty_bar[s], 128);
+      mbar_init(&tempty_bar[s], kEpiGroups * 128);
     }
     fence_mbar_init();
   }
@@ -224,6 +229,8 @@ moe_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     // ------------------------------ epilogue (warps 2..5) ------------------------------
     const uint32_t q = warp & 3;          // TMEM lane quarter this warp may access
     const int row = q * 32 + lane;        // accumulator row (lane) of this thread
+    const int group = (warp - 2) >> 2;    // column group: 32-token chunks group, group + kEpiGroups, ...
+    float* gx = xbuf + group * 64 * kXStride;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = blockIdx.x; u < total; u += gridDim.x) {
@@ -237,10 +244,10 @@ moe_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const bool is_up = q >= 2;
         const int f = row & 63;
         __nv_bfloat16* ocol = out + (size_t)tok0 * ldo + mt * kRowsPerUnit + f;
-        for (int c0 = 0; c0 < n; c0 += 32) gated_chunk(tl, c0, n, is_up, f, xbuf, ocol, ldo);
+        for (int c0 = 32 * group; c0 < n; c0 += 32 * kEpiGroups) gated_chunk(tl, c0, n, is_up, f, gx, ocol, ldo, group);
       } else {
         __nv_bfloat16* ocol = out + (size_t)tok0 * ldo + mt * kRowsPerUnit + row;
-        for (int c0 = 0; c0 < n; c0 += 32) {
+        for (int c0 = 32 * group; c0 < n; c0 += 32 * kEpiGroups) {
           uint32_t v[32];
           tmem_ld32(tl + c0, v);
           tmem_ld_wait();
@@ -271,10 +278,10 @@ constexpr int kPStages = 6;
 constexpr int kPBRows = 16;                                   // token rows per TMA box (2 KB)
 constexpr int kPBBoxBytes = kPBRows * kBK * 2;
 constexpr int kPStageBytes = kATileBytes + (kBNMax / 2) * kBK * 2;  // 16 KB A + <= 16 KB half-B
-constexpr int kPairSmem = kPStages * kPStageBytes + 64 * kXStride * 4 + 1024 + 256;
+constexpr int kPairSmem = kPStages * kPStageBytes + kXBytes + 1024 + 256;
 
 template <bool GATED>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const int* __restrict__ offsets, int E, int MT, int K, int rows_per_expert, int half_rows,
                      __nv_bfloat16* __restrict__ out, int ldo, bool balanced) {
@@ -282,7 +289,7 @@ moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* tiles = smem;
   float* xbuf = reinterpret_cast<float*>(smem + kPStages * kPStageBytes);
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(xbuf + 64 * kXStride);
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kPStages * kPStageBytes + kXBytes);
   uint64_t* empty_bar = full_bar + kPStages;
   uint64_t* tfull_bar = empty_bar + kPStages;
   uint64_t* tempty_bar = tfull_bar + kAccStages;
@@ -313,7 +320,7 @@ moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
     }
     for (int s = 0; s < kAccStages; ++s) {
       mbar_init(&tfull_bar[s], 1);
-      mbar_init(&tempty_bar[s], 2 * 4);  // both CTAs' epilogue warps (used on the leader)
+      mbar_init(&tempty_bar[s], 2 * 4 * kEpiGroups);  // both CTAs' epilogue warps (used on the leader)
     }
     fence_mbar_init();
   }
@@ -399,6 +406,8 @@ moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
     // ------------------------------ epilogue (warps 2..5, both CTAs) ------------------------------
     const uint32_t q = warp & 3;
     const int row = q * 32 + lane;
+    const int group = (warp - 2) >> 2;
+    float* gx = xbuf + group * 64 * kXStride;
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty_bar[0]), 0);
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -413,10 +422,10 @@ moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
         const bool is_up = q >= 2;
         const int f = row & 63;
         __nv_bfloat16* ocol = out + (size_t)tok0 * ldo + col0 + f;
-        for (int c0 = 0; c0 < n; c0 += 32) gated_chunk(tl, c0, n, is_up, f, xbuf, ocol, ldo);
+        for (int c0 = 32 * group; c0 < n; c0 += 32 * kEpiGroups) gated_chunk(tl, c0, n, is_up, f, gx, ocol, ldo, group);
       } else {
         __nv_bfloat16* ocol = out + (size_t)tok0 * ldo + col0 + row;
-        for (int c0 = 0; c0 < n; c0 += 32) {
+        for (int c0 = 32 * group; c0 < n; c0 += 32 * kEpiGroups) {
           uint32_t v[32];
           tmem_ld32(tl + c0, v);
           tmem_ld_wait();
@@ -479,7 +488,7 @@ int launch_moe_gemm(const void* w, int w_rows_total, const void* act, int act_ro
       attr_p = true;
     }
     const int grid = mgb_host::num_sms() & ~1;
-    mgb::moe_gemm_pair_kernel<GATED><<<grid, 192, mgb::kPairSmem, stream>>>(
+    mgb::moe_gemm_pair_kernel<GATED><<<grid, mgb::kThreads, mgb::kPairSmem, stream>>>(
         tmA, tmB, offsets, E, MT / 2, K, rows_per_expert, half_rows, reinterpret_cast<__nv_bfloat16*>(out), ldo,
         balanced);
     return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
@@ -492,7 +501,7 @@ int launch_moe_gemm(const void* w, int w_rows_total, const void* act, int act_ro
     attr_set = true;
   }
   const int grid = mgb_host::num_sms();
-  mgb::moe_gemm_kernel<GATED><<<grid, 192, mgb::kGemmSmem, stream>>>(
+  mgb::moe_gemm_kernel<GATED><<<grid, mgb::kThreads, mgb::kGemmSmem, stream>>>(
       tmA, tmB, offsets, E, MT, K, rows_per_expert, half_rows, reinterpret_cast<__nv_bfloat16*>(out), ldo, balanced);
   return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
 }

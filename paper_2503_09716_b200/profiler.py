@@ -11,6 +11,7 @@ on one decoder layer of the model, and timed with CUDA events (median of `reps` 
     post_attention            O projection + residual add + RMSNorm (+ DeepSeek shared experts)
     router                    gate logits GEMM + fused top-k/softmax/counts + stable permutation
     expert                    grouped gate/up+SiLU and down GEMMs of ONE expert with `tokens` rows
+    attention_mechanism_cpu   (GQA models, `cpu_token_grid`) the host-core attention of the CPU share
 
 The result is a profile document in the reference's schema (hw_profile.py:156-249, ingestible by
 its `ingest_profile`), with the machine's capacities and measured link/HBM rates.
@@ -74,9 +75,41 @@ def measured_hardware(host_bytes: int | None = None) -> Hardware:
                     cpu_attn_flops=0.0)
 
 
+def _profile_cpu_attention(arch: ModelArch, token_grid: Sequence[int], ctx_grid: Sequence[int]):
+    """ATTN_MECH_CPU on the host cores (csrc/cpu_attn.cpp) for T sequences over `ctx` keys; also the
+    achieved attention FLOP/s (the reference's cpu_attn_flops, hw_profile.py:52-149)."""
+    import ctypes
+    import time
+
+    a, P = arch, ops.kv_page_size()
+    Tm, cm = max(token_grid), max(ctx_grid)
+    pps = (cm + P - 1) // P
+    blk = a.n_kv_heads * a.head_dim * P
+    k = torch.zeros(Tm * pps * blk, dtype=BF16)
+    v = torch.zeros(Tm * pps * blk, dtype=BF16)
+    q = torch.zeros(Tm, a.n_heads * a.head_dim, dtype=BF16)
+    out = torch.empty_like(q)
+    rows, rate = [], 0.0
+    for T in token_grid:
+        for ctx in ctx_grid:
+            lens = torch.full((T,), ctx, dtype=torch.int32)
+            d = nat.CpuAttnGqa(k.data_ptr(), v.data_ptr(), q.data_ptr(), lens.data_ptr(), out.data_ptr(), 0, pps, T,
+                               a.n_heads, a.n_kv_heads, a.head_dim, P, 1.0, 0)
+            nat.call("mgb_cpu_attn_gqa", ctypes.byref(d))
+            ts = []
+            for _ in range(3):
+                t0 = time.perf_counter()
+                nat.call("mgb_cpu_attn_gqa", ctypes.byref(d))
+                ts.append(time.perf_counter() - t0)
+            sec = statistics.median(ts)
+            rows.append([T, ctx, sec])
+            rate = max(rate, T * ctx * 4 * a.n_heads * a.head_dim / sec)
+    return rows, rate
+
+
 def profile_engine(arch: ModelArch | str, token_grid: Sequence[int] | None = None,
                    ctx_grid: Sequence[int] = (128, 512, 768), reps: int = 5,
-                   hardware: Hardware | None = None) -> dict:
+                   hardware: Hardware | None = None, cpu_token_grid: Sequence[int] = ()) -> dict:
     """Profile document with measured tables for every GPU module kind of `arch` (one decoder
     layer of it is instantiated; the latency of a job does not depend on the layer index)."""
     from .engine import Engine
@@ -164,6 +197,9 @@ def profile_engine(arch: ModelArch | str, token_grid: Sequence[int] | None = Non
             tables["attention_mechanism_gpu"].append([T, ctx, _time(attn, reps)])
     del eng
     torch.cuda.empty_cache()
+    cpu_rate = 0.0
+    if not full.is_mla and cpu_token_grid:
+        tables["attention_mechanism_cpu"], cpu_rate = _profile_cpu_attention(one, cpu_token_grid, ctx_grid)
     # the reference requires tables monotone in tokens (hw_profile.py:117-142): running max per context
     for k, v in tables.items():
         best: dict[int, float] = {}
@@ -171,4 +207,6 @@ def profile_engine(arch: ModelArch | str, token_grid: Sequence[int] | None = Non
             e[2] = best[e[1]] = max(e[2], best.get(e[1], 0.0))
     curves = [LatencyCurve(k, [tuple(e) for e in v]) for k, v in tables.items()]
     hw = hardware or measured_hardware()
+    if cpu_rate > 0:
+        hw = Hardware(**{**hw.__dict__, "cpu_attn_flops": cpu_rate})
     return profile_document(hw, curves)

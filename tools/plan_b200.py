@@ -30,6 +30,7 @@ ap.add_argument("--host-gb", type=float, default=170.0)
 ap.add_argument("--reserve-gb", type=float, default=12.0)
 ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--profile-in", default=None)
+ap.add_argument("--cpu-attention", action="store_true", help="profile the host-core attention and search omega")
 ap.add_argument("--out", default=None)
 args = ap.parse_args()
 
@@ -39,7 +40,8 @@ t0 = time.time()
 if args.profile_in:
     prof = json.load(open(args.profile_in))
 else:
-    prof = profile_engine(arch, token_grid=[2 ** i for i in range(0, 14)])
+    prof = profile_engine(arch, token_grid=[2 ** i for i in range(0, 14)],
+                          cpu_token_grid=[16, 64, 256, 1024] if args.cpu_attention else ())
     if args.out:
         with open(args.out + ".profile.json", "w") as f:
             json.dump(prof, f)
@@ -49,7 +51,8 @@ hw = Hardware(**{**hw.__dict__, "m_g": hw.m_g - int(args.reserve_gb * 2**30), "m
 lat = latency_from_curves(curves)
 spec = ModelSpec.from_document(arch.model_spec_document())
 wl = WorkloadSpec(512, 256, 1_000_000, "decode")
-space = SearchSpace(b_a_grid=(64, 128, 256, 512, 1024), b_e_grid=(1024, 4096, 16384), omega_grid=(0.0,),
+omegas = tuple(round(0.1 * i, 1) for i in range(9)) if args.cpu_attention else (0.0,)
+space = SearchSpace(b_a_grid=(64, 128, 256, 512, 1024), b_e_grid=(1024, 4096, 16384), omega_grid=omegas,
                     s_expert_slots_grid=(2, 4, 8), s_params_fracs=(0.0, 0.25, 0.5, 0.75, 1.0))
 t0 = time.time()
 best = search(spec, hw, lat, wl, space, kv_policy=args.kv_policy)
@@ -73,7 +76,12 @@ for _ in range(args.steps):
 e1.record()
 torch.cuda.synchronize()
 t_meas = e0.elapsed_time(e1) * 1e-3 / args.steps
+base = None
+if args.cpu_attention:  # the best all-GPU plan of the same search, for the omega > 0 gain
+    base = search(spec, hw, lat, wl, dataclasses.replace(space, omega_grid=(0.0,)), kv_policy=args.kv_policy)
 out = {"config": arch.name, "kv_policy": args.kv_policy, "plan": plan.to_document(),
+       "omega0_plan": base.plan.to_document() if base else None,
+       "omega0_predicted_tokens_per_s": base.throughput if base else None,
        "predicted_forward_s": best.t_forward, "measured_forward_s": t_meas,
        "predicted_tokens_per_s": best.throughput, "measured_tokens_per_s": plan.B / t_meas,
        "rel_err": (t_meas - best.t_forward) / best.t_forward,
