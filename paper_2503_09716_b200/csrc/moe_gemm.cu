@@ -37,10 +37,20 @@ constexpr int kStages = 4;
 constexpr int kStageBytes = kATileBytes + kBTileBytes;
 constexpr int kAccStages = 2;                      // 2 x 256 TMEM columns
 constexpr int kXStride = 33;                       // padded row of the gate/up exchange buffer
-constexpr int kEpiGroups = 2;                      // epilogue warp groups (4 warps each, one per TMEM lane quarter)
-constexpr int kThreads = 64 + kEpiGroups * 128;    // TMA warp + MMA warp + epilogue warps
-constexpr int kXBytes = kEpiGroups * 64 * kXStride * 4;
-constexpr int kGemmSmem = kStages * kStageBytes + kXBytes + 1024 /*align*/ + 256 /*barriers*/;
+// epilogue warp groups (4 warps each, one per TMEM lane quarter): the gated epilogue (SiLU*up with a
+// shared-memory exchange) is the critical path of the gate/up GEMM at DeepSeek shapes, so it gets two
+// groups working on alternate 32-token chunks; the plain epilogue keeps one
+#ifndef MGB_GATED_EPI_GROUPS
+#define MGB_GATED_EPI_GROUPS 2
+#endif
+template <bool GATED> struct Epi {
+  static constexpr int kGroups = GATED ? MGB_GATED_EPI_GROUPS : 1;
+  static constexpr int kThreads = 64 + kGroups * 128;  // TMA warp + MMA warp + epilogue warps
+  static constexpr int kXBytes = GATED ? kGroups * 64 * kXStride * 4 : 0;  // gate/up exchange buffers
+};
+template <bool GATED> constexpr int gemm_smem() {
+  return kStages * kStageBytes + Epi<GATED>::kXBytes + 1024 /*align*/ + 256 /*barriers*/;
+}
 
 // Token tiles of an expert: as few as fit N <= 256.  The gated GEMM (heavier per-token epilogue)
 // sizes them equally (multiple of 32) so no unit is a tiny remainder whose epilogue cannot hide
@@ -113,7 +123,7 @@ MGB_DEVINL void gated_chunk(uint32_t tl, int c0, int n, bool is_up, int f, float
 }
 
 template <bool GATED>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(Epi<GATED>::kThreads, 1)
 moe_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const int* __restrict__ offsets, int E, int MT, int K, int rows_per_expert, int half_rows,
                 __nv_bfloat16* __restrict__ out, int ldo, bool balanced) {
@@ -121,7 +131,7 @@ moe_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* tiles = smem;
   float* xbuf = reinterpret_cast<float*>(smem + kStages * kStageBytes);  // [group][64][kXStride] exchange
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes + kXBytes);
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes + Epi<GATED>::kXBytes);
   uint64_t* empty_bar = full_bar + kStages;
   uint64_t* tfull_bar = empty_bar + kStages;
   uint64_t* tempty_bar = tfull_bar + kAccStages;
@@ -151,7 +161,7 @@ moe_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     }
     for (int s = 0; s < kAccStages; ++s) {
       mbar_init(&tfull_bar[s], 1);
-      mbar_init(&tempty_bar[s], kEpiGroups * 128);
+      mbar_init(&tempty_bar[s], Epi<GATED>::kGroups * 128);
     }
     fence_mbar_init();
   }
@@ -229,7 +239,7 @@ moe_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     // ------------------------------ epilogue (warps 2..5) ------------------------------
     const uint32_t q = warp & 3;          // TMEM lane quarter this warp may access
     const int row = q * 32 + lane;        // accumulator row (lane) of this thread
-    const int group = (warp - 2) >> 2;    // column group: 32-token chunks group, group + kEpiGroups, ...
+    const int group = Epi<GATED>::kGroups > 1 ? (int)(warp - 2) >> 2 : 0;  // column group (32-token chunks)
     float* gx = xbuf + group * 64 * kXStride;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -244,10 +254,10 @@ moe_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const bool is_up = q >= 2;
         const int f = row & 63;
         __nv_bfloat16* ocol = out + (size_t)tok0 * ldo + mt * kRowsPerUnit + f;
-        for (int c0 = 32 * group; c0 < n; c0 += 32 * kEpiGroups) gated_chunk(tl, c0, n, is_up, f, gx, ocol, ldo, group);
+        for (int c0 = 32 * group; c0 < n; c0 += 32 * Epi<GATED>::kGroups) gated_chunk(tl, c0, n, is_up, f, gx, ocol, ldo, group);
       } else {
         __nv_bfloat16* ocol = out + (size_t)tok0 * ldo + mt * kRowsPerUnit + row;
-        for (int c0 = 32 * group; c0 < n; c0 += 32 * kEpiGroups) {
+        for (int c0 = 32 * group; c0 < n; c0 += 32 * Epi<GATED>::kGroups) {
           uint32_t v[32];
           tmem_ld32(tl + c0, v);
           tmem_ld_wait();
@@ -278,10 +288,12 @@ constexpr int kPStages = 6;
 constexpr int kPBRows = 16;                                   // token rows per TMA box (2 KB)
 constexpr int kPBBoxBytes = kPBRows * kBK * 2;
 constexpr int kPStageBytes = kATileBytes + (kBNMax / 2) * kBK * 2;  // 16 KB A + <= 16 KB half-B
-constexpr int kPairSmem = kPStages * kPStageBytes + kXBytes + 1024 + 256;
+template <bool GATED> constexpr int pair_smem() {
+  return kPStages * kPStageBytes + Epi<GATED>::kXBytes + 1024 + 256;
+}
 
 template <bool GATED>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Epi<GATED>::kThreads, 1)
 moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const int* __restrict__ offsets, int E, int MT, int K, int rows_per_expert, int half_rows,
                      __nv_bfloat16* __restrict__ out, int ldo, bool balanced) {
@@ -289,7 +301,7 @@ moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* tiles = smem;
   float* xbuf = reinterpret_cast<float*>(smem + kPStages * kPStageBytes);
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kPStages * kPStageBytes + kXBytes);
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kPStages * kPStageBytes + Epi<GATED>::kXBytes);
   uint64_t* empty_bar = full_bar + kPStages;
   uint64_t* tfull_bar = empty_bar + kPStages;
   uint64_t* tempty_bar = tfull_bar + kAccStages;
@@ -320,7 +332,7 @@ moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
     }
     for (int s = 0; s < kAccStages; ++s) {
       mbar_init(&tfull_bar[s], 1);
-      mbar_init(&tempty_bar[s], 2 * 4 * kEpiGroups);  // both CTAs' epilogue warps (used on the leader)
+      mbar_init(&tempty_bar[s], 2 * 4 * Epi<GATED>::kGroups);  // both CTAs' epilogue warps (used on the leader)
     }
     fence_mbar_init();
   }
@@ -406,7 +418,7 @@ moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
     // ------------------------------ epilogue (warps 2..5, both CTAs) ------------------------------
     const uint32_t q = warp & 3;
     const int row = q * 32 + lane;
-    const int group = (warp - 2) >> 2;
+    const int group = Epi<GATED>::kGroups > 1 ? (int)(warp - 2) >> 2 : 0;
     float* gx = xbuf + group * 64 * kXStride;
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty_bar[0]), 0);
     int acc = 0;
@@ -422,10 +434,10 @@ moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
         const bool is_up = q >= 2;
         const int f = row & 63;
         __nv_bfloat16* ocol = out + (size_t)tok0 * ldo + col0 + f;
-        for (int c0 = 32 * group; c0 < n; c0 += 32 * kEpiGroups) gated_chunk(tl, c0, n, is_up, f, gx, ocol, ldo, group);
+        for (int c0 = 32 * group; c0 < n; c0 += 32 * Epi<GATED>::kGroups) gated_chunk(tl, c0, n, is_up, f, gx, ocol, ldo, group);
       } else {
         __nv_bfloat16* ocol = out + (size_t)tok0 * ldo + col0 + row;
-        for (int c0 = 32 * group; c0 < n; c0 += 32 * kEpiGroups) {
+        for (int c0 = 32 * group; c0 < n; c0 += 32 * Epi<GATED>::kGroups) {
           uint32_t v[32];
           tmem_ld32(tl + c0, v);
           tmem_ld_wait();
@@ -483,12 +495,12 @@ int launch_moe_gemm(const void* w, int w_rows_total, const void* act, int act_ro
     static bool attr_p = false;
     if (!attr_p) {
       if (cudaFuncSetAttribute(mgb::moe_gemm_pair_kernel<GATED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               mgb::kPairSmem) != cudaSuccess)
+                               mgb::pair_smem<GATED>()) != cudaSuccess)
         return MGB_ECUDA;
       attr_p = true;
     }
     const int grid = mgb_host::num_sms() & ~1;
-    mgb::moe_gemm_pair_kernel<GATED><<<grid, mgb::kThreads, mgb::kPairSmem, stream>>>(
+    mgb::moe_gemm_pair_kernel<GATED><<<grid, mgb::Epi<GATED>::kThreads, mgb::pair_smem<GATED>(), stream>>>(
         tmA, tmB, offsets, E, MT / 2, K, rows_per_expert, half_rows, reinterpret_cast<__nv_bfloat16*>(out), ldo,
         balanced);
     return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
@@ -496,12 +508,12 @@ int launch_moe_gemm(const void* w, int w_rows_total, const void* act, int act_ro
   static bool attr_set = false;
   if (!attr_set) {
     if (cudaFuncSetAttribute(mgb::moe_gemm_kernel<GATED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             mgb::kGemmSmem) != cudaSuccess)
+                             mgb::gemm_smem<GATED>()) != cudaSuccess)
       return MGB_ECUDA;
     attr_set = true;
   }
   const int grid = mgb_host::num_sms();
-  mgb::moe_gemm_kernel<GATED><<<grid, mgb::kThreads, mgb::kGemmSmem, stream>>>(
+  mgb::moe_gemm_kernel<GATED><<<grid, mgb::Epi<GATED>::kThreads, mgb::gemm_smem<GATED>(), stream>>>(
       tmA, tmB, offsets, E, MT, K, rows_per_expert, half_rows, reinterpret_cast<__nv_bfloat16*>(out), ldo, balanced);
   return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
 }

@@ -69,12 +69,20 @@ def run(E, d, f, counts, check=True, iters=0):
             t2 += ev1.elapsed_time(ev2)
         t1 /= iters
         t2 /= iters
+        t3 = 0.0
+        for _ in range(iters):  # down alone, back to back (no gate/up in between)
+            ev1.record()
+            nat.call("mgb_moe_gemm_down", wd.data_ptr(), H.data_ptr(), offs_t.data_ptr(), E, d, f, cap, Y.data_ptr(), s)
+            ev2.record()
+            torch.cuda.synchronize()
+            t3 += ev1.elapsed_time(ev2)
+        t3 /= iters
         nz = sum(1 for c in counts if c > 0)
         b1 = nz * 2 * f * d * 2
         b2 = nz * d * f * 2
         fl1 = 2 * rows * d * 2 * f
         fl2 = 2 * rows * d * f
-        print(f"  gate_up {t1*1e3:.1f} us  {b1/t1/1e6:.0f} GB/s  {fl1/t1/1e9:.0f} TF/s | down {t2*1e3:.1f} us {b2/t2/1e6:.0f} GB/s {fl2/t2/1e9:.0f} TF/s")
+        print(f"  gate_up {t1*1e3:.1f} us  {b1/t1/1e6:.0f} GB/s  {fl1/t1/1e9:.0f} TF/s | down {t2*1e3:.1f} us {b2/t2/1e6:.0f} GB/s {fl2/t2/1e9:.0f} TF/s | down alone {t3*1e3:.1f} us")
 
 
 SHAPES = {  # bench shapes: tokens per expert at the planner's batch
