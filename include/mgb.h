@@ -118,6 +118,11 @@ int mgb_add_rmsnorm(const void* x, const void* delta, const void* weight, float 
 int mgb_rope_append_gqa(const void* qkv, int T, int seq0, const int* positions, const float* cos_t,
                         const float* sin_t, int Hq, int Hkv, int head_dim, const int* block_table, int max_pages,
                         void* k_cache, void* v_cache, void* q_out, int* seq_lens, void* stream);
+/* prefill (T = n_seq * P prompt tokens, token t = position t % P of sequence seq0 + t / P): RoPE'd q
+ * to q_out, K/V into the pages and into contiguous k_out / v_out [T, Hkv, hd] for the causal attention */
+int mgb_rope_append_gqa_prefill(const void* qkv, int T, int seq0, int P, const float* cos_t, const float* sin_t,
+                                int Hq, int Hkv, int head_dim, const int* block_table, int max_pages, void* k_cache,
+                                void* v_cache, void* q_out, void* k_out, void* v_out, void* stream);
 int mgb_embed(const int* ids, const void* table, int T, int d, void* out, void* stream);
 /* h[T,F] = bf16(bf16(silu(g)) * u) for gate_up[T, 2F] = [g | u] (dense/shared-expert MLP epilogue) */
 int mgb_silu_mul(const void* gate_up, int T, int F, void* h, void* stream);

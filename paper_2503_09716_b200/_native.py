@@ -38,6 +38,7 @@ SIGNATURES: dict[str, list] = {
     # elementwise.cu
     "mgb_add_rmsnorm": [P, P, P, F, I, I, P, P, P],
     "mgb_rope_append_gqa": [P, I, I, P, P, P, I, I, I, P, I, P, P, P, P, P],
+    "mgb_rope_append_gqa_prefill": [P, I, I, I, P, P, I, I, I, P, I, P, P, P, P, P, P],
     "mgb_embed": [P, P, I, I, P, P],
     "mgb_silu_mul": [P, I, I, P, P],
     "mgb_argmax": [P, I, I, P, P],

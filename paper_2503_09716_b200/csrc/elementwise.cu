@@ -133,6 +133,61 @@ __global__ void rope_append_gqa_kernel(const __nv_bfloat16* __restrict__ qkv, in
   }
 }
 
+// Prefill variant: T = n_seq * P prompt tokens, token t of the batch is position t % P of sequence
+// seq0 + t / P.  q heads are rotated into q_out [T, Hq, hd]; k heads rotated and v heads copied into
+// the chunk-major KV pages AND into the contiguous k_out / v_out [T, Hkv, hd] rows the causal
+// prefill attention reads.  Same rotation arithmetic as rope_append_gqa_kernel.
+__global__ void rope_append_gqa_prefill_kernel(const __nv_bfloat16* __restrict__ qkv, int T, int seq0, int P,
+                                               const float* __restrict__ cos_t, const float* __restrict__ sin_t,
+                                               int Hq, int Hkv, int hd, const int* __restrict__ block_table,
+                                               int max_pages, __nv_bfloat16* __restrict__ k_cache,
+                                               __nv_bfloat16* __restrict__ v_cache, __nv_bfloat16* __restrict__ q_out,
+                                               __nv_bfloat16* __restrict__ k_out, __nv_bfloat16* __restrict__ v_out) {
+  const int nch = hd / 8;
+  const int H = Hq + 2 * Hkv;
+  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (long long)T * H * nch) return;
+  const int c = (int)(gid % nch);
+  const long long th = gid / nch;
+  const int t = (int)(th / H), hh = (int)(th - (long long)t * H);
+  const int seq = seq0 + t / P;
+  const int pos = t % P;
+  const __nv_bfloat16* src = qkv + ((size_t)t * H + hh) * hd;
+  const uint4 xv = reinterpret_cast<const uint4*>(src)[c];
+  uint4 ov = xv;
+  if (hh < Hq + Hkv) {
+    const int half_ch = nch / 2;
+    const bool lo = c < half_ch;
+    const uint4 pv = reinterpret_cast<const uint4*>(src)[lo ? c + half_ch : c - half_ch];
+    const float x[8] = {bf16lo(xv.x), bf16hi(xv.x), bf16lo(xv.y), bf16hi(xv.y),
+                        bf16lo(xv.z), bf16hi(xv.z), bf16lo(xv.w), bf16hi(xv.w)};
+    const float pr[8] = {bf16lo(pv.x), bf16hi(pv.x), bf16lo(pv.y), bf16hi(pv.y),
+                         bf16lo(pv.z), bf16hi(pv.z), bf16lo(pv.w), bf16hi(pv.w)};
+    const int fi0 = (lo ? c : c - half_ch) * 8;
+    const float* cs = cos_t + (size_t)pos * (hd / 2) + fi0;
+    const float* sn = sin_t + (size_t)pos * (hd / 2) + fi0;
+    float r[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float rh = lo ? -pr[i] : pr[i];  // rotate_half
+      r[i] = bf16_round(x[i] * cs[i]) + bf16_round(rh * sn[i]);
+    }
+    ov.x = pack_bf16x2(r[0], r[1]); ov.y = pack_bf16x2(r[2], r[3]);
+    ov.z = pack_bf16x2(r[4], r[5]); ov.w = pack_bf16x2(r[6], r[7]);
+  }
+  if (hh < Hq) {
+    reinterpret_cast<uint4*>(q_out + ((size_t)t * Hq + hh) * hd)[c] = ov;
+  } else {
+    const bool is_k = hh < Hq + Hkv;
+    const int kh = is_k ? hh - Hq : hh - Hq - Hkv;
+    const int page = block_table[(size_t)seq * max_pages + pos / kPageTok];
+    const size_t blk = ((size_t)page * Hkv + kh) * hd * kPageTok;
+    __nv_bfloat16* dst = (is_k ? k_cache : v_cache) + blk + ((size_t)c * kPageTok + pos % kPageTok) * 8;
+    *reinterpret_cast<uint4*>(dst) = ov;
+    reinterpret_cast<uint4*>((is_k ? k_out : v_out) + ((size_t)t * Hkv + kh) * hd)[c] = ov;
+  }
+}
+
 // h = bf16(bf16(silu(g)) * u) for gu = [g | u] rows (HF DeepseekV2MLP / MixtralExperts act-mul on the
 // bf16 outputs of a cuBLAS gate|up GEMM).  8 features per thread, 16 B in/out.
 __global__ void silu_mul_kernel(const __nv_bfloat16* __restrict__ gu, int T, int F, __nv_bfloat16* __restrict__ h) {
@@ -270,6 +325,21 @@ int mgb_rope_append_gqa(const void* qkv, int T, int seq0, const int* positions, 
       reinterpret_cast<const __nv_bfloat16*>(qkv), T, seq0, positions, cos_t, sin_t, Hq, Hkv, head_dim, block_table,
       max_pages, reinterpret_cast<__nv_bfloat16*>(k_cache), reinterpret_cast<__nv_bfloat16*>(v_cache),
       reinterpret_cast<__nv_bfloat16*>(q_out), seq_lens);
+  return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
+}
+
+int mgb_rope_append_gqa_prefill(const void* qkv, int T, int seq0, int P, const float* cos_t, const float* sin_t,
+                                int Hq, int Hkv, int head_dim, const int* block_table, int max_pages, void* k_cache,
+                                void* v_cache, void* q_out, void* k_out, void* v_out, void* stream) {
+  if (T < 1 || P < 1 || T % P || head_dim % 16 || Hq % Hkv) return MGB_EINVAL;
+  const long long items = (long long)T * (Hq + 2 * Hkv) * (head_dim / 8);
+  const int threads = 256;
+  mgb::rope_append_gqa_prefill_kernel<<<(int)((items + threads - 1) / threads), threads, 0,
+                                        reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const __nv_bfloat16*>(qkv), T, seq0, P, cos_t, sin_t, Hq, Hkv, head_dim, block_table, max_pages,
+      reinterpret_cast<__nv_bfloat16*>(k_cache), reinterpret_cast<__nv_bfloat16*>(v_cache),
+      reinterpret_cast<__nv_bfloat16*>(q_out), reinterpret_cast<__nv_bfloat16*>(k_out),
+      reinterpret_cast<__nv_bfloat16*>(v_out));
   return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
 }
 

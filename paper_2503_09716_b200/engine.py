@@ -841,18 +841,98 @@ class Engine:
             self.run_step()
         return self.out_tokens[:, :n_steps].to("cpu", non_blocking=False)
 
+    def can_prefill(self) -> bool:
+        """Batched prefill is built for GQA models with HBM-resident weights and KV."""
+        return (not self.mla and self.kv_policy == "resident" and not self.offload and self.n_cpu == 0
+                and self.ep is None)
+
     @torch.no_grad()
-    def generate(self, input_ids: torch.Tensor, max_new_tokens: int) -> torch.Tensor:
+    def prefill(self, input_ids: torch.Tensor, chunk_tokens: int = 32768) -> torch.Tensor:
+        """Batched prefill (the reference's prefill phase: every prompt token of a sequence in one
+        forward, tokens_per_seq_in_flight = P, memory_model.py:53-60; PAPER.md:547-569).  Sequences
+        are processed `chunk_tokens // P` at a time: embed -> per layer RMSNorm, QKV GEMM, RoPE +
+        paged KV write (mgb_rope_append_gqa_prefill), causal GQA attention (torch SDPA over the
+        contiguous K/V rows), O GEMM + residual/norm, router, grouped expert GEMMs, fused combine ->
+        LM head on each sequence's last position.  Leaves every sequence at position P with its
+        first generated token in next_ids (and out_tokens[:, P-1]); returns it (host int64 [B])."""
+        if not self.can_prefill():
+            raise NotImplementedError("batched prefill needs a GQA model with resident weights and KV")
+        a, b = self.arch, self.buf
+        B, P = input_ids.shape
+        assert B == self.B and 1 <= P <= self.max_ctx
+        Bp = max(1, min(B, chunk_tokens // P))
+        T = Bp * P
+        d, hd, Hq, Hkv, k = a.hidden, a.head_dim, a.n_heads, a.n_kv_heads, a.top_k
+        bf = dict(dtype=BF16, device=self.device)
+        if getattr(self, "_pf_T", 0) < T:  # scratch for one chunk of prompt tokens
+            self._pf = dict(x=torch.empty(T, d, **bf), h=torch.empty(T, d, **bf),
+                            qkv=torch.empty(T, (Hq + 2 * Hkv) * hd, **bf), q=torch.empty(T, Hq * hd, **bf),
+                            k=torch.empty(T, Hkv * hd, **bf), v=torch.empty(T, Hkv * hd, **bf),
+                            o=torch.empty(T, d, **bf), xp=torch.empty(T * k, d, **bf),
+                            hf=torch.empty(T * k, a.moe_ffn, **bf), yp=torch.empty(T * k, d, **bf),
+                            lg=torch.empty(T, a.n_experts, dtype=torch.float32, device=self.device),
+                            ws=ops.RouterWorkspace(T, a.n_experts, k, device=self.device))
+            self._pf_T = T
+        S = self._pf
+        ids = input_ids.to(self.device, torch.int32)
+        self.reset(0)
+        self.stream.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(self.stream):
+            for s0 in range(0, B, Bp):
+                n = min(Bp, B - s0)
+                t = n * P
+                x, h, qkv, q, kk, vv, o = (S[key][:t] for key in ("x", "h", "qkv", "q", "k", "v", "o"))
+                ops.embed(ids[s0:s0 + n].reshape(-1), self.w.embed, x)
+                ws = S["ws"]
+                for l in range(a.layers):
+                    W = self.w.layers[l]
+                    if l == 0:
+                        ops.add_rmsnorm(x, W["ln1"], a.rms_eps, h)
+                    torch.mm(h, W["wqkv"].t(), out=qkv)
+                    nat.call("mgb_rope_append_gqa_prefill", qkv.data_ptr(), t, s0, P, self.cos_t.data_ptr(),
+                             self.sin_t.data_ptr(), Hq, Hkv, hd, self.block_table.data_ptr(), self.pps,
+                             self.k_cache[l].data_ptr(), self.v_cache[l].data_ptr(), q.data_ptr(), kk.data_ptr(),
+                             vv.data_ptr(), torch.cuda.current_stream().cuda_stream)
+                    att = torch.nn.functional.scaled_dot_product_attention(
+                        q.view(n, P, Hq, hd).transpose(1, 2), kk.view(n, P, Hkv, hd).transpose(1, 2),
+                        vv.view(n, P, Hkv, hd).transpose(1, 2), is_causal=True, enable_gqa=True)
+                    torch.mm(att.transpose(1, 2).reshape(t, Hq * hd), W["wo"].t(), out=o)
+                    ops.add_rmsnorm(x, W["ln2"], a.rms_eps, h, delta=o, x_out=x)
+                    S["lg"][:t].copy_(torch.mm(h, W["router"].t(), out_dtype=torch.float32))
+                    ops.router_topk(None, None, ws, k, a.router_mode, a.routed_scaling, a.n_group, a.topk_group,
+                                    logits_in=S["lg"][:t])
+                    ops.permute(h, ws, S["xp"])
+                    ops.moe_gemm_gate_up(W["w_gate_up"], S["xp"], ws.offsets, S["hf"])
+                    ops.moe_gemm_down(W["w_down"], S["hf"], ws.offsets, S["yp"])
+                    nxt = self.w.layers[l + 1]["ln1"] if l + 1 < a.layers else self.w.final_norm
+                    ops.unpermute_combine(S["yp"], ws, x, t, residual=x, norm_w=nxt, eps=a.rms_eps, norm_out=h)
+                last = h.view(n, P, d)[:, P - 1].contiguous()
+                logits = torch.mm(last, self.w.lm_head.t())
+                b.logits[s0:s0 + n].copy_(logits)
+                ops.argmax(logits, b.next_ids[s0:s0 + n])
+            b.positions.fill_(P)
+            b.seq_lens.fill_(P)
+            b.step.fill_(P)
+            self.out_tokens[:, P - 1].copy_(b.next_ids)
+        torch.cuda.current_stream().wait_stream(self.stream)
+        self.host_pos = P
+        return b.next_ids.to("cpu", torch.int64)
+
+    @torch.no_grad()
+    def generate(self, input_ids: torch.Tensor, max_new_tokens: int, prefill: bool = True) -> torch.Tensor:
         """Greedy generation (HF generate semantics: no EOS stop, equal-length prompts).  The
         prompt is consumed through the same decode step, one position per step."""
         B, P = input_ids.shape
         assert B == self.B, f"engine was planned for B={self.B}"
         assert P + max_new_tokens <= self.max_ctx
-        self.reset(0)
-        prompt = input_ids.to(self.device, torch.int32)
-        for p in range(P):
-            self.buf.next_ids.copy_(prompt[:, p])
-            self.run_step()
+        if prefill and self.can_prefill():
+            self.prefill(input_ids)
+        else:  # the prompt through the decode step, one position per step
+            self.reset(0)
+            prompt = input_ids.to(self.device, torch.int32)
+            for p in range(P):
+                self.buf.next_ids.copy_(prompt[:, p])
+                self.run_step()
         # step P-1 predicted the first new token; it is already in next_ids
         for _ in range(max_new_tokens - 1):
             self.run_step()

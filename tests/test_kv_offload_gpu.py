@@ -63,7 +63,7 @@ def test_kv_offload_generate_equals_resident(family):
     B, P, N = 8, 5, 6
     plan = _plan(A, B, 3)  # micro-batches of 3, 3, 2 sequences
     ids = torch.randint(0, A.vocab, (B, P), generator=torch.Generator().manual_seed(21))
-    ref = Engine(A, plan, prompt_len=P, decode_len=N, use_graph=False).generate(ids, N)
+    ref = Engine(A, plan, prompt_len=P, decode_len=N, use_graph=False).generate(ids, N, prefill=False)
     for graph in (False, True):
         eng = Engine(A, plan, prompt_len=P, decode_len=N, use_graph=graph, kv_policy="offload", kv_ring_slots=2)
         assert not eng.kv[0][0].is_cuda and eng.kv_ring_n == 2
