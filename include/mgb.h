@@ -91,6 +91,10 @@ int mgb_kv_token_copy(const void* src, const int* src_table, int src_max_pages, 
                       int dst_max_pages, const int* positions, int B, int page_tokens, long long page_bytes,
                       int unit_bytes, int n_units, long long unit_stride, void* stream);
 
+/* SM-driven byte copy (16 B aligned; either side may be mapped pinned host memory): the CPU share's
+ * small per-layer q / length / output transfers, kept off the copy engines the KV slices occupy. */
+int mgb_copy_bytes(void* dst, const void* src, long long nbytes, void* stream);
+
 /* ---- ATTN_MECH_CPU (offload_dag.py:328-357; ModuleKind.ATTN_MECH_CPU hw_profile.py:55) -----
  * GQA decode attention on the host cores over the host KV page store (GPU page layout), for the
  * plan's CPU share of sequences (omega > 0).  AVX-512 BF16 when the host has it, scalar otherwise.

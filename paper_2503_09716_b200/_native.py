@@ -51,6 +51,7 @@ SIGNATURES: dict[str, list] = {
     "mgb_mla_append": [P, P, P, F, I, I, I, I, I, P, P, P, P, I, P, P, P, P, P],
     # kv_stream.cu
     "mgb_kv_token_copy": [P, P, I, P, P, I, P, I, I, L, I, I, L, P],
+    "mgb_copy_bytes": [P, P, L, P],
     # cpu_attn.cpp (host code: ATTN_MECH_CPU)
     "mgb_cpu_attn_gqa": [P],
     "mgb_cpu_attn_gqa_enqueue": [P, P],

@@ -40,9 +40,30 @@ __global__ void kv_token_copy_kernel(const uint8_t* __restrict__ src, const int*
   *reinterpret_cast<uint4*>(dst + dp * page_bytes + off) = x;
 }
 
+// Plain byte copy by SM loads/stores (16 B per thread-iteration; either side may be mapped pinned
+// host memory).  Used for the small per-layer transfers of the CPU attention share, which would
+// otherwise queue on a copy engine behind the multi-hundred-MB KV_COPY_IN slices.
+__global__ void copy_bytes_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src, long long n16) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += (long long)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
 }  // namespace mgb
 
 extern "C" {
+
+int mgb_copy_bytes(void* dst, const void* src, long long nbytes, void* stream) {
+  if (nbytes < 0 || nbytes % 16 || (reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) % 16)
+    return MGB_EINVAL;
+  if (nbytes == 0) return MGB_OK;
+  const long long n16 = nbytes / 16;
+  long long blocks = (n16 + 255) / 256;
+  if (blocks > 4 * 148) blocks = 4 * 148;
+  mgb::copy_bytes_kernel<<<(int)blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<uint4*>(dst), reinterpret_cast<const uint4*>(src), n16);
+  return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
+}
+
 
 // Copy the token at positions[b] of every sequence b in [0, B) from page src_table[b][pos / page_tokens]
 // of `src` to page dst_table[b][pos / page_tokens] of `dst` (same in-page slot).  `dst` / `src` may be

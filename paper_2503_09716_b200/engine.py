@@ -225,7 +225,7 @@ class Engine:
             q=torch.zeros(B, attn_cols, **bf), attn=torch.zeros(B, attn_cols, **bf), o=torch.zeros(B, d, **bf),
             x_perm=torch.zeros(rows, d, **bf), h_ffn=torch.zeros(rows, f, **bf), y_perm=torch.zeros(rows, d, **bf),
             logits=torch.zeros(B, a.vocab, **bf), next_ids=torch.zeros(B, **i32), positions=torch.zeros(B, **i32),
-            seq_lens=torch.zeros(B, **i32), step=torch.zeros(1, **i32))
+            seq_lens=torch.zeros(B + 4, **i32), step=torch.zeros(1, **i32))  # +4: 16-byte copies
         self.rws = ops.RouterWorkspace(B, a.n_experts, k, device=device)
         self.out_tokens = torch.zeros(B, max(1, self.max_ctx), dtype=torch.int64, device=device)
         self.graph: torch.cuda.CUDAGraph | None = None
@@ -457,7 +457,8 @@ class Engine:
         a, n = self.arch, self.n_cpu
         width = a.n_heads * a.head_dim
         self.cpu_q = torch.empty(n, width, dtype=BF16, pin_memory=True)
-        self.cpu_lens = torch.empty(n, dtype=torch.int32, pin_memory=True)
+        self.cpu_lens_bytes = (4 * n + 15) // 16 * 16  # copied in whole 16-byte units
+        self.cpu_lens = torch.empty(self.cpu_lens_bytes // 4, dtype=torch.int32, pin_memory=True)
         self.cpu_out = torch.empty(n, width, dtype=BF16, pin_memory=True)
         self.cpu_desc = [nat.CpuAttnGqa(self.kv[l][0].data_ptr(), self.kv[l][1].data_ptr(), self.cpu_q.data_ptr(),
                                         self.cpu_lens.data_ptr(), self.cpu_out.data_ptr(), 0, self.pps, n, a.n_heads,
@@ -471,10 +472,13 @@ class Engine:
         import ctypes
 
         b, n = self.buf, self.n_cpu
-        self.cpu_q.copy_(b.q[:n], non_blocking=True)
-        self.cpu_lens.copy_(b.seq_lens[:n], non_blocking=True)
-        nat.call("mgb_cpu_attn_gqa_enqueue", ctypes.byref(self.cpu_desc[l]), torch.cuda.current_stream().cuda_stream)
-        b.attn[:n].copy_(self.cpu_out, non_blocking=True)
+        st = torch.cuda.current_stream().cuda_stream
+        # SM-driven copies through mapped pinned memory: these few MB must not queue on a copy
+        # engine behind the GPU share's KV_COPY_IN slices
+        nat.call("mgb_copy_bytes", self.cpu_q.data_ptr(), b.q.data_ptr(), self.cpu_q.nbytes, st)
+        nat.call("mgb_copy_bytes", self.cpu_lens.data_ptr(), b.seq_lens.data_ptr(), self.cpu_lens_bytes, st)
+        nat.call("mgb_cpu_attn_gqa_enqueue", ctypes.byref(self.cpu_desc[l]), st)
+        nat.call("mgb_copy_bytes", b.attn.data_ptr(), self.cpu_out.data_ptr(), self.cpu_out.nbytes, st)
 
     def _moved_bytes(self, j) -> float:
         """Bytes a copy job really moves: the schedule's bytes, except the expert copies the

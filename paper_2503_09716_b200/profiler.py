@@ -75,11 +75,36 @@ def measured_hardware(host_bytes: int | None = None) -> Hardware:
                     cpu_attn_flops=0.0)
 
 
-def _profile_cpu_attention(arch: ModelArch, token_grid: Sequence[int], ctx_grid: Sequence[int]):
+def _profile_cpu_attention(arch: ModelArch, token_grid: Sequence[int], ctx_grid: Sequence[int],
+                           under_copy_load: bool = True):
     """ATTN_MECH_CPU on the host cores (csrc/cpu_attn.cpp) for T sequences over `ctx` keys; also the
-    achieved attention FLOP/s (the reference's cpu_attn_flops, hw_profile.py:52-149)."""
+    achieved attention FLOP/s (the reference's cpu_attn_flops, hw_profile.py:52-149).
+
+    With `under_copy_load` the timing runs while the copy engine streams pinned host memory to the
+    GPU back to back, as the KV_COPY_IN slices of the GPU share do during a step: the CPU share and
+    the host link read the same host DRAM, and a table measured on an idle host overestimates the
+    CPU share's speed (a 29 % optimistic plan estimate in profiles/r1_plan_mixtral8x7b_cpu.json)."""
     import ctypes
+    import threading
     import time
+
+    stop = threading.Event()
+    loader = None
+    if under_copy_load and torch.cuda.is_available():
+        src = torch.empty(1 << 30, dtype=torch.uint8).pin_memory()
+        dst = torch.empty(1 << 30, dtype=torch.uint8, device="cuda")
+        side = torch.cuda.Stream()
+
+        def load():
+            with torch.cuda.stream(side):
+                while not stop.is_set():
+                    for _ in range(4):
+                        dst.copy_(src, non_blocking=True)
+                    side.synchronize()
+
+        loader = threading.Thread(target=load, daemon=True)
+        loader.start()
+        time.sleep(0.2)
 
     a, P = arch, ops.kv_page_size()
     Tm, cm = max(token_grid), max(ctx_grid)
@@ -104,6 +129,9 @@ def _profile_cpu_attention(arch: ModelArch, token_grid: Sequence[int], ctx_grid:
             sec = statistics.median(ts)
             rows.append([T, ctx, sec])
             rate = max(rate, T * ctx * 4 * a.n_heads * a.head_dim / sec)
+    stop.set()
+    if loader is not None:
+        loader.join()
     return rows, rate
 
 
