@@ -34,6 +34,10 @@
 
 #include "common.cuh"
 
+#ifndef MGB_MLA_SACC
+#define MGB_MLA_SACC 4
+#endif
+
 namespace mgb {
 
 constexpr int kMlaPage = 56;     // tokens per latent page (7 swizzle atoms of 8 tokens)
@@ -59,7 +63,7 @@ struct MlaCfg {
   // Small MMAs accumulating into one TMEM tile serialise on their latency, so S^T is split over
   // kSAcc independent partial accumulators (k-step k -> partial k % kSAcc, summed by the softmax
   // warps) and the P.V MMAs interleave their MT independent M tiles.
-  static constexpr int kSAcc = KS % 2 == 0 ? 2 : 1;
+  static constexpr int kSAcc = KS % MGB_MLA_SACC == 0 ? MGB_MLA_SACC : (KS % 2 == 0 ? 2 : 1);
   static constexpr uint32_t kSCol = 0;                        // S^T: 2 buffers x kSAcc x 16 columns
   static constexpr uint32_t kOCol = 2 * kSAcc * 16;           // O^T: 2 buffers x MT x 16 columns
   static constexpr uint32_t kTmemCols = kOCol + 2 * MT * 16 <= 128 ? 128 : 256;

@@ -201,7 +201,7 @@ __global__ void silu_mul_kernel(const __nv_bfloat16* __restrict__ gu, int T, int
   const float uf[8] = {bf16lo(u.x), bf16hi(u.x), bf16lo(u.y), bf16hi(u.y), bf16lo(u.z), bf16hi(u.z), bf16lo(u.w), bf16hi(u.w)};
   float r[8];
 #pragma unroll
-  for (int j = 0; j < 8; ++j) r[j] = bf16_round(gf[j] / (1.0f + expf(-gf[j]))) * uf[j];
+  for (int j = 0; j < 8; ++j) r[j] = bf16_round(__fdividef(gf[j], 1.0f + __expf(-gf[j]))) * uf[j];
   uint4 o;
   o.x = pack_bf16x2(r[0], r[1]); o.y = pack_bf16x2(r[2], r[3]); o.z = pack_bf16x2(r[4], r[5]); o.w = pack_bf16x2(r[6], r[7]);
   reinterpret_cast<uint4*>(h + (size_t)t * F)[c] = o;

@@ -395,24 +395,25 @@ combine_kernel(const __nv_bfloat16* __restrict__ y_perm, const int* __restrict__
   for (int u = 0; u < kCombineVec; ++u)
 #pragma unroll
     for (int i = 0; i < 8; ++i) acc[u][i] = 0.f;
-  for (int j = 0; j < k; ++j) {
-    const uint4* yrow = reinterpret_cast<const uint4*>(y_perm + (size_t)s_pos[j] * d);
-    const float w = s_w[j];
-    uint4 v[kCombineVec];
+  // all k rows of a 16-byte column in flight at once (k independent loads per thread), then the fp32
+  // weighted sum in j order (j ascending, as the oracle)
 #pragma unroll
-    for (int u = 0; u < kCombineVec; ++u) {
-      const int c = threadIdx.x + u * kCombineThreads;
-      if (c < nvec) v[u] = ld_nc_v4(yrow + c);
-    }
+  for (int u = 0; u < kCombineVec; ++u) {
+    const int c = threadIdx.x + u * kCombineThreads;
+    if (c < nvec) {
+      uint4 v[kMaxK];
 #pragma unroll
-    for (int u = 0; u < kCombineVec; ++u) {
-      const int c = threadIdx.x + u * kCombineThreads;
-      if (c < nvec) {
-        acc[u][0] += w * bf16lo(v[u].x); acc[u][1] += w * bf16hi(v[u].x);
-        acc[u][2] += w * bf16lo(v[u].y); acc[u][3] += w * bf16hi(v[u].y);
-        acc[u][4] += w * bf16lo(v[u].z); acc[u][5] += w * bf16hi(v[u].z);
-        acc[u][6] += w * bf16lo(v[u].w); acc[u][7] += w * bf16hi(v[u].w);
-      }
+      for (int j = 0; j < kMaxK; ++j)
+        if (j < k) v[j] = ld_nc_v4(reinterpret_cast<const uint4*>(y_perm + (size_t)s_pos[j] * d) + c);
+#pragma unroll
+      for (int j = 0; j < kMaxK; ++j)
+        if (j < k) {
+          const float w = s_w[j];
+          acc[u][0] += w * bf16lo(v[j].x); acc[u][1] += w * bf16hi(v[j].x);
+          acc[u][2] += w * bf16lo(v[j].y); acc[u][3] += w * bf16hi(v[j].y);
+          acc[u][4] += w * bf16lo(v[j].z); acc[u][5] += w * bf16hi(v[j].z);
+          acc[u][6] += w * bf16lo(v[j].w); acc[u][7] += w * bf16hi(v[j].w);
+        }
     }
   }
   float ss = 0.f;
