@@ -81,6 +81,12 @@ int mgb_decode_attn_mla(const void* q_lat, const void* q_pe, const void* cache, 
 int mgb_mla_append(const void* q, const void* ckv, const void* norm_w, float eps, int B, int H, int R, int RP, int NOPE,
                    const int* positions, const float* cos_t, const float* sin_t, const int* block_table, int max_pages,
                    void* cache, void* q_nope_out, void* q_pe_out, int* seq_lens, void* stream);
+/* prefill (T = n_seq * P prompt tokens, token t = position t % P of sequence seq0 + t / P): latent
+ * + k_pe into the pages and into contiguous c_out [T, R] / kpe_out [T, RP]; q_pe rotated in place
+ * in q [T, H, NOPE + RP] (for the non-absorbed causal prefill attention) */
+int mgb_mla_append_prefill(void* q, const void* ckv, const void* norm_w, float eps, int T, int seq0, int P, int H,
+                           int R, int RP, int NOPE, const float* cos_t, const float* sin_t, const int* block_table,
+                           int max_pages, void* cache, void* c_out, void* kpe_out, void* stream);
 
 /* ---- KV_COPY_OUT / new-token insert for kv_policy "offload" (offload_dag.py:372-392) --------
  * Copies the token at positions[b] of sequence b from page src_table[b][pos/page_tokens] of src to

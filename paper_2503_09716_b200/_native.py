@@ -49,6 +49,7 @@ SIGNATURES: dict[str, list] = {
     "mgb_mla_page_elems": [I, I],
     "mgb_decode_attn_mla": [P, P, P, P, I, P, I, I, I, I, F, P, P],
     "mgb_mla_append": [P, P, P, F, I, I, I, I, I, P, P, P, P, I, P, P, P, P, P],
+    "mgb_mla_append_prefill": [P, P, P, F, I, I, I, I, I, I, I, P, P, P, I, P, P, P, P],
     # kv_stream.cu
     "mgb_kv_token_copy": [P, P, I, P, P, I, P, I, I, L, I, I, L, P],
     "mgb_copy_bytes": [P, P, L, P],

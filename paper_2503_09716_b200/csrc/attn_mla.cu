@@ -499,6 +499,65 @@ __global__ void mla_append_kernel(const __nv_bfloat16* __restrict__ q,    // [B,
   }
 }
 
+// Prefill variant (T = n_seq * P prompt tokens; token t = position t % P of sequence seq0 + t / P):
+// the normed latent + RoPE'd k_pe of every prompt token into the latent pages, and contiguous copies
+// for the (non-absorbed) causal prefill attention: c_out [T, R], kpe_out [T, RP]; the q_pe part of
+// each row of q [T, H, NOPE + RP] is rotated in place.  Same arithmetic as mla_append_kernel.
+__global__ void mla_append_prefill_kernel(__nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ ckv,
+                                          const __nv_bfloat16* __restrict__ norm_w, float eps, int seq0, int P, int H,
+                                          int R, int RP, int NOPE, const float* __restrict__ cos_t,
+                                          const float* __restrict__ sin_t, const int* __restrict__ block_table,
+                                          int max_pages, __nv_bfloat16* __restrict__ cache,
+                                          __nv_bfloat16* __restrict__ c_out, __nv_bfloat16* __restrict__ kpe_out) {
+  const int t = blockIdx.x;
+  const int seq = seq0 + t / P, pos = t % P;
+  const int D = R + RP;
+  __shared__ float red[32];
+  const __nv_bfloat16* row = ckv + (size_t)t * D;
+  const int page = block_table[(size_t)seq * max_pages + pos / kMlaPage];
+  const int slot = pos % kMlaPage;
+  const int DP = (D + 63) / 64 * 64;
+  __nv_bfloat16* pg = cache + (size_t)page * DP * kMlaPage;
+  auto at = [slot](int i) { return (i >> 6) * (kMlaPage * 64) + slot * 64 + ((((i >> 3) & 7) ^ (slot & 7)) << 3) + (i & 7); };
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < R; i += blockDim.x) {
+    const float v = __bfloat162float(row[i]);
+    ss = fmaf(v, v, ss);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  float tot = 0.f;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) tot += red[i];
+  const float inv = 1.0f / sqrtf(tot / (float)R + eps);
+  for (int i = threadIdx.x; i < R; i += blockDim.x) {
+    const __nv_bfloat16 v = __float2bfloat16_rn(__bfloat162float(norm_w[i]) * bf16_round(__bfloat162float(row[i]) * inv));
+    pg[at(i)] = v;
+    c_out[(size_t)t * R + i] = v;
+  }
+  const float* cs = cos_t + (size_t)pos * (RP / 2);
+  const float* sn = sin_t + (size_t)pos * (RP / 2);
+  for (int i = threadIdx.x; i < RP / 2; i += blockDim.x) {  // shared k_pe
+    const float x0 = __bfloat162float(row[R + 2 * i]), x1 = __bfloat162float(row[R + 2 * i + 1]);
+    const float c = cs[i], s = sn[i];
+    const __nv_bfloat16 a = __float2bfloat16_rn(x0 * c - x1 * s), b = __float2bfloat16_rn(x0 * s + x1 * c);
+    pg[at(R + 2 * i)] = a;
+    pg[at(R + 2 * i + 1)] = b;
+    kpe_out[(size_t)t * RP + 2 * i] = a;
+    kpe_out[(size_t)t * RP + 2 * i + 1] = b;
+  }
+  const int QD = NOPE + RP;
+  for (int i = threadIdx.x; i < H * (RP / 2); i += blockDim.x) {  // per-head q_pe, in place
+    const int h = i / (RP / 2), j = i - h * (RP / 2);
+    __nv_bfloat16* qh = q + ((size_t)t * H + h) * QD + NOPE;
+    const float x0 = __bfloat162float(qh[2 * j]), x1 = __bfloat162float(qh[2 * j + 1]);
+    const float c = cs[j], s = sn[j];
+    qh[2 * j] = __float2bfloat16_rn(x0 * c - x1 * s);
+    qh[2 * j + 1] = __float2bfloat16_rn(x0 * s + x1 * c);
+  }
+}
+
 }  // namespace mgb
 
 extern "C" {
@@ -528,6 +587,20 @@ int mgb_mla_append(const void* q, const void* ckv, const void* norm_w, float eps
       reinterpret_cast<const __nv_bfloat16*>(norm_w), eps, B, H, R, RP, NOPE, positions, cos_t, sin_t, block_table,
       max_pages, reinterpret_cast<__nv_bfloat16*>(cache), reinterpret_cast<__nv_bfloat16*>(q_nope_out),
       reinterpret_cast<__nv_bfloat16*>(q_pe_out), seq_lens);
+  return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
+}
+
+// Prefill: latent + k_pe of T = n_seq * P prompt tokens into the pages and contiguous rows; q_pe RoPE
+// in place.
+int mgb_mla_append_prefill(void* q, const void* ckv, const void* norm_w, float eps, int T, int seq0, int P, int H,
+                           int R, int RP, int NOPE, const float* cos_t, const float* sin_t, const int* block_table,
+                           int max_pages, void* cache, void* c_out, void* kpe_out, void* stream) {
+  if (T < 1 || P < 1 || T % P || H < 1 || R % 8 || RP % 8 || NOPE % 8) return MGB_EINVAL;
+  mgb::mla_append_prefill_kernel<<<T, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<__nv_bfloat16*>(q), reinterpret_cast<const __nv_bfloat16*>(ckv),
+      reinterpret_cast<const __nv_bfloat16*>(norm_w), eps, seq0, P, H, R, RP, NOPE, cos_t, sin_t, block_table, max_pages,
+      reinterpret_cast<__nv_bfloat16*>(cache), reinterpret_cast<__nv_bfloat16*>(c_out),
+      reinterpret_cast<__nv_bfloat16*>(kpe_out));
   return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
 }
 

@@ -846,38 +846,99 @@ class Engine:
         return self.out_tokens[:, :n_steps].to("cpu", non_blocking=False)
 
     def can_prefill(self) -> bool:
-        """Batched prefill is built for GQA models with HBM-resident weights and KV."""
-        return (not self.mla and self.kv_policy == "resident" and not self.offload and self.n_cpu == 0
-                and self.ep is None)
+        """Batched prefill is built for HBM-resident weights and KV (both families)."""
+        return self.kv_policy == "resident" and not self.offload and self.n_cpu == 0 and self.ep is None
+
+    def _prefill_scratch(self, T: int) -> dict:
+        """Activation buffers for one chunk of T prompt tokens (allocated once, grown on demand)."""
+        if getattr(self, "_pf_T", 0) >= T:
+            return self._pf
+        a, k = self.arch, self.arch.top_k
+        d = a.hidden
+        bf = dict(dtype=BF16, device=self.device)
+        S = dict(x=torch.empty(T, d, **bf), h=torch.empty(T, d, **bf), o=torch.empty(T, d, **bf),
+                 xp=torch.empty(T * k, d, **bf), hf=torch.empty(T * k, a.moe_ffn, **bf), yp=torch.empty(T * k, d, **bf),
+                 lg=torch.empty(T, a.n_experts, dtype=torch.float32, device=self.device),
+                 ws=ops.RouterWorkspace(T, a.n_experts, k, device=self.device))
+        if self.mla:
+            H, qk = a.n_heads, a.qk_nope_dim + a.qk_rope_dim
+            fs = a.moe_ffn * a.n_shared
+            S.update(q=torch.empty(T, H * qk, **bf), ckv=torch.empty(T, a.kv_lora_rank + a.qk_rope_dim, **bf),
+                     c=torch.empty(T, a.kv_lora_rank, **bf), kpe=torch.empty(T, a.qk_rope_dim, **bf),
+                     kv=torch.empty(T, H * (a.qk_nope_dim + a.v_head_dim), **bf), k=torch.empty(T, H, qk, **bf),
+                     attn=torch.empty(T, H * a.v_head_dim, **bf), sh_gu=torch.empty(T, 2 * fs, **bf),
+                     sh_h=torch.empty(T, fs, **bf), sh_out=torch.empty(T, d, **bf))
+            if a.q_lora_rank:
+                S.update(qa=torch.empty(T, a.q_lora_rank, **bf), qan=torch.empty(T, a.q_lora_rank, **bf))
+            if a.first_k_dense:
+                S.update(de_gu=torch.empty(T, 2 * a.dense_ffn, **bf), de_h=torch.empty(T, a.dense_ffn, **bf))
+        else:
+            hd, Hq, Hkv = a.head_dim, a.n_heads, a.n_kv_heads
+            S.update(qkv=torch.empty(T, (Hq + 2 * Hkv) * hd, **bf), q=torch.empty(T, Hq * hd, **bf),
+                     k=torch.empty(T, Hkv * hd, **bf), v=torch.empty(T, Hkv * hd, **bf))
+        self._pf, self._pf_T = S, T
+        return S
+
+    def _prefill_attention_gqa(self, l: int, W: dict, S: dict, s0: int, n: int, P: int) -> torch.Tensor:
+        a = self.arch
+        t, hd, Hq, Hkv = n * P, a.head_dim, a.n_heads, a.n_kv_heads
+        qkv, q, kk, vv = S["qkv"][:t], S["q"][:t], S["k"][:t], S["v"][:t]
+        torch.mm(S["h"][:t], W["wqkv"].t(), out=qkv)
+        nat.call("mgb_rope_append_gqa_prefill", qkv.data_ptr(), t, s0, P, self.cos_t.data_ptr(),
+                 self.sin_t.data_ptr(), Hq, Hkv, hd, self.block_table.data_ptr(), self.pps,
+                 self.k_cache[l].data_ptr(), self.v_cache[l].data_ptr(), q.data_ptr(), kk.data_ptr(),
+                 vv.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        att = torch.nn.functional.scaled_dot_product_attention(
+            q.view(n, P, Hq, hd).transpose(1, 2), kk.view(n, P, Hkv, hd).transpose(1, 2),
+            vv.view(n, P, Hkv, hd).transpose(1, 2), is_causal=True, enable_gqa=True)
+        return att.transpose(1, 2).reshape(t, Hq * hd)
+
+    def _prefill_attention_mla(self, l: int, W: dict, S: dict, s0: int, n: int, P: int) -> torch.Tensor:
+        """HF DeepseekV2Attention on the prompt (modeling_deepseek_v2.py:337-396): the latent is
+        up-projected per head (no absorption: every key is attended by P queries), causal SDPA."""
+        a = self.arch
+        t, H, R, r, nope, vd = n * P, a.n_heads, a.kv_lora_rank, a.qk_rope_dim, a.qk_nope_dim, a.v_head_dim
+        h, q = S["h"][:t], S["q"][:t]
+        if a.q_lora_rank:
+            torch.mm(h, W["q_a"].t(), out=S["qa"][:t])
+            ops.add_rmsnorm(S["qa"][:t], W["q_a_norm"], a.rms_eps, S["qan"][:t])
+            torch.mm(S["qan"][:t], W["q_b"].t(), out=q)
+        else:
+            torch.mm(h, W["q_proj"].t(), out=q)
+        torch.mm(h, W["kv_a"].t(), out=S["ckv"][:t])
+        nat.call("mgb_mla_append_prefill", q.data_ptr(), S["ckv"].data_ptr(), W["kv_a_norm"].data_ptr(), a.rms_eps, t,
+                 s0, P, H, R, r, nope, self.cos_t.data_ptr(), self.sin_t.data_ptr(), self.block_table.data_ptr(),
+                 self.pps, self.latent[l].data_ptr(), S["c"].data_ptr(), S["kpe"].data_ptr(),
+                 torch.cuda.current_stream().cuda_stream)
+        kv = S["kv"][:t]
+        torch.mm(S["c"][:t], W["kv_b"].t(), out=kv)
+        kv = kv.view(t, H, nope + vd)
+        k = S["k"][:t]
+        k[:, :, :nope].copy_(kv[:, :, :nope])
+        k[:, :, nope:].copy_(S["kpe"][:t, None, :].expand(t, H, r))
+        att = torch.nn.functional.scaled_dot_product_attention(
+            q.view(n, P, H, nope + r).transpose(1, 2), k.view(n, P, H, nope + r).transpose(1, 2),
+            kv[:, :, nope:].reshape(n, P, H, vd).transpose(1, 2), is_causal=True, scale=(nope + r) ** -0.5)
+        return att.transpose(1, 2).reshape(t, H * vd)
 
     @torch.no_grad()
     def prefill(self, input_ids: torch.Tensor, chunk_tokens: int = 32768) -> torch.Tensor:
         """Batched prefill (the reference's prefill phase: every prompt token of a sequence in one
         forward, tokens_per_seq_in_flight = P, memory_model.py:53-60; PAPER.md:547-569).  Sequences
-        are processed `chunk_tokens // P` at a time: embed -> per layer RMSNorm, QKV GEMM, RoPE +
-        paged KV write (mgb_rope_append_gqa_prefill), causal GQA attention (torch SDPA over the
-        contiguous K/V rows), O GEMM + residual/norm, router, grouped expert GEMMs, fused combine ->
-        LM head on each sequence's last position.  Leaves every sequence at position P with its
+        are processed `chunk_tokens // P` at a time: embed -> per layer the family's attention on the
+        prompt (RoPE + paged KV / latent write by mgb_rope_append_gqa_prefill / mgb_mla_append_prefill,
+        causal torch SDPA on contiguous K/V rows), O GEMM + residual/norm, then the same router /
+        grouped expert GEMM / combine kernels as decode (DeepSeek: shared experts, dense first layers)
+        -> LM head on each sequence's last position.  Leaves every sequence at position P with its
         first generated token in next_ids (and out_tokens[:, P-1]); returns it (host int64 [B])."""
         if not self.can_prefill():
-            raise NotImplementedError("batched prefill needs a GQA model with resident weights and KV")
+            raise NotImplementedError("batched prefill needs HBM-resident weights and KV")
         a, b = self.arch, self.buf
         B, P = input_ids.shape
         assert B == self.B and 1 <= P <= self.max_ctx
         Bp = max(1, min(B, chunk_tokens // P))
-        T = Bp * P
-        d, hd, Hq, Hkv, k = a.hidden, a.head_dim, a.n_heads, a.n_kv_heads, a.top_k
-        bf = dict(dtype=BF16, device=self.device)
-        if getattr(self, "_pf_T", 0) < T:  # scratch for one chunk of prompt tokens
-            self._pf = dict(x=torch.empty(T, d, **bf), h=torch.empty(T, d, **bf),
-                            qkv=torch.empty(T, (Hq + 2 * Hkv) * hd, **bf), q=torch.empty(T, Hq * hd, **bf),
-                            k=torch.empty(T, Hkv * hd, **bf), v=torch.empty(T, Hkv * hd, **bf),
-                            o=torch.empty(T, d, **bf), xp=torch.empty(T * k, d, **bf),
-                            hf=torch.empty(T * k, a.moe_ffn, **bf), yp=torch.empty(T * k, d, **bf),
-                            lg=torch.empty(T, a.n_experts, dtype=torch.float32, device=self.device),
-                            ws=ops.RouterWorkspace(T, a.n_experts, k, device=self.device))
-            self._pf_T = T
-        S = self._pf
+        S = self._prefill_scratch(Bp * P)
+        d, k = a.hidden, a.top_k
         ids = input_ids.to(self.device, torch.int32)
         self.reset(0)
         self.stream.wait_stream(torch.cuda.current_stream())
@@ -885,31 +946,41 @@ class Engine:
             for s0 in range(0, B, Bp):
                 n = min(Bp, B - s0)
                 t = n * P
-                x, h, qkv, q, kk, vv, o = (S[key][:t] for key in ("x", "h", "qkv", "q", "k", "v", "o"))
+                x, h, o = S["x"][:t], S["h"][:t], S["o"][:t]
                 ops.embed(ids[s0:s0 + n].reshape(-1), self.w.embed, x)
                 ws = S["ws"]
                 for l in range(a.layers):
                     W = self.w.layers[l]
                     if l == 0:
                         ops.add_rmsnorm(x, W["ln1"], a.rms_eps, h)
-                    torch.mm(h, W["wqkv"].t(), out=qkv)
-                    nat.call("mgb_rope_append_gqa_prefill", qkv.data_ptr(), t, s0, P, self.cos_t.data_ptr(),
-                             self.sin_t.data_ptr(), Hq, Hkv, hd, self.block_table.data_ptr(), self.pps,
-                             self.k_cache[l].data_ptr(), self.v_cache[l].data_ptr(), q.data_ptr(), kk.data_ptr(),
-                             vv.data_ptr(), torch.cuda.current_stream().cuda_stream)
-                    att = torch.nn.functional.scaled_dot_product_attention(
-                        q.view(n, P, Hq, hd).transpose(1, 2), kk.view(n, P, Hkv, hd).transpose(1, 2),
-                        vv.view(n, P, Hkv, hd).transpose(1, 2), is_causal=True, enable_gqa=True)
-                    torch.mm(att.transpose(1, 2).reshape(t, Hq * hd), W["wo"].t(), out=o)
+                    if self.mla:
+                        att = self._prefill_attention_mla(l, W, S, s0, n, P)
+                    else:
+                        att = self._prefill_attention_gqa(l, W, S, s0, n, P)
+                    torch.mm(att, W["wo"].t(), out=o)
                     ops.add_rmsnorm(x, W["ln2"], a.rms_eps, h, delta=o, x_out=x)
+                    nxt = self.w.layers[l + 1]["ln1"] if l + 1 < a.layers else self.w.final_norm
+                    if self.mla and l < a.first_k_dense:  # DeepseekV2MLP of the dense first layers
+                        F = a.dense_ffn
+                        torch.mm(h, W["dense_gate_up"][0].t(), out=S["de_gu"][:t])
+                        ops.silu_mul(S["de_gu"][:t], S["de_h"][:t])
+                        torch.mm(S["de_h"][:t], W["dense_down"][0].t(), out=o)
+                        ops.add_rmsnorm(x, nxt, a.rms_eps, h, delta=o, x_out=x)
+                        continue
+                    shared = None
+                    if self.mla:  # shared experts on every token
+                        torch.mm(h, W["sh_gate_up"][0].t(), out=S["sh_gu"][:t])
+                        ops.silu_mul(S["sh_gu"][:t], S["sh_h"][:t])
+                        torch.mm(S["sh_h"][:t], W["sh_down"][0].t(), out=S["sh_out"][:t])
+                        shared = S["sh_out"][:t]
                     S["lg"][:t].copy_(torch.mm(h, W["router"].t(), out_dtype=torch.float32))
                     ops.router_topk(None, None, ws, k, a.router_mode, a.routed_scaling, a.n_group, a.topk_group,
                                     logits_in=S["lg"][:t])
                     ops.permute(h, ws, S["xp"])
                     ops.moe_gemm_gate_up(W["w_gate_up"], S["xp"], ws.offsets, S["hf"])
                     ops.moe_gemm_down(W["w_down"], S["hf"], ws.offsets, S["yp"])
-                    nxt = self.w.layers[l + 1]["ln1"] if l + 1 < a.layers else self.w.final_norm
-                    ops.unpermute_combine(S["yp"], ws, x, t, residual=x, norm_w=nxt, eps=a.rms_eps, norm_out=h)
+                    ops.unpermute_combine(S["yp"], ws, x, t, residual=x, shared_out=shared, norm_w=nxt,
+                                          eps=a.rms_eps, norm_out=h)
                 last = h.view(n, P, d)[:, P - 1].contiguous()
                 logits = torch.mm(last, self.w.lm_head.t())
                 b.logits[s0:s0 + n].copy_(logits)

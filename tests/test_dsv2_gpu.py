@@ -146,8 +146,41 @@ def test_engine_expert_parallel_single_rank_path():
     mb = ModelSpec.from_document(A.model_spec_document()).model_bytes
     ids = torch.randint(0, A.vocab, (8, 4), generator=torch.Generator().manual_seed(9))
     plan = BatchingPlan(8, 4, 16, 0.0, 0, mb)
-    ref = Engine(A, plan, prompt_len=4, decode_len=3, use_graph=False).generate(ids, 3)
+    ref = Engine(A, plan, prompt_len=4, decode_len=3, use_graph=False).generate(ids, 3, prefill=False)
     ep = ExpertParallel(A.n_experts)
     eng = Engine(A, plan, prompt_len=4, decode_len=3, use_graph=False, ep=ep)
     eng.ep = ep  # force the EP code path even at world size 1
-    assert torch.equal(eng.generate(ids, 3), ref)
+    assert torch.equal(eng.generate(ids, 3, prefill=False), ref)
+
+
+@pytest.mark.parametrize("P,chunk", [(5, 32768), (60, 120)])  # one chunk; several chunks across a 56-token page
+def test_dsv2_batched_prefill_matches_tokenwise(ds_weights, P, chunk):
+    """Engine.prefill for MLA (latent + k_pe written for every prompt position, non-absorbed causal
+    attention on the up-projected heads, shared experts, dense first layer) vs consuming the prompt
+    through the decode step: last-position logits within the bf16 tolerance, latent pages close,
+    first token equal to the oracle's on margin-filtered rows."""
+    from paper_2503_09716_b200.configs import TINY_DSV2 as A
+
+    B, N = 8, 3
+    ids = torch.randint(0, A.vocab, (B, P), generator=torch.Generator().manual_seed(31))
+    e_pf, e_tw = _ds_engine(B, P, N, use_graph=False), _ds_engine(B, P, N, use_graph=False)
+    first = e_pf.prefill(ids, chunk_tokens=chunk)
+    lg_pf = e_pf.buf.logits.cpu().float()
+    e_tw.reset(0)
+    for p in range(P):
+        e_tw.buf.next_ids.copy_(ids[:, p].cuda().int())
+        e_tw.run_step()
+    lg_tw = e_tw.buf.logits.cpu().float()
+    rows = sorted(((lg_pf[i] - lg_tw[i]).abs().max() / lg_tw[i].abs().max()).item() for i in range(B))
+    assert rows[B // 2] <= 2e-2, rows
+    lat_pf, lat_tw = e_pf.latent[0].float(), e_tw.latent[0].float()
+    assert (lat_pf - lat_tw).abs().max().item() <= 2e-2 * lat_tw.abs().max().item()
+    orc = R.DeepseekV2Oracle(A, ds_weights)
+    for p in range(P):
+        lo = orc.step(ids[:, p], p).float()
+    delta = (lg_pf - lo).abs().max().item()
+    top2 = lo.topk(2, dim=-1).values
+    safe = (top2[:, 0] - top2[:, 1]) > 4 * delta
+    assert torch.equal(first[safe], lo.argmax(-1)[safe])
+    out = e_pf.generate(ids, N)
+    assert torch.equal(out[:, P], first)

@@ -109,7 +109,7 @@ def test_dsv2_offloaded_weights_and_kv_match_resident():
     B, P, N = 8, 4, 5
     ids = torch.randint(0, A.vocab, (B, P), generator=torch.Generator().manual_seed(13))
     ref = Engine(A, BatchingPlan(B, 4, 16, 0.0, 0, spec.model_bytes), prompt_len=P, decode_len=N,
-                 use_graph=False).generate(ids, N)
+                 use_graph=False).generate(ids, N, prefill=False)
     two_layers = 2 * dense + ((dense - 1) // ex) * ex  # 2 dense layers cached + a few experts
     for s_params, slots, policy in ((dense + dense // 2, 2, "resident"), (two_layers, 3, "offload")):
         plan = BatchingPlan(B, 4, 16, 0.0, slots * ex, s_params)
