@@ -40,9 +40,16 @@
 
 namespace mgb {
 
-constexpr int kMlaPage = 56;     // tokens per latent page (7 swizzle atoms of 8 tokens)
+#ifndef MGB_MLA_PAGE
+#define MGB_MLA_PAGE 56
+#endif
+#ifndef MGB_MLA_STAGES
+#define MGB_MLA_STAGES 3
+#endif
+constexpr int kMlaPage = MGB_MLA_PAGE;     // tokens per latent page (swizzle atoms of 8 tokens)
 constexpr int kMlaTile = 64;     // M of the S^T MMA / K of P.V: a page plus 8 phantom rows
-constexpr int kMlaStages = 3;    // pages in flight per SM (3 x 63 KB for R = 512)
+constexpr int kMlaStages = MGB_MLA_STAGES;  // pages in flight per SM (3 x 63 KB for R = 512)
+static_assert(kMlaPage % 8 == 0 && kMlaPage <= 64, "latent page = whole swizzle atoms within one MMA tile");
 constexpr int kMlaHeads = 16;    // heads per work item = N of both MMAs
 constexpr int kMlaThreads = 192;
 
@@ -72,7 +79,8 @@ struct MlaCfg {
   static constexpr int kOffP = kOffQ + kQBytes;
   static constexpr int kOffRed = kOffP + 2 * kPBytes;      // float [2][4][16] max + [4][16] sum
   static constexpr int kOffBar = kOffRed + 3 * 4 * 16 * 4;
-  static constexpr size_t kSmem = kOffBar + 18 * 8 + 16;
+  static constexpr int kBars = 2 * kMlaStages + 12;
+  static constexpr size_t kSmem = kOffBar + kBars * 8 + 16;
   static_assert(R % 128 == 0 && RP % 16 == 0 && kBlockBytes % 1024 == 0, "MLA shape");
   static_assert(kSmem <= 227 * 1024, "MLA smem");
 };
@@ -111,9 +119,11 @@ decode_attn_mla_kernel(const __grid_constant__ CUtensorMap tm_qlat,  // q_lat [H
   float* red = reinterpret_cast<float*>(smem + C::kOffRed);  // [2][4][16]
   float* lred = red + 2 * 4 * 16;                              // [4][16]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
-  uint64_t *full = bars, *empty = bars + 3, *qfull = bars + 6, *qempty = bars + 7, *sfull = bars + 8,
-           *sempty = bars + 10, *pfull = bars + 12, *ofull = bars + 14, *oempty = bars + 16;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
+  constexpr int S = kMlaStages;
+  uint64_t *full = bars, *empty = bars + S, *qfull = bars + 2 * S, *qempty = bars + 2 * S + 1,
+           *sfull = bars + 2 * S + 2, *sempty = bars + 2 * S + 4, *pfull = bars + 2 * S + 6, *ofull = bars + 2 * S + 8,
+           *oempty = bars + 2 * S + 10;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 12);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_hg = (H + kMlaHeads - 1) / kMlaHeads;
