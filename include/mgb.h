@@ -52,6 +52,20 @@ int mgb_moe_gemm_gate_up(const void* w_gate_up, const void* x_perm, const int* o
                          int rows_cap, void* h_out, void* stream);
 int mgb_moe_gemm_down(const void* w_down, const void* h, const int* offsets, int E, int d, int f, int rows_cap,
                       void* y_out, void* stream);
+/* expert parallelism fused with the data path (peer memory over NVLink, UVA pointers):
+ *  - mgb_ep_permute_dispatch: the permutation writes row (t, j) of expert e straight into the owner
+ *    rank's receive buffer peer_base[e / E_local] at row disp_row[e] + (position within e's segment);
+ *  - mgb_ep_row_ptrs: per receive-buffer row, the home address in the source rank's y_perm
+ *    ((local expert, source) segments: start, length, row delta; peer_base = sources' y_perm);
+ *  - mgb_moe_gemm_down_ep: the down GEMM whose epilogue stores each row at row_ptr[row] (the combine
+ *    send fused into the GEMM). */
+int mgb_ep_permute_dispatch(const void* x, const int* topk_idx, const int* local_rank, const int* block_base,
+                            const int* offsets, int T, int d, int k, int E, int E_local, const long long* peer_base,
+                            const int* disp_row, int* src_token, int* dst_pos, void* stream);
+int mgb_ep_row_ptrs(const int* seg_start, const int* seg_len, const int* seg_delta, int n_seg, int W,
+                    const long long* peer_base, int row_bytes, int rows_cap, long long* row_ptr, void* stream);
+int mgb_moe_gemm_down_ep(const void* w_down, const void* h, const int* offsets, int E, int d, int f, int rows_cap,
+                         const long long* row_ptr, void* stream);
 int mgb_grouped_ffn(const void* w_gate_up, const void* w_down, const void* x_perm, const int* offsets, int E, int d,
                     int f, int rows_cap, void* h_scratch, void* y_out, void* stream);
 

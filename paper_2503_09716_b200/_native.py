@@ -33,6 +33,9 @@ SIGNATURES: dict[str, list] = {
     "mgb_moe_gemm_gate_up": [P, P, P, I, I, I, I, P, P],
     "mgb_moe_gemm_down": [P, P, P, I, I, I, I, P, P],
     "mgb_grouped_ffn": [P, P, P, P, I, I, I, I, P, P, P],
+    "mgb_moe_gemm_down_ep": [P, P, P, I, I, I, I, P, P],
+    "mgb_ep_permute_dispatch": [P, P, P, P, P, I, I, I, I, I, P, P, P, P, P],
+    "mgb_ep_row_ptrs": [P, P, P, I, I, P, I, I, P, P],
     # attention (attn_gqa.cu)
     "mgb_decode_attn_gqa": [P, P, P, P, I, P, I, I, I, I, F, P, P],
     # elementwise.cu

@@ -122,11 +122,12 @@ MGB_DEVINL void gated_chunk(uint32_t tl, int c0, int n, bool is_up, int f, float
   epi_bar(group);
 }
 
-template <bool GATED>
+template <bool GATED, bool ROWPTR = false>
 __global__ void __launch_bounds__(Epi<GATED>::kThreads, 1)
 moe_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const int* __restrict__ offsets, int E, int MT, int K, int rows_per_expert, int half_rows,
-                __nv_bfloat16* __restrict__ out, int ldo, bool balanced) {
+                __nv_bfloat16* __restrict__ out, int ldo, bool balanced,
+                const long long* __restrict__ row_ptr) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* tiles = smem;
@@ -256,14 +257,23 @@ moe_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         __nv_bfloat16* ocol = out + (size_t)tok0 * ldo + mt * kRowsPerUnit + f;
         for (int c0 = 32 * group; c0 < n; c0 += 32 * Epi<GATED>::kGroups) gated_chunk(tl, c0, n, is_up, f, gx, ocol, ldo, group);
       } else {
-        __nv_bfloat16* ocol = out + (size_t)tok0 * ldo + mt * kRowsPerUnit + row;
+        const int col = mt * kRowsPerUnit + row;
+        __nv_bfloat16* ocol = out + (size_t)tok0 * ldo + col;
         for (int c0 = 32 * group; c0 < n; c0 += 32 * Epi<GATED>::kGroups) {
           uint32_t v[32];
           tmem_ld32(tl + c0, v);
           tmem_ld_wait();
+          if (ROWPTR) {  // expert-parallel combine fused into the epilogue: the row goes home (peer memory)
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (c0 + j < n) ocol[(size_t)(c0 + j) * ldo] = __float2bfloat16_rn(__uint_as_float(v[j]));
+            for (int j = 0; j < 32; ++j) {
+              const long long p = c0 + j < n ? row_ptr[tok0 + c0 + j] : 0;
+              if (p) reinterpret_cast<__nv_bfloat16*>(p)[col] = __float2bfloat16_rn(__uint_as_float(v[j]));
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (c0 + j < n) ocol[(size_t)(c0 + j) * ldo] = __float2bfloat16_rn(__uint_as_float(v[j]));
+          }
         }
       }
       tc_fence_before();
@@ -292,11 +302,12 @@ template <bool GATED> constexpr int pair_smem() {
   return kPStages * kPStageBytes + Epi<GATED>::kXBytes + 1024 + 256;
 }
 
-template <bool GATED>
+template <bool GATED, bool ROWPTR = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Epi<GATED>::kThreads, 1)
 moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const int* __restrict__ offsets, int E, int MT, int K, int rows_per_expert, int half_rows,
-                     __nv_bfloat16* __restrict__ out, int ldo, bool balanced) {
+                     __nv_bfloat16* __restrict__ out, int ldo, bool balanced,
+                const long long* __restrict__ row_ptr) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* tiles = smem;
@@ -436,14 +447,23 @@ moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
         __nv_bfloat16* ocol = out + (size_t)tok0 * ldo + col0 + f;
         for (int c0 = 32 * group; c0 < n; c0 += 32 * Epi<GATED>::kGroups) gated_chunk(tl, c0, n, is_up, f, gx, ocol, ldo, group);
       } else {
-        __nv_bfloat16* ocol = out + (size_t)tok0 * ldo + col0 + row;
+        const int col = col0 + row;
+        __nv_bfloat16* ocol = out + (size_t)tok0 * ldo + col;
         for (int c0 = 32 * group; c0 < n; c0 += 32 * Epi<GATED>::kGroups) {
           uint32_t v[32];
           tmem_ld32(tl + c0, v);
           tmem_ld_wait();
+          if (ROWPTR) {  // expert-parallel combine fused into the epilogue: the row goes home (peer memory)
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (c0 + j < n) ocol[(size_t)(c0 + j) * ldo] = __float2bfloat16_rn(__uint_as_float(v[j]));
+            for (int j = 0; j < 32; ++j) {
+              const long long p = c0 + j < n ? row_ptr[tok0 + c0 + j] : 0;
+              if (p) reinterpret_cast<__nv_bfloat16*>(p)[col] = __float2bfloat16_rn(__uint_as_float(v[j]));
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (c0 + j < n) ocol[(size_t)(c0 + j) * ldo] = __float2bfloat16_rn(__uint_as_float(v[j]));
+          }
         }
       }
       tc_fence_before();
@@ -472,11 +492,43 @@ bool use_pair_kernel() {
   return v;
 }
 
+template <bool GATED, bool PAIR, bool ROWPTR>
+int launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, const int* offsets, int E, int MT, int K,
+                   int rows_per_expert, int half_rows, void* out, int ldo, bool balanced, const long long* row_ptr,
+                   cudaStream_t stream) {
+  static bool attr = false;
+  if (PAIR) {
+    if (!attr) {
+      if (cudaFuncSetAttribute(mgb::moe_gemm_pair_kernel<GATED, ROWPTR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               mgb::pair_smem<GATED>()) != cudaSuccess)
+        return MGB_ECUDA;
+      attr = true;
+    }
+    const int grid = mgb_host::num_sms() & ~1;
+    mgb::moe_gemm_pair_kernel<GATED, ROWPTR><<<grid, mgb::Epi<GATED>::kThreads, mgb::pair_smem<GATED>(), stream>>>(
+        tmA, tmB, offsets, E, MT / 2, K, rows_per_expert, half_rows, reinterpret_cast<__nv_bfloat16*>(out), ldo,
+        balanced, row_ptr);
+  } else {
+    if (!attr) {
+      if (cudaFuncSetAttribute(mgb::moe_gemm_kernel<GATED, ROWPTR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               mgb::gemm_smem<GATED>()) != cudaSuccess)
+        return MGB_ECUDA;
+      attr = true;
+    }
+    mgb::moe_gemm_kernel<GATED, ROWPTR><<<mgb_host::num_sms(), mgb::Epi<GATED>::kThreads, mgb::gemm_smem<GATED>(),
+                                          stream>>>(
+        tmA, tmB, offsets, E, MT, K, rows_per_expert, half_rows, reinterpret_cast<__nv_bfloat16*>(out), ldo, balanced,
+        row_ptr);
+  }
+  return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
+}
+
 // rows_per_unit: weight rows one CTA covers per unit (64 gated / 128 down); the pair kernel
 // covers twice that per unit, so MT is given for the single-CTA tiling and halved here.
 template <bool GATED>
 int launch_moe_gemm(const void* w, int w_rows_total, const void* act, int act_rows, const int* offsets, int E,
-                    int MT, int K, int rows_per_expert, int half_rows, void* out, int ldo, cudaStream_t stream) {
+                    int MT, int K, int rows_per_expert, int half_rows, void* out, int ldo, cudaStream_t stream,
+                    const long long* row_ptr = nullptr) {
   const bool pair = use_pair_kernel() && MT % 2 == 0 && (mgb_host::num_sms() & ~1) >= 2;
   // token tiling: the gated GEMM balances its tiles (see token_tile); MGB_GEMM_BALANCED=0/1 overrides
   static const int bal_env = [] {
@@ -491,31 +543,17 @@ int launch_moe_gemm(const void* w, int w_rows_total, const void* act, int act_ro
   if (mgb_host::encode_tmap_2d_bf16(&tmB, act, K, act_rows, (uint64_t)K * 2, mgb::kBK,
                                     pair ? mgb::kPBRows : mgb::kBRows) != CUDA_SUCCESS)
     return MGB_ECUDA;
-  if (pair) {
-    static bool attr_p = false;
-    if (!attr_p) {
-      if (cudaFuncSetAttribute(mgb::moe_gemm_pair_kernel<GATED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               mgb::pair_smem<GATED>()) != cudaSuccess)
-        return MGB_ECUDA;
-      attr_p = true;
-    }
-    const int grid = mgb_host::num_sms() & ~1;
-    mgb::moe_gemm_pair_kernel<GATED><<<grid, mgb::Epi<GATED>::kThreads, mgb::pair_smem<GATED>(), stream>>>(
-        tmA, tmB, offsets, E, MT / 2, K, rows_per_expert, half_rows, reinterpret_cast<__nv_bfloat16*>(out), ldo,
-        balanced);
-    return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
+  if (row_ptr) {
+    if (GATED) return MGB_EINVAL;  // only the down GEMM sends rows home
+    return pair ? launch_variant<GATED, true, true>(tmA, tmB, offsets, E, MT, K, rows_per_expert, half_rows, out, ldo,
+                                                   balanced, row_ptr, stream)
+                : launch_variant<GATED, false, true>(tmA, tmB, offsets, E, MT, K, rows_per_expert, half_rows, out, ldo,
+                                                    balanced, row_ptr, stream);
   }
-  static bool attr_set = false;
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(mgb::moe_gemm_kernel<GATED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             mgb::gemm_smem<GATED>()) != cudaSuccess)
-      return MGB_ECUDA;
-    attr_set = true;
-  }
-  const int grid = mgb_host::num_sms();
-  mgb::moe_gemm_kernel<GATED><<<grid, mgb::Epi<GATED>::kThreads, mgb::gemm_smem<GATED>(), stream>>>(
-      tmA, tmB, offsets, E, MT, K, rows_per_expert, half_rows, reinterpret_cast<__nv_bfloat16*>(out), ldo, balanced);
-  return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
+  return pair ? launch_variant<GATED, true, false>(tmA, tmB, offsets, E, MT, K, rows_per_expert, half_rows, out, ldo,
+                                                  balanced, nullptr, stream)
+              : launch_variant<GATED, false, false>(tmA, tmB, offsets, E, MT, K, rows_per_expert, half_rows, out, ldo,
+                                                   balanced, nullptr, stream);
 }
 }  // namespace
 
@@ -540,6 +578,15 @@ int mgb_moe_gemm_down(const void* w_down, const void* h, const int* offsets, int
   if (E < 1 || E > mgb::kMaxExperts || f % mgb::kBK || d % mgb::kBM || rows_cap < 1) return MGB_EINVAL;
   return launch_moe_gemm<false>(w_down, E * d, h, rows_cap, offsets, E, d / mgb::kBM, f, d, 0, y_out, d,
                                 reinterpret_cast<cudaStream_t>(stream));
+}
+
+// GEMM2 with the expert-parallel combine fused into the epilogue: output row r is written to
+// row_ptr[r] (a UVA pointer into the source rank's y_perm, mgb_ep_row_ptrs; 0 = skip) instead of y.
+int mgb_moe_gemm_down_ep(const void* w_down, const void* h, const int* offsets, int E, int d, int f, int rows_cap,
+                         const long long* row_ptr, void* stream) {
+  if (E < 1 || E > mgb::kMaxExperts || f % mgb::kBK || d % mgb::kBM || rows_cap < 1 || !row_ptr) return MGB_EINVAL;
+  return launch_moe_gemm<false>(w_down, E * d, h, rows_cap, offsets, E, d / mgb::kBM, f, d, 0, nullptr, d,
+                                reinterpret_cast<cudaStream_t>(stream), row_ptr);
 }
 
 // Both GEMMs back to back (h is caller-owned scratch [rows_cap, f]).

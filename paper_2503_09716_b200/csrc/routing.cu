@@ -340,7 +340,8 @@ __global__ void permute_kernel(const __nv_bfloat16* __restrict__ x, const int* _
                                const int* __restrict__ local_rank, const int* __restrict__ block_base,
                                const int* __restrict__ offsets, int T, int d, int k, int E, int tpb,
                                __nv_bfloat16* __restrict__ x_perm, int* __restrict__ src_token,
-                               int* __restrict__ dst_pos) {
+                               int* __restrict__ dst_pos, const long long* __restrict__ peer_base,
+                               const int* __restrict__ disp_row, int E_local) {
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (gw >= T * k) return;
@@ -352,7 +353,11 @@ __global__ void permute_kernel(const __nv_bfloat16* __restrict__ x, const int* _
     src_token[pos] = t;
   }
   const uint4* src = reinterpret_cast<const uint4*>(x + (size_t)t * d);
-  uint4* dst = reinterpret_cast<uint4*>(x_perm + (size_t)pos * d);
+  // expert-parallel dispatch fused into the permutation: the row goes straight into the receive
+  // buffer of the expert's owner rank (peer memory over NVLink), at this source's segment of expert e
+  uint4* dst = peer_base ? reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(peer_base[e / E_local]) +
+                                                     (size_t)(disp_row[e] + pos - offsets[e]) * d)
+                         : reinterpret_cast<uint4*>(x_perm + (size_t)pos * d);
   // all of the lane's 16 B vectors in flight before any store (row <= 8 KB -> <= 24 vectors/lane)
   constexpr int U = 8;
   const int nvec = d / 8;
@@ -520,7 +525,54 @@ int mgb_permute(const void* x, const int* topk_idx, const int* local_rank, const
   const int blocks = (warps * 32 + threads - 1) / threads;
   mgb::permute_kernel<<<blocks, threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<const __nv_bfloat16*>(x), topk_idx, local_rank, block_base, offsets, T, d, k, E,
-      mgb::kRouterTPB, reinterpret_cast<__nv_bfloat16*>(x_perm), src_token, dst_pos);
+      mgb::kRouterTPB, reinterpret_cast<__nv_bfloat16*>(x_perm), src_token, dst_pos, nullptr, nullptr, 1);
+  return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
+}
+
+// Expert-parallel dispatch fused with the permutation: row (t, j) of expert e = topk_idx[t, j] is
+// written to peer_base[e / E_local] (the owner rank's receive buffer, a UVA peer pointer) at row
+// disp_row[e] + (its position within expert e's segment).  dst_pos / src_token are the local
+// permuted positions, as mgb_permute writes them (the combine on this rank uses them).
+int mgb_ep_permute_dispatch(const void* x, const int* topk_idx, const int* local_rank, const int* block_base,
+                            const int* offsets, int T, int d, int k, int E, int E_local, const long long* peer_base,
+                            const int* disp_row, int* src_token, int* dst_pos, void* stream) {
+  if (T < 1 || d % 8 || k < 1 || k > mgb::kMaxK || E_local < 1 || E % E_local || !peer_base || !disp_row)
+    return MGB_EINVAL;
+  const int warps = T * k;
+  const int threads = 256;
+  const int blocks = (warps * 32 + threads - 1) / threads;
+  mgb::permute_kernel<<<blocks, threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const __nv_bfloat16*>(x), topk_idx, local_rank, block_base, offsets, T, d, k, E,
+      mgb::kRouterTPB, nullptr, src_token, dst_pos, peer_base, disp_row, E_local);
+  return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
+}
+
+// Destination of every row of the owner's expert-major receive buffer for the combine send: the
+// rows are (local expert i, source s) segments in that order; segment j = i * W + s starts at
+// seg_start[j] (ascending), holds seg_len[j] rows and maps row q to row q + seg_delta[j] of source
+// s's y_perm, whose base is peer_base[s].  Rows past the last segment get 0 (skipped).
+__global__ void ep_row_ptrs_kernel(const int* __restrict__ seg_start, const int* __restrict__ seg_len,
+                                   const int* __restrict__ seg_delta, int n_seg, int W,
+                                   const long long* __restrict__ peer_base, int row_bytes, int rows_cap,
+                                   long long* __restrict__ row_ptr) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= rows_cap) return;
+  int lo = 0, hi = n_seg - 1;  // last segment with start <= q
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (seg_start[mid] <= q) lo = mid; else hi = mid - 1;
+  }
+  long long p = 0;
+  if (seg_start[lo] <= q && q < seg_start[lo] + seg_len[lo])
+    p = peer_base[lo % W] + (long long)(q + seg_delta[lo]) * row_bytes;
+  row_ptr[q] = p;
+}
+
+int mgb_ep_row_ptrs(const int* seg_start, const int* seg_len, const int* seg_delta, int n_seg, int W,
+                    const long long* peer_base, int row_bytes, int rows_cap, long long* row_ptr, void* stream) {
+  if (n_seg < 1 || W < 1 || n_seg % W || row_bytes < 16 || rows_cap < 1) return MGB_EINVAL;
+  ep_row_ptrs_kernel<<<(rows_cap + 255) / 256, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      seg_start, seg_len, seg_delta, n_seg, W, peer_base, row_bytes, rows_cap, row_ptr);
   return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
 }
 

@@ -98,3 +98,81 @@ def shard_sequences(B_total: int, rank: int, world: int) -> tuple[int, int]:
     q, r = divmod(B_total, world)
     s0 = rank * q + min(rank, r)
     return s0, s0 + q + (rank < r)
+
+
+class PeerExpertParallel:
+    """Expert parallelism with the exchange fused into the kernels over peer memory (NVLink 5 /
+    NVSwitch, UVA peer pointers), the B200-native alternative to the all_to_all path above:
+
+      dispatch  the permutation kernel writes each routed row straight into the receive buffer of
+                the expert's owner rank (mgb_ep_permute_dispatch), at this source's slot of the
+                expert's segment -- no x_perm round trip, no packing, no collective on the data;
+      combine   the down-projection GEMM's epilogue stores each output row straight into the home
+                rank's y_perm (mgb_moe_gemm_down_ep with mgb_ep_row_ptrs), where the usual weighted
+                unpermute_combine runs -- so results stay bit-identical to the single-GPU path.
+
+    Only the per-expert counts (E ints per rank) are exchanged as a collective.  Every offset is
+    computed on the device from them (`tables`), so the layer has no host synchronisation.  The
+    receive-buffer layout per owner rank is expert-major over its E/W local experts and
+    source-rank-major within an expert.  `recv_ptrs[r]` / `yperm_ptrs[r]` are rank r's buffers as
+    seen from this rank (torch symmetric memory buffer_ptrs on a multi-GPU box; plain device
+    pointers when several virtual ranks share one GPU, as in tests/test_ep_peer_gpu.py).
+    Cross-rank ordering (all writes into a buffer landed before it is read) is the caller's
+    barrier between the three phases."""
+
+    def __init__(self, n_experts: int, world: int, rank: int, recv_ptrs, yperm_ptrs, device="cuda"):
+        if n_experts % world:
+            raise ValueError(f"{n_experts} experts do not shard over {world} ranks")
+        self.E, self.W, self.rank = n_experts, world, rank
+        self.L = n_experts // world
+        self.first = rank * self.L
+        self.peer_recv = torch.tensor([int(p) for p in recv_ptrs], dtype=torch.int64, device=device)
+        self.peer_y = torch.tensor([int(p) for p in yperm_ptrs], dtype=torch.int64, device=device)
+
+    def tables(self, counts_all: torch.Tensor) -> dict:
+        """counts_all [W, E]: rows source s routes to expert e.  Returns this rank's dispatch rows
+        (as a source) and receive / combine tables (as an owner), all int32 on counts_all's device."""
+        C = counts_all.to(torch.int64)
+        W, L, r, E = self.W, self.L, self.rank, self.E
+        tot = C.sum(0)                                    # [E] rows per expert over all sources
+        tr = tot.view(W, L)
+        loc_base = (tr.cumsum(1) - tr).reshape(E)         # expert e's block start in its owner's buffer
+        pre_src = C.cumsum(0) - C                         # [W, E] rows of e from earlier sources
+        src_off = C.cumsum(1) - C                         # [W, E] e's segment start in source s's x_perm
+        e0 = r * L
+        seg_start = loc_base[e0:e0 + L][:, None] + pre_src[:, e0:e0 + L].t()   # [L, W], i-major
+        loc_offsets = torch.zeros(L + 1, dtype=torch.int64, device=C.device)
+        loc_offsets[1:] = tot[e0:e0 + L].cumsum(0)
+        i32 = torch.int32
+        return dict(disp_row=(loc_base + pre_src[r]).to(i32), loc_offsets=loc_offsets.to(i32),
+                    n_recv=loc_offsets[-1:].to(i32),
+                    seg_start=seg_start.reshape(-1).to(i32), seg_len=C[:, e0:e0 + L].t().reshape(-1).to(i32),
+                    seg_delta=(src_off[:, e0:e0 + L].t() - seg_start).reshape(-1).to(i32))
+
+    # ---- the three phases (each rank issues its own; barriers between phases are the caller's) ----
+    def dispatch(self, h: torch.Tensor, ws, tab: dict) -> None:
+        """Route + permute + send: this rank's routed rows land in the owners' receive buffers."""
+        from . import _native as nat
+
+        T, d = h.shape
+        nat.call("mgb_ep_permute_dispatch", h.data_ptr(), ws.topk_idx.data_ptr(), ws.local_rank.data_ptr(),
+                 ws.block_hist.data_ptr(), ws.offsets.data_ptr(), T, d, ws.k, self.E, self.L,
+                 self.peer_recv.data_ptr(), tab["disp_row"].data_ptr(), ws.src_token.data_ptr(),
+                 ws.dst_pos.data_ptr(), torch.cuda.current_stream().cuda_stream)
+
+    def experts(self, w_gate_up: torch.Tensor, w_down: torch.Tensor, recv: torch.Tensor, h_ffn: torch.Tensor,
+                row_ptr: torch.Tensor, tab: dict) -> None:
+        """The local experts' grouped GEMMs over the receive buffer; the down GEMM's epilogue sends
+        every output row home.  w_gate_up / w_down are this rank's [E/W, ...] expert shards."""
+        from . import _native as nat
+        from . import ops
+
+        st = torch.cuda.current_stream().cuda_stream
+        L, d = self.L, recv.shape[1]
+        f = w_down.shape[2]
+        ops.moe_gemm_gate_up(w_gate_up, recv, tab["loc_offsets"], h_ffn)
+        nat.call("mgb_ep_row_ptrs", tab["seg_start"].data_ptr(), tab["seg_len"].data_ptr(),
+                 tab["seg_delta"].data_ptr(), L * self.W, self.W, self.peer_y.data_ptr(), d * 2, recv.shape[0],
+                 row_ptr.data_ptr(), st)
+        nat.call("mgb_moe_gemm_down_ep", w_down.data_ptr(), h_ffn.data_ptr(), tab["loc_offsets"].data_ptr(), L, d, f,
+                 recv.shape[0], row_ptr.data_ptr(), st)

@@ -98,3 +98,39 @@ def test_single_rank_is_identity():
     x = _tokens(1)
     assert torch.equal(_moe_ep(x, ep, wr, wgu, wd), R.moe_block(x, wr, wgu, wd, K, 0))
     assert shard_sequences(10, 0, 3) == (0, 4) and shard_sequences(10, 2, 3) == (7, 10)
+
+
+@pytest.mark.parametrize("W,E", [(2, 8), (4, 16), (8, 64)])
+def test_peer_ep_tables_route_every_row_home(W, E):
+    """PeerExpertParallel.tables (host-independent, computed on the counts alone): the dispatch rows
+    of all sources tile each owner's receive buffer exactly (expert-major, source-major within an
+    expert), and the owner's combine segments send every row back to the position it came from in
+    its source's expert-major permutation."""
+    from paper_2503_09716_b200.ep import PeerExpertParallel
+
+    g = torch.Generator().manual_seed(W * E)
+    C = torch.randint(0, 9, (W, E), generator=g)
+    peps = [PeerExpertParallel(E, W, r, [0] * W, [0] * W, device="cpu") for r in range(W)]
+    tabs = [p.tables(C) for p in peps]
+    L = E // W
+    src_off = torch.cumsum(C, 1) - C
+    for r in range(W):
+        owner = tabs[r]
+        n = int(owner["n_recv"][0])
+        filled = torch.zeros(n, dtype=torch.int64) - 1
+        back = {}
+        for s in range(W):
+            for e in range(r * L, (r + 1) * L):
+                for m in range(int(C[s, e])):
+                    q = int(tabs[s]["disp_row"][e]) + m          # where source s's row lands
+                    assert filled[q] == -1
+                    filled[q] = s
+                    back[q] = (s, int(src_off[s, e]) + m)         # where it must go home
+        assert (filled >= 0).all()
+        seg_start, seg_len, seg_delta = owner["seg_start"], owner["seg_len"], owner["seg_delta"]
+        for q, (s, home) in back.items():
+            j = int((seg_start <= q).nonzero().max())
+            while int(seg_len[j]) == 0 or q >= int(seg_start[j]) + int(seg_len[j]):
+                j -= 1
+            assert j % W == s and q + int(seg_delta[j]) == home
+        assert torch.equal(owner["loc_offsets"][1:].long() - owner["loc_offsets"][:-1].long(), C[:, r * L:(r + 1) * L].sum(0))
