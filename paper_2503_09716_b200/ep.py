@@ -176,3 +176,36 @@ class PeerExpertParallel:
                  row_ptr.data_ptr(), st)
         nat.call("mgb_moe_gemm_down_ep", w_down.data_ptr(), h_ffn.data_ptr(), tab["loc_offsets"].data_ptr(), L, d, f,
                  recv.shape[0], row_ptr.data_ptr(), st)
+
+    # ---- multi-GPU wiring: torch symmetric memory (NVLink peer mappings + device-side barrier) ----
+    @classmethod
+    def from_symmetric_memory(cls, n_experts: int, group, recv_rows: int, yperm_rows: int, d: int,
+                              device: str = "cuda") -> "PeerExpertParallel":
+        """Allocate this rank's receive buffer and y_perm in symmetric memory and exchange their
+        peer mappings (one rendezvous at setup).  `recv_rows` must cover the worst case (every
+        source's T*k rows landing on this rank's experts)."""
+        import torch.distributed._symmetric_memory as symm
+
+        recv = symm.empty(recv_rows, d, dtype=torch.bfloat16, device=device)
+        yperm = symm.empty(yperm_rows, d, dtype=torch.bfloat16, device=device)
+        hr, hy = symm.rendezvous(recv, group), symm.rendezvous(yperm, group)
+        self = cls(n_experts, hr.world_size, hr.rank, hr.buffer_ptrs, hy.buffer_ptrs, device=device)
+        self.recv, self.yperm, self.group, self._handle = recv, yperm, group, hr
+        return self
+
+    def barrier(self) -> None:
+        """Stream-ordered cross-rank barrier (all peer writes of the phase have landed)."""
+        self._handle.barrier()
+
+    def moe(self, h: torch.Tensor, ws, w_gate_up_local: torch.Tensor, w_down_local: torch.Tensor,
+            h_ffn: torch.Tensor, row_ptr: torch.Tensor) -> torch.Tensor:
+        """One routed-expert layer across the group after this rank's router: returns this rank's
+        y_perm (home rows of its tokens' expert outputs) for mgb_unpermute_combine."""
+        counts_all = torch.empty(self.W, self.E, dtype=ws.counts.dtype, device=ws.counts.device)
+        dist.all_gather_into_tensor(counts_all, ws.counts, group=self.group)
+        tab = self.tables(counts_all)
+        self.dispatch(h, ws, tab)
+        self.barrier()
+        self.experts(w_gate_up_local, w_down_local, self.recv, h_ffn, row_ptr, tab)
+        self.barrier()
+        return self.yperm

@@ -59,3 +59,58 @@ def test_peer_ep_bit_exact(W, E, k, d, f, T):
         ops.unpermute_combine(yperm[r], wss[r], out, T)
         assert torch.equal(yperm[r], ref_y[r]), f"rank {r}: y_perm differs"
         assert torch.equal(out, ref_out[r]), f"rank {r}: MoE output differs"
+
+
+def _symm_worker(rank, world, port, q):
+    import os
+
+    import torch.distributed as dist
+
+    from paper_2503_09716_b200 import ops
+    from paper_2503_09716_b200.ep import PeerExpertParallel
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world)
+    E, k, d, f, T = 8, 2, 256, 512, 24
+    dev = f"cuda:{rank}"
+    wr, wgu, wd = (uniform_bf16((E, d), 0, 1, 0.3).to(dev), uniform_bf16((E, 2 * f, d), 0, 2, 0.05).to(dev),
+                   uniform_bf16((E, d, f), 0, 3, 0.05).to(dev))
+    x = uniform_bf16((T, d), 0, 10 + rank, 1.0).to(dev)
+    ws = ops.RouterWorkspace(T, E, k, device=dev)
+    ops.router_topk(None, None, ws, k, 0, logits_in=torch.mm(x, wr.t(), out_dtype=torch.float32))
+    L = E // world
+    pep = PeerExpertParallel.from_symmetric_memory(E, dist.group.WORLD, world * T * k, T * k, d, device=dev)
+    y = pep.moe(x, ws, wgu[rank * L:(rank + 1) * L], wd[rank * L:(rank + 1) * L],
+                torch.empty(world * T * k, f, dtype=torch.bfloat16, device=dev),
+                torch.empty(world * T * k, dtype=torch.int64, device=dev))
+    xp = torch.empty(T * k, d, dtype=torch.bfloat16, device=dev)
+    ops.permute(x, ws, xp)
+    h = torch.empty(T * k, f, dtype=torch.bfloat16, device=dev)
+    ref = torch.empty(T * k, d, dtype=torch.bfloat16, device=dev)
+    ops.moe_gemm_gate_up(wgu, xp, ws.offsets, h)
+    ops.moe_gemm_down(wd, h, ws.offsets, ref)
+    torch.cuda.synchronize()
+    q.put((rank, bool(torch.equal(y, ref))))
+    dist.destroy_process_group()
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs with NVLink peer access")
+def test_symmetric_memory_two_ranks():
+    """The same fused dispatch/combine across two real GPUs through torch symmetric memory."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_symm_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    assert res == {0: True, 1: True}
