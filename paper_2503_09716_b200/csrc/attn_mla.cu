@@ -53,6 +53,22 @@ static_assert(kMlaPage % 8 == 0 && kMlaPage <= 64, "latent page = whole swizzle 
 constexpr int kMlaHeads = 16;    // heads per work item = N of both MMAs
 constexpr int kMlaThreads = 192;
 
+// Optional per-page timeline of CTA 0 (build with -DMGB_MLA_TRACE; tools/mla_trace.py):
+// trace[ev * kTraceN + page] = %globaltimer (ns) of event ev for the CTA's page number `page`.
+#ifdef MGB_MLA_TRACE
+constexpr int kTraceN = 256;
+__device__ unsigned long long g_mla_trace[16 * kTraceN];
+MGB_DEVINL void mla_trace(int ev, int page) {
+  if (blockIdx.x == 0 && page < kTraceN) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_mla_trace[ev * kTraceN + page] = t;
+  }
+}
+#else
+MGB_DEVINL void mla_trace(int, int) {}
+#endif
+
 MGB_DEVINL void cons_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
 template <int R, int RP>  // latent width, rope width
@@ -181,6 +197,7 @@ decode_attn_mla_kernel(const __grid_constant__ CUtensorMap tm_qlat,  // q_lat [H
         for (int p = 0; p < np; ++p, ++g) {
           const int s = g % kMlaStages;
           mbar_wait(&empty[s], ((g / kMlaStages) & 1) ^ 1);
+          mla_trace(0, g);  // 0: stage free, page load issued
           prefetch_next();
           mbar_arrive_expect_tx(&full[s], C::kPageBytes);
           bulk_load(pages + s * C::kPageBytes, cache + (size_t)bt[p] * (C::kPageBytes / 2), C::kPageBytes, &full[s],
@@ -241,6 +258,7 @@ decode_attn_mla_kernel(const __grid_constant__ CUtensorMap tm_qlat,  // q_lat [H
       const bool can_pv = gpv < gs && __all_sync(0xffffffffu, mbar_test(&pfull[pb], (gpv >> 1) & 1) &&
                                                                    mbar_test(&oempty[pb], ((gpv >> 1) & 1) ^ 1));
       if (can_pv) {  // O^T[pb] = C_gpv[:, :R]^T . P_gpv^T, then release the page's stage
+        if (lane == 0) mla_trace(2, gpv);  // 2: P.V issued
         tc_fence_after();
         const uint64_t a0 = dC_o + ((uint32_t)(pst * C::kPageBytes) >> 4), b0 = dP + ((uint32_t)(pb * C::kPBytes) >> 4);
         const uint32_t d0 = tm + C::kOCol + pb * C::MT * 16;
@@ -254,6 +272,7 @@ decode_attn_mla_kernel(const __grid_constant__ CUtensorMap tm_qlat,  // q_lat [H
         umma_commit_warp(&empty[pst]);
         ++gpv;
       } else if (can_s) {  // S^T[sb] = C_gs . Q^T over kSAcc partial accumulators
+        if (lane == 0) mla_trace(1, gs);  // 1: page landed (+ S buffer free): S issued
         tc_fence_after();
         const uint64_t a0 = dC_s + ((uint32_t)(sst * C::kPageBytes) >> 4);
         const uint64_t b0 = dQ;
@@ -282,6 +301,7 @@ decode_attn_mla_kernel(const __grid_constant__ CUtensorMap tm_qlat,  // q_lat [H
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
       const int b = it / n_hg, hg = it - b * n_hg;
       const int len = seq_lens[b];
+      if (tid == 0) mla_trace(12, g);  // 12: next item's length loaded
       const int np = (len + kMlaPage - 1) / kMlaPage;
       if (np == 0) {
         for (int i = tid; i < kMlaHeads * R; i += 128) {
@@ -302,6 +322,7 @@ decode_attn_mla_kernel(const __grid_constant__ CUtensorMap tm_qlat,  // q_lat [H
       auto accumulate_o = [&](int t) {  // O = O * alpha(t) + O^T tile t (lane = latent dim)
         const int s = t & 1;
         mbar_wait(&ofull[s], (t >> 1) & 1);
+        if (threadIdx.x == 0) mla_trace(5, t);  // 5: P.V of page t done (O pulled)
         tc_fence_after();
         uint32_t v[C::MT][16];
 #pragma unroll
@@ -320,6 +341,7 @@ decode_attn_mla_kernel(const __grid_constant__ CUtensorMap tm_qlat,  // q_lat [H
         const int s = g & 1, st = g % kMlaStages;
         const int n = min(kMlaPage, len - p * kMlaPage);
         mbar_wait(&sfull[s], (g >> 1) & 1);
+        if (tid == 0) mla_trace(3, g);  // 3: S ready at the softmax warps
         tc_fence_after();
         uint32_t sv[C::kSAcc][16];
 #pragma unroll
@@ -372,28 +394,41 @@ decode_attn_mla_kernel(const __grid_constant__ CUtensorMap tm_qlat,  // q_lat [H
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&pfull[s]);
+        if (lane == 0) mla_trace(warp == 0 ? 4 : 5 + warp, g);  // 4, 6, 7, 8: P written by warp 0..3
         if (p > 0) accumulate_o(g - 1);
 #pragma unroll
         for (int h = 0; h < 16; ++h) alpha_prev[h] = alpha[h];
       }
       accumulate_o(g - 1);
+      if (tid == 0) mla_trace(9, g - 1);  // 9: item's last O pulled
 
       // ---- normalise and store: lane = latent dim, 16 heads per thread ----
       const float lsum = xreduce16<false>(lpart, lane);
+      if (tid == 0) mla_trace(13, g - 1);  // 13: l reduced
       if (lane < 16) lred[warp * 16 + lane] = lsum;
       cons_bar();
+      if (tid == 0) mla_trace(14, g - 1);  // 14: l shared
+      // the per-item epilogue sits between two items on the softmax warps' critical path, with one
+      // warp per scheduler: 16 independent reciprocals first (approximate: far below bf16 rounding),
+      // then 64 independent scale + convert + store chains
+      float inv[16];
+#pragma unroll
+      for (int h = 0; h < 16; ++h) {
+        const float l = lred[h] + lred[16 + h] + lred[32 + h] + lred[48 + h];
+        inv[h] = l > 0.f ? __fdividef(1.0f, l) : 0.f;
+      }
 #pragma unroll
       for (int h = 0; h < 16; ++h) {
         const int hh = hg * kMlaHeads + h;
-        const float l = lred[h] + lred[16 + h] + lred[32 + h] + lred[48 + h];
-        const float inv = l > 0.f ? 1.0f / l : 0.f;
         if (hh < H) {
           __nv_bfloat16* dst = o_lat + ((size_t)hh * B + b) * R + warp * 32 + lane;
 #pragma unroll
-          for (int mt = 0; mt < C::MT; ++mt) dst[mt * 128] = __float2bfloat16_rn(O[mt][h] * inv);
+          for (int mt = 0; mt < C::MT; ++mt) dst[mt * 128] = __float2bfloat16_rn(O[mt][h] * inv[h]);
         }
       }
+      if (tid == 0) mla_trace(10, g - 1);  // 10: O stores issued
       cons_bar();  // lred reused by the next item
+      if (tid == 0) mla_trace(11, g - 1);  // 11: item epilogue done
     }
   }
   tc_fence_before();
@@ -613,5 +648,11 @@ int mgb_mla_append_prefill(void* q, const void* ckv, const void* norm_w, float e
       reinterpret_cast<__nv_bfloat16*>(kpe_out));
   return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
 }
+
+#ifdef MGB_MLA_TRACE
+int mgb_mla_trace_read(unsigned long long* host_out) {
+  return cudaMemcpyFromSymbol(host_out, mgb::g_mla_trace, sizeof(mgb::g_mla_trace)) == cudaSuccess ? MGB_OK : MGB_ECUDA;
+}
+#endif
 
 }  // extern "C"
