@@ -199,9 +199,19 @@ decode_attn_mla_kernel(const __grid_constant__ CUtensorMap tm_qlat,  // q_lat [H
           mbar_wait(&empty[s], ((g / kMlaStages) & 1) ^ 1);
           mla_trace(0, g);  // 0: stage free, page load issued
           prefetch_next();
-          mbar_arrive_expect_tx(&full[s], C::kPageBytes);
-          bulk_load(pages + s * C::kPageBytes, cache + (size_t)bt[p] * (C::kPageBytes / 2), C::kPageBytes, &full[s],
-                    pol);
+          const int rows = min(kMlaPage, seq_lens[b] - p * kMlaPage);
+          const __nv_bfloat16* src = cache + (size_t)bt[p] * (C::kPageBytes / 2);
+          if (rows == kMlaPage) {
+            mbar_arrive_expect_tx(&full[s], C::kPageBytes);
+            bulk_load(pages + s * C::kPageBytes, src, C::kPageBytes, &full[s], pol);
+          } else {  // a sequence's last, partial page: only its valid token rows of every 64-dim block
+            // (rows past the end keep stale finite data; the softmax warps mask them and zero them
+            // before P.V)
+            mbar_arrive_expect_tx(&full[s], C::NKB * rows * 128);
+            for (int kb = 0; kb < C::NKB; ++kb)
+              bulk_load(pages + s * C::kPageBytes + kb * C::kBlockBytes, src + kb * (C::kBlockBytes / 2), rows * 128,
+                        &full[s], pol);
+          }
         }
       }
     } else if (lane == 1) {
