@@ -263,10 +263,12 @@ moe_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           uint32_t v[32];
           tmem_ld32(tl + c0, v);
           tmem_ld_wait();
-          if (ROWPTR) {  // expert-parallel combine fused into the epilogue: the row goes home (peer memory)
+          if (ROWPTR) {  // row stores to per-row destinations (EP combine, layout transposes)
+            // one coalesced load of the chunk's 32 row pointers, broadcast lane by lane
+            const long long mine = c0 + (int)lane < n ? row_ptr[tok0 + c0 + lane] : 0;
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-              const long long p = c0 + j < n ? row_ptr[tok0 + c0 + j] : 0;
+              const long long p = __shfl_sync(0xffffffffu, mine, j);
               if (p) reinterpret_cast<__nv_bfloat16*>(p)[col] = __float2bfloat16_rn(__uint_as_float(v[j]));
             }
           } else {
@@ -453,10 +455,12 @@ moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
           uint32_t v[32];
           tmem_ld32(tl + c0, v);
           tmem_ld_wait();
-          if (ROWPTR) {  // expert-parallel combine fused into the epilogue: the row goes home (peer memory)
+          if (ROWPTR) {  // row stores to per-row destinations (EP combine, layout transposes)
+            // one coalesced load of the chunk's 32 row pointers, broadcast lane by lane
+            const long long mine = c0 + (int)lane < n ? row_ptr[tok0 + c0 + lane] : 0;
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-              const long long p = c0 + j < n ? row_ptr[tok0 + c0 + j] : 0;
+              const long long p = __shfl_sync(0xffffffffu, mine, j);
               if (p) reinterpret_cast<__nv_bfloat16*>(p)[col] = __float2bfloat16_rn(__uint_as_float(v[j]));
             }
           } else {
