@@ -846,8 +846,29 @@ class Engine:
         return self.out_tokens[:, :n_steps].to("cpu", non_blocking=False)
 
     def can_prefill(self) -> bool:
-        """Batched prefill is built for HBM-resident weights and KV (both families)."""
-        return self.kv_policy == "resident" and not self.offload and self.n_cpu == 0 and self.ep is None
+        """Batched prefill is built for HBM-resident weights (both families; KV resident or in the
+        host page store, including plans with a CPU attention share)."""
+        return not self.offload and self.ep is None
+
+    def _prefill_kv_target(self, l: int, s0: int, n: int):
+        """(stores, block table, seq0) the prefill KV write of sequences [s0, s0+n) goes to: the HBM
+        page store, or -- with the KV offloaded -- a device staging copy of the chunk's pages that
+        `_prefill_kv_flush` then moves to the host store in one contiguous copy per store."""
+        if self.kv_policy == "resident":
+            return self.kv[l], self.block_table, s0
+        pe, pps = self.page_elems, self.pps
+        if getattr(self, "_pf_stage_pages", 0) < n * pps:
+            self._pf_stage = [torch.empty(n * pps * pe, dtype=BF16, device=self.device) for _ in self.kv[l]]
+            self._pf_stage_table = torch.arange(n * pps, dtype=torch.int32, device=self.device).view(n, pps)
+            self._pf_stage_pages = n * pps
+        return self._pf_stage, self._pf_stage_table, 0
+
+    def _prefill_kv_flush(self, l: int, s0: int, n: int) -> None:
+        if self.kv_policy == "resident":
+            return
+        pe, pps = self.page_elems, self.pps
+        for s, host in enumerate(self.kv[l]):
+            host[s0 * pps * pe:(s0 + n) * pps * pe].copy_(self._pf_stage[s][:n * pps * pe], non_blocking=True)
 
     def _prefill_scratch(self, T: int) -> dict:
         """Activation buffers for one chunk of T prompt tokens (allocated once, grown on demand)."""
@@ -884,10 +905,11 @@ class Engine:
         t, hd, Hq, Hkv = n * P, a.head_dim, a.n_heads, a.n_kv_heads
         qkv, q, kk, vv = S["qkv"][:t], S["q"][:t], S["k"][:t], S["v"][:t]
         torch.mm(S["h"][:t], W["wqkv"].t(), out=qkv)
-        nat.call("mgb_rope_append_gqa_prefill", qkv.data_ptr(), t, s0, P, self.cos_t.data_ptr(),
-                 self.sin_t.data_ptr(), Hq, Hkv, hd, self.block_table.data_ptr(), self.pps,
-                 self.k_cache[l].data_ptr(), self.v_cache[l].data_ptr(), q.data_ptr(), kk.data_ptr(),
-                 vv.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        (kc, vc), table, seq0 = self._prefill_kv_target(l, s0, n)
+        nat.call("mgb_rope_append_gqa_prefill", qkv.data_ptr(), t, seq0, P, self.cos_t.data_ptr(),
+                 self.sin_t.data_ptr(), Hq, Hkv, hd, table.data_ptr(), self.pps, kc.data_ptr(), vc.data_ptr(),
+                 q.data_ptr(), kk.data_ptr(), vv.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        self._prefill_kv_flush(l, s0, n)
         att = torch.nn.functional.scaled_dot_product_attention(
             q.view(n, P, Hq, hd).transpose(1, 2), kk.view(n, P, Hkv, hd).transpose(1, 2),
             vv.view(n, P, Hkv, hd).transpose(1, 2), is_causal=True, enable_gqa=True)
@@ -906,10 +928,12 @@ class Engine:
         else:
             torch.mm(h, W["q_proj"].t(), out=q)
         torch.mm(h, W["kv_a"].t(), out=S["ckv"][:t])
+        (cache,), table, seq0 = self._prefill_kv_target(l, s0, n)
         nat.call("mgb_mla_append_prefill", q.data_ptr(), S["ckv"].data_ptr(), W["kv_a_norm"].data_ptr(), a.rms_eps, t,
-                 s0, P, H, R, r, nope, self.cos_t.data_ptr(), self.sin_t.data_ptr(), self.block_table.data_ptr(),
-                 self.pps, self.latent[l].data_ptr(), S["c"].data_ptr(), S["kpe"].data_ptr(),
+                 seq0, P, H, R, r, nope, self.cos_t.data_ptr(), self.sin_t.data_ptr(), table.data_ptr(),
+                 self.pps, cache.data_ptr(), S["c"].data_ptr(), S["kpe"].data_ptr(),
                  torch.cuda.current_stream().cuda_stream)
+        self._prefill_kv_flush(l, s0, n)
         kv = S["kv"][:t]
         torch.mm(S["c"][:t], W["kv_b"].t(), out=kv)
         kv = kv.view(t, H, nope + vd)
@@ -932,7 +956,7 @@ class Engine:
         -> LM head on each sequence's last position.  Leaves every sequence at position P with its
         first generated token in next_ids (and out_tokens[:, P-1]); returns it (host int64 [B])."""
         if not self.can_prefill():
-            raise NotImplementedError("batched prefill needs HBM-resident weights and KV")
+            raise NotImplementedError("batched prefill needs HBM-resident weights")
         a, b = self.arch, self.buf
         B, P = input_ids.shape
         assert B == self.B and 1 <= P <= self.max_ctx

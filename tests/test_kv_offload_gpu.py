@@ -63,11 +63,14 @@ def test_kv_offload_generate_equals_resident(family):
     B, P, N = 8, 5, 6
     plan = _plan(A, B, 3)  # micro-batches of 3, 3, 2 sequences
     ids = torch.randint(0, A.vocab, (B, P), generator=torch.Generator().manual_seed(21))
-    ref = Engine(A, plan, prompt_len=P, decode_len=N, use_graph=False).generate(ids, N, prefill=False)
+    res = Engine(A, plan, prompt_len=P, decode_len=N, use_graph=False)
+    ref = res.generate(ids, N, prefill=False)
+    ref_pf = res.generate(ids, N)  # batched prefill (KV written to the host store through staging)
     for graph in (False, True):
         eng = Engine(A, plan, prompt_len=P, decode_len=N, use_graph=graph, kv_policy="offload", kv_ring_slots=2)
         assert not eng.kv[0][0].is_cuda and eng.kv_ring_n == 2
-        assert torch.equal(eng.generate(ids, N), ref)
+        assert torch.equal(eng.generate(ids, N, prefill=False), ref)
+        assert torch.equal(eng.generate(ids, N), ref_pf)
 
 
 @pytest.mark.parametrize("family", ["mixtral", "deepseek_v2"])
@@ -118,7 +121,7 @@ def test_dsv2_offloaded_weights_and_kv_match_resident():
         for graph in (False, True):
             eng = Engine(A, plan, prompt_len=P, decode_len=N, use_graph=graph, kv_policy=policy)
             assert eng.offload
-            assert torch.equal(eng.generate(ids, N), ref), (s_params, policy, graph)
+            assert torch.equal(eng.generate(ids, N, prefill=False), ref), (s_params, policy, graph)
         recs, rep = eng.trace_step()
         uncached = (A.layers - pl.dense_layers) * dense + pl.uncached_expert_count * ex
         # the reference's all-MoE model charges experts to the dense first layer too: none move
