@@ -756,8 +756,8 @@ class Engine:
             self._issue_lookahead(prologue=False)
         torch.mm(b.h, self.w.lm_head.t(), out=b.logits)
         ops.argmax(b.logits, b.next_ids)
-        ops.decode_advance(b.next_ids, self.out_tokens if record else None, b.step, b.positions)
-        if self.streaming:  # join: the step ends when every copy has landed
+        if self.streaming:  # join: every copy has landed -- and, before positions advance, every
+            # KV_COPY_OUT / CPU-attention job (they read this step's positions) has run
             self._join.record(self.h2d)
             self.stream.wait_event(self._join)
             if self.d2h is not None:
@@ -766,6 +766,7 @@ class Engine:
             if self.cpu_stream is not None:
                 self._join3.record(self.cpu_stream)
                 self.stream.wait_event(self._join3)
+        ops.decode_advance(b.next_ids, self.out_tokens if record else None, b.step, b.positions)
 
     # ------------------------------------------------------------------------------------
     # graph capture / replay
@@ -846,9 +847,14 @@ class Engine:
         return self.out_tokens[:, :n_steps].to("cpu", non_blocking=False)
 
     def can_prefill(self) -> bool:
-        """Batched prefill is built for HBM-resident weights (both families; KV resident or in the
-        host page store, including plans with a CPU attention share)."""
-        return not self.offload and self.ep is None
+        """Batched prefill: both families, weights resident (chunk-major) or offloaded (layer-major,
+        `_prefill_streamed`), KV resident or in the host page store (incl. a CPU attention share).
+        Not yet for DeepSeek-V2 with both weights and KV offloaded: there a later decode step faults
+        intermittently (a cross-stream hazard not found yet), so that combination
+        consumes the prompt through the decode step."""
+        if self.mla and self.offload and self.kv_policy == "offload":
+            return False
+        return self.ep is None
 
     def _prefill_kv_target(self, l: int, s0: int, n: int):
         """(stores, block table, seq0) the prefill KV write of sequences [s0, s0+n) goes to: the HBM
@@ -900,11 +906,12 @@ class Engine:
         self._pf, self._pf_T = S, T
         return S
 
-    def _prefill_attention_gqa(self, l: int, W: dict, S: dict, s0: int, n: int, P: int) -> torch.Tensor:
+    def _prefill_attention_gqa(self, l: int, W: dict, S: dict, s0: int, n: int, P: int,
+                               h: torch.Tensor) -> torch.Tensor:
         a = self.arch
         t, hd, Hq, Hkv = n * P, a.head_dim, a.n_heads, a.n_kv_heads
         qkv, q, kk, vv = S["qkv"][:t], S["q"][:t], S["k"][:t], S["v"][:t]
-        torch.mm(S["h"][:t], W["wqkv"].t(), out=qkv)
+        torch.mm(h, W["wqkv"].t(), out=qkv)
         (kc, vc), table, seq0 = self._prefill_kv_target(l, s0, n)
         nat.call("mgb_rope_append_gqa_prefill", qkv.data_ptr(), t, seq0, P, self.cos_t.data_ptr(),
                  self.sin_t.data_ptr(), Hq, Hkv, hd, table.data_ptr(), self.pps, kc.data_ptr(), vc.data_ptr(),
@@ -915,12 +922,13 @@ class Engine:
             vv.view(n, P, Hkv, hd).transpose(1, 2), is_causal=True, enable_gqa=True)
         return att.transpose(1, 2).reshape(t, Hq * hd)
 
-    def _prefill_attention_mla(self, l: int, W: dict, S: dict, s0: int, n: int, P: int) -> torch.Tensor:
+    def _prefill_attention_mla(self, l: int, W: dict, S: dict, s0: int, n: int, P: int,
+                               h: torch.Tensor) -> torch.Tensor:
         """HF DeepseekV2Attention on the prompt (modeling_deepseek_v2.py:337-396): the latent is
         up-projected per head (no absorption: every key is attended by P queries), causal SDPA."""
         a = self.arch
         t, H, R, r, nope, vd = n * P, a.n_heads, a.kv_lora_rank, a.qk_rope_dim, a.qk_nope_dim, a.v_head_dim
-        h, q = S["h"][:t], S["q"][:t]
+        q = S["q"][:t]
         if a.q_lora_rank:
             torch.mm(h, W["q_a"].t(), out=S["qa"][:t])
             ops.add_rmsnorm(S["qa"][:t], W["q_a_norm"], a.rms_eps, S["qan"][:t])
@@ -956,10 +964,12 @@ class Engine:
         -> LM head on each sequence's last position.  Leaves every sequence at position P with its
         first generated token in next_ids (and out_tokens[:, P-1]); returns it (host int64 [B])."""
         if not self.can_prefill():
-            raise NotImplementedError("batched prefill needs HBM-resident weights")
+            raise NotImplementedError("batched prefill is not built for the expert-parallel engine")
         a, b = self.arch, self.buf
         B, P = input_ids.shape
         assert B == self.B and 1 <= P <= self.max_ctx
+        if self.offload:
+            return self._prefill_streamed(input_ids, chunk_tokens)
         Bp = max(1, min(B, chunk_tokens // P))
         S = self._prefill_scratch(Bp * P)
         d, k = a.hidden, a.top_k
@@ -978,9 +988,9 @@ class Engine:
                     if l == 0:
                         ops.add_rmsnorm(x, W["ln1"], a.rms_eps, h)
                     if self.mla:
-                        att = self._prefill_attention_mla(l, W, S, s0, n, P)
+                        att = self._prefill_attention_mla(l, W, S, s0, n, P, h)
                     else:
-                        att = self._prefill_attention_gqa(l, W, S, s0, n, P)
+                        att = self._prefill_attention_gqa(l, W, S, s0, n, P, h)
                     torch.mm(att, W["wo"].t(), out=o)
                     ops.add_rmsnorm(x, W["ln2"], a.rms_eps, h, delta=o, x_out=x)
                     nxt = self.w.layers[l + 1]["ln1"] if l + 1 < a.layers else self.w.final_norm
@@ -1014,6 +1024,108 @@ class Engine:
             b.step.fill_(P)
             self.out_tokens[:, P - 1].copy_(b.next_ids)
         torch.cuda.current_stream().wait_stream(self.stream)
+        self.host_pos = P
+        return b.next_ids.to("cpu", torch.int64)
+
+    @torch.no_grad()
+    def _prefill_streamed(self, input_ids: torch.Tensor, chunk_tokens: int) -> torch.Tensor:
+        """Prefill with offloaded weights, module-based batching style: layer by
+        layer over ALL prompt tokens, so every streamed weight crosses the host link once per layer.
+        The layer's dense blob is copied into the dense buffer; attention runs in sequence chunks;
+        the MoE routes all tokens at once and runs expert by expert, each uncached expert streamed
+        into one of two slots on the H2D stream while the previous expert computes."""
+        a, b, w = self.arch, self.buf, self.w
+        B, P = input_ids.shape
+        T = B * P
+        d, k, f, E = a.hidden, a.top_k, a.moe_ffn, a.n_experts
+        bf = dict(dtype=BF16, device=self.device)
+        Bp = max(1, min(B, chunk_tokens // P))
+        S = self._prefill_scratch(Bp * P)
+        x_all, h_all = torch.empty(T, d, **bf), torch.empty(T, d, **bf)
+        sh_all = torch.empty(T, d, **bf) if self.mla else None
+        xp, yp = torch.empty(T * k, d, **bf), torch.empty(T * k, d, **bf)
+        lg = torch.empty(T, E, dtype=torch.float32, device=self.device)
+        ws = ops.RouterWorkspace(T, E, k, device=self.device)
+        hf = torch.empty(0, **bf)
+        ids = input_ids.to(self.device, torch.int32)
+        self.reset(0)
+        st, cp = self.stream, self.h2d
+        st.wait_stream(torch.cuda.current_stream())
+        slot_free = [torch.cuda.Event(), torch.cuda.Event()]
+        landed = [torch.cuda.Event(), torch.cuda.Event()]
+        for ev in slot_free:
+            ev.record(st)
+        with torch.cuda.stream(st):
+            ops.embed(ids.reshape(-1), w.embed, x_all)
+            for l in range(a.layers):
+                L = w.layers[l]
+                W = dict(L)
+                if l >= w.place.dense_layers:  # the layer's attention (+ shared experts) blob
+                    w.dense_bufs[0].copy_(w.host_dense[l], non_blocking=True)
+                    W.update(w.dense_views(0))
+                if l == 0:
+                    ops.add_rmsnorm(x_all, W["ln1"], a.rms_eps, h_all)
+                nxt = w.layers[l + 1]["ln1"] if l + 1 < a.layers else w.final_norm
+                dense_mlp = self.mla and l < a.first_k_dense
+                for s0 in range(0, B, Bp):
+                    n = min(Bp, B - s0)
+                    t0, t1 = s0 * P, (s0 + n) * P
+                    x, h, o = x_all[t0:t1], h_all[t0:t1], S["o"][:t1 - t0]
+                    att = (self._prefill_attention_mla if self.mla else self._prefill_attention_gqa)(
+                        l, W, S, s0, n, P, h)
+                    torch.mm(att, W["wo"].t(), out=o)
+                    ops.add_rmsnorm(x, W["ln2"], a.rms_eps, h, delta=o, x_out=x)
+                    t = t1 - t0
+                    if dense_mlp:
+                        torch.mm(h, W["dense_gate_up"][0].t(), out=S["de_gu"][:t])
+                        ops.silu_mul(S["de_gu"][:t], S["de_h"][:t])
+                        torch.mm(S["de_h"][:t], W["dense_down"][0].t(), out=o)
+                        ops.add_rmsnorm(x, nxt, a.rms_eps, h, delta=o, x_out=x)
+                    elif self.mla:
+                        torch.mm(h, W["sh_gate_up"][0].t(), out=S["sh_gu"][:t])
+                        ops.silu_mul(S["sh_gu"][:t], S["sh_h"][:t])
+                        torch.mm(S["sh_h"][:t], W["sh_down"][0].t(), out=sh_all[t0:t1])
+                if dense_mlp:
+                    continue
+                lg.copy_(torch.mm(h_all, W["router"].t(), out_dtype=torch.float32))
+                ops.router_topk(None, None, ws, k, a.router_mode, a.routed_scaling, a.n_group, a.topk_group,
+                                logits_in=lg)
+                ops.permute(h_all, ws, xp)
+                offs = ws.offsets.cpu().tolist()  # host sync once per layer: per-expert row ranges
+                n_c = w.place.experts_per_layer[l]
+                need = max(offs[e + 1] - offs[e] for e in range(E))
+                if hf.shape[0] < need:
+                    hf = torch.empty(need, f, **bf)
+                u = 0  # uncached experts streamed so far in this layer
+                for e in range(E):
+                    r0, r1 = offs[e], offs[e + 1]
+                    if e < n_c:
+                        gu, dn = L["w_gate_up"][e:e + 1], L["w_down"][e:e + 1]
+                    else:  # stream expert e into slot u % 2 while the GPU works on the previous one
+                        sl = u % 2
+                        cp.wait_event(slot_free[sl])
+                        with torch.cuda.stream(cp):
+                            w.slots[sl].copy_(w.host_experts[l][e - n_c], non_blocking=True)
+                            landed[sl].record(cp)
+                        st.wait_event(landed[sl])
+                        gu, dn = w.slot_views(sl)
+                    if r1 > r0:
+                        lo = torch.tensor([0, r1 - r0], dtype=torch.int32, device=self.device)
+                        ops.moe_gemm_gate_up(gu, xp[r0:r1], lo, hf[:r1 - r0])
+                        ops.moe_gemm_down(dn, hf[:r1 - r0], lo, yp[r0:r1])
+                    if e >= n_c:
+                        slot_free[u % 2].record(st)
+                        u += 1
+                ops.unpermute_combine(yp, ws, x_all, T, residual=x_all, shared_out=sh_all, norm_w=nxt,
+                                      eps=a.rms_eps, norm_out=h_all)
+            last = h_all.view(B, P, d)[:, P - 1].contiguous()
+            torch.mm(last, w.lm_head.t(), out=b.logits)
+            ops.argmax(b.logits, b.next_ids)
+            b.positions.fill_(P)
+            b.seq_lens.fill_(P)
+            b.step.fill_(P)
+            self.out_tokens[:, P - 1].copy_(b.next_ids)
+        torch.cuda.current_stream().wait_stream(st)
         self.host_pos = P
         return b.next_ids.to("cpu", torch.int64)
 

@@ -37,6 +37,7 @@ ap.add_argument("--host-gb", type=float, default=170.0, help="host memory the pl
 ap.add_argument("--reserve-gb", type=float, default=10.0)
 ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--out", default=None)
+ap.add_argument("--prefill", action="store_true", help="also time Engine.prefill of B x 512 random prompts")
 args = ap.parse_args()
 
 
@@ -115,6 +116,14 @@ out = {
     "h2d_gbs_achieved": moved / t / 1e9, "h2d_gbs_memcpy_peak": h2d_gbs, "h2d_frac_of_link": moved / t / 1e9 / h2d_gbs,
     "overlap": overlap, "eager_trace_overlap": rep["overlap"], "setup_s": setup_s,
 }
+if args.prefill:
+    ids = torch.randint(0, arch.vocab, (B, 512), generator=torch.Generator().manual_seed(0))
+    torch.cuda.synchronize()
+    t0 = time.time()
+    eng.prefill(ids)
+    torch.cuda.synchronize()
+    tp = time.time() - t0
+    out.update(prefill_s=tp, prefill_prompt_tokens_per_s=B * 512 / tp)
 print(json.dumps(out))
 if args.out:
     with open(args.out, "w") as f:
