@@ -964,7 +964,7 @@ class Engine:
         -> LM head on each sequence's last position.  Leaves every sequence at position P with its
         first generated token in next_ids (and out_tokens[:, P-1]); returns it (host int64 [B])."""
         if not self.can_prefill():
-            raise NotImplementedError("batched prefill is not built for the expert-parallel engine")
+            raise NotImplementedError("batched prefill is not available for this engine configuration (see can_prefill)")
         a, b = self.arch, self.buf
         B, P = input_ids.shape
         assert B == self.B and 1 <= P <= self.max_ctx
