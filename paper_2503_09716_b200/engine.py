@@ -19,6 +19,7 @@ CUDA graph and replayed per generated token, so the host issues one launch per t
 from __future__ import annotations
 
 import json
+import os
 import math
 import time
 from dataclasses import dataclass
@@ -230,7 +231,7 @@ class Engine:
         self.out_tokens = torch.zeros(B, max(1, self.max_ctx), dtype=torch.int64, device=device)
         self.graph: torch.cuda.CUDAGraph | None = None
         self.debug_taps: dict | None = None
-        self.router_logits = "cublas"  # or "fused": gate GEMV inside mgb_router_topk
+        self.router_logits = os.environ.get("MGB_ROUTER_LOGITS", "cublas")  # or "fused": GEMV in mgb_router_topk
         self.logits_r = torch.zeros(B, a.n_experts, dtype=torch.float32, device=device)
         self.stream = torch.cuda.Stream(device=device)
         self.streaming = self.offload or kv_policy == "offload"
