@@ -23,12 +23,13 @@
 // so a page is one contiguous cp.async.bulk and both GEMMs run on tcgen05 with fp32 accumulators in
 // TMEM ("swap-AB": tokens / latent dims fill the MMA M side, the 16 heads of a work item are N).
 //
-// Persistent kernel, one CTA per SM, 6 warps:
-//   warp 4  producer: streams the pages of every work item through a 3-stage smem ring, and Q
-//   warp 5  MMA issuer (one elected lane): S^T of each page and P.V of each softmaxed page, issued
+// Persistent kernel, one CTA per SM, 10 warps:
+//   warp 8  producer: streams the pages of every work item through a 3-stage smem ring, and Q
+//   warp 9  MMA issuer (one elected lane): S^T of each page and P.V of each softmaxed page, issued
 //           as each becomes ready (double-buffered TMEM accumulators)
-//   warps 0-3 softmax + correction: TMEM -> registers (lane = token), per-head online softmax with a
-//           warp transpose-reduction, P^T -> smem, O accumulated in registers (lane = latent dim)
+//   warps 0-7 softmax + correction, two groups of four (heads 0-7, heads 8-15): TMEM -> registers
+//           (lane = token), per-head online softmax with a warp transpose-reduction, P^T -> smem,
+//           O accumulated in registers (lane = latent dim)
 // A work item is (sequence, 16-head group); heads >= H are zero rows of Q and never stored.
 #include <cstdlib>
 
@@ -51,7 +52,7 @@ constexpr int kMlaTile = 64;     // M of the S^T MMA / K of P.V: a page plus 8 p
 constexpr int kMlaStages = MGB_MLA_STAGES;  // pages in flight per SM (3 x 63 KB for R = 512)
 static_assert(kMlaPage % 8 == 0 && kMlaPage <= 64, "latent page = whole swizzle atoms within one MMA tile");
 constexpr int kMlaHeads = 16;    // heads per work item = N of both MMAs
-constexpr int kMlaThreads = 192;
+constexpr int kMlaThreads = 320;  // 8 softmax warps + producer + MMA issuer
 
 // Optional per-page timeline of CTA 0 (build with -DMGB_MLA_TRACE; tools/mla_trace.py):
 // trace[ev * kTraceN + page] = %globaltimer (ns) of event ev for the CTA's page number `page`.
@@ -69,7 +70,8 @@ MGB_DEVINL void mla_trace(int ev, int page) {
 MGB_DEVINL void mla_trace(int, int) {}
 #endif
 
-MGB_DEVINL void cons_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+// named barrier of one softmax warp group (ids 1, 2; 128 threads); 0 is __syncthreads
+MGB_DEVINL void grp_bar(int grp) { asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory"); }
 
 template <int R, int RP>  // latent width, rope width
 struct MlaCfg {
@@ -101,22 +103,24 @@ struct MlaCfg {
   static_assert(kSmem <= 227 * 1024, "MLA smem");
 };
 
-// Reduce 16 per-head values over the 16 lanes of each half-warp (max or sum); lane l ends with
-// head (l & 15).  15 shuffles instead of 64 by halving the vector at every step.
+// Reduce 8 per-head values over the 16 lanes of each half-warp (max or sum); afterwards lane l holds
+// head (l >> 1) & 7 (both lanes of a pair agree).  7 shuffles by halving, then one pairwise step.
 template <bool kMax>
-MGB_DEVINL float xreduce16(float (&v)[16], int lane) {
+MGB_DEVINL float xreduce8(float (&v)[8], int lane) {
 #pragma unroll
-  for (int o = 8; o >= 1; o >>= 1) {
+  for (int o = 8; o >= 2; o >>= 1) {
     const bool hi = lane & o;
+    const int half = o >> 1;  // 8 values -> 4 -> 2 -> 1
 #pragma unroll
-    for (int i = 0; i < o; ++i) {
-      const float keep = hi ? v[i + o] : v[i];
-      const float send = hi ? v[i] : v[i + o];
+    for (int i = 0; i < half; ++i) {
+      const float keep = hi ? v[i + half] : v[i];
+      const float send = hi ? v[i] : v[i + half];
       const float got = __shfl_xor_sync(0xffffffffu, send, o);
       v[i] = kMax ? fmaxf(keep, got) : keep + got;
     }
   }
-  return v[0];
+  const float got = __shfl_xor_sync(0xffffffffu, v[0], 1);
+  return kMax ? fmaxf(v[0], got) : v[0] + got;
 }
 
 template <int R, int RP>
@@ -153,20 +157,20 @@ decode_attn_mla_kernel(const __grid_constant__ CUtensorMap tm_qlat,  // q_lat [H
     mbar_init(qempty, 1);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&sfull[s], 1);
-      mbar_init(&sempty[s], 4);
-      mbar_init(&pfull[s], 4);
+      mbar_init(&sempty[s], 8);
+      mbar_init(&pfull[s], 8);
       mbar_init(&ofull[s], 1);
-      mbar_init(&oempty[s], 4);
+      mbar_init(&oempty[s], 8);
     }
     fence_mbar_init();
   }
-  if (warp == 5) tmem_alloc<C::kTmemCols>(tmem_slot);
+  if (warp == 9) tmem_alloc<C::kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 4) {
+  if (warp == 8) {
     // ------------------------------ producer ------------------------------
     // lane 0 streams pages through the 3-stage ring; lane 1 refills the single Q buffer as soon as
     // the previous item's last S^T has consumed it (the two lanes wait independently).
@@ -231,7 +235,7 @@ decode_attn_mla_kernel(const __grid_constant__ CUtensorMap tm_qlat,  // q_lat [H
         ++qi;
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == 9) {
     // ------------------------------ MMA issuer ------------------------------
     // Two independent in-order streams: S^T of page g needs page g in smem; P.V of page t needs
     // the softmax warps' P_t.  The warp polls both and issues whichever is ready, so a late page
@@ -305,24 +309,31 @@ decode_attn_mla_kernel(const __grid_constant__ CUtensorMap tm_qlat,  // q_lat [H
     }
   } else {
     // ------------------------- softmax + correction -------------------------
-    const int tid = threadIdx.x;  // 0..127
-    const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+    // Eight warps: warp w reads TMEM lane quarter w % 4 (tokens 16*(w%4) .. +15 of the page) for the
+    // eight heads of group w / 4.  Heads are independent, so the two groups never combine state;
+    // splitting them halves every warp's per-page softmax chain and puts two warps on each
+    // scheduler to hide its latencies.
+    constexpr int HG = kMlaHeads / 2;  // heads per warp group
+    const int q = warp & 3, grp = warp >> 2;
+    const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
+    const uint32_t col0 = grp * HG;     // first TMEM column of the group's heads in S / O tiles
+    float* gred = red;  // [2][4][16] row maxima; this group owns heads [col0, col0 + HG)
     int g = 0;
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
       const int b = it / n_hg, hg = it - b * n_hg;
       const int len = seq_lens[b];
-      if (tid == 0) mla_trace(12, g);  // 12: next item's length loaded
+      if (threadIdx.x == 0) mla_trace(12, g);  // 12: next item's length loaded
       const int np = (len + kMlaPage - 1) / kMlaPage;
       if (np == 0) {
-        for (int i = tid; i < kMlaHeads * R; i += 128) {
+        for (int i = threadIdx.x; i < kMlaHeads * R; i += 256) {
           const int h = hg * kMlaHeads + i / R;
           if (h < H) o_lat[((size_t)h * B + b) * R + i % R] = __float2bfloat16_rn(0.f);
         }
         continue;
       }
-      float m_run[16], lpart[16], alpha_prev[16], O[C::MT][16];
+      float m_run[HG], lpart[HG], alpha_prev[HG], O[C::MT][HG];
 #pragma unroll
-      for (int h = 0; h < 16; ++h) {
+      for (int h = 0; h < HG; ++h) {
         m_run[h] = -INFINITY;
         lpart[h] = 0.f;
         alpha_prev[h] = 0.f;
@@ -334,9 +345,9 @@ decode_attn_mla_kernel(const __grid_constant__ CUtensorMap tm_qlat,  // q_lat [H
         mbar_wait(&ofull[s], (t >> 1) & 1);
         if (threadIdx.x == 0) mla_trace(5, t);  // 5: P.V of page t done (O pulled)
         tc_fence_after();
-        uint32_t v[C::MT][16];
+        uint32_t v[C::MT][HG];
 #pragma unroll
-        for (int mt = 0; mt < C::MT; ++mt) tmem_ld16(trow + C::kOCol + (s * C::MT + mt) * 16, v[mt]);
+        for (int mt = 0; mt < C::MT; ++mt) tmem_ld8(trow + C::kOCol + (s * C::MT + mt) * 16 + col0, v[mt]);
         tmem_ld_wait();
         tc_fence_before();
         __syncwarp();
@@ -344,106 +355,98 @@ decode_attn_mla_kernel(const __grid_constant__ CUtensorMap tm_qlat,  // q_lat [H
 #pragma unroll
         for (int mt = 0; mt < C::MT; ++mt)
 #pragma unroll
-          for (int h = 0; h < 16; ++h) O[mt][h] = fmaf(O[mt][h], alpha_prev[h], __uint_as_float(v[mt][h]));
+          for (int h = 0; h < HG; ++h) O[mt][h] = fmaf(O[mt][h], alpha_prev[h], __uint_as_float(v[mt][h]));
       };
 
       for (int p = 0; p < np; ++p, ++g) {
         const int s = g & 1, st = g % kMlaStages;
         const int n = min(kMlaPage, len - p * kMlaPage);
         mbar_wait(&sfull[s], (g >> 1) & 1);
-        if (tid == 0) mla_trace(3, g);  // 3: S ready at the softmax warps
+        if (threadIdx.x == 0) mla_trace(3, g);  // 3: S ready at the softmax warps
         tc_fence_after();
-        uint32_t sv[C::kSAcc][16];
+        uint32_t sv[C::kSAcc][HG];
 #pragma unroll
-        for (int j = 0; j < C::kSAcc; ++j) tmem_ld16(trow + C::kSCol + (s * C::kSAcc + j) * 16, sv[j]);
+        for (int j = 0; j < C::kSAcc; ++j) tmem_ld8(trow + C::kSCol + (s * C::kSAcc + j) * 16 + col0, sv[j]);
         tmem_ld_wait();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sempty[s]);
-        // M = 64 accumulator: token 16*warp + lane sits in TMEM lane 32*warp + lane (lanes < 16)
-        const int tok = warp * 16 + lane;
+        // M = 64 accumulator: token 16*q + lane sits in TMEM lane 32*q + lane (lanes < 16)
+        const int tok = q * 16 + lane;
         const bool valid = lane < 16 && tok < n;
-        float x[16], r[16];
+        float x[HG], r[HG];
 #pragma unroll
-        for (int h = 0; h < 16; ++h) {
+        for (int h = 0; h < HG; ++h) {
           float acc = __uint_as_float(sv[0][h]);
 #pragma unroll
           for (int j = 1; j < C::kSAcc; ++j) acc += __uint_as_float(sv[j][h]);
           x[h] = valid ? acc * scale_log2 : -INFINITY;
           r[h] = x[h];
         }
-        const float wmax = xreduce16<true>(r, lane);
-        if (lane < 16) red[(s * 4 + warp) * 16 + lane] = wmax;
-        cons_bar();
-        float alpha[16], pv[16];
+        const float wmax = xreduce8<true>(r, lane);  // lane l (< 16, even) holds head (l >> 1) & 7
+        if (lane < 16 && !(lane & 1)) gred[(s * 4 + q) * 16 + col0 + (lane >> 1)] = wmax;
+        grp_bar(grp);
+        float alpha[HG], pv[HG];
 #pragma unroll
-        for (int h = 0; h < 16; ++h) {
-          const float* rr = red + s * 64 + h;
+        for (int h = 0; h < HG; ++h) {
+          const float* rr = gred + s * 64 + col0 + h;
           const float m_new = fmaxf(fmaxf(m_run[h], fmaxf(rr[0], rr[16])), fmaxf(rr[32], rr[48]));
           alpha[h] = exp2f(m_run[h] - m_new);
           m_run[h] = m_new;
           pv[h] = exp2f(x[h] - m_new);
           lpart[h] = fmaf(lpart[h], alpha[h], pv[h]);
         }
-        if (lane < 16) {
-          uint8_t* pd = p_s + s * C::kPBytes;
-          *reinterpret_cast<uint4*>(pd + tok * 16) = make_uint4(
-              pack_bf16x2(pv[0], pv[1]), pack_bf16x2(pv[2], pv[3]), pack_bf16x2(pv[4], pv[5]), pack_bf16x2(pv[6], pv[7]));
-          *reinterpret_cast<uint4*>(pd + (kMlaTile + tok) * 16) =
-              make_uint4(pack_bf16x2(pv[8], pv[9]), pack_bf16x2(pv[10], pv[11]), pack_bf16x2(pv[12], pv[13]),
-                         pack_bf16x2(pv[14], pv[15]));
+        if (lane < 16) {  // P^T layout [2 head groups][64 tok][8 heads]
+          uint8_t* pd = p_s + s * C::kPBytes + (grp * kMlaTile + tok) * 16;
+          *reinterpret_cast<uint4*>(pd) = make_uint4(pack_bf16x2(pv[0], pv[1]), pack_bf16x2(pv[2], pv[3]),
+                                                     pack_bf16x2(pv[4], pv[5]), pack_bf16x2(pv[6], pv[7]));
         }
         if (n < kMlaPage) {  // rows past the sequence end: P = 0, and V must not hold NaN/Inf
           const int tail = kMlaPage - n;
           uint8_t* pg = pages + st * C::kPageBytes + n * 128;  // token rows are contiguous 128 B
-          for (int i = tid; i < tail * 8 * C::NKB; i += 128) {  // (P.V's phantom rows alias the next block)
-            const int kb = i / (tail * 8), r = i - kb * tail * 8;
-            *reinterpret_cast<uint4*>(pg + kb * C::kBlockBytes + r * 16) = make_uint4(0, 0, 0, 0);
+          for (int i = threadIdx.x; i < tail * 8 * C::NKB; i += 256) {  // (P.V's phantom rows alias the next block)
+            const int kb = i / (tail * 8), rr = i - kb * tail * 8;
+            *reinterpret_cast<uint4*>(pg + kb * C::kBlockBytes + rr * 16) = make_uint4(0, 0, 0, 0);
           }
         }
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&pfull[s]);
-        if (lane == 0) mla_trace(warp == 0 ? 4 : 5 + warp, g);  // 4, 6, 7, 8: P written by warp 0..3
+        if (threadIdx.x == 0) mla_trace(4, g);  // 4: P written (warp 0)
         if (p > 0) accumulate_o(g - 1);
 #pragma unroll
-        for (int h = 0; h < 16; ++h) alpha_prev[h] = alpha[h];
+        for (int h = 0; h < HG; ++h) alpha_prev[h] = alpha[h];
       }
       accumulate_o(g - 1);
-      if (tid == 0) mla_trace(9, g - 1);  // 9: item's last O pulled
+      if (threadIdx.x == 0) mla_trace(9, g - 1);  // 9: item's last O pulled
 
-      // ---- normalise and store: lane = latent dim, 16 heads per thread ----
-      const float lsum = xreduce16<false>(lpart, lane);
-      if (tid == 0) mla_trace(13, g - 1);  // 13: l reduced
-      if (lane < 16) lred[warp * 16 + lane] = lsum;
-      cons_bar();
-      if (tid == 0) mla_trace(14, g - 1);  // 14: l shared
-      // the per-item epilogue sits between two items on the softmax warps' critical path, with one
-      // warp per scheduler: 16 independent reciprocals first (approximate: far below bf16 rounding),
-      // then 64 independent scale + convert + store chains
-      float inv[16];
+      // ---- normalise and store: lane = latent dim, the group's 8 heads per thread ----
+      const float lsum = xreduce8<false>(lpart, lane);
+      if (lane < 16 && !(lane & 1)) lred[q * 16 + col0 + (lane >> 1)] = lsum;
+      grp_bar(grp);
+      float inv[HG];
 #pragma unroll
-      for (int h = 0; h < 16; ++h) {
-        const float l = lred[h] + lred[16 + h] + lred[32 + h] + lred[48 + h];
-        inv[h] = l > 0.f ? __fdividef(1.0f, l) : 0.f;
+      for (int h = 0; h < HG; ++h) {
+        const int c = col0 + h;
+        const float l = lred[c] + lred[16 + c] + lred[32 + c] + lred[48 + c];
+        inv[h] = l > 0.f ? __fdividef(1.0f, l) : 0.f;  // approximate: far below bf16 rounding
       }
 #pragma unroll
-      for (int h = 0; h < 16; ++h) {
-        const int hh = hg * kMlaHeads + h;
+      for (int h = 0; h < HG; ++h) {
+        const int hh = hg * kMlaHeads + col0 + h;
         if (hh < H) {
-          __nv_bfloat16* dst = o_lat + ((size_t)hh * B + b) * R + warp * 32 + lane;
+          __nv_bfloat16* dst = o_lat + ((size_t)hh * B + b) * R + q * 32 + lane;
 #pragma unroll
           for (int mt = 0; mt < C::MT; ++mt) dst[mt * 128] = __float2bfloat16_rn(O[mt][h] * inv[h]);
         }
       }
-      if (tid == 0) mla_trace(10, g - 1);  // 10: O stores issued
-      cons_bar();  // lred reused by the next item
-      if (tid == 0) mla_trace(11, g - 1);  // 11: item epilogue done
+      if (threadIdx.x == 0) mla_trace(10, g - 1);  // 10: O stores issued
+      grp_bar(grp);  // lred reused by the next item
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) {
+  if (warp == 9) {
     tc_fence_after();
     tmem_dealloc<C::kTmemCols>(tmem);
   }

@@ -258,6 +258,13 @@ MGB_DEVINL uint64_t make_sdesc_sw128_mn(uint32_t smem_addr, uint32_t lbo, uint32
   return d;
 }
 
+// 32 lanes x 8 columns of fp32 from TMEM -> 8 registers per thread.
+MGB_DEVINL void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
+
 // 32 lanes x 16 columns of fp32 from TMEM -> 16 registers per thread.
 MGB_DEVINL void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile(
