@@ -243,7 +243,7 @@ int launch_gqa(const void* q, const void* kc, const void* vc, const int* bt, int
       reinterpret_cast<const __nv_bfloat16*>(q), reinterpret_cast<const __nv_bfloat16*>(kc),
       reinterpret_cast<const __nv_bfloat16*>(vc), bt, max_pages, lens, B, Hkv, scale * 1.4426950408889634f,
       reinterpret_cast<__nv_bfloat16*>(out));
-  return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
+  return mgb_host::launch_status();
 }
 
 }  // namespace mgb

@@ -19,7 +19,9 @@
 // (masked to P = 0).  56-token pages let three stages (189 KB) fit in shared memory, which keeps
 // enough bytes in flight per SM while a page is held for S^T -> softmax -> P.V.  The swizzle keeps
 // the tensor cores' shared-memory reads conflict free; R + r is padded to a multiple of 64 in the
-// page, and the padding is never read.
+// page, and the append kernels write the padding of every token row as zeros (it is a K column of
+// the S^T MMA against Q's zero padding, so it must be finite; rows past a sequence's length may
+// hold anything).
 // so a page is one contiguous cp.async.bulk and both GEMMs run on tcgen05 with fp32 accumulators in
 // TMEM ("swap-AB": tokens / latent dims fill the MMA M side, the 16 heads of a work item are N).
 //
@@ -489,7 +491,7 @@ int launch_mla(const void* q_lat, const void* q_pe, const void* cache, const int
   decode_attn_mla_kernel<R, RP><<<grid, kMlaThreads, C::kSmem, st>>>(
       tq, tp, reinterpret_cast<const __nv_bfloat16*>(cache), bt, max_pages, lens, B, H, scale * 1.4426950408889634f,
       reinterpret_cast<__nv_bfloat16*>(out), pf_dist);
-  return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
+  return mgb_host::launch_status();
 }
 
 // Per token: latent RMSNorm (kv_a_layernorm) + interleaved RoPE of the shared k_pe, appended to
@@ -540,6 +542,9 @@ __global__ void mla_append_kernel(const __nv_bfloat16* __restrict__ q,    // [B,
     pg[at(d0)] = __float2bfloat16_rn(x0 * c - x1 * s);
     pg[at(d0 + 1)] = __float2bfloat16_rn(x0 * s + x1 * c);
   }
+  // the row's padding dims [D, DP) are K columns of the S^T MMA (times Q's zero padding): they must
+  // hold finite values, whatever the page held before (0 * NaN would poison the row's scores)
+  for (int i = D + threadIdx.x; i < DP; i += blockDim.x) pg[at(i)] = __float2bfloat16_rn(0.f);
   const int QD = NOPE + RP;
   for (int i = threadIdx.x; i < H * (RP / 2); i += blockDim.x) {  // per-head q_pe
     const int h = i / (RP / 2), j = i - h * (RP / 2);
@@ -605,6 +610,7 @@ __global__ void mla_append_prefill_kernel(__nv_bfloat16* __restrict__ q, const _
     kpe_out[(size_t)t * RP + 2 * i] = a;
     kpe_out[(size_t)t * RP + 2 * i + 1] = b;
   }
+  for (int i = D + threadIdx.x; i < DP; i += blockDim.x) pg[at(i)] = __float2bfloat16_rn(0.f);  // padding
   const int QD = NOPE + RP;
   for (int i = threadIdx.x; i < H * (RP / 2); i += blockDim.x) {  // per-head q_pe, in place
     const int h = i / (RP / 2), j = i - h * (RP / 2);
@@ -645,7 +651,7 @@ int mgb_mla_append(const void* q, const void* ckv, const void* norm_w, float eps
       reinterpret_cast<const __nv_bfloat16*>(norm_w), eps, B, H, R, RP, NOPE, positions, cos_t, sin_t, block_table,
       max_pages, reinterpret_cast<__nv_bfloat16*>(cache), reinterpret_cast<__nv_bfloat16*>(q_nope_out),
       reinterpret_cast<__nv_bfloat16*>(q_pe_out), seq_lens);
-  return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
+  return mgb_host::launch_status();
 }
 
 // Prefill: latent + k_pe of T = n_seq * P prompt tokens into the pages and contiguous rows; q_pe RoPE
@@ -659,7 +665,7 @@ int mgb_mla_append_prefill(void* q, const void* ckv, const void* norm_w, float e
       reinterpret_cast<const __nv_bfloat16*>(norm_w), eps, seq0, P, H, R, RP, NOPE, cos_t, sin_t, block_table, max_pages,
       reinterpret_cast<__nv_bfloat16*>(cache), reinterpret_cast<__nv_bfloat16*>(c_out),
       reinterpret_cast<__nv_bfloat16*>(kpe_out));
-  return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
+  return mgb_host::launch_status();
 }
 
 #ifdef MGB_MLA_TRACE

@@ -377,6 +377,9 @@ MGB_DEVINL uint4 ld_nc_v4(const void* p) {
 
 // Host-side helpers shared by the launchers.
 namespace mgb_host {
+// MGB_OK, or MGB_ECUDA after recording the pending launch error for mgb_last_error (which
+// cudaGetLastError would otherwise consume).
+int launch_status();
 // cuTensorMapEncodeTiled resolved through the runtime's driver entry point (no -lcuda).
 CUresult encode_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
                              uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer);

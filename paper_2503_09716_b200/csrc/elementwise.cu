@@ -311,7 +311,7 @@ int mgb_add_rmsnorm(const void* x, const void* delta, const void* weight, float 
       reinterpret_cast<const __nv_bfloat16*>(x), reinterpret_cast<const __nv_bfloat16*>(delta),
       reinterpret_cast<const __nv_bfloat16*>(weight), eps, d, reinterpret_cast<__nv_bfloat16*>(x_out),
       reinterpret_cast<__nv_bfloat16*>(y));
-  return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
+  return mgb_host::launch_status();
 }
 
 int mgb_rope_append_gqa(const void* qkv, int T, int seq0, const int* positions, const float* cos_t,
@@ -325,7 +325,7 @@ int mgb_rope_append_gqa(const void* qkv, int T, int seq0, const int* positions, 
       reinterpret_cast<const __nv_bfloat16*>(qkv), T, seq0, positions, cos_t, sin_t, Hq, Hkv, head_dim, block_table,
       max_pages, reinterpret_cast<__nv_bfloat16*>(k_cache), reinterpret_cast<__nv_bfloat16*>(v_cache),
       reinterpret_cast<__nv_bfloat16*>(q_out), seq_lens);
-  return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
+  return mgb_host::launch_status();
 }
 
 int mgb_rope_append_gqa_prefill(const void* qkv, int T, int seq0, int P, const float* cos_t, const float* sin_t,
@@ -340,7 +340,7 @@ int mgb_rope_append_gqa_prefill(const void* qkv, int T, int seq0, int P, const f
       reinterpret_cast<__nv_bfloat16*>(k_cache), reinterpret_cast<__nv_bfloat16*>(v_cache),
       reinterpret_cast<__nv_bfloat16*>(q_out), reinterpret_cast<__nv_bfloat16*>(k_out),
       reinterpret_cast<__nv_bfloat16*>(v_out));
-  return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
+  return mgb_host::launch_status();
 }
 
 int mgb_silu_mul(const void* gate_up, int T, int F, void* h, void* stream) {
@@ -348,21 +348,21 @@ int mgb_silu_mul(const void* gate_up, int T, int F, void* h, void* stream) {
   const long long n = (long long)T * (F / 8);
   mgb::silu_mul_kernel<<<(int)((n + 255) / 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<const __nv_bfloat16*>(gate_up), T, F, reinterpret_cast<__nv_bfloat16*>(h));
-  return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
+  return mgb_host::launch_status();
 }
 
 int mgb_embed(const int* ids, const void* table, int T, int d, void* out, void* stream) {
   if (T < 1 || d % 8) return MGB_EINVAL;
   mgb::embed_kernel<<<T, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       ids, reinterpret_cast<const __nv_bfloat16*>(table), d, reinterpret_cast<__nv_bfloat16*>(out));
-  return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
+  return mgb_host::launch_status();
 }
 
 int mgb_argmax(const void* logits, int T, int V, int* out, void* stream) {
   if (T < 1 || V < 1) return MGB_EINVAL;
   mgb::argmax_kernel<<<T, 512, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<const __nv_bfloat16*>(logits), V, out);
-  return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
+  return mgb_host::launch_status();
 }
 
 int mgb_decode_advance(const int* next, int B, long long* out_tokens, int ld, int* step, int* positions,
@@ -370,7 +370,7 @@ int mgb_decode_advance(const int* next, int B, long long* out_tokens, int ld, in
   if (B < 1) return MGB_EINVAL;
   mgb::decode_advance_kernel<<<1, 1024, 0, reinterpret_cast<cudaStream_t>(stream)>>>(next, B, out_tokens, ld, step,
                                                                                      positions);
-  return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
+  return mgb_host::launch_status();
 }
 
 // mode 0: counter-based uniform with standard deviation `std`; mode 1: constant fill.
@@ -384,7 +384,7 @@ int mgb_fill_uniform_bf16(void* out, long long n, unsigned long long seed, unsig
   if (blocks > 148 * 64) blocks = 148 * 64;
   mgb::fill_uniform_kernel<<<(int)blocks, threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<__nv_bfloat16*>(out), (size_t)n, seed, tensor_id, scale, constant, mode);
-  return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
+  return mgb_host::launch_status();
 }
 
 }  // extern "C"

@@ -63,6 +63,17 @@ int num_sms() {
   return n;
 }
 
+namespace {
+cudaError_t g_last_err = cudaSuccess;  // first launch error a libmgb entry point returned MGB_ECUDA for
+}
+
+int launch_status() {
+  const cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) return MGB_OK;
+  g_last_err = e;
+  return MGB_ECUDA;
+}
+
 }  // namespace mgb_host
 
 extern "C" {
@@ -71,7 +82,12 @@ extern "C" {
 int mgb_abi_version(void) { return 1; }
 
 // Name of the last CUDA error seen by the runtime in this library (for loud failures).
-const char* mgb_last_error(void) { return cudaGetErrorString(cudaPeekAtLastError()); }
+// A launch error an entry point already consumed (returned as MGB_ECUDA) is reported, then cleared.
+const char* mgb_last_error(void) {
+  const cudaError_t e = mgb_host::g_last_err != cudaSuccess ? mgb_host::g_last_err : cudaPeekAtLastError();
+  mgb_host::g_last_err = cudaSuccess;
+  return cudaGetErrorString(e);
+}
 
 // Number of SMs of the current device (148 on B200).
 int mgb_num_sms(void) { return mgb_host::num_sms(); }

@@ -61,7 +61,7 @@ int mgb_copy_bytes(void* dst, const void* src, long long nbytes, void* stream) {
   if (blocks > 4 * 148) blocks = 4 * 148;
   mgb::copy_bytes_kernel<<<(int)blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<uint4*>(dst), reinterpret_cast<const uint4*>(src), n16);
-  return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
+  return mgb_host::launch_status();
 }
 
 
@@ -80,7 +80,7 @@ int mgb_kv_token_copy(const void* src, const int* src_table, int src_max_pages, 
                               reinterpret_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<const uint8_t*>(src), src_table, src_max_pages, reinterpret_cast<uint8_t*>(dst), dst_table,
       dst_max_pages, positions, B, page_tokens, page_bytes, unit_bytes, n_units, unit_stride);
-  return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
+  return mgb_host::launch_status();
 }
 
 }  // extern "C"

@@ -524,7 +524,7 @@ int launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, const int* of
         tmA, tmB, offsets, E, MT, K, rows_per_expert, half_rows, reinterpret_cast<__nv_bfloat16*>(out), ldo, balanced,
         row_ptr);
   }
-  return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
+  return mgb_host::launch_status();
 }
 
 // rows_per_unit: weight rows one CTA covers per unit (64 gated / 128 down); the pair kernel

@@ -511,7 +511,7 @@ int mgb_router_topk(const void* x, const void* w_gate, const float* logits_in, i
   if (nblk > mgb::kFusedScanMaxBlocks)
     mgb::router_scan_kernel<<<E, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(block_hist, nblk, E, counts, offsets,
                                                                                    ticket);
-  return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
+  return mgb_host::launch_status();
 }
 
 // Stable expert-major permutation: x_perm[pos] = x[t] for every (t, j), pos = offsets[e] +
@@ -526,7 +526,7 @@ int mgb_permute(const void* x, const int* topk_idx, const int* local_rank, const
   mgb::permute_kernel<<<blocks, threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<const __nv_bfloat16*>(x), topk_idx, local_rank, block_base, offsets, T, d, k, E,
       mgb::kRouterTPB, reinterpret_cast<__nv_bfloat16*>(x_perm), src_token, dst_pos, nullptr, nullptr, 1);
-  return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
+  return mgb_host::launch_status();
 }
 
 // Expert-parallel dispatch fused with the permutation: row (t, j) of expert e = topk_idx[t, j] is
@@ -544,7 +544,7 @@ int mgb_ep_permute_dispatch(const void* x, const int* topk_idx, const int* local
   mgb::permute_kernel<<<blocks, threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<const __nv_bfloat16*>(x), topk_idx, local_rank, block_base, offsets, T, d, k, E,
       mgb::kRouterTPB, nullptr, src_token, dst_pos, peer_base, disp_row, E_local);
-  return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
+  return mgb_host::launch_status();
 }
 
 // Destination of every row of the owner's expert-major receive buffer for the combine send: the
@@ -573,7 +573,7 @@ int mgb_ep_row_ptrs(const int* seg_start, const int* seg_len, const int* seg_del
   if (n_seg < 1 || W < 1 || n_seg % W || row_bytes < 16 || rows_cap < 1) return MGB_EINVAL;
   ep_row_ptrs_kernel<<<(rows_cap + 255) / 256, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       seg_start, seg_len, seg_delta, n_seg, W, peer_base, row_bytes, rows_cap, row_ptr);
-  return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
+  return mgb_host::launch_status();
 }
 
 // Weighted un-permute + combine (fp32, j ascending, one bf16 rounding), optional shared-expert
@@ -590,7 +590,7 @@ int mgb_unpermute_combine(const void* y_perm, const int* dst_pos, const float* t
       reinterpret_cast<const __nv_bfloat16*>(shared_out), reinterpret_cast<const __nv_bfloat16*>(residual), T, d,
       k, reinterpret_cast<__nv_bfloat16*>(out), reinterpret_cast<const __nv_bfloat16*>(norm_w), eps,
       reinterpret_cast<__nv_bfloat16*>(norm_out));
-  return cudaGetLastError() == cudaSuccess ? MGB_OK : MGB_ECUDA;
+  return mgb_host::launch_status();
 }
 
 }  // extern "C"

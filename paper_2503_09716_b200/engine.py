@@ -849,12 +849,8 @@ class Engine:
 
     def can_prefill(self) -> bool:
         """Batched prefill: both families, weights resident (chunk-major) or offloaded (layer-major,
-        `_prefill_streamed`), KV resident or in the host page store (incl. a CPU attention share).
-        Not yet for DeepSeek-V2 with both weights and KV offloaded: there a later decode step faults
-        intermittently (a cross-stream hazard not found yet), so that combination
-        consumes the prompt through the decode step."""
-        if self.mla and self.offload and self.kv_policy == "offload":
-            return False
+        `_prefill_streamed`), KV resident or in the host page store (incl. a CPU attention share);
+        not under expert parallelism (the prompt then goes through the decode step)."""
         return self.ep is None
 
     def _prefill_kv_target(self, l: int, s0: int, n: int):

@@ -15,12 +15,14 @@ BF16 = torch.bfloat16
 TOL = 2e-2
 
 
-def _latent_pages(c, pe, B, ctx, page, pps):
+def _latent_pages(c, pe, B, ctx, page, pps, tail=0.0):
     """dense [B,ctx,R] + [B,ctx,r] -> latent pages [B*pps][ceil(D/64)][page][64] with the 16-byte
-    chunks of every token row 128B-swizzled (chunk j of token t stored at j ^ (t % 8)); attn_mla.cu."""
+    chunks of every token row 128B-swizzled (chunk j of token t stored at j ^ (t % 8)); attn_mla.cu.
+    Rows past ctx hold `tail` (the kernel must ignore them); a row's padding dims are zero."""
     D = c.shape[-1] + pe.shape[-1]
     NKB = (D + 63) // 64
-    full = torch.zeros(B, pps * page, NKB * 64, dtype=BF16)
+    full = torch.full((B, pps * page, NKB * 64), tail, dtype=BF16)
+    full[:, :ctx] = 0
     full[:, :ctx, :D] = torch.cat([c, pe], -1)
     t = torch.arange(page)
     j = torch.arange(8)
@@ -31,18 +33,20 @@ def _latent_pages(c, pe, B, ctx, page, pps):
     return x.contiguous().reshape(-1)
 
 
-@pytest.mark.parametrize("B,H,RL,r,ctx", [(3, 16, 512, 64, 1), (4, 16, 512, 64, 100), (2, 128, 512, 64, 70),
-                                         (5, 4, 128, 32, 33), (2, 20, 512, 64, 64)])
-def test_decode_attn_mla(B, H, RL, r, ctx):
+@pytest.mark.parametrize("B,H,RL,r,ctx,tail", [(3, 16, 512, 64, 1, 0.0), (4, 16, 512, 64, 100, 0.0),
+                                              (2, 128, 512, 64, 70, 0.0), (5, 4, 128, 32, 33, 0.0),
+                                              (2, 20, 512, 64, 64, 0.0), (3, 16, 512, 64, 45, float("nan")),
+                                              (4, 8, 128, 32, 61, float("nan")), (2, 16, 512, 64, 112, float("inf"))])
+def test_decode_attn_mla(B, H, RL, r, ctx, tail):
     from paper_2503_09716_b200 import _native as nat
 
     page = nat.value("mgb_mla_page_size")
-    pps = math.ceil(ctx / page)
+    pps = math.ceil(ctx / page) + (1 if tail != 0.0 else 0)  # + an unused page of garbage
     q_lat = uniform_bf16((H, B, RL), 1, 1, 0.5)
     q_pe = uniform_bf16((B, H, r), 1, 2, 0.5)
     c = uniform_bf16((B, ctx, RL), 1, 3, 1.0)
     pe = uniform_bf16((B, ctx, r), 1, 4, 1.0)
-    cache = _latent_pages(c, pe, B, ctx, page, pps).cuda()
+    cache = _latent_pages(c, pe, B, ctx, page, pps, tail).cuda()
     bt = torch.arange(B * pps, dtype=torch.int32).view(B, pps).cuda()
     lens = torch.full((B,), ctx, dtype=torch.int32).cuda()
     out = torch.zeros(H, B, RL, dtype=BF16, device="cuda")
