@@ -3,6 +3,8 @@
 // generator.  Numerics follow HF transformers 5.5.0 (MixtralRMSNorm, apply_rotary_pos_emb),
 // including every intermediate bf16 rounding, so these match the CPU oracle bit-exactly except
 // for the RMS reduction order.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace mgb {
@@ -77,59 +79,65 @@ add_rmsnorm_kernel(const __nv_bfloat16* x, const __nv_bfloat16* __restrict__ del
   }
 }
 
-// One warp per (token, head) of the fused qkv row [Hq | Hkv | Hkv] x hd.  q heads are rotated
-// into q_out; k heads rotated and written into the chunk-major K page; v heads copied into the
-// row-major V page.  Rotation = HF rotate_half with bf16 products and sum.
+// RoPE of one 16-byte chunk c (8 dims) of a head row: HF rotate_half with bf16 products and sum.
+MGB_DEVINL uint4 rope_chunk(const uint4* src, int c, int nch, const float* cos_row, const float* sin_row) {
+  const uint4 xv = src[c];
+  const int half_ch = nch >> 1;
+  const bool lo = c < half_ch;
+  const uint4 pv = src[lo ? c + half_ch : c - half_ch];
+  const float x[8] = {bf16lo(xv.x), bf16hi(xv.x), bf16lo(xv.y), bf16hi(xv.y),
+                      bf16lo(xv.z), bf16hi(xv.z), bf16lo(xv.w), bf16hi(xv.w)};
+  const float pr[8] = {bf16lo(pv.x), bf16hi(pv.x), bf16lo(pv.y), bf16hi(pv.y),
+                       bf16lo(pv.z), bf16hi(pv.z), bf16lo(pv.w), bf16hi(pv.w)};
+  const int fi0 = (lo ? c : c - half_ch) * 8;
+  const float4 c0 = *reinterpret_cast<const float4*>(cos_row + fi0), c1 = *reinterpret_cast<const float4*>(cos_row + fi0 + 4);
+  const float4 s0 = *reinterpret_cast<const float4*>(sin_row + fi0), s1 = *reinterpret_cast<const float4*>(sin_row + fi0 + 4);
+  const float cs[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+  const float sn[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+  float r[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float rh = lo ? -pr[i] : pr[i];  // rotate_half
+    r[i] = bf16_round(x[i] * cs[i]) + bf16_round(rh * sn[i]);
+  }
+  uint4 ov;
+  ov.x = pack_bf16x2(r[0], r[1]); ov.y = pack_bf16x2(r[2], r[3]);
+  ov.z = pack_bf16x2(r[4], r[5]); ov.w = pack_bf16x2(r[6], r[7]);
+  return ov;
+}
+
+// One CTA per token, one thread per (head, 16-byte chunk) of its fused qkv row [Hq | Hkv | Hkv] x hd
+// (32-bit index arithmetic; the token's position, page and slot are CTA-uniform).  q heads are
+// rotated into q_out; k heads rotated and written into the chunk-major K page; v heads copied into
+// the V page.
 __global__ void rope_append_gqa_kernel(const __nv_bfloat16* __restrict__ qkv, int T, int seq0,
                                        const int* __restrict__ positions, const float* __restrict__ cos_t,
                                        const float* __restrict__ sin_t, int Hq, int Hkv, int hd,
                                        const int* __restrict__ block_table, int max_pages,
                                        __nv_bfloat16* __restrict__ k_cache, __nv_bfloat16* __restrict__ v_cache,
                                        __nv_bfloat16* __restrict__ q_out, int* __restrict__ seq_lens) {
-  // one thread per (token, head, 8-dim chunk): 16 B in, 16 B out
-  const int nch = hd / 8;
-  const int H = Hq + 2 * Hkv;
-  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid >= (long long)T * H * nch) return;
-  const int c = (int)(gid % nch);
-  const long long th = gid / nch;
-  const int t = (int)(th / H), hh = (int)(th - (long long)t * H);
+  const int t = blockIdx.x;
+  const int nch = hd >> 3, H = Hq + 2 * Hkv;
   const int seq = seq0 + t;
   const int pos = positions[seq];
-  const __nv_bfloat16* src = qkv + ((size_t)t * H + hh) * hd;
   const int page = block_table[(size_t)seq * max_pages + pos / kPageTok];
   const int slot = pos % kPageTok;
-  if (seq_lens && hh == 0 && c == 0) seq_lens[seq] = pos + 1;  // cache length after the append
-  const uint4 xv = reinterpret_cast<const uint4*>(src)[c];
-  uint4 ov = xv;
-  if (hh < Hq + Hkv) {
-    const int half_ch = nch / 2;
-    const bool lo = c < half_ch;
-    const uint4 pv = reinterpret_cast<const uint4*>(src)[lo ? c + half_ch : c - half_ch];
-    const float x[8] = {bf16lo(xv.x), bf16hi(xv.x), bf16lo(xv.y), bf16hi(xv.y),
-                        bf16lo(xv.z), bf16hi(xv.z), bf16lo(xv.w), bf16hi(xv.w)};
-    const float pr[8] = {bf16lo(pv.x), bf16hi(pv.x), bf16lo(pv.y), bf16hi(pv.y),
-                         bf16lo(pv.z), bf16hi(pv.z), bf16lo(pv.w), bf16hi(pv.w)};
-    const int fi0 = (lo ? c : c - half_ch) * 8;
-    const float* cs = cos_t + (size_t)pos * (hd / 2) + fi0;
-    const float* sn = sin_t + (size_t)pos * (hd / 2) + fi0;
-    float r[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const float rh = lo ? -pr[i] : pr[i];  // rotate_half
-      r[i] = bf16_round(x[i] * cs[i]) + bf16_round(rh * sn[i]);
+  if (seq_lens && threadIdx.x == 0) seq_lens[seq] = pos + 1;  // cache length after the append
+  const float* cs = cos_t + (size_t)pos * (hd / 2);
+  const float* sn = sin_t + (size_t)pos * (hd / 2);
+  const __nv_bfloat16* row = qkv + (size_t)t * H * hd;
+  for (int i = threadIdx.x; i < H * nch; i += blockDim.x) {
+    const int hh = i / nch, c = i - hh * nch;
+    const uint4* src = reinterpret_cast<const uint4*>(row + hh * hd);
+    const uint4 ov = hh < Hq + Hkv ? rope_chunk(src, c, nch, cs, sn) : src[c];
+    if (hh < Hq) {
+      reinterpret_cast<uint4*>(q_out + ((size_t)t * Hq + hh) * hd)[c] = ov;
+    } else {
+      const bool is_k = hh < Hq + Hkv;
+      const int kh = is_k ? hh - Hq : hh - Hq - Hkv;
+      const size_t blk = ((size_t)page * Hkv + kh) * hd * kPageTok;
+      *reinterpret_cast<uint4*>((is_k ? k_cache : v_cache) + blk + ((size_t)c * kPageTok + slot) * 8) = ov;
     }
-    ov.x = pack_bf16x2(r[0], r[1]); ov.y = pack_bf16x2(r[2], r[3]);
-    ov.z = pack_bf16x2(r[4], r[5]); ov.w = pack_bf16x2(r[6], r[7]);
-  }
-  if (hh < Hq) {
-    reinterpret_cast<uint4*>(q_out + ((size_t)t * Hq + hh) * hd)[c] = ov;
-  } else {
-    const bool is_k = hh < Hq + Hkv;
-    const int kh = is_k ? hh - Hq : hh - Hq - Hkv;
-    const size_t blk = ((size_t)page * Hkv + kh) * hd * kPageTok;
-    __nv_bfloat16* dst = (is_k ? k_cache : v_cache) + blk + ((size_t)c * kPageTok + slot) * 8;
-    *reinterpret_cast<uint4*>(dst) = ov;
   }
 }
 
@@ -143,68 +151,47 @@ __global__ void rope_append_gqa_prefill_kernel(const __nv_bfloat16* __restrict__
                                                int max_pages, __nv_bfloat16* __restrict__ k_cache,
                                                __nv_bfloat16* __restrict__ v_cache, __nv_bfloat16* __restrict__ q_out,
                                                __nv_bfloat16* __restrict__ k_out, __nv_bfloat16* __restrict__ v_out) {
-  const int nch = hd / 8;
-  const int H = Hq + 2 * Hkv;
-  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid >= (long long)T * H * nch) return;
-  const int c = (int)(gid % nch);
-  const long long th = gid / nch;
-  const int t = (int)(th / H), hh = (int)(th - (long long)t * H);
-  const int seq = seq0 + t / P;
-  const int pos = t % P;
-  const __nv_bfloat16* src = qkv + ((size_t)t * H + hh) * hd;
-  const uint4 xv = reinterpret_cast<const uint4*>(src)[c];
-  uint4 ov = xv;
-  if (hh < Hq + Hkv) {
-    const int half_ch = nch / 2;
-    const bool lo = c < half_ch;
-    const uint4 pv = reinterpret_cast<const uint4*>(src)[lo ? c + half_ch : c - half_ch];
-    const float x[8] = {bf16lo(xv.x), bf16hi(xv.x), bf16lo(xv.y), bf16hi(xv.y),
-                        bf16lo(xv.z), bf16hi(xv.z), bf16lo(xv.w), bf16hi(xv.w)};
-    const float pr[8] = {bf16lo(pv.x), bf16hi(pv.x), bf16lo(pv.y), bf16hi(pv.y),
-                         bf16lo(pv.z), bf16hi(pv.z), bf16lo(pv.w), bf16hi(pv.w)};
-    const int fi0 = (lo ? c : c - half_ch) * 8;
-    const float* cs = cos_t + (size_t)pos * (hd / 2) + fi0;
-    const float* sn = sin_t + (size_t)pos * (hd / 2) + fi0;
-    float r[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const float rh = lo ? -pr[i] : pr[i];  // rotate_half
-      r[i] = bf16_round(x[i] * cs[i]) + bf16_round(rh * sn[i]);
+  const int t = blockIdx.x;
+  const int nch = hd >> 3, H = Hq + 2 * Hkv;
+  const int seq = seq0 + t / P, pos = t % P;
+  const int page = block_table[(size_t)seq * max_pages + pos / kPageTok];
+  const int slot = pos % kPageTok;
+  const float* cs = cos_t + (size_t)pos * (hd / 2);
+  const float* sn = sin_t + (size_t)pos * (hd / 2);
+  const __nv_bfloat16* row = qkv + (size_t)t * H * hd;
+  for (int i = threadIdx.x; i < H * nch; i += blockDim.x) {
+    const int hh = i / nch, c = i - hh * nch;
+    const uint4* src = reinterpret_cast<const uint4*>(row + hh * hd);
+    const uint4 ov = hh < Hq + Hkv ? rope_chunk(src, c, nch, cs, sn) : src[c];
+    if (hh < Hq) {
+      reinterpret_cast<uint4*>(q_out + ((size_t)t * Hq + hh) * hd)[c] = ov;
+    } else {
+      const bool is_k = hh < Hq + Hkv;
+      const int kh = is_k ? hh - Hq : hh - Hq - Hkv;
+      const size_t blk = ((size_t)page * Hkv + kh) * hd * kPageTok;
+      *reinterpret_cast<uint4*>((is_k ? k_cache : v_cache) + blk + ((size_t)c * kPageTok + slot) * 8) = ov;
+      reinterpret_cast<uint4*>((is_k ? k_out : v_out) + ((size_t)t * Hkv + kh) * hd)[c] = ov;
     }
-    ov.x = pack_bf16x2(r[0], r[1]); ov.y = pack_bf16x2(r[2], r[3]);
-    ov.z = pack_bf16x2(r[4], r[5]); ov.w = pack_bf16x2(r[6], r[7]);
-  }
-  if (hh < Hq) {
-    reinterpret_cast<uint4*>(q_out + ((size_t)t * Hq + hh) * hd)[c] = ov;
-  } else {
-    const bool is_k = hh < Hq + Hkv;
-    const int kh = is_k ? hh - Hq : hh - Hq - Hkv;
-    const int page = block_table[(size_t)seq * max_pages + pos / kPageTok];
-    const size_t blk = ((size_t)page * Hkv + kh) * hd * kPageTok;
-    __nv_bfloat16* dst = (is_k ? k_cache : v_cache) + blk + ((size_t)c * kPageTok + pos % kPageTok) * 8;
-    *reinterpret_cast<uint4*>(dst) = ov;
-    reinterpret_cast<uint4*>((is_k ? k_out : v_out) + ((size_t)t * Hkv + kh) * hd)[c] = ov;
   }
 }
 
 // h = bf16(bf16(silu(g)) * u) for gu = [g | u] rows (HF DeepseekV2MLP / MixtralExperts act-mul on the
 // bf16 outputs of a cuBLAS gate|up GEMM).  8 features per thread, 16 B in/out.
 __global__ void silu_mul_kernel(const __nv_bfloat16* __restrict__ gu, int T, int F, __nv_bfloat16* __restrict__ h) {
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const int nv = F / 8;
-  if (i >= (long long)T * nv) return;
-  const int t = (int)(i / nv), c = (int)(i - (long long)t * nv);
-  const uint4 g = reinterpret_cast<const uint4*>(gu + (size_t)t * 2 * F)[c];
-  const uint4 u = reinterpret_cast<const uint4*>(gu + (size_t)t * 2 * F + F)[c];
-  const float gf[8] = {bf16lo(g.x), bf16hi(g.x), bf16lo(g.y), bf16hi(g.y), bf16lo(g.z), bf16hi(g.z), bf16lo(g.w), bf16hi(g.w)};
-  const float uf[8] = {bf16lo(u.x), bf16hi(u.x), bf16lo(u.y), bf16hi(u.y), bf16lo(u.z), bf16hi(u.z), bf16lo(u.w), bf16hi(u.w)};
-  float r[8];
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;  // 16-byte chunk of the row
+  if (c >= F / 8) return;
+  for (int t = blockIdx.y; t < T; t += gridDim.y) {  // tokens on grid.y (32-bit index arithmetic)
+    const uint4 g = reinterpret_cast<const uint4*>(gu + (size_t)t * 2 * F)[c];
+    const uint4 u = reinterpret_cast<const uint4*>(gu + (size_t)t * 2 * F + F)[c];
+    const float gf[8] = {bf16lo(g.x), bf16hi(g.x), bf16lo(g.y), bf16hi(g.y), bf16lo(g.z), bf16hi(g.z), bf16lo(g.w), bf16hi(g.w)};
+    const float uf[8] = {bf16lo(u.x), bf16hi(u.x), bf16lo(u.y), bf16hi(u.y), bf16lo(u.z), bf16hi(u.z), bf16lo(u.w), bf16hi(u.w)};
+    float r[8];
 #pragma unroll
-  for (int j = 0; j < 8; ++j) r[j] = bf16_round(__fdividef(gf[j], 1.0f + __expf(-gf[j]))) * uf[j];
-  uint4 o;
-  o.x = pack_bf16x2(r[0], r[1]); o.y = pack_bf16x2(r[2], r[3]); o.z = pack_bf16x2(r[4], r[5]); o.w = pack_bf16x2(r[6], r[7]);
-  reinterpret_cast<uint4*>(h + (size_t)t * F)[c] = o;
+    for (int j = 0; j < 8; ++j) r[j] = bf16_round(__fdividef(gf[j], 1.0f + __expf(-gf[j]))) * uf[j];
+    uint4 o;
+    o.x = pack_bf16x2(r[0], r[1]); o.y = pack_bf16x2(r[2], r[3]); o.z = pack_bf16x2(r[4], r[5]); o.w = pack_bf16x2(r[6], r[7]);
+    reinterpret_cast<uint4*>(h + (size_t)t * F)[c] = o;
+  }
 }
 
 __global__ void embed_kernel(const int* __restrict__ ids, const __nv_bfloat16* __restrict__ table, int d,
@@ -314,13 +301,16 @@ int mgb_add_rmsnorm(const void* x, const void* delta, const void* weight, float 
   return mgb_host::launch_status();
 }
 
+namespace {
+int rope_threads(int H, int hd) { return std::min(1024, (H * (hd / 8) + 31) / 32 * 32); }
+}  // namespace
+
 int mgb_rope_append_gqa(const void* qkv, int T, int seq0, const int* positions, const float* cos_t,
                         const float* sin_t, int Hq, int Hkv, int head_dim, const int* block_table, int max_pages,
                         void* k_cache, void* v_cache, void* q_out, int* seq_lens, void* stream) {
   if (T < 1 || head_dim % 16 || Hq % Hkv) return MGB_EINVAL;
-  const long long items = (long long)T * (Hq + 2 * Hkv) * (head_dim / 8);
-  const int threads = 256;
-  mgb::rope_append_gqa_kernel<<<(int)((items + threads - 1) / threads), threads, 0,
+  const int threads = rope_threads(Hq + 2 * Hkv, head_dim);
+  mgb::rope_append_gqa_kernel<<<T, threads, 0,
                                 reinterpret_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<const __nv_bfloat16*>(qkv), T, seq0, positions, cos_t, sin_t, Hq, Hkv, head_dim, block_table,
       max_pages, reinterpret_cast<__nv_bfloat16*>(k_cache), reinterpret_cast<__nv_bfloat16*>(v_cache),
@@ -332,9 +322,8 @@ int mgb_rope_append_gqa_prefill(const void* qkv, int T, int seq0, int P, const f
                                 int Hq, int Hkv, int head_dim, const int* block_table, int max_pages, void* k_cache,
                                 void* v_cache, void* q_out, void* k_out, void* v_out, void* stream) {
   if (T < 1 || P < 1 || T % P || head_dim % 16 || Hq % Hkv) return MGB_EINVAL;
-  const long long items = (long long)T * (Hq + 2 * Hkv) * (head_dim / 8);
-  const int threads = 256;
-  mgb::rope_append_gqa_prefill_kernel<<<(int)((items + threads - 1) / threads), threads, 0,
+  const int threads = rope_threads(Hq + 2 * Hkv, head_dim);
+  mgb::rope_append_gqa_prefill_kernel<<<T, threads, 0,
                                         reinterpret_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<const __nv_bfloat16*>(qkv), T, seq0, P, cos_t, sin_t, Hq, Hkv, head_dim, block_table, max_pages,
       reinterpret_cast<__nv_bfloat16*>(k_cache), reinterpret_cast<__nv_bfloat16*>(v_cache),
@@ -345,8 +334,7 @@ int mgb_rope_append_gqa_prefill(const void* qkv, int T, int seq0, int P, const f
 
 int mgb_silu_mul(const void* gate_up, int T, int F, void* h, void* stream) {
   if (T < 1 || F % 8) return MGB_EINVAL;
-  const long long n = (long long)T * (F / 8);
-  mgb::silu_mul_kernel<<<(int)((n + 255) / 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+  mgb::silu_mul_kernel<<<dim3((F / 8 + 255) / 256, std::min(T, 65535)), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<const __nv_bfloat16*>(gate_up), T, F, reinterpret_cast<__nv_bfloat16*>(h));
   return mgb_host::launch_status();
 }
