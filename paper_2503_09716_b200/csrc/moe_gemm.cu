@@ -297,7 +297,7 @@ moe_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 // barrier.  Unit = (expert, token tile, 256-row pair tile).
 // ------------------------------------------------------------------------------------------
 constexpr int kPStages = 6;
-constexpr int kPBRows = 16;                                   // token rows per TMA box (2 KB)
+constexpr int kPBRows = 16;                                   // token rows per TMA box (2 KB); + one 8-row box for N/2 % 16
 constexpr int kPBBoxBytes = kPBRows * kBK * 2;
 constexpr int kPStageBytes = kATileBytes + (kBNMax / 2) * kBK * 2;  // 16 KB A + <= 16 KB half-B
 template <bool GATED> constexpr int pair_smem() {
@@ -307,9 +307,10 @@ template <bool GATED> constexpr int pair_smem() {
 template <bool GATED, bool ROWPTR = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Epi<GATED>::kThreads, 1)
 moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ CUtensorMap tmB8,
                      const int* __restrict__ offsets, int E, int MT, int K, int rows_per_expert, int half_rows,
                      __nv_bfloat16* __restrict__ out, int ldo, bool balanced,
-                const long long* __restrict__ row_ptr) {
+                     const long long* __restrict__ row_ptr, int nalign) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* tiles = smem;
@@ -339,6 +340,7 @@ moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
+    prefetch_tmap(&tmB8);
     for (int s = 0; s < kPStages; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
@@ -373,10 +375,10 @@ moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
         int e, nt, mt, tok0, n;
         sched.decode(u, offsets, e, nt, mt, tok0, n);
         const uint64_t pol_w = token_tiles(offsets[e + 1] - offsets[e], balanced) > 1 ? pol_shared : pol_once;
-        const int N = (n + 31) & ~31;
+        const int N = (n + nalign - 1) & ~(nalign - 1);
         const int half = N / 2;
-        const int nb = half / kPBRows;
-        const uint32_t bytes = 2u * (kATileBytes + nb * kPBBoxBytes);
+        const int nb = half / kPBRows, r8 = (half / 8) & 1;  // 16-row boxes + one 8-row box
+        const uint32_t bytes = 2u * (kATileBytes + half * kBK * 2);
         const int arow0 = e * rows_per_expert + mt * 2 * kRowsPerCta + rank * kRowsPerCta;
         const int trow0 = tok0 + rank * half;
         for (int kb = 0; kb < KB; ++kb) {
@@ -392,6 +394,7 @@ moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
           uint8_t* bt = st + kATileBytes;
           for (int j = 0; j < nb; ++j)
             tma_load_2d_pair(bt + j * kPBBoxBytes, &tmB, &full_bar[stage], kb * kBK, trow0 + j * kPBRows, pol_x);
+          if (r8) tma_load_2d_pair(bt + nb * kPBBoxBytes, &tmB8, &full_bar[stage], kb * kBK, trow0 + nb * kPBRows, pol_x);
           if (++stage == kPStages) { stage = 0; phase ^= 1; }
         }
       }
@@ -406,7 +409,7 @@ moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
       for (int u = pair; u < total; u += npairs) {
         int e, nt, mt, tok0, n;
         sched.decode(u, offsets, e, nt, mt, tok0, n);
-        const uint32_t N = (uint32_t)((n + 31) & ~31);
+        const uint32_t N = (uint32_t)((n + nalign - 1) & ~(nalign - 1));
         const uint32_t idesc = make_idesc_bf16(2 * kBM, N);
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
@@ -497,7 +500,7 @@ bool use_pair_kernel() {
 }
 
 template <bool GATED, bool PAIR, bool ROWPTR>
-int launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, const int* offsets, int E, int MT, int K,
+int launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmB8, const int* offsets, int E, int MT, int K,
                    int rows_per_expert, int half_rows, void* out, int ldo, bool balanced, const long long* row_ptr,
                    cudaStream_t stream) {
   static bool attr = false;
@@ -509,9 +512,15 @@ int launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, const int* of
       attr = true;
     }
     const int grid = mgb_host::num_sms() & ~1;
+    // pair MMA N: a multiple of 16 (each CTA holds N/2 token rows, whole 8-row swizzle atoms);
+    // MGB_PAIR_NALIGN=32 pads further
+    static const int nalign = [] {
+      const char* e = getenv("MGB_PAIR_NALIGN");
+      return (e && atoi(e) == 32) ? 32 : 16;
+    }();
     mgb::moe_gemm_pair_kernel<GATED, ROWPTR><<<grid, mgb::Epi<GATED>::kThreads, mgb::pair_smem<GATED>(), stream>>>(
-        tmA, tmB, offsets, E, MT / 2, K, rows_per_expert, half_rows, reinterpret_cast<__nv_bfloat16*>(out), ldo,
-        balanced, row_ptr);
+        tmA, tmB, tmB8, offsets, E, MT / 2, K, rows_per_expert, half_rows, reinterpret_cast<__nv_bfloat16*>(out), ldo,
+        balanced, row_ptr, nalign);
   } else {
     if (!attr) {
       if (cudaFuncSetAttribute(mgb::moe_gemm_kernel<GATED, ROWPTR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -540,23 +549,25 @@ int launch_moe_gemm(const void* w, int w_rows_total, const void* act, int act_ro
     return e ? (e[0] == '1' ? 1 : 0) : -1;
   }();
   const bool balanced = bal_env < 0 ? GATED : bal_env == 1;
-  CUtensorMap tmA, tmB;
+  CUtensorMap tmA, tmB, tmB8;
   if (mgb_host::encode_tmap_2d_bf16(&tmA, w, K, w_rows_total, (uint64_t)K * 2, mgb::kBK,
                                     GATED ? mgb::kBM / 2 : mgb::kBM) != CUDA_SUCCESS)
     return MGB_ECUDA;
   if (mgb_host::encode_tmap_2d_bf16(&tmB, act, K, act_rows, (uint64_t)K * 2, mgb::kBK,
                                     pair ? mgb::kPBRows : mgb::kBRows) != CUDA_SUCCESS)
     return MGB_ECUDA;
+  if (pair && mgb_host::encode_tmap_2d_bf16(&tmB8, act, K, act_rows, (uint64_t)K * 2, mgb::kBK, 8) != CUDA_SUCCESS)
+    return MGB_ECUDA;
   if (row_ptr) {
     if (GATED) return MGB_EINVAL;  // only the down GEMM sends rows home
-    return pair ? launch_variant<GATED, true, true>(tmA, tmB, offsets, E, MT, K, rows_per_expert, half_rows, out, ldo,
+    return pair ? launch_variant<GATED, true, true>(tmA, tmB, tmB8, offsets, E, MT, K, rows_per_expert, half_rows, out, ldo,
                                                    balanced, row_ptr, stream)
-                : launch_variant<GATED, false, true>(tmA, tmB, offsets, E, MT, K, rows_per_expert, half_rows, out, ldo,
+                : launch_variant<GATED, false, true>(tmA, tmB, tmB, offsets, E, MT, K, rows_per_expert, half_rows, out, ldo,
                                                     balanced, row_ptr, stream);
   }
-  return pair ? launch_variant<GATED, true, false>(tmA, tmB, offsets, E, MT, K, rows_per_expert, half_rows, out, ldo,
+  return pair ? launch_variant<GATED, true, false>(tmA, tmB, tmB8, offsets, E, MT, K, rows_per_expert, half_rows, out, ldo,
                                                   balanced, nullptr, stream)
-              : launch_variant<GATED, false, false>(tmA, tmB, offsets, E, MT, K, rows_per_expert, half_rows, out, ldo,
+              : launch_variant<GATED, false, false>(tmA, tmB, tmB, offsets, E, MT, K, rows_per_expert, half_rows, out, ldo,
                                                    balanced, nullptr, stream);
 }
 }  // namespace
