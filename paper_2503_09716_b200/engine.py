@@ -207,7 +207,6 @@ class Engine:
                            q_pe=torch.zeros(B, H, a.qk_rope_dim, **bf),
                            q_lat=torch.zeros(H * B * a.kv_lora_rank, **bf),
                            o_lat=torch.zeros(H * B * a.kv_lora_rank, **bf),
-                           o_hb=torch.zeros(H * B * a.v_head_dim, **bf),
                            o_cat=torch.zeros(B, H * a.v_head_dim, **bf),
                            offsets_all=torch.tensor([0, B], dtype=torch.int32, device=device))
             if a.q_lora_rank:
@@ -559,7 +558,8 @@ class Engine:
         return (m["q_nope"][off * nope:(off + H * n) * nope].view(H, n, nope),
                 m["q_lat"][off * R:(off + H * n) * R].view(H, n, R),
                 m["o_lat"][off * R:(off + H * n) * R].view(H, n, R),
-                m["o_hb"][off * v:(off + H * n) * v].view(H, n, v))
+                # W_UV o_lat lands head-major straight in o_cat's rows (strided batched GEMM output)
+                m["o_cat"][s0:s1].view(n, H, v).transpose(0, 1))
 
     def _ds_job(self, l: int, j, W: dict) -> None:
         """DeepseekV2DecoderLayer (modeling_deepseek_v2.py:399-430) as module jobs; attention in the
@@ -594,8 +594,7 @@ class Engine:
             nat.call("mgb_decode_attn_mla", q_lat.data_ptr(), m["q_pe"][s0:s1].data_ptr(), cache.data_ptr(),
                      table.data_ptr(), self.pps, b.seq_lens[s0:].data_ptr(), s1 - s0, H, R, r, scale,
                      o_lat.data_ptr(), torch.cuda.current_stream().cuda_stream)
-            torch.bmm(o_lat, W["w_uv_t"], out=o_hb)
-            m["o_cat"][s0:s1].view(s1 - s0, H, a.v_head_dim).copy_(o_hb.transpose(0, 1))
+            torch.bmm(o_lat, W["w_uv_t"], out=o_hb)  # o_hb is a [H, n, v] view of o_cat[s0:s1]
         elif j.kind == "post_attention":
             torch.mm(m["o_cat"], W["wo"].t(), out=b.o)
             ops.add_rmsnorm(b.x, W["ln2"], a.rms_eps, b.h, delta=b.o, x_out=b.x)
