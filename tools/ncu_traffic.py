@@ -34,7 +34,9 @@ for cfg, rep in CASES.items():
     if not os.path.exists(path):
         continue
     for name, b in launches(path):
-        key = "gate_up" if "<1>" in name or "<true>" in name else "down"
+        # template argument GATED (first): <1, ...> / <true, ...> is the gate/up GEMM
+        targs = name.split("<", 1)[1].split(">", 1)[0] if "<" in name else ""
+        key = "gate_up" if targs.split(",")[0].strip() in ("1", "true") else "down"
         out.setdefault(cfg, {})[key] = {"dram_bytes": b, "kernel": name.split("(")[0],
                                         "source": f"ncu --set full of tools/gemm_check.py ({os.path.basename(rep)})"}
 with open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w") as f:
