@@ -45,7 +45,22 @@ def test_router_topk_bitexact_given_logits(T, E, k, mode, ng, tg):
     assert int(ws.ticket.item()) == 0
 
 
-@pytest.mark.parametrize("T,d,E,k,mode", [(64, 256, 8, 2, 0), (513, 4096, 8, 2, 0), (200, 2048, 64, 6, 1)])
+def test_router_workspace_serves_smaller_batches():
+    """One workspace sized for 6058 tokens routes micro-batches of other sizes in turn (histograms,
+    ticket and offsets reused; the ticket self-resets between calls)."""
+    ops = _ops()
+    ws = ops.RouterWorkspace(6058, 64, 6)
+    for T in (2000, 6058, 5):
+        logits = torch.randn(T, 64, generator=torch.Generator().manual_seed(T))
+        ops.router_topk(None, None, ws, 6, 1, 1.0, logits_in=logits.cuda())
+        idx_ref, _ = R.route(logits, 6, 1, 1.0)
+        assert torch.equal(ws.topk_idx[:T].cpu().long(), idx_ref)
+        _, _, counts, offsets = R.permutation(idx_ref, 64)
+        assert torch.equal(ws.offsets.cpu().long(), offsets)
+
+
+@pytest.mark.parametrize("T,d,E,k,mode", [(64, 256, 8, 2, 0), (513, 4096, 8, 2, 0), (200, 2048, 64, 6, 1),
+                                          (3001, 1024, 64, 6, 1)])
 def test_router_gemv_and_permutation(T, d, E, k, mode):
     ops = _ops()
     x = uniform_bf16((T, d), 3, 7, 1.0)
