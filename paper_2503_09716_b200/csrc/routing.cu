@@ -379,6 +379,11 @@ __global__ void permute_kernel(const __nv_bfloat16* __restrict__ x, const int* _
 // One CTA per token; the whole row lives in registers (<= kCombineVec 16 B vectors / thread).
 constexpr int kCombineThreads = 256;
 constexpr int kCombineVec = 4;  // d <= 8192
+// One CTA per token; VEC 16-byte columns per thread (the launcher picks the smallest VEC that covers
+// d, so registers -- and with them resident CTAs per SM -- follow the row width).  The token's
+// residual / shared-expert rows are requested before its routing entries arrive, and all k expert
+// rows of a column are in flight together: a CTA waits for two memory round trips, not four.
+template <int VEC>
 __global__ void __launch_bounds__(kCombineThreads)
 combine_kernel(const __nv_bfloat16* __restrict__ y_perm, const int* __restrict__ dst_pos,
                const float* __restrict__ topk_w, const __nv_bfloat16* __restrict__ shared_out,
@@ -389,21 +394,30 @@ combine_kernel(const __nv_bfloat16* __restrict__ y_perm, const int* __restrict__
   __shared__ int s_pos[kMaxK];
   __shared__ float s_w[kMaxK];
   __shared__ float s_red[kCombineThreads / 32];
+  const int nvec = d / 8;
+  uint4 rv[VEC], sv[VEC];
+#pragma unroll
+  for (int u = 0; u < VEC; ++u) {  // routing-independent rows first (read before out is written)
+    const int c = threadIdx.x + u * kCombineThreads;
+    if (c < nvec) {
+      if (residual) rv[u] = reinterpret_cast<const uint4*>(residual + (size_t)t * d)[c];
+      if (shared_out) sv[u] = ld_nc_v4(reinterpret_cast<const uint4*>(shared_out + (size_t)t * d) + c);
+    }
+  }
   if (threadIdx.x < k) {
     s_pos[threadIdx.x] = dst_pos[(size_t)t * k + threadIdx.x];
     s_w[threadIdx.x] = topk_w[(size_t)t * k + threadIdx.x];
   }
   __syncthreads();
-  const int nvec = d / 8;
-  float acc[kCombineVec][8];
+  float acc[VEC][8];
 #pragma unroll
-  for (int u = 0; u < kCombineVec; ++u)
+  for (int u = 0; u < VEC; ++u)
 #pragma unroll
     for (int i = 0; i < 8; ++i) acc[u][i] = 0.f;
   // all k rows of a 16-byte column in flight at once (k independent loads per thread), then the fp32
   // weighted sum in j order (j ascending, as the oracle)
 #pragma unroll
-  for (int u = 0; u < kCombineVec; ++u) {
+  for (int u = 0; u < VEC; ++u) {
     const int c = threadIdx.x + u * kCombineThreads;
     if (c < nvec) {
       uint4 v[kMaxK];
@@ -423,22 +437,20 @@ combine_kernel(const __nv_bfloat16* __restrict__ y_perm, const int* __restrict__
   }
   float ss = 0.f;
 #pragma unroll
-  for (int u = 0; u < kCombineVec; ++u) {
+  for (int u = 0; u < VEC; ++u) {
     const int c = threadIdx.x + u * kCombineThreads;
     if (c >= nvec) continue;
 #pragma unroll
     for (int i = 0; i < 8; ++i) acc[u][i] = bf16_round(acc[u][i]);
     if (shared_out) {
-      const uint4 sv = ld_nc_v4(reinterpret_cast<const uint4*>(shared_out + (size_t)t * d) + c);
-      const float f[8] = {bf16lo(sv.x), bf16hi(sv.x), bf16lo(sv.y), bf16hi(sv.y),
-                          bf16lo(sv.z), bf16hi(sv.z), bf16lo(sv.w), bf16hi(sv.w)};
+      const float f[8] = {bf16lo(sv[u].x), bf16hi(sv[u].x), bf16lo(sv[u].y), bf16hi(sv[u].y),
+                          bf16lo(sv[u].z), bf16hi(sv[u].z), bf16lo(sv[u].w), bf16hi(sv[u].w)};
 #pragma unroll
       for (int i = 0; i < 8; ++i) acc[u][i] = bf16_round(acc[u][i] + f[i]);
     }
     if (residual) {
-      const uint4 r = reinterpret_cast<const uint4*>(residual + (size_t)t * d)[c];
-      const float f[8] = {bf16lo(r.x), bf16hi(r.x), bf16lo(r.y), bf16hi(r.y),
-                          bf16lo(r.z), bf16hi(r.z), bf16lo(r.w), bf16hi(r.w)};
+      const float f[8] = {bf16lo(rv[u].x), bf16hi(rv[u].x), bf16lo(rv[u].y), bf16hi(rv[u].y),
+                          bf16lo(rv[u].z), bf16hi(rv[u].z), bf16lo(rv[u].w), bf16hi(rv[u].w)};
 #pragma unroll
       for (int i = 0; i < 8; ++i) acc[u][i] = bf16_round(acc[u][i] + f[i]);
     }
@@ -450,7 +462,14 @@ combine_kernel(const __nv_bfloat16* __restrict__ y_perm, const int* __restrict__
     for (int i = 0; i < 8; ++i) ss = fmaf(acc[u][i], acc[u][i], ss);
   }
   if (!norm_out) return;
-  // fused RMSNorm of the row just written (block reduction of the sum of squares)
+  // fused RMSNorm of the row just written (block reduction of the sum of squares); the norm weights
+  // are requested before the reduction's barrier
+  uint4 wv[VEC];
+#pragma unroll
+  for (int u = 0; u < VEC; ++u) {
+    const int c = threadIdx.x + u * kCombineThreads;
+    if (c < nvec) wv[u] = reinterpret_cast<const uint4*>(norm_w)[c];
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
   if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = ss;
@@ -460,12 +479,11 @@ combine_kernel(const __nv_bfloat16* __restrict__ y_perm, const int* __restrict__
   for (int i = 0; i < kCombineThreads / 32; ++i) tot += s_red[i];
   const float inv = 1.0f / sqrtf(tot / (float)d + eps);
 #pragma unroll
-  for (int u = 0; u < kCombineVec; ++u) {
+  for (int u = 0; u < VEC; ++u) {
     const int c = threadIdx.x + u * kCombineThreads;
     if (c >= nvec) continue;
-    const uint4 wv = reinterpret_cast<const uint4*>(norm_w)[c];
-    const float wf[8] = {bf16lo(wv.x), bf16hi(wv.x), bf16lo(wv.y), bf16hi(wv.y),
-                         bf16lo(wv.z), bf16hi(wv.z), bf16lo(wv.w), bf16hi(wv.w)};
+    const float wf[8] = {bf16lo(wv[u].x), bf16hi(wv[u].x), bf16lo(wv[u].y), bf16hi(wv[u].y),
+                         bf16lo(wv[u].z), bf16hi(wv[u].z), bf16lo(wv[u].w), bf16hi(wv[u].w)};
     float r[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) r[i] = wf[i] * bf16_round(acc[u][i] * inv);
@@ -585,7 +603,9 @@ int mgb_unpermute_combine(const void* y_perm, const int* dst_pos, const float* t
   if (T < 1 || d % 8 || d > 8 * mgb::kCombineThreads * mgb::kCombineVec || k < 1 || k > mgb::kMaxK ||
       (norm_out && !norm_w))
     return MGB_EINVAL;
-  mgb::combine_kernel<<<T, mgb::kCombineThreads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+  const int vec = (d / 8 + mgb::kCombineThreads - 1) / mgb::kCombineThreads;
+  auto kern = vec <= 1 ? mgb::combine_kernel<1> : vec <= 2 ? mgb::combine_kernel<2> : mgb::combine_kernel<mgb::kCombineVec>;
+  kern<<<T, mgb::kCombineThreads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<const __nv_bfloat16*>(y_perm), dst_pos, topk_w,
       reinterpret_cast<const __nv_bfloat16*>(shared_out), reinterpret_cast<const __nv_bfloat16*>(residual), T, d,
       k, reinterpret_cast<__nv_bfloat16*>(out), reinterpret_cast<const __nv_bfloat16*>(norm_w), eps,
