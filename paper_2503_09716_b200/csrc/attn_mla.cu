@@ -414,7 +414,8 @@ decode_attn_mla_kernel(const __grid_constant__ CUtensorMap tm_qlat,  // q_lat [H
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&pfull[s]);
-        if (threadIdx.x == 0) mla_trace(4, g);  // 4: P written (warp 0)
+        if (threadIdx.x == 0) mla_trace(4, g);    // 4: P written (warp 0, heads 0-7)
+        if (threadIdx.x == 128) mla_trace(6, g);  // 6: P written (warp 4, heads 8-15)
         if (p > 0) accumulate_o(g - 1);
 #pragma unroll
         for (int h = 0; h < HG; ++h) alpha_prev[h] = alpha[h];

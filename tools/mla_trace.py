@@ -42,15 +42,13 @@ def d(a, b, lo=20, hi=200):
     return statistics.median((ev[b][p] - ev[a][p]) / 1e3 for p in range(lo, hi) if ev[a][p] and ev[b][p])
 print("median per page (us): load->S_iss %.2f  S_iss->S_rdy %.2f  S_rdy->P_wr %.2f  P_wr->PV_iss %.2f  PV_iss->PV_done %.2f" % (
     d(0, 1), d(1, 3), d(3, 4), d(4, 2), d(2, 5)))
-print("P written by warps 1..3 after warp 0 (us): %.2f %.2f %.2f; last warp -> PV_iss %.2f" % (
-    d(4, 6), d(4, 7), d(4, 8),
-    statistics.median((ev[2][p] - max(ev[4][p], ev[6][p], ev[7][p], ev[8][p])) / 1e3 for p in range(20, 200))))
+print("P written by warp 4 (heads 8-15) after warp 0 (us): %.2f; later of the two -> PV_iss %.2f" % (
+    d(4, 6), statistics.median((ev[2][p] - max(ev[4][p], ev[6][p])) / 1e3 for p in range(20, 200))))
 print("page period (us): %.2f" % statistics.median((ev[0][p + 1] - ev[0][p]) / 1e3 for p in range(20, 200)))
 
 ends = [p for p in range(N) if ev[9][p]]
 for p in ends[2:8]:
     q = p + 1
-    print(f"  l reduced +{(ev[13][p]-ev[9][p])/1e3:.2f}  l shared +{(ev[14][p]-ev[9][p])/1e3:.2f}")
     print(f"item end page {p}: last O pulled {(ev[9][p]-t0)/1e3:.2f}  stores issued +{(ev[10][p]-ev[9][p])/1e3:.2f}  "
           f"epilogue done +{(ev[11][p]-ev[9][p])/1e3:.2f}  next len loaded +{(ev[12][q]-ev[9][p])/1e3:.2f}  "
           f"next S ready +{(ev[3][q]-ev[9][p])/1e3:.2f}  (next S issued at {(ev[1][q]-ev[9][p])/1e3:+.2f}, "
