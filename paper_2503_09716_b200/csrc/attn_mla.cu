@@ -19,10 +19,11 @@
 // (masked to P = 0).  56-token pages let three stages (189 KB) fit in shared memory, which keeps
 // enough bytes in flight per SM while a page is held for S^T -> softmax -> P.V.  The swizzle keeps
 // the tensor cores' shared-memory reads conflict free; R + r is padded to a multiple of 64 in the
-// page, and the append kernels write the padding of every token row as zeros (it is a K column of
-// the S^T MMA against Q's zero padding, so it must be finite; rows past a sequence's length may
-// hold anything).
-// so a page is one contiguous cp.async.bulk and both GEMMs run on tcgen05 with fp32 accumulators in
+// page, and the append kernels write the padding of every token row as zeros: P.V's phantom rows
+// (tokens 56-63 of a 64-dim block alias the next block's first 8 token rows) multiply P = 0 by those
+// rows, padding included, so they must be finite.  Rows past a sequence's length may hold anything
+// (masked from S, zeroed in shared memory before P.V).
+// A page is one contiguous cp.async.bulk, and both GEMMs run on tcgen05 with fp32 accumulators in
 // TMEM ("swap-AB": tokens / latent dims fill the MMA M side, the 16 heads of a work item are N).
 //
 // Persistent kernel, one CTA per SM, 10 warps:
@@ -543,8 +544,8 @@ __global__ void mla_append_kernel(const __nv_bfloat16* __restrict__ q,    // [B,
     pg[at(d0)] = __float2bfloat16_rn(x0 * c - x1 * s);
     pg[at(d0 + 1)] = __float2bfloat16_rn(x0 * s + x1 * c);
   }
-  // the row's padding dims [D, DP) are K columns of the S^T MMA (times Q's zero padding): they must
-  // hold finite values, whatever the page held before (0 * NaN would poison the row's scores)
+  // the row's padding dims [D, DP) must be finite whatever the page held before: P.V's phantom rows
+  // read them (times P = 0) for the page's first 8 tokens, and 0 * NaN would poison O
   for (int i = D + threadIdx.x; i < DP; i += blockDim.x) pg[at(i)] = __float2bfloat16_rn(0.f);
   const int QD = NOPE + RP;
   for (int i = threadIdx.x; i < H * (RP / 2); i += blockDim.x) {  // per-head q_pe
