@@ -109,6 +109,8 @@ def _dist():
         import torch.distributed as dist
 
         backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if torch.cuda.is_available():  # bind the rank's GPU before NCCL's communicator is built
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")) % torch.cuda.device_count())
         dist.init_process_group(backend)
         return dist, dist.get_rank(), ws, int(os.environ.get("LOCAL_RANK", "0"))
     return None, 0, 1, 0
