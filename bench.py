@@ -320,6 +320,28 @@ def run_ours(args, dist, rank, world) -> None:
     t_e2e = _max_over_ranks(dist, statistics.median(e2e_times))
     e2e_value = B * N * world / t_e2e
 
+    # ---- the same decode step behind a real batched prefill of the B prompts (SURVEY.md §8d asks for
+    # the incl.-prefill figure too): B x prompt_len tokens through Engine.prefill, device-timed ----
+    incl = None
+    if args.incl_prefill:
+        try:
+            ids = torch.randint(0, arch.vocab, (B, args.prompt_len), generator=torch.Generator().manual_seed(11))
+            torch.cuda.synchronize()
+            p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            p0.record()
+            eng.prefill(ids)
+            p1.record()
+            torch.cuda.synchronize()
+            t_pf = _max_over_ranks(dist, p0.elapsed_time(p1) / 1e3)
+            t_dec = t / args.steps
+            incl = {"value": B * N * world / (t_pf + t_dec), "unit": UNIT, "prefill_ms": 1e3 * t_pf,
+                    "decode_ms": 1e3 * t_dec, "prefill_tokens_per_s": B * args.prompt_len * world / t_pf,
+                    "convention": f"B*{N} generated tokens / (batched prefill of B x {args.prompt_len} prompt tokens"
+                                  f" + {N} decode forwards); the first generated token comes from the prefill"}
+        except torch.OutOfMemoryError as e:  # report, do not lose the line
+            incl = {"value": None, "unit": UNIT, "error": f"prefill out of memory: {str(e).splitlines()[0]}"}
+            torch.cuda.empty_cache()
+
     # ---- per-kernel breakdown and roofline of the dominant kernel ----
     eng.reset(args.prompt_len + args.decode_len // 2)
     bd = kernel_breakdown(eng)
@@ -351,6 +373,22 @@ def run_ours(args, dist, rank, world) -> None:
     roofline.update({"traffic": traffic, "traffic_source": traffic_src, "algorithmic_bytes_per_launch": gu_bytes, "algorithmic_flops_per_launch": gu_flops,
                      "avg_launch_ms": gu["avg_ms"], "peak_source": src, "tokens_per_expert": tok_per_expert,
                      "share_of_step": gu["ms_per_step"] / step_ms_eager})
+    # achieved HBM bandwidth of the HBM-bound kernels (SURVEY.md §8d per-kernel algorithmic bytes;
+    # attention at the breakdown's context, prompt_len + decode_len / 2 + 1)
+    T, d, k, E = B, a.hidden, a.top_k, a.n_experts
+    ctx_bd = args.prompt_len + args.decode_len // 2 + 1
+    if a.family == "deepseek_v2":
+        attn_name, attn_bytes = "decode_attn_mla", B * ctx_bd * (a.kv_lora_rank + a.qk_rope_dim) * 2
+    else:
+        attn_name, attn_bytes = "decode_attn_gqa", B * ctx_bd * a.n_kv_heads * a.head_dim * 2 * 2
+    shared = 2 if a.family == "deepseek_v2" else 0  # shared-expert rows read by the combine
+    algo = {"router_topk": T * E * 4 + T * k * 12, "permute": T * d * 2 + T * k * d * 2,
+            "unpermute_combine": T * k * d * 2 + T * d * 2 * (3 + (1 if shared else 0)), attn_name: attn_bytes}
+    kernel_hbm = {}
+    for name, nbytes in algo.items():
+        if name in bd:
+            gbs = nbytes / (bd[name]["avg_ms"] * 1e-3) / 1e9
+            kernel_hbm[name] = {"algorithmic_bytes": nbytes, "avg_ms": bd[name]["avg_ms"], "gbs": gbs, "frac": gbs / hbm}
     launches_per_step = eng.kernel_launches_per_step * N
     ctx_avg = args.prompt_len + args.decode_len / 2
 
@@ -369,6 +407,8 @@ def run_ours(args, dist, rank, world) -> None:
         "expert_gemm": {"tflops": expert_tflops, "tensor_util_of_bf16_peak": expert_tflops / tf_burst,
                         "tokens_per_expert": rows / a.n_experts, "gate_up_ms": gu["avg_ms"], "down_ms": dn["avg_ms"],
                         "gate_up_gbs": gu_gbs, "down_gbs": dn_bytes / (dn["avg_ms"] * 1e-3) / 1e9},
+        "incl_prefill": incl,
+        "kernel_hbm": kernel_hbm,
         "kernel_ms_per_forward": {k: round(v["ms_per_step"], 4) for k, v in sorted(bd.items())},
         "forward_ms": 1e3 * t / args.steps / N, "context_avg": ctx_avg,
         "clocks": clk.summary(), "gpu_launches": launches_per_step * args.steps,
@@ -395,6 +435,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-batch", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--no-incl-prefill", dest="incl_prefill", action="store_false",
+                    help="skip the batched-prefill pass behind the incl_prefill figure")
     args = ap.parse_args()
     dist, rank, world, local = _dist()
     if args.impl == "reference":
