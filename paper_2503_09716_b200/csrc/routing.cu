@@ -336,6 +336,7 @@ __global__ void __launch_bounds__(256) router_scan_kernel(int* __restrict__ bloc
 }
 
 // One warp per (token, slot) entry: compute the permuted row and copy x[t] there (16 B vectors).
+template <int U>  // 16-byte vectors per lane held in flight (the launcher sizes it to the row)
 __global__ void permute_kernel(const __nv_bfloat16* __restrict__ x, const int* __restrict__ topk_idx,
                                const int* __restrict__ local_rank, const int* __restrict__ block_base,
                                const int* __restrict__ offsets, int T, int d, int k, int E, int tpb,
@@ -346,23 +347,29 @@ __global__ void permute_kernel(const __nv_bfloat16* __restrict__ x, const int* _
   const int lane = threadIdx.x & 31;
   if (gw >= T * k) return;
   const int t = gw / k;
+  const uint4* src = reinterpret_cast<const uint4*>(x + (size_t)t * d);
+  // the token's row (its first 512*U bytes) is requested before the routing lookups that place it, so the row
+  // and the index chain (expert -> offsets / block base / rank) are in flight together
+  const int nvec = d / 8;
+  uint4 v[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+    if (lane + 32 * u < nvec) v[u] = ld_nc_v4(src + lane + 32 * u);
   const int e = topk_idx[gw];
   const int pos = offsets[e] + block_base[(size_t)(t / tpb) * E + e] + local_rank[gw];
   if (lane == 0) {
     dst_pos[gw] = pos;
     src_token[pos] = t;
   }
-  const uint4* src = reinterpret_cast<const uint4*>(x + (size_t)t * d);
   // expert-parallel dispatch fused into the permutation: the row goes straight into the receive
   // buffer of the expert's owner rank (peer memory over NVLink), at this source's segment of expert e
   uint4* dst = peer_base ? reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(peer_base[e / E_local]) +
                                                      (size_t)(disp_row[e] + pos - offsets[e]) * d)
                          : reinterpret_cast<uint4*>(x_perm + (size_t)pos * d);
-  // all of the lane's 16 B vectors in flight before any store (row <= 8 KB -> <= 24 vectors/lane)
-  constexpr int U = 8;
-  const int nvec = d / 8;
-  for (int c0 = lane; c0 < nvec; c0 += 32 * U) {
-    uint4 v[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+    if (lane + 32 * u < nvec) dst[lane + 32 * u] = v[u];
+  for (int c0 = lane + 32 * U; c0 < nvec; c0 += 32 * U) {  // rows wider than 512*U bytes
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (c0 + 32 * u < nvec) v[u] = ld_nc_v4(src + c0 + 32 * u);
@@ -541,7 +548,7 @@ int mgb_permute(const void* x, const int* topk_idx, const int* local_rank, const
   const int warps = T * k;
   const int threads = 256;
   const int blocks = (warps * 32 + threads - 1) / threads;
-  mgb::permute_kernel<<<blocks, threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+  (d <= 2048 ? mgb::permute_kernel<8> : mgb::permute_kernel<16>)<<<blocks, threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<const __nv_bfloat16*>(x), topk_idx, local_rank, block_base, offsets, T, d, k, E,
       mgb::kRouterTPB, reinterpret_cast<__nv_bfloat16*>(x_perm), src_token, dst_pos, nullptr, nullptr, 1);
   return mgb_host::launch_status();
@@ -559,7 +566,7 @@ int mgb_ep_permute_dispatch(const void* x, const int* topk_idx, const int* local
   const int warps = T * k;
   const int threads = 256;
   const int blocks = (warps * 32 + threads - 1) / threads;
-  mgb::permute_kernel<<<blocks, threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+  (d <= 2048 ? mgb::permute_kernel<8> : mgb::permute_kernel<16>)<<<blocks, threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<const __nv_bfloat16*>(x), topk_idx, local_rank, block_base, offsets, T, d, k, E,
       mgb::kRouterTPB, nullptr, src_token, dst_pos, peer_base, disp_row, E_local);
   return mgb_host::launch_status();
