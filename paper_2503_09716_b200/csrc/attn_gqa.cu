@@ -10,9 +10,8 @@
 // "chunk-major": [hd/8 chunks][64 tokens][8 dims].  Eight consecutive tokens of one 8-dim chunk
 // are 128 contiguous bytes, so every ldmatrix (K) / ldmatrix.trans (V) is bank-conflict free.
 //
-// Persistent kernel (1 CTA per SM with a 4-stage ring for large batches, 2 with 3 stages for
-// small ones): warp 4 is a bulk-copy producer streaming the pages of the
-// CTA's (sequence, kv-head) work items through a shared-memory ring (cp.async.bulk +
+// Persistent kernel, 2 CTAs per SM: warp 4 is a bulk-copy producer streaming the pages of the
+// CTA's (sequence, kv-head) work items through a 3-stage shared-memory ring (cp.async.bulk +
 // mbarrier), running ahead across work-item boundaries; warps 0-3 consume, each owning 16 tokens
 // of every page: S = Q K^T and O += P V on the tensor cores (mma.sync m16n8k16, the G query heads
 // of the group are rows 0..G-1 of the 16-row tile), online softmax per warp, then a 4-way merge
@@ -22,20 +21,18 @@
 namespace mgb {
 
 constexpr int kPage = 64;
-// Two ring shapes (same bytes in flight per SM): 2 CTAs x 3 stages keeps more items in flight for
-// small batches; 1 CTA x 4 stages streams large batches ~5 % faster (B=827: 306 vs 323 us).
-constexpr int kLargeStages = 4, kSmallStages = 3;
+constexpr int kAttnStages = 3;
 constexpr int kConsumerWarps = 4;
 constexpr int kAttnThreads = (kConsumerWarps + 1) * 32;
 
-template <int HD, int G, int STAGES>
+template <int HD, int G>
 struct GqaSmem {
   static constexpr int kTileElems = HD * kPage;
   static constexpr int kTileBytes = kTileElems * 2;                 // one K (or V) page-head block
   static constexpr int kStageBytes = 2 * kTileBytes;
   static constexpr int kMergeStride = G * HD + 16;                  // per warp: O (G rows) + m[8] + l[8]
   static constexpr int kMergeBytes = kConsumerWarps * kMergeStride * 4;
-  static constexpr size_t kBytes = (size_t)STAGES * kStageBytes + kMergeBytes + 128;
+  static constexpr size_t kBytes = (size_t)kAttnStages * kStageBytes + kMergeBytes + 128;
 };
 
 MGB_DEVINL void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
@@ -59,7 +56,7 @@ MGB_DEVINL void mma_bf16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t
 }
 MGB_DEVINL void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-template <int HD, int G, int kAttnStages>
+template <int HD, int G>
 __global__ void __launch_bounds__(kAttnThreads, 2)
 decode_attn_gqa_kernel(const __nv_bfloat16* __restrict__ q,       // [B, Hkv*G, HD]
                        const __nv_bfloat16* __restrict__ k_cache,  // pages, chunk-major
@@ -68,7 +65,7 @@ decode_attn_gqa_kernel(const __nv_bfloat16* __restrict__ q,       // [B, Hkv*G, 
                        const int* __restrict__ seq_lens, int B, int Hkv, float scale_log2,
                        __nv_bfloat16* __restrict__ out) {          // [B, Hkv*G*HD]
   static_assert(G <= 8 && HD % 16 == 0, "GQA tile: G <= 8 query heads per kv head");
-  using S = GqaSmem<HD, G, kAttnStages>;
+  using S = GqaSmem<HD, G>;
   constexpr int KSTEPS = HD / 16;   // k-steps of QK^T
   constexpr int NT = HD / 8;        // n-tiles of PV (8 dims each)
   extern __shared__ __align__(128) uint8_t smem[];
@@ -228,32 +225,25 @@ decode_attn_gqa_kernel(const __nv_bfloat16* __restrict__ q,       // [B, Hkv*G, 
   }
 }
 
-template <int HD, int G, int STAGES>
-int launch_gqa_cfg(const void* q, const void* kc, const void* vc, const int* bt, int max_pages, const int* lens,
-                   int B, int Hkv, float scale, void* out, int grid, cudaStream_t st) {
-  using S = GqaSmem<HD, G, STAGES>;
+template <int HD, int G>
+int launch_gqa(const void* q, const void* kc, const void* vc, const int* bt, int max_pages, const int* lens, int B,
+               int Hkv, float scale, void* out, cudaStream_t st) {
+  using S = GqaSmem<HD, G>;
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(decode_attn_gqa_kernel<HD, G, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(decode_attn_gqa_kernel<HD, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)S::kBytes) != cudaSuccess)
       return MGB_ECUDA;
     attr = true;
   }
-  decode_attn_gqa_kernel<HD, G, STAGES><<<grid, kAttnThreads, S::kBytes, st>>>(
+  const int items = B * Hkv;
+  int grid = 2 * mgb_host::num_sms();
+  if (grid > items) grid = items;
+  decode_attn_gqa_kernel<HD, G><<<grid, kAttnThreads, S::kBytes, st>>>(
       reinterpret_cast<const __nv_bfloat16*>(q), reinterpret_cast<const __nv_bfloat16*>(kc),
       reinterpret_cast<const __nv_bfloat16*>(vc), bt, max_pages, lens, B, Hkv, scale * 1.4426950408889634f,
       reinterpret_cast<__nv_bfloat16*>(out));
   return mgb_host::launch_status();
-}
-
-template <int HD, int G>
-int launch_gqa(const void* q, const void* kc, const void* vc, const int* bt, int max_pages, const int* lens, int B,
-               int Hkv, float scale, void* out, cudaStream_t st) {
-  const int items = B * Hkv, sms = mgb_host::num_sms();
-  if (items >= 8 * sms)  // many items per CTA: one deep ring per SM
-    return launch_gqa_cfg<HD, G, kLargeStages>(q, kc, vc, bt, max_pages, lens, B, Hkv, scale, out, sms, st);
-  const int grid = items < 2 * sms ? items : 2 * sms;
-  return launch_gqa_cfg<HD, G, kSmallStages>(q, kc, vc, bt, max_pages, lens, B, Hkv, scale, out, grid, st);
 }
 
 }  // namespace mgb
