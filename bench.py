@@ -193,6 +193,18 @@ def cpu_layer_sample(arch, B: int, ctx: int, reps: int, threads: int) -> tuple[f
     return B / (t_layer * a.layers), sample
 
 
+def _workload_config(args, arch, world: int) -> dict:
+    """The workload both arms are quoted on (the GPU arm's batch: the planner's largest resident B)."""
+    from paper_2503_09716_b200.engine import resident_plan
+
+    plan = resident_plan(arch, args.prompt_len, args.decode_len, B=args.batch, reserve_bytes=args.reserve_gb << 30)
+    return {"workload": f"{arch.name} decode phase, prompt {args.prompt_len} / gen {args.decode_len}, 1 B200 resident "
+                        f"({'BASELINE configs[1]' if arch.name == 'mixtral-8x7b' else 'BASELINE configs[2] shape'});"
+                        f" step = {args.decode_len} decode forwards of B={plan.B} sequences",
+            "batch": plan.B, "b_a": plan.b_a, "b_e": plan.b_e, "kv_policy": "resident (paged, HBM)",
+            "parallelism": f"replicas x{world}", "l2": "inputs larger than L2 (all weights stream from HBM every forward)"}
+
+
 def run_reference(args, dist, rank, world) -> None:
     from paper_2503_09716_b200.configs import get_arch
 
@@ -215,8 +227,7 @@ def run_reference(args, dist, rank, world) -> None:
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / max(1, args.steps),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic", "config": {"workload": f"{arch.name} decode, prompt {args.prompt_len} / gen "
-                                                        f"{args.decode_len}", "batch": B, "context": ctx},
+            "data": "synthetic", "config": _workload_config(args, arch, world),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -396,11 +407,7 @@ def run_ours(args, dist, rank, world) -> None:
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (random-init counter-based weights, synthetic prefill KV)",
-        "config": {"workload": f"{arch.name} decode phase, prompt {args.prompt_len} / gen {N}, 1 B200 resident "
-                               f"({'BASELINE configs[1]' if arch.name == 'mixtral-8x7b' else 'BASELINE configs[2] shape'});"
-                               f" step = {N} decode forwards of B={B} sequences",
-                   "batch": B, "b_a": plan.b_a, "b_e": plan.b_e, "kv_policy": "resident (paged, HBM)",
-                   "parallelism": f"replicas x{world}", "l2": "inputs larger than L2 (93 GB weights streamed/forward)"},
+        "config": _workload_config(args, arch, world),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(first_pinned.numel() * 4),
                 "d2h_bytes_per_step": int(out.numel() * out.element_size())},
         "roofline": roofline,
