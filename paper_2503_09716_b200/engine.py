@@ -609,7 +609,7 @@ class Engine:
             if l >= a.first_k_dense:
                 # fp32 router logits (HF: F.linear(x.float(), W.float()), modeling_deepseek_v2.py:125) as a
                 # bf16 tensor-core GEMM with fp32 output (exact products, fp32 accumulation)
-                m["logits_r"].copy_(torch.mm(b.h, W["router"].t(), out_dtype=torch.float32))
+                torch.mm(b.h, W["router"].t(), out_dtype=torch.float32, out=m["logits_r"])
                 ops.router_topk(None, None, self.rws, a.top_k, a.router_mode, a.routed_scaling, a.n_group,
                                 a.topk_group, logits_in=m["logits_r"])
                 ops.permute(b.h, self.rws, b.x_perm)
@@ -702,7 +702,7 @@ class Engine:
             if self.router_logits == "cublas":
                 # gate GEMM on the tensor cores with fp32 output; the router kernel rounds it to
                 # bf16 exactly as HF's bf16 F.linear does (modeling_mixtral.py:111)
-                self.logits_r.copy_(torch.mm(b.h, W["router"].t(), out_dtype=torch.float32))
+                torch.mm(b.h, W["router"].t(), out_dtype=torch.float32, out=self.logits_r)
                 ops.router_topk(None, None, self.rws, a.top_k, a.router_mode, a.routed_scaling, a.n_group,
                                 a.topk_group, logits_in=self.logits_r)
             else:
@@ -1003,7 +1003,7 @@ class Engine:
                         ops.silu_mul(S["sh_gu"][:t], S["sh_h"][:t])
                         torch.mm(S["sh_h"][:t], W["sh_down"][0].t(), out=S["sh_out"][:t])
                         shared = S["sh_out"][:t]
-                    S["lg"][:t].copy_(torch.mm(h, W["router"].t(), out_dtype=torch.float32))
+                    torch.mm(h, W["router"].t(), out_dtype=torch.float32, out=S["lg"][:t])
                     ops.router_topk(None, None, ws, k, a.router_mode, a.routed_scaling, a.n_group, a.topk_group,
                                     logits_in=S["lg"][:t])
                     ops.permute(h, ws, S["xp"])
@@ -1083,7 +1083,7 @@ class Engine:
                         torch.mm(S["sh_h"][:t], W["sh_down"][0].t(), out=sh_all[t0:t1])
                 if dense_mlp:
                     continue
-                lg.copy_(torch.mm(h_all, W["router"].t(), out_dtype=torch.float32))
+                torch.mm(h_all, W["router"].t(), out_dtype=torch.float32, out=lg)
                 ops.router_topk(None, None, ws, k, a.router_mode, a.routed_scaling, a.n_group, a.topk_group,
                                 logits_in=lg)
                 ops.permute(h_all, ws, xp)
