@@ -302,7 +302,9 @@ int mgb_add_rmsnorm(const void* x, const void* delta, const void* weight, float 
 }
 
 namespace {
-int rope_threads(int H, int hd) { return std::min(1024, (H * (hd / 8) + 31) / 32 * 32); }
+// 256 threads per token CTA (a few (head, chunk) items each): 8 CTAs per SM put a whole decode batch
+// in one wave (Mixtral B=827: 0.44 vs 0.47 ms per forward with one item per thread)
+int rope_threads(int H, int hd) { return std::min(256, (H * (hd / 8) + 31) / 32 * 32); }
 }  // namespace
 
 int mgb_rope_append_gqa(const void* qkv, int T, int seq0, const int* positions, const float* cos_t,
