@@ -188,9 +188,31 @@ def cpu_layer_sample(arch, B: int, ctx: int, reps: int, threads: int) -> tuple[f
         orc.layer_forward(li, x, ctx - 1)
         times.append(time.perf_counter() - t0)
     t_layer = statistics.median(times[1:])
-    sample = (f"oracle/moe_ref.py {name}: one {a.name} MoE decoder layer, B={B} sequences, context {ctx}, "
-              f"bf16 torch-CPU, median of {reps}; tokens/s = B / (t_layer x {a.layers} layers)")
+    sample = (f"oracle/moe_ref.py {name}: one {a.name} MoE decoder layer, B={B} sequences (the run's batch), "
+              f"context {ctx}, bf16 torch-CPU on {threads} threads of {_cpu_model()}, median of {reps}; "
+              f"tokens/s = B / (t_layer x {a.layers} layers)")
     return B / (t_layer * a.layers), sample
+
+
+def _cpu_model() -> str:
+    """Host CPU model and the matrix/vector extensions torch's CPU kernels can use."""
+    name, flags = "unknown CPU", set()
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name") and name == "unknown CPU":
+                    name = line.split(":", 1)[1].strip()
+                elif line.startswith("flags") and not flags:
+                    flags = set(line.split(":", 1)[1].split())
+    except OSError:
+        pass
+    ext = [x for x in ("avx512f", "avx512_bf16", "amx_bf16") if x in flags]
+    return f"{name} ({', '.join(ext) or 'no AVX-512'})"
+
+
+_BASELINE_CFG = {"mixtral-8x7b": "BASELINE configs[1]", "deepseek-v2-lite": "BASELINE configs[2], 1 GPU",
+                 "tiny-mixtral": "BASELINE configs[0] model", "mixtral-8x22b": "BASELINE configs[3] model",
+                 "deepseek-v2-236b": "BASELINE configs[4] model"}
 
 
 def _workload_config(args, arch, world: int) -> dict:
@@ -199,7 +221,7 @@ def _workload_config(args, arch, world: int) -> dict:
 
     plan = resident_plan(arch, args.prompt_len, args.decode_len, B=args.batch, reserve_bytes=args.reserve_gb << 30)
     return {"workload": f"{arch.name} decode phase, prompt {args.prompt_len} / gen {args.decode_len}, 1 B200 resident "
-                        f"({'BASELINE configs[1]' if arch.name == 'mixtral-8x7b' else 'BASELINE configs[2] shape'});"
+                        f"({_BASELINE_CFG.get(arch.name, 'not a BASELINE config')});"
                         f" step = {args.decode_len} decode forwards of B={plan.B} sequences",
             "batch": plan.B, "b_a": plan.b_a, "b_e": plan.b_e, "kv_policy": "resident (paged, HBM)",
             "parallelism": f"replicas x{world}", "l2": "inputs larger than L2 (all weights stream from HBM every forward)"}
@@ -212,7 +234,8 @@ def run_reference(args, dist, rank, world) -> None:
         return
     arch = get_arch(args.config)
     threads = os.cpu_count() or 1
-    B = args.cpu_batch
+    cfg = _workload_config(args, arch, world)
+    B = args.cpu_batch or cfg["batch"]  # the GPU arm's batch (one layer at the run's B)
     ctx = args.prompt_len + args.decode_len // 2
     vals = []
     sample = ""
@@ -227,8 +250,9 @@ def run_reference(args, dist, rank, world) -> None:
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / max(1, args.steps),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic", "config": _workload_config(args, arch, world),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+            "data": "synthetic", "config": cfg,
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
+                             "cpu_model": _cpu_model(), "batch": B},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -298,7 +322,7 @@ def run_ours(args, dist, rank, world) -> None:
         eng.reset(args.prompt_len)
         eng.buf.next_ids.copy_(first_pinned, non_blocking=True)
         for _ in range(N):
-            eng.graph.replay()
+            eng.run_step()  # graph replay (host position checked against the planned context)
 
     for _ in range(args.warmup):
         one_step()
@@ -422,9 +446,10 @@ def run_ours(args, dist, rank, world) -> None:
     }
     if rank == 0:
         if args.cpu_baseline:
-            v, sample = cpu_layer_sample(arch, args.cpu_batch, int(ctx_avg), 2, os.cpu_count() or 1)
+            cb = args.cpu_batch or B
+            v, sample = cpu_layer_sample(arch, cb, int(ctx_avg), 2, os.cpu_count() or 1)
             line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-                                    "sample": sample}
+                                    "sample": sample, "cpu_model": _cpu_model(), "batch": cb}
         print(json.dumps(line), flush=True)
 
 
@@ -440,7 +465,7 @@ def main():
     ap.add_argument("--decode-len", type=int, default=256)
     ap.add_argument("--reserve-gb", type=int, default=14)
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--cpu-batch", type=int, default=64)
+    ap.add_argument("--cpu-batch", type=int, default=None, help="CPU arm batch (default: the GPU arm's B)")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--no-incl-prefill", dest="incl_prefill", action="store_false",
                     help="skip the batched-prefill pass behind the incl_prefill figure")

@@ -161,6 +161,9 @@ def gqa_decode_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, impl
     impl="sdpa" (HF's default attn_implementation): scores, softmax and P.V in fp32, one bf16
     rounding of the output.  impl="eager" (modeling_mixtral.py:269-291): bf16 scores and bf16 P."""
     B, Hq, hd = q.shape
+    if B > 128:  # bounded temporaries at bench batch sizes (sequences are independent)
+        return torch.cat([gqa_decode_attention(q[b:b + 128], k[b:b + 128], v[b:b + 128], impl)
+                          for b in range(0, B, 128)])
     G = Hq // k.shape[1]
     kk = k.repeat_interleave(G, dim=1)
     vv = v.repeat_interleave(G, dim=1)
@@ -372,6 +375,36 @@ class DeepseekV2Oracle:
         self.a, self.w = arch, weights
         self.kc = [None] * arch.layers
         self.vc = [None] * arch.layers
+        # latent caches (c [B, ctx, R] normed, k_pe [B, ctx, r] rotated): when set for a layer, that
+        # layer attends in the latent form (`_latent_attention`) instead of per-head K/V caches
+        self.lat = [None] * arch.layers
+
+    def set_latent(self, layer: int, c: torch.Tensor, k_pe: torch.Tensor) -> None:
+        self.lat[layer] = (c, k_pe)
+
+    def _latent_attention(self, l: int, query_nope, q_pe, c, k_pe, B: int) -> torch.Tensor:
+        """HF DeepseekV2Attention (modeling_deepseek_v2.py:337-396) over a latent cache, evaluated
+        in fp32 by associativity instead of materialising per-head K/V for the whole context:
+        q.k_h = (q_nope W_UK_h) . c + q_pe . k_pe and o_h = (P c) W_UV_h^T, with
+        kv_b_proj = [W_UK_h ; W_UV_h] per head (:356-370).  Exact arithmetic equals HF's; HF rounds
+        k_nope / v to bf16 first, which the bf16 tolerance covers.  One bf16 rounding of o."""
+        a, W = self.a, self.w.layers[l]
+        H, nope, rope, vd, R = a.n_heads, a.qk_nope_dim, a.qk_rope_dim, a.v_head_dim, a.kv_lora_rank
+        c0, pe0 = self.lat[l]
+        self.lat[l] = (torch.cat([c0, c[:, None]], 1), torch.cat([pe0, k_pe.view(B, 1, rope)], 1))
+        cc, pp = self.lat[l]
+        kvb = W["kv_b"].float().view(H, nope + vd, R)
+        w_uk, w_uv = kvb[:, :nope], kvb[:, nope:]                     # [H, nope, R], [H, vd, R]
+        scale = (nope + rope) ** -0.5
+        out = torch.empty(B, H, vd)
+        for b0 in range(0, B, 256):                                   # bounded fp32 temporaries
+            b1 = min(B, b0 + 256)
+            q_lat = torch.einsum("bhn,hnr->bhr", query_nope[b0:b1].float(), w_uk)
+            s = (torch.einsum("bhr,btr->bht", q_lat, cc[b0:b1].float())
+                 + torch.einsum("bhr,btr->bht", q_pe[b0:b1].float(), pp[b0:b1].float())) * scale
+            o_lat = torch.einsum("bht,btr->bhr", torch.softmax(s, dim=-1), cc[b0:b1].float())
+            out[b0:b1] = torch.einsum("bhr,hvr->bhv", o_lat, w_uv)
+        return out.reshape(B, H * vd).to(BF16)
 
     def attention(self, l: int, h: torch.Tensor, pos: int, trace: dict | None = None) -> torch.Tensor:
         a, W = self.a, self.w.layers[l]
@@ -386,9 +419,16 @@ class DeepseekV2Oracle:
         ckv = F.linear(h, W["kv_a"])
         c, k_pe = ckv[:, :a.kv_lora_rank], ckv[:, a.kv_lora_rank:]
         c = rmsnorm(c, W["kv_a_norm"], a.rms_eps)
+        posv = torch.full((B,), pos)
+        if self.lat[l] is not None:
+            q_pe = rope_interleaved(q_pe, posv, a.rope_theta)
+            k_pe = rope_interleaved(k_pe.view(B, 1, rope), posv, a.rope_theta).view(B, rope)
+            o = self._latent_attention(l, q_nope, q_pe, c, k_pe, B)
+            if trace is not None:
+                trace.update(c=c, k_pe=k_pe, q_nope=q_nope, q_pe=q_pe, attn=o)
+            return F.linear(o, W["wo"])
         kvb = F.linear(c, W["kv_b"]).view(B, H, nope + vd)
         k_nope, v = kvb[..., :nope], kvb[..., nope:]
-        posv = torch.full((B,), pos)
         q_pe = rope_interleaved(q_pe, posv, a.rope_theta)
         k_pe = rope_interleaved(k_pe.view(B, 1, rope), posv, a.rope_theta)
         key = torch.cat([k_nope, k_pe.expand(B, H, rope)], dim=-1)

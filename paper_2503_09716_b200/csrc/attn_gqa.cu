@@ -169,6 +169,20 @@ decode_attn_gqa_kernel(const __nv_bfloat16* __restrict__ q,       // [B, Hkv*G, 
         o[n][0] *= alpha;
         o[n][1] *= alpha;
       }
+      // V rows past the sequence end (last, partial page) may hold any bits -- an offloaded host
+      // page store or a reused staging page -- and P = 0 there would still give 0 * NaN = NaN in
+      // the MMA: zero this warp's invalid V rows in the stage before P.V reads them
+      if (n_valid < 16) {
+        const int first = n_valid < 0 ? 0 : n_valid;
+        uint8_t* vb = ring + stage * S::kStageBytes + S::kTileBytes;
+        for (int i = lane; i < (16 - first) * (HD / 8); i += 32) {
+          const int tk = tok0 + first + i / (HD / 8), c = i % (HD / 8);
+          *reinterpret_cast<uint4*>(vb + (c * kPage + tk) * 16) = make_uint4(0u, 0u, 0u, 0u);
+        }
+        // generic-proxy writes, then the producer's next bulk copy (async proxy) into this stage
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+      }
       // P as the A operand (k = 16 tokens): rows >= G are zero
       const uint32_t pa0 = row_ok ? pack_bf16x2(p0, p1) : 0u;
       const uint32_t pa2 = row_ok ? pack_bf16x2(p2, p3) : 0u;
@@ -229,13 +243,7 @@ template <int HD, int G>
 int launch_gqa(const void* q, const void* kc, const void* vc, const int* bt, int max_pages, const int* lens, int B,
                int Hkv, float scale, void* out, cudaStream_t st) {
   using S = GqaSmem<HD, G>;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(decode_attn_gqa_kernel<HD, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)S::kBytes) != cudaSuccess)
-      return MGB_ECUDA;
-    attr = true;
-  }
+  if (const int rc = mgb_host::ensure_max_smem((const void*)decode_attn_gqa_kernel<HD, G>, (int)S::kBytes)) return rc;
   const int items = B * Hkv;
   int grid = 2 * mgb_host::num_sms();
   if (grid > items) grid = items;

@@ -460,13 +460,7 @@ template <int R, int RP>
 int launch_mla(const void* q_lat, const void* q_pe, const void* cache, const int* bt, int max_pages, const int* lens,
                int B, int H, float scale, void* out, cudaStream_t st) {
   using C = MlaCfg<R, RP>;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(decode_attn_mla_kernel<R, RP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)C::kSmem) != cudaSuccess)
-      return MGB_ECUDA;
-    attr = true;
-  }
+  if (const int rc = mgb_host::ensure_max_smem((const void*)decode_attn_mla_kernel<R, RP>, (int)C::kSmem)) return rc;
   const int items = B * ((H + kMlaHeads - 1) / kMlaHeads);
   int grid = mgb_host::num_sms();
   if (grid > items) grid = items;
@@ -508,6 +502,7 @@ __global__ void mla_append_kernel(const __nv_bfloat16* __restrict__ q,    // [B,
                                   __nv_bfloat16* __restrict__ q_pe_out, int* __restrict__ seq_lens) {
   const int b = blockIdx.x;
   const int pos = positions[b];
+  if (pos < 0 || pos >= max_pages * kMlaPage) return;  // past the planned context: no page to write
   const int D = R + RP;
   __shared__ float red[32];
   const __nv_bfloat16* row = ckv + (size_t)b * D;

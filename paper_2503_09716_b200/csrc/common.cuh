@@ -387,4 +387,6 @@ CUresult encode_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner,
 CUresult encode_tmap_bf16(CUtensorMap* map, const void* base, int rank, const uint64_t* dims,
                           const uint64_t* strides_bytes, const uint32_t* box, bool swizzle128 = false);
 int num_sms();
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device); MGB_OK or MGB_ECUDA.
+int ensure_max_smem(const void* fn, int bytes);
 }  // namespace mgb_host

@@ -120,6 +120,9 @@ __global__ void rope_append_gqa_kernel(const __nv_bfloat16* __restrict__ qkv, in
   const int nch = hd >> 3, H = Hq + 2 * Hkv;
   const int seq = seq0 + t;
   const int pos = positions[seq];
+  // a position past the planned context has no page (and no RoPE row): write nothing rather than
+  // index the next sequence's block-table row (the host refuses such steps, Engine.run_step)
+  if (pos < 0 || pos >= max_pages * kPageTok) return;
   const int page = block_table[(size_t)seq * max_pages + pos / kPageTok];
   const int slot = pos % kPageTok;
   if (seq_lens && threadIdx.x == 0) seq_lens[seq] = pos + 1;  // cache length after the append

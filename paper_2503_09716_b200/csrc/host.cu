@@ -4,6 +4,8 @@
 #include <cudaTypedefs.h>
 
 #include <mutex>
+#include <set>
+#include <utility>
 
 #include "common.cuh"
 
@@ -61,6 +63,23 @@ int num_sms() {
     if (n <= 0) n = mgb::kNumSMsB200;
   }
   return n;
+}
+
+int ensure_max_smem(const void* fn, int bytes) {
+  // cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device attribute: remember (kernel,
+  // device) pairs, not kernels, so a process driving several GPUs configures each one
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return MGB_ECUDA;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count({fn, dev})) return MGB_OK;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) {
+    launch_status();  // record the error for mgb_last_error
+    return MGB_ECUDA;
+  }
+  done.insert({fn, dev});
+  return MGB_OK;
 }
 
 namespace {

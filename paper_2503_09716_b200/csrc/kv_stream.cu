@@ -33,6 +33,7 @@ __global__ void kv_token_copy_kernel(const uint8_t* __restrict__ src, const int*
   const int u = v / vec_per_unit, w = v - u * vec_per_unit;
   const int pos = positions[b];
   const int pg = pos / page_tokens, slot = pos - pg * page_tokens;
+  if (pos < 0 || pg >= src_max_pages || pg >= dst_max_pages) return;  // past the planned context
   const long long off = (long long)u * unit_stride + (long long)slot * unit_bytes + (long long)w * 16;
   const long long sp = src_table[(size_t)b * src_max_pages + pg];
   const long long dp = dst_table[(size_t)b * dst_max_pages + pg];

@@ -503,14 +503,10 @@ template <bool GATED, bool PAIR, bool ROWPTR>
 int launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmB8, const int* offsets, int E, int MT, int K,
                    int rows_per_expert, int half_rows, void* out, int ldo, bool balanced, const long long* row_ptr,
                    cudaStream_t stream) {
-  static bool attr = false;
   if (PAIR) {
-    if (!attr) {
-      if (cudaFuncSetAttribute(mgb::moe_gemm_pair_kernel<GATED, ROWPTR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               mgb::pair_smem<GATED>()) != cudaSuccess)
-        return MGB_ECUDA;
-      attr = true;
-    }
+    if (const int rc = mgb_host::ensure_max_smem((const void*)mgb::moe_gemm_pair_kernel<GATED, ROWPTR>,
+                                                 mgb::pair_smem<GATED>()))
+      return rc;
     const int grid = mgb_host::num_sms() & ~1;
     // pair MMA N: a multiple of 16 (each CTA holds N/2 token rows, whole 8-row swizzle atoms);
     // MGB_PAIR_NALIGN=32 pads further
@@ -522,12 +518,9 @@ int launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtenso
         tmA, tmB, tmB8, offsets, E, MT / 2, K, rows_per_expert, half_rows, reinterpret_cast<__nv_bfloat16*>(out), ldo,
         balanced, row_ptr, nalign);
   } else {
-    if (!attr) {
-      if (cudaFuncSetAttribute(mgb::moe_gemm_kernel<GATED, ROWPTR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               mgb::gemm_smem<GATED>()) != cudaSuccess)
-        return MGB_ECUDA;
-      attr = true;
-    }
+    if (const int rc = mgb_host::ensure_max_smem((const void*)mgb::moe_gemm_kernel<GATED, ROWPTR>,
+                                                 mgb::gemm_smem<GATED>()))
+      return rc;
     mgb::moe_gemm_kernel<GATED, ROWPTR><<<mgb_host::num_sms(), mgb::Epi<GATED>::kThreads, mgb::gemm_smem<GATED>(),
                                           stream>>>(
         tmA, tmB, offsets, E, MT, K, rows_per_expert, half_rows, reinterpret_cast<__nv_bfloat16*>(out), ldo, balanced,

@@ -120,6 +120,10 @@ class Engine:
         # rows are dispatched/combined over torch.distributed; the host-side split sizes make the
         # EP step eager (no CUDA graph) in this build
         self.ep = ep if (ep is not None and ep.world > 1) else None
+        if ep is not None and self.plan.s_params < self.spec.model_bytes:
+            # the EP path slices this rank's expert range out of the resident expert tensors; streamed
+            # experts live in slots indexed by copy order, which the dispatch offsets do not describe
+            raise ValueError("expert parallelism needs HBM-resident weights (plan.s_params = model bytes)")
         self.use_graph = use_graph and self.ep is None
         # ---- job list (structure only; durations are measured, not modelled) ----
         # ---- CPU attention share (omega > 0): GQA over the host page store on the host cores ----
@@ -456,6 +460,12 @@ class Engine:
         for the host node (csrc/cpu_attn.cpp)."""
         a, n = self.arch, self.n_cpu
         width = a.n_heads * a.head_dim
+        # the host kernel's limits (csrc/cpu_attn.cpp): refuse here, where the error is visible, instead
+        # of a host node that only sets desc.status inside a replayed graph
+        G = a.n_heads // a.n_kv_heads
+        if a.n_heads % a.n_kv_heads or G > 16 or a.head_dim % 8 or a.head_dim // 8 > 16 or self.page % 4:
+            raise ValueError(f"CPU attention share: unsupported shape (G={G}, head_dim={a.head_dim}, "
+                             f"page={self.page})")
         self.cpu_q = torch.empty(n, width, dtype=BF16, pin_memory=True)
         self.cpu_lens_bytes = (4 * n + 15) // 16 * 16  # copied in whole 16-byte units
         self.cpu_lens = torch.empty(self.cpu_lens_bytes // 4, dtype=torch.int32, pin_memory=True)
@@ -836,6 +846,14 @@ class Engine:
         self._primed = False
         self.reset(self.prompt_len)
 
+    def check_cpu_attention(self) -> None:
+        """Raise if a CPU-attention host node reported invalid input (desc.status != 0); call after
+        the steps have completed (the status is written by the host node when it runs)."""
+        if self.n_cpu > 0:
+            bad = [l for l, dsc in enumerate(self.cpu_desc) if dsc.status != 0]
+            if bad:
+                raise RuntimeError(f"CPU attention failed (status != 0) in layers {bad}")
+
     def decode(self, first_tokens: torch.Tensor, n_steps: int) -> torch.Tensor:
         """Decode phase through the public API: host `first_tokens` [B] (pinned H2D), n_steps
         greedy forwards from the current positions; returns host int64 [B, n_steps]."""
@@ -844,7 +862,9 @@ class Engine:
         self.buf.step.zero_()
         for _ in range(n_steps):
             self.run_step()
-        return self.out_tokens[:, :n_steps].to("cpu", non_blocking=False)
+        out = self.out_tokens[:, :n_steps].to("cpu", non_blocking=False)
+        self.check_cpu_attention()
+        return out
 
     def can_prefill(self) -> bool:
         """Batched prefill: both families, weights resident (chunk-major) or offloaded (layer-major,
@@ -860,7 +880,9 @@ class Engine:
             return self.kv[l], self.block_table, s0
         pe, pps = self.page_elems, self.pps
         if getattr(self, "_pf_stage_pages", 0) < n * pps:
-            self._pf_stage = [torch.empty(n * pps * pe, dtype=BF16, device=self.device) for _ in self.kv[l]]
+            # zeros: the flush copies whole pages, so positions >= P of every staged page reach the host
+            # store; decode reads those rows (as P = 0 columns) and they must never hold NaN / Inf bits
+            self._pf_stage = [torch.zeros(n * pps * pe, dtype=BF16, device=self.device) for _ in self.kv[l]]
             self._pf_stage_table = torch.arange(n * pps, dtype=torch.int32, device=self.device).view(n, pps)
             self._pf_stage_pages = n * pps
         return self._pf_stage, self._pf_stage_table, 0
@@ -1144,6 +1166,7 @@ class Engine:
         for _ in range(max_new_tokens - 1):
             self.run_step()
         gen = self.out_tokens[:, P - 1:P - 1 + max_new_tokens].cpu()
+        self.check_cpu_attention()
         return torch.cat([input_ids.cpu().to(torch.int64), gen], dim=1)
 
     def debug_forward(self, tokens: torch.Tensor, pos: int) -> dict:
@@ -1176,6 +1199,7 @@ class Engine:
             t1 = torch.cuda.Event(enable_timing=True)
             t1.record(self.stream)
         torch.cuda.synchronize()
+        self.check_cpu_attention()
         for t, s in zip((self.buf.positions, self.buf.step, self.buf.next_ids, self.buf.seq_lens), saved):
             t.copy_(s)
         jobs = self.schedule.jobs

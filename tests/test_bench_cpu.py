@@ -15,7 +15,7 @@ def _args(**kw):
 
 
 def test_workload_config_is_the_planners_resident_batch():
-    for name, tag in (("mixtral-8x7b", "BASELINE configs[1]"), ("deepseek-v2-lite", "BASELINE configs[2] shape")):
+    for name, tag in (("mixtral-8x7b", "BASELINE configs[1]"), ("deepseek-v2-lite", "BASELINE configs[2], 1 GPU")):
         arch = get_arch(name)
         B = resident_plan(arch, 512, 256, reserve_bytes=14 << 30).B
         cfg = bench._workload_config(_args(), arch, 8)

@@ -171,10 +171,11 @@ def test_add_rmsnorm():
     assert R.rel_err(y.cpu(), ref) <= 1e-2
 
 
-def _paged_kv(kc, vc, B, Hkv, hd, ctx, page, pps):
-    """dense [B,Hkv,ctx,hd] -> engine page layout (K and V chunk-major [hd/8][page][8])."""
-    kp = torch.zeros(B * pps, Hkv, hd // 8, page, 8, dtype=BF16)
-    vp = torch.zeros(B * pps, Hkv, hd // 8, page, 8, dtype=BF16)
+def _paged_kv(kc, vc, B, Hkv, hd, ctx, page, pps, tail=0.0):
+    """dense [B,Hkv,ctx,hd] -> engine page layout (K and V chunk-major [hd/8][page][8]); rows past
+    ctx hold `tail` (the kernel must ignore them, NaN / Inf included)."""
+    kp = torch.full((B * pps, Hkv, hd // 8, page, 8), tail, dtype=BF16)
+    vp = torch.full((B * pps, Hkv, hd // 8, page, 8), tail, dtype=BF16)
     for b in range(B):
         for t in range(ctx):
             pg, s = b * pps + t // page, t % page
@@ -183,16 +184,18 @@ def _paged_kv(kc, vc, B, Hkv, hd, ctx, page, pps):
     return kp.reshape(-1), vp.reshape(-1)
 
 
-@pytest.mark.parametrize("B,Hq,Hkv,hd,ctx", [(3, 32, 8, 128, 1), (5, 32, 8, 128, 200), (4, 8, 2, 32, 130),
-                                             (2, 48, 8, 128, 64)])
-def test_decode_attn_gqa(B, Hq, Hkv, hd, ctx):
+@pytest.mark.parametrize("B,Hq,Hkv,hd,ctx,tail", [(3, 32, 8, 128, 1, 0.0), (5, 32, 8, 128, 200, 0.0),
+                                                  (4, 8, 2, 32, 130, 0.0), (2, 48, 8, 128, 64, 0.0),
+                                                  (3, 32, 8, 128, 70, float("nan")), (2, 32, 8, 128, 17, float("inf")),
+                                                  (4, 8, 2, 32, 100, float("nan"))])
+def test_decode_attn_gqa(B, Hq, Hkv, hd, ctx, tail):
     ops = _ops()
     page = ops.kv_page_size()
     pps = math.ceil(ctx / page)
     q = uniform_bf16((B, Hq, hd), 4, 1, 1.0)
     kc = uniform_bf16((B, Hkv, ctx, hd), 4, 2, 1.0)
     vc = uniform_bf16((B, Hkv, ctx, hd), 4, 3, 1.0)
-    kp, vp = _paged_kv(kc, vc, B, Hkv, hd, ctx, page, pps)
+    kp, vp = _paged_kv(kc, vc, B, Hkv, hd, ctx, page, pps, tail)
     bt = torch.arange(B * pps, dtype=torch.int32).view(B, pps)
     lens = torch.full((B,), ctx, dtype=torch.int32)
     out = torch.zeros(B, Hq * hd, dtype=BF16, device="cuda")

@@ -69,7 +69,11 @@ def test_kv_offload_generate_equals_resident(family):
     for graph in (False, True):
         eng = Engine(A, plan, prompt_len=P, decode_len=N, use_graph=graph, kv_policy="offload", kv_ring_slots=2)
         assert not eng.kv[0][0].is_cuda and eng.kv_ring_n == 2
+        # host pages start as garbage: every row a step reads past a sequence's length must be
+        # ignored (0 * NaN would poison P.V), so fill the whole host store with NaN first
+        eng.kv_host.fill_(float("nan"))
         assert torch.equal(eng.generate(ids, N, prefill=False), ref)
+        eng.kv_host.fill_(float("nan"))
         assert torch.equal(eng.generate(ids, N), ref_pf)
 
 

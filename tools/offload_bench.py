@@ -87,19 +87,24 @@ eng.reset(640)
 eng.buf.next_ids.random_(0, arch.vocab)
 setup_s = time.time() - t0
 recs, rep = eng.trace_step()
+# replays go through Engine.run_step (host position checked against the planned context); every
+# timed block restarts at the same mid-decode position
 eng.capture()
-eng.graph.replay()
-t = timed(eng.graph.replay, args.steps)
+eng.reset(640)
+eng.run_step()
+t = timed(eng.run_step, args.steps)
 eng.copies_enabled = False
 eng.graph = None
 eng.capture()
-eng.graph.replay()
-t_gpu = timed(eng.graph.replay, args.steps)
+eng.reset(640)
+eng.run_step()
+t_gpu = timed(eng.run_step, args.steps)
 eng.copies_enabled, eng.compute_enabled = True, False
 eng.graph = None
 eng.capture()
-eng.graph.replay()
-t_h2d = timed(eng.graph.replay, args.steps)  # the same step's copies alone (measured, same buffers)
+eng.reset(640)
+eng.run_step()
+t_h2d = timed(eng.run_step, args.steps)  # the same step's copies alone (measured, same buffers)
 moved = rep["bytes_htod"]
 # exposed = step time beyond the longer of the two; a step no slower than its copies alone hides
 # all of its compute (overlap 1)
