@@ -248,6 +248,8 @@ class Engine:
         self._fork, self._join = torch.cuda.Event(), torch.cuda.Event()
         self.events = {i: torch.cuda.Event() for i in self.need_event}
         self.trace_events: dict | None = None  # job id -> (start, end) timing events (eager trace mode)
+        self._trace_counts: torch.Tensor | None = None  # [layers, E] routed rows per expert (trace mode)
+        self._forced_logits: torch.Tensor | None = None  # [layers, B, E] router input (force_routing)
         self.kernel_launches_per_step = self._count_launches()
         self.host_pos = 0
 
@@ -549,6 +551,8 @@ class Engine:
                 if te is not None:
                     e1.record(st)
                     te[j.id] = (e0, e1)
+                    if j.kind == "router" and self._trace_counts is not None:  # outside the timed span
+                        self._trace_counts[l].copy_(self.rws.counts)
                 if j.id in self.need_event:
                     self.events[j.id].record(st)
 
@@ -619,9 +623,13 @@ class Engine:
             if l >= a.first_k_dense:
                 # fp32 router logits (HF: F.linear(x.float(), W.float()), modeling_deepseek_v2.py:125) as a
                 # bf16 tensor-core GEMM with fp32 output (exact products, fp32 accumulation)
-                torch.mm(b.h, W["router"].t(), out_dtype=torch.float32, out=m["logits_r"])
+                lg = m["logits_r"]
+                if self._forced_logits is not None:
+                    lg = self._forced_logits[l]
+                else:
+                    torch.mm(b.h, W["router"].t(), out_dtype=torch.float32, out=lg)
                 ops.router_topk(None, None, self.rws, a.top_k, a.router_mode, a.routed_scaling, a.n_group,
-                                a.topk_group, logits_in=m["logits_r"])
+                                a.topk_group, logits_in=lg)
                 ops.permute(b.h, self.rws, b.x_perm)
                 if self.debug_taps is not None:
                     self.debug_taps.update(h2=b.h.clone(), topk_idx=self.rws.topk_idx.clone())
@@ -709,7 +717,10 @@ class Engine:
             torch.mm(b.attn, W["wo"].t(), out=b.o)
             ops.add_rmsnorm(b.x, W["ln2"], a.rms_eps, b.h, delta=b.o, x_out=b.x)
         elif j.kind == "router":
-            if self.router_logits == "cublas":
+            if self._forced_logits is not None:
+                ops.router_topk(None, None, self.rws, a.top_k, a.router_mode, a.routed_scaling, a.n_group,
+                                a.topk_group, logits_in=self._forced_logits[l])
+            elif self.router_logits == "cublas":
                 # gate GEMM on the tensor cores with fp32 output; the router kernel rounds it to
                 # bf16 exactly as HF's bf16 F.linear does (modeling_mixtral.py:111)
                 torch.mm(b.h, W["router"].t(), out_dtype=torch.float32, out=self.logits_r)
@@ -845,6 +856,35 @@ class Engine:
         torch.cuda.synchronize()
         self._primed = False
         self.reset(self.prompt_len)
+
+    def force_routing(self, counts: list | None) -> None:
+        """Route every decode step by prescribed per-expert token counts instead of the gate GEMM
+        (counts[l][e] rows of layer l go to expert e, sum B * top_k) -- the reference simulator's
+        routing stand-in (exec_sim.py:61-81, `simulate.sample_routing`), so a measured step and
+        `simulate_plan` see the same expert groups.  The assignment lists expert e counts[l][e]
+        times in expert order and hands entry i to token i % B as its (i // B)-th choice; a token
+        never gets one expert twice because counts[l][e] <= B.  The router kernel then runs on
+        logits that are 0 for a token's experts and -1e4 elsewhere.  None restores the gate."""
+        if counts is None:
+            self._forced_logits = None
+            return
+        a, B, k, E = self.arch, self.B, self.arch.top_k, self.arch.n_experts
+        if a.router_mode == 2:
+            raise NotImplementedError("forced routing under group-limited selection")
+        if len(counts) != a.layers:
+            raise ValueError(f"need counts for {a.layers} layers, got {len(counts)}")
+        lg = torch.full((a.layers, B, E), -1e4, dtype=torch.float32)
+        for l, row in enumerate(counts):
+            row = [int(c) for c in row]
+            if len(row) != E or sum(row) != B * k or min(row) < 0:
+                raise ValueError(f"layer {l}: counts must be {E} non-negative ints summing to B*top_k={B * k}")
+            if max(row) > B:
+                raise ValueError(f"layer {l}: an expert cannot take {max(row)} of {B} tokens (each token picks it once)")
+            flat = torch.repeat_interleave(torch.arange(E), torch.tensor(row))
+            tok = torch.arange(B * k) % B
+            lg[l, tok, flat] = 0.0
+        self._forced_logits = lg.to(self.device)
+        self.graph = None  # the captured step read the gate GEMM's output
 
     def check_cpu_attention(self) -> None:
         """Raise if a CPU-attention host node reported invalid input (desc.status != 0); call after
@@ -1189,6 +1229,9 @@ class Engine:
         report carries SimReport-style busy / idle / bytes / makespan (exec_sim.py:84-110) plus the
         transfer/compute overlap 1 - (makespan - max(busy)) / min(busy)."""
         self.trace_events = {}
+        self._trace_counts = torch.zeros(self.arch.layers, self.arch.n_experts, dtype=torch.int32, device=self.device)
+        torch.cuda.synchronize()
+        torch.cuda.reset_peak_memory_stats(self.device)
         t0 = torch.cuda.Event(enable_timing=True)
         saved = [t.clone() for t in (self.buf.positions, self.buf.step, self.buf.next_ids, self.buf.seq_lens)]
         self.stream.wait_stream(torch.cuda.current_stream())
@@ -1214,6 +1257,12 @@ class Engine:
             if j.resource in nbytes:
                 nbytes[j.resource] += self._moved_bytes(j)
         self.trace_events = None
+        peak = float(torch.cuda.max_memory_allocated(self.device))
+        routed = self._trace_counts.cpu().tolist()
+        self._trace_counts = None
+        # layers without a router launch (DeepSeek's dense first layers) keep the schedule's counts
+        sched = self.schedule_counts()
+        expert_tokens = [routed[l] if self._has_router(l) else sched[l] for l in range(self.arch.layers)]
         recs.sort(key=lambda r: (r["time"], r["node"], r["action"] != "start"))
         makespan = t0.elapsed_time(t1) * 1e-3
         g, h = busy.get("gpu_compute", 0.0), busy.get("htod_link", 0.0)
@@ -1222,8 +1271,24 @@ class Engine:
                   "idle_fraction": {r: 1.0 - v / makespan for r, v in busy.items()},
                   "bytes_htod": nbytes["htod_link"], "bytes_dtoh": nbytes["dtoh_link"],
                   "htod_gbs": nbytes["htod_link"] / h / 1e9 if h > 0 else None,
-                  "throughput": self.B / makespan, "overlap": overlap}
+                  "throughput": self.B / makespan, "overlap": overlap,
+                  # SimReport fields (exec_sim.py:97-110): measured allocator peak of the step (every
+                  # HBM buffer the engine holds plus the step's transients), the routed rows per
+                  # expert and layer, and whether the peak exceeded the device
+                  "peak_gpu_bytes": peak, "oom_flag": peak > torch.cuda.get_device_properties(self.device).total_memory,
+                  "expert_tokens": expert_tokens,
+                  "mean_tokens_per_expert": sum(map(sum, expert_tokens)) / (len(expert_tokens) * self.arch.n_experts)}
         return recs, report
+
+    def _has_router(self, l: int) -> bool:
+        return not (self.mla and l < self.arch.first_k_dense)
+
+    def schedule_counts(self) -> list[list[int]]:
+        """Per-layer expert token counts the job list was built with (even split: the schedule's
+        default, offload_dag.py:173-185)."""
+        from .schedule import even_split
+
+        return [even_split(self.B * self.arch.top_k, self.arch.n_experts) for _ in range(self.arch.layers)]
 
     def job_trace(self) -> list[dict]:
         """The issued job list (kinds/labels/shapes), in submission order."""
