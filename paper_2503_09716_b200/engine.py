@@ -96,11 +96,29 @@ class Engine:
     """Greedy MoE decoding engine (Mixtral and DeepSeek-V2 families; HBM-resident or partly
     host-offloaded weights, paged KV in HBM, optional expert parallelism)."""
 
-    def __init__(self, arch: ModelArch | str, plan=None, *, prompt_len: int, decode_len: int, seed: int = 0,
+    def __init__(self, arch: ModelArch | str | None, plan=None, *, prompt_len: int, decode_len: int, seed: int = 0,
                  kv_policy: str = "resident", use_graph: bool = True, device: str = "cuda", ep=None,
-                 kv_ring_slots: int = 3, lookahead: bool = True):
+                 kv_ring_slots: int = 3, lookahead: bool = True, checkpoint=None):
+        """`checkpoint`: a HF safetensors checkpoint directory (checkpoint.py) to load the weights
+        from instead of the counter-based random init; `arch` None takes the architecture from its
+        config.json, an explicit arch may truncate the depth (layers <= the checkpoint's)."""
         if not torch.cuda.is_available():
             raise RuntimeError("the B200 engine needs a CUDA device (there is no CPU fallback)")
+        self.source = None
+        if checkpoint is not None:
+            from .checkpoint import open_checkpoint
+
+            self.source = open_checkpoint(checkpoint)
+            ck = self.source.arch
+            if arch is None:
+                arch = ck
+            else:
+                arch = get_arch(arch) if isinstance(arch, str) else arch
+                import dataclasses as _dc
+                if _dc.replace(arch, name=ck.name, layers=ck.layers, init_std=ck.init_std) != ck or arch.layers > ck.layers:
+                    raise ValueError(f"architecture {arch.name!r} does not match the checkpoint's config.json ({ck})")
+        elif arch is None:
+            raise ValueError("arch is required without a checkpoint")
         self.arch = get_arch(arch) if isinstance(arch, str) else arch
         if self.arch.family not in ("mixtral", "deepseek_v2"):
             raise NotImplementedError(f"unknown model family {self.arch.family!r}")
@@ -153,11 +171,11 @@ class Engine:
             from .offload import OffloadedWeights
             self.w = OffloadedWeights(a, self.spec, self.plan.s_params, self.plan.s_expert, seed=seed,
                                       extra_slots=self.lookahead_expert_slots, extra_dense=len(self.dense_buf_of),
-                                             device=device)
+                                      device=device, source=self.source)
         elif self.mla:
-            self.w = DeepseekDeviceWeights(a, seed=seed, device=device)
+            self.w = DeepseekDeviceWeights(a, seed=seed, device=device, source=self.source)
         else:
-            self.w = MixtralDeviceWeights(a, seed=seed, device=device)
+            self.w = MixtralDeviceWeights(a, seed=seed, device=device, source=self.source)
         d, k, f = a.hidden, a.top_k, a.moe_ffn
         bf = dict(dtype=BF16, device=device)
         i32 = dict(dtype=torch.int32, device=device)

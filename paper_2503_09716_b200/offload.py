@@ -20,8 +20,7 @@ import torch
 from .configs import ModelArch
 from .hostmem import pinned_empty
 from .planner import placement, ModelSpec
-from .weights import (DERIVED, TID_EMBED, TID_LM_HEAD, deepseek_layer, dense_keys, derive_views, fill_const_,
-                      fill_uniform_, mixtral_layer)
+from .weights import DERIVED, deepseek_layer, dense_keys, derive_views, global_tensors, mixtral_layer
 
 BF16 = torch.bfloat16
 
@@ -33,7 +32,7 @@ class OffloadedWeights:
     attention projections plus its shared experts (the reference's dense_bytes_per_layer)."""
 
     def __init__(self, arch: ModelArch, spec: ModelSpec, s_params: int, s_expert: int, seed: int = 0,
-                 device: str = "cuda", extra_slots: int = 0, extra_dense: int = 0):
+                 device: str = "cuda", extra_slots: int = 0, extra_dense: int = 0, source=None):
         a = arch
         d, f, E = a.hidden, a.moe_ffn, a.n_experts
         std = a.init_std
@@ -45,9 +44,7 @@ class OffloadedWeights:
         self.n_slots = s_expert // spec.expert_bytes if spec.expert_bytes else 0
         if self.place.uncached_expert_count > 0 and self.n_slots < 2:
             raise ValueError("offloaded experts need at least 2 expert slots (double buffering)")
-        self.embed = fill_uniform_(torch.empty(a.vocab, d, **bf), seed, TID_EMBED, std)
-        self.final_norm = fill_const_(torch.empty(d, **bf), 1.0)
-        self.lm_head = fill_uniform_(torch.empty(a.vocab, d, **bf), seed, TID_LM_HEAD, std)
+        self.embed, self.final_norm, self.lm_head = global_tensors(a, seed, device, source)
         build = deepseek_layer if a.is_mla else mixtral_layer
         self.dense_keys = dense_keys(a)
         self.dense_shapes: dict[str, tuple] | None = None
@@ -61,7 +58,8 @@ class OffloadedWeights:
         self.host_experts: list[torch.Tensor | None] = []
         moe_first = a.first_k_dense if a.is_mla else 0
         for l in range(a.layers):
-            L = build(a, l, seed, device)  # generated on the device (bit-identical to the resident build)
+            # generated on the device (bit-identical to the resident build), or loaded from a checkpoint
+            L = build(a, l, seed, device, source)
             if l >= moe_first and self.dense_shapes is None:
                 self.dense_shapes = {k: tuple(L[k].shape) for k in self.dense_keys}
                 self.dense_elems = sum(L[k].numel() for k in self.dense_keys)

@@ -36,10 +36,13 @@ def fill_const_(t: torch.Tensor, value: float) -> torch.Tensor:
     return t
 
 
-def mixtral_layer(a: ModelArch, l: int, seed: int, device: str = "cuda") -> dict:
+def mixtral_layer(a: ModelArch, l: int, seed: int, device: str = "cuda", source=None) -> dict:
     """Layer l of a Mixtral-family model in the engine's layout.  q/k/v projections are stored
     fused as one [Hq*hd + 2*Hkv*hd, d] matrix (rows = wq | wk | wv), each part generated with its
-    own tensor id so it equals the oracle's separate wq/wk/wv."""
+    own tensor id so it equals the oracle's separate wq/wk/wv.  `source` (checkpoint.Checkpoint)
+    loads the layer from a safetensors checkpoint instead of generating it."""
+    if source is not None:
+        return {k: v.to(device) for k, v in source.layer(l).items()}
     d, hd = a.hidden, a.head_dim
     qd, kvd = a.n_heads * hd, a.n_kv_heads * hd
     std = a.init_std
@@ -62,21 +65,29 @@ def mixtral_layer(a: ModelArch, l: int, seed: int, device: str = "cuda") -> dict
 class _DeviceWeights:
     """All weights HBM-resident, generated layer by layer by the family's layer builder."""
 
-    def __init__(self, arch: ModelArch, seed: int = 0, device: str = "cuda"):
+    def __init__(self, arch: ModelArch, seed: int = 0, device: str = "cuda", source=None):
         a = arch
         bf = dict(dtype=torch.bfloat16, device=device)
         self.arch = a
-        self.embed = fill_uniform_(torch.empty(a.vocab, a.hidden, **bf), seed, TID_EMBED, a.init_std)
-        self.final_norm = fill_const_(torch.empty(a.hidden, **bf), 1.0)
-        self.lm_head = fill_uniform_(torch.empty(a.vocab, a.hidden, **bf), seed, TID_LM_HEAD, a.init_std)
+        self.embed, self.final_norm, self.lm_head = global_tensors(a, seed, device, source)
         build = deepseek_layer if a.is_mla else mixtral_layer
-        self.layers = [build(a, l, seed, device) for l in range(a.layers)]
+        self.layers = [build(a, l, seed, device, source) for l in range(a.layers)]
 
     def nbytes(self) -> int:
         n = self.embed.nbytes + self.final_norm.nbytes + self.lm_head.nbytes
         for L in self.layers:
             n += sum(t.nbytes for k, t in L.items() if k not in DERIVED)
         return n
+
+
+def global_tensors(a: ModelArch, seed: int, device: str, source=None):
+    """(embed, final norm, lm_head): generated, or loaded from a checkpoint `source`."""
+    if source is not None:
+        return source.embed().to(device), source.final_norm().to(device), source.lm_head().to(device)
+    bf = dict(dtype=torch.bfloat16, device=device)
+    return (fill_uniform_(torch.empty(a.vocab, a.hidden, **bf), seed, TID_EMBED, a.init_std),
+            fill_const_(torch.empty(a.hidden, **bf), 1.0),
+            fill_uniform_(torch.empty(a.vocab, a.hidden, **bf), seed, TID_LM_HEAD, a.init_std))
 
 
 class MixtralDeviceWeights(_DeviceWeights):
@@ -95,10 +106,12 @@ def ds_tid(layer: int, name: str) -> int:
     return LAYER_BASE + LAYER_STRIDE * layer + DS_SLOT[name]
 
 
-def deepseek_layer(a: ModelArch, l: int, seed: int, device: str = "cuda") -> dict:
+def deepseek_layer(a: ModelArch, l: int, seed: int, device: str = "cuda", source=None) -> dict:
     """Layer l of a DeepSeek-V2-family model in HF layouts (q_proj or q_a/q_b, kv_a_proj_with_mqa,
     kv_b_proj, o_proj; routed experts [E,2f,d]/[E,d,f]; shared experts and the dense first layers
     as fused gate|up [2f,d] + down [d,f]).  Tensor ids mirror oracle/moe_ref.py DS_SLOT."""
+    if source is not None:
+        return derive_views(a, {k: v.to(device) for k, v in source.layer(l).items()})
     d, H = a.hidden, a.n_heads
     qk = a.qk_nope_dim + a.qk_rope_dim
     std = a.init_std

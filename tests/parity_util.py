@@ -6,8 +6,10 @@ oracle after every layer, and applies the north_star bar per layer (BASELINE.jso
 error 2e-2 per layer"):
 
   - routing: the engine's top-k indices are bit-exact vs the oracle router run on the engine's own
-    router logits, and the engine-vs-oracle expert sets (each side routing its
-    own hidden state) agree on >= 99 % of tokens;
+    router logits; where the engine-vs-oracle expert sets (each side routing
+    its own hidden state) differ, the oracle's k-th / (k+1)-th router logit gap is within 4x the
+    largest router-logit difference (a near-tie; greedy modes), and at most max(2, B/50) rows
+    of a layer differ;
   - every row: attention output and router input h2 within max|a-b|/max|b| <= 2e-2;
   - every row whose routing matches the oracle's: the layer output row within 2e-2.  A row whose
     near-tied bf16 router logit picked another expert is reported, not failed.
