@@ -304,11 +304,34 @@ def kernel_breakdown(eng, reps: int = 2) -> dict:
 
 
 def run_ours(args, dist, rank, world) -> None:
+    import gc
+
     from paper_2503_09716_b200.configs import get_arch
-    from paper_2503_09716_b200.engine import Engine, resident_plan
 
     torch.cuda.set_device(rank % torch.cuda.device_count())
-    arch = get_arch(args.config)
+    line = measure(args, get_arch(args.config), dist, rank, world, args.steps, args.warmup, main=True)
+    # the other 1-GPU BASELINE configuration (configs[2], DeepSeek-V2-Lite) measured in the same run, so
+    # the driver's bench records it too; same contract (device-timed decode steps, e2e through the
+    # public API, roofline of the dominant GEMM), fewer steps
+    extra = {}
+    for name in [c for c in args.also.split(",") if c and c != args.config]:
+        gc.collect()
+        torch.cuda.empty_cache()
+        sub = measure(args, get_arch(name), dist, rank, world, args.also_steps, max(3, min(args.warmup, 3)), main=False)
+        extra[name] = {k: sub[k] for k in ("value", "unit", "ms_per_step", "steps", "warmup", "forward_ms", "config",
+                                           "e2e", "roofline", "expert_gemm", "incl_prefill", "kernel_hbm",
+                                           "kernel_ms_per_forward", "clocks", "gpu_launches", "dtype")}
+    if extra:
+        line["also"] = extra
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def measure(args, arch, dist, rank, world, steps: int, warmup: int, main: bool) -> dict:
+    """Time one configuration (the bench contract: `warmup` untimed steps, then exactly `steps`
+    device-timed decode phases, max over ranks); returns its JSON line."""
+    from paper_2503_09716_b200.engine import Engine, resident_plan
+
     plan = resident_plan(arch, args.prompt_len, args.decode_len, B=args.batch, reserve_bytes=args.reserve_gb << 30)
     eng = Engine(arch, plan, prompt_len=args.prompt_len, decode_len=args.decode_len, seed=0, use_graph=True)
     B = eng.B
@@ -324,7 +347,7 @@ def run_ours(args, dist, rank, world) -> None:
         for _ in range(N):
             eng.run_step()  # graph replay (host position checked against the planned context)
 
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         one_step()
     torch.cuda.synchronize()
     if dist is not None:
@@ -333,14 +356,14 @@ def run_ours(args, dist, rank, world) -> None:
     with ClockSampler(torch.cuda.current_device()) as clk:
         torch.cuda.synchronize()
         e0.record()
-        for _ in range(args.steps):
+        for _ in range(steps):
             one_step()
         e1.record()
         torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
     t = _max_over_ranks(dist, e0.elapsed_time(e1) / 1e3)
-    tokens = B * N * args.steps * world
+    tokens = B * N * steps * world
     value = tokens / t
 
     # ---- end-to-end through the public API (host tokens in, host tokens out) ----
@@ -368,7 +391,7 @@ def run_ours(args, dist, rank, world) -> None:
             p1.record()
             torch.cuda.synchronize()
             t_pf = _max_over_ranks(dist, p0.elapsed_time(p1) / 1e3)
-            t_dec = t / args.steps
+            t_dec = t / steps
             incl = {"value": B * N * world / (t_pf + t_dec), "unit": UNIT, "prefill_ms": 1e3 * t_pf,
                     "decode_ms": 1e3 * t_dec, "prefill_tokens_per_s": B * args.prompt_len * world / t_pf,
                     "convention": f"B*{N} generated tokens / (batched prefill of B x {args.prompt_len} prompt tokens"
@@ -428,8 +451,8 @@ def run_ours(args, dist, rank, world) -> None:
     ctx_avg = args.prompt_len + args.decode_len / 2
 
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps, "warmup": warmup,
+        "ms_per_step": 1e3 * t / steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (random-init counter-based weights, synthetic prefill KV)",
         "config": _workload_config(args, arch, world),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(first_pinned.numel() * 4),
@@ -441,16 +464,16 @@ def run_ours(args, dist, rank, world) -> None:
         "incl_prefill": incl,
         "kernel_hbm": kernel_hbm,
         "kernel_ms_per_forward": {k: round(v["ms_per_step"], 4) for k, v in sorted(bd.items())},
-        "forward_ms": 1e3 * t / args.steps / N, "context_avg": ctx_avg,
-        "clocks": clk.summary(), "gpu_launches": launches_per_step * args.steps,
+        "forward_ms": 1e3 * t / steps / N, "context_avg": ctx_avg,
+        "clocks": clk.summary(), "gpu_launches": launches_per_step * steps,
     }
-    if rank == 0:
-        if args.cpu_baseline:
-            cb = args.cpu_batch or B
-            v, sample = cpu_layer_sample(arch, cb, int(ctx_avg), 2, os.cpu_count() or 1)
-            line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-                                    "sample": sample, "cpu_model": _cpu_model(), "batch": cb}
-        print(json.dumps(line), flush=True)
+    del eng
+    if rank == 0 and main and args.cpu_baseline:
+        cb = args.cpu_batch or B
+        v, sample = cpu_layer_sample(arch, cb, int(ctx_avg), 2, os.cpu_count() or 1)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                                "sample": sample, "cpu_model": _cpu_model(), "batch": cb}
+    return line
 
 
 def main():
@@ -467,9 +490,22 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-batch", type=int, default=None, help="CPU arm batch (default: the GPU arm's B)")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--also", default="deepseek-v2-lite",
+                    help="comma-separated extra configs measured after the main one (\"\" = none)")
+    ap.add_argument("--also-steps", type=int, default=3)
     ap.add_argument("--no-incl-prefill", dest="incl_prefill", action="store_false",
                     help="skip the batched-prefill pass behind the incl_prefill figure")
     args = ap.parse_args()
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # --gpus N without a launcher: start N ranks (one process per GPU) over torch.distributed.run
+        # and exit with its status, so `python bench.py --gpus 8` measures 8 GPUs, not one
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", os.environ.get("MASTER_PORT", "29511"),
+               os.path.abspath(__file__)] + sys.argv[1:]
+        raise SystemExit(subprocess.call(cmd))
+    if ws != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}; launch one rank per GPU")
     dist, rank, world, local = _dist()
     if args.impl == "reference":
         run_reference(args, dist, rank, world)

@@ -234,9 +234,8 @@ class Engine:
             if a.q_lora_rank:
                 self.mb.update(q_a=torch.zeros(B, a.q_lora_rank, **bf), q_an=torch.zeros(B, a.q_lora_rank, **bf))
             fs = a.moe_ffn * a.n_shared
-            self.mb.update(sh_h=torch.zeros(B, fs, **bf), sh_gu=torch.zeros(B, 2 * fs, **bf),
-                           de_h=torch.zeros(B, max(a.dense_ffn, 8), **bf),
-                           de_gu=torch.zeros(B, 2 * max(a.dense_ffn, 8), **bf), sh_out=torch.zeros(B, d, **bf),
+            self.mb.update(sh_h=torch.zeros(B, fs, **bf), de_h=torch.zeros(B, max(a.dense_ffn, 8), **bf),
+                           sh_out=torch.zeros(B, d, **bf),
                            logits_r=torch.zeros(B, a.n_experts, dtype=torch.float32, device=device))
             qkv_cols, attn_cols = 8, 8  # unused for MLA
         else:
@@ -268,6 +267,8 @@ class Engine:
         self.trace_events: dict | None = None  # job id -> (start, end) timing events (eager trace mode)
         self._trace_counts: torch.Tensor | None = None  # [layers, E] routed rows per expert (trace mode)
         self._forced_logits: torch.Tensor | None = None  # [layers, B, E] router input (force_routing)
+        self._segments: dict[int, torch.Tensor] = {}
+        self._dense_mlp_cublas = os.environ.get("MGB_DENSE_MLP", "gemm") == "cublas"
         self.kernel_launches_per_step = self._count_launches()
         self.host_pos = 0
 
@@ -634,9 +635,7 @@ class Engine:
                 # shared experts on every token (DeepseekV2Moe.shared_experts): dense -> cuBLAS.  They are
                 # part of the layer's dense modules (dense_bytes_per_layer), so they run before the
                 # single dense buffer is handed to the next layer's copy (offload_dag.py:308-321)
-                torch.mm(b.h, W["sh_gate_up"][0].t(), out=m["sh_gu"])
-                ops.silu_mul(m["sh_gu"], m["sh_h"])
-                torch.mm(m["sh_h"], W["sh_down"][0].t(), out=m["sh_out"])
+                self._dense_mlp(W["sh_gate_up"], W["sh_down"], b.h, m["sh_h"], m["sh_out"], m["offsets_all"])
         elif j.kind == "router":
             if l >= a.first_k_dense:
                 # fp32 router logits (HF: F.linear(x.float(), W.float()), modeling_deepseek_v2.py:125) as a
@@ -657,14 +656,33 @@ class Engine:
                 if j.id == self.first_expert_job[l]:
                     nxt = self.w.layers[l + 1]["ln1"] if l + 1 < a.layers else self.w.final_norm
                     F = a.dense_ffn
-                    torch.mm(b.h, W["dense_gate_up"][0].t(), out=m["de_gu"][:, :2 * F])
-                    ops.silu_mul(m["de_gu"][:, :2 * F], m["de_h"][:, :F])
-                    torch.mm(m["de_h"][:, :F], W["dense_down"][0].t(), out=b.o)
+                    self._dense_mlp(W["dense_gate_up"], W["dense_down"], b.h, m["de_h"][:, :F], b.o, m["offsets_all"])
                     ops.add_rmsnorm(b.x, nxt, a.rms_eps, b.h, delta=b.o, x_out=b.x)
                 return
             self._expert_job(l, j, W, shared_out=m["sh_out"])
         else:
             raise RuntimeError(f"job kind {j.kind!r} is not executable under kv_policy={self.kv_policy!r}")
+
+    def _dense_mlp(self, w_gate_up, w_down, x, h, y, seg) -> None:
+        """A dense SwiGLU MLP (DeepSeek-V2's shared experts, DeepseekV2Moe.shared_experts, and the dense
+        first layers' DeepseekV2MLP, modeling_deepseek_v2.py:134-146) as ONE segment of the grouped
+        expert GEMMs: w_gate_up [1, 2F, d] (gate rows then up rows), w_down [1, d, F], all T rows of x
+        in segment `seg` = [0, T]; SiLU*up is formed in the gate/up GEMM's epilogue (no separate
+        activation pass).  MGB_DENSE_MLP=cublas restores cuBLAS + mgb_silu_mul (A/B measurement)."""
+        if self._dense_mlp_cublas:
+            gu = torch.mm(x, w_gate_up[0].t())
+            ops.silu_mul(gu, h)
+            torch.mm(h, w_down[0].t(), out=y)
+            return
+        ops.moe_gemm_gate_up(w_gate_up, x, seg, h)
+        ops.moe_gemm_down(w_down, h, seg, y)
+
+    def _segment(self, T: int) -> torch.Tensor:
+        """Device offsets [0, T] of a one-segment grouped GEMM (cached per T)."""
+        seg = self._segments.get(T)
+        if seg is None:
+            seg = self._segments[T] = torch.tensor([0, T], dtype=torch.int32, device=self.device)
+        return seg
 
     def _expert_job(self, l: int, j, W: dict, shared_out=None) -> None:
         """EXPERT_COMPUTE (offload_dag.py:449-463).  The b_e chunks of one expert run inside one
@@ -969,12 +987,12 @@ class Engine:
             S.update(q=torch.empty(T, H * qk, **bf), ckv=torch.empty(T, a.kv_lora_rank + a.qk_rope_dim, **bf),
                      c=torch.empty(T, a.kv_lora_rank, **bf), kpe=torch.empty(T, a.qk_rope_dim, **bf),
                      kv=torch.empty(T, H * (a.qk_nope_dim + a.v_head_dim), **bf), k=torch.empty(T, H, qk, **bf),
-                     attn=torch.empty(T, H * a.v_head_dim, **bf), sh_gu=torch.empty(T, 2 * fs, **bf),
-                     sh_h=torch.empty(T, fs, **bf), sh_out=torch.empty(T, d, **bf))
+                     attn=torch.empty(T, H * a.v_head_dim, **bf), sh_h=torch.empty(T, fs, **bf),
+                     sh_out=torch.empty(T, d, **bf))
             if a.q_lora_rank:
                 S.update(qa=torch.empty(T, a.q_lora_rank, **bf), qan=torch.empty(T, a.q_lora_rank, **bf))
             if a.first_k_dense:
-                S.update(de_gu=torch.empty(T, 2 * a.dense_ffn, **bf), de_h=torch.empty(T, a.dense_ffn, **bf))
+                S.update(de_h=torch.empty(T, a.dense_ffn, **bf))
         else:
             hd, Hq, Hkv = a.head_dim, a.n_heads, a.n_kv_heads
             S.update(qkv=torch.empty(T, (Hq + 2 * Hkv) * hd, **bf), q=torch.empty(T, Hq * hd, **bf),
@@ -1070,18 +1088,14 @@ class Engine:
                     torch.mm(att, W["wo"].t(), out=o)
                     ops.add_rmsnorm(x, W["ln2"], a.rms_eps, h, delta=o, x_out=x)
                     nxt = self.w.layers[l + 1]["ln1"] if l + 1 < a.layers else self.w.final_norm
+                    seg = self._segment(t)
                     if self.mla and l < a.first_k_dense:  # DeepseekV2MLP of the dense first layers
-                        F = a.dense_ffn
-                        torch.mm(h, W["dense_gate_up"][0].t(), out=S["de_gu"][:t])
-                        ops.silu_mul(S["de_gu"][:t], S["de_h"][:t])
-                        torch.mm(S["de_h"][:t], W["dense_down"][0].t(), out=o)
+                        self._dense_mlp(W["dense_gate_up"], W["dense_down"], h, S["de_h"][:t], o, seg)
                         ops.add_rmsnorm(x, nxt, a.rms_eps, h, delta=o, x_out=x)
                         continue
                     shared = None
                     if self.mla:  # shared experts on every token
-                        torch.mm(h, W["sh_gate_up"][0].t(), out=S["sh_gu"][:t])
-                        ops.silu_mul(S["sh_gu"][:t], S["sh_h"][:t])
-                        torch.mm(S["sh_h"][:t], W["sh_down"][0].t(), out=S["sh_out"][:t])
+                        self._dense_mlp(W["sh_gate_up"], W["sh_down"], h, S["sh_h"][:t], S["sh_out"][:t], seg)
                         shared = S["sh_out"][:t]
                     torch.mm(h, W["router"].t(), out_dtype=torch.float32, out=S["lg"][:t])
                     ops.router_topk(None, None, ws, k, a.router_mode, a.routed_scaling, a.n_group, a.topk_group,
@@ -1152,15 +1166,12 @@ class Engine:
                     torch.mm(att, W["wo"].t(), out=o)
                     ops.add_rmsnorm(x, W["ln2"], a.rms_eps, h, delta=o, x_out=x)
                     t = t1 - t0
+                    seg = self._segment(t)
                     if dense_mlp:
-                        torch.mm(h, W["dense_gate_up"][0].t(), out=S["de_gu"][:t])
-                        ops.silu_mul(S["de_gu"][:t], S["de_h"][:t])
-                        torch.mm(S["de_h"][:t], W["dense_down"][0].t(), out=o)
+                        self._dense_mlp(W["dense_gate_up"], W["dense_down"], h, S["de_h"][:t], o, seg)
                         ops.add_rmsnorm(x, nxt, a.rms_eps, h, delta=o, x_out=x)
                     elif self.mla:
-                        torch.mm(h, W["sh_gate_up"][0].t(), out=S["sh_gu"][:t])
-                        ops.silu_mul(S["sh_gu"][:t], S["sh_h"][:t])
-                        torch.mm(S["sh_h"][:t], W["sh_down"][0].t(), out=sh_all[t0:t1])
+                        self._dense_mlp(W["sh_gate_up"], W["sh_down"], h, S["sh_h"][:t], sh_all[t0:t1], seg)
                 if dense_mlp:
                     continue
                 torch.mm(h_all, W["router"].t(), out_dtype=torch.float32, out=lg)

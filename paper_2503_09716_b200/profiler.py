@@ -175,9 +175,7 @@ def profile_engine(arch: ModelArch | str, token_grid: Sequence[int] | None = Non
             def post():
                 torch.mm(m["o_cat"][:T], W["wo"].t(), out=b.o[:T])
                 ops.add_rmsnorm(b.x[:T], W["ln2"], a.rms_eps, b.h[:T], delta=b.o[:T], x_out=b.x[:T])
-                torch.mm(b.h[:T], W["sh_gate_up"][0].t(), out=m["sh_gu"][:T])
-                ops.silu_mul(m["sh_gu"][:T], m["sh_h"][:T])
-                torch.mm(m["sh_h"][:T], W["sh_down"][0].t(), out=m["sh_out"][:T])
+                eng._dense_mlp(W["sh_gate_up"], W["sh_down"], b.h[:T], m["sh_h"][:T], m["sh_out"][:T], eng._segment(T))
         else:
             def post():
                 torch.mm(b.attn[:T], W["wo"].t(), out=b.o[:T])
