@@ -102,6 +102,19 @@ int mgb_mla_append_prefill(void* q, const void* ckv, const void* norm_w, float e
                            int R, int RP, int NOPE, const float* cos_t, const float* sin_t, const int* block_table,
                            int max_pages, void* cache, void* c_out, void* kpe_out, void* stream);
 
+/* ---- prefill attention (the prefill phase's ATTN_MECH_GPU: tokens_per_seq_in_flight = P, no KV
+ * copy-in, memory_model.py:53-60, offload_dag.py:359-372) -----------------------------------------
+ * Causal attention of n_seq equal-length prompts of P tokens (rows s*P .. s*P+P-1), tcgen05 + TMA
+ * (attn_prefill.cu).  q [T, q_cols] head h at column h*q_head_cols; k [T, k_cols] kv head g = h/(Hq/Hkv)
+ * at g*k_head_cols (hd_qk - kr_dim dims) + the last kr_dim dims from kr [T, kr_cols] (MLA's shared
+ * k_pe; NULL / 0 for GQA); v [T, v_cols] at v_col0 + g*v_head_cols; out [T, out_cols] head h at
+ * h*hd_v.  Supported (hd_qk, hd_v): (128, 128), (192, 128), (64, 64) -- mgb_prefill_attn_supported. */
+int mgb_prefill_attn_supported(int hd_qk, int hd_v);
+int mgb_prefill_attn(const void* q, int q_cols, int q_head_cols, const void* k, int k_cols, int k_head_cols,
+                     const void* kr, int kr_cols, int kr_dim, const void* v, int v_cols, int v_head_cols, int v_col0,
+                     int n_seq, int P, int Hq, int Hkv, int hd_qk, int hd_v, float scale, void* out, int out_cols,
+                     void* stream);
+
 /* ---- KV_COPY_OUT / new-token insert for kv_policy "offload" (offload_dag.py:372-392) --------
  * Copies the token at positions[b] of sequence b from page src_table[b][pos/page_tokens] of src to
  * page dst_table[b][pos/page_tokens] of dst (same in-page slot).  A token's bytes inside a page are

@@ -53,6 +53,9 @@ SIGNATURES: dict[str, list] = {
     "mgb_decode_attn_mla": [P, P, P, P, I, P, I, I, I, I, F, P, P],
     "mgb_mla_append": [P, P, P, F, I, I, I, I, I, P, P, P, P, I, P, P, P, P, P],
     "mgb_mla_append_prefill": [P, P, P, F, I, I, I, I, I, I, I, P, P, P, I, P, P, P, P],
+    # attn_prefill.cu
+    "mgb_prefill_attn_supported": [I, I],
+    "mgb_prefill_attn": [P, I, I, P, I, I, P, I, I, P, I, I, I, I, I, I, I, I, I, F, P, I, P],
     # kv_stream.cu
     "mgb_kv_token_copy": [P, P, I, P, P, I, P, I, I, L, I, I, L, P],
     "mgb_copy_bytes": [P, P, L, P],
@@ -72,7 +75,7 @@ class CpuAttnGqa(ctypes.Structure):
                 ("hd", ctypes.c_int32), ("page_tokens", ctypes.c_int32), ("scale", F), ("status", ctypes.c_int32)]
 
 # entry points that return a value rather than a status
-VALUE_FNS = {"mgb_cpu_threads", "mgb_cpu_attn_simd", "mgb_abi_version", "mgb_num_sms", "mgb_kv_page_size", "mgb_mla_page_size", "mgb_mla_page_elems",
+VALUE_FNS = {"mgb_prefill_attn_supported", "mgb_cpu_threads", "mgb_cpu_attn_simd", "mgb_abi_version", "mgb_num_sms", "mgb_kv_page_size", "mgb_mla_page_size", "mgb_mla_page_elems",
              "mgb_router_num_blocks", "mgb_router_tokens_per_block"}
 
 STATUS = {0: "ok", -1: "invalid argument", -2: "capacity exceeded", -3: "CUDA error"}

@@ -996,7 +996,8 @@ class Engine:
         else:
             hd, Hq, Hkv = a.head_dim, a.n_heads, a.n_kv_heads
             S.update(qkv=torch.empty(T, (Hq + 2 * Hkv) * hd, **bf), q=torch.empty(T, Hq * hd, **bf),
-                     k=torch.empty(T, Hkv * hd, **bf), v=torch.empty(T, Hkv * hd, **bf))
+                     k=torch.empty(T, Hkv * hd, **bf), v=torch.empty(T, Hkv * hd, **bf),
+                     attn=torch.empty(T, Hq * hd, **bf))
         self._pf, self._pf_T = S, T
         return S
 
@@ -1011,10 +1012,21 @@ class Engine:
                  self.sin_t.data_ptr(), Hq, Hkv, hd, table.data_ptr(), self.pps, kc.data_ptr(), vc.data_ptr(),
                  q.data_ptr(), kk.data_ptr(), vv.data_ptr(), torch.cuda.current_stream().cuda_stream)
         self._prefill_kv_flush(l, s0, n)
+        if self._prefill_kernel(hd, hd):  # tcgen05 causal attention (attn_prefill.cu)
+            att = S["attn"][:t]
+            ops.prefill_attn(q, kk, vv, att, n, P, Hq, Hkv, hd, hd, hd ** -0.5, hd, hd, hd)
+            return att
+        # head dims the kernel is not instantiated for (the tiny test models): torch SDPA
         att = torch.nn.functional.scaled_dot_product_attention(
             q.view(n, P, Hq, hd).transpose(1, 2), kk.view(n, P, Hkv, hd).transpose(1, 2),
             vv.view(n, P, Hkv, hd).transpose(1, 2), is_causal=True, enable_gqa=True)
         return att.transpose(1, 2).reshape(t, Hq * hd)
+
+    def _prefill_kernel(self, hd_qk: int, hd_v: int, rope: int = 0) -> bool:
+        """Whether the prefill attention runs on mgb_prefill_attn (MGB_PREFILL_ATTN=sdpa: torch SDPA, A/B)."""
+        if os.environ.get("MGB_PREFILL_ATTN", "mgb") == "sdpa":
+            return False
+        return ops.prefill_attn_supported(hd_qk, hd_v) and rope % 64 == 0 and (hd_qk - rope) % 64 == 0
 
     def _prefill_attention_mla(self, l: int, W: dict, S: dict, s0: int, n: int, P: int,
                                h: torch.Tensor) -> torch.Tensor:
@@ -1038,6 +1050,13 @@ class Engine:
         self._prefill_kv_flush(l, s0, n)
         kv = S["kv"][:t]
         torch.mm(S["c"][:t], W["kv_b"].t(), out=kv)
+        if self._prefill_kernel(nope + r, vd, r):
+            # K_h = [k_nope_h | k_pe] read straight from the up-projected rows and the shared rotated
+            # k_pe rows; V_h = the v part of the same rows (no per-head K is materialised)
+            att = S["attn"][:t]
+            ops.prefill_attn(q, kv, kv, att, n, P, H, H, nope + r, vd, (nope + r) ** -0.5, nope + r, nope + vd,
+                             nope + vd, v_col0=nope, kr=S["kpe"][:t])
+            return att
         kv = kv.view(t, H, nope + vd)
         k = S["k"][:t]
         k[:, :, :nope].copy_(kv[:, :, :nope])

@@ -104,6 +104,24 @@ def decode_attn_gqa(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tenso
              _p(seq_lens), B, Hq, Hkv, hd, scale, _p(out), _s())
 
 
+def prefill_attn_supported(hd_qk: int, hd_v: int) -> bool:
+    return bool(nat.value("mgb_prefill_attn_supported", hd_qk, hd_v))
+
+
+def prefill_attn(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, out: torch.Tensor, n_seq: int, P: int, Hq: int,
+                 Hkv: int, hd_qk: int, hd_v: int, scale: float, q_head_cols: int, k_head_cols: int, v_head_cols: int,
+                 v_col0: int = 0, kr: torch.Tensor | None = None) -> None:
+    """Causal prefill attention (tcgen05, attn_prefill.cu) over 2-D row-major [n_seq*P, cols] tensors;
+    `kr` holds MLA's shared rope part of K (its width is the last kr.shape[1] dims of hd_qk)."""
+    for t in (q, k, v, out) + ((kr,) if kr is not None else ()):
+        assert t.dim() == 2 and t.stride(1) == 1 and t.dtype == BF16
+    kr_cols = kr.stride(0) if kr is not None else 0
+    kr_dim = kr.shape[1] if kr is not None else 0
+    nat.call("mgb_prefill_attn", _p(q), q.stride(0), q_head_cols, _p(k), k.stride(0), k_head_cols, _p(kr), kr_cols,
+             kr_dim, _p(v), v.stride(0), v_head_cols, v_col0, n_seq, P, Hq, Hkv, hd_qk, hd_v, scale, _p(out),
+             out.stride(0), _s())
+
+
 def silu_mul(gate_up: torch.Tensor, h: torch.Tensor) -> None:
     T, F = h.shape
     assert gate_up.shape == (T, 2 * F) and gate_up.is_contiguous() and h.is_contiguous()

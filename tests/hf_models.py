@@ -37,6 +37,11 @@ def tiny_dsv2_hf(layers: int = 3, vocab: int = 512, seed: int = 0):
         for n, p in m.named_parameters():
             if "norm" in n:
                 p.copy_(1.0 + 0.1 * torch.randn_like(p.float()).to(p.dtype))
+    # HF 5.5.0 DeepseekV2Moe.route_tokens_to_experts reads self.num_experts for group_limited_greedy
+    # (modeling_deepseek_v2.py:112) but never sets it (same workaround as tests/golden/make_golden.py)
+    for layer in m.model.layers:
+        if hasattr(layer.mlp, "experts"):
+            layer.mlp.num_experts = cfg.n_routed_experts
     return m
 
 

@@ -37,7 +37,7 @@ def test_engine_from_checkpoint_matches_hf(tmp_path, family):
     B, P, N = 8, 12, 8
     ids = torch.randint(0, V, (B, P), generator=torch.Generator().manual_seed(4))
     with torch.no_grad():
-        ref = m.generate(ids, max_new_tokens=N, min_new_tokens=N, do_sample=False)
+        ref = m.generate(ids, max_new_tokens=N, min_new_tokens=N, do_sample=False, pad_token_id=0)
         lg_hf = m(ref).logits.float()  # teacher-forced logits at every position
     eng = _engine(path, B, P, N, use_graph=False)
     assert eng.w.layers[0]["ln1"].float().std() > 0  # real (non-unit) norms were loaded
