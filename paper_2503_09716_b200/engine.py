@@ -137,12 +137,18 @@ class Engine:
         # expert parallelism (ep.ExpertParallel): experts of this rank's range run locally, token
         # rows are dispatched/combined over torch.distributed; the host-side split sizes make the
         # EP step eager (no CUDA graph) in this build
-        self.ep = ep if (ep is not None and ep.world > 1) else None
+        from .ep import PeerExpertParallel
+
+        # PeerExpertParallel: dispatch fused into the permutation, combine into the down GEMM's epilogue,
+        # only the E counts exchanged, all offsets on the device -> the EP step is graph-capturable when
+        # its comm is (NCCL + symmetric memory); kept even at world 1 (the same code path, one rank)
+        self.peer_ep = isinstance(ep, PeerExpertParallel)
+        self.ep = ep if (ep is not None and (self.peer_ep or ep.world > 1)) else None
         if ep is not None and self.plan.s_params < self.spec.model_bytes:
             # the EP path slices this rank's expert range out of the resident expert tensors; streamed
             # experts live in slots indexed by copy order, which the dispatch offsets do not describe
             raise ValueError("expert parallelism needs HBM-resident weights (plan.s_params = model bytes)")
-        self.use_graph = use_graph and self.ep is None
+        self.use_graph = use_graph and (self.ep is None or (self.peer_ep and getattr(ep.comm, "graph_safe", False)))
         # ---- job list (structure only; durations are measured, not modelled) ----
         # ---- CPU attention share (omega > 0): GQA over the host page store on the host cores ----
         self.n_cpu = self.plan.cpu_sequences()
@@ -176,9 +182,20 @@ class Engine:
             self.w = DeepseekDeviceWeights(a, seed=seed, device=device, source=self.source)
         else:
             self.w = MixtralDeviceWeights(a, seed=seed, device=device, source=self.source)
+        if self.ep is not None:  # this rank holds only its expert range [first, first + E_local)
+            lo, nl = self.ep.first, self.ep.E_local
+            for W_ in self.w.layers:
+                if W_.get("w_gate_up") is not None:
+                    W_["w_gate_up"] = W_["w_gate_up"][lo:lo + nl].clone()
+                    W_["w_down"] = W_["w_down"][lo:lo + nl].clone()
+            torch.cuda.empty_cache()
         d, k, f = a.hidden, a.top_k, a.moe_ffn
         bf = dict(dtype=BF16, device=device)
         i32 = dict(dtype=torch.int32, device=device)
+        if self.peer_ep:  # local expert GEMM scratch over the whole receive buffer, per-row home pointers
+            cap = self.ep.recv.shape[0]
+            self.ep_h = torch.zeros(cap, f, **bf)
+            self.ep_row_ptr = torch.zeros(cap, dtype=torch.int64, device=device)
         # ---- paged KV (identity block table: sequence b owns pages [b*pps, (b+1)*pps)) ----
         if self.mla:
             # latent pages: swizzled 64-dim blocks [ceil((R + r)/64)][page tok][64] (attn_mla.cu)
@@ -647,7 +664,8 @@ class Engine:
                     torch.mm(b.h, W["router"].t(), out_dtype=torch.float32, out=lg)
                 ops.router_topk(None, None, self.rws, a.top_k, a.router_mode, a.routed_scaling, a.n_group,
                                 a.topk_group, logits_in=lg)
-                ops.permute(b.h, self.rws, b.x_perm)
+                if not self.peer_ep:
+                    ops.permute(b.h, self.rws, b.x_perm)
                 if self.debug_taps is not None:
                     self.debug_taps.update(h2=b.h.clone(), topk_idx=self.rws.topk_idx.clone())
         elif j.kind == "expert_compute":
@@ -703,7 +721,8 @@ class Engine:
             ops.moe_gemm_down(dn, b.h_ffn, offs, b.y_perm)
         if j.id == self.last_expert_job[l]:
             nxt = self.w.layers[l + 1]["ln1"] if l + 1 < a.layers else self.w.final_norm
-            ops.unpermute_combine(b.y_perm, self.rws, b.x, self.B, residual=b.x, shared_out=shared_out,
+            y_perm = self.ep.yperm if self.peer_ep else b.y_perm
+            ops.unpermute_combine(y_perm, self.rws, b.x, self.B, residual=b.x, shared_out=shared_out,
                                   norm_w=nxt, eps=a.rms_eps, norm_out=b.h)
 
     def _routed_experts(self, W: dict) -> None:
@@ -715,14 +734,25 @@ class Engine:
             ops.moe_gemm_down(W["w_down"], b.h_ffn, self.rws.offsets, b.y_perm)
             return
         a, ep = self.arch, self.ep
+        if self.peer_ep:
+            # counts of every rank -> device tables; this rank's routed rows into the owners' receive
+            # buffers; barrier; local experts, each output row stored at its home rank's y_perm by the
+            # down GEMM's epilogue; barrier (offload_dag.py:418-472: the exchange sits on the
+            # router -> expert and expert -> combine edges)
+            counts_all = ep.comm.exchange_counts(self.rws.counts)
+            tab = ep.tables(counts_all)
+            ep.dispatch(b.h, self.rws, tab)
+            ep.comm.barrier()
+            ep.experts(W["w_gate_up"], W["w_down"], ep.recv, self.ep_h, self.ep_row_ptr, tab)
+            ep.comm.barrier()
+            return
         x_loc, offs, st = ep.dispatch(b.x_perm, self.rws.counts)
         n = x_loc.shape[0]
         y_loc = torch.empty(n, a.hidden, dtype=BF16, device=self.device)
         if n > 0:
             h = torch.empty(n, a.moe_ffn, dtype=BF16, device=self.device)
-            lo = ep.first
-            ops.moe_gemm_gate_up(W["w_gate_up"][lo:lo + ep.E_local], x_loc, offs, h)
-            ops.moe_gemm_down(W["w_down"][lo:lo + ep.E_local], h, offs, y_loc)
+            ops.moe_gemm_gate_up(W["w_gate_up"], x_loc, offs, h)
+            ops.moe_gemm_down(W["w_down"], h, offs, y_loc)
         y = ep.combine(y_loc, st)
         b.y_perm[:y.shape[0]].copy_(y)
 
@@ -765,7 +795,8 @@ class Engine:
             else:
                 ops.router_topk(b.h, W["router"], self.rws, a.top_k, a.router_mode, a.routed_scaling,
                                 a.n_group, a.topk_group)
-            ops.permute(b.h, self.rws, b.x_perm)
+            if not self.peer_ep:  # peer EP permutes inside its dispatch (rows go straight to the owners)
+                ops.permute(b.h, self.rws, b.x_perm)
             if self.debug_taps is not None:  # eager-only parity hook
                 self.debug_taps.update(h2=b.h.clone(), topk_idx=self.rws.topk_idx.clone(), attn=b.attn.clone())
         elif j.kind == "expert_compute":

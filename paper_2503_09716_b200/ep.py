@@ -120,14 +120,23 @@ class PeerExpertParallel:
     Cross-rank ordering (all writes into a buffer landed before it is read) is the caller's
     barrier between the three phases."""
 
-    def __init__(self, n_experts: int, world: int, rank: int, recv_ptrs, yperm_ptrs, device="cuda"):
+    def __init__(self, n_experts: int, world: int, rank: int, recv_ptrs, yperm_ptrs, device="cuda",
+                 recv: torch.Tensor | None = None, yperm: torch.Tensor | None = None, comm=None):
         if n_experts % world:
             raise ValueError(f"{n_experts} experts do not shard over {world} ranks")
         self.E, self.W, self.rank = n_experts, world, rank
+        self.world = world
         self.L = n_experts // world
+        self.E_local = self.L
         self.first = rank * self.L
         self.peer_recv = torch.tensor([int(p) for p in recv_ptrs], dtype=torch.int64, device=device)
         self.peer_y = torch.tensor([int(p) for p in yperm_ptrs], dtype=torch.int64, device=device)
+        # this rank's own buffers (the engine's EP path reads them) and the count exchange / barrier
+        # (`comm`: _SymmComm over NCCL + symmetric memory, or VirtualPeerGroup.member for virtual ranks)
+        self.recv, self.yperm, self.comm = recv, yperm, comm
+
+    def local_experts(self) -> range:
+        return range(self.first, self.first + self.L)
 
     def tables(self, counts_all: torch.Tensor) -> dict:
         """counts_all [W, E]: rows source s routes to expert e.  Returns this rank's dispatch rows
@@ -189,23 +198,82 @@ class PeerExpertParallel:
         recv = symm.empty(recv_rows, d, dtype=torch.bfloat16, device=device)
         yperm = symm.empty(yperm_rows, d, dtype=torch.bfloat16, device=device)
         hr, hy = symm.rendezvous(recv, group), symm.rendezvous(yperm, group)
-        self = cls(n_experts, hr.world_size, hr.rank, hr.buffer_ptrs, hy.buffer_ptrs, device=device)
-        self.recv, self.yperm, self.group, self._handle = recv, yperm, group, hr
+        comm = _SymmComm(group, hr, hr.world_size, n_experts, device)
+        self = cls(n_experts, hr.world_size, hr.rank, hr.buffer_ptrs, hy.buffer_ptrs, device=device, recv=recv,
+                   yperm=yperm, comm=comm)
+        self.group, self._handle = group, hr
         return self
 
     def barrier(self) -> None:
         """Stream-ordered cross-rank barrier (all peer writes of the phase have landed)."""
-        self._handle.barrier()
+        self.comm.barrier()
 
     def moe(self, h: torch.Tensor, ws, w_gate_up_local: torch.Tensor, w_down_local: torch.Tensor,
             h_ffn: torch.Tensor, row_ptr: torch.Tensor) -> torch.Tensor:
         """One routed-expert layer across the group after this rank's router: returns this rank's
         y_perm (home rows of its tokens' expert outputs) for mgb_unpermute_combine."""
-        counts_all = torch.empty(self.W, self.E, dtype=ws.counts.dtype, device=ws.counts.device)
-        dist.all_gather_into_tensor(counts_all, ws.counts, group=self.group)
+        counts_all = self.comm.exchange_counts(ws.counts)
         tab = self.tables(counts_all)
         self.dispatch(h, ws, tab)
         self.barrier()
         self.experts(w_gate_up_local, w_down_local, self.recv, h_ffn, row_ptr, tab)
         self.barrier()
         return self.yperm
+
+
+class _SymmComm:
+    """Count exchange + barrier of PeerExpertParallel across real GPUs: NCCL all-gather of the E
+    per-expert counts into a fixed device table (graph-capturable: fixed size, fixed address) and
+    torch symmetric memory's stream-ordered signal-pad barrier."""
+
+    graph_safe = True
+
+    def __init__(self, group, handle, world: int, E: int, device):
+        self.group, self.handle = group, handle
+        self.counts_all = torch.zeros(world, E, dtype=torch.int32, device=device)
+
+    def exchange_counts(self, counts: torch.Tensor) -> torch.Tensor:
+        dist.all_gather_into_tensor(self.counts_all, counts, group=self.group)
+        return self.counts_all
+
+    def barrier(self) -> None:
+        self.handle.barrier()
+
+
+class VirtualPeerGroup:
+    """W virtual ranks sharing one GPU (tests and single-GPU validation of the EP data path): each
+    rank is an Engine driven from its own host thread on its own CUDA stream; the barrier is a
+    host-thread rendezvous plus cross-stream event waits (every rank's stream waits for every
+    rank's work issued before the barrier), the count exchange a shared device table.  Eager only:
+    the phases of different ranks are different streams' work, not one capturable graph."""
+
+    def __init__(self, W: int, E: int, device="cuda"):
+        import threading
+
+        self.W = W
+        self.counts_all = torch.zeros(W, E, dtype=torch.int32, device=device)
+        self._tb = threading.Barrier(W)
+        self._ev = [torch.cuda.Event() for _ in range(W)]
+
+    def member(self, rank: int) -> "_VirtualComm":
+        return _VirtualComm(self, rank)
+
+
+class _VirtualComm:
+    graph_safe = False
+
+    def __init__(self, group: VirtualPeerGroup, rank: int):
+        self.g, self.rank = group, rank
+
+    def exchange_counts(self, counts: torch.Tensor) -> torch.Tensor:
+        self.g.counts_all[self.rank].copy_(counts)
+        self.barrier()
+        return self.g.counts_all
+
+    def barrier(self) -> None:
+        g, st = self.g, torch.cuda.current_stream()
+        g._ev[self.rank].record(st)
+        g._tb.wait()
+        for e in g._ev:
+            st.wait_event(e)
+        g._tb.wait()  # nobody re-records before every rank has queued its waits
