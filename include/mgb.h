@@ -30,6 +30,18 @@ int mgb_kv_page_size(void);                /* tokens per KV page (64) */
 int mgb_router_num_blocks(int T);          /* rows of the router block_hist workspace */
 int mgb_router_tokens_per_block(void);
 
+/* ---- capacity contract (exec_sim.py:170-175: groups larger than their buffer are split, not
+ * overrun; SPEC.md "Invariants": every scheduled row is either processed or reported) ------
+ *  - mgb_moe_check_capacity: host pre-flight of a grouped launch whose offsets[E+1] are on the
+ *    device: writes per-expert counts to counts_out[E] (host) and returns -2 when the segments need
+ *    more than rows_cap rows (the caller re-splits the group by b_e);
+ *  - inside a launch (device offsets, graph-replayed steps) the grouped GEMMs and the EP dispatch
+ *    check rows_cap on the device, do no out-of-bounds work, and record {-2, rows needed, rows_cap,
+ *    site 1 gate/up | 2 down | 3 EP dispatch}; mgb_capacity_status (synchronising) reads it into
+ *    out4 (may be NULL), clears it when reset != 0, and returns -2 if an overflow was recorded. */
+int mgb_moe_check_capacity(const int* offsets, int E, int rows_cap, int* counts_out, void* stream);
+int mgb_capacity_status(int* out4, int reset);
+
 /* ---- ROUTER (offload_dag.py:418-425, ModuleKind.ROUTER hw_profile.py:58) -----------------
  * x[T,d] bf16, w_gate[E,d] bf16 (or logits_in[T,E] fp32 to route given logits).
  * mode 0 Mixtral softmax->topk->renorm; 1 DeepSeek greedy (x scaling); 2 group-limited greedy.
@@ -61,7 +73,7 @@ int mgb_moe_gemm_down(const void* w_down, const void* h, const int* offsets, int
  *    send fused into the GEMM). */
 int mgb_ep_permute_dispatch(const void* x, const int* topk_idx, const int* local_rank, const int* block_base,
                             const int* offsets, int T, int d, int k, int E, int E_local, const long long* peer_base,
-                            const int* disp_row, int* src_token, int* dst_pos, void* stream);
+                            const int* disp_row, int recv_rows_cap, int* src_token, int* dst_pos, void* stream);
 int mgb_ep_row_ptrs(const int* seg_start, const int* seg_len, const int* seg_delta, int n_seg, int W,
                     const long long* peer_base, int row_bytes, int rows_cap, long long* row_ptr, void* stream);
 int mgb_moe_gemm_down_ep(const void* w_down, const void* h, const int* offsets, int E, int d, int f, int rows_cap,

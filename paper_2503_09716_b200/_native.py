@@ -22,6 +22,8 @@ SIGNATURES: dict[str, list] = {
     # introspection
     "mgb_abi_version": [],
     "mgb_num_sms": [],
+    "mgb_moe_check_capacity": [P, I, I, P, P],
+    "mgb_capacity_status": [P, I],
     "mgb_kv_page_size": [],
     "mgb_router_num_blocks": [I],
     "mgb_router_tokens_per_block": [],
@@ -34,7 +36,7 @@ SIGNATURES: dict[str, list] = {
     "mgb_moe_gemm_down": [P, P, P, I, I, I, I, P, P],
     "mgb_grouped_ffn": [P, P, P, P, I, I, I, I, P, P, P],
     "mgb_moe_gemm_down_ep": [P, P, P, I, I, I, I, P, P],
-    "mgb_ep_permute_dispatch": [P, P, P, P, P, I, I, I, I, I, P, P, P, P, P],
+    "mgb_ep_permute_dispatch": [P, P, P, P, P, I, I, I, I, I, P, P, I, P, P, P],
     "mgb_ep_row_ptrs": [P, P, P, I, I, P, I, I, P, P],
     # attention (attn_gqa.cu)
     "mgb_decode_attn_gqa": [P, P, P, P, I, P, I, I, I, I, F, P, P],
@@ -112,6 +114,10 @@ class _Lib:
         assert name in VALUE_FNS
         return int(getattr(self.load(), name)(*args))
 
+    def raw(self, name: str, *args) -> int:
+        """Call an entry point and return its status (for callers that handle MGB_ECAPACITY)."""
+        return int(getattr(self.load(), name)(*args))
+
     def call(self, name: str, *args) -> None:
         lib = self.load()
         self.calls += 1
@@ -130,6 +136,10 @@ LIB = _Lib()
 
 def call(name: str, *args) -> None:
     LIB.call(name, *args)
+
+
+def raw(name: str, *args) -> int:
+    return LIB.raw(name, *args)
 
 
 def value(name: str, *args) -> int:

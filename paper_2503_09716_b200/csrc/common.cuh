@@ -386,6 +386,30 @@ MGB_DEVINL uint4 ld_nc_v4(const void* p) {
   return r;
 }
 
+// ----------------------------------------------------------------------------------------
+// capacity contract (exec_sim.py:170-175: token groups larger than the buffers they land in are
+// a status, not an out-of-bounds write).  A kernel whose row segments do not fit the caller's
+// rows_cap does no work and records {MGB_ECAPACITY, rows needed, rows_cap, site} in the
+// library's device status word (mgb_capacity_status reads and clears it).
+// ----------------------------------------------------------------------------------------
+enum CapSite { kCapGateUp = 1, kCapDown = 2, kCapDispatch = 3 };
+MGB_DEVINL bool segments_fit(const int* offsets, int E, int rows_cap, int* status, int site) {
+  int prev = offsets[0];
+  bool ok = prev >= 0;
+  for (int e = 1; e <= E; ++e) {
+    const int o = offsets[e];
+    ok = ok && o >= prev;
+    prev = o;
+  }
+  ok = ok && prev <= rows_cap;
+  if (!ok && status && atomicCAS(status, 0, MGB_ECAPACITY) == 0) {
+    status[1] = prev;
+    status[2] = rows_cap;
+    status[3] = site;
+  }
+  return ok;
+}
+
 }  // namespace mgb
 
 // Host-side helpers shared by the launchers.
@@ -402,4 +426,7 @@ CUresult encode_tmap_bf16(CUtensorMap* map, const void* base, int rank, const ui
 int num_sms();
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device); MGB_OK or MGB_ECUDA.
 int ensure_max_smem(const void* fn, int bytes);
+// The current device's capacity status word (int[4], see mgb::segments_fit), a __device__ symbol of
+// the library (no allocation, so launchers may call it while a graph is being captured).
+int* capacity_status_ptr();
 }  // namespace mgb_host

@@ -9,6 +9,9 @@
 
 #include "common.cuh"
 
+// {code, rows needed, rows_cap, site} of the first capacity overflow since the last read
+__device__ int g_capacity_status[4];
+
 namespace mgb_host {
 
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -82,6 +85,20 @@ int ensure_max_smem(const void* fn, int bytes) {
   return MGB_OK;
 }
 
+int* capacity_status_ptr() {
+  static std::mutex mu;
+  static int* ptrs[64] = {nullptr};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!ptrs[dev]) {
+    void* p = nullptr;
+    if (cudaGetSymbolAddress(&p, g_capacity_status) != cudaSuccess) return nullptr;
+    ptrs[dev] = static_cast<int*>(p);
+  }
+  return ptrs[dev];
+}
+
 namespace {
 cudaError_t g_last_err = cudaSuccess;  // first launch error a libmgb entry point returned MGB_ECUDA for
 }
@@ -98,7 +115,7 @@ int launch_status() {
 extern "C" {
 
 // ABI version of include/mgb.h; bumped whenever a signature changes.
-int mgb_abi_version(void) { return 1; }
+int mgb_abi_version(void) { return 2; }
 
 // Name of the last CUDA error seen by the runtime in this library (for loud failures).
 // A launch error an entry point already consumed (returned as MGB_ECUDA) is reported, then cleared.
@@ -106,6 +123,43 @@ const char* mgb_last_error(void) {
   const cudaError_t e = mgb_host::g_last_err != cudaSuccess ? mgb_host::g_last_err : cudaPeekAtLastError();
   mgb_host::g_last_err = cudaSuccess;
   return cudaGetErrorString(e);
+}
+
+// Capacity status of the current device: synchronises the device, copies {code, rows needed,
+// rows_cap, site} of the first overflow a grouped GEMM / EP dispatch saw since the last call into
+// out4 (may be NULL), clears it when `reset`, and returns MGB_ECAPACITY if one was recorded.
+int mgb_capacity_status(int* out4, int reset) {
+  int* p = mgb_host::capacity_status_ptr();
+  if (!p) return MGB_ECUDA;
+  int h[4] = {0, 0, 0, 0};
+  if (cudaDeviceSynchronize() != cudaSuccess || cudaMemcpy(h, p, sizeof h, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return mgb_host::launch_status(), MGB_ECUDA;
+  if (reset && h[0] && cudaMemset(p, 0, sizeof h) != cudaSuccess) return MGB_ECUDA;
+  if (out4)
+    for (int i = 0; i < 4; ++i) out4[i] = h[i];
+  return h[0] ? MGB_ECAPACITY : MGB_OK;
+}
+
+// Host-side capacity check in front of a grouped launch whose offsets live on the device (the
+// scheduler's pre-flight, exec_sim.py:170-175): copies offsets[E+1] on `stream`, waits, writes the
+// per-expert row counts to counts_out[E] (host) and returns MGB_ECAPACITY if the segments need more
+// than rows_cap rows (or are not monotone) -- the caller then re-splits the group by b_e.
+int mgb_moe_check_capacity(const int* offsets, int E, int rows_cap, int* counts_out, void* stream) {
+  if (E < 1 || E > 4096 || rows_cap < 0 || !offsets) return MGB_EINVAL;
+  int h[4097];
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (cudaMemcpyAsync(h, offsets, sizeof(int) * (E + 1), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess) {
+    mgb_host::launch_status();
+    return MGB_ECUDA;
+  }
+  bool ok = h[0] >= 0;
+  for (int e = 0; e < E; ++e) {
+    const int c = h[e + 1] - h[e];
+    ok = ok && c >= 0;
+    if (counts_out) counts_out[e] = c;
+  }
+  return ok && h[E] <= rows_cap ? MGB_OK : MGB_ECAPACITY;
 }
 
 // Number of SMs of the current device (148 on B200).

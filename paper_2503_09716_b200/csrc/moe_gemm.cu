@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(Epi<GATED>::kThreads, 1)
 moe_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const int* __restrict__ offsets, int E, int MT, int K, int rows_per_expert, int half_rows,
                 __nv_bfloat16* __restrict__ out, int ldo, bool balanced,
-                const long long* __restrict__ row_ptr) {
+                const long long* __restrict__ row_ptr, int rows_cap, int* __restrict__ cap_status) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* tiles = smem;
@@ -146,12 +146,13 @@ moe_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   // unit prefix over experts: units(e) = ceil(n_e / BN) * MT
   if (threadIdx.x == 0) {
     int acc = 0;
+    const bool fit = segments_fit(offsets, E, rows_cap, cap_status, GATED ? kCapGateUp : kCapDown);
     for (int e = 0; e < E; ++e) {
       s_prefix[e] = acc;
       const int cnt = offsets[e + 1] - offsets[e];
       acc += token_tiles(cnt, balanced) * MT;
     }
-    s_prefix[E] = acc;
+    s_prefix[E] = fit ? acc : 0;  // overflow: no unit runs (status recorded), nothing is written
   }
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
@@ -310,7 +311,7 @@ moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                      const __grid_constant__ CUtensorMap tmB8,
                      const int* __restrict__ offsets, int E, int MT, int K, int rows_per_expert, int half_rows,
                      __nv_bfloat16* __restrict__ out, int ldo, bool balanced,
-                     const long long* __restrict__ row_ptr, int nalign) {
+                     const long long* __restrict__ row_ptr, int nalign, int rows_cap, int* __restrict__ cap_status) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* tiles = smem;
@@ -330,12 +331,13 @@ moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
 
   if (threadIdx.x == 0) {
     int acc = 0;
+    const bool fit = segments_fit(offsets, E, rows_cap, cap_status, GATED ? kCapGateUp : kCapDown);
     for (int e = 0; e < E; ++e) {
       s_prefix[e] = acc;
       const int cnt = offsets[e + 1] - offsets[e];
       acc += token_tiles(cnt, balanced) * MT;
     }
-    s_prefix[E] = acc;
+    s_prefix[E] = fit ? acc : 0;  // overflow: no unit runs (status recorded), nothing is written
   }
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
@@ -502,7 +504,9 @@ bool use_pair_kernel() {
 template <bool GATED, bool PAIR, bool ROWPTR>
 int launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmB8, const int* offsets, int E, int MT, int K,
                    int rows_per_expert, int half_rows, void* out, int ldo, bool balanced, const long long* row_ptr,
-                   cudaStream_t stream) {
+                   int rows_cap, cudaStream_t stream) {
+  int* cap_status = mgb_host::capacity_status_ptr();
+  if (!cap_status) return MGB_ECUDA;
   if (PAIR) {
     if (const int rc = mgb_host::ensure_max_smem((const void*)mgb::moe_gemm_pair_kernel<GATED, ROWPTR>,
                                                  mgb::pair_smem<GATED>()))
@@ -516,7 +520,7 @@ int launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtenso
     }();
     mgb::moe_gemm_pair_kernel<GATED, ROWPTR><<<grid, mgb::Epi<GATED>::kThreads, mgb::pair_smem<GATED>(), stream>>>(
         tmA, tmB, tmB8, offsets, E, MT / 2, K, rows_per_expert, half_rows, reinterpret_cast<__nv_bfloat16*>(out), ldo,
-        balanced, row_ptr, nalign);
+        balanced, row_ptr, nalign, rows_cap, cap_status);
   } else {
     if (const int rc = mgb_host::ensure_max_smem((const void*)mgb::moe_gemm_kernel<GATED, ROWPTR>,
                                                  mgb::gemm_smem<GATED>()))
@@ -524,7 +528,7 @@ int launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtenso
     mgb::moe_gemm_kernel<GATED, ROWPTR><<<mgb_host::num_sms(), mgb::Epi<GATED>::kThreads, mgb::gemm_smem<GATED>(),
                                           stream>>>(
         tmA, tmB, offsets, E, MT, K, rows_per_expert, half_rows, reinterpret_cast<__nv_bfloat16*>(out), ldo, balanced,
-        row_ptr);
+        row_ptr, rows_cap, cap_status);
   }
   return mgb_host::launch_status();
 }
@@ -554,14 +558,14 @@ int launch_moe_gemm(const void* w, int w_rows_total, const void* act, int act_ro
   if (row_ptr) {
     if (GATED) return MGB_EINVAL;  // only the down GEMM sends rows home
     return pair ? launch_variant<GATED, true, true>(tmA, tmB, tmB8, offsets, E, MT, K, rows_per_expert, half_rows, out, ldo,
-                                                   balanced, row_ptr, stream)
+                                                   balanced, row_ptr, act_rows, stream)
                 : launch_variant<GATED, false, true>(tmA, tmB, tmB, offsets, E, MT, K, rows_per_expert, half_rows, out, ldo,
-                                                    balanced, row_ptr, stream);
+                                                    balanced, row_ptr, act_rows, stream);
   }
   return pair ? launch_variant<GATED, true, false>(tmA, tmB, tmB8, offsets, E, MT, K, rows_per_expert, half_rows, out, ldo,
-                                                  balanced, nullptr, stream)
+                                                  balanced, nullptr, act_rows, stream)
               : launch_variant<GATED, false, false>(tmA, tmB, tmB, offsets, E, MT, K, rows_per_expert, half_rows, out, ldo,
-                                                   balanced, nullptr, stream);
+                                                   balanced, nullptr, act_rows, stream);
 }
 }  // namespace
 

@@ -342,7 +342,8 @@ __global__ void permute_kernel(const __nv_bfloat16* __restrict__ x, const int* _
                                const int* __restrict__ offsets, int T, int d, int k, int E, int tpb,
                                __nv_bfloat16* __restrict__ x_perm, int* __restrict__ src_token,
                                int* __restrict__ dst_pos, const long long* __restrict__ peer_base,
-                               const int* __restrict__ disp_row, int E_local) {
+                               const int* __restrict__ disp_row, int E_local, int recv_cap,
+                               int* __restrict__ cap_status) {
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (gw >= T * k) return;
@@ -363,9 +364,21 @@ __global__ void permute_kernel(const __nv_bfloat16* __restrict__ x, const int* _
   }
   // expert-parallel dispatch fused into the permutation: the row goes straight into the receive
   // buffer of the expert's owner rank (peer memory over NVLink), at this source's segment of expert e
-  uint4* dst = peer_base ? reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(peer_base[e / E_local]) +
-                                                     (size_t)(disp_row[e] + pos - offsets[e]) * d)
-                         : reinterpret_cast<uint4*>(x_perm + (size_t)pos * d);
+  uint4* dst;
+  if (peer_base) {
+    const int row = disp_row[e] + pos - offsets[e];
+    if (row < 0 || row >= recv_cap) {  // the owner's receive buffer is full: status, no write
+      if (lane == 0 && atomicCAS(cap_status, 0, MGB_ECAPACITY) == 0) {
+        cap_status[1] = row + 1;
+        cap_status[2] = recv_cap;
+        cap_status[3] = kCapDispatch;
+      }
+      return;
+    }
+    dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(peer_base[e / E_local]) + (size_t)row * d);
+  } else {
+    dst = reinterpret_cast<uint4*>(x_perm + (size_t)pos * d);
+  }
 #pragma unroll
   for (int u = 0; u < U; ++u)
     if (lane + 32 * u < nvec) dst[lane + 32 * u] = v[u];
@@ -550,25 +563,30 @@ int mgb_permute(const void* x, const int* topk_idx, const int* local_rank, const
   const int blocks = (warps * 32 + threads - 1) / threads;
   (d <= 2048 ? mgb::permute_kernel<8> : mgb::permute_kernel<16>)<<<blocks, threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<const __nv_bfloat16*>(x), topk_idx, local_rank, block_base, offsets, T, d, k, E,
-      mgb::kRouterTPB, reinterpret_cast<__nv_bfloat16*>(x_perm), src_token, dst_pos, nullptr, nullptr, 1);
+      mgb::kRouterTPB, reinterpret_cast<__nv_bfloat16*>(x_perm), src_token, dst_pos, nullptr, nullptr, 1, 0, nullptr);
   return mgb_host::launch_status();
 }
 
 // Expert-parallel dispatch fused with the permutation: row (t, j) of expert e = topk_idx[t, j] is
 // written to peer_base[e / E_local] (the owner rank's receive buffer, a UVA peer pointer) at row
 // disp_row[e] + (its position within expert e's segment).  dst_pos / src_token are the local
-// permuted positions, as mgb_permute writes them (the combine on this rank uses them).
+// permuted positions, as mgb_permute writes them (the combine on this rank uses them).  A row that
+// would land at or past recv_rows_cap (the owner's fixed-capacity receive buffer) is not written;
+// the overflow is recorded for mgb_capacity_status.
 int mgb_ep_permute_dispatch(const void* x, const int* topk_idx, const int* local_rank, const int* block_base,
                             const int* offsets, int T, int d, int k, int E, int E_local, const long long* peer_base,
-                            const int* disp_row, int* src_token, int* dst_pos, void* stream) {
-  if (T < 1 || d % 8 || k < 1 || k > mgb::kMaxK || E_local < 1 || E % E_local || !peer_base || !disp_row)
+                            const int* disp_row, int recv_rows_cap, int* src_token, int* dst_pos, void* stream) {
+  if (T < 1 || d % 8 || k < 1 || k > mgb::kMaxK || E_local < 1 || E % E_local || !peer_base || !disp_row ||
+      recv_rows_cap < 1)
     return MGB_EINVAL;
+  int* cap_status = mgb_host::capacity_status_ptr();
+  if (!cap_status) return MGB_ECUDA;
   const int warps = T * k;
   const int threads = 256;
   const int blocks = (warps * 32 + threads - 1) / threads;
   (d <= 2048 ? mgb::permute_kernel<8> : mgb::permute_kernel<16>)<<<blocks, threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<const __nv_bfloat16*>(x), topk_idx, local_rank, block_base, offsets, T, d, k, E,
-      mgb::kRouterTPB, nullptr, src_token, dst_pos, peer_base, disp_row, E_local);
+      mgb::kRouterTPB, nullptr, src_token, dst_pos, peer_base, disp_row, E_local, recv_rows_cap, cap_status);
   return mgb_host::launch_status();
 }
 

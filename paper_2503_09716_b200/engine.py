@@ -1167,6 +1167,8 @@ class Engine:
         self.host_pos = P
         return b.next_ids.to("cpu", torch.int64)
 
+    prefill_min_be = 256  # floor of the streamed prefill's expert scratch (rows)
+
     @torch.no_grad()
     def _prefill_streamed(self, input_ids: torch.Tensor, chunk_tokens: int) -> torch.Tensor:
         """Prefill with offloaded weights, module-based batching style: layer by
@@ -1186,7 +1188,10 @@ class Engine:
         xp, yp = torch.empty(T * k, d, **bf), torch.empty(T * k, d, **bf)
         lg = torch.empty(T, E, dtype=torch.float32, device=self.device)
         ws = ops.RouterWorkspace(T, E, k, device=self.device)
-        hf = torch.empty(0, **bf)
+        # expert activation scratch of b_e rows (the planner's memory model, memory_model.py): an expert
+        # group larger than b_e is re-split into b_e-row launches (exec_sim.py:170-175), never overrun
+        be = max(self.prefill_min_be, int(self.plan.b_e))
+        hf = torch.empty(be, f, **bf)
         ids = input_ids.to(self.device, torch.int32)
         self.reset(0)
         st, cp = self.stream, self.h2d
@@ -1228,11 +1233,13 @@ class Engine:
                 ops.router_topk(None, None, ws, k, a.router_mode, a.routed_scaling, a.n_group, a.topk_group,
                                 logits_in=lg)
                 ops.permute(h_all, ws, xp)
-                offs = ws.offsets.cpu().tolist()  # host sync once per layer: per-expert row ranges
+                # host sync once per layer: per-expert row counts (the capacity pre-flight; x_perm holds
+                # all T*k rows by construction, the b_e scratch is handled by the re-split below)
+                cnt = ops.check_capacity(ws.offsets, T * k)
+                offs = [0]
+                for c in cnt:
+                    offs.append(offs[-1] + c)
                 n_c = w.place.experts_per_layer[l]
-                need = max(offs[e + 1] - offs[e] for e in range(E))
-                if hf.shape[0] < need:
-                    hf = torch.empty(need, f, **bf)
                 u = 0  # uncached experts streamed so far in this layer
                 for e in range(E):
                     r0, r1 = offs[e], offs[e + 1]
@@ -1246,10 +1253,11 @@ class Engine:
                             landed[sl].record(cp)
                         st.wait_event(landed[sl])
                         gu, dn = w.slot_views(sl)
-                    if r1 > r0:
-                        lo = torch.tensor([0, r1 - r0], dtype=torch.int32, device=self.device)
-                        ops.moe_gemm_gate_up(gu, xp[r0:r1], lo, hf[:r1 - r0])
-                        ops.moe_gemm_down(dn, hf[:r1 - r0], lo, yp[r0:r1])
+                    for c0 in range(r0, r1, be):  # b_e-row pieces of the expert's group
+                        c1 = min(r1, c0 + be)
+                        lo = self._segment(c1 - c0)
+                        ops.moe_gemm_gate_up(gu, xp[c0:c1], lo, hf[:c1 - c0])
+                        ops.moe_gemm_down(dn, hf[:c1 - c0], lo, yp[c0:c1])
                     if e >= n_c:
                         slot_free[u % 2].record(st)
                         u += 1

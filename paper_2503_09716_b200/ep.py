@@ -121,7 +121,8 @@ class PeerExpertParallel:
     barrier between the three phases."""
 
     def __init__(self, n_experts: int, world: int, rank: int, recv_ptrs, yperm_ptrs, device="cuda",
-                 recv: torch.Tensor | None = None, yperm: torch.Tensor | None = None, comm=None):
+                 recv: torch.Tensor | None = None, yperm: torch.Tensor | None = None, comm=None,
+                 recv_rows: int | None = None):
         if n_experts % world:
             raise ValueError(f"{n_experts} experts do not shard over {world} ranks")
         self.E, self.W, self.rank = n_experts, world, rank
@@ -134,6 +135,9 @@ class PeerExpertParallel:
         # this rank's own buffers (the engine's EP path reads them) and the count exchange / barrier
         # (`comm`: _SymmComm over NCCL + symmetric memory, or VirtualPeerGroup.member for virtual ranks)
         self.recv, self.yperm, self.comm = recv, yperm, comm
+        # rows of every rank's (equal-sized) receive buffer: the dispatch kernel never writes past it
+        # and records an overflow for ops.capacity_status instead (SPEC.md invariants: no silent drop)
+        self.recv_rows = int(recv_rows if recv_rows is not None else recv.shape[0] if recv is not None else 2 ** 31 - 1)
 
     def local_experts(self) -> range:
         return range(self.first, self.first + self.L)
@@ -166,7 +170,7 @@ class PeerExpertParallel:
         T, d = h.shape
         nat.call("mgb_ep_permute_dispatch", h.data_ptr(), ws.topk_idx.data_ptr(), ws.local_rank.data_ptr(),
                  ws.block_hist.data_ptr(), ws.offsets.data_ptr(), T, d, ws.k, self.E, self.L,
-                 self.peer_recv.data_ptr(), tab["disp_row"].data_ptr(), ws.src_token.data_ptr(),
+                 self.peer_recv.data_ptr(), tab["disp_row"].data_ptr(), self.recv_rows, ws.src_token.data_ptr(),
                  ws.dst_pos.data_ptr(), torch.cuda.current_stream().cuda_stream)
 
     def experts(self, w_gate_up: torch.Tensor, w_down: torch.Tensor, recv: torch.Tensor, h_ffn: torch.Tensor,

@@ -62,6 +62,49 @@ def permute(x: torch.Tensor, ws: RouterWorkspace, x_perm: torch.Tensor, T: int |
              x.shape[1], ws.k, ws.E, _p(x_perm), _p(ws.src_token), _p(ws.dst_pos), _s())
 
 
+class CapacityError(RuntimeError):
+    """A grouped launch's row segments exceed the buffer they land in (MGB_ECAPACITY); `counts`
+    are the per-expert rows (pre-flight) or {needed, rows_cap, site} (recorded on the device)."""
+
+    def __init__(self, msg: str, counts=None, needed: int = 0, rows_cap: int = 0, site: int = 0):
+        super().__init__(msg)
+        self.counts, self.needed, self.rows_cap, self.site = counts, needed, rows_cap, site
+
+
+def check_capacity(offsets: torch.Tensor, rows_cap: int) -> list[int]:
+    """Host pre-flight of a grouped launch (synchronises the current stream): per-expert row counts,
+    or CapacityError when offsets[E] > rows_cap -- the scheduler then re-splits by b_e."""
+    import ctypes
+
+    E = offsets.numel() - 1
+    counts = (ctypes.c_int * E)()
+    rc = nat.raw("mgb_moe_check_capacity", _p(offsets), E, rows_cap, counts, _s())
+    out = list(counts)
+    if rc == -2:
+        raise CapacityError(f"row segments need {sum(out)} rows > capacity {rows_cap}", counts=out,
+                            needed=sum(out), rows_cap=rows_cap)
+    if rc != 0:
+        raise nat.NativeError(f"mgb_moe_check_capacity failed: {nat.STATUS.get(rc, rc)}")
+    return out
+
+
+SITES = {1: "moe_gemm_gate_up", 2: "moe_gemm_down", 3: "ep_permute_dispatch"}
+
+
+def capacity_status(reset: bool = True) -> None:
+    """Raise CapacityError if a grouped GEMM / EP dispatch recorded an overflow on this device since
+    the last call (synchronises the device; cleared when reset)."""
+    import ctypes
+
+    st = (ctypes.c_int * 4)()
+    rc = nat.raw("mgb_capacity_status", st, int(reset))
+    if rc == -2:
+        raise CapacityError(f"{SITES.get(st[3], st[3])}: {st[1]} rows needed > capacity {st[2]} (no rows were "
+                            f"written past the buffer)", needed=st[1], rows_cap=st[2], site=st[3])
+    if rc != 0:
+        raise nat.NativeError(f"mgb_capacity_status failed: {nat.STATUS.get(rc, rc)}")
+
+
 def moe_gemm_gate_up(w_gate_up: torch.Tensor, x_perm: torch.Tensor, offsets: torch.Tensor, h_out: torch.Tensor) -> None:
     E, two_f, d = w_gate_up.shape
     nat.call("mgb_moe_gemm_gate_up", _p(w_gate_up), _p(x_perm), _p(offsets), E, d, two_f // 2, x_perm.shape[0],

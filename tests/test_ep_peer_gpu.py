@@ -45,7 +45,8 @@ def test_peer_ep_bit_exact(W, E, k, d, f, T):
     yperm = [torch.zeros(T * k, d, dtype=torch.bfloat16, device=dev) for _ in range(W)]
     counts_all = torch.stack([ws.counts for ws in wss])
     L = E // W
-    peps = [PeerExpertParallel(E, W, r, [b.data_ptr() for b in recv], [b.data_ptr() for b in yperm]) for r in range(W)]
+    peps = [PeerExpertParallel(E, W, r, [b.data_ptr() for b in recv], [b.data_ptr() for b in yperm], recv_rows=cap)
+            for r in range(W)]
     tabs = [p.tables(counts_all) for p in peps]
     for r in range(W):  # phase 1: every source dispatches
         peps[r].dispatch(xs[r], wss[r], tabs[r])

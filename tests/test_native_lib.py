@@ -44,7 +44,7 @@ def test_python_binding_covers_header():
 def test_value_entry_points_without_gpu(lib):
     from paper_2503_09716_b200 import _native
 
-    assert _native.value("mgb_abi_version") == 1
+    assert _native.value("mgb_abi_version") == 2
     assert _native.value("mgb_kv_page_size") == 64
     assert _native.value("mgb_router_num_blocks", 827) == 104
 
