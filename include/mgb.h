@@ -52,6 +52,19 @@ int mgb_router_topk(const void* x, const void* w_gate, const float* logits_in, i
                     float* topk_w, int* local_rank, int* block_hist, int* counts, int* offsets, int* ticket,
                     void* stream);
 
+/* ---- fused decode routing front end (route.cu): residual add + RMSNorm (x <- x + delta,
+ * h = RMSNorm(x) * ln_w), router logits on the tensor cores, softmax / top-k, counts / offsets and
+ * the stable expert-major permutation of h into x_perm -- one launch for ROUTER + the grouping in
+ * front of EXPERT_COMPUTE (offload_dag.py:418-463).  chunk_hist: mgb_moe_route_chunks(T) x E ints;
+ * sync: 2 ints zeroed once.  -1 (and no launch) when T is beyond one co-resident grid
+ * (mgb_moe_route_supported); the unfused entry points cover every T. */
+int mgb_moe_route_chunks(int T);
+int mgb_moe_route_supported(int T, int d, int E);
+int mgb_moe_route(const void* x, const void* delta, const void* ln_w, float eps, int T, int d, void* x_out,
+                  void* h_out, const void* w_router, int E, int k, int mode, float scaling, int n_group,
+                  int topk_group, float* logits_out, int* topk_idx, float* topk_w, int* local_rank, int* chunk_hist,
+                  int* counts, int* offsets, void* x_perm, int* src_token, int* dst_pos, int* sync, void* stream);
+
 /* ---- token grouping in front of EXPERT_COMPUTE (offload_dag.py:427-463) ------------------
  * Stable expert-major permutation; x_perm[rows_cap,d], src_token[rows_cap], dst_pos[T*k]. */
 int mgb_permute(const void* x, const int* topk_idx, const int* local_rank, const int* block_base,

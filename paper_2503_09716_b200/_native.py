@@ -23,6 +23,9 @@ SIGNATURES: dict[str, list] = {
     "mgb_abi_version": [],
     "mgb_num_sms": [],
     "mgb_moe_check_capacity": [P, I, I, P, P],
+    "mgb_moe_route_chunks": [I],
+    "mgb_moe_route_supported": [I, I, I],
+    "mgb_moe_route": [P, P, P, F, I, I, P, P, P, I, I, I, F, I, I, P, P, P, P, P, P, P, P, P, P, P, P],
     "mgb_capacity_status": [P, I],
     "mgb_kv_page_size": [],
     "mgb_router_num_blocks": [I],
@@ -77,7 +80,7 @@ class CpuAttnGqa(ctypes.Structure):
                 ("hd", ctypes.c_int32), ("page_tokens", ctypes.c_int32), ("scale", F), ("status", ctypes.c_int32)]
 
 # entry points that return a value rather than a status
-VALUE_FNS = {"mgb_prefill_attn_supported", "mgb_cpu_threads", "mgb_cpu_attn_simd", "mgb_abi_version", "mgb_num_sms", "mgb_kv_page_size", "mgb_mla_page_size", "mgb_mla_page_elems",
+VALUE_FNS = {"mgb_moe_route_chunks", "mgb_moe_route_supported", "mgb_prefill_attn_supported", "mgb_cpu_threads", "mgb_cpu_attn_simd", "mgb_abi_version", "mgb_num_sms", "mgb_kv_page_size", "mgb_mla_page_size", "mgb_mla_page_elems",
              "mgb_router_num_blocks", "mgb_router_tokens_per_block"}
 
 STATUS = {0: "ok", -1: "invalid argument", -2: "capacity exceeded", -3: "CUDA error"}

@@ -286,6 +286,13 @@ class Engine:
         self._forced_logits: torch.Tensor | None = None  # [layers, B, E] router input (force_routing)
         self._segments: dict[int, torch.Tensor] = {}
         self._dense_mlp_cublas = os.environ.get("MGB_DENSE_MLP", "gemm") == "cublas"
+        # decode routing front end as ONE launch (route.cu: residual add + RMSNorm + router logits +
+        # top-k + counts/offsets + permutation) for HBM-resident weights without EP; MGB_FUSED_ROUTE=0
+        # restores add_rmsnorm + cuBLAS logits + router_topk + permute
+        # (measured, tools/route_bench.py: faster for Mixtral's 8 experts; DeepSeek's 64-160-expert routing
+        # stays on the unfused kernels, whose cuBLAS logits GEMM and wide top-k grid win there)
+        self.fused_route = (os.environ.get("MGB_FUSED_ROUTE", "1") != "0" and not self.offload and self.ep is None
+                            and a.n_experts <= 16 and ops.moe_route_supported(B, a.hidden, a.n_experts))
         self.kernel_launches_per_step = self._count_launches()
         self.host_pos = 0
 
@@ -647,6 +654,8 @@ class Engine:
             torch.bmm(o_lat, W["w_uv_t"], out=o_hb)  # o_hb is a [H, n, v] view of o_cat[s0:s1]
         elif j.kind == "post_attention":
             torch.mm(m["o_cat"], W["wo"].t(), out=b.o)
+            if self._route_fused(l):
+                return  # residual add + norm, routing and the shared experts run in the router job
             ops.add_rmsnorm(b.x, W["ln2"], a.rms_eps, b.h, delta=b.o, x_out=b.x)
             if l >= a.first_k_dense:
                 # shared experts on every token (DeepseekV2Moe.shared_experts): dense -> cuBLAS.  They are
@@ -654,7 +663,13 @@ class Engine:
                 # single dense buffer is handed to the next layer's copy (offload_dag.py:308-321)
                 self._dense_mlp(W["sh_gate_up"], W["sh_down"], b.h, m["sh_h"], m["sh_out"], m["offsets_all"])
         elif j.kind == "router":
-            if l >= a.first_k_dense:
+            if self._route_fused(l):
+                ops.moe_route(b.x, b.o, W["ln2"], a.rms_eps, b.h, W["router"], self.rws, b.x_perm, a.router_mode,
+                              a.routed_scaling, a.n_group, a.topk_group, x_out=b.x, logits_out=m["logits_r"])
+                self._dense_mlp(W["sh_gate_up"], W["sh_down"], b.h, m["sh_h"], m["sh_out"], m["offsets_all"])
+                if self.debug_taps is not None:
+                    self.debug_taps.update(h2=b.h.clone(), topk_idx=self.rws.topk_idx.clone())
+            elif l >= a.first_k_dense:
                 # fp32 router logits (HF: F.linear(x.float(), W.float()), modeling_deepseek_v2.py:125) as a
                 # bf16 tensor-core GEMM with fp32 output (exact products, fp32 accumulation)
                 lg = m["logits_r"]
@@ -781,9 +796,13 @@ class Engine:
                                 b.attn[s0:s1])
         elif j.kind == "post_attention":
             torch.mm(b.attn, W["wo"].t(), out=b.o)
-            ops.add_rmsnorm(b.x, W["ln2"], a.rms_eps, b.h, delta=b.o, x_out=b.x)
+            if not self._route_fused(l):  # else the router job's fused kernel adds + normalises
+                ops.add_rmsnorm(b.x, W["ln2"], a.rms_eps, b.h, delta=b.o, x_out=b.x)
         elif j.kind == "router":
-            if self._forced_logits is not None:
+            if self._route_fused(l):
+                ops.moe_route(b.x, b.o, W["ln2"], a.rms_eps, b.h, W["router"], self.rws, b.x_perm, a.router_mode,
+                              a.routed_scaling, a.n_group, a.topk_group, x_out=b.x, logits_out=self.logits_r)
+            elif self._forced_logits is not None:
                 ops.router_topk(None, None, self.rws, a.top_k, a.router_mode, a.routed_scaling, a.n_group,
                                 a.topk_group, logits_in=self._forced_logits[l])
             elif self.router_logits == "cublas":
@@ -795,7 +814,7 @@ class Engine:
             else:
                 ops.router_topk(b.h, W["router"], self.rws, a.top_k, a.router_mode, a.routed_scaling,
                                 a.n_group, a.topk_group)
-            if not self.peer_ep:  # peer EP permutes inside its dispatch (rows go straight to the owners)
+            if not self.peer_ep and not self._route_fused(l):  # peer EP permutes inside its dispatch
                 ops.permute(b.h, self.rws, b.x_perm)
             if self.debug_taps is not None:  # eager-only parity hook
                 self.debug_taps.update(h2=b.h.clone(), topk_idx=self.rws.topk_idx.clone(), attn=b.attn.clone())
@@ -803,6 +822,12 @@ class Engine:
             self._expert_job(l, j, W)
         else:
             raise RuntimeError(f"job kind {j.kind!r} is not executable under kv_policy={self.kv_policy!r}")
+
+    def _route_fused(self, l: int) -> bool:
+        """Layer l's routing front end runs as the fused mgb_moe_route launch (MoE layers of a resident,
+        non-EP engine without forced routing)."""
+        return (self.fused_route and self._forced_logits is None
+                and not (self.mla and l < self.arch.first_k_dense))
 
     def _mb_range(self, j) -> tuple[int, int]:
         """Sequences of a per-micro-batch job: the CPU share is [0, n_cpu), GPU micro-batch m is
@@ -818,9 +843,10 @@ class Engine:
     def _count_launches(self) -> int:
         n = 1  # embed (the final norm is fused into the last combine)
         for l in range(self.arch.layers):
+            fused = self._route_fused(l)  # one mgb_moe_route instead of add_rmsnorm + router_topk + permute
             for j in self.layer_jobs[l]:
-                n += {"pre_attention": 2 if l == 0 else 1, "attn_mech_gpu": 1, "post_attention": 1,
-                      "router": 2}.get(j.kind, 0)
+                n += {"pre_attention": 2 if l == 0 else 1, "attn_mech_gpu": 1, "post_attention": 0 if fused else 1,
+                      "router": 1 if fused else 2}.get(j.kind, 0)
             n += 3  # gate_up, down, combine
         return n + 2  # argmax, advance  (cuBLAS GEMMs are library launches, not counted)
 

@@ -39,6 +39,8 @@ class RouterWorkspace:
         self.ticket = torch.zeros(1, **i32)
         self.src_token = torch.zeros(T * k, **i32)
         self.dst_pos = torch.zeros(T * k, **i32)
+        self.sync = torch.zeros(2, **i32)  # grid barrier of mgb_moe_route
+        assert nblk >= nat.value("mgb_moe_route_chunks", T)  # block_hist doubles as its chunk_hist
 
 
 def router_topk(x: torch.Tensor | None, w_gate: torch.Tensor | None, ws: RouterWorkspace, k: int, mode: int,
@@ -54,6 +56,24 @@ def router_topk(x: torch.Tensor | None, w_gate: torch.Tensor | None, ws: RouterW
     nat.call("mgb_router_topk", _p(x), _p(w_gate), _p(logits_in), T, d, E, k, mode, scaling, n_group, topk_group,
              _p(logits_out), _p(ws.topk_idx), _p(ws.topk_w), _p(ws.local_rank), _p(ws.block_hist), _p(ws.counts),
              _p(ws.offsets), _p(ws.ticket), _s())
+
+
+def moe_route_supported(T: int, d: int, E: int) -> bool:
+    return bool(nat.value("mgb_moe_route_supported", T, d, E))
+
+
+def moe_route(x: torch.Tensor, delta: torch.Tensor | None, ln_w: torch.Tensor, eps: float, h_out: torch.Tensor,
+              w_router: torch.Tensor, ws: RouterWorkspace, x_perm: torch.Tensor, mode: int, scaling: float = 1.0,
+              n_group: int = 1, topk_group: int = 1, x_out: torch.Tensor | None = None,
+              logits_out: torch.Tensor | None = None) -> None:
+    """Fused decode routing front end (route.cu): x_out = x + delta, h_out = RMSNorm(x_out) * ln_w,
+    top-k routing of h_out, and the stable expert-major permutation of h_out into x_perm."""
+    T, d = x.shape
+    E = w_router.shape[0]
+    nat.call("mgb_moe_route", _p(x), _p(delta), _p(ln_w), eps, T, d, _p(x_out), _p(h_out), _p(w_router), E, ws.k,
+             mode, scaling, n_group, topk_group, _p(logits_out), _p(ws.topk_idx), _p(ws.topk_w), _p(ws.local_rank),
+             _p(ws.block_hist), _p(ws.counts), _p(ws.offsets), _p(x_perm), _p(ws.src_token), _p(ws.dst_pos),
+             _p(ws.sync), _s())
 
 
 def permute(x: torch.Tensor, ws: RouterWorkspace, x_perm: torch.Tensor, T: int | None = None) -> None:

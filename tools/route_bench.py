@@ -1,0 +1,58 @@
+"""Decode routing front end at the bench shapes (CUDA events, us per call): the fused mgb_moe_route
+against the unfused chain add_rmsnorm + cuBLAS fp32 logits + router_topk + permute.
+
+python tools/route_bench.py   -> one JSON line per shape
+"""
+import json
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2503_09716_b200 import ops  # noqa: E402
+
+BF16 = torch.bfloat16
+SHAPES = [("mixtral-8x7b", 827, 4096, 8, 2, 0, 1, 1), ("deepseek-v2-lite", 6058, 2048, 64, 6, 1, 1, 1),
+          ("mixtral-8x22b", 271, 6144, 8, 2, 0, 1, 1), ("deepseek-v2", 1024, 5120, 160, 6, 2, 8, 3)]
+
+
+def timed(fn, n=50):
+    for _ in range(5):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(n):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / n * 1e3
+
+
+for name, T, d, E, k, mode, ng, tg in SHAPES:
+    x = torch.randn(T, d, device="cuda").to(BF16)
+    o = torch.randn(T, d, device="cuda").to(BF16)
+    ln = torch.ones(d, device="cuda", dtype=BF16)
+    wr = (torch.randn(E, d, device="cuda") * 0.02).to(BF16)
+    ws = ops.RouterWorkspace(T, E, k)
+    h = torch.empty(T, d, device="cuda", dtype=BF16)
+    xo = torch.empty_like(h)
+    xp = torch.empty(T * k, d, device="cuda", dtype=BF16)
+    lg = torch.empty(T, E, device="cuda", dtype=torch.float32)
+    row = {"shape": name, "T": T, "d": d, "E": E, "k": k}
+    if ops.moe_route_supported(T, d, E):
+        row["fused_us"] = timed(lambda: ops.moe_route(x, o, ln, 1e-5, h, wr, ws, xp, mode, 1.0, ng, tg, x_out=xo,
+                                                      logits_out=lg))
+
+    def unfused():
+        ops.add_rmsnorm(x, ln, 1e-5, h, delta=o, x_out=xo)
+        torch.mm(h, wr.t(), out_dtype=torch.float32, out=lg)
+        ops.router_topk(None, None, ws, k, mode, 1.0, ng, tg, logits_in=lg)
+        ops.permute(h, ws, xp)
+    row["unfused_us"] = timed(unfused)
+    row["norm_us"] = timed(lambda: ops.add_rmsnorm(x, ln, 1e-5, h, delta=o, x_out=xo))
+    row["logits_us"] = timed(lambda: torch.mm(h, wr.t(), out_dtype=torch.float32, out=lg))
+    row["topk_us"] = timed(lambda: ops.router_topk(None, None, ws, k, mode, 1.0, ng, tg, logits_in=lg))
+    row["permute_us"] = timed(lambda: ops.permute(h, ws, xp))
+    print(json.dumps({k_: (round(v, 2) if isinstance(v, float) else v) for k_, v in row.items()}), flush=True)
