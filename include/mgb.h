@@ -59,6 +59,7 @@ int mgb_router_topk(const void* x, const void* w_gate, const float* logits_in, i
  * sync: 2 ints zeroed once.  -1 (and no launch) when T is beyond one co-resident grid
  * (mgb_moe_route_supported); the unfused entry points cover every T. */
 int mgb_moe_route_chunks(int T);
+int mgb_moe_route_stamps(long long* stamps); /* profiling: per-CTA phase globaltimer stamps [G][16], NULL = off */
 int mgb_moe_route_supported(int T, int d, int E);
 int mgb_moe_route(const void* x, const void* delta, const void* ln_w, float eps, int T, int d, void* x_out,
                   void* h_out, const void* w_router, int E, int k, int mode, float scaling, int n_group,

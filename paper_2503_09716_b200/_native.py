@@ -24,6 +24,7 @@ SIGNATURES: dict[str, list] = {
     "mgb_num_sms": [],
     "mgb_moe_check_capacity": [P, I, I, P, P],
     "mgb_moe_route_chunks": [I],
+    "mgb_moe_route_stamps": [P],
     "mgb_moe_route_supported": [I, I, I],
     "mgb_moe_route": [P, P, P, F, I, I, P, P, P, I, I, I, F, I, I, P, P, P, P, P, P, P, P, P, P, P, P],
     "mgb_capacity_status": [P, I],

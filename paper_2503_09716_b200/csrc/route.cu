@@ -26,13 +26,14 @@
 
 namespace mgb {
 
-constexpr int kRteTPC = 16;       // tokens per chunk (the MMA M)
-constexpr int kRteThreads = 512;  // 16 warps: one token of a chunk per warp
+constexpr int kRteTPC = 8;        // tokens per chunk (half the MMA M: rows 8-15 of the A tile alias 0-7)
+constexpr int kRteThreads = 256;  // 8 warps: one token of a chunk per warp
 constexpr int kRteWarps = kRteThreads / 32;
 constexpr int kRteMaxE = 256;
 constexpr int kRteMaxK = 8;
 constexpr int kRteMaxOwn = 4;     // chunks per CTA
-constexpr int kRteU = 4;          // 16-byte vectors per lane in flight in the row passes
+constexpr int kRteU = 4;          // 16-byte vectors per lane in flight in the permutation copies
+constexpr int kRteDU = 8;         // delta vectors per lane in flight per batch
 constexpr int kRteKB = 8;         // k-steps of router-weight fragments in flight per warp
 
 struct RouteArgs {
@@ -58,7 +59,16 @@ struct RouteArgs {
   int* dst_pos;                // [T * k]
   int* sync;                   // [2] grid barrier {arrivals, generation}, zero on first use
   int nchunks;
+  long long* stamps;           // optional [G][16] globaltimer per phase (tools/route_bench.py --phases)
 };
+
+MGB_DEVINL long long rte_globaltimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define MGB_RTE_STAMP(i) \
+  if (a.stamps && threadIdx.x == 0) a.stamps[blockIdx.x * 16 + (i)] = rte_globaltimer()
 
 MGB_DEVINL bool rte_better(float va, int ia, float vb, int ib) { return va > vb || (va == vb && ia < ib); }
 
@@ -127,9 +137,10 @@ struct RteSmem {
   __nv_bfloat16* lnw;  // [d] norm weight (staged once per CTA)
 };
 
-__global__ void __launch_bounds__(kRteThreads, 1) moe_route_kernel(RouteArgs a) {
+__global__ void __launch_bounds__(kRteThreads, 2) moe_route_kernel(RouteArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int d = a.d, E = a.E, k = a.k;
+  MGB_RTE_STAMP(9);
   RteSmem s;
   s.hstride = d + 8;
   s.h = reinterpret_cast<__nv_bfloat16*>(smem);
@@ -137,8 +148,13 @@ __global__ void __launch_bounds__(kRteThreads, 1) moe_route_kernel(RouteArgs a) 
   s.part = s.logit + kRteTPC * E;
   s.exp = reinterpret_cast<int*>(s.part + kRteWarps * kRteTPC * 8);
   s.lnw = reinterpret_cast<__nv_bfloat16*>(s.exp + kRteTPC * kRteMaxK);
+  __shared__ __align__(8) uint64_t s_xbar;  // the chunk's x rows landed (bulk copies)
   for (int i = threadIdx.x; i < d / 8; i += kRteThreads)
     reinterpret_cast<uint4*>(s.lnw)[i] = ld_nc_v4(reinterpret_cast<const uint4*>(a.ln_w) + i);
+  if (threadIdx.x == 0) {
+    mbar_init(&s_xbar, 1);
+    fence_mbar_init();
+  }
   __syncthreads();
   __shared__ int s_tot[kRteMaxE];
   __shared__ int s_off[kRteMaxE + 1];
@@ -151,6 +167,7 @@ __global__ void __launch_bounds__(kRteThreads, 1) moe_route_kernel(RouteArgs a) 
   int n_own = 0;
 
   // ======================= phase 1: per owned chunk =======================
+  MGB_RTE_STAMP(0);
   for (int c = blockIdx.x; c < a.nchunks; c += G, ++n_own) {
     const int t0 = c * kRteTPC;
     const int ntok = min(kRteTPC, a.T - t0);
@@ -178,6 +195,15 @@ __global__ void __launch_bounds__(kRteThreads, 1) moe_route_kernel(RouteArgs a) 
     if (mma_warp) load_b(bcur, nt0, ks0);
 
     // ---- residual add + RMSNorm, warp per token; rows land in smem (and h_out) ----
+    // the chunk's x rows arrive by bulk copy (TMA engine) while every lane has all of its delta
+    // vectors in flight: one memory round trip per chunk instead of one per vector batch
+    if (threadIdx.x == 0) {
+      fence_proxy_async_smem();  // the previous chunk's generic writes to s.h precede the async-proxy fill
+      mbar_arrive_expect_tx(&s_xbar, (uint32_t)ntok * d * 2);
+      for (int tl = 0; tl < ntok; ++tl)
+        bulk_load(s.h + (size_t)tl * s.hstride, a.x + (size_t)(t0 + tl) * d, (uint32_t)d * 2, &s_xbar,
+                  policy_evict_normal());
+    }
     for (int tl = warp; tl < kRteTPC; tl += kRteWarps) {
       uint4* srow = reinterpret_cast<uint4*>(s.h + (size_t)tl * s.hstride);
       if (tl >= ntok) {  // tail rows of the last chunk: zeros (they never leave smem)
@@ -185,34 +211,35 @@ __global__ void __launch_bounds__(kRteThreads, 1) moe_route_kernel(RouteArgs a) 
         continue;
       }
       const size_t t = (size_t)(t0 + tl);
-      const uint4* xr = reinterpret_cast<const uint4*>(a.x + t * d);
       const uint4* dr = a.delta ? reinterpret_cast<const uint4*>(a.delta + t * d) : nullptr;
       float ss = 0.f;
-      // kRteU 16-byte vectors per lane in flight (x and delta) before any store of the batch
-      for (int c0 = lane; c0 < nvec; c0 += 32 * kRteU) {
-        uint4 v[kRteU], dv[kRteU];
+      bool landed = false;
+      for (int c0 = lane; c0 < nvec; c0 += 32 * kRteDU) {
+        uint4 dv[kRteDU];
+        if (dr) {
 #pragma unroll
-        for (int u = 0; u < kRteU; ++u) {
-          const int cc = c0 + 32 * u;
-          if (cc < nvec) {
-            v[u] = xr[cc];
-            if (dr) dv[u] = dr[cc];
-          }
+          for (int u = 0; u < kRteDU; ++u)
+            if (c0 + 32 * u < nvec) dv[u] = ld_nc_v4(dr + c0 + 32 * u);
+        }
+        if (!landed) {
+          mbar_wait(&s_xbar, n_own & 1);
+          landed = true;
         }
 #pragma unroll
-        for (int u = 0; u < kRteU; ++u) {
+        for (int u = 0; u < kRteDU; ++u) {
           const int cc = c0 + 32 * u;
           if (cc >= nvec) continue;
+          uint4 v = srow[cc];
           if (dr) {
-            v[u].x = pack_bf16x2(bf16lo(v[u].x) + bf16lo(dv[u].x), bf16hi(v[u].x) + bf16hi(dv[u].x));
-            v[u].y = pack_bf16x2(bf16lo(v[u].y) + bf16lo(dv[u].y), bf16hi(v[u].y) + bf16hi(dv[u].y));
-            v[u].z = pack_bf16x2(bf16lo(v[u].z) + bf16lo(dv[u].z), bf16hi(v[u].z) + bf16hi(dv[u].z));
-            v[u].w = pack_bf16x2(bf16lo(v[u].w) + bf16lo(dv[u].w), bf16hi(v[u].w) + bf16hi(dv[u].w));
+            v.x = pack_bf16x2(bf16lo(v.x) + bf16lo(dv[u].x), bf16hi(v.x) + bf16hi(dv[u].x));
+            v.y = pack_bf16x2(bf16lo(v.y) + bf16lo(dv[u].y), bf16hi(v.y) + bf16hi(dv[u].y));
+            v.z = pack_bf16x2(bf16lo(v.z) + bf16lo(dv[u].z), bf16hi(v.z) + bf16hi(dv[u].z));
+            v.w = pack_bf16x2(bf16lo(v.w) + bf16lo(dv[u].w), bf16hi(v.w) + bf16hi(dv[u].w));
+            srow[cc] = v;
           }
-          if (a.x_out) reinterpret_cast<uint4*>(a.x_out + t * d)[cc] = v[u];
-          srow[cc] = v[u];
-          const float f[8] = {bf16lo(v[u].x), bf16hi(v[u].x), bf16lo(v[u].y), bf16hi(v[u].y),
-                              bf16lo(v[u].z), bf16hi(v[u].z), bf16lo(v[u].w), bf16hi(v[u].w)};
+          if (a.x_out) reinterpret_cast<uint4*>(a.x_out + t * d)[cc] = v;
+          const float f[8] = {bf16lo(v.x), bf16hi(v.x), bf16lo(v.y), bf16hi(v.y),
+                              bf16lo(v.z), bf16hi(v.z), bf16lo(v.w), bf16hi(v.w)};
 #pragma unroll
           for (int i = 0; i < 8; ++i) ss = fmaf(f[i], f[i], ss);
         }
@@ -233,11 +260,13 @@ __global__ void __launch_bounds__(kRteThreads, 1) moe_route_kernel(RouteArgs a) 
     }
     __syncthreads();
 
+    MGB_RTE_STAMP(1);
     // ---- logits[16 tokens][E] = H W_r^T on mma.sync (bf16 in, fp32 accumulate) ----
     {
       const uint32_t hbase = smem_u32(s.h);
       // ldmatrix.x4 row address of this lane: rows 0-15, the lane's 8-column half
-      const uint32_t arow = hbase + (uint32_t)((lane & 15) * s.hstride + (lane >> 4) * 8) * 2;
+      // (rows 8-15 of the 16-row A tile alias rows 0-7: their results are discarded)
+      const uint32_t arow = hbase + (uint32_t)((lane & 7) * s.hstride + (lane >> 4) * 8) * 2;
       for (int nt = nt0; mma_warp && nt < ntiles; nt += kRteWarps) {
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
         if (nt != nt0) load_b(bcur, nt, ks0);
@@ -259,14 +288,12 @@ __global__ void __launch_bounds__(kRteThreads, 1) moe_route_kernel(RouteArgs a) 
         const int r = lane >> 2, cn = 2 * (lane & 3);
         if (ksplit == 1) {
           const int e0 = nt * 8 + cn;
-          if (e0 < E) { s.logit[r * E + e0] = acc[0]; s.logit[(r + 8) * E + e0] = acc[2]; }
-          if (e0 + 1 < E) { s.logit[r * E + e0 + 1] = acc[1]; s.logit[(r + 8) * E + e0 + 1] = acc[3]; }
+          if (e0 < E) s.logit[r * E + e0] = acc[0];
+          if (e0 + 1 < E) s.logit[r * E + e0 + 1] = acc[1];
         } else {
           float* p = s.part + warp * kRteTPC * 8;
           p[r * 8 + cn] = acc[0];
           p[r * 8 + cn + 1] = acc[1];
-          p[(r + 8) * 8 + cn] = acc[2];
-          p[(r + 8) * 8 + cn + 1] = acc[3];
         }
       }
       if (ksplit > 1) {
@@ -281,6 +308,7 @@ __global__ void __launch_bounds__(kRteThreads, 1) moe_route_kernel(RouteArgs a) 
     }
     __syncthreads();
 
+    MGB_RTE_STAMP(2);
     // ---- softmax + pinned-order top-k, warp per token ----
     for (int tl = warp; tl < ntok; tl += kRteWarps) {
       const int t = t0 + tl;
@@ -343,6 +371,7 @@ __global__ void __launch_bounds__(kRteThreads, 1) moe_route_kernel(RouteArgs a) 
     }
     __syncthreads();
 
+    MGB_RTE_STAMP(3);
     // ---- chunk histogram + stable in-chunk ranks ----
     const int nent = ntok * k;
     for (int i = threadIdx.x; i < nent; i += kRteThreads) {
@@ -356,11 +385,14 @@ __global__ void __launch_bounds__(kRteThreads, 1) moe_route_kernel(RouteArgs a) 
       for (int j = 0; j < nent; ++j) cnt += (s.exp[j] == e);
       a.chunk_hist[(size_t)c * E + e] = cnt;
     }
+    MGB_RTE_STAMP(4);
     __syncthreads();  // s.h / s.exp are reused by the next chunk
   }
 
   // ======================= grid barrier =======================
+  MGB_RTE_STAMP(5);
   grid_barrier(a.sync, G);
+  MGB_RTE_STAMP(6);
 
   // ======================= phase 2: bases, offsets, permutation =======================
   {
@@ -412,6 +444,7 @@ __global__ void __launch_bounds__(kRteThreads, 1) moe_route_kernel(RouteArgs a) 
       }
     }
   }
+  MGB_RTE_STAMP(7);
   // permutation: warp per (token, slot) entry; the last chunk's rows are still in smem
   for (int i = 0; i < n_own; ++i) {
     const int c = blockIdx.x + i * G;
@@ -441,6 +474,7 @@ __global__ void __launch_bounds__(kRteThreads, 1) moe_route_kernel(RouteArgs a) 
       }
     }
   }
+  MGB_RTE_STAMP(8);
 }
 
 // Allow the largest dynamic smem the device offers once per device (the attribute is per kernel and
@@ -462,7 +496,18 @@ size_t route_smem(int d, int E) {
 
 }  // namespace mgb
 
+namespace {
+long long* g_route_stamps = nullptr;  // phase timestamps of the next launches (profiling only)
+}
+
 extern "C" {
+
+// Profiling hook: record per-CTA globaltimer stamps of mgb_moe_route's phases into stamps[G][16]
+// (device memory) on subsequent launches; NULL turns it off.
+int mgb_moe_route_stamps(long long* stamps) {
+  g_route_stamps = stamps;
+  return MGB_OK;
+}
 
 // Rows of the chunk_hist workspace mgb_moe_route needs for T tokens (16-token chunks).
 int mgb_moe_route_chunks(int T) { return (T + mgb::kRteTPC - 1) / mgb::kRteTPC; }
@@ -496,7 +541,8 @@ int mgb_moe_route(const void* x, const void* delta, const void* ln_w, float eps,
                    reinterpret_cast<const __nv_bfloat16*>(ln_w), eps, T, d, E, k, mode, scaling, n_group, topk_group,
                    reinterpret_cast<const __nv_bfloat16*>(w_router), reinterpret_cast<__nv_bfloat16*>(x_out),
                    reinterpret_cast<__nv_bfloat16*>(h_out), logits_out, topk_idx, topk_w, local_rank, chunk_hist,
-                   counts, offsets, reinterpret_cast<__nv_bfloat16*>(x_perm), src_token, dst_pos, sync, nchunks};
+                   counts, offsets, reinterpret_cast<__nv_bfloat16*>(x_perm), src_token, dst_pos, sync, nchunks,
+                   g_route_stamps};
   mgb::moe_route_kernel<<<G, mgb::kRteThreads, smem, reinterpret_cast<cudaStream_t>(stream)>>>(a);
   return mgb_host::launch_status();
 }

@@ -30,7 +30,10 @@ def timed(fn, n=50):
     return e0.elapsed_time(e1) / n * 1e3
 
 
+ONLY = sys.argv[1].split(",") if len(sys.argv) > 1 else None
 for name, T, d, E, k, mode, ng, tg in SHAPES:
+    if ONLY and name not in ONLY:
+        continue
     x = torch.randn(T, d, device="cuda").to(BF16)
     o = torch.randn(T, d, device="cuda").to(BF16)
     ln = torch.ones(d, device="cuda", dtype=BF16)
@@ -50,6 +53,20 @@ for name, T, d, E, k, mode, ng, tg in SHAPES:
         torch.mm(h, wr.t(), out_dtype=torch.float32, out=lg)
         ops.router_topk(None, None, ws, k, mode, 1.0, ng, tg, logits_in=lg)
         ops.permute(h, ws, xp)
+    if "fused_us" in row:  # per-phase split of one launch (globaltimer stamps, mgb_moe_route_stamps)
+        from paper_2503_09716_b200 import _native as nat
+        st = torch.zeros(1024, 16, dtype=torch.int64, device="cuda")
+        nat.call("mgb_moe_route_stamps", st.data_ptr())
+        ops.moe_route(x, o, ln, 1e-5, h, wr, ws, xp, mode, 1.0, ng, tg, x_out=xo, logits_out=lg)
+        torch.cuda.synchronize()
+        nat.call("mgb_moe_route_stamps", None)
+        st = st[(st[:, 9] > 0)].double()
+        t0 = st[:, 9].min()
+        names = {9: "start", 0: "lnw_staged", 1: "norm", 2: "logits", 3: "topk", 4: "hist", 5: "phase1_end",
+                 6: "barrier_out", 7: "scan", 8: "end"}
+        row["phases_us_mean_since_first_cta"] = {names[i]: round(float((st[:, i] - t0).mean()) / 1e3, 2)
+                                                 for i in (9, 0, 1, 2, 3, 4, 5, 6, 7, 8)}
+        row["phases_us_max"] = {names[i]: round(float((st[:, i] - t0).max()) / 1e3, 2) for i in (9, 5, 6, 8)}
     row["unfused_us"] = timed(unfused)
     row["norm_us"] = timed(lambda: ops.add_rmsnorm(x, ln, 1e-5, h, delta=o, x_out=xo))
     row["logits_us"] = timed(lambda: torch.mm(h, wr.t(), out_dtype=torch.float32, out=lg))
