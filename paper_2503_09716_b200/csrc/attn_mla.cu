@@ -34,6 +34,7 @@
 //           (lane = token), per-head online softmax with a warp transpose-reduction, P^T -> smem,
 //           O accumulated in registers (lane = latent dim)
 // A work item is (sequence, 16-head group); heads >= H are zero rows of Q and never stored.
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -54,6 +55,7 @@ constexpr int kMlaPage = MGB_MLA_PAGE;     // tokens per latent page (swizzle at
 constexpr int kMlaTile = 64;     // M of the S^T MMA / K of P.V: a page plus 8 phantom rows
 constexpr int kMlaStages = MGB_MLA_STAGES;  // pages in flight per SM (3 x 63 KB for R = 512)
 static_assert(kMlaPage % 8 == 0 && kMlaPage <= 64, "latent page = whole swizzle atoms within one MMA tile");
+static_assert(kMlaStages <= 8, "the MMA issuer's page ring holds 8 pages between S^T and P.V");
 constexpr int kMlaHeads = 16;    // heads per work item = N of both MMAs
 constexpr int kMlaThreads = 320;  // 8 softmax warps + producer + MMA issuer
 
@@ -100,7 +102,7 @@ struct MlaCfg {
   static constexpr int kOffP = kOffQ + kQBytes;
   static constexpr int kOffRed = kOffP + 2 * kPBytes;      // float [2][4][16] max + [4][16] sum
   static constexpr int kOffBar = kOffRed + 3 * 4 * 16 * 4;
-  static constexpr int kBars = 2 * kMlaStages + 12;
+  static constexpr int kBars = 3 * kMlaStages + 12;  // + per-stage cluster-empty barriers (multicast)
   static constexpr size_t kSmem = kOffBar + kBars * 8 + 16;
   static_assert(R % 128 == 0 && RP % 16 == 0 && kBlockBytes % 1024 == 0, "MLA shape");
   static_assert(kSmem <= 227 * 1024, "MLA smem");
@@ -133,7 +135,7 @@ decode_attn_mla_kernel(const __grid_constant__ CUtensorMap tm_qlat,  // q_lat [H
                        const __nv_bfloat16* __restrict__ cache,      // latent pages
                        const int* __restrict__ block_table, int max_pages, const int* __restrict__ seq_lens,
                        int B, int H, float scale_log2, __nv_bfloat16* __restrict__ o_lat,  // [H, B, R]
-                       int pf_dist) {
+                       int pf_dist, int cl) {
   using C = MlaCfg<R, RP>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* pages = smem;
@@ -145,8 +147,8 @@ decode_attn_mla_kernel(const __grid_constant__ CUtensorMap tm_qlat,  // q_lat [H
   constexpr int S = kMlaStages;
   uint64_t *full = bars, *empty = bars + S, *qfull = bars + 2 * S, *qempty = bars + 2 * S + 1,
            *sfull = bars + 2 * S + 2, *sempty = bars + 2 * S + 4, *pfull = bars + 2 * S + 6, *ofull = bars + 2 * S + 8,
-           *oempty = bars + 2 * S + 10;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 12);
+           *oempty = bars + 2 * S + 10, *cempty = bars + 2 * S + 12;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 12);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_hg = (H + kMlaHeads - 1) / kMlaHeads;
@@ -155,6 +157,7 @@ decode_attn_mla_kernel(const __grid_constant__ CUtensorMap tm_qlat,  // q_lat [H
     for (int s = 0; s < kMlaStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
+      mbar_init(&cempty[s], cl);  // (the leader's are used: every CTA of the cluster freed stage s)
     }
     mbar_init(qfull, 1);
     mbar_init(qempty, 1);
@@ -170,6 +173,7 @@ decode_attn_mla_kernel(const __grid_constant__ CUtensorMap tm_qlat,  // q_lat [H
   if (warp == 9) tmem_alloc<C::kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
+  if (cl > 1) cluster_sync();  // peers' barriers initialised before any remote arrive / multicast
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -178,8 +182,15 @@ decode_attn_mla_kernel(const __grid_constant__ CUtensorMap tm_qlat,  // q_lat [H
     // lane 0 streams pages through the 3-stage ring; lane 1 refills the single Q buffer as soon as
     // the previous item's last S^T has consumed it (the two lanes wait independently).
     if (lane == 0) {
-      // pages are read once per head group: stream them past L2 unless several groups share them
-      const uint64_t pol = n_hg == 1 ? policy_evict_first() : policy_evict_last();
+      // Cluster of cl CTAs = the cl head groups of one sequence (cl == n_hg): the leader streams each
+      // page ONCE and multicasts it into every CTA's stage (the latent is read once per sequence, not
+      // once per head group); each CTA arms its own full barrier and tells the leader its stage is
+      // free.  Pages are read once: stream them past L2 (unless unclustered head groups share them).
+      const bool mc = cl > 1;
+      const bool leader = !mc || cluster_ctarank() == 0;
+      const uint16_t mask = (uint16_t)((1u << cl) - 1);
+      const uint32_t cempty_leader = mc ? mapa_shared(smem_u32(cempty), 0) : 0u;
+      const uint64_t pol = (n_hg == 1 || mc) ? policy_evict_first() : policy_evict_last();
       // L2 prefetch cursor running pf_dist pages ahead of the smem ring
       int pf_it = blockIdx.x, pf_p = 0;
       auto prefetch_next = [&]() {
@@ -195,7 +206,8 @@ decode_attn_mla_kernel(const __grid_constant__ CUtensorMap tm_qlat,  // q_lat [H
           pf_p = 0;
         }
       };
-      for (int i = 0; i < pf_dist; ++i) prefetch_next();
+      if (leader)
+        for (int i = 0; i < pf_dist; ++i) prefetch_next();
       int g = 0;
       for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
         const int b = it / n_hg;
@@ -205,19 +217,27 @@ decode_attn_mla_kernel(const __grid_constant__ CUtensorMap tm_qlat,  // q_lat [H
           const int s = g % kMlaStages;
           mbar_wait(&empty[s], ((g / kMlaStages) & 1) ^ 1);
           mla_trace(0, g);  // 0: stage free, page load issued
-          prefetch_next();
           const int rows = min(kMlaPage, seq_lens[b] - p * kMlaPage);
           const __nv_bfloat16* src = cache + (size_t)bt[p] * (C::kPageBytes / 2);
+          // a sequence's last, partial page: only its valid token rows of every 64-dim block (rows past
+          // the end keep stale finite data; the softmax warps mask them and zero them before P.V)
+          mbar_arrive_expect_tx(&full[s], rows == kMlaPage ? C::kPageBytes : C::NKB * rows * 128);
+          if (mc) {
+            mbar_arrive_cluster(cempty_leader + s * 8);
+            if (!leader) continue;
+            mbar_wait(&cempty[s], (g / kMlaStages) & 1);
+          }
+          prefetch_next();
           if (rows == kMlaPage) {
-            mbar_arrive_expect_tx(&full[s], C::kPageBytes);
-            bulk_load(pages + s * C::kPageBytes, src, C::kPageBytes, &full[s], pol);
-          } else {  // a sequence's last, partial page: only its valid token rows of every 64-dim block
-            // (rows past the end keep stale finite data; the softmax warps mask them and zero them
-            // before P.V)
-            mbar_arrive_expect_tx(&full[s], C::NKB * rows * 128);
-            for (int kb = 0; kb < C::NKB; ++kb)
-              bulk_load(pages + s * C::kPageBytes + kb * C::kBlockBytes, src + kb * (C::kBlockBytes / 2), rows * 128,
-                        &full[s], pol);
+            if (mc) bulk_load_multicast(pages + s * C::kPageBytes, src, C::kPageBytes, &full[s], mask, pol);
+            else bulk_load(pages + s * C::kPageBytes, src, C::kPageBytes, &full[s], pol);
+          } else {
+            for (int kb = 0; kb < C::NKB; ++kb) {
+              uint8_t* dst = pages + s * C::kPageBytes + kb * C::kBlockBytes;
+              const __nv_bfloat16* gsrc = src + kb * (C::kBlockBytes / 2);
+              if (mc) bulk_load_multicast(dst, gsrc, rows * 128, &full[s], mask, pol);
+              else bulk_load(dst, gsrc, rows * 128, &full[s], pol);
+            }
           }
         }
       }
@@ -256,6 +276,10 @@ decode_attn_mla_kernel(const __grid_constant__ CUtensorMap tm_qlat,  // q_lat [H
     const uint64_t dP = make_sdesc_noswz(p_a, 128, C::kChunkBytes);
     int gs = 0, gpv = 0;            // next page for S^T / for P.V (global page counters)
     int it = blockIdx.x, p = 0, np = -1, qi = 0;  // S^T cursor: item, page in item
+    int items_s = 0;                // items whose S^T stream has started (O buffer = item parity)
+    // per page in flight between S^T and P.V: bit 0 = first page of its item, bit 1 = O buffer, bits
+    // 2+ = the item's O-buffer use count (for the oempty phase)
+    int ring[8];
     bool s_done = false;
     while (true) {
       if (!s_done && np < 0) {  // advance the S^T cursor to the next item with pages
@@ -267,24 +291,35 @@ decode_attn_mla_kernel(const __grid_constant__ CUtensorMap tm_qlat,  // q_lat [H
         if (it >= n_items) s_done = true;
         p = 0;
       }
-      const int sb = gs & 1, pb = gpv & 1;                       // TMEM / P buffers
+      const int sb = gs & 1, pb = gpv & 1;                       // TMEM S / P buffers
       const int sst = gs % kMlaStages, pst = gpv % kMlaStages;  // smem stages
-      const bool can_s = !s_done && __all_sync(0xffffffffu, mbar_test(&full[sst], (gs / kMlaStages) & 1) &&
-                                                                mbar_test(&sempty[sb], ((gs >> 1) & 1) ^ 1) &&
-                                                                mbar_test(qfull, qi & 1));
-      const bool can_pv = gpv < gs && __all_sync(0xffffffffu, mbar_test(&pfull[pb], (gpv >> 1) & 1) &&
-                                                                   mbar_test(&oempty[pb], ((gpv >> 1) & 1) ^ 1));
-      if (can_pv) {  // O^T[pb] = C_gpv[:, :R]^T . P_gpv^T, then release the page's stage
+      const bool can_s = !s_done && gs - gpv < 8 &&
+                         __all_sync(0xffffffffu, mbar_test(&full[sst], (gs / kMlaStages) & 1) &&
+                                                     mbar_test(&sempty[sb], ((gs >> 1) & 1) ^ 1) &&
+                                                     mbar_test(qfull, qi & 1));
+      bool can_pv = false;
+      int rg = 0;
+      if (gpv < gs) {
+        rg = ring[gpv & 7];
+        const int ob = (rg >> 1) & 1, use = rg >> 2;
+        // the first P.V of an item overwrites its O buffer: the softmax warps must have read the
+        // item that used it before (two items ago)
+        can_pv = __all_sync(0xffffffffu, mbar_test(&pfull[pb], (gpv >> 1) & 1) &&
+                                             (!(rg & 1) || mbar_test(&oempty[ob], (use & 1) ^ 1)));
+      }
+      if (can_pv) {  // O^T[ob] (+)= C_gpv[:, :R]^T . P_gpv^T (accumulated over the item's pages in TMEM)
         if (lane == 0) mla_trace(2, gpv);  // 2: P.V issued
         tc_fence_after();
+        const int ob = (rg >> 1) & 1;
+        const uint32_t first = rg & 1;
         const uint64_t a0 = dC_o + ((uint32_t)(pst * C::kPageBytes) >> 4), b0 = dP + ((uint32_t)(pb * C::kPBytes) >> 4);
-        const uint32_t d0 = tm + C::kOCol + pb * C::MT * 16;
+        const uint32_t d0 = tm + C::kOCol + ob * C::MT * 16;
 #pragma unroll
         for (int k = 0; k < kMlaTile / 16; ++k)
 #pragma unroll
           for (int mt = 0; mt < C::MT; ++mt)
             umma_bf16_warp(d0 + mt * 16, a0 + ((mt * 2 * C::kBlockBytes + k * 2048) >> 4), b0 + ((k * 256) >> 4),
-                           idesc_o, k > 0);
+                           idesc_o, (k > 0 || !first) ? 1u : 0u);
         umma_commit_warp(&ofull[pb]);
         umma_commit_warp(&empty[pst]);
         ++gpv;
@@ -299,10 +334,12 @@ decode_attn_mla_kernel(const __grid_constant__ CUtensorMap tm_qlat,  // q_lat [H
           umma_bf16_warp(d + (k % C::kSAcc) * 16, a0 + (((k >> 2) * C::kBlockBytes + (k & 3) * 32) >> 4),
                          b0 + (((k >> 2) * C::kQBlockBytes + (k & 3) * 32) >> 4), idesc_s, k >= C::kSAcc);
         umma_commit_warp(&sfull[sb]);
+        ring[gs & 7] = (p == 0 ? 1 : 0) | ((items_s & 1) << 1) | ((items_s >> 1) << 2);
         ++gs;
         if (++p == np) {  // last page of the item: its Q buffer may be refilled
           umma_commit_warp(qempty);
           ++qi;
+          ++items_s;
           it += gridDim.x;
           np = -1;
         }
@@ -322,6 +359,16 @@ decode_attn_mla_kernel(const __grid_constant__ CUtensorMap tm_qlat,  // q_lat [H
     const uint32_t col0 = grp * HG;     // first TMEM column of the group's heads in S / O tiles
     float* gred = red;  // [2][4][16] row maxima; this group owns heads [col0, col0 + HG)
     int g = 0;
+    int items_sm = 0;  // items with pages processed (O buffer = parity)
+    int pvw = 0;       // P.V completions (ofull phases) consumed, in page order
+    // ofull[g & 1] completes once per page; waiting for every phase in order keeps the parity waits
+    // unambiguous (the MMA can never be two phases ahead of pvw: P.V(g) needs P(g) first)
+    auto wait_pv_upto = [&](int G) {
+      while (pvw <= G) {
+        mbar_wait(&ofull[pvw & 1], (pvw >> 1) & 1);
+        ++pvw;
+      }
+    };
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
       const int b = it / n_hg, hg = it - b * n_hg;
       const int len = seq_lens[b];
@@ -334,33 +381,18 @@ decode_attn_mla_kernel(const __grid_constant__ CUtensorMap tm_qlat,  // q_lat [H
         }
         continue;
       }
-      float m_run[HG], lpart[HG], alpha_prev[HG], O[C::MT][HG];
+      // Online softmax with the O accumulator resident in TMEM (the P.V MMAs accumulate over the
+      // item's pages): the running max a head's P is computed against is only raised when a page's
+      // max exceeds it by more than 2^8 (P <= 256 is exact enough in bf16 and fp32), so the O
+      // rescale (TMEM load, scale, store) happens on a handful of pages per item, not every page.
+      const int ob = items_sm & 1;
+      float m_used[HG], lpart[HG];
 #pragma unroll
       for (int h = 0; h < HG; ++h) {
-        m_run[h] = -INFINITY;
+        m_used[h] = -INFINITY;
         lpart[h] = 0.f;
-        alpha_prev[h] = 0.f;
-#pragma unroll
-        for (int mt = 0; mt < C::MT; ++mt) O[mt][h] = 0.f;
       }
-      auto accumulate_o = [&](int t) {  // O = O * alpha(t) + O^T tile t (lane = latent dim)
-        const int s = t & 1;
-        mbar_wait(&ofull[s], (t >> 1) & 1);
-        if (threadIdx.x == 0) mla_trace(5, t);  // 5: P.V of page t done (O pulled)
-        tc_fence_after();
-        uint32_t v[C::MT][HG];
-#pragma unroll
-        for (int mt = 0; mt < C::MT; ++mt) tmem_ld8(trow + C::kOCol + (s * C::MT + mt) * 16 + col0, v[mt]);
-        tmem_ld_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&oempty[s]);
-#pragma unroll
-        for (int mt = 0; mt < C::MT; ++mt)
-#pragma unroll
-          for (int h = 0; h < HG; ++h) O[mt][h] = fmaf(O[mt][h], alpha_prev[h], __uint_as_float(v[mt][h]));
-      };
-
+      const uint32_t ocol = C::kOCol + ob * C::MT * 16 + col0;
       for (int p = 0; p < np; ++p, ++g) {
         const int s = g & 1, st = g % kMlaStages;
         const int n = min(kMlaPage, len - p * kMlaPage);
@@ -389,15 +421,43 @@ decode_attn_mla_kernel(const __grid_constant__ CUtensorMap tm_qlat,  // q_lat [H
         const float wmax = xreduce8<true>(r, lane);  // lane l (< 16, even) holds head (l >> 1) & 7
         if (lane < 16 && !(lane & 1)) gred[(s * 4 + q) * 16 + col0 + (lane >> 1)] = wmax;
         grp_bar(grp);
-        float alpha[HG], pv[HG];
+        float alpha[HG];
+        bool rescale = false;  // group-uniform (every thread derives it from the same gred values)
 #pragma unroll
         for (int h = 0; h < HG; ++h) {
           const float* rr = gred + s * 64 + col0 + h;
-          const float m_new = fmaxf(fmaxf(m_run[h], fmaxf(rr[0], rr[16])), fmaxf(rr[32], rr[48]));
-          alpha[h] = exp2f(m_run[h] - m_new);
-          m_run[h] = m_new;
-          pv[h] = exp2f(x[h] - m_new);
-          lpart[h] = fmaf(lpart[h], alpha[h], pv[h]);
+          const float pm = fmaxf(fmaxf(rr[0], rr[16]), fmaxf(rr[32], rr[48]));
+          alpha[h] = 1.f;
+          if (pm > m_used[h] + 8.f) {
+            alpha[h] = exp2f(m_used[h] - pm);  // 0 on the first page (m_used = -inf)
+            m_used[h] = pm;
+            rescale = true;
+          }
+        }
+        if (rescale) {
+#pragma unroll
+          for (int h = 0; h < HG; ++h) lpart[h] *= alpha[h];
+          if (p > 0) {  // O holds pages 0..p-1: wait for the last of them, then scale it in TMEM
+            wait_pv_upto(g - 1);
+            tc_fence_after();
+            uint32_t v[C::MT][HG];
+#pragma unroll
+            for (int mt = 0; mt < C::MT; ++mt) tmem_ld8(trow + ocol + mt * 16, v[mt]);
+            tmem_ld_wait();
+#pragma unroll
+            for (int mt = 0; mt < C::MT; ++mt) {
+#pragma unroll
+              for (int h = 0; h < HG; ++h) v[mt][h] = __float_as_uint(__uint_as_float(v[mt][h]) * alpha[h]);
+              tmem_st8(trow + ocol + mt * 16, v[mt]);
+            }
+            tmem_st_wait();
+          }
+        }
+        float pv[HG];
+#pragma unroll
+        for (int h = 0; h < HG; ++h) {
+          pv[h] = exp2f(x[h] - m_used[h]);
+          lpart[h] += pv[h];
         }
         if (lane < 16) {  // P^T layout [2 head groups][64 tok][8 heads]
           uint8_t* pd = p_s + s * C::kPBytes + (grp * kMlaTile + tok) * 16;
@@ -413,16 +473,25 @@ decode_attn_mla_kernel(const __grid_constant__ CUtensorMap tm_qlat,  // q_lat [H
           }
         }
         fence_proxy_async_smem();
+        tc_fence_before();  // the O rescale's TMEM stores precede the next P.V (ordered by pfull)
         __syncwarp();
         if (lane == 0) mbar_arrive(&pfull[s]);
         if (threadIdx.x == 0) mla_trace(4, g);    // 4: P written (warp 0, heads 0-7)
         if (threadIdx.x == 128) mla_trace(6, g);  // 6: P written (warp 4, heads 8-15)
-        if (p > 0) accumulate_o(g - 1);
-#pragma unroll
-        for (int h = 0; h < HG; ++h) alpha_prev[h] = alpha[h];
+        wait_pv_upto(g - 1);  // keep pace with the P.V stream (see wait_pv_upto)
       }
-      accumulate_o(g - 1);
-      if (threadIdx.x == 0) mla_trace(9, g - 1);  // 9: item's last O pulled
+      // ---- the item's O: wait for its last P.V, normalise, store; free the O buffer ----
+      wait_pv_upto(g - 1);
+      tc_fence_after();
+      uint32_t ov[C::MT][HG];
+#pragma unroll
+      for (int mt = 0; mt < C::MT; ++mt) tmem_ld8(trow + ocol + mt * 16, ov[mt]);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&oempty[ob]);
+      ++items_sm;
+      if (threadIdx.x == 0) mla_trace(9, g - 1);  // 9: item's O pulled
 
       // ---- normalise and store: lane = latent dim, the group's 8 heads per thread ----
       const float lsum = xreduce8<false>(lpart, lane);
@@ -441,7 +510,7 @@ decode_attn_mla_kernel(const __grid_constant__ CUtensorMap tm_qlat,  // q_lat [H
         if (hh < H) {
           __nv_bfloat16* dst = o_lat + ((size_t)hh * B + b) * R + q * 32 + lane;
 #pragma unroll
-          for (int mt = 0; mt < C::MT; ++mt) dst[mt * 128] = __float2bfloat16_rn(O[mt][h] * inv[h]);
+          for (int mt = 0; mt < C::MT; ++mt) dst[mt * 128] = __float2bfloat16_rn(__uint_as_float(ov[mt][h]) * inv[h]);
         }
       }
       if (threadIdx.x == 0) mla_trace(10, g - 1);  // 10: O stores issued
@@ -450,6 +519,7 @@ decode_attn_mla_kernel(const __grid_constant__ CUtensorMap tm_qlat,  // q_lat [H
   }
   tc_fence_before();
   __syncthreads();
+  if (cl > 1) cluster_sync();  // no CTA leaves while a peer may still multicast into it / arrive on it
   if (warp == 9) {
     tc_fence_after();
     tmem_dealloc<C::kTmemCols>(tmem);
@@ -461,9 +531,39 @@ int launch_mla(const void* q_lat, const void* q_pe, const void* cache, const int
                int B, int H, float scale, void* out, cudaStream_t st) {
   using C = MlaCfg<R, RP>;
   if (const int rc = mgb_host::ensure_max_smem((const void*)decode_attn_mla_kernel<R, RP>, (int)C::kSmem)) return rc;
-  const int items = B * ((H + kMlaHeads - 1) / kMlaHeads);
+  const int n_hg = (H + kMlaHeads - 1) / kMlaHeads;
+  const int items = B * n_hg;
+  // the head groups of a sequence share its latent pages.  Default: independent CTAs on neighbouring
+  // SMs, the pages shared through L2 (consecutive items are the head groups of one sequence, so each
+  // page is read from HBM about once).  MGB_MLA_CLUSTER=1: one cluster per sequence whose leader
+  // multicasts each page into all of its CTAs (L2 -> SM traffic once per sequence as well) --
+  // measured slower at 128 heads (1.43 vs 1.04 ms, B=1024, ctx 640): the kernel is bound by the
+  // per-page chain of each head group, and the cluster makes its CTAs wait for the slowest one.
+  static const bool cl_env = [] {
+    const char* e = getenv("MGB_MLA_CLUSTER");
+    return e && e[0] == '1';
+  }();
+  const int cl = (cl_env && (n_hg == 2 || n_hg == 4 || n_hg == 8)) ? n_hg : 1;
   int grid = mgb_host::num_sms();
-  if (grid > items) grid = items;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  if (cl > 1) {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.blockDim = dim3(kMlaThreads);
+    cfg.dynamicSmemBytes = C::kSmem;
+    cfg.gridDim = dim3(grid / cl * cl);
+    int nclusters = 0;  // co-resident clusters: the persistent grid must fit in one wave
+    if (cudaOccupancyMaxActiveClusters(&nclusters, decode_attn_mla_kernel<R, RP>, &cfg) != cudaSuccess ||
+        nclusters < 1)
+      return mgb_host::launch_status(), MGB_ECUDA;
+    grid = std::min(nclusters * cl, grid / cl * cl);
+  }
+  if (grid > items) grid = (items + cl - 1) / cl * cl;
   static const int pf_dist = [] {
     const char* e = getenv("MGB_MLA_PREFETCH");
     return e ? atoi(e) : 4;
@@ -484,9 +584,20 @@ int launch_mla(const void* q_lat, const void* q_pe, const void* cache, const int
     const uint32_t box[3] = {64, kMlaHeads, 1};
     if (mgb_host::encode_tmap_bf16(&tp, q_pe, 3, d, s, box, true) != CUDA_SUCCESS) return MGB_ECUDA;
   }
+  if (cl > 1) {
+    cfg.gridDim = dim3(grid);
+    cfg.stream = st;
+    const __nv_bfloat16* cp = reinterpret_cast<const __nv_bfloat16*>(cache);
+    __nv_bfloat16* op = reinterpret_cast<__nv_bfloat16*>(out);
+    const float sl2 = scale * 1.4426950408889634f;
+    if (cudaLaunchKernelEx(&cfg, decode_attn_mla_kernel<R, RP>, tq, tp, cp, bt, max_pages, lens, B, H, sl2, op,
+                           pf_dist, cl) != cudaSuccess)
+      return mgb_host::launch_status(), MGB_ECUDA;
+    return mgb_host::launch_status();
+  }
   decode_attn_mla_kernel<R, RP><<<grid, kMlaThreads, C::kSmem, st>>>(
       tq, tp, reinterpret_cast<const __nv_bfloat16*>(cache), bt, max_pages, lens, B, H, scale * 1.4426950408889634f,
-      reinterpret_cast<__nv_bfloat16*>(out), pf_dist);
+      reinterpret_cast<__nv_bfloat16*>(out), pf_dist, 1);
   return mgb_host::launch_status();
 }
 

@@ -36,7 +36,9 @@ def _latent_pages(c, pe, B, ctx, page, pps, tail=0.0):
 @pytest.mark.parametrize("B,H,RL,r,ctx,tail", [(3, 16, 512, 64, 1, 0.0), (4, 16, 512, 64, 100, 0.0),
                                               (2, 128, 512, 64, 70, 0.0), (5, 4, 128, 32, 33, 0.0),
                                               (2, 20, 512, 64, 64, 0.0), (3, 16, 512, 64, 45, float("nan")),
-                                              (4, 8, 128, 32, 61, float("nan")), (2, 16, 512, 64, 112, float("inf"))])
+                                              (4, 8, 128, 32, 61, float("nan")), (2, 16, 512, 64, 112, float("inf")),
+                                              (37, 128, 512, 64, 300, float("nan")), (9, 64, 512, 64, 130, 0.0),
+                                              (3, 32, 128, 32, 57, float("inf"))])
 def test_decode_attn_mla(B, H, RL, r, ctx, tail):
     from paper_2503_09716_b200 import _native as nat
 

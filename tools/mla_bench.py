@@ -1,6 +1,11 @@
 """Absorbed-MLA decode kernel alone at the DeepSeek-V2-Lite bench shape (CUDA events).
 
 python tools/mla_bench.py [B] [ctx] [H]   -> us per launch, latent-cache GB/s, fraction of HBM peak
+
+The byte count is the latent cache read ONCE per sequence (the algorithmic bytes: every head group
+of a sequence attends over the same latent rows), whatever the kernel's head-group split re-reads.
+MGB_MLA_CLUSTER=1 runs the head groups of a sequence as one multicast cluster instead of independent
+CTAs sharing the pages through L2.
 """
 import json
 import math
@@ -43,7 +48,8 @@ for _ in range(reps):
 e1.record()
 torch.cuda.synchronize()
 us = e0.elapsed_time(e1) / reps * 1e3
-byts = B * CTX * (RL + RP) * 2 * math.ceil(H / 16)
+byts = B * CTX * (RL + RP) * 2
 peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))
 hbm = next(v for k, v in peak.items() if "hbm" in k.lower() and isinstance(v, (int, float)))
-print(f"B={B} ctx={CTX} H={H} page={page}: {us:.1f} us  {byts / us / 1e3:.0f} GB/s  ({byts / us / 1e3 / hbm:.2f} of {hbm} GB/s)")
+print(f"B={B} ctx={CTX} H={H} page={page} cluster={os.environ.get('MGB_MLA_CLUSTER', '0')}: {us:.1f} us  "
+      f"{byts / us / 1e3:.0f} GB/s  ({byts / us / 1e3 / hbm:.2f} of {hbm} GB/s)")
