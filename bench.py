@@ -215,16 +215,20 @@ _BASELINE_CFG = {"mixtral-8x7b": "BASELINE configs[1]", "deepseek-v2-lite": "BAS
                  "deepseek-v2-236b": "BASELINE configs[4] model"}
 
 
-def _workload_config(args, arch, world: int) -> dict:
+def _workload_config(args, arch, world: int, ep: bool = False) -> dict:
     """The workload both arms are quoted on (the GPU arm's batch: the planner's largest resident B)."""
     from paper_2503_09716_b200.engine import resident_plan
 
     plan = resident_plan(arch, args.prompt_len, args.decode_len, B=args.batch, reserve_bytes=args.reserve_gb << 30)
-    return {"workload": f"{arch.name} decode phase, prompt {args.prompt_len} / gen {args.decode_len}, 1 B200 resident "
+    where = (f"{world} B200 expert-parallel" if ep else "1 B200 resident")
+    par = (f"ep{world}: experts {arch.n_experts // world} per rank, each rank's B sequences data-parallel, token "
+           f"dispatch/combine fused into the permutation / down-GEMM kernels over NVLink peer memory (torch symmetric "
+           f"memory), per-expert counts all-gathered over NCCL" if ep else f"replicas x{world}")
+    return {"workload": f"{arch.name} decode phase, prompt {args.prompt_len} / gen {args.decode_len}, {where} "
                         f"({_BASELINE_CFG.get(arch.name, 'not a BASELINE config')});"
-                        f" step = {args.decode_len} decode forwards of B={plan.B} sequences",
+                        f" step = {args.decode_len} decode forwards of B={plan.B} sequences per GPU",
             "batch": plan.B, "b_a": plan.b_a, "b_e": plan.b_e, "kv_policy": "resident (paged, HBM)",
-            "parallelism": f"replicas x{world}", "l2": "inputs larger than L2 (all weights stream from HBM every forward)"}
+            "parallelism": par, "l2": "inputs larger than L2 (all weights stream from HBM every forward)"}
 
 
 def run_reference(args, dist, rank, world) -> None:
@@ -309,7 +313,9 @@ def run_ours(args, dist, rank, world) -> None:
     from paper_2503_09716_b200.configs import get_arch
 
     torch.cuda.set_device(rank % torch.cuda.device_count())
-    line = measure(args, get_arch(args.config), dist, rank, world, args.steps, args.warmup, main=True)
+    arch0 = get_arch(args.config)
+    ep0 = (world > 1 or args.ep == "force") and args.ep != "off" and arch0.family == "deepseek_v2"
+    line = measure(args, arch0, dist, rank, world, args.steps, args.warmup, main=True, ep=ep0)
     # the other 1-GPU BASELINE configuration (configs[2], DeepSeek-V2-Lite) measured in the same run, so
     # the driver's bench records it too; same contract (device-timed decode steps, e2e through the
     # public API, roofline of the dominant GEMM), fewer steps
@@ -317,8 +323,15 @@ def run_ours(args, dist, rank, world) -> None:
     for name in [c for c in args.also.split(",") if c and c != args.config]:
         gc.collect()
         torch.cuda.empty_cache()
-        sub = measure(args, get_arch(name), dist, rank, world, args.also_steps, max(3, min(args.warmup, 3)), main=False)
-        extra[name] = {k: sub[k] for k in ("value", "unit", "ms_per_step", "steps", "warmup", "forward_ms", "config",
+        # DeepSeek-V2-Lite is BASELINE configs[2]: expert-parallel across the job's GPUs (1 GPU: plain)
+        ep = (world > 1 or args.ep == "force") and args.ep != "off" and get_arch(name).family == "deepseek_v2"
+        try:
+            sub = measure(args, get_arch(name), dist, rank, world, args.also_steps, max(3, min(args.warmup, 3)),
+                          main=False, ep=ep)
+        except Exception as e:  # noqa: BLE001 -- report it in the line instead of losing the main result
+            extra[name] = {"error": f"{type(e).__name__}: {str(e).splitlines()[0] if str(e) else ''}"[:300]}
+            continue
+        extra[name] = {k: sub[k] for k in ("value", "unit", "ms_per_step", "steps", "warmup", "forward_ms", "config", "graph",
                                            "e2e", "roofline", "expert_gemm", "incl_prefill", "kernel_hbm",
                                            "kernel_ms_per_forward", "clocks", "gpu_launches", "dtype")}
     if extra:
@@ -327,13 +340,22 @@ def run_ours(args, dist, rank, world) -> None:
         print(json.dumps(line), flush=True)
 
 
-def measure(args, arch, dist, rank, world, steps: int, warmup: int, main: bool) -> dict:
+def measure(args, arch, dist, rank, world, steps: int, warmup: int, main: bool, ep: bool = False) -> dict:
     """Time one configuration (the bench contract: `warmup` untimed steps, then exactly `steps`
-    device-timed decode phases, max over ranks); returns its JSON line."""
+    device-timed decode phases, max over ranks); returns its JSON line.  ep: experts sharded over the
+    job's ranks (PeerExpertParallel over symmetric memory), each rank decoding its own B sequences."""
     from paper_2503_09716_b200.engine import Engine, resident_plan
 
     plan = resident_plan(arch, args.prompt_len, args.decode_len, B=args.batch, reserve_bytes=args.reserve_gb << 30)
-    eng = Engine(arch, plan, prompt_len=args.prompt_len, decode_len=args.decode_len, seed=0, use_graph=True)
+    pep = None
+    if ep:
+        from paper_2503_09716_b200.ep import PeerExpertParallel
+
+        rows = plan.B * arch.top_k  # this rank's routed rows; a receive buffer holds every source's worst case
+        pep = PeerExpertParallel.from_symmetric_memory(arch.n_experts, dist.group.WORLD, world * rows, rows,
+                                                       arch.hidden)
+    eng = Engine(arch, plan, prompt_len=args.prompt_len, decode_len=args.decode_len, seed=0,
+                 use_graph=True, ep=pep)
     B = eng.B
     N = args.decode_len
     eng.synthetic_prefill(seed=1)
@@ -381,7 +403,7 @@ def measure(args, arch, dist, rank, world, steps: int, warmup: int, main: bool) 
     # ---- the same decode step behind a real batched prefill of the B prompts (SURVEY.md §8d asks for
     # the incl.-prefill figure too): B x prompt_len tokens through Engine.prefill, device-timed ----
     incl = None
-    if args.incl_prefill:
+    if args.incl_prefill and eng.can_prefill():
         try:
             ids = torch.randint(0, arch.vocab, (B, args.prompt_len), generator=torch.Generator().manual_seed(11))
             torch.cuda.synchronize()
@@ -406,10 +428,11 @@ def measure(args, arch, dist, rank, world, steps: int, warmup: int, main: bool) 
     hbm, tf_burst, tf_sust, src = _peaks()
     a = arch
     rows = B * a.top_k
-    k_active = a.n_experts  # every expert is hit at these batch sizes
+    e_launch = arch.n_experts // world if ep else arch.n_experts  # experts per routed grouped launch
+    k_active = e_launch  # every (local) expert is hit at these batch sizes
     nan = {"avg_ms": float("nan"), "ms_per_step": float("nan")}
-    gu = bd.get(f"moe_gemm_gate_up[E={arch.n_experts}]", nan)  # the routed-expert launches
-    dn = bd.get(f"moe_gemm_down[E={arch.n_experts}]", nan)
+    gu = bd.get(f"moe_gemm_gate_up[E={e_launch}]", nan)  # the routed-expert launches
+    dn = bd.get(f"moe_gemm_down[E={e_launch}]", bd.get(f"moe_gemm_down_ep[E={e_launch}]", nan))
     gu_bytes = k_active * 2 * a.moe_ffn * a.hidden * 2 + rows * a.hidden * 2 + rows * a.moe_ffn * 2
     dn_bytes = k_active * a.hidden * a.moe_ffn * 2 + rows * a.moe_ffn * 2 + rows * a.hidden * 2
     gu_flops = 2.0 * rows * a.hidden * 2 * a.moe_ffn
@@ -454,7 +477,8 @@ def measure(args, arch, dist, rank, world, steps: int, warmup: int, main: bool) 
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps, "warmup": warmup,
         "ms_per_step": 1e3 * t / steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (random-init counter-based weights, synthetic prefill KV)",
-        "config": _workload_config(args, arch, world),
+        "config": _workload_config(args, arch, world, ep=ep),
+        "graph": bool(eng.graph is not None),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(first_pinned.numel() * 4),
                 "d2h_bytes_per_step": int(out.numel() * out.element_size())},
         "roofline": roofline,
@@ -493,6 +517,9 @@ def main():
     ap.add_argument("--also", default="deepseek-v2-lite",
                     help="comma-separated extra configs measured after the main one (\"\" = none)")
     ap.add_argument("--also-steps", type=int, default=3)
+    ap.add_argument("--ep", default="auto", choices=["auto", "off", "force"],
+                    help="auto: DeepSeek-V2-Lite runs expert-parallel over the job's GPUs when N > 1; force: also "
+                         "at N = 1 (a one-rank NCCL group, the EP code path on one GPU)")
     ap.add_argument("--no-incl-prefill", dest="incl_prefill", action="store_false",
                     help="skip the batched-prefill pass behind the incl_prefill figure")
     args = ap.parse_args()
@@ -507,6 +534,14 @@ def main():
     if ws != args.gpus:
         raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}; launch one rank per GPU")
     dist, rank, world, local = _dist()
+    if dist is None and args.ep == "force" and args.impl == "ours":  # one-rank group for the EP path
+        import torch.distributed as tdist
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", os.environ.get("MGB_EP_PORT", "29533"))
+        torch.cuda.set_device(0)
+        tdist.init_process_group("nccl", rank=0, world_size=1)
+        dist = tdist
     if args.impl == "reference":
         run_reference(args, dist, rank, world)
     else:
