@@ -1222,23 +1222,67 @@ class Engine:
         self.reset(0)
         st, cp = self.stream, self.h2d
         st.wait_stream(torch.cuda.current_stream())
-        slot_free = [torch.cuda.Event(), torch.cuda.Event()]
-        landed = [torch.cuda.Event(), torch.cuda.Event()]
+        cp.wait_stream(torch.cuda.current_stream())
+        # every uncached expert of every layer, in compute order, streamed through the expert slots: the
+        # copy of the i-th one is issued as soon as the compute that last read its slot (i - nsl) has
+        # been issued, so the link runs up to nsl experts ahead of the GEMMs -- across layer
+        # boundaries, through the next layer's attention and the per-layer routing sync
+        nsl = max(2, int(w.slots.shape[0]))
+        stream_order = [(l, e) for l in range(a.layers) if self._has_router(l)
+                        for e in range(w.place.experts_per_layer[l], E)]
+        slot_free = [torch.cuda.Event() for _ in range(nsl)]
+        landed = [torch.cuda.Event() for _ in range(nsl)]
+        dense_landed, dense_free = torch.cuda.Event(), torch.cuda.Event()
         for ev in slot_free:
             ev.record(st)
+        issued = [0]
+
+        def issue_copies(upto: int) -> None:
+            while issued[0] < min(upto, len(stream_order)):
+                i = issued[0]
+                l2, e2 = stream_order[i]
+                sl = i % nsl
+                cp.wait_event(slot_free[sl])  # recorded by the compute of stream_order[i - nsl]
+                with torch.cuda.stream(cp):
+                    if copy:
+                        w.slots[sl].copy_(w.host_experts[l2][e2 - w.place.experts_per_layer[l2]], non_blocking=True)
+                    landed[sl].record(cp)
+                issued[0] += 1
+        # copies_enabled / compute_enabled = False: the same prefill with its host->device copies or its
+        # kernels skipped (the copies-only / compute-only times of the overlap measurement)
+        run, copy = self.compute_enabled, self.copies_enabled
+
+        def dense_copy(l: int) -> None:
+            """Layer l's dense blob (attention + router + shared experts) into the dense buffer on the
+            H2D stream, after the previous layer's last reader of the buffer (its router)."""
+            if l >= a.layers or l < w.place.dense_layers:
+                return
+            cp.wait_event(dense_free)
+            with torch.cuda.stream(cp):
+                if copy:
+                    w.dense_bufs[0].copy_(w.host_dense[l], non_blocking=True)
+                dense_landed.record(cp)
+
+        dense_free.record(st)
+        dense_copy(0)
+        issue_copies(nsl)
+        computed = 0  # uncached experts whose GEMMs are issued
         with torch.cuda.stream(st):
-            ops.embed(ids.reshape(-1), w.embed, x_all)
+            if run:
+                ops.embed(ids.reshape(-1), w.embed, x_all)
             for l in range(a.layers):
                 L = w.layers[l]
                 W = dict(L)
                 if l >= w.place.dense_layers:  # the layer's attention (+ shared experts) blob
-                    w.dense_bufs[0].copy_(w.host_dense[l], non_blocking=True)
+                    st.wait_event(dense_landed)
                     W.update(w.dense_views(0))
-                if l == 0:
+                if l == 0 and run:
                     ops.add_rmsnorm(x_all, W["ln1"], a.rms_eps, h_all)
                 nxt = w.layers[l + 1]["ln1"] if l + 1 < a.layers else w.final_norm
                 dense_mlp = self.mla and l < a.first_k_dense
                 for s0 in range(0, B, Bp):
+                    if not run:
+                        break
                     n = min(Bp, B - s0)
                     t0, t1 = s0 * P, (s0 + n) * P
                     x, h, o = x_all[t0:t1], h_all[t0:t1], S["o"][:t1 - t0]
@@ -1254,11 +1298,15 @@ class Engine:
                     elif self.mla:
                         self._dense_mlp(W["sh_gate_up"], W["sh_down"], h, S["sh_h"][:t], sh_all[t0:t1], seg)
                 if dense_mlp:
+                    dense_free.record(st)
+                    dense_copy(l + 1)
                     continue
-                torch.mm(h_all, W["router"].t(), out_dtype=torch.float32, out=lg)
-                ops.router_topk(None, None, ws, k, a.router_mode, a.routed_scaling, a.n_group, a.topk_group,
-                                logits_in=lg)
-                ops.permute(h_all, ws, xp)
+                if run:
+                    torch.mm(h_all, W["router"].t(), out_dtype=torch.float32, out=lg)
+                    ops.router_topk(None, None, ws, k, a.router_mode, a.routed_scaling, a.n_group, a.topk_group,
+                                    logits_in=lg)
+                    ops.permute(h_all, ws, xp)
+                dense_free.record(st)  # the layer's last reader of the dense buffer was the router
                 # host sync once per layer: per-expert row counts (the capacity pre-flight; x_perm holds
                 # all T*k rows by construction, the b_e scratch is handled by the re-split below)
                 cnt = ops.check_capacity(ws.offsets, T * k)
@@ -1266,32 +1314,32 @@ class Engine:
                 for c in cnt:
                     offs.append(offs[-1] + c)
                 n_c = w.place.experts_per_layer[l]
-                u = 0  # uncached experts streamed so far in this layer
+                dense_copy(l + 1)  # the dense buffer is free again (the router was its last reader)
                 for e in range(E):
                     r0, r1 = offs[e], offs[e + 1]
                     if e < n_c:
                         gu, dn = L["w_gate_up"][e:e + 1], L["w_down"][e:e + 1]
-                    else:  # stream expert e into slot u % 2 while the GPU works on the previous one
-                        sl = u % 2
-                        cp.wait_event(slot_free[sl])
-                        with torch.cuda.stream(cp):
-                            w.slots[sl].copy_(w.host_experts[l][e - n_c], non_blocking=True)
-                            landed[sl].record(cp)
+                    else:  # streamed: wait for its copy (issued up to nsl experts earlier)
+                        assert stream_order[computed] == (l, e)
+                        sl = computed % nsl
                         st.wait_event(landed[sl])
                         gu, dn = w.slot_views(sl)
-                    for c0 in range(r0, r1, be):  # b_e-row pieces of the expert's group
+                    for c0 in range(r0, r1, be) if run else ():  # b_e-row pieces of the expert's group
                         c1 = min(r1, c0 + be)
                         lo = self._segment(c1 - c0)
                         ops.moe_gemm_gate_up(gu, xp[c0:c1], lo, hf[:c1 - c0])
                         ops.moe_gemm_down(dn, hf[:c1 - c0], lo, yp[c0:c1])
                     if e >= n_c:
-                        slot_free[u % 2].record(st)
-                        u += 1
-                ops.unpermute_combine(yp, ws, x_all, T, residual=x_all, shared_out=sh_all, norm_w=nxt,
-                                      eps=a.rms_eps, norm_out=h_all)
-            last = h_all.view(B, P, d)[:, P - 1].contiguous()
-            torch.mm(last, w.lm_head.t(), out=b.logits)
-            ops.argmax(b.logits, b.next_ids)
+                        slot_free[computed % nsl].record(st)
+                        computed += 1
+                        issue_copies(computed + nsl)
+                if run:
+                    ops.unpermute_combine(yp, ws, x_all, T, residual=x_all, shared_out=sh_all, norm_w=nxt,
+                                          eps=a.rms_eps, norm_out=h_all)
+            if run:
+                last = h_all.view(B, P, d)[:, P - 1].contiguous()
+                torch.mm(last, w.lm_head.t(), out=b.logits)
+                ops.argmax(b.logits, b.next_ids)
             b.positions.fill_(P)
             b.seq_lens.fill_(P)
             b.step.fill_(P)

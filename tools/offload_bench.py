@@ -38,6 +38,7 @@ ap.add_argument("--reserve-gb", type=float, default=10.0)
 ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--out", default=None)
 ap.add_argument("--prefill", action="store_true", help="also time Engine.prefill of B x 512 random prompts")
+ap.add_argument("--prefill-batch", type=int, default=None, help="sequences of the prefill pass (default: B)")
 args = ap.parse_args()
 
 
@@ -119,16 +120,37 @@ out = {
     "decode_tokens_per_s": B / t,
     "decode_tokens_per_s_full_depth": B / (t * full.layers / arch.layers),
     "h2d_gbs_achieved": moved / t / 1e9, "h2d_gbs_memcpy_peak": h2d_gbs, "h2d_frac_of_link": moved / t / 1e9 / h2d_gbs,
-    "overlap": overlap, "eager_trace_overlap": rep["overlap"], "setup_s": setup_s,
+    "overlap": overlap, "eager_trace_overlap": rep["overlap"],
+    "eager_trace": {"makespan_ms": rep["makespan"] * 1e3, "busy_ms": {k: v * 1e3 for k, v in rep["busy"].items()}},
+    "setup_s": setup_s,
 }
 if args.prefill:
-    ids = torch.randint(0, arch.vocab, (B, 512), generator=torch.Generator().manual_seed(0))
-    torch.cuda.synchronize()
-    t0 = time.time()
-    eng.prefill(ids)
-    torch.cuda.synchronize()
-    tp = time.time() - t0
-    out.update(prefill_s=tp, prefill_prompt_tokens_per_s=B * 512 / tp)
+    # module-based batching's prefill pass (every streamed weight crosses the link once per layer while
+    # all B x 512 prompt tokens go through it): the same pass timed with its copies skipped
+    # (compute-only) and with its kernels skipped (copies-only) gives the transfer/compute overlap at a
+    # batch where the two are comparable
+    pB = args.prefill_batch or B
+    ids = torch.randint(0, arch.vocab, (pB, 512), generator=torch.Generator().manual_seed(0))
+
+    def pf():
+        torch.cuda.synchronize()
+        t0 = time.time()
+        eng.prefill(ids)
+        torch.cuda.synchronize()
+        return time.time() - t0
+
+    eng.copies_enabled = eng.compute_enabled = True
+    pf()  # warm-up (allocator, first-use costs)
+    tp = pf()
+    eng.copies_enabled = False
+    tp_gpu = pf()
+    eng.copies_enabled, eng.compute_enabled = True, False
+    tp_h2d = pf()
+    eng.compute_enabled = True
+    out.update(prefill_batch=pB, prefill_s=tp, prefill_prompt_tokens_per_s=pB * 512 / tp,
+               prefill_compute_only_s=tp_gpu, prefill_copies_only_s=tp_h2d,
+               prefill_overlap=1.0 - max(0.0, tp - max(tp_gpu, tp_h2d)) / min(tp_gpu, tp_h2d),
+               prefill_h2d_gbs=eng.w.host_bytes() / tp / 1e9)
 print(json.dumps(out))
 if args.out:
     with open(args.out, "w") as f:
