@@ -287,7 +287,8 @@ def kernel_breakdown(eng, reps: int = 2) -> dict:
     orig_call, mm, bmm = nat.call, torch.mm, torch.bmm
     try:
         # grouped GEMM launches are keyed by expert count (routed E vs shared / dense E = 1)
-        nat.call = timed(lambda a: f"{a[0]}[E={a[4]}]" if a[0].startswith("mgb_moe_gemm") else a[0], orig_call)
+        nat.call = timed(lambda a: f"{a[0]}[E={a[5]}]" if a[0] == "mgb_moe_ffn" else
+                         f"{a[0]}[E={a[4]}]" if a[0].startswith("mgb_moe_gemm") else a[0], orig_call)
         torch.mm = timed("cublas_gemm", mm)
         torch.bmm = timed("cublas_bmm", bmm)
         saved = [t.clone() for t in (eng.buf.positions, eng.buf.step, eng.buf.next_ids, eng.buf.seq_lens)]
@@ -431,29 +432,37 @@ def measure(args, arch, dist, rank, world, steps: int, warmup: int, main: bool, 
     e_launch = arch.n_experts // world if ep else arch.n_experts  # experts per routed grouped launch
     k_active = e_launch  # every (local) expert is hit at these batch sizes
     nan = {"avg_ms": float("nan"), "ms_per_step": float("nan")}
-    gu = bd.get(f"moe_gemm_gate_up[E={e_launch}]", nan)  # the routed-expert launches
-    dn = bd.get(f"moe_gemm_down[E={e_launch}]", bd.get(f"moe_gemm_down_ep[E={e_launch}]", nan))
     gu_bytes = k_active * 2 * a.moe_ffn * a.hidden * 2 + rows * a.hidden * 2 + rows * a.moe_ffn * 2
     dn_bytes = k_active * a.hidden * a.moe_ffn * 2 + rows * a.moe_ffn * 2 + rows * a.hidden * 2
     gu_flops = 2.0 * rows * a.hidden * 2 * a.moe_ffn
     dn_flops = 2.0 * rows * a.hidden * a.moe_ffn
-    gu_gbs = gu_bytes / (gu["avg_ms"] * 1e-3) / 1e9
     step_ms_eager = sum(v["ms_per_step"] for v in bd.values())
-    ffn_ms = gu["avg_ms"] + dn["avg_ms"]
-    expert_tflops = (gu_flops + dn_flops) / (ffn_ms * 1e-3) / 1e12
     tok_per_expert = rows / a.n_experts
     ridge = tf_burst * 1e12 / (hbm * 1e9)  # flop/B; expert GEMM intensity = tokens/expert flop/B
+    ffn = bd.get(f"moe_ffn[E={e_launch}]")  # the fused launch (gate/up + SiLU*up + down), routed experts
+    if ffn is not None:
+        kname, kbytes, kflops, kr = ("mgb_moe_ffn (one tcgen05 CTA-pair launch: grouped gate/up + SiLU*up + down)",
+                                     gu_bytes + dn_bytes, gu_flops + dn_flops, ffn)
+        ffn_ms, gu_ms, dn_ms = ffn["avg_ms"], None, None
+        traffic_key = "ffn"
+    else:  # separate launches (EP path, MGB_FFN_FUSED=0)
+        gu = bd.get(f"moe_gemm_gate_up[E={e_launch}]", nan)
+        dn = bd.get(f"moe_gemm_down[E={e_launch}]", bd.get(f"moe_gemm_down_ep[E={e_launch}]", nan))
+        kname, kbytes, kflops, kr = "mgb_moe_gemm_gate_up (tcgen05 grouped GEMM + SiLU*up)", gu_bytes, gu_flops, gu
+        ffn_ms, gu_ms, dn_ms = gu["avg_ms"] + dn["avg_ms"], gu["avg_ms"], dn["avg_ms"]
+        traffic_key = "gate_up"
+    expert_tflops = (gu_flops + dn_flops) / (ffn_ms * 1e-3) / 1e12
+    k_gbs = kbytes / (kr["avg_ms"] * 1e-3) / 1e9
     if tok_per_expert < ridge:
-        roofline = {"kernel": "mgb_moe_gemm_gate_up (tcgen05 grouped GEMM + SiLU*up)", "bound": "hbm",
-                    "achieved": gu_gbs, "peak": hbm, "unit": "GB/s", "frac": gu_gbs / hbm}
+        roofline = {"kernel": kname, "bound": "hbm", "achieved": k_gbs, "peak": hbm, "unit": "GB/s", "frac": k_gbs / hbm}
     else:
-        gu_tf = gu_flops / (gu["avg_ms"] * 1e-3) / 1e12
-        roofline = {"kernel": "mgb_moe_gemm_gate_up (tcgen05 grouped GEMM + SiLU*up)", "bound": "tensor",
-                    "achieved": gu_tf, "peak": tf_burst, "unit": "TFLOP/s", "frac": gu_tf / tf_burst}
-    traffic, traffic_src = _ncu_traffic(args.config, "gate_up")
-    roofline.update({"traffic": traffic, "traffic_source": traffic_src, "algorithmic_bytes_per_launch": gu_bytes, "algorithmic_flops_per_launch": gu_flops,
-                     "avg_launch_ms": gu["avg_ms"], "peak_source": src, "tokens_per_expert": tok_per_expert,
-                     "share_of_step": gu["ms_per_step"] / step_ms_eager})
+        k_tf = kflops / (kr["avg_ms"] * 1e-3) / 1e12
+        roofline = {"kernel": kname, "bound": "tensor", "achieved": k_tf, "peak": tf_burst, "unit": "TFLOP/s",
+                    "frac": k_tf / tf_burst}
+    traffic, traffic_src = _ncu_traffic(args.config, traffic_key)
+    roofline.update({"traffic": traffic, "traffic_source": traffic_src, "algorithmic_bytes_per_launch": kbytes,
+                     "algorithmic_flops_per_launch": kflops, "avg_launch_ms": kr["avg_ms"], "peak_source": src,
+                     "tokens_per_expert": tok_per_expert, "share_of_step": kr["ms_per_step"] / step_ms_eager})
     # achieved HBM bandwidth of the HBM-bound kernels (SURVEY.md §8d per-kernel algorithmic bytes;
     # attention at the breakdown's context, prompt_len + decode_len / 2 + 1)
     T, d, k, E = B, a.hidden, a.top_k, a.n_experts
@@ -483,8 +492,8 @@ def measure(args, arch, dist, rank, world, steps: int, warmup: int, main: bool, 
                 "d2h_bytes_per_step": int(out.numel() * out.element_size())},
         "roofline": roofline,
         "expert_gemm": {"tflops": expert_tflops, "tensor_util_of_bf16_peak": expert_tflops / tf_burst,
-                        "tokens_per_expert": rows / a.n_experts, "gate_up_ms": gu["avg_ms"], "down_ms": dn["avg_ms"],
-                        "gate_up_gbs": gu_gbs, "down_gbs": dn_bytes / (dn["avg_ms"] * 1e-3) / 1e9},
+                        "tokens_per_expert": rows / a.n_experts, "ffn_ms": ffn_ms, "gate_up_ms": gu_ms, "down_ms": dn_ms,
+                        "ffn_gbs": (gu_bytes + dn_bytes) / (ffn_ms * 1e-3) / 1e9},
         "incl_prefill": incl,
         "kernel_hbm": kernel_hbm,
         "kernel_ms_per_forward": {k: round(v["ms_per_step"], 4) for k, v in sorted(bd.items())},

@@ -92,6 +92,12 @@ int mgb_ep_row_ptrs(const int* seg_start, const int* seg_len, const int* seg_del
                     const long long* peer_base, int row_bytes, int rows_cap, long long* row_ptr, void* stream);
 int mgb_moe_gemm_down_ep(const void* w_down, const void* h, const int* offsets, int E, int d, int f, int rows_cap,
                          const long long* row_ptr, void* stream);
+/* The whole expert FFN as ONE persistent tcgen05 CTA-pair launch: gate/up (+ SiLU*up) and down units
+ * share one unit list, the down units of expert e waiting on a device counter of e's finished gate/up
+ * units (one wave tail, no launch gap).  h_scratch [rows_cap, f]; sync: 257 ints zeroed once (left
+ * zero).  Shapes outside the pair tiling (f % 128, d % 256) run the two GEMMs back to back. */
+int mgb_moe_ffn(const void* w_gate_up, const void* w_down, const void* x_perm, const int* offsets, int E, int d, int f,
+                int rows_cap, void* h_scratch, void* y_out, int* sync, void* stream);
 int mgb_grouped_ffn(const void* w_gate_up, const void* w_down, const void* x_perm, const int* offsets, int E, int d,
                     int f, int rows_cap, void* h_scratch, void* y_out, void* stream);
 

@@ -38,6 +38,7 @@ SIGNATURES: dict[str, list] = {
     # grouped expert FFN (moe_gemm.cu)
     "mgb_moe_gemm_gate_up": [P, P, P, I, I, I, I, P, P],
     "mgb_moe_gemm_down": [P, P, P, I, I, I, I, P, P],
+    "mgb_moe_ffn": [P, P, P, P, I, I, I, I, P, P, P, P],
     "mgb_grouped_ffn": [P, P, P, P, I, I, I, I, P, P, P],
     "mgb_moe_gemm_down_ep": [P, P, P, I, I, I, I, P, P],
     "mgb_ep_permute_dispatch": [P, P, P, P, P, I, I, I, I, I, P, P, I, P, P, P],

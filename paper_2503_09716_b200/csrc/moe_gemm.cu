@@ -89,6 +89,12 @@ struct UnitSched {
   }
 };
 
+MGB_DEVINL int ld_acquire_gpu_s32(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // named barrier of one epilogue group (ids 1.., 128 threads); 0 is __syncthreads
 MGB_DEVINL void epi_bar(int group) { asm volatile("bar.sync %0, 128;" ::"r"(1 + group) : "memory"); }
 
@@ -487,6 +493,255 @@ moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
   if (warp == 1) tmem_dealloc_pair<512>(tmem_base);
 }
 
+// ------------------------------------------------------------------------------------------
+// Fused expert FFN: gate/up AND down of every expert in ONE persistent CTA-pair launch.
+// The unit list is [all gate/up units | all down units] (each part ordered as the separate kernels
+// order theirs); pair p runs units p, p + npairs, ... .  A down unit of expert e needs all of e's
+// h rows: its producers wait until the epilogue warps of every gate/up unit of e have stored their
+// rows and counted them on done[e] (release: fence + atomic; acquire + proxy fence before the TMA
+// reads h).  No deadlock: a pair reaches a down unit only after issuing all of its own gate/up
+// units, every gate/up unit precedes every down unit in the list, and the persistent grid is
+// co-resident.  What it buys: the two launches' wave tails (Mixtral: 896 gate/up units of 64 K
+// blocks then 128 down units of 224 on 74 pairs: 13 + 2 rounds) become one tail, and the gap
+// between the launches disappears.  The last pair to finish zeroes done[] for the next launch.
+// ------------------------------------------------------------------------------------------
+struct FfnGemm {
+  int MT;               // pair row tiles per expert
+  int KB;               // K blocks
+  int rows_per_expert;  // weight rows per expert (2f gated, d down)
+  int half_rows;        // f (gated: offset of the up rows)
+  int ldo;              // output row stride
+  __nv_bfloat16* out;
+};
+
+MGB_DEVINL void ffn_decode(int u, int total_gu, const int* s_pgu, const int* s_pdn, int E, const int* offs,
+                           const FfnGemm& gu, const FfnGemm& dn, bool& gated, int& e, int& mt, int& tok0, int& n) {
+  gated = u < total_gu;
+  const int* pre = gated ? s_pgu : s_pdn;
+  const int v = gated ? u : u - total_gu;
+  int lo = 0, hi = E - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (pre[mid] <= v) lo = mid; else hi = mid - 1;
+  }
+  e = lo;
+  const int local = v - pre[e];
+  const int beg = offs[e], cnt = offs[e + 1] - beg;
+  const int tile = token_tile(cnt, gated), NT = (cnt + tile - 1) / tile;
+  mt = local / NT;
+  const int nt = local - mt * NT;
+  tok0 = beg + nt * tile;
+  n = min(tile, cnt - nt * tile);
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Epi<true>::kThreads, 1)
+moe_ffn_pair_kernel(const __grid_constant__ CUtensorMap tmAg, const __grid_constant__ CUtensorMap tmBx,
+                    const __grid_constant__ CUtensorMap tmB8x, const __grid_constant__ CUtensorMap tmAd,
+                    const __grid_constant__ CUtensorMap tmBh, const __grid_constant__ CUtensorMap tmB8h,
+                    const int* __restrict__ offsets, int E, FfnGemm gu, FfnGemm dn, int nalign, int rows_cap,
+                    int* __restrict__ cap_status, int* __restrict__ done) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* tiles = smem;
+  float* xbuf = reinterpret_cast<float*>(smem + kPStages * kPStageBytes);
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kPStages * kPStageBytes + Epi<true>::kXBytes);
+  uint64_t* empty_bar = full_bar + kPStages;
+  uint64_t* tfull_bar = empty_bar + kPStages;
+  uint64_t* tempty_bar = tfull_bar + kAccStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + kAccStages);
+  __shared__ int s_pgu[kMaxExperts + 1], s_pdn[kMaxExperts + 1], s_need[kMaxExperts];
+  __shared__ bool s_last;
+  constexpr int kGroups = Epi<true>::kGroups;
+  constexpr int kArrivals = 2 * 4 * kGroups;  // epilogue warps of both CTAs per unit
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+
+  if (threadIdx.x == 0) {
+    const bool fit = segments_fit(offsets, E, rows_cap, cap_status, kCapGateUp);
+    int ag = 0, ad = 0;
+    for (int e = 0; e < E; ++e) {
+      s_pgu[e] = ag;
+      s_pdn[e] = ad;
+      const int cnt = offsets[e + 1] - offsets[e];
+      const int ug = token_tiles(cnt, true) * gu.MT;
+      s_need[e] = ug * kArrivals;
+      ag += ug;
+      ad += token_tiles(cnt, false) * dn.MT;
+    }
+    s_pgu[E] = fit ? ag : 0;
+    s_pdn[E] = fit ? ad : 0;
+  }
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmAg);
+    prefetch_tmap(&tmBx);
+    prefetch_tmap(&tmB8x);
+    prefetch_tmap(&tmAd);
+    prefetch_tmap(&tmBh);
+    prefetch_tmap(&tmB8h);
+    for (int s = 0; s < kPStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < kAccStages; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], kArrivals);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc_pair<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int total_gu = s_pgu[E];
+  const int total = total_gu + s_pdn[E];
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+
+  if (warp == 0) {
+    // ------------------------------ TMA producer (both CTAs) ------------------------------
+    if (elect_one()) {
+      const uint64_t pol_once = policy_evict_first(), pol_shared = policy_evict_normal();
+      const uint64_t pol_x = policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = pair; u < total; u += npairs) {
+        bool gated;
+        int e, mt, tok0, n;
+        ffn_decode(u, total_gu, s_pgu, s_pdn, E, offsets, gu, dn, gated, e, mt, tok0, n);
+        const FfnGemm& G = gated ? gu : dn;
+        const CUtensorMap* tA = gated ? &tmAg : &tmAd;
+        const CUtensorMap* tB = gated ? &tmBx : &tmBh;
+        const CUtensorMap* tB8 = gated ? &tmB8x : &tmB8h;
+        if (!gated) {  // h rows of expert e: every gate/up unit of e has stored and counted them
+          const int need = s_need[e];
+          while (ld_acquire_gpu_s32(done + e) < need) __nanosleep(64);
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+        const int rows_cta = gated ? kBM / 2 : kBM;
+        const uint64_t pol_w = token_tiles(offsets[e + 1] - offsets[e], gated) > 1 ? pol_shared : pol_once;
+        const int N = (n + nalign - 1) & ~(nalign - 1);
+        const int half = N / 2;
+        const int nb = half / kPBRows, r8 = (half / 8) & 1;
+        const uint32_t bytes = 2u * (kATileBytes + half * kBK * 2);
+        const int arow0 = e * G.rows_per_expert + mt * 2 * rows_cta + rank * rows_cta;
+        const int trow0 = tok0 + rank * half;
+        for (int kb = 0; kb < G.KB; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          if (leader) mbar_arrive_expect_tx(&full_bar[stage], bytes);
+          uint8_t* st = tiles + stage * kPStageBytes;
+          if (gated) {
+            tma_load_2d_pair(st, tA, &full_bar[stage], kb * kBK, arow0, pol_w);
+            tma_load_2d_pair(st + kAHalfBytes, tA, &full_bar[stage], kb * kBK, arow0 + G.half_rows, pol_w);
+          } else {
+            tma_load_2d_pair(st, tA, &full_bar[stage], kb * kBK, arow0, pol_w);
+          }
+          uint8_t* bt = st + kATileBytes;
+          for (int j = 0; j < nb; ++j)
+            tma_load_2d_pair(bt + j * kPBBoxBytes, tB, &full_bar[stage], kb * kBK, trow0 + j * kPBRows, pol_x);
+          if (r8) tma_load_2d_pair(bt + nb * kPBBoxBytes, tB8, &full_bar[stage], kb * kBK, trow0 + nb * kPBRows, pol_x);
+          if (++stage == kPStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------ MMA issuer (leader only) ------------------------------
+    if (leader && elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int u = pair; u < total; u += npairs) {
+        bool gated;
+        int e, mt, tok0, n;
+        ffn_decode(u, total_gu, s_pgu, s_pdn, E, offsets, gu, dn, gated, e, mt, tok0, n);
+        const int KB = gated ? gu.KB : dn.KB;
+        const uint32_t N = (uint32_t)((n + nalign - 1) & ~(nalign - 1));
+        const uint32_t idesc = make_idesc_bf16(2 * kBM, N);
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d0 = tmem_base + acc * kBNMax;
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t st = smem_u32(tiles + stage * kPStageBytes);
+          const uint64_t a0 = make_sdesc_sw128(st);
+          const uint64_t b0 = make_sdesc_sw128(st + kATileBytes);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k)
+            umma_bf16_pair(d0, a0 + 2 * k, b0 + 2 * k, idesc, (kb | k) ? 1u : 0u);
+          umma_commit_pair(&empty_bar[stage], 0x3);
+          if (++stage == kPStages) { stage = 0; phase ^= 1; }
+        }
+        umma_commit_pair(&tfull_bar[acc], 0x3);
+        if (++acc == kAccStages) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else {
+    // ------------------------------ epilogue (warps 2..9, both CTAs) ------------------------------
+    const uint32_t q = warp & 3;
+    const int row = q * 32 + lane;
+    const int group = (int)(warp - 2) >> 2;
+    float* gx = xbuf + group * 64 * kXStride;
+    const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty_bar[0]), 0);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int u = pair; u < total; u += npairs) {
+      bool gated;
+      int e, mt, tok0, n;
+      ffn_decode(u, total_gu, s_pgu, s_pdn, E, offsets, gu, dn, gated, e, mt, tok0, n);
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t tl = tmem_base + ((q * 32) << 16) + acc * kBNMax;
+      if (gated) {
+        const int col0 = mt * 2 * (kBM / 2) + rank * (kBM / 2);
+        const bool is_up = q >= 2;
+        const int f = row & 63;
+        __nv_bfloat16* ocol = gu.out + (size_t)tok0 * gu.ldo + col0 + f;
+        for (int c0 = 32 * group; c0 < n; c0 += 32 * kGroups) gated_chunk(tl, c0, n, is_up, f, gx, ocol, gu.ldo, group);
+      } else {
+        const int col = mt * 2 * kBM + rank * kBM + row;
+        __nv_bfloat16* ocol = dn.out + (size_t)tok0 * dn.ldo + col;
+        for (int c0 = 32 * group; c0 < n; c0 += 32 * kGroups) {
+          uint32_t v[32];
+          tmem_ld32(tl + c0, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (c0 + j < n) ocol[(size_t)(c0 + j) * dn.ldo] = __float2bfloat16_rn(__uint_as_float(v[j]));
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (gated) {  // this warp's share of e's h rows is stored: count it (release to the down units)
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicAdd(done + e, 1);
+      }
+      if (lane == 0) mbar_arrive_cluster(tempty_leader0 + acc * 8);
+      if (++acc == kAccStages) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 1) tmem_dealloc_pair<512>(tmem_base);
+  // the last CTA out resets the per-expert counters (and the exit ticket) for the next launch
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(done + kMaxExperts, 1) == (int)gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last) {
+    for (int e = threadIdx.x; e < E; e += blockDim.x) done[e] = 0;
+    if (threadIdx.x == 0) done[kMaxExperts] = 0;
+  }
+}
+
 }  // namespace mgb
 
 // ------------------------------------------------------------------------------------------
@@ -599,6 +854,47 @@ int mgb_moe_gemm_down_ep(const void* w_down, const void* h, const int* offsets, 
   if (E < 1 || E > mgb::kMaxExperts || f % mgb::kBK || d % mgb::kBM || rows_cap < 1 || !row_ptr) return MGB_EINVAL;
   return launch_moe_gemm<false>(w_down, E * d, h, rows_cap, offsets, E, d / mgb::kBM, f, d, 0, nullptr, d,
                                 reinterpret_cast<cudaStream_t>(stream), row_ptr);
+}
+
+// The whole expert FFN (gate/up + SiLU*up + down) as ONE persistent CTA-pair launch (moe_ffn_pair_kernel):
+// the down units of expert e start as soon as e's h rows are complete, so the two GEMMs share one
+// wave tail.  sync: 257 ints, zero before the first launch and left zero by every launch (per-expert
+// completion counters + the exit ticket).  Shapes the pair tiling does not cover (f % 128, d % 256)
+// or MGB_GEMM_PAIR=0 run the two grouped GEMMs back to back instead.
+int mgb_moe_ffn(const void* w_gate_up, const void* w_down, const void* x_perm, const int* offsets, int E, int d, int f,
+                int rows_cap, void* h_scratch, void* y_out, int* sync, void* stream) {
+  if (E < 1 || E > mgb::kMaxExperts || d % mgb::kBM || f % (mgb::kBM / 2) || d % mgb::kBK || f % mgb::kBK ||
+      rows_cap < 1 || !sync)
+    return MGB_EINVAL;
+  const bool fused = use_pair_kernel() && f % 128 == 0 && d % 256 == 0 && (mgb_host::num_sms() & ~1) >= 2;
+  if (!fused) {
+    const int rc = mgb_moe_gemm_gate_up(w_gate_up, x_perm, offsets, E, d, f, rows_cap, h_scratch, stream);
+    return rc ? rc : mgb_moe_gemm_down(w_down, h_scratch, offsets, E, d, f, rows_cap, y_out, stream);
+  }
+  CUtensorMap tAg, tBx, tB8x, tAd, tBh, tB8h;
+  using mgb_host::encode_tmap_2d_bf16;
+  if (encode_tmap_2d_bf16(&tAg, w_gate_up, d, (uint64_t)E * 2 * f, (uint64_t)d * 2, mgb::kBK, mgb::kBM / 2) ||
+      encode_tmap_2d_bf16(&tBx, x_perm, d, rows_cap, (uint64_t)d * 2, mgb::kBK, mgb::kPBRows) ||
+      encode_tmap_2d_bf16(&tB8x, x_perm, d, rows_cap, (uint64_t)d * 2, mgb::kBK, 8) ||
+      encode_tmap_2d_bf16(&tAd, w_down, f, (uint64_t)E * d, (uint64_t)f * 2, mgb::kBK, mgb::kBM) ||
+      encode_tmap_2d_bf16(&tBh, h_scratch, f, rows_cap, (uint64_t)f * 2, mgb::kBK, mgb::kPBRows) ||
+      encode_tmap_2d_bf16(&tB8h, h_scratch, f, rows_cap, (uint64_t)f * 2, mgb::kBK, 8))
+    return MGB_ECUDA;
+  int* cap_status = mgb_host::capacity_status_ptr();
+  if (!cap_status) return MGB_ECUDA;
+  if (const int rc = mgb_host::ensure_max_smem((const void*)mgb::moe_ffn_pair_kernel, mgb::pair_smem<true>()))
+    return rc;
+  const mgb::FfnGemm gu{f / 128, d / mgb::kBK, 2 * f, f, f, reinterpret_cast<__nv_bfloat16*>(h_scratch)};
+  const mgb::FfnGemm dn{d / 256, f / mgb::kBK, d, 0, d, reinterpret_cast<__nv_bfloat16*>(y_out)};
+  static const int nalign = [] {
+    const char* e = getenv("MGB_PAIR_NALIGN");
+    return (e && atoi(e) == 32) ? 32 : 16;
+  }();
+  const int grid = mgb_host::num_sms() & ~1;
+  mgb::moe_ffn_pair_kernel<<<grid, mgb::Epi<true>::kThreads, mgb::pair_smem<true>(),
+                             reinterpret_cast<cudaStream_t>(stream)>>>(tAg, tBx, tB8x, tAd, tBh, tB8h, offsets, E, gu, dn,
+                                                                       nalign, rows_cap, cap_status, sync);
+  return mgb_host::launch_status();
 }
 
 // Both GEMMs back to back (h is caller-owned scratch [rows_cap, f]).

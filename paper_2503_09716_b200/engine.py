@@ -285,6 +285,11 @@ class Engine:
         self._trace_counts: torch.Tensor | None = None  # [layers, E] routed rows per expert (trace mode)
         self._forced_logits: torch.Tensor | None = None  # [layers, B, E] router input (force_routing)
         self._segments: dict[int, torch.Tensor] = {}
+        # completion counters of the fused expert FFN launch (mgb_moe_ffn); every launch of this engine
+        # runs on its compute stream, one after another, and leaves them zero
+        self.ffn_sync = torch.zeros(257, dtype=torch.int32, device=device)
+        ffn_env = os.environ.get("MGB_FFN_FUSED")
+        self._ffn_fused = None if ffn_env is None else ffn_env != "0"
         self._dense_mlp_cublas = os.environ.get("MGB_DENSE_MLP", "gemm") == "cublas"
         # decode routing front end as ONE launch (route.cu: residual add + RMSNorm + router logits +
         # top-k + counts/offsets + permutation) for HBM-resident weights without EP; MGB_FUSED_ROUTE=0
@@ -707,8 +712,21 @@ class Engine:
             ops.silu_mul(gu, h)
             torch.mm(h, w_down[0].t(), out=y)
             return
-        ops.moe_gemm_gate_up(w_gate_up, x, seg, h)
-        ops.moe_gemm_down(w_down, h, seg, y)
+        self._ffn(w_gate_up, w_down, x, seg, h, y)
+
+    def _ffn(self, w_gate_up, w_down, x, offsets, h, y) -> None:
+        """Expert FFN over expert-major rows: the fused single launch (mgb_moe_ffn) for a few large
+        experts (Mixtral: its gate/up and down waves share one tail, -3.5 % of the FFN time in the bench,
+        same-box A/B), two grouped launches otherwise (DeepSeek's 64 routed experts: +3 % fused; a
+        single expert segment: every down unit would wait for the last gate/up unit anyway).
+        MGB_FFN_FUSED=0/1 forces either."""
+        E = w_gate_up.shape[0]
+        fused = self._ffn_fused if self._ffn_fused is not None else 2 <= E <= 16
+        if fused:
+            ops.moe_ffn(w_gate_up, w_down, x, offsets, h, y, self.ffn_sync)
+        else:
+            ops.moe_gemm_gate_up(w_gate_up, x, offsets, h)
+            ops.moe_gemm_down(w_down, h, offsets, y)
 
     def _segment(self, T: int) -> torch.Tensor:
         """Device offsets [0, T] of a one-segment grouped GEMM (cached per T)."""
@@ -732,8 +750,7 @@ class Engine:
         elif first_chunk and e >= n_c:
             gu, dn = self.w.slot_views(self.slot_of[(l, e)])
             offs = self.rws.offsets[e:e + 2]
-            ops.moe_gemm_gate_up(gu, b.x_perm, offs, b.h_ffn)
-            ops.moe_gemm_down(dn, b.h_ffn, offs, b.y_perm)
+            self._ffn(gu, dn, b.x_perm, offs, b.h_ffn, b.y_perm)
         if j.id == self.last_expert_job[l]:
             nxt = self.w.layers[l + 1]["ln1"] if l + 1 < a.layers else self.w.final_norm
             y_perm = self.ep.yperm if self.peer_ep else b.y_perm
@@ -745,8 +762,7 @@ class Engine:
         experts' owner ranks and back around the local grouped GEMMs (ep.py)."""
         b = self.buf
         if self.ep is None:
-            ops.moe_gemm_gate_up(W["w_gate_up"], b.x_perm, self.rws.offsets, b.h_ffn)
-            ops.moe_gemm_down(W["w_down"], b.h_ffn, self.rws.offsets, b.y_perm)
+            self._ffn(W["w_gate_up"], W["w_down"], b.x_perm, self.rws.offsets, b.h_ffn, b.y_perm)
             return
         a, ep = self.arch, self.ep
         if self.peer_ep:
@@ -766,8 +782,7 @@ class Engine:
         y_loc = torch.empty(n, a.hidden, dtype=BF16, device=self.device)
         if n > 0:
             h = torch.empty(n, a.moe_ffn, dtype=BF16, device=self.device)
-            ops.moe_gemm_gate_up(W["w_gate_up"], x_loc, offs, h)
-            ops.moe_gemm_down(W["w_down"], h, offs, y_loc)
+            self._ffn(W["w_gate_up"], W["w_down"], x_loc, offs, h, y_loc)
         y = ep.combine(y_loc, st)
         b.y_perm[:y.shape[0]].copy_(y)
 
@@ -1177,8 +1192,7 @@ class Engine:
                     ops.router_topk(None, None, ws, k, a.router_mode, a.routed_scaling, a.n_group, a.topk_group,
                                     logits_in=S["lg"][:t])
                     ops.permute(h, ws, S["xp"])
-                    ops.moe_gemm_gate_up(W["w_gate_up"], S["xp"], ws.offsets, S["hf"])
-                    ops.moe_gemm_down(W["w_down"], S["hf"], ws.offsets, S["yp"])
+                    self._ffn(W["w_gate_up"], W["w_down"], S["xp"], ws.offsets, S["hf"], S["yp"])
                     ops.unpermute_combine(S["yp"], ws, x, t, residual=x, shared_out=shared, norm_w=nxt,
                                           eps=a.rms_eps, norm_out=h)
                 last = h.view(n, P, d)[:, P - 1].contiguous()
@@ -1327,8 +1341,7 @@ class Engine:
                     for c0 in range(r0, r1, be) if run else ():  # b_e-row pieces of the expert's group
                         c1 = min(r1, c0 + be)
                         lo = self._segment(c1 - c0)
-                        ops.moe_gemm_gate_up(gu, xp[c0:c1], lo, hf[:c1 - c0])
-                        ops.moe_gemm_down(dn, hf[:c1 - c0], lo, yp[c0:c1])
+                        self._ffn(gu, dn, xp[c0:c1], lo, hf[:c1 - c0], yp[c0:c1])
                     if e >= n_c:
                         slot_free[computed % nsl].record(st)
                         computed += 1

@@ -136,6 +136,16 @@ def moe_gemm_down(w_down: torch.Tensor, h: torch.Tensor, offsets: torch.Tensor, 
     nat.call("mgb_moe_gemm_down", _p(w_down), _p(h), _p(offsets), E, d, f, h.shape[0], _p(y_out), _s())
 
 
+def moe_ffn(w_gate_up: torch.Tensor, w_down: torch.Tensor, x_perm: torch.Tensor, offsets: torch.Tensor,
+            h: torch.Tensor, y_out: torch.Tensor, sync: torch.Tensor) -> None:
+    """The whole grouped expert FFN in one launch (gate/up + SiLU*up + down; mgb_moe_ffn).
+    sync: int32 [257] zeros, reused across launches (each launch leaves it zero)."""
+    E, two_f, d = w_gate_up.shape
+    assert sync.numel() >= 257 and sync.dtype == torch.int32
+    nat.call("mgb_moe_ffn", _p(w_gate_up), _p(w_down), _p(x_perm), _p(offsets), E, d, two_f // 2, x_perm.shape[0],
+             _p(h), _p(y_out), _p(sync), _s())
+
+
 def unpermute_combine(y_perm: torch.Tensor, ws: RouterWorkspace, out: torch.Tensor, T: int,
                       residual: torch.Tensor | None = None, shared_out: torch.Tensor | None = None,
                       norm_w: torch.Tensor | None = None, eps: float = 0.0,
