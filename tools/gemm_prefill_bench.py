@@ -2,7 +2,8 @@
 per expert, SURVEY.md §7.1): Mixtral-8x7B / DeepSeek-V2-Lite expert dims, CUDA-event timed;
 TFLOP/s and the fraction of the measured dense bf16 peak (MEASURED_PEAKS.json, burst).
 
-python tools/gemm_prefill_bench.py [config] [tokens_per_expert,...]   -> one JSON line per size
+python tools/gemm_prefill_bench.py [config] [tokens_per_expert,...] [ffn]   -> one JSON line per size
+("ffn" also times the fused single-launch FFN, mgb_moe_ffn, on the same rows)
 """
 import json
 import os
@@ -24,6 +25,8 @@ bf = torch.bfloat16
 wgu = (torch.randn(E, 2 * f, d, device="cuda") * 0.02).to(bf)
 wd = (torch.randn(E, d, f, device="cuda") * 0.02).to(bf)
 reps = int(os.environ.get("REPS", "10"))
+with_ffn = len(sys.argv) > 3 and sys.argv[3] == "ffn"
+sync = torch.zeros(257, dtype=torch.int32, device="cuda")
 for n in sizes:
     T = n * E
     x = torch.randn(T, d, device="cuda").to(bf)
@@ -31,8 +34,11 @@ for n in sizes:
     y = torch.empty(T, d, device="cuda", dtype=bf)
     offs = torch.arange(0, T + 1, n, dtype=torch.int32, device="cuda")
     row = {"config": cfg, "tokens_per_expert": n, "E": E, "d": d, "f": f}
-    for name, fn, flops in (("gate_up", lambda: ops.moe_gemm_gate_up(wgu, x, offs, h), 2.0 * T * d * 2 * f),
-                            ("down", lambda: ops.moe_gemm_down(wd, h, offs, y), 2.0 * T * f * d)):
+    cases = [("gate_up", lambda: ops.moe_gemm_gate_up(wgu, x, offs, h), 2.0 * T * d * 2 * f),
+             ("down", lambda: ops.moe_gemm_down(wd, h, offs, y), 2.0 * T * f * d)]
+    if with_ffn:
+        cases.append(("ffn", lambda: ops.moe_ffn(wgu, wd, x, offs, h, y, sync), 2.0 * T * d * 3 * f))
+    for name, fn, flops in cases:
         for _ in range(2):
             fn()
         torch.cuda.synchronize()
@@ -44,5 +50,7 @@ for n in sizes:
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / reps
         tf = flops / (ms * 1e-3) / 1e12
-        row[name] = {"ms": round(ms, 4), "tflops": round(tf, 1), "frac_of_bf16_peak": round(tf / peak, 3)}
+        byts = E * 3 * f * d * 2 + T * (2 * d + 2 * f) * 2  # weights once + rows in/out of both GEMMs
+        row[name] = {"ms": round(ms, 4), "tflops": round(tf, 1), "frac_of_bf16_peak": round(tf / peak, 3),
+                     "ffn_gbs_if_all_weights": round(byts / (ms * 1e-3) / 1e9, 1)}
     print(json.dumps(row), flush=True)
