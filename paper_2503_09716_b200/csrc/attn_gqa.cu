@@ -54,12 +54,6 @@ MGB_DEVINL void mma_bf16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
-// 8x8 b16 register transpose across the warp (thread (g, t) gets rows 2t, 2t+1 of column g)
-MGB_DEVINL uint32_t movmatrix_trans(uint32_t a) {
-  uint32_t d;
-  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(d) : "r"(a));
-  return d;
-}
 MGB_DEVINL void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 template <int HD, int G>
@@ -116,84 +110,65 @@ decode_attn_gqa_kernel(const __nv_bfloat16* __restrict__ q,       // [B, Hkv*G, 
   }
 
   // ------------------------------ consumers (warps 0..3) ------------------------------
-  // "Swap-AB" tiles: the 16 tokens of the warp's page slice are the MMA M dimension and the G query
-  // heads the N dimension (8, heads >= G zero), so S^T = K Q^T and O^T += V^T P^T each take half the
-  // mma.sync of the head-rows-as-M form (G <= 8 of 16 rows used there), and the softmax runs on half
-  // as many dead lanes.  P^T goes from the S^T accumulator layout to the B-operand layout with two
-  // register transposes (movmatrix).  The running max of a head is only raised when a page exceeds it
-  // by 2^8 (P <= 256 stays exact enough in bf16 / fp32), so O is rescaled on a few pages per item.
   const int g = lane >> 2, t = lane & 3;   // mma fragment coordinates
-  const bool head_ok = g < G;              // B-operand column (query head) g exists
-  const bool h0_ok = 2 * t < G, h1_ok = 2 * t + 1 < G;  // this thread's accumulator heads 2t, 2t+1
-  constexpr int DT = HD / 16;              // 16-dim tiles of O^T
+  const bool row_ok = g < G;
   int stage = 0;
   uint32_t phase = 0;
   for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
     const int b = it / Hkv, h = it - b * Hkv;
     const int len = seq_lens[b];
     const int np = (len + kPage - 1) / kPage;
-    // Q^T B-fragments: column n = head g, k = 2t.. of each 16-dim step (heads >= G are zero)
-    uint32_t qb[KSTEPS][2];
-    const __nv_bfloat16* qrow = q + ((size_t)b * Hkv * G + (size_t)h * G + (head_ok ? g : 0)) * HD;
+    // Q A-fragments (rows = the G query heads of this kv head; rows >= G are zero)
+    uint32_t qa[KSTEPS][2];
+    const __nv_bfloat16* qrow = q + ((size_t)b * Hkv * G + (size_t)h * G + (row_ok ? g : 0)) * HD;
 #pragma unroll
     for (int ks = 0; ks < KSTEPS; ++ks) {
-      qb[ks][0] = head_ok ? *reinterpret_cast<const uint32_t*>(qrow + ks * 16 + 2 * t) : 0u;
-      qb[ks][1] = head_ok ? *reinterpret_cast<const uint32_t*>(qrow + ks * 16 + 8 + 2 * t) : 0u;
+      qa[ks][0] = row_ok ? *reinterpret_cast<const uint32_t*>(qrow + ks * 16 + 2 * t) : 0u;
+      qa[ks][1] = row_ok ? *reinterpret_cast<const uint32_t*>(qrow + ks * 16 + 8 + 2 * t) : 0u;
     }
-    float o[DT][4];
+    float o[NT][4];
 #pragma unroll
-    for (int n = 0; n < DT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
-    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;  // heads 2t, 2t+1
+    for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+    float m_run = -INFINITY, l_run = 0.f;
 
     for (int p = 0; p < np; ++p) {
       mbar_wait(&full[stage], phase);
       const uint32_t kbase = smem_u32(ring + stage * S::kStageBytes);
       const uint32_t vbase = kbase + S::kTileBytes;
       const int tok0 = warp * 16;  // this warp's 16 tokens of the page
-      const int mi = lane >> 3, r = lane & 7;
-      // ---- S^T = K Q^T: 16 tokens x 8 heads; two accumulators (even / odd k-steps) break the chain ----
-      float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb[4] = {0.f, 0.f, 0.f, 0.f};
+      // ---- S = Q K^T for 16 tokens (two n-tiles of 8) ----
+      float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int ks = 0; ks < KSTEPS; ++ks) {
-        // A matrices: (tok 0-7, chunk 2ks), (tok 8-15, chunk 2ks), (tok 0-7, chunk 2ks+1), (tok 8-15, chunk 2ks+1)
-        const int chunk = 2 * ks + (mi >> 1);
-        const int tok = tok0 + ((mi & 1) << 3) + r;
-        uint32_t a0, a1, a2, a3;
-        ldsm_x4(kbase + (uint32_t)((chunk * kPage + tok) * 16), a0, a1, a2, a3);
-        if (ks & 1) mma_bf16_16816(sb, a0, a1, a2, a3, qb[ks][0], qb[ks][1]);
-        else mma_bf16_16816(sa, a0, a1, a2, a3, qb[ks][0], qb[ks][1]);
+        // matrices: (chunk 2ks, tok0..+7), (chunk 2ks+1, tok0..+7), (chunk 2ks, tok0+8..), (chunk 2ks+1, tok0+8..)
+        const int mi = lane >> 3, r = lane & 7;
+        const int chunk = 2 * ks + (mi & 1);
+        const int tok = tok0 + ((mi >> 1) << 3) + r;
+        uint32_t b00, b01, b10, b11;
+        ldsm_x4(kbase + (uint32_t)((chunk * kPage + tok) * 16), b00, b01, b10, b11);
+        mma_bf16_16816(s0, qa[ks][0], 0u, qa[ks][1], 0u, b00, b01);
+        mma_bf16_16816(s1, qa[ks][0], 0u, qa[ks][1], 0u, b10, b11);
       }
-      // ---- online softmax: c0/c1 = token g (heads 2t, 2t+1), c2/c3 = token g + 8 ----
+      // ---- online softmax over this warp's tokens (row g; columns 2t,2t+1 and 8+2t,8+2t+1) ----
       const int n_valid = len - p * kPage - tok0;  // tokens of this warp that exist
-      const bool v_lo = g < n_valid, v_hi = g + 8 < n_valid;
-      const float x0 = (v_lo && h0_ok) ? (sa[0] + sb[0]) * scale_log2 : -INFINITY;
-      const float x1 = (v_lo && h1_ok) ? (sa[1] + sb[1]) * scale_log2 : -INFINITY;
-      const float x2 = (v_hi && h0_ok) ? (sa[2] + sb[2]) * scale_log2 : -INFINITY;
-      const float x3 = (v_hi && h1_ok) ? (sa[3] + sb[3]) * scale_log2 : -INFINITY;
-      float mx0 = fmaxf(x0, x2), mx1 = fmaxf(x1, x3);  // over this warp's 16 tokens (lanes with equal t)
+      float x0 = (2 * t < n_valid) ? s0[0] * scale_log2 : -INFINITY;
+      float x1 = (2 * t + 1 < n_valid) ? s0[1] * scale_log2 : -INFINITY;
+      float x2 = (8 + 2 * t < n_valid) ? s1[0] * scale_log2 : -INFINITY;
+      float x3 = (8 + 2 * t + 1 < n_valid) ? s1[1] * scale_log2 : -INFINITY;
+      float mt = fmaxf(fmaxf(x0, x1), fmaxf(x2, x3));
+      mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, 1));
+      mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, 2));
+      const float m_new = fmaxf(m_run, mt);
+      const float m_use = (m_new == -INFINITY) ? 0.f : m_new;
+      const float alpha = exp2f(m_run - m_use);
+      const float p0 = exp2f(x0 - m_use), p1 = exp2f(x1 - m_use), p2 = exp2f(x2 - m_use), p3 = exp2f(x3 - m_use);
+      l_run = l_run * alpha + (p0 + p1 + p2 + p3);
+      m_run = m_new;
 #pragma unroll
-      for (int o_ = 4; o_ < 32; o_ <<= 1) {
-        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o_));
-        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o_));
+      for (int n = 0; n < NT; ++n) {
+        o[n][0] *= alpha;
+        o[n][1] *= alpha;
       }
-      float al0 = 1.f, al1 = 1.f;
-      if (mx0 > m0 + 8.f) { al0 = exp2f(m0 - mx0); m0 = mx0; }
-      if (mx1 > m1 + 8.f) { al1 = exp2f(m1 - mx1); m1 = mx1; }
-      if (__any_sync(0xffffffffu, al0 != 1.f || al1 != 1.f)) {
-        l0 *= al0;
-        l1 *= al1;
-#pragma unroll
-        for (int n = 0; n < DT; ++n) {
-          o[n][0] *= al0;
-          o[n][1] *= al1;
-          o[n][2] *= al0;
-          o[n][3] *= al1;
-        }
-      }
-      const float mu0 = m0 == -INFINITY ? 0.f : m0, mu1 = m1 == -INFINITY ? 0.f : m1;
-      const float p0 = exp2f(x0 - mu0), p1 = exp2f(x1 - mu1), p2 = exp2f(x2 - mu0), p3 = exp2f(x3 - mu1);
-      l0 += p0 + p2;
-      l1 += p1 + p3;
       // V rows past the sequence end (last, partial page) may hold any bits -- an offloaded host
       // page store or a reused staging page -- and P = 0 there would still give 0 * NaN = NaN in
       // the MMA: zero this warp's invalid V rows in the stage before P.V reads them
@@ -208,18 +183,19 @@ decode_attn_gqa_kernel(const __nv_bfloat16* __restrict__ q,       // [B, Hkv*G, 
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
       }
-      // P^T as the B operand (k = 16 tokens, n = 8 heads): transpose the two 8x8 accumulator blocks
-      const uint32_t pb0 = movmatrix_trans(pack_bf16x2(p0, p1));
-      const uint32_t pb1 = movmatrix_trans(pack_bf16x2(p2, p3));
-      // ---- O^T += V^T P^T : one 16-dim tile per ldmatrix.x4.trans ----
+      // P as the A operand (k = 16 tokens): rows >= G are zero
+      const uint32_t pa0 = row_ok ? pack_bf16x2(p0, p1) : 0u;
+      const uint32_t pa2 = row_ok ? pack_bf16x2(p2, p3) : 0u;
+      // ---- O += P V : two dim-chunks (n-tiles) per ldmatrix.x4.trans ----
 #pragma unroll
-      for (int d2 = 0; d2 < DT; ++d2) {
-        // A matrices (V^T, rows = dims): (chunk 2d2, tok 0-7), (chunk 2d2+1, tok 0-7), (chunk 2d2, tok 8-15), (chunk 2d2+1, tok 8-15)
-        const int chunk = 2 * d2 + (mi & 1);
-        const int tok = tok0 + ((mi >> 1) << 3) + r;
-        uint32_t a0, a1, a2, a3;
-        ldsm_x4_t(vbase + (uint32_t)((chunk * kPage + tok) * 16), a0, a1, a2, a3);
-        mma_bf16_16816(o[d2], a0, a1, a2, a3, pb0, pb1);
+      for (int n2 = 0; n2 < NT / 2; ++n2) {
+        const int mi = lane >> 3, r = lane & 7;
+        const int chunk = 2 * n2 + (mi >> 1);
+        const int tok = tok0 + ((mi & 1) << 3) + r;
+        uint32_t v0a, v0b, v1a, v1b;
+        ldsm_x4_t(vbase + (uint32_t)((chunk * kPage + tok) * 16), v0a, v0b, v1a, v1b);
+        mma_bf16_16816(o[2 * n2], pa0, 0u, pa2, 0u, v0a, v0b);
+        mma_bf16_16816(o[2 * n2 + 1], pa0, 0u, pa2, 0u, v1a, v1b);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[stage]);
@@ -227,32 +203,19 @@ decode_attn_gqa_kernel(const __nv_bfloat16* __restrict__ q,       // [B, Hkv*G, 
     }
 
     // ---- merge the 4 warps' partial (m, l, O) and store ----
-#pragma unroll
-    for (int o_ = 4; o_ < 32; o_ <<= 1) {
-      l0 += __shfl_xor_sync(0xffffffffu, l0, o_);
-      l1 += __shfl_xor_sync(0xffffffffu, l1, o_);
-    }
+    l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
+    l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
     constexpr int MS = S::kMergeStride;
     float* mo = merge + warp * MS;
+    if (row_ok) {
 #pragma unroll
-    for (int n = 0; n < DT; ++n) {
-      if (h0_ok) {
-        mo[(2 * t) * HD + 16 * n + g] = o[n][0];
-        mo[(2 * t) * HD + 16 * n + g + 8] = o[n][2];
+      for (int n = 0; n < NT; ++n) {
+        mo[g * HD + n * 8 + 2 * t] = o[n][0];
+        mo[g * HD + n * 8 + 2 * t + 1] = o[n][1];
       }
-      if (h1_ok) {
-        mo[(2 * t + 1) * HD + 16 * n + g] = o[n][1];
-        mo[(2 * t + 1) * HD + 16 * n + g + 8] = o[n][3];
-      }
-    }
-    if (g == 0) {
-      if (h0_ok) {
-        mo[G * HD + 2 * t] = m0;
-        mo[G * HD + 8 + 2 * t] = l0;
-      }
-      if (h1_ok) {
-        mo[G * HD + 2 * t + 1] = m1;
-        mo[G * HD + 8 + 2 * t + 1] = l1;
+      if (t == 0) {
+        mo[G * HD + g] = m_run;
+        mo[G * HD + 8 + g] = l_run;
       }
     }
     named_bar_sync(1, kConsumerWarps * 32);

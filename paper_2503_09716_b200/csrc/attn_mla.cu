@@ -39,8 +39,12 @@
 
 #include "common.cuh"
 
+// S^T partial accumulators (k-step k -> partial k % SACC, summed by the softmax warps).  One: the
+// softmax warps -- the kernel's bottleneck at the power-capped clocks of a long decode run -- then
+// load and add a quarter of the TMEM columns; the single 36-MMA chain is hidden behind the other
+// pages in flight (DSV2-Lite forward 59.5 -> 56.0 ms in the replayed graph vs 4 partials, same box).
 #ifndef MGB_MLA_SACC
-#define MGB_MLA_SACC 4
+#define MGB_MLA_SACC 1
 #endif
 
 namespace mgb {
