@@ -459,7 +459,7 @@ def measure(args, arch, dist, rank, world, steps: int, warmup: int, main: bool, 
         k_tf = kflops / (kr["avg_ms"] * 1e-3) / 1e12
         roofline = {"kernel": kname, "bound": "tensor", "achieved": k_tf, "peak": tf_burst, "unit": "TFLOP/s",
                     "frac": k_tf / tf_burst}
-    traffic, traffic_src = _ncu_traffic(args.config, traffic_key)
+    traffic, traffic_src = _ncu_traffic(arch.name, traffic_key)
     roofline.update({"traffic": traffic, "traffic_source": traffic_src, "algorithmic_bytes_per_launch": kbytes,
                      "algorithmic_flops_per_launch": kflops, "avg_launch_ms": kr["avg_ms"], "peak_source": src,
                      "tokens_per_expert": tok_per_expert, "share_of_step": kr["ms_per_step"] / step_ms_eager})
