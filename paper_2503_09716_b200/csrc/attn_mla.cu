@@ -674,6 +674,107 @@ __global__ void mla_append_kernel(const __nv_bfloat16* __restrict__ q,    // [B,
   }
 }
 
+// Warp-per-token version of mla_append_kernel (same arithmetic; the variance is summed per lane then
+// across the warp): 16-byte loads and stores throughout, every load of a token's latent row and of a
+// batch of its q row in flight together, 8 tokens per CTA -- the decode step's append was a chain of
+// scalar loads / block barriers per token (DSV2-Lite B = 6058: 41 us per layer).
+constexpr int kAppTok = 8;  // tokens (warps) per CTA
+MGB_DEVINL uint4 rope_pairs(uint4 v, const float* cs, const float* sn, int pair0) {
+  // interleaved RoPE on the 4 (even, odd) pairs of one 16-byte chunk; fp32 rotation, one bf16 cast
+  float x[8] = {bf16lo(v.x), bf16hi(v.x), bf16lo(v.y), bf16hi(v.y), bf16lo(v.z), bf16hi(v.z), bf16lo(v.w), bf16hi(v.w)};
+  float y[8];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float c = cs[pair0 + i], s = sn[pair0 + i];
+    y[2 * i] = x[2 * i] * c - x[2 * i + 1] * s;
+    y[2 * i + 1] = x[2 * i] * s + x[2 * i + 1] * c;
+  }
+  return make_uint4(pack_bf16x2(y[0], y[1]), pack_bf16x2(y[2], y[3]), pack_bf16x2(y[4], y[5]), pack_bf16x2(y[6], y[7]));
+}
+
+__global__ void __launch_bounds__(kAppTok * 32)
+mla_append_warp_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ ckv,
+                       const __nv_bfloat16* __restrict__ norm_w, float eps, int B, int H, int R, int RP, int NOPE,
+                       const int* __restrict__ positions, const float* __restrict__ cos_t,
+                       const float* __restrict__ sin_t, const int* __restrict__ block_table, int max_pages,
+                       __nv_bfloat16* __restrict__ cache, __nv_bfloat16* __restrict__ q_nope_out,
+                       __nv_bfloat16* __restrict__ q_pe_out, int* __restrict__ seq_lens) {
+  const int lane = threadIdx.x & 31;
+  const int b = blockIdx.x * kAppTok + (threadIdx.x >> 5);
+  if (b >= B) return;
+  const int pos = positions[b];
+  if (pos < 0 || pos >= max_pages * kMlaPage) return;  // past the planned context: no page to write
+  const int D = R + RP, DP = (D + 63) / 64 * 64;
+  const int nR = R / 8, nD = D / 8, nDP = DP / 8;     // 16-byte chunks: latent, row, padded row
+  constexpr int kLat = 4;                              // latent-row chunks per lane (D <= 1024)
+  const uint4* row = reinterpret_cast<const uint4*>(ckv + (size_t)b * D);
+  uint4 v[kLat];
+#pragma unroll
+  for (int u = 0; u < kLat; ++u)
+    if (lane + 32 * u < nD) v[u] = ld_nc_v4(row + lane + 32 * u);
+  const int page = block_table[(size_t)b * max_pages + pos / kMlaPage];
+  const int slot = pos % kMlaPage;
+  uint4* pg = reinterpret_cast<uint4*>(cache + (size_t)page * DP * kMlaPage);
+  // chunk c (8 dims) of this token inside the swizzled page: block c / 8, row `slot`, chunk c ^ slot
+  auto at = [slot](int c) { return (c >> 3) * (kMlaPage * 8) + slot * 8 + ((c & 7) ^ (slot & 7)); };
+  if (seq_lens && lane == 0) seq_lens[b] = pos + 1;
+  const float* cs = cos_t + (size_t)pos * (RP / 2);
+  const float* sn = sin_t + (size_t)pos * (RP / 2);
+  // latent RMSNorm (HF DeepseekV2RMSNorm: fp32 variance, bf16 cast, times weight)
+  float ss = 0.f;
+#pragma unroll
+  for (int u = 0; u < kLat; ++u) {
+    const int c = lane + 32 * u;
+    if (c < nR) {
+      const float f[8] = {bf16lo(v[u].x), bf16hi(v[u].x), bf16lo(v[u].y), bf16hi(v[u].y),
+                          bf16lo(v[u].z), bf16hi(v[u].z), bf16lo(v[u].w), bf16hi(v[u].w)};
+#pragma unroll
+      for (int i = 0; i < 8; ++i) ss = fmaf(f[i], f[i], ss);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  const float inv = 1.0f / sqrtf(ss / (float)R + eps);
+#pragma unroll
+  for (int u = 0; u < kLat; ++u) {
+    const int c = lane + 32 * u;
+    if (c < nR) {
+      const uint4 w = ld_nc_v4(reinterpret_cast<const uint4*>(norm_w) + c);
+      const float f[8] = {bf16lo(v[u].x), bf16hi(v[u].x), bf16lo(v[u].y), bf16hi(v[u].y),
+                          bf16lo(v[u].z), bf16hi(v[u].z), bf16lo(v[u].w), bf16hi(v[u].w)};
+      const float wf[8] = {bf16lo(w.x), bf16hi(w.x), bf16lo(w.y), bf16hi(w.y), bf16lo(w.z), bf16hi(w.z), bf16lo(w.w), bf16hi(w.w)};
+      float y[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) y[i] = wf[i] * bf16_round(f[i] * inv);
+      pg[at(c)] = make_uint4(pack_bf16x2(y[0], y[1]), pack_bf16x2(y[2], y[3]), pack_bf16x2(y[4], y[5]), pack_bf16x2(y[6], y[7]));
+    } else if (c < nD) {  // the shared k_pe: interleaved RoPE
+      pg[at(c)] = rope_pairs(v[u], cs, sn, (c - nR) * 4);
+    } else if (c < nDP) {  // padding dims: finite (P.V's phantom rows read them times P = 0)
+      pg[at(c)] = make_uint4(0u, 0u, 0u, 0u);
+    }
+  }
+  // q row [H, NOPE + RP]: q_nope -> [H, B, NOPE], q_pe RoPE'd -> [B, H, RP]; kQ chunks per lane in flight
+  const int qc = (NOPE + RP) / 8, nq = H * qc, nope_c = NOPE / 8;
+  const uint4* qrow = reinterpret_cast<const uint4*>(q + (size_t)b * H * (NOPE + RP));
+  constexpr int kQ = 8;
+  for (int c0 = lane; c0 < nq; c0 += 32 * kQ) {
+    uint4 x[kQ];
+#pragma unroll
+    for (int u = 0; u < kQ; ++u)
+      if (c0 + 32 * u < nq) x[u] = ld_nc_v4(qrow + c0 + 32 * u);
+#pragma unroll
+    for (int u = 0; u < kQ; ++u) {
+      const int c = c0 + 32 * u;
+      if (c >= nq) continue;
+      const int h = c / qc, cc = c - h * qc;
+      if (cc < nope_c)
+        reinterpret_cast<uint4*>(q_nope_out + ((size_t)h * B + b) * NOPE)[cc] = x[u];
+      else
+        reinterpret_cast<uint4*>(q_pe_out + ((size_t)b * H + h) * RP)[cc - nope_c] = rope_pairs(x[u], cs, sn, (cc - nope_c) * 4);
+    }
+  }
+}
+
 // Prefill variant (T = n_seq * P prompt tokens; token t = position t % P of sequence seq0 + t / P):
 // the normed latent + RoPE'd k_pe of every prompt token into the latent pages, and contiguous copies
 // for the (non-absorbed) causal prefill attention: c_out [T, R], kpe_out [T, RP]; the q_pe part of
@@ -758,6 +859,16 @@ int mgb_mla_append(const void* q, const void* ckv, const void* norm_w, float eps
                    const int* positions, const float* cos_t, const float* sin_t, const int* block_table, int max_pages,
                    void* cache, void* q_nope_out, void* q_pe_out, int* seq_lens, void* stream) {
   if (B < 1 || H < 1 || R % 8 || RP % 8 || NOPE % 8) return MGB_EINVAL;
+  const char* blk = getenv("MGB_MLA_APPEND_BLOCK");  // the per-token-CTA kernel (A/B and tests)
+  if (!(blk && blk[0] == '1') && ((R + RP + 63) / 64 * 64) <= 1024) {
+    mgb::mla_append_warp_kernel<<<(B + mgb::kAppTok - 1) / mgb::kAppTok, mgb::kAppTok * 32, 0,
+                                  reinterpret_cast<cudaStream_t>(stream)>>>(
+        reinterpret_cast<const __nv_bfloat16*>(q), reinterpret_cast<const __nv_bfloat16*>(ckv),
+        reinterpret_cast<const __nv_bfloat16*>(norm_w), eps, B, H, R, RP, NOPE, positions, cos_t, sin_t, block_table,
+        max_pages, reinterpret_cast<__nv_bfloat16*>(cache), reinterpret_cast<__nv_bfloat16*>(q_nope_out),
+        reinterpret_cast<__nv_bfloat16*>(q_pe_out), seq_lens);
+    return mgb_host::launch_status();
+  }
   mgb::mla_append_kernel<<<B, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<const __nv_bfloat16*>(q), reinterpret_cast<const __nv_bfloat16*>(ckv),
       reinterpret_cast<const __nv_bfloat16*>(norm_w), eps, B, H, R, RP, NOPE, positions, cos_t, sin_t, block_table,
