@@ -106,10 +106,11 @@ MGB_DEVINL uint4 rope_chunk(const uint4* src, int c, int nch, const float* cos_r
   return ov;
 }
 
-// One CTA per token, one thread per (head, 16-byte chunk) of its fused qkv row [Hq | Hkv | Hkv] x hd
-// (32-bit index arithmetic; the token's position, page and slot are CTA-uniform).  q heads are
-// rotated into q_out; k heads rotated and written into the chunk-major K page; v heads copied into
-// the V page.
+// One CTA per token, one thread per (head, chunk pair (j, j + hd/16)) of its fused qkv row
+// [Hq | Hkv | Hkv] x hd: rotate_half pairs exactly those two 16-byte chunks, so each thread loads its
+// two chunks once (no partner re-loads) and issues all of its loads before any store (one memory round
+// trip per token).  q heads are rotated into q_out; k heads rotated and written into the chunk-major K
+// page; v heads copied into the V page.  Same rotation arithmetic as rope_chunk.
 __global__ void rope_append_gqa_kernel(const __nv_bfloat16* __restrict__ qkv, int T, int seq0,
                                        const int* __restrict__ positions, const float* __restrict__ cos_t,
                                        const float* __restrict__ sin_t, int Hq, int Hkv, int hd,
@@ -117,30 +118,49 @@ __global__ void rope_append_gqa_kernel(const __nv_bfloat16* __restrict__ qkv, in
                                        __nv_bfloat16* __restrict__ k_cache, __nv_bfloat16* __restrict__ v_cache,
                                        __nv_bfloat16* __restrict__ q_out, int* __restrict__ seq_lens) {
   const int t = blockIdx.x;
-  const int nch = hd >> 3, H = Hq + 2 * Hkv;
+  const int nch = hd >> 3, half = nch >> 1, H = Hq + 2 * Hkv;
   const int seq = seq0 + t;
+  const int i = threadIdx.x;
+  if (i >= H * half) return;
+  const int hh = i / half, j = i - hh * half;
+  const uint4* src = reinterpret_cast<const uint4*>(qkv + (size_t)t * H * hd + hh * hd);
+  const uint4 xl = src[j], xh = src[j + half];  // requested before the position / page lookups land
   const int pos = positions[seq];
   // a position past the planned context has no page (and no RoPE row): write nothing rather than
   // index the next sequence's block-table row (the host refuses such steps, Engine.run_step)
   if (pos < 0 || pos >= max_pages * kPageTok) return;
-  const int page = block_table[(size_t)seq * max_pages + pos / kPageTok];
+  const int page = hh >= Hq ? block_table[(size_t)seq * max_pages + pos / kPageTok] : 0;
   const int slot = pos % kPageTok;
-  if (seq_lens && threadIdx.x == 0) seq_lens[seq] = pos + 1;  // cache length after the append
-  const float* cs = cos_t + (size_t)pos * (hd / 2);
-  const float* sn = sin_t + (size_t)pos * (hd / 2);
-  const __nv_bfloat16* row = qkv + (size_t)t * H * hd;
-  for (int i = threadIdx.x; i < H * nch; i += blockDim.x) {
-    const int hh = i / nch, c = i - hh * nch;
-    const uint4* src = reinterpret_cast<const uint4*>(row + hh * hd);
-    const uint4 ov = hh < Hq + Hkv ? rope_chunk(src, c, nch, cs, sn) : src[c];
-    if (hh < Hq) {
-      reinterpret_cast<uint4*>(q_out + ((size_t)t * Hq + hh) * hd)[c] = ov;
-    } else {
-      const bool is_k = hh < Hq + Hkv;
-      const int kh = is_k ? hh - Hq : hh - Hq - Hkv;
-      const size_t blk = ((size_t)page * Hkv + kh) * hd * kPageTok;
-      *reinterpret_cast<uint4*>((is_k ? k_cache : v_cache) + blk + ((size_t)c * kPageTok + slot) * 8) = ov;
+  if (seq_lens && i == 0) seq_lens[seq] = pos + 1;  // cache length after the append
+  uint4 ol = xl, oh = xh;
+  if (hh < Hq + Hkv) {
+    const float* cr = cos_t + (size_t)pos * (hd / 2) + j * 8;
+    const float* sr = sin_t + (size_t)pos * (hd / 2) + j * 8;
+    const float4 c0 = *reinterpret_cast<const float4*>(cr), c1 = *reinterpret_cast<const float4*>(cr + 4);
+    const float4 s0 = *reinterpret_cast<const float4*>(sr), s1 = *reinterpret_cast<const float4*>(sr + 4);
+    const float cs[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+    const float sn[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+    const float a[8] = {bf16lo(xl.x), bf16hi(xl.x), bf16lo(xl.y), bf16hi(xl.y), bf16lo(xl.z), bf16hi(xl.z), bf16lo(xl.w), bf16hi(xl.w)};
+    const float b[8] = {bf16lo(xh.x), bf16hi(xh.x), bf16lo(xh.y), bf16hi(xh.y), bf16lo(xh.z), bf16hi(xh.z), bf16lo(xh.w), bf16hi(xh.w)};
+    float rl[8], rh[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {  // HF rotate_half: lo' = lo*cos - hi*sin, hi' = hi*cos + lo*sin (bf16 products)
+      rl[k] = bf16_round(a[k] * cs[k]) + bf16_round(-b[k] * sn[k]);
+      rh[k] = bf16_round(b[k] * cs[k]) + bf16_round(a[k] * sn[k]);
     }
+    ol = make_uint4(pack_bf16x2(rl[0], rl[1]), pack_bf16x2(rl[2], rl[3]), pack_bf16x2(rl[4], rl[5]), pack_bf16x2(rl[6], rl[7]));
+    oh = make_uint4(pack_bf16x2(rh[0], rh[1]), pack_bf16x2(rh[2], rh[3]), pack_bf16x2(rh[4], rh[5]), pack_bf16x2(rh[6], rh[7]));
+  }
+  if (hh < Hq) {
+    uint4* dst = reinterpret_cast<uint4*>(q_out + ((size_t)t * Hq + hh) * hd);
+    dst[j] = ol;
+    dst[j + half] = oh;
+  } else {
+    const bool is_k = hh < Hq + Hkv;
+    const int kh = is_k ? hh - Hq : hh - Hq - Hkv;
+    __nv_bfloat16* blk = (is_k ? k_cache : v_cache) + ((size_t)page * Hkv + kh) * hd * kPageTok;
+    *reinterpret_cast<uint4*>(blk + ((size_t)j * kPageTok + slot) * 8) = ol;
+    *reinterpret_cast<uint4*>(blk + ((size_t)(j + half) * kPageTok + slot) * 8) = oh;
   }
 }
 
@@ -308,13 +328,15 @@ namespace {
 // 256 threads per token CTA (a few (head, chunk) items each): 8 CTAs per SM put a whole decode batch
 // in one wave (Mixtral B=827: 0.44 vs 0.47 ms per forward with one item per thread)
 int rope_threads(int H, int hd) { return std::min(256, (H * (hd / 8) + 31) / 32 * 32); }
+int rope_pair_threads(int H, int hd) { return (H * (hd / 16) + 31) / 32 * 32; }  // one thread per chunk pair
 }  // namespace
 
 int mgb_rope_append_gqa(const void* qkv, int T, int seq0, const int* positions, const float* cos_t,
                         const float* sin_t, int Hq, int Hkv, int head_dim, const int* block_table, int max_pages,
                         void* k_cache, void* v_cache, void* q_out, int* seq_lens, void* stream) {
   if (T < 1 || head_dim % 16 || Hq % Hkv) return MGB_EINVAL;
-  const int threads = rope_threads(Hq + 2 * Hkv, head_dim);
+  const int threads = rope_pair_threads(Hq + 2 * Hkv, head_dim);
+  if (threads > 1024) return MGB_EINVAL;
   mgb::rope_append_gqa_kernel<<<T, threads, 0,
                                 reinterpret_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<const __nv_bfloat16*>(qkv), T, seq0, positions, cos_t, sin_t, Hq, Hkv, head_dim, block_table,
