@@ -403,8 +403,8 @@ constexpr int kCombineVec = 4;  // d <= 8192
 // d, so registers -- and with them resident CTAs per SM -- follow the row width).  The token's
 // residual / shared-expert rows are requested before its routing entries arrive, and all k expert
 // rows of a column are in flight together: a CTA waits for two memory round trips, not four.
-template <int VEC>
-__global__ void __launch_bounds__(kCombineThreads)
+template <int VEC, int KMAX = kMaxK, int NTH = kCombineThreads>
+__global__ void __launch_bounds__(NTH)
 combine_kernel(const __nv_bfloat16* __restrict__ y_perm, const int* __restrict__ dst_pos,
                const float* __restrict__ topk_w, const __nv_bfloat16* __restrict__ shared_out,
                const __nv_bfloat16* residual, int T, int d, int k,
@@ -413,12 +413,12 @@ combine_kernel(const __nv_bfloat16* __restrict__ y_perm, const int* __restrict__
   const int t = blockIdx.x;
   __shared__ int s_pos[kMaxK];
   __shared__ float s_w[kMaxK];
-  __shared__ float s_red[kCombineThreads / 32];
+  __shared__ float s_red[NTH / 32];
   const int nvec = d / 8;
   uint4 rv[VEC], sv[VEC];
 #pragma unroll
   for (int u = 0; u < VEC; ++u) {  // routing-independent rows first (read before out is written)
-    const int c = threadIdx.x + u * kCombineThreads;
+    const int c = threadIdx.x + u * NTH;
     if (c < nvec) {
       if (residual) rv[u] = reinterpret_cast<const uint4*>(residual + (size_t)t * d)[c];
       if (shared_out) sv[u] = ld_nc_v4(reinterpret_cast<const uint4*>(shared_out + (size_t)t * d) + c);
@@ -438,14 +438,14 @@ combine_kernel(const __nv_bfloat16* __restrict__ y_perm, const int* __restrict__
   // weighted sum in j order (j ascending, as the oracle)
 #pragma unroll
   for (int u = 0; u < VEC; ++u) {
-    const int c = threadIdx.x + u * kCombineThreads;
+    const int c = threadIdx.x + u * NTH;
     if (c < nvec) {
-      uint4 v[kMaxK];
+      uint4 v[KMAX];
 #pragma unroll
-      for (int j = 0; j < kMaxK; ++j)
+      for (int j = 0; j < KMAX; ++j)
         if (j < k) v[j] = ld_nc_v4(reinterpret_cast<const uint4*>(y_perm + (size_t)s_pos[j] * d) + c);
 #pragma unroll
-      for (int j = 0; j < kMaxK; ++j)
+      for (int j = 0; j < KMAX; ++j)
         if (j < k) {
           const float w = s_w[j];
           acc[u][0] += w * bf16lo(v[j].x); acc[u][1] += w * bf16hi(v[j].x);
@@ -458,7 +458,7 @@ combine_kernel(const __nv_bfloat16* __restrict__ y_perm, const int* __restrict__
   float ss = 0.f;
 #pragma unroll
   for (int u = 0; u < VEC; ++u) {
-    const int c = threadIdx.x + u * kCombineThreads;
+    const int c = threadIdx.x + u * NTH;
     if (c >= nvec) continue;
 #pragma unroll
     for (int i = 0; i < 8; ++i) acc[u][i] = bf16_round(acc[u][i]);
@@ -487,7 +487,7 @@ combine_kernel(const __nv_bfloat16* __restrict__ y_perm, const int* __restrict__
   uint4 wv[VEC];
 #pragma unroll
   for (int u = 0; u < VEC; ++u) {
-    const int c = threadIdx.x + u * kCombineThreads;
+    const int c = threadIdx.x + u * NTH;
     if (c < nvec) wv[u] = reinterpret_cast<const uint4*>(norm_w)[c];
   }
 #pragma unroll
@@ -496,11 +496,11 @@ combine_kernel(const __nv_bfloat16* __restrict__ y_perm, const int* __restrict__
   __syncthreads();
   float tot = 0.f;
 #pragma unroll
-  for (int i = 0; i < kCombineThreads / 32; ++i) tot += s_red[i];
+  for (int i = 0; i < NTH / 32; ++i) tot += s_red[i];
   const float inv = 1.0f / sqrtf(tot / (float)d + eps);
 #pragma unroll
   for (int u = 0; u < VEC; ++u) {
-    const int c = threadIdx.x + u * kCombineThreads;
+    const int c = threadIdx.x + u * NTH;
     if (c >= nvec) continue;
     const float wf[8] = {bf16lo(wv[u].x), bf16hi(wv[u].x), bf16lo(wv[u].y), bf16hi(wv[u].y),
                          bf16lo(wv[u].z), bf16hi(wv[u].z), bf16lo(wv[u].w), bf16hi(wv[u].w)};
@@ -630,7 +630,15 @@ int mgb_unpermute_combine(const void* y_perm, const int* dst_pos, const float* t
     return MGB_EINVAL;
   const int vec = (d / 8 + mgb::kCombineThreads - 1) / mgb::kCombineThreads;
   auto kern = vec <= 1 ? mgb::combine_kernel<1> : vec <= 2 ? mgb::combine_kernel<2> : mgb::combine_kernel<mgb::kCombineVec>;
-  kern<<<T, mgb::kCombineThreads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+  int nth = mgb::kCombineThreads;
+  if (k <= 2 && d / 8 <= 128 * 4 && d / 8 > 256) {
+    // top-2 rows of a 2-4 k-wide row (Mixtral): 128 threads x 4 vectors and a k <= 2 register budget, so
+    // a decode batch's CTAs are resident in one wave (256 x 2 with room for 8 rows: 80 registers, 3 CTAs
+    // per SM, 1.9 waves at B = 827)
+    kern = mgb::combine_kernel<4, 2, 128>;
+    nth = 128;
+  }
+  kern<<<T, nth, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<const __nv_bfloat16*>(y_perm), dst_pos, topk_w,
       reinterpret_cast<const __nv_bfloat16*>(shared_out), reinterpret_cast<const __nv_bfloat16*>(residual), T, d,
       k, reinterpret_cast<__nv_bfloat16*>(out), reinterpret_cast<const __nv_bfloat16*>(norm_w), eps,
