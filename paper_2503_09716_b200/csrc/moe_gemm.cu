@@ -304,8 +304,27 @@ moe_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 // barrier.  Unit = (expert, token tile, 256-row pair tile).
 // ------------------------------------------------------------------------------------------
 constexpr int kPStages = 6;
-constexpr int kPBRows = 16;                                   // token rows per TMA box (2 KB); + one 8-row box for N/2 % 16
-constexpr int kPBBoxBytes = kPBRows * kBK * 2;
+// A CTA's half of the token tile (N/2 rows, a multiple of 8) is loaded as boxes of 64 / 32 / 16 / 8
+// rows (N = 208: 64 + 32 + 8 -- three TMA requests instead of seven 16-row ones).  The TMA request
+// count, not the bytes, is what bounded the ring: streaming Mixtral's W_gate_up at 64-row A boxes with
+// a 104-row B slice per stage runs at 4.1 TB/s of A with 16-row B boxes and at 6.5 TB/s -- the A-only
+// rate -- with 64+32+8 (tools/tma_pattern_bench.cu).  Every box starts on a whole 8-row (1 KB) swizzle
+// atom, so the boxes together land exactly where one tall box would.
+struct BMaps {
+  CUtensorMap m[4];  // box heights 64, 32, 16, 8 rows (box width kBK)
+};
+MGB_DEVINL void load_b_rows_pair(uint8_t* bt, const BMaps& mp, uint64_t* bar, int kcol, int row0, int rows,
+                                 uint64_t pol) {
+  int r = 0;
+  for (; rows - r >= 64; r += 64) tma_load_2d_pair(bt + r * 128, &mp.m[0], bar, kcol, row0 + r, pol);
+  if (rows - r >= 32) { tma_load_2d_pair(bt + r * 128, &mp.m[1], bar, kcol, row0 + r, pol); r += 32; }
+  if (rows - r >= 16) { tma_load_2d_pair(bt + r * 128, &mp.m[2], bar, kcol, row0 + r, pol); r += 16; }
+  if (rows - r >= 8) tma_load_2d_pair(bt + r * 128, &mp.m[3], bar, kcol, row0 + r, pol);
+}
+MGB_DEVINL void prefetch_bmaps(const BMaps& mp) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) prefetch_tmap(&mp.m[i]);
+}
 constexpr int kPStageBytes = kATileBytes + (kBNMax / 2) * kBK * 2;  // 16 KB A + <= 16 KB half-B
 template <bool GATED> constexpr int pair_smem() {
   return kPStages * kPStageBytes + Epi<GATED>::kXBytes + 1024 + 256;
@@ -313,8 +332,7 @@ template <bool GATED> constexpr int pair_smem() {
 
 template <bool GATED, bool ROWPTR = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Epi<GATED>::kThreads, 1)
-moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const __grid_constant__ CUtensorMap tmB8,
+moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ BMaps tmB,
                      const int* __restrict__ offsets, int E, int MT, int K, int rows_per_expert, int half_rows,
                      __nv_bfloat16* __restrict__ out, int ldo, bool balanced,
                      const long long* __restrict__ row_ptr, int nalign, int rows_cap, int* __restrict__ cap_status) {
@@ -347,8 +365,7 @@ moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
   }
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
-    prefetch_tmap(&tmB);
-    prefetch_tmap(&tmB8);
+    prefetch_bmaps(tmB);
     for (int s = 0; s < kPStages; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
@@ -385,7 +402,6 @@ moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
         const uint64_t pol_w = token_tiles(offsets[e + 1] - offsets[e], balanced) > 1 ? pol_shared : pol_once;
         const int N = (n + nalign - 1) & ~(nalign - 1);
         const int half = N / 2;
-        const int nb = half / kPBRows, r8 = (half / 8) & 1;  // 16-row boxes + one 8-row box
         const uint32_t bytes = 2u * (kATileBytes + half * kBK * 2);
         const int arow0 = e * rows_per_expert + mt * 2 * kRowsPerCta + rank * kRowsPerCta;
         const int trow0 = tok0 + rank * half;
@@ -399,10 +415,7 @@ moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
           } else {
             tma_load_2d_pair(st, &tmA, &full_bar[stage], kb * kBK, arow0, pol_w);
           }
-          uint8_t* bt = st + kATileBytes;
-          for (int j = 0; j < nb; ++j)
-            tma_load_2d_pair(bt + j * kPBBoxBytes, &tmB, &full_bar[stage], kb * kBK, trow0 + j * kPBRows, pol_x);
-          if (r8) tma_load_2d_pair(bt + nb * kPBBoxBytes, &tmB8, &full_bar[stage], kb * kBK, trow0 + nb * kPBRows, pol_x);
+          load_b_rows_pair(st + kATileBytes, tmB, &full_bar[stage], kb * kBK, trow0, half, pol_x);
           if (++stage == kPStages) { stage = 0; phase ^= 1; }
         }
       }
@@ -535,9 +548,8 @@ MGB_DEVINL void ffn_decode(int u, int total_gu, const int* s_pgu, const int* s_p
 }
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Epi<true>::kThreads, 1)
-moe_ffn_pair_kernel(const __grid_constant__ CUtensorMap tmAg, const __grid_constant__ CUtensorMap tmBx,
-                    const __grid_constant__ CUtensorMap tmB8x, const __grid_constant__ CUtensorMap tmAd,
-                    const __grid_constant__ CUtensorMap tmBh, const __grid_constant__ CUtensorMap tmB8h,
+moe_ffn_pair_kernel(const __grid_constant__ CUtensorMap tmAg, const __grid_constant__ BMaps tmBx,
+                    const __grid_constant__ CUtensorMap tmAd, const __grid_constant__ BMaps tmBh,
                     const int* __restrict__ offsets, int E, FfnGemm gu, FfnGemm dn, int nalign, int rows_cap,
                     int* __restrict__ cap_status, int* __restrict__ done) {
   extern __shared__ uint8_t smem_raw[];
@@ -576,11 +588,9 @@ moe_ffn_pair_kernel(const __grid_constant__ CUtensorMap tmAg, const __grid_const
   }
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmAg);
-    prefetch_tmap(&tmBx);
-    prefetch_tmap(&tmB8x);
+    prefetch_bmaps(tmBx);
     prefetch_tmap(&tmAd);
-    prefetch_tmap(&tmBh);
-    prefetch_tmap(&tmB8h);
+    prefetch_bmaps(tmBh);
     for (int s = 0; s < kPStages; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
@@ -614,8 +624,7 @@ moe_ffn_pair_kernel(const __grid_constant__ CUtensorMap tmAg, const __grid_const
         ffn_decode(u, total_gu, s_pgu, s_pdn, E, offsets, gu, dn, gated, e, mt, tok0, n);
         const FfnGemm& G = gated ? gu : dn;
         const CUtensorMap* tA = gated ? &tmAg : &tmAd;
-        const CUtensorMap* tB = gated ? &tmBx : &tmBh;
-        const CUtensorMap* tB8 = gated ? &tmB8x : &tmB8h;
+        const BMaps& tB = gated ? tmBx : tmBh;
         if (!gated) {  // h rows of expert e: every gate/up unit of e has stored and counted them
           const int need = s_need[e];
           while (ld_acquire_gpu_s32(done + e) < need) __nanosleep(64);
@@ -625,7 +634,6 @@ moe_ffn_pair_kernel(const __grid_constant__ CUtensorMap tmAg, const __grid_const
         const uint64_t pol_w = token_tiles(offsets[e + 1] - offsets[e], gated) > 1 ? pol_shared : pol_once;
         const int N = (n + nalign - 1) & ~(nalign - 1);
         const int half = N / 2;
-        const int nb = half / kPBRows, r8 = (half / 8) & 1;
         const uint32_t bytes = 2u * (kATileBytes + half * kBK * 2);
         const int arow0 = e * G.rows_per_expert + mt * 2 * rows_cta + rank * rows_cta;
         const int trow0 = tok0 + rank * half;
@@ -639,10 +647,7 @@ moe_ffn_pair_kernel(const __grid_constant__ CUtensorMap tmAg, const __grid_const
           } else {
             tma_load_2d_pair(st, tA, &full_bar[stage], kb * kBK, arow0, pol_w);
           }
-          uint8_t* bt = st + kATileBytes;
-          for (int j = 0; j < nb; ++j)
-            tma_load_2d_pair(bt + j * kPBBoxBytes, tB, &full_bar[stage], kb * kBK, trow0 + j * kPBRows, pol_x);
-          if (r8) tma_load_2d_pair(bt + nb * kPBBoxBytes, tB8, &full_bar[stage], kb * kBK, trow0 + nb * kPBRows, pol_x);
+          load_b_rows_pair(st + kATileBytes, tB, &full_bar[stage], kb * kBK, trow0, half, pol_x);
           if (++stage == kPStages) { stage = 0; phase ^= 1; }
         }
       }
@@ -756,8 +761,17 @@ bool use_pair_kernel() {
   return v;
 }
 
+// token-operand maps of the pair kernels: box heights 64 / 32 / 16 / 8 rows over [rows, K] bf16
+int encode_bmaps(mgb::BMaps* mp, const void* act, int K, int rows) {
+  const uint32_t h[4] = {64, 32, 16, 8};
+  for (int i = 0; i < 4; ++i)
+    if (mgb_host::encode_tmap_2d_bf16(&mp->m[i], act, K, rows, (uint64_t)K * 2, mgb::kBK, h[i]) != CUDA_SUCCESS)
+      return 1;
+  return 0;
+}
+
 template <bool GATED, bool PAIR, bool ROWPTR>
-int launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmB8, const int* offsets, int E, int MT, int K,
+int launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, const mgb::BMaps& tmBs, const int* offsets, int E, int MT, int K,
                    int rows_per_expert, int half_rows, void* out, int ldo, bool balanced, const long long* row_ptr,
                    int rows_cap, cudaStream_t stream) {
   int* cap_status = mgb_host::capacity_status_ptr();
@@ -774,7 +788,7 @@ int launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtenso
       return (e && atoi(e) == 32) ? 32 : 16;
     }();
     mgb::moe_gemm_pair_kernel<GATED, ROWPTR><<<grid, mgb::Epi<GATED>::kThreads, mgb::pair_smem<GATED>(), stream>>>(
-        tmA, tmB, tmB8, offsets, E, MT / 2, K, rows_per_expert, half_rows, reinterpret_cast<__nv_bfloat16*>(out), ldo,
+        tmA, tmBs, offsets, E, MT / 2, K, rows_per_expert, half_rows, reinterpret_cast<__nv_bfloat16*>(out), ldo,
         balanced, row_ptr, nalign, rows_cap, cap_status);
   } else {
     if (const int rc = mgb_host::ensure_max_smem((const void*)mgb::moe_gemm_kernel<GATED, ROWPTR>,
@@ -801,25 +815,24 @@ int launch_moe_gemm(const void* w, int w_rows_total, const void* act, int act_ro
     return e ? (e[0] == '1' ? 1 : 0) : -1;
   }();
   const bool balanced = bal_env < 0 ? GATED : bal_env == 1;
-  CUtensorMap tmA, tmB, tmB8;
+  CUtensorMap tmA, tmB;
+  mgb::BMaps tmBs;
   if (mgb_host::encode_tmap_2d_bf16(&tmA, w, K, w_rows_total, (uint64_t)K * 2, mgb::kBK,
                                     GATED ? mgb::kBM / 2 : mgb::kBM) != CUDA_SUCCESS)
     return MGB_ECUDA;
-  if (mgb_host::encode_tmap_2d_bf16(&tmB, act, K, act_rows, (uint64_t)K * 2, mgb::kBK,
-                                    pair ? mgb::kPBRows : mgb::kBRows) != CUDA_SUCCESS)
+  if (mgb_host::encode_tmap_2d_bf16(&tmB, act, K, act_rows, (uint64_t)K * 2, mgb::kBK, mgb::kBRows) != CUDA_SUCCESS)
     return MGB_ECUDA;
-  if (pair && mgb_host::encode_tmap_2d_bf16(&tmB8, act, K, act_rows, (uint64_t)K * 2, mgb::kBK, 8) != CUDA_SUCCESS)
-    return MGB_ECUDA;
+  if (pair && encode_bmaps(&tmBs, act, K, act_rows)) return MGB_ECUDA;
   if (row_ptr) {
     if (GATED) return MGB_EINVAL;  // only the down GEMM sends rows home
-    return pair ? launch_variant<GATED, true, true>(tmA, tmB, tmB8, offsets, E, MT, K, rows_per_expert, half_rows, out, ldo,
+    return pair ? launch_variant<GATED, true, true>(tmA, tmB, tmBs, offsets, E, MT, K, rows_per_expert, half_rows, out, ldo,
                                                    balanced, row_ptr, act_rows, stream)
-                : launch_variant<GATED, false, true>(tmA, tmB, tmB, offsets, E, MT, K, rows_per_expert, half_rows, out, ldo,
+                : launch_variant<GATED, false, true>(tmA, tmB, tmBs, offsets, E, MT, K, rows_per_expert, half_rows, out, ldo,
                                                     balanced, row_ptr, act_rows, stream);
   }
-  return pair ? launch_variant<GATED, true, false>(tmA, tmB, tmB8, offsets, E, MT, K, rows_per_expert, half_rows, out, ldo,
+  return pair ? launch_variant<GATED, true, false>(tmA, tmB, tmBs, offsets, E, MT, K, rows_per_expert, half_rows, out, ldo,
                                                   balanced, nullptr, act_rows, stream)
-              : launch_variant<GATED, false, false>(tmA, tmB, tmB, offsets, E, MT, K, rows_per_expert, half_rows, out, ldo,
+              : launch_variant<GATED, false, false>(tmA, tmB, tmBs, offsets, E, MT, K, rows_per_expert, half_rows, out, ldo,
                                                    balanced, nullptr, act_rows, stream);
 }
 }  // namespace
@@ -871,14 +884,12 @@ int mgb_moe_ffn(const void* w_gate_up, const void* w_down, const void* x_perm, c
     const int rc = mgb_moe_gemm_gate_up(w_gate_up, x_perm, offsets, E, d, f, rows_cap, h_scratch, stream);
     return rc ? rc : mgb_moe_gemm_down(w_down, h_scratch, offsets, E, d, f, rows_cap, y_out, stream);
   }
-  CUtensorMap tAg, tBx, tB8x, tAd, tBh, tB8h;
+  CUtensorMap tAg, tAd;
+  mgb::BMaps tBx, tBh;
   using mgb_host::encode_tmap_2d_bf16;
   if (encode_tmap_2d_bf16(&tAg, w_gate_up, d, (uint64_t)E * 2 * f, (uint64_t)d * 2, mgb::kBK, mgb::kBM / 2) ||
-      encode_tmap_2d_bf16(&tBx, x_perm, d, rows_cap, (uint64_t)d * 2, mgb::kBK, mgb::kPBRows) ||
-      encode_tmap_2d_bf16(&tB8x, x_perm, d, rows_cap, (uint64_t)d * 2, mgb::kBK, 8) ||
       encode_tmap_2d_bf16(&tAd, w_down, f, (uint64_t)E * d, (uint64_t)f * 2, mgb::kBK, mgb::kBM) ||
-      encode_tmap_2d_bf16(&tBh, h_scratch, f, rows_cap, (uint64_t)f * 2, mgb::kBK, mgb::kPBRows) ||
-      encode_tmap_2d_bf16(&tB8h, h_scratch, f, rows_cap, (uint64_t)f * 2, mgb::kBK, 8))
+      encode_bmaps(&tBx, x_perm, d, rows_cap) || encode_bmaps(&tBh, h_scratch, f, rows_cap))
     return MGB_ECUDA;
   int* cap_status = mgb_host::capacity_status_ptr();
   if (!cap_status) return MGB_ECUDA;
@@ -892,7 +903,7 @@ int mgb_moe_ffn(const void* w_gate_up, const void* w_down, const void* x_perm, c
   }();
   const int grid = mgb_host::num_sms() & ~1;
   mgb::moe_ffn_pair_kernel<<<grid, mgb::Epi<true>::kThreads, mgb::pair_smem<true>(),
-                             reinterpret_cast<cudaStream_t>(stream)>>>(tAg, tBx, tB8x, tAd, tBh, tB8h, offsets, E, gu, dn,
+                             reinterpret_cast<cudaStream_t>(stream)>>>(tAg, tBx, tAd, tBh, offsets, E, gu, dn,
                                                                        nalign, rows_cap, cap_status, sync);
   return mgb_host::launch_status();
 }
