@@ -79,6 +79,66 @@ add_rmsnorm_kernel(const __nv_bfloat16* x, const __nv_bfloat16* __restrict__ del
   }
 }
 
+// Warp-per-token add + RMSNorm for rows of <= 2048 dims (DeepSeek-V2-Lite's 6058-token decode batch):
+// 8 tokens per CTA, the row in registers, a warp-shuffle sum instead of the block reduction, every
+// load of the row (x, delta, weight) in flight together -- the CTA-per-token kernel is a chain of two
+// block barriers per token over five waves of CTAs.  Same arithmetic per element.
+constexpr int kNormWarpTok = 8;
+template <int V>  // 16-byte vectors per lane (d = 256 * V)
+__global__ void __launch_bounds__(kNormWarpTok * 32)
+add_rmsnorm_warp_kernel(const __nv_bfloat16* x, const __nv_bfloat16* __restrict__ delta,
+                        const __nv_bfloat16* __restrict__ w, float eps, int T, int d, __nv_bfloat16* x_out,
+                        __nv_bfloat16* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const size_t row = (size_t)blockIdx.x * kNormWarpTok + (threadIdx.x >> 5);
+  if (row >= (size_t)T) return;
+  const int nvec = d / 8;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + row * d);
+  const uint4* dr = delta ? reinterpret_cast<const uint4*>(delta + row * d) : nullptr;
+  const uint4* wr = reinterpret_cast<const uint4*>(w);
+  uint4 v[V], dv[V], wv[V];
+#pragma unroll
+  for (int u = 0; u < V; ++u) {
+    const int c = lane + 32 * u;
+    if (c < nvec) {
+      v[u] = xr[c];
+      if (dr) dv[u] = dr[c];
+      wv[u] = wr[c];
+    }
+  }
+  float ss = 0.f;
+#pragma unroll
+  for (int u = 0; u < V; ++u) {
+    const int c = lane + 32 * u;
+    if (c >= nvec) continue;
+    if (dr) {
+      v[u].x = pack_bf16x2(bf16lo(v[u].x) + bf16lo(dv[u].x), bf16hi(v[u].x) + bf16hi(dv[u].x));
+      v[u].y = pack_bf16x2(bf16lo(v[u].y) + bf16lo(dv[u].y), bf16hi(v[u].y) + bf16hi(dv[u].y));
+      v[u].z = pack_bf16x2(bf16lo(v[u].z) + bf16lo(dv[u].z), bf16hi(v[u].z) + bf16hi(dv[u].z));
+      v[u].w = pack_bf16x2(bf16lo(v[u].w) + bf16lo(dv[u].w), bf16hi(v[u].w) + bf16hi(dv[u].w));
+    }
+    if (x_out) reinterpret_cast<uint4*>(x_out + row * d)[c] = v[u];
+    const float f[8] = {bf16lo(v[u].x), bf16hi(v[u].x), bf16lo(v[u].y), bf16hi(v[u].y),
+                        bf16lo(v[u].z), bf16hi(v[u].z), bf16lo(v[u].w), bf16hi(v[u].w)};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ss = fmaf(f[i], f[i], ss);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  const float inv = 1.0f / sqrtf(ss / (float)d + eps);
+#pragma unroll
+  for (int u = 0; u < V; ++u) {
+    const int c = lane + 32 * u;
+    if (c >= nvec) continue;
+    uint4 o;
+    o.x = pack_bf16x2(bf16lo(wv[u].x) * bf16_round(bf16lo(v[u].x) * inv), bf16hi(wv[u].x) * bf16_round(bf16hi(v[u].x) * inv));
+    o.y = pack_bf16x2(bf16lo(wv[u].y) * bf16_round(bf16lo(v[u].y) * inv), bf16hi(wv[u].y) * bf16_round(bf16hi(v[u].y) * inv));
+    o.z = pack_bf16x2(bf16lo(wv[u].z) * bf16_round(bf16lo(v[u].z) * inv), bf16hi(wv[u].z) * bf16_round(bf16hi(v[u].z) * inv));
+    o.w = pack_bf16x2(bf16lo(wv[u].w) * bf16_round(bf16lo(v[u].w) * inv), bf16hi(wv[u].w) * bf16_round(bf16hi(v[u].w) * inv));
+    reinterpret_cast<uint4*>(y + row * d)[c] = o;
+  }
+}
+
 // RoPE of one 16-byte chunk c (8 dims) of a head row: HF rotate_half with bf16 products and sum.
 MGB_DEVINL uint4 rope_chunk(const uint4* src, int c, int nch, const float* cos_row, const float* sin_row) {
   const uint4 xv = src[c];
@@ -317,6 +377,15 @@ extern "C" {
 int mgb_add_rmsnorm(const void* x, const void* delta, const void* weight, float eps, int T, int d, void* x_out,
                     void* y, void* stream) {
   if (T < 1 || d % 8 || d > 8 * mgb::kNormThreads * mgb::kNormVec) return MGB_EINVAL;
+  if (T >= 1024 && d <= 2048) {  // large decode batches of narrow rows: warp per token
+    const int blocks = (T + mgb::kNormWarpTok - 1) / mgb::kNormWarpTok;
+    auto kern = d <= 1024 ? mgb::add_rmsnorm_warp_kernel<4> : mgb::add_rmsnorm_warp_kernel<8>;
+    kern<<<blocks, mgb::kNormWarpTok * 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+        reinterpret_cast<const __nv_bfloat16*>(x), reinterpret_cast<const __nv_bfloat16*>(delta),
+        reinterpret_cast<const __nv_bfloat16*>(weight), eps, T, d, reinterpret_cast<__nv_bfloat16*>(x_out),
+        reinterpret_cast<__nv_bfloat16*>(y));
+    return mgb_host::launch_status();
+  }
   mgb::add_rmsnorm_kernel<<<T, mgb::kNormThreads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<const __nv_bfloat16*>(x), reinterpret_cast<const __nv_bfloat16*>(delta),
       reinterpret_cast<const __nv_bfloat16*>(weight), eps, d, reinterpret_cast<__nv_bfloat16*>(x_out),
