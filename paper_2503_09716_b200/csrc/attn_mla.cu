@@ -81,6 +81,24 @@ MGB_DEVINL void mla_trace(int, int) {}
 
 // named barrier of one softmax warp group (ids 1, 2; 128 threads); 0 is __syncthreads
 MGB_DEVINL void grp_bar(int grp) { asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory"); }
+// the same barrier, returning whether any thread of the group passed true
+MGB_DEVINL bool grp_bar_or(int grp, bool v) {
+  uint32_t r;
+  asm volatile(
+      "{\n\t.reg .pred pi, po;\n\tsetp.ne.u32 pi, %1, 0;\n\tbar.red.or.pred po, %2, 128, pi;\n\t"
+      "selp.u32 %0, 1, 0, po;\n\t}"
+      : "=r"(r)
+      : "r"((uint32_t)v), "r"(1 + grp)
+      : "memory");
+  return r != 0;
+}
+// A page whose scores all stay within 2^kMlaSlack of their heads' running max takes the fast path:
+// one barrier-with-OR instead of the max exchange (P <= 2^kMlaSlack stays exact to bf16 rounding,
+// and fp32 l / O have the range).  Any score beyond it (always the item's first page) takes the
+// exchange, which raises each head's max to its page max where that exceeds it by 2^8.
+#ifndef MGB_MLA_SLACK
+#define MGB_MLA_SLACK 32
+#endif
 
 template <int R, int RP>  // latent width, rope width
 struct MlaCfg {
@@ -413,29 +431,35 @@ decode_attn_mla_kernel(const __grid_constant__ CUtensorMap tm_qlat,  // q_lat [H
         // M = 64 accumulator: token 16*q + lane sits in TMEM lane 32*q + lane (lanes < 16)
         const int tok = q * 16 + lane;
         const bool valid = lane < 16 && tok < n;
-        float x[HG], r[HG];
+        float x[HG];
+        bool over = false;
 #pragma unroll
         for (int h = 0; h < HG; ++h) {
           float acc = __uint_as_float(sv[0][h]);
 #pragma unroll
           for (int j = 1; j < C::kSAcc; ++j) acc += __uint_as_float(sv[j][h]);
           x[h] = valid ? acc * scale_log2 : -INFINITY;
-          r[h] = x[h];
+          over |= x[h] > m_used[h] + (float)MGB_MLA_SLACK;  // (m_used = -inf: every valid score)
         }
-        const float wmax = xreduce8<true>(r, lane);  // lane l (< 16, even) holds head (l >> 1) & 7
-        if (lane < 16 && !(lane & 1)) gred[(s * 4 + q) * 16 + col0 + (lane >> 1)] = wmax;
-        grp_bar(grp);
         float alpha[HG];
         bool rescale = false;  // group-uniform (every thread derives it from the same gred values)
+        if (grp_bar_or(grp, over)) {  // slow path: exchange the page maxima
+          float r[HG];
 #pragma unroll
-        for (int h = 0; h < HG; ++h) {
-          const float* rr = gred + s * 64 + col0 + h;
-          const float pm = fmaxf(fmaxf(rr[0], rr[16]), fmaxf(rr[32], rr[48]));
-          alpha[h] = 1.f;
-          if (pm > m_used[h] + 8.f) {
-            alpha[h] = exp2f(m_used[h] - pm);  // 0 on the first page (m_used = -inf)
-            m_used[h] = pm;
-            rescale = true;
+          for (int h = 0; h < HG; ++h) r[h] = x[h];
+          const float wmax = xreduce8<true>(r, lane);  // lane l (< 16, even) holds head (l >> 1) & 7
+          if (lane < 16 && !(lane & 1)) gred[(s * 4 + q) * 16 + col0 + (lane >> 1)] = wmax;
+          grp_bar(grp);
+#pragma unroll
+          for (int h = 0; h < HG; ++h) {
+            const float* rr = gred + s * 64 + col0 + h;
+            const float pm = fmaxf(fmaxf(rr[0], rr[16]), fmaxf(rr[32], rr[48]));
+            alpha[h] = 1.f;
+            if (pm > m_used[h] + 8.f) {
+              alpha[h] = exp2f(m_used[h] - pm);  // 0 on the first page (m_used = -inf)
+              m_used[h] = pm;
+              rescale = true;
+            }
           }
         }
         if (rescale) {
