@@ -113,6 +113,12 @@ int mgb_unpermute_combine(const void* y_perm, const int* dst_pos, const float* t
 int mgb_decode_attn_gqa(const void* q, const void* k_cache, const void* v_cache, const int* block_table,
                         int max_pages, const int* seq_lens, int B, int Hq, int Hkv, int head_dim, float scale,
                         void* out, void* stream);
+/* ... with dynamic work-item scheduling: CTAs take (sequence, kv-head) items from a global counter as
+ * they stream, so none idles while others finish a static share; sched = 2 ints zeroed once, left
+ * zero by every launch (one per stream). */
+int mgb_decode_attn_gqa_sched(const void* q, const void* k_cache, const void* v_cache, const int* block_table,
+                              int max_pages, const int* seq_lens, int B, int Hq, int Hkv, int head_dim, float scale,
+                              void* out, int* sched, void* stream);
 
 /* ---- ATTN_MECH_GPU for MLA models (DeepSeek-V2; model_catalog.py:242-295 prices it) -------
  * Absorbed latent attention: q_lat [H,B,R], q_pe [B,H,RP], latent pages of mgb_mla_page_size()

@@ -20,6 +20,21 @@
 
 namespace mgb {
 
+// Optional per-page timeline of CTA 0 (build with -DMGB_GQA_TRACE; tools/gqa_trace.py):
+// g_gqa_trace[ev * 512 + i] = %globaltimer of event ev at the CTA's i-th page (or item)
+#ifdef MGB_GQA_TRACE
+__device__ unsigned long long g_gqa_trace[8 * 512];
+MGB_DEVINL void gqa_trace(int ev, int i) {
+  if (blockIdx.x == 0 && i < 512) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_gqa_trace[ev * 512 + i] = t;
+  }
+}
+#else
+MGB_DEVINL void gqa_trace(int, int) {}
+#endif
+
 constexpr int kPage = 64;
 constexpr int kAttnStages = 3;
 constexpr int kConsumerWarps = 4;
@@ -63,7 +78,8 @@ decode_attn_gqa_kernel(const __nv_bfloat16* __restrict__ q,       // [B, Hkv*G, 
                        const __nv_bfloat16* __restrict__ v_cache,
                        const int* __restrict__ block_table, int max_pages,
                        const int* __restrict__ seq_lens, int B, int Hkv, float scale_log2,
-                       __nv_bfloat16* __restrict__ out) {          // [B, Hkv*G*HD]
+                       __nv_bfloat16* __restrict__ out,            // [B, Hkv*G*HD]
+                       int* __restrict__ sched) {                  // optional {next item, exit ticket}
   static_assert(G <= 8 && HD % 16 == 0, "GQA tile: G <= 8 query heads per kv head");
   using S = GqaSmem<HD, G>;
   constexpr int KSTEPS = HD / 16;   // k-steps of QK^T
@@ -73,6 +89,12 @@ decode_attn_gqa_kernel(const __nv_bfloat16* __restrict__ q,       // [B, Hkv*G, 
   float* merge = reinterpret_cast<float*>(smem + kAttnStages * S::kStageBytes);  // [warp][8][HD] + m,l
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kAttnStages * S::kStageBytes + S::kMergeBytes);
   uint64_t* empty = full + kAttnStages;
+  // Work items reach the consumers through a 4-slot ring: with `sched`, the producer takes the next
+  // item from a global counter as it starts loading it (dynamic: every CTA keeps streaming until the
+  // work runs out, instead of the static share of 22-23 items leaving the last wave part-idle); without
+  // it, the static round-robin share.  Item -1 ends the CTA.
+  __shared__ int s_item[4];
+  __shared__ __align__(8) uint64_t item_full[4], item_empty[4];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_items = B * Hkv;
@@ -80,6 +102,10 @@ decode_attn_gqa_kernel(const __nv_bfloat16* __restrict__ q,       // [B, Hkv*G, 
     for (int s = 0; s < kAttnStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kConsumerWarps);
+    }
+    for (int s = 0; s < 4; ++s) {
+      mbar_init(&item_full[s], 1);
+      mbar_init(&item_empty[s], kConsumerWarps);
     }
     fence_mbar_init();
   }
@@ -89,14 +115,21 @@ decode_attn_gqa_kernel(const __nv_bfloat16* __restrict__ q,       // [B, Hkv*G, 
     // ------------------------------ producer ------------------------------
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
-      int stage = 0;
+      int stage = 0, gp = 0;
       uint32_t phase = 0;
-      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+      for (int k = 0;; ++k) {
+        int it = sched ? atomicAdd(sched, 1) : (int)blockIdx.x + k * (int)gridDim.x;
+        if (it >= n_items) it = -1;
+        mbar_wait(&item_empty[k & 3], ((k >> 2) & 1) ^ 1);
+        s_item[k & 3] = it;
+        mbar_arrive(&item_full[k & 3]);
+        if (it < 0) break;
         const int b = it / Hkv, h = it - b * Hkv;
         const int np = (seq_lens[b] + kPage - 1) / kPage;
         const int* bt = block_table + (size_t)b * max_pages;
         for (int p = 0; p < np; ++p) {
           mbar_wait(&empty[stage], phase ^ 1);
+          gqa_trace(0, gp++);  // 0: stage free, page load issued
           const size_t blk = ((size_t)bt[p] * Hkv + h) * S::kTileElems;
           uint8_t* dst = ring + stage * S::kStageBytes;
           mbar_arrive_expect_tx(&full[stage], S::kStageBytes);
@@ -112,11 +145,15 @@ decode_attn_gqa_kernel(const __nv_bfloat16* __restrict__ q,       // [B, Hkv*G, 
   // ------------------------------ consumers (warps 0..3) ------------------------------
   const int g = lane >> 2, t = lane & 3;   // mma fragment coordinates
   const bool row_ok = g < G;
-  int stage = 0;
+  int stage = 0, gc = 0, item = 0;
   uint32_t phase = 0;
-  for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+  for (;; ++item) {
+    mbar_wait(&item_full[item & 3], (item >> 2) & 1);
+    const int it = s_item[item & 3];
+    if (it < 0) break;
     const int b = it / Hkv, h = it - b * Hkv;
     const int len = seq_lens[b];
+    if (threadIdx.x == 0) gqa_trace(4, item);  // 4: item start (consumers)
     const int np = (len + kPage - 1) / kPage;
     // Q A-fragments (rows = the G query heads of this kv head; rows >= G are zero)
     uint32_t qa[KSTEPS][2];
@@ -131,8 +168,9 @@ decode_attn_gqa_kernel(const __nv_bfloat16* __restrict__ q,       // [B, Hkv*G, 
     for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
     float m_run = -INFINITY, l_run = 0.f;
 
-    for (int p = 0; p < np; ++p) {
+    for (int p = 0; p < np; ++p, ++gc) {
       mbar_wait(&full[stage], phase);
+      if (threadIdx.x == 0) gqa_trace(1, gc);  // 1: page landed at consumer warp 0
       const uint32_t kbase = smem_u32(ring + stage * S::kStageBytes);
       const uint32_t vbase = kbase + S::kTileBytes;
       const int tok0 = warp * 16;  // this warp's 16 tokens of the page
@@ -199,10 +237,12 @@ decode_attn_gqa_kernel(const __nv_bfloat16* __restrict__ q,       // [B, Hkv*G, 
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[stage]);
+      if (threadIdx.x == 0) gqa_trace(2, gc);  // 2: page released by consumer warp 0
       if (++stage == kAttnStages) { stage = 0; phase ^= 1; }
     }
 
     // ---- merge the 4 warps' partial (m, l, O) and store ----
+    if (threadIdx.x == 0) gqa_trace(5, item);  // 5: merge start
     l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
     l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
     constexpr int MS = S::kMergeStride;
@@ -236,12 +276,22 @@ decode_attn_gqa_kernel(const __nv_bfloat16* __restrict__ q,       // [B, Hkv*G, 
       out[((size_t)b * Hkv * G + (size_t)h * G + row) * HD + col] = __float2bfloat16_rn(den > 0.f ? num / den : 0.f);
     }
     named_bar_sync(1, kConsumerWarps * 32);  // merge buffer reused by the next item
+    if (lane == 0) mbar_arrive(&item_empty[item & 3]);
+    if (threadIdx.x == 0) gqa_trace(6, item);  // 6: merge done
+  }
+  // the last CTA out (all grabs of every CTA done) resets the scheduler for the next launch
+  if (sched && threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(sched + 1, 1) == (int)gridDim.x - 1) {
+      sched[0] = 0;
+      sched[1] = 0;
+    }
   }
 }
 
 template <int HD, int G>
 int launch_gqa(const void* q, const void* kc, const void* vc, const int* bt, int max_pages, const int* lens, int B,
-               int Hkv, float scale, void* out, cudaStream_t st) {
+               int Hkv, float scale, void* out, cudaStream_t st, int* sched) {
   using S = GqaSmem<HD, G>;
   if (const int rc = mgb_host::ensure_max_smem((const void*)decode_attn_gqa_kernel<HD, G>, (int)S::kBytes)) return rc;
   const int items = B * Hkv;
@@ -250,7 +300,7 @@ int launch_gqa(const void* q, const void* kc, const void* vc, const int* bt, int
   decode_attn_gqa_kernel<HD, G><<<grid, kAttnThreads, S::kBytes, st>>>(
       reinterpret_cast<const __nv_bfloat16*>(q), reinterpret_cast<const __nv_bfloat16*>(kc),
       reinterpret_cast<const __nv_bfloat16*>(vc), bt, max_pages, lens, B, Hkv, scale * 1.4426950408889634f,
-      reinterpret_cast<__nv_bfloat16*>(out));
+      reinterpret_cast<__nv_bfloat16*>(out), sched);
   return mgb_host::launch_status();
 }
 
@@ -260,16 +310,39 @@ extern "C" {
 
 int mgb_kv_page_size(void) { return mgb::kPage; }
 
+// Copy the GQA trace buffer (MGB_GQA_TRACE builds) to host_out[8 * 512]; MGB_EINVAL otherwise.
+int mgb_gqa_trace_read(unsigned long long* host_out) {
+#ifdef MGB_GQA_TRACE
+  return cudaMemcpyFromSymbol(host_out, mgb::g_gqa_trace, sizeof(mgb::g_gqa_trace)) == cudaSuccess ? MGB_OK : MGB_ECUDA;
+#else
+  (void)host_out;
+  return MGB_EINVAL;
+#endif
+}
+
 // Decode attention for B sequences, one new query token each (already RoPE'd and appended to
 // the cache by mgb_rope_append_gqa).  seq_lens[b] counts the cached tokens including the new one.
+int mgb_decode_attn_gqa_sched(const void* q, const void* k_cache, const void* v_cache, const int* block_table,
+                              int max_pages, const int* seq_lens, int B, int Hq, int Hkv, int head_dim, float scale,
+                              void* out, int* sched, void* stream);
+
 int mgb_decode_attn_gqa(const void* q, const void* k_cache, const void* v_cache, const int* block_table,
                         int max_pages, const int* seq_lens, int B, int Hq, int Hkv, int head_dim, float scale,
                         void* out, void* stream) {
+  return mgb_decode_attn_gqa_sched(q, k_cache, v_cache, block_table, max_pages, seq_lens, B, Hq, Hkv, head_dim, scale,
+                                   out, nullptr, stream);
+}
+
+// Same, with dynamic item scheduling through `sched` (2 ints, zero before the first launch and left
+// zero by every launch; one per stream).
+int mgb_decode_attn_gqa_sched(const void* q, const void* k_cache, const void* v_cache, const int* block_table,
+                              int max_pages, const int* seq_lens, int B, int Hq, int Hkv, int head_dim, float scale,
+                              void* out, int* sched, void* stream) {
   if (B < 1 || Hkv < 1 || Hq % Hkv) return MGB_EINVAL;
   const int G = Hq / Hkv;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
 #define MGB_GQA_CASE(HD_, G_) \
-  if (head_dim == HD_ && G == G_) return mgb::launch_gqa<HD_, G_>(q, k_cache, v_cache, block_table, max_pages, seq_lens, B, Hkv, scale, out, st);
+  if (head_dim == HD_ && G == G_) return mgb::launch_gqa<HD_, G_>(q, k_cache, v_cache, block_table, max_pages, seq_lens, B, Hkv, scale, out, st, sched);
   MGB_GQA_CASE(128, 4)
   MGB_GQA_CASE(128, 6)
   MGB_GQA_CASE(128, 8)

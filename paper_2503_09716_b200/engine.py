@@ -288,6 +288,9 @@ class Engine:
         # completion counters of the fused expert FFN launch (mgb_moe_ffn); every launch of this engine
         # runs on its compute stream, one after another, and leaves them zero
         self.ffn_sync = torch.zeros(257, dtype=torch.int32, device=device)
+        # dynamic work-item counter of the GQA decode attention launches (all on the compute stream)
+        self.attn_sched = (torch.zeros(2, dtype=torch.int32, device=device)
+                           if os.environ.get("MGB_ATTN_SCHED", "1") != "0" else None)
         ffn_env = os.environ.get("MGB_FFN_FUSED")
         self._ffn_fused = None if ffn_env is None else ffn_env != "0"
         self._dense_mlp_cublas = os.environ.get("MGB_DENSE_MLP", "gemm") == "cublas"
@@ -808,7 +811,7 @@ class Engine:
             s0, s1 = self._mb_range(j)
             (kc, vc), table = self._kv_views(l, j, s0, s1, "attend")
             ops.decode_attn_gqa(b.q[s0:s1], kc, vc, table[:s1 - s0], b.seq_lens[s0:s1], Hq, Hkv, hd,
-                                b.attn[s0:s1])
+                                b.attn[s0:s1], sched=self.attn_sched)
         elif j.kind == "post_attention":
             torch.mm(b.attn, W["wo"].t(), out=b.o)
             if not self._route_fused(l):  # else the router job's fused kernel adds + normalises

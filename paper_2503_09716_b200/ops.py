@@ -170,11 +170,17 @@ def rope_append_gqa(qkv: torch.Tensor, seq0: int, positions: torch.Tensor, cos_t
 
 def decode_attn_gqa(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor, block_table: torch.Tensor,
                     seq_lens: torch.Tensor, Hq: int, Hkv: int, hd: int, out: torch.Tensor,
-                    scale: float | None = None) -> None:
+                    scale: float | None = None, sched: torch.Tensor | None = None) -> None:
+    """sched: int32 [2] zeros (reused; launches sharing it must be stream-ordered) -> dynamic item
+    scheduling across the persistent CTAs; None -> the static round-robin share."""
     B = q.shape[0]
     scale = hd ** -0.5 if scale is None else scale
-    nat.call("mgb_decode_attn_gqa", _p(q), _p(k_cache), _p(v_cache), _p(block_table), block_table.shape[1],
-             _p(seq_lens), B, Hq, Hkv, hd, scale, _p(out), _s())
+    if sched is None:
+        nat.call("mgb_decode_attn_gqa", _p(q), _p(k_cache), _p(v_cache), _p(block_table), block_table.shape[1],
+                 _p(seq_lens), B, Hq, Hkv, hd, scale, _p(out), _s())
+    else:
+        nat.call("mgb_decode_attn_gqa_sched", _p(q), _p(k_cache), _p(v_cache), _p(block_table), block_table.shape[1],
+                 _p(seq_lens), B, Hq, Hkv, hd, scale, _p(out), _p(sched), _s())
 
 
 def prefill_attn_supported(hd_qk: int, hd_v: int) -> bool:

@@ -206,6 +206,30 @@ def test_decode_attn_gqa(B, Hq, Hkv, hd, ctx, tail):
     assert R.rel_err(out.cpu(), eager) <= 2e-2
 
 
+@pytest.mark.parametrize("B,ctx", [(3, 200), (600, 70), (2000, 33)])
+def test_decode_attn_gqa_dynamic_schedule(B, ctx):
+    """Dynamic item scheduling (mgb_decode_attn_gqa_sched) gives the static kernel's output bit for bit
+    (every item is computed the same way, only its CTA changes) and leaves its counters at zero."""
+    ops = _ops()
+    Hq, Hkv, hd = 32, 8, 128
+    page = ops.kv_page_size()
+    pps = math.ceil(ctx / page)
+    q = uniform_bf16((B, Hq, hd), 6, 1, 1.0).cuda()
+    kp = uniform_bf16((B * pps * Hkv * hd * page,), 6, 2, 1.0).cuda()
+    vp = uniform_bf16((B * pps * Hkv * hd * page,), 6, 3, 1.0).cuda()
+    bt = torch.arange(B * pps, dtype=torch.int32, device="cuda").view(B, pps)
+    lens = torch.randint(1, ctx + 1, (B,), generator=torch.Generator().manual_seed(B)).int().cuda()
+    ref = torch.zeros(B, Hq * hd, dtype=BF16, device="cuda")
+    ops.decode_attn_gqa(q, kp, vp, bt, lens, Hq, Hkv, hd, ref)
+    sched = torch.zeros(2, dtype=torch.int32, device="cuda")
+    for _ in range(3):
+        out = torch.zeros_like(ref)
+        ops.decode_attn_gqa(q, kp, vp, bt, lens, Hq, Hkv, hd, out, sched=sched)
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref)
+        assert int(sched.abs().sum()) == 0
+
+
 def test_rope_append_matches_oracle():
     ops = _ops()
     B, Hq, Hkv, hd, pos = 3, 8, 2, 32, 70
