@@ -108,6 +108,8 @@ class _Lib:
             _build.build(verbose=False)
         lib = ctypes.CDLL(str(path), mode=ctypes.RTLD_GLOBAL)
         for name, args in SIGNATURES.items():
+            if "MGB_LIB" in os.environ and not hasattr(lib, name):
+                continue  # an A/B variant build (tools/build_variant.py) of an older tree
             fn = getattr(lib, name)
             fn.argtypes = args
             fn.restype = ctypes.c_int
