@@ -14,7 +14,7 @@ from paper_2503_09716_b200.engine import Engine, resident_plan  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="mixtral-8x7b")
 ap.add_argument("--prompt-len", type=int, default=512)
-ap.add_argument("--chunk-tokens", type=int, default=32768)
+ap.add_argument("--chunk-tokens", type=int, default=None, help="default: the engine's choice")
 ap.add_argument("--reserve-gb", type=int, default=14)
 args = ap.parse_args()
 arch = get_arch(args.config)
