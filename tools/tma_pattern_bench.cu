@@ -99,11 +99,10 @@ int main() {
   cudaFuncSetAttribute(stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   struct Case { int mode, b_rows, hold, box, spread; const char* what; };
   const Case cases[] = {{0, 0, 0, 8, 1, "A only"},
-                        {0, 104, 0, 16, 8, "A + B 16-row x6, 8 slices"},
                         {0, 104, 0, 3, 8, "A + B 64+32+8, 8 slices"},
-                        {0, 104, 0, 104, 8, "A + B one 104-row box, 8 slices"},
-                        {1, 104, 0, 104, 8, "K-blocked A + one 104-row B box"},
-                        {1, 104, 0, 3, 8, "K-blocked A + B 64+32+8"}};
+                        {0, 104, 200, 3, 8, "A + B 64+32+8, 200 ns hold"},
+                        {0, 104, 300, 3, 8, "A + B 64+32+8, 300 ns hold"},
+                        {0, 104, 400, 3, 8, "A + B 64+32+8, 400 ns hold"}};
   for (const Case& c : cases) {
     const int mode = c.mode;
     CUtensorMap tm;
