@@ -89,6 +89,18 @@ struct UnitSched {
   }
 };
 
+// Wait-time accounting of the fused FFN kernel (build with -DMGB_GEMM_TRACE; tools/ffn_trace.py):
+// g_ffn_trace[cta][i] = cycles spent in: 0 producer empty waits, 1 MMA full waits, 2 MMA TMEM-empty
+// waits, 3 epilogue TMEM-full waits (warp 2), 4 producer dependency waits, 5 kernel cycles (thread 0)
+#ifdef MGB_GEMM_TRACE
+__device__ long long g_ffn_trace[256][8];
+#define FFN_T0() const long long _t0 = clock64()
+#define FFN_ACC(i) g_ffn_trace[blockIdx.x][i] += clock64() - _t0
+#else
+#define FFN_T0()
+#define FFN_ACC(i)
+#endif
+
 MGB_DEVINL int ld_acquire_gpu_s32(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -610,6 +622,9 @@ moe_ffn_pair_kernel(const __grid_constant__ CUtensorMap tmAg, const __grid_const
   const int total_gu = s_pgu[E];
   const int total = total_gu + s_pdn[E];
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+#ifdef MGB_GEMM_TRACE
+  const long long _kt0 = clock64();
+#endif
 
   if (warp == 0) {
     // ------------------------------ TMA producer (both CTAs) ------------------------------
@@ -627,7 +642,11 @@ moe_ffn_pair_kernel(const __grid_constant__ CUtensorMap tmAg, const __grid_const
         const BMaps& tB = gated ? tmBx : tmBh;
         if (!gated) {  // h rows of expert e: every gate/up unit of e has stored and counted them
           const int need = s_need[e];
-          while (ld_acquire_gpu_s32(done + e) < need) __nanosleep(64);
+          {
+            FFN_T0();
+            while (ld_acquire_gpu_s32(done + e) < need) __nanosleep(64);
+            FFN_ACC(4);
+          }
           asm volatile("fence.proxy.async.global;" ::: "memory");
         }
         const int rows_cta = gated ? kBM / 2 : kBM;
@@ -638,7 +657,7 @@ moe_ffn_pair_kernel(const __grid_constant__ CUtensorMap tmAg, const __grid_const
         const int arow0 = e * G.rows_per_expert + mt * 2 * rows_cta + rank * rows_cta;
         const int trow0 = tok0 + rank * half;
         for (int kb = 0; kb < G.KB; ++kb) {
-          mbar_wait(&empty_bar[stage], phase ^ 1);
+          { FFN_T0(); mbar_wait(&empty_bar[stage], phase ^ 1); FFN_ACC(0); }
           if (leader) mbar_arrive_expect_tx(&full_bar[stage], bytes);
           uint8_t* st = tiles + stage * kPStageBytes;
           if (gated) {
@@ -666,11 +685,11 @@ moe_ffn_pair_kernel(const __grid_constant__ CUtensorMap tmAg, const __grid_const
         const int KB = gated ? gu.KB : dn.KB;
         const uint32_t N = (uint32_t)((n + nalign - 1) & ~(nalign - 1));
         const uint32_t idesc = make_idesc_bf16(2 * kBM, N);
-        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        { FFN_T0(); mbar_wait(&tempty_bar[acc], acc_phase ^ 1); FFN_ACC(2); }
         tc_fence_after();
         const uint32_t d0 = tmem_base + acc * kBNMax;
         for (int kb = 0; kb < KB; ++kb) {
-          mbar_wait(&full_bar[stage], phase);
+          { FFN_T0(); mbar_wait(&full_bar[stage], phase); FFN_ACC(1); }
           tc_fence_after();
           const uint32_t st = smem_u32(tiles + stage * kPStageBytes);
           const uint64_t a0 = make_sdesc_sw128(st);
@@ -698,6 +717,7 @@ moe_ffn_pair_kernel(const __grid_constant__ CUtensorMap tmAg, const __grid_const
       bool gated;
       int e, mt, tok0, n;
       ffn_decode(u, total_gu, s_pgu, s_pdn, E, offsets, gu, dn, gated, e, mt, tok0, n);
+      if (warp == 2 && lane == 0) { FFN_T0(); mbar_wait(&tfull_bar[acc], acc_phase); FFN_ACC(3); }
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t tl = tmem_base + ((q * 32) << 16) + acc * kBNMax;
@@ -735,6 +755,9 @@ moe_ffn_pair_kernel(const __grid_constant__ CUtensorMap tmAg, const __grid_const
   __syncthreads();
   cluster_sync();
   if (warp == 1) tmem_dealloc_pair<512>(tmem_base);
+#ifdef MGB_GEMM_TRACE
+  if (threadIdx.x == 0) g_ffn_trace[blockIdx.x][5] = clock64() - _kt0;
+#endif
   // the last CTA out resets the per-expert counters (and the exit ticket) for the next launch
   if (threadIdx.x == 0) {
     __threadfence();
@@ -867,6 +890,18 @@ int mgb_moe_gemm_down_ep(const void* w_down, const void* h, const int* offsets, 
   if (E < 1 || E > mgb::kMaxExperts || f % mgb::kBK || d % mgb::kBM || rows_cap < 1 || !row_ptr) return MGB_EINVAL;
   return launch_moe_gemm<false>(w_down, E * d, h, rows_cap, offsets, E, d / mgb::kBM, f, d, 0, nullptr, d,
                                 reinterpret_cast<cudaStream_t>(stream), row_ptr);
+}
+
+// Trace read-out (MGB_GEMM_TRACE builds): copies g_ffn_trace [256][8] cycles and zeroes it.
+int mgb_ffn_trace_read(long long* host_out) {
+#ifdef MGB_GEMM_TRACE
+  if (cudaMemcpyFromSymbol(host_out, mgb::g_ffn_trace, sizeof(mgb::g_ffn_trace)) != cudaSuccess) return MGB_ECUDA;
+  static long long zero[256][8] = {};
+  return cudaMemcpyToSymbol(mgb::g_ffn_trace, zero, sizeof(zero)) == cudaSuccess ? MGB_OK : MGB_ECUDA;
+#else
+  (void)host_out;
+  return MGB_EINVAL;
+#endif
 }
 
 // The whole expert FFN (gate/up + SiLU*up + down) as ONE persistent CTA-pair launch (moe_ffn_pair_kernel):
