@@ -398,6 +398,9 @@ moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
   UnitSched sched{s_prefix, E, MT, balanced};
   const int KB = K / kBK;
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+#ifdef MGB_GEMM_TRACE
+  const long long _kt0 = clock64();
+#endif
 
   if (warp == 0) {
     // ------------------------------ TMA producer (both CTAs) ------------------------------
@@ -418,7 +421,7 @@ moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
         const int arow0 = e * rows_per_expert + mt * 2 * kRowsPerCta + rank * kRowsPerCta;
         const int trow0 = tok0 + rank * half;
         for (int kb = 0; kb < KB; ++kb) {
-          mbar_wait(&empty_bar[stage], phase ^ 1);
+          { FFN_T0(); mbar_wait(&empty_bar[stage], phase ^ 1); FFN_ACC(0); }
           if (leader) mbar_arrive_expect_tx(&full_bar[stage], bytes);
           uint8_t* st = tiles + stage * kPStageBytes;
           if (GATED) {
@@ -444,11 +447,11 @@ moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
         sched.decode(u, offsets, e, nt, mt, tok0, n);
         const uint32_t N = (uint32_t)((n + nalign - 1) & ~(nalign - 1));
         const uint32_t idesc = make_idesc_bf16(2 * kBM, N);
-        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        { FFN_T0(); mbar_wait(&tempty_bar[acc], acc_phase ^ 1); FFN_ACC(2); }
         tc_fence_after();
         const uint32_t d0 = tmem_base + acc * kBNMax;
         for (int kb = 0; kb < KB; ++kb) {
-          mbar_wait(&full_bar[stage], phase);
+          { FFN_T0(); mbar_wait(&full_bar[stage], phase); FFN_ACC(1); }
           tc_fence_after();
           const uint32_t st = smem_u32(tiles + stage * kPStageBytes);
           const uint64_t a0 = make_sdesc_sw128(st);
@@ -475,6 +478,7 @@ moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
     for (int u = pair; u < total; u += npairs) {
       int e, nt, mt, tok0, n;
       sched.decode(u, offsets, e, nt, mt, tok0, n);
+      if (warp == 2 && lane == 0) { FFN_T0(); mbar_wait(&tfull_bar[acc], acc_phase); FFN_ACC(3); }
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t tl = tmem_base + ((q * 32) << 16) + acc * kBNMax;
@@ -516,6 +520,9 @@ moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
   __syncthreads();
   cluster_sync();
   if (warp == 1) tmem_dealloc_pair<512>(tmem_base);
+#ifdef MGB_GEMM_TRACE
+  if (threadIdx.x == 0) g_ffn_trace[blockIdx.x][5] = clock64() - _kt0;
+#endif
 }
 
 // ------------------------------------------------------------------------------------------

@@ -14,7 +14,12 @@ from paper_2503_09716_b200 import _native as nat  # noqa: E402
 from paper_2503_09716_b200 import ops  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 207
-E, d, f = 8, 4096, 14336
+cfg = sys.argv[2] if len(sys.argv) > 2 else "mixtral-8x7b"  # deepseek-v2-lite: the two grouped launches
+from paper_2503_09716_b200.configs import get_arch  # noqa: E402
+
+_a = get_arch(cfg)
+E, d, f = _a.n_experts, _a.hidden, _a.moe_ffn
+fused = E <= 16
 bf = torch.bfloat16
 wgu = (torch.randn(E, 2 * f, d, device="cuda") * 0.02).to(bf)
 wd = (torch.randn(E, d, f, device="cuda") * 0.02).to(bf)
@@ -26,11 +31,21 @@ offs = torch.arange(0, T + 1, n, dtype=torch.int32, device="cuda")
 sync = torch.zeros(257, dtype=torch.int32, device="cuda")
 lib = nat.LIB.load()
 buf = (ctypes.c_longlong * (256 * 8))()
+def run(which):
+    if fused:
+        ops.moe_ffn(wgu, wd, x, offs, h, y, sync)
+    elif which == "gate_up":
+        ops.moe_gemm_gate_up(wgu, x, offs, h)
+    else:
+        ops.moe_gemm_down(wd, h, offs, y)
+
+
+which = sys.argv[3] if len(sys.argv) > 3 else "gate_up"
 for _ in range(3):
-    ops.moe_ffn(wgu, wd, x, offs, h, y, sync)
+    run(which)
 torch.cuda.synchronize()
 lib.mgb_ffn_trace_read(buf)
-ops.moe_ffn(wgu, wd, x, offs, h, y, sync)
+run(which)
 torch.cuda.synchronize()
 assert lib.mgb_ffn_trace_read(buf) == 0
 rows = [[buf[c * 8 + i] for i in range(8)] for c in range(148)]
