@@ -470,10 +470,15 @@ def measure(args, arch, dist, rank, world, steps: int, warmup: int, main: bool, 
     if a.family == "deepseek_v2":
         attn_name, attn_bytes = "decode_attn_mla", B * ctx_bd * (a.kv_lora_rank + a.qk_rope_dim) * 2
     else:
-        attn_name, attn_bytes = "decode_attn_gqa", B * ctx_bd * a.n_kv_heads * a.head_dim * 2 * 2
+        attn_name = "decode_attn_gqa_sched" if "decode_attn_gqa_sched" in bd else "decode_attn_gqa"
+        attn_bytes = B * ctx_bd * a.n_kv_heads * a.head_dim * 2 * 2
     shared = 2 if a.family == "deepseek_v2" else 0  # shared-expert rows read by the combine
     algo = {"router_topk": T * E * 4 + T * k * 12, "permute": T * d * 2 + T * k * d * 2,
-            "unpermute_combine": T * k * d * 2 + T * d * 2 * (3 + (1 if shared else 0)), attn_name: attn_bytes}
+            "unpermute_combine": T * k * d * 2 + T * d * 2 * (3 + (1 if shared else 0)), attn_name: attn_bytes,
+            # fused residual add + RMSNorm + router + top-k + permute (route.cu): x and the attention
+            # delta in, x_out and h out, router and norm weights, the k permuted copies of h, routing
+            # records (topk idx/weight, dst_pos, src_token)
+            "moe_route": T * d * 2 * 4 + (E + 1) * d * 2 + T * k * d * 2 + T * k * 16}
     kernel_hbm = {}
     for name, nbytes in algo.items():
         if name in bd:
