@@ -15,6 +15,16 @@ on one decoder layer of the model, and timed with CUDA events (median of `reps` 
 
 The result is a profile document in the reference's schema (hw_profile.py:156-249, ingestible by
 its `ingest_profile`), with the machine's capacities and measured link/HBM rates.
+
+Peak memory per module ("latency and peak memory usage for each module ...
+measured using the torch memory stats related APIs") rides in the same document under
+`memory_tables` (`ingest_profile` reads only `hardware` and `latency_tables`, so the document stays
+ingestible): entries `[tokens, context, bytes]` = the engine's own activation buffers that module
+reads or writes for `tokens` rows (sizes taken from the allocated tensors) plus the transient peak
+the torch allocator records across the job (`max_memory_allocated` above the pre-call level).
+`activation_coefficients` fits the reference's three per-token memory-model coefficients
+(model_catalog.py:82-84, memory_model.py:201-213) from those tables, so the planner's memory
+constraint can run on measured rather than assumed activation sizes.
 """
 
 from __future__ import annotations
@@ -48,6 +58,72 @@ def _time(fn, reps: int) -> float:
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1) * 1e-3)
     return statistics.median(ts)
+
+
+def _transient_peak(fn) -> int:
+    """Bytes the torch allocator holds above its pre-call level at the peak of one call of fn."""
+    torch.cuda.synchronize()
+    base = torch.cuda.memory_allocated()
+    torch.cuda.reset_peak_memory_stats()
+    fn()
+    torch.cuda.synchronize()
+    return max(0, torch.cuda.max_memory_allocated() - base)
+
+
+def _per_row(t: torch.Tensor, rows: int) -> int:
+    return t.numel() * t.element_size() // rows
+
+
+def module_row_bytes(eng) -> dict[str, int]:
+    """Activation bytes per token row of each module kind: the engine buffers the module's job reads
+    or writes (engine.py _issue_job / _ds_job), sized from the tensors the engine allocated.  The
+    resident hidden state x is excluded (the reference charges it separately as hidden residency,
+    memory_model.py:207); `expert` is per routed row (x_perm in, h_ffn, y_perm out)."""
+    b, B = eng.buf, eng.B
+    rw = eng.rws
+    router = [b.h, eng.logits_r]
+    per_tok = lambda ts: sum(_per_row(t, B) for t in ts)  # noqa: E731
+    out = {"router": per_tok(router + [rw.topk_idx, rw.topk_w, rw.local_rank, rw.src_token, rw.dst_pos])
+           + _per_row(b.x_perm, B)}
+    if eng.mla:
+        m = eng.mb
+        pre = [b.h, m["q"], m["ckv"], m["q_nope"], m["q_pe"], m["q_lat"]] + [m[n] for n in ("q_a", "q_an") if n in m]
+        out["pre_attention"] = per_tok(pre)
+        out["attention_mechanism_gpu"] = per_tok([m["q_lat"], m["q_pe"], m["o_lat"]])
+        out["post_attention"] = per_tok([m["o_lat"], m["o_cat"], b.o, b.h, m["sh_h"], m["sh_out"]])
+    else:
+        out["pre_attention"] = per_tok([b.h, b.qkv, b.q])
+        out["attention_mechanism_gpu"] = per_tok([b.q, b.attn])
+        out["post_attention"] = per_tok([b.attn, b.o, b.h])
+    rows = b.x_perm.shape[0]
+    out["expert"] = sum(_per_row(t, rows) for t in (b.x_perm, b.h_ffn, b.y_perm))
+    return out
+
+
+def activation_coefficients(doc: dict) -> dict[str, float]:
+    """The reference memory model's per-token activation coefficients (ModelSpec fields,
+    model_catalog.py:82-84; used by memory_model.intermediate_bytes) fitted to a profile's
+    `memory_tables`: the attention coefficient is the largest per-token slope of the three attention
+    modules (the reference charges the peak per-kernel activation), the context coefficient the
+    attention module's slope over context per sequence, the expert coefficient the expert module's
+    slope per routed row.  Merge the result into a model-spec document to plan on measured sizes."""
+    tabs = {t["module_kind"]: t["entries"] for t in doc["memory_tables"]}
+
+    def slope(entries, ctx=None):
+        es = sorted((e for e in entries if ctx is None or e[1] == ctx), key=lambda e: e[0])
+        (t0, _, b0), (t1, _, b1) = es[0], es[-1]
+        return (b1 - b0) / (t1 - t0) if t1 > t0 else b1 / max(t1, 1)
+
+    attn = tabs["attention_mechanism_gpu"]
+    ctxs = sorted({e[1] for e in attn})
+    per_tok = max(slope(tabs["pre_attention"]), slope(tabs["post_attention"]), slope(attn, ctxs[0]))
+    Tmax = max(e[0] for e in attn)
+    at_t = sorted((e for e in attn if e[0] == Tmax), key=lambda e: e[1])
+    per_ctx = 0.0
+    if len(at_t) > 1 and at_t[-1][1] > at_t[0][1]:
+        per_ctx = max(0.0, (at_t[-1][2] - at_t[0][2]) / ((at_t[-1][1] - at_t[0][1]) * Tmax))
+    return {"attn_activation_bytes_per_token": float(per_tok), "attn_activation_bytes_per_ctx_token": per_ctx,
+            "expert_activation_bytes_per_token": float(slope(tabs["expert"]))}
 
 
 def measure_links(nbytes: int = 1 << 30, reps: int = 5) -> tuple[float, float]:
@@ -160,14 +236,20 @@ def profile_engine(arch: ModelArch | str, token_grid: Sequence[int] | None = Non
     g = torch.Generator(device="cuda").manual_seed(0)
     tables: dict[str, list] = {k: [] for k in ("pre_attention", "attention_mechanism_gpu", "post_attention",
                                                "router", "expert")}
+    mem: dict[str, list] = {k: [] for k in tables}
+    row_bytes = module_row_bytes(eng)
     from .schedule import Job
+
+    def timed(kind: str, T: int, fn, ctx: int = 0) -> None:
+        tables[kind].append([T, ctx, _time(fn, reps)])
+        mem[kind].append([T, ctx, T * row_bytes[kind] + _transient_peak(fn)])
 
     def job(kind: str, T: int):
         return Job(0, kind, "gpu_compute", 0.0, f"L{l}/{kind}/mb0", layer=l, tokens=T, seqs=T)
 
     for T in token_grid:
         # pre-attention: exactly the engine's job on micro-batch [0, T)
-        tables["pre_attention"].append([T, 0, _time(lambda: eng._issue_job(l, job("pre_attention", T)), reps)])
+        timed("pre_attention", T, lambda: eng._issue_job(l, job("pre_attention", T)))
         # post-attention on T tokens (O projection + residual/norm [+ shared experts])
         if eng.mla:
             m = eng.mb
@@ -180,7 +262,7 @@ def profile_engine(arch: ModelArch | str, token_grid: Sequence[int] | None = Non
             def post():
                 torch.mm(b.attn[:T], W["wo"].t(), out=b.o[:T])
                 ops.add_rmsnorm(b.x[:T], W["ln2"], a.rms_eps, b.h[:T], delta=b.o[:T], x_out=b.x[:T])
-        tables["post_attention"].append([T, 0, _time(post, reps)])
+        timed("post_attention", T, post)
         # router on T tokens: logits GEMM + fused top-k + stable permutation
         ws = ops.RouterWorkspace(T, a.n_experts, a.top_k)
         logits = torch.empty(T, a.n_experts, dtype=torch.float32, device="cuda")
@@ -191,7 +273,7 @@ def profile_engine(arch: ModelArch | str, token_grid: Sequence[int] | None = Non
             ops.router_topk(None, None, ws, a.top_k, a.router_mode, a.routed_scaling, a.n_group, a.topk_group,
                             logits_in=logits)
             ops.permute(b.h[:T], ws, xp)
-        tables["router"].append([T, 0, _time(route, reps)])
+        timed("router", T, route)
         # one expert with T rows (the EXPERT_COMPUTE chunk): gate/up+SiLU then down
         rows = max(T, 1)
         x = torch.randn(rows, d, generator=g, device="cuda").to(BF16)
@@ -203,7 +285,7 @@ def profile_engine(arch: ModelArch | str, token_grid: Sequence[int] | None = Non
         def expert():
             ops.moe_gemm_gate_up(gu, x, offs, h)
             ops.moe_gemm_down(dn, h, offs, y)
-        tables["expert"].append([T, 0, _time(expert, reps)])
+        timed("expert", T, expert)
         # attention over `ctx` keys for T sequences
         for ctx in ctx_grid:
             b.seq_lens[:T].fill_(ctx)
@@ -220,7 +302,7 @@ def profile_engine(arch: ModelArch | str, token_grid: Sequence[int] | None = Non
                 def attn():
                     ops.decode_attn_gqa(b.q[:T], eng.k_cache[l], eng.v_cache[l], eng.block_table[:T],
                                         b.seq_lens[:T], a.n_heads, a.n_kv_heads, a.head_dim, b.attn[:T])
-            tables["attention_mechanism_gpu"].append([T, ctx, _time(attn, reps)])
+            timed("attention_mechanism_gpu", T, attn, ctx)
     del eng
     torch.cuda.empty_cache()
     cpu_rate = 0.0
@@ -235,4 +317,7 @@ def profile_engine(arch: ModelArch | str, token_grid: Sequence[int] | None = Non
     hw = hardware or measured_hardware()
     if cpu_rate > 0:
         hw = Hardware(**{**hw.__dict__, "cpu_attn_flops": cpu_rate})
-    return profile_document(hw, curves)
+    doc = profile_document(hw, curves)
+    doc["memory_tables"] = [{"module_kind": k, "entries": v} for k, v in mem.items()]
+    doc["activation_coefficients"] = activation_coefficients(doc)
+    return doc

@@ -106,3 +106,34 @@ def test_measured_profile_feeds_search(name):
                         s_params_fracs=(0.0, 1.0))
     best = search(spec, hw, latency_from_curves(curves), WorkloadSpec(64, 32, 10_000), space)
     assert best.throughput > 0
+    # per-module peak memory: every module kind, at every latency point, at least
+    # the engine buffers it touches; the expert module's fitted per-row bytes are its x_perm, h_ffn
+    # and y_perm rows (no transient allocation inside the grouped GEMMs)
+    mkinds = {t["module_kind"]: t["entries"] for t in doc["memory_tables"]}
+    assert set(mkinds) == kinds
+    for t in doc["latency_tables"]:
+        assert [e[:2] for e in mkinds[t["module_kind"]]] == [e[:2] for e in t["entries"]]
+        assert all(e[2] > 0 for e in mkinds[t["module_kind"]])
+    co = doc["activation_coefficients"]
+    assert co["expert_activation_bytes_per_token"] == 2 * (2 * arch.hidden + arch.moe_ffn)
+    assert co["attn_activation_bytes_per_token"] >= 2 * arch.hidden
+    assert co["attn_activation_bytes_per_ctx_token"] == 0.0  # paged kernels: nothing per context token
+    mspec = ModelSpec.from_document({**arch.model_spec_document(), **co})
+    assert search(mspec, hw, latency_from_curves(curves), WorkloadSpec(64, 32, 10_000), space).throughput > 0
+
+
+def test_activation_coefficients_fit():
+    """The fit of profiler.activation_coefficients on a hand-made memory table: slopes per token
+    (max over the attention modules), per context token per sequence, per routed expert row."""
+    from paper_2503_09716_b200.profiler import activation_coefficients
+
+    doc = {"memory_tables": [
+        {"module_kind": "pre_attention", "entries": [[1, 0, 100 + 10], [64, 0, 100 + 640]]},
+        {"module_kind": "post_attention", "entries": [[1, 0, 30], [64, 0, 30 * 64]]},
+        {"module_kind": "attention_mechanism_gpu",
+         "entries": [[1, 16, 8 + 16 * 2], [1, 64, 8 + 64 * 2], [64, 16, 64 * (8 + 16 * 2)], [64, 64, 64 * (8 + 64 * 2)]]},
+        {"module_kind": "router", "entries": [[1, 0, 5], [64, 0, 320]]},
+        {"module_kind": "expert", "entries": [[1, 0, 7 + 1000], [64, 0, 64 * 7 + 1000]]}]}
+    co = activation_coefficients(doc)
+    assert co == {"attn_activation_bytes_per_token": 40.0, "attn_activation_bytes_per_ctx_token": 2.0,
+                  "expert_activation_bytes_per_token": 7.0}

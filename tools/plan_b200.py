@@ -18,7 +18,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2503_09716_b200.configs import get_arch  # noqa: E402
 from paper_2503_09716_b200.engine import Engine  # noqa: E402
 from paper_2503_09716_b200.plan_search import SearchSpace, evaluate_plan, search  # noqa: E402
-from paper_2503_09716_b200.planner import Hardware, ModelSpec, WorkloadSpec, load_profile_document  # noqa: E402
+from paper_2503_09716_b200.planner import (Hardware, ModelSpec, WorkloadSpec, footprint,  # noqa: E402
+                                           load_profile_document)
 from paper_2503_09716_b200.profiler import profile_engine  # noqa: E402
 from paper_2503_09716_b200.schedule import latency_from_curves  # noqa: E402
 
@@ -31,6 +32,8 @@ ap.add_argument("--reserve-gb", type=float, default=12.0)
 ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--profile-in", default=None)
 ap.add_argument("--cpu-attention", action="store_true", help="profile the host-core attention and search omega")
+ap.add_argument("--measured-memory", action="store_true",
+                help="plan with the activation coefficients fitted to the profile's per-module memory tables")
 ap.add_argument("--out", default=None)
 args = ap.parse_args()
 
@@ -49,7 +52,10 @@ t_prof = time.time() - t0
 hw, curves = load_profile_document(prof)
 hw = Hardware(**{**hw.__dict__, "m_g": hw.m_g - int(args.reserve_gb * 2**30), "m_c": int(args.host_gb * 1e9)})
 lat = latency_from_curves(curves)
-spec = ModelSpec.from_document(arch.model_spec_document())
+spec_doc = arch.model_spec_document()
+if args.measured_memory and "activation_coefficients" in prof:
+    spec_doc = {**spec_doc, **prof["activation_coefficients"]}
+spec = ModelSpec.from_document(spec_doc)
 wl = WorkloadSpec(512, 256, 1_000_000, "decode")
 omegas = tuple(round(0.1 * i, 1) for i in range(9)) if args.cpu_attention else (0.0,)
 space = SearchSpace(b_a_grid=(64, 128, 256, 512, 1024), b_e_grid=(1024, 4096, 16384), omega_grid=omegas,
@@ -59,6 +65,9 @@ best = search(spec, hw, lat, wl, space, kv_policy=args.kv_policy)
 t_search = time.time() - t0
 plan = best.plan
 print("plan", plan, "predicted", best.t_forward, flush=True)
+torch.cuda.synchronize()
+mem0 = torch.cuda.memory_allocated()
+torch.cuda.reset_peak_memory_stats()
 eng = Engine(arch, plan, prompt_len=512, decode_len=256, use_graph=True, kv_policy=args.kv_policy)
 eng.synthetic_prefill()
 # the planner prices attention at the full context (max_context, offload_dag.py:353): time the last
@@ -75,6 +84,10 @@ for _ in range(args.steps):
 e1.record()
 torch.cuda.synchronize()
 t_meas = e0.elapsed_time(e1) * 1e-3 / args.steps
+# the GPU memory the run actually held (torch allocator peak, engine construction through the timed
+# steps) next to the memory model's Eq. 3 total for the same plan
+peak_gpu = torch.cuda.max_memory_allocated() - mem0
+fp = footprint(spec, hw, wl, plan, kv_policy=args.kv_policy)
 base = None
 if args.cpu_attention:  # the best all-GPU plan of the same search, for the omega > 0 gain
     base = search(spec, hw, lat, wl, dataclasses.replace(space, omega_grid=(0.0,)), kv_policy=args.kv_policy)
@@ -84,6 +97,8 @@ out = {"config": arch.name, "kv_policy": args.kv_policy, "plan": plan.to_documen
        "predicted_forward_s": best.t_forward, "measured_forward_s": t_meas,
        "predicted_tokens_per_s": best.throughput, "measured_tokens_per_s": plan.B / t_meas,
        "rel_err": (t_meas - best.t_forward) / best.t_forward,
+       "peak_gpu_bytes": peak_gpu, "model_gpu_bytes": fp.gpu_total, "model_s_is": fp.s_is,
+       "activation_coefficients": prof.get("activation_coefficients"), "measured_memory": args.measured_memory,
        "profile_s": t_prof, "search_s": t_search, "hardware": prof["hardware"]}
 print(json.dumps(out))
 if args.out:
