@@ -79,7 +79,8 @@ decode_attn_gqa_kernel(const __nv_bfloat16* __restrict__ q,       // [B, Hkv*G, 
                        const int* __restrict__ block_table, int max_pages,
                        const int* __restrict__ seq_lens, int B, int Hkv, float scale_log2,
                        __nv_bfloat16* __restrict__ out,            // [B, Hkv*G*HD]
-                       int* __restrict__ sched) {                  // optional {next item, exit ticket}
+                       int* __restrict__ sched) {  // optional {next item, exit ticket}
+  mgb::pdl_enter();
   static_assert(G <= 8 && HD % 16 == 0, "GQA tile: G <= 8 query heads per kv head");
   using S = GqaSmem<HD, G>;
   constexpr int KSTEPS = HD / 16;   // k-steps of QK^T
@@ -297,7 +298,7 @@ int launch_gqa(const void* q, const void* kc, const void* vc, const int* bt, int
   const int items = B * Hkv;
   int grid = 2 * mgb_host::num_sms();
   if (grid > items) grid = items;
-  decode_attn_gqa_kernel<HD, G><<<grid, kAttnThreads, S::kBytes, st>>>(
+  mgb_host::launch(decode_attn_gqa_kernel<HD, G>, dim3(grid), dim3(kAttnThreads), S::kBytes, st, nullptr,
       reinterpret_cast<const __nv_bfloat16*>(q), reinterpret_cast<const __nv_bfloat16*>(kc),
       reinterpret_cast<const __nv_bfloat16*>(vc), bt, max_pages, lens, B, Hkv, scale * 1.4426950408889634f,
       reinterpret_cast<__nv_bfloat16*>(out), sched);

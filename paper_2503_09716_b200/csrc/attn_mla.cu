@@ -158,6 +158,7 @@ decode_attn_mla_kernel(const __grid_constant__ CUtensorMap tm_qlat,  // q_lat [H
                        const int* __restrict__ block_table, int max_pages, const int* __restrict__ seq_lens,
                        int B, int H, float scale_log2, __nv_bfloat16* __restrict__ o_lat,  // [H, B, R]
                        int pf_dist, int cl) {
+  mgb::pdl_enter();
   using C = MlaCfg<R, RP>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* pages = smem;
@@ -618,12 +619,11 @@ int launch_mla(const void* q_lat, const void* q_pe, const void* cache, const int
     const __nv_bfloat16* cp = reinterpret_cast<const __nv_bfloat16*>(cache);
     __nv_bfloat16* op = reinterpret_cast<__nv_bfloat16*>(out);
     const float sl2 = scale * 1.4426950408889634f;
-    if (cudaLaunchKernelEx(&cfg, decode_attn_mla_kernel<R, RP>, tq, tp, cp, bt, max_pages, lens, B, H, sl2, op,
-                           pf_dist, cl) != cudaSuccess)
-      return mgb_host::launch_status(), MGB_ECUDA;
+    mgb_host::launch(decode_attn_mla_kernel<R, RP>, dim3(grid), dim3(kMlaThreads), C::kSmem, st, &attr[0], tq, tp,
+                     cp, bt, max_pages, lens, B, H, sl2, op, pf_dist, cl);
     return mgb_host::launch_status();
   }
-  decode_attn_mla_kernel<R, RP><<<grid, kMlaThreads, C::kSmem, st>>>(
+  mgb_host::launch(decode_attn_mla_kernel<R, RP>, dim3(grid), dim3(kMlaThreads), C::kSmem, st, nullptr,
       tq, tp, reinterpret_cast<const __nv_bfloat16*>(cache), bt, max_pages, lens, B, H, scale * 1.4426950408889634f,
       reinterpret_cast<__nv_bfloat16*>(out), pf_dist, 1);
   return mgb_host::launch_status();
@@ -639,6 +639,7 @@ __global__ void mla_append_kernel(const __nv_bfloat16* __restrict__ q,    // [B,
                                   const float* __restrict__ sin_t, const int* __restrict__ block_table, int max_pages,
                                   __nv_bfloat16* __restrict__ cache, __nv_bfloat16* __restrict__ q_nope_out,
                                   __nv_bfloat16* __restrict__ q_pe_out, int* __restrict__ seq_lens) {
+  mgb::pdl_enter();
   const int b = blockIdx.x;
   const int pos = positions[b];
   if (pos < 0 || pos >= max_pages * kMlaPage) return;  // past the planned context: no page to write
@@ -723,6 +724,7 @@ mla_append_warp_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16*
                        const float* __restrict__ sin_t, const int* __restrict__ block_table, int max_pages,
                        __nv_bfloat16* __restrict__ cache, __nv_bfloat16* __restrict__ q_nope_out,
                        __nv_bfloat16* __restrict__ q_pe_out, int* __restrict__ seq_lens) {
+  mgb::pdl_enter();
   const int lane = threadIdx.x & 31;
   const int b = blockIdx.x * kAppTok + (threadIdx.x >> 5);
   if (b >= B) return;
@@ -809,6 +811,7 @@ __global__ void mla_append_prefill_kernel(__nv_bfloat16* __restrict__ q, const _
                                           const float* __restrict__ sin_t, const int* __restrict__ block_table,
                                           int max_pages, __nv_bfloat16* __restrict__ cache,
                                           __nv_bfloat16* __restrict__ c_out, __nv_bfloat16* __restrict__ kpe_out) {
+  mgb::pdl_enter();
   const int t = blockIdx.x;
   const int seq = seq0 + t / P, pos = t % P;
   const int D = R + RP;
@@ -885,15 +888,14 @@ int mgb_mla_append(const void* q, const void* ckv, const void* norm_w, float eps
   if (B < 1 || H < 1 || R % 8 || RP % 8 || NOPE % 8) return MGB_EINVAL;
   const char* blk = getenv("MGB_MLA_APPEND_BLOCK");  // the per-token-CTA kernel (A/B and tests)
   if (!(blk && blk[0] == '1') && ((R + RP + 63) / 64 * 64) <= 1024) {
-    mgb::mla_append_warp_kernel<<<(B + mgb::kAppTok - 1) / mgb::kAppTok, mgb::kAppTok * 32, 0,
-                                  reinterpret_cast<cudaStream_t>(stream)>>>(
+    mgb_host::launch(mgb::mla_append_warp_kernel, dim3((B + mgb::kAppTok - 1) / mgb::kAppTok), dim3(mgb::kAppTok * 32), 0, reinterpret_cast<cudaStream_t>(stream), nullptr,
         reinterpret_cast<const __nv_bfloat16*>(q), reinterpret_cast<const __nv_bfloat16*>(ckv),
         reinterpret_cast<const __nv_bfloat16*>(norm_w), eps, B, H, R, RP, NOPE, positions, cos_t, sin_t, block_table,
         max_pages, reinterpret_cast<__nv_bfloat16*>(cache), reinterpret_cast<__nv_bfloat16*>(q_nope_out),
         reinterpret_cast<__nv_bfloat16*>(q_pe_out), seq_lens);
     return mgb_host::launch_status();
   }
-  mgb::mla_append_kernel<<<B, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+  mgb_host::launch(mgb::mla_append_kernel, dim3(B), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream), nullptr,
       reinterpret_cast<const __nv_bfloat16*>(q), reinterpret_cast<const __nv_bfloat16*>(ckv),
       reinterpret_cast<const __nv_bfloat16*>(norm_w), eps, B, H, R, RP, NOPE, positions, cos_t, sin_t, block_table,
       max_pages, reinterpret_cast<__nv_bfloat16*>(cache), reinterpret_cast<__nv_bfloat16*>(q_nope_out),
@@ -907,7 +909,7 @@ int mgb_mla_append_prefill(void* q, const void* ckv, const void* norm_w, float e
                            int R, int RP, int NOPE, const float* cos_t, const float* sin_t, const int* block_table,
                            int max_pages, void* cache, void* c_out, void* kpe_out, void* stream) {
   if (T < 1 || P < 1 || T % P || H < 1 || R % 8 || RP % 8 || NOPE % 8) return MGB_EINVAL;
-  mgb::mla_append_prefill_kernel<<<T, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+  mgb_host::launch(mgb::mla_append_prefill_kernel, dim3(T), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream), nullptr,
       reinterpret_cast<__nv_bfloat16*>(q), reinterpret_cast<const __nv_bfloat16*>(ckv),
       reinterpret_cast<const __nv_bfloat16*>(norm_w), eps, seq0, P, H, R, RP, NOPE, cos_t, sin_t, block_table, max_pages,
       reinterpret_cast<__nv_bfloat16*>(cache), reinterpret_cast<__nv_bfloat16*>(c_out),

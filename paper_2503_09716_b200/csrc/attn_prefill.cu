@@ -73,6 +73,7 @@ template <int HD_QK, int HD_V, int KS, int VS>
 __global__ void __launch_bounds__(kPfThreads, 1)
 prefill_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmKr, const __grid_constant__ CUtensorMap tmV, PfArgs a) {
+  mgb::pdl_enter();
   using C = PfCfg<HD_QK, HD_V, KS, VS>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -316,7 +317,8 @@ int launch_prefill(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorM
   const int items = a.n_qt * a.n_seq * a.Hq;
   int grid = mgb_host::num_sms();
   if (grid > items) grid = items;
-  prefill_attn_kernel<HD_QK, HD_V, KS, VS><<<grid, kPfThreads, C::kSmem, st>>>(tq, tk, tkr, tv, a);
+  mgb_host::launch(prefill_attn_kernel<HD_QK, HD_V, KS, VS>, dim3(grid), dim3(kPfThreads), C::kSmem, st, nullptr,
+      tq, tk, tkr, tv, a);
   return mgb_host::launch_status();
 }
 

@@ -35,6 +35,22 @@ MGB_DEVINL uint32_t pack_bf16x2(float lo, float hi) {
 // ----------------------------------------------------------------------------------------
 // shared-memory addressing, mbarriers
 // ----------------------------------------------------------------------------------------
+// ----------------------------------------------------------------------------------------
+// Programmatic dependent launch (PDL).  Launched with the programmatic-stream-serialization
+// attribute (mgb_host::launch), a kernel's CTAs may be scheduled while its stream predecessor is
+// still draining; griddepcontrol.wait holds them until that grid has completed and its writes are
+// visible, so it comes before the first global access of EVERY kernel (reads, and writes the
+// predecessor might still read).  launch_dependents then lets this grid's own successor be
+// scheduled: it can launch only once every CTA of this grid has issued it (i.e. is resident), so
+// its parked CTAs never take a slot this grid still needs -- including the grid-barrier and
+// completion-counter kernels, which rely on all their CTAs being co-resident.  Without the
+// attribute both instructions are no-ops.
+// ----------------------------------------------------------------------------------------
+MGB_DEVINL void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 MGB_DEVINL uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -446,4 +462,35 @@ int ensure_max_smem(const void* fn, int bytes);
 // The current device's capacity status word (int[4], see mgb::segments_fit), a __device__ symbol of
 // the library (no allocation, so launchers may call it while a graph is being captured).
 int* capacity_status_ptr();
+// MGB_PDL=1: launch with programmatic stream serialization (see mgb::pdl_enter).  Off by default:
+// same-box A/B of the replayed decode step showed no difference (Mixtral 32.45 vs 32.41 ms, DSV2-Lite
+// 54.96 vs 54.86 ms per forward) -- the graph already pipelines the launches, and a persistent
+// kernel's successor cannot take its SMs before the tail drains anyway.
+bool pdl_enabled();
+// records a launch failure for the next launch_status() (cudaLaunchKernelEx reports it by return value)
+void note_launch_error(cudaError_t e);
+// cudaLaunchKernelEx with the PDL attribute when enabled (plus an optional extra attribute, e.g. a
+// cluster dimension).  Captured into CUDA graphs as programmatic edges.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                          const cudaLaunchAttribute* extra, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  unsigned n = 0;
+  if (extra) attr[n++] = *extra;
+  if (pdl_enabled()) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = n;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+  if (e != cudaSuccess) note_launch_error(e);
+  return e;
+}
 }  // namespace mgb_host

@@ -32,6 +32,7 @@ __global__ void __launch_bounds__(kNormThreads)
 add_rmsnorm_kernel(const __nv_bfloat16* x, const __nv_bfloat16* __restrict__ delta,
                    const __nv_bfloat16* __restrict__ w, float eps, int d, __nv_bfloat16* x_out,
                    __nv_bfloat16* __restrict__ y) {
+  mgb::pdl_enter();
   __shared__ float red[32];
   const size_t row = blockIdx.x;
   const int nvec = d / 8;
@@ -89,6 +90,7 @@ __global__ void __launch_bounds__(kNormWarpTok * 32)
 add_rmsnorm_warp_kernel(const __nv_bfloat16* x, const __nv_bfloat16* __restrict__ delta,
                         const __nv_bfloat16* __restrict__ w, float eps, int T, int d, __nv_bfloat16* x_out,
                         __nv_bfloat16* __restrict__ y) {
+  mgb::pdl_enter();
   const int lane = threadIdx.x & 31;
   const size_t row = (size_t)blockIdx.x * kNormWarpTok + (threadIdx.x >> 5);
   if (row >= (size_t)T) return;
@@ -177,6 +179,7 @@ __global__ void rope_append_gqa_kernel(const __nv_bfloat16* __restrict__ qkv, in
                                        const int* __restrict__ block_table, int max_pages,
                                        __nv_bfloat16* __restrict__ k_cache, __nv_bfloat16* __restrict__ v_cache,
                                        __nv_bfloat16* __restrict__ q_out, int* __restrict__ seq_lens) {
+  mgb::pdl_enter();
   const int t = blockIdx.x;
   const int nch = hd >> 3, half = nch >> 1, H = Hq + 2 * Hkv;
   const int seq = seq0 + t;
@@ -234,6 +237,7 @@ __global__ void rope_append_gqa_prefill_kernel(const __nv_bfloat16* __restrict__
                                                int max_pages, __nv_bfloat16* __restrict__ k_cache,
                                                __nv_bfloat16* __restrict__ v_cache, __nv_bfloat16* __restrict__ q_out,
                                                __nv_bfloat16* __restrict__ k_out, __nv_bfloat16* __restrict__ v_out) {
+  mgb::pdl_enter();
   const int t = blockIdx.x;
   const int nch = hd >> 3, H = Hq + 2 * Hkv;
   const int seq = seq0 + t / P, pos = t % P;
@@ -261,6 +265,7 @@ __global__ void rope_append_gqa_prefill_kernel(const __nv_bfloat16* __restrict__
 // h = bf16(bf16(silu(g)) * u) for gu = [g | u] rows (HF DeepseekV2MLP / MixtralExperts act-mul on the
 // bf16 outputs of a cuBLAS gate|up GEMM).  8 features per thread, 16 B in/out.
 __global__ void silu_mul_kernel(const __nv_bfloat16* __restrict__ gu, int T, int F, __nv_bfloat16* __restrict__ h) {
+  mgb::pdl_enter();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;  // 16-byte chunk of the row
   if (c >= F / 8) return;
   for (int t = blockIdx.y; t < T; t += gridDim.y) {  // tokens on grid.y (32-bit index arithmetic)
@@ -279,6 +284,7 @@ __global__ void silu_mul_kernel(const __nv_bfloat16* __restrict__ gu, int T, int
 
 __global__ void embed_kernel(const int* __restrict__ ids, const __nv_bfloat16* __restrict__ table, int d,
                              __nv_bfloat16* __restrict__ out) {
+  mgb::pdl_enter();
   const size_t t = blockIdx.x;
   const uint4* src = reinterpret_cast<const uint4*>(table + (size_t)ids[t] * d);
   uint4* dst = reinterpret_cast<uint4*>(out + t * d);
@@ -287,6 +293,7 @@ __global__ void embed_kernel(const int* __restrict__ ids, const __nv_bfloat16* _
 
 // Greedy argmax over a bf16 logits row (first maximal index wins, like torch.argmax).
 __global__ void argmax_kernel(const __nv_bfloat16* __restrict__ logits, int V, int* __restrict__ out) {
+  mgb::pdl_enter();
   const size_t row = blockIdx.x;
   const __nv_bfloat16* lr = logits + row * V;
   float bv = -INFINITY;
@@ -338,6 +345,7 @@ __global__ void argmax_kernel(const __nv_bfloat16* __restrict__ logits, int V, i
 // out_tokens[b * ld + *step] = next[b]; positions[b] += 1; then ++*step.
 __global__ void decode_advance_kernel(const int* __restrict__ next, int B, long long* __restrict__ out_tokens,
                                       int ld, int* __restrict__ step, int* __restrict__ positions) {
+  mgb::pdl_enter();
   const int s = *step;
   for (int b = threadIdx.x; b < B; b += blockDim.x) {
     if (out_tokens && s < ld) out_tokens[(size_t)b * ld + s] = next[b];
@@ -358,6 +366,7 @@ MGB_DEVINL uint64_t splitmix64_mix(uint64_t z) {
 }
 __global__ void fill_uniform_kernel(__nv_bfloat16* __restrict__ out, size_t n, uint64_t seed, uint64_t tensor_id,
                                     float scale, float constant, int mode) {
+  mgb::pdl_enter();
   const uint64_t base = (seed * 0x9E3779B97F4A7C15ull + tensor_id) * 0xD1B54A32D192ED03ull;
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     if (mode == 1) {
@@ -380,13 +389,13 @@ int mgb_add_rmsnorm(const void* x, const void* delta, const void* weight, float 
   if (T >= 1024 && d <= 2048) {  // large decode batches of narrow rows: warp per token
     const int blocks = (T + mgb::kNormWarpTok - 1) / mgb::kNormWarpTok;
     auto kern = d <= 1024 ? mgb::add_rmsnorm_warp_kernel<4> : mgb::add_rmsnorm_warp_kernel<8>;
-    kern<<<blocks, mgb::kNormWarpTok * 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+    mgb_host::launch(kern, dim3(blocks), dim3(mgb::kNormWarpTok * 32), 0, reinterpret_cast<cudaStream_t>(stream), nullptr,
         reinterpret_cast<const __nv_bfloat16*>(x), reinterpret_cast<const __nv_bfloat16*>(delta),
         reinterpret_cast<const __nv_bfloat16*>(weight), eps, T, d, reinterpret_cast<__nv_bfloat16*>(x_out),
         reinterpret_cast<__nv_bfloat16*>(y));
     return mgb_host::launch_status();
   }
-  mgb::add_rmsnorm_kernel<<<T, mgb::kNormThreads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+  mgb_host::launch(mgb::add_rmsnorm_kernel, dim3(T), dim3(mgb::kNormThreads), 0, reinterpret_cast<cudaStream_t>(stream), nullptr,
       reinterpret_cast<const __nv_bfloat16*>(x), reinterpret_cast<const __nv_bfloat16*>(delta),
       reinterpret_cast<const __nv_bfloat16*>(weight), eps, d, reinterpret_cast<__nv_bfloat16*>(x_out),
       reinterpret_cast<__nv_bfloat16*>(y));
@@ -406,8 +415,7 @@ int mgb_rope_append_gqa(const void* qkv, int T, int seq0, const int* positions, 
   if (T < 1 || head_dim % 16 || Hq % Hkv) return MGB_EINVAL;
   const int threads = rope_pair_threads(Hq + 2 * Hkv, head_dim);
   if (threads > 1024) return MGB_EINVAL;
-  mgb::rope_append_gqa_kernel<<<T, threads, 0,
-                                reinterpret_cast<cudaStream_t>(stream)>>>(
+  mgb_host::launch(mgb::rope_append_gqa_kernel, dim3(T), dim3(threads), 0, reinterpret_cast<cudaStream_t>(stream), nullptr,
       reinterpret_cast<const __nv_bfloat16*>(qkv), T, seq0, positions, cos_t, sin_t, Hq, Hkv, head_dim, block_table,
       max_pages, reinterpret_cast<__nv_bfloat16*>(k_cache), reinterpret_cast<__nv_bfloat16*>(v_cache),
       reinterpret_cast<__nv_bfloat16*>(q_out), seq_lens);
@@ -419,8 +427,7 @@ int mgb_rope_append_gqa_prefill(const void* qkv, int T, int seq0, int P, const f
                                 void* v_cache, void* q_out, void* k_out, void* v_out, void* stream) {
   if (T < 1 || P < 1 || T % P || head_dim % 16 || Hq % Hkv) return MGB_EINVAL;
   const int threads = rope_threads(Hq + 2 * Hkv, head_dim);
-  mgb::rope_append_gqa_prefill_kernel<<<T, threads, 0,
-                                        reinterpret_cast<cudaStream_t>(stream)>>>(
+  mgb_host::launch(mgb::rope_append_gqa_prefill_kernel, dim3(T), dim3(threads), 0, reinterpret_cast<cudaStream_t>(stream), nullptr,
       reinterpret_cast<const __nv_bfloat16*>(qkv), T, seq0, P, cos_t, sin_t, Hq, Hkv, head_dim, block_table, max_pages,
       reinterpret_cast<__nv_bfloat16*>(k_cache), reinterpret_cast<__nv_bfloat16*>(v_cache),
       reinterpret_cast<__nv_bfloat16*>(q_out), reinterpret_cast<__nv_bfloat16*>(k_out),
@@ -430,21 +437,21 @@ int mgb_rope_append_gqa_prefill(const void* qkv, int T, int seq0, int P, const f
 
 int mgb_silu_mul(const void* gate_up, int T, int F, void* h, void* stream) {
   if (T < 1 || F % 8) return MGB_EINVAL;
-  mgb::silu_mul_kernel<<<dim3((F / 8 + 255) / 256, std::min(T, 65535)), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+  mgb_host::launch(mgb::silu_mul_kernel, dim3(dim3((F / 8 + 255) / 256, std::min(T, 65535))), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream), nullptr,
       reinterpret_cast<const __nv_bfloat16*>(gate_up), T, F, reinterpret_cast<__nv_bfloat16*>(h));
   return mgb_host::launch_status();
 }
 
 int mgb_embed(const int* ids, const void* table, int T, int d, void* out, void* stream) {
   if (T < 1 || d % 8) return MGB_EINVAL;
-  mgb::embed_kernel<<<T, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+  mgb_host::launch(mgb::embed_kernel, dim3(T), dim3(128), 0, reinterpret_cast<cudaStream_t>(stream), nullptr,
       ids, reinterpret_cast<const __nv_bfloat16*>(table), d, reinterpret_cast<__nv_bfloat16*>(out));
   return mgb_host::launch_status();
 }
 
 int mgb_argmax(const void* logits, int T, int V, int* out, void* stream) {
   if (T < 1 || V < 1) return MGB_EINVAL;
-  mgb::argmax_kernel<<<T, 512, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+  mgb_host::launch(mgb::argmax_kernel, dim3(T), dim3(512), 0, reinterpret_cast<cudaStream_t>(stream), nullptr,
       reinterpret_cast<const __nv_bfloat16*>(logits), V, out);
   return mgb_host::launch_status();
 }
@@ -452,7 +459,8 @@ int mgb_argmax(const void* logits, int T, int V, int* out, void* stream) {
 int mgb_decode_advance(const int* next, int B, long long* out_tokens, int ld, int* step, int* positions,
                        void* stream) {
   if (B < 1) return MGB_EINVAL;
-  mgb::decode_advance_kernel<<<1, 1024, 0, reinterpret_cast<cudaStream_t>(stream)>>>(next, B, out_tokens, ld, step,
+  mgb_host::launch(mgb::decode_advance_kernel, dim3(1), dim3(1024), 0, reinterpret_cast<cudaStream_t>(stream), nullptr,
+      next, B, out_tokens, ld, step,
                                                                                      positions);
   return mgb_host::launch_status();
 }
@@ -466,7 +474,7 @@ int mgb_fill_uniform_bf16(void* out, long long n, unsigned long long seed, unsig
   const int threads = 256;
   long long blocks = (n + threads - 1) / threads;
   if (blocks > 148 * 64) blocks = 148 * 64;
-  mgb::fill_uniform_kernel<<<(int)blocks, threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+  mgb_host::launch(mgb::fill_uniform_kernel, dim3((int)blocks), dim3(threads), 0, reinterpret_cast<cudaStream_t>(stream), nullptr,
       reinterpret_cast<__nv_bfloat16*>(out), (size_t)n, seed, tensor_id, scale, constant, mode);
   return mgb_host::launch_status();
 }

@@ -103,8 +103,26 @@ namespace {
 cudaError_t g_last_err = cudaSuccess;  // first launch error a libmgb entry point returned MGB_ECUDA for
 }
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("MGB_PDL");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+namespace {
+thread_local cudaError_t t_pending = cudaSuccess;  // a cudaLaunchKernelEx failure (mgb_host::launch)
+}
+
+void note_launch_error(cudaError_t e) {
+  if (t_pending == cudaSuccess) t_pending = e;
+}
+
 int launch_status() {
-  const cudaError_t e = cudaGetLastError();
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = t_pending;
+  t_pending = cudaSuccess;
   if (e == cudaSuccess) return MGB_OK;
   g_last_err = e;
   return MGB_ECUDA;

@@ -24,6 +24,7 @@ __global__ void kv_token_copy_kernel(const uint8_t* __restrict__ src, const int*
                                      int src_max_pages, uint8_t* __restrict__ dst, const int* __restrict__ dst_table,
                                      int dst_max_pages, const int* __restrict__ positions, int B, int page_tokens,
                                      long long page_bytes, int unit_bytes, int n_units, long long unit_stride) {
+  mgb::pdl_enter();
   const int vec_per_unit = unit_bytes >> 4;
   const int vec_per_tok = n_units * vec_per_unit;
   const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -45,6 +46,7 @@ __global__ void kv_token_copy_kernel(const uint8_t* __restrict__ src, const int*
 // host memory).  Used for the small per-layer transfers of the CPU attention share, which would
 // otherwise queue on a copy engine behind the multi-hundred-MB KV_COPY_IN slices.
 __global__ void copy_bytes_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src, long long n16) {
+  mgb::pdl_enter();
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += (long long)gridDim.x * blockDim.x)
     dst[i] = src[i];
 }
@@ -60,7 +62,7 @@ int mgb_copy_bytes(void* dst, const void* src, long long nbytes, void* stream) {
   const long long n16 = nbytes / 16;
   long long blocks = (n16 + 255) / 256;
   if (blocks > 4 * 148) blocks = 4 * 148;
-  mgb::copy_bytes_kernel<<<(int)blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+  mgb_host::launch(mgb::copy_bytes_kernel, dim3((int)blocks), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream), nullptr,
       reinterpret_cast<uint4*>(dst), reinterpret_cast<const uint4*>(src), n16);
   return mgb_host::launch_status();
 }
@@ -77,8 +79,7 @@ int mgb_kv_token_copy(const void* src, const int* src_table, int src_max_pages, 
     return MGB_EINVAL;
   const long long items = (long long)B * n_units * (unit_bytes / 16);
   const int threads = 256;
-  mgb::kv_token_copy_kernel<<<(int)((items + threads - 1) / threads), threads, 0,
-                              reinterpret_cast<cudaStream_t>(stream)>>>(
+  mgb_host::launch(mgb::kv_token_copy_kernel, dim3((int)((items + threads - 1) / threads)), dim3(threads), 0, reinterpret_cast<cudaStream_t>(stream), nullptr,
       reinterpret_cast<const uint8_t*>(src), src_table, src_max_pages, reinterpret_cast<uint8_t*>(dst), dst_table,
       dst_max_pages, positions, B, page_tokens, page_bytes, unit_bytes, n_units, unit_stride);
   return mgb_host::launch_status();

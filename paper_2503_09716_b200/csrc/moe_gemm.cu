@@ -146,6 +146,7 @@ moe_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 const int* __restrict__ offsets, int E, int MT, int K, int rows_per_expert, int half_rows,
                 __nv_bfloat16* __restrict__ out, int ldo, bool balanced,
                 const long long* __restrict__ row_ptr, int rows_cap, int* __restrict__ cap_status) {
+  mgb::pdl_enter();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* tiles = smem;
@@ -348,6 +349,7 @@ moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                      const int* __restrict__ offsets, int E, int MT, int K, int rows_per_expert, int half_rows,
                      __nv_bfloat16* __restrict__ out, int ldo, bool balanced,
                      const long long* __restrict__ row_ptr, int nalign, int rows_cap, int* __restrict__ cap_status) {
+  mgb::pdl_enter();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* tiles = smem;
@@ -571,6 +573,7 @@ moe_ffn_pair_kernel(const __grid_constant__ CUtensorMap tmAg, const __grid_const
                     const __grid_constant__ CUtensorMap tmAd, const __grid_constant__ BMaps tmBh,
                     const int* __restrict__ offsets, int E, FfnGemm gu, FfnGemm dn, int nalign, int rows_cap,
                     int* __restrict__ cap_status, int* __restrict__ done) {
+  mgb::pdl_enter();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* tiles = smem;
@@ -817,15 +820,14 @@ int launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, const mgb::BM
       const char* e = getenv("MGB_PAIR_NALIGN");
       return (e && atoi(e) == 32) ? 32 : 16;
     }();
-    mgb::moe_gemm_pair_kernel<GATED, ROWPTR><<<grid, mgb::Epi<GATED>::kThreads, mgb::pair_smem<GATED>(), stream>>>(
+    mgb_host::launch(mgb::moe_gemm_pair_kernel<GATED, ROWPTR>, dim3(grid), dim3(mgb::Epi<GATED>::kThreads), mgb::pair_smem<GATED>(), stream, nullptr,
         tmA, tmBs, offsets, E, MT / 2, K, rows_per_expert, half_rows, reinterpret_cast<__nv_bfloat16*>(out), ldo,
         balanced, row_ptr, nalign, rows_cap, cap_status);
   } else {
     if (const int rc = mgb_host::ensure_max_smem((const void*)mgb::moe_gemm_kernel<GATED, ROWPTR>,
                                                  mgb::gemm_smem<GATED>()))
       return rc;
-    mgb::moe_gemm_kernel<GATED, ROWPTR><<<mgb_host::num_sms(), mgb::Epi<GATED>::kThreads, mgb::gemm_smem<GATED>(),
-                                          stream>>>(
+    mgb_host::launch(mgb::moe_gemm_kernel<GATED, ROWPTR>, dim3(mgb_host::num_sms()), dim3(mgb::Epi<GATED>::kThreads), mgb::gemm_smem<GATED>(), stream, nullptr,
         tmA, tmB, offsets, E, MT, K, rows_per_expert, half_rows, reinterpret_cast<__nv_bfloat16*>(out), ldo, balanced,
         row_ptr, rows_cap, cap_status);
   }
@@ -944,8 +946,8 @@ int mgb_moe_ffn(const void* w_gate_up, const void* w_down, const void* x_perm, c
     return (e && atoi(e) == 32) ? 32 : 16;
   }();
   const int grid = mgb_host::num_sms() & ~1;
-  mgb::moe_ffn_pair_kernel<<<grid, mgb::Epi<true>::kThreads, mgb::pair_smem<true>(),
-                             reinterpret_cast<cudaStream_t>(stream)>>>(tAg, tBx, tAd, tBh, offsets, E, gu, dn,
+  mgb_host::launch(mgb::moe_ffn_pair_kernel, dim3(grid), dim3(mgb::Epi<true>::kThreads), mgb::pair_smem<true>(), reinterpret_cast<cudaStream_t>(stream), nullptr,
+      tAg, tBx, tAd, tBh, offsets, E, gu, dn,
                                                                        nalign, rows_cap, cap_status, sync);
   return mgb_host::launch_status();
 }

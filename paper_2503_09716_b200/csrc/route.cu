@@ -138,6 +138,7 @@ struct RteSmem {
 };
 
 __global__ void __launch_bounds__(kRteThreads, 2) moe_route_kernel(RouteArgs a) {
+  mgb::pdl_enter();
   extern __shared__ __align__(16) uint8_t smem[];
   const int d = a.d, E = a.E, k = a.k;
   MGB_RTE_STAMP(9);
@@ -543,7 +544,8 @@ int mgb_moe_route(const void* x, const void* delta, const void* ln_w, float eps,
                    reinterpret_cast<__nv_bfloat16*>(h_out), logits_out, topk_idx, topk_w, local_rank, chunk_hist,
                    counts, offsets, reinterpret_cast<__nv_bfloat16*>(x_perm), src_token, dst_pos, sync, nchunks,
                    g_route_stamps};
-  mgb::moe_route_kernel<<<G, mgb::kRteThreads, smem, reinterpret_cast<cudaStream_t>(stream)>>>(a);
+  mgb_host::launch(mgb::moe_route_kernel, dim3(G), dim3(mgb::kRteThreads), smem, reinterpret_cast<cudaStream_t>(stream), nullptr,
+      a);
   return mgb_host::launch_status();
 }
 

@@ -64,6 +64,7 @@ MGB_DEVINL float warp_sum(float v) {
 }
 
 __global__ void __launch_bounds__(kRouterThreads) router_topk_kernel(RouterArgs a) {
+  mgb::pdl_enter();
   extern __shared__ __align__(16) uint8_t smem[];
   float* s_logit = reinterpret_cast<float*>(smem);                          // [TPB][E]
   int* s_exp = reinterpret_cast<int*>(s_logit + kRouterTPB * kMaxE);        // [TPB*k]
@@ -284,6 +285,7 @@ __global__ void __launch_bounds__(kRouterThreads) router_topk_kernel(RouterArgs 
 __global__ void __launch_bounds__(256) router_scan_kernel(int* __restrict__ block_hist, int nblk, int E,
                                                           int* __restrict__ counts, int* __restrict__ offsets,
                                                           int* __restrict__ ticket) {
+  mgb::pdl_enter();
   const int e = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   __shared__ int s_warp[8];
@@ -344,6 +346,7 @@ __global__ void permute_kernel(const __nv_bfloat16* __restrict__ x, const int* _
                                int* __restrict__ dst_pos, const long long* __restrict__ peer_base,
                                const int* __restrict__ disp_row, int E_local, int recv_cap,
                                int* __restrict__ cap_status) {
+  mgb::pdl_enter();
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (gw >= T * k) return;
@@ -410,6 +413,7 @@ combine_kernel(const __nv_bfloat16* __restrict__ y_perm, const int* __restrict__
                const __nv_bfloat16* residual, int T, int d, int k,
                __nv_bfloat16* out,  // may alias residual (in-place residual add)
                const __nv_bfloat16* __restrict__ norm_w, float eps, __nv_bfloat16* __restrict__ norm_out) {
+  mgb::pdl_enter();
   const int t = blockIdx.x;
   __shared__ int s_pos[kMaxK];
   __shared__ float s_w[kMaxK];
@@ -545,9 +549,11 @@ int mgb_router_topk(const void* x, const void* w_gate, const float* logits_in, i
         cudaSuccess)
       return MGB_ECUDA;
   }
-  mgb::router_topk_kernel<<<nblk, mgb::kRouterThreads, smem, reinterpret_cast<cudaStream_t>(stream)>>>(a);
+  mgb_host::launch(mgb::router_topk_kernel, dim3(nblk), dim3(mgb::kRouterThreads), smem, reinterpret_cast<cudaStream_t>(stream), nullptr,
+      a);
   if (nblk > mgb::kFusedScanMaxBlocks)
-    mgb::router_scan_kernel<<<E, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(block_hist, nblk, E, counts, offsets,
+    mgb_host::launch(mgb::router_scan_kernel, dim3(E), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream), nullptr,
+        block_hist, nblk, E, counts, offsets,
                                                                                    ticket);
   return mgb_host::launch_status();
 }
@@ -561,7 +567,7 @@ int mgb_permute(const void* x, const int* topk_idx, const int* local_rank, const
   const int warps = T * k;
   const int threads = 256;
   const int blocks = (warps * 32 + threads - 1) / threads;
-  (d <= 2048 ? mgb::permute_kernel<8> : mgb::permute_kernel<16>)<<<blocks, threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+  mgb_host::launch((d <= 2048 ? mgb::permute_kernel<8> : mgb::permute_kernel<16>), dim3(blocks), dim3(threads), 0, reinterpret_cast<cudaStream_t>(stream), nullptr,
       reinterpret_cast<const __nv_bfloat16*>(x), topk_idx, local_rank, block_base, offsets, T, d, k, E,
       mgb::kRouterTPB, reinterpret_cast<__nv_bfloat16*>(x_perm), src_token, dst_pos, nullptr, nullptr, 1, 0, nullptr);
   return mgb_host::launch_status();
@@ -584,7 +590,7 @@ int mgb_ep_permute_dispatch(const void* x, const int* topk_idx, const int* local
   const int warps = T * k;
   const int threads = 256;
   const int blocks = (warps * 32 + threads - 1) / threads;
-  (d <= 2048 ? mgb::permute_kernel<8> : mgb::permute_kernel<16>)<<<blocks, threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+  mgb_host::launch((d <= 2048 ? mgb::permute_kernel<8> : mgb::permute_kernel<16>), dim3(blocks), dim3(threads), 0, reinterpret_cast<cudaStream_t>(stream), nullptr,
       reinterpret_cast<const __nv_bfloat16*>(x), topk_idx, local_rank, block_base, offsets, T, d, k, E,
       mgb::kRouterTPB, nullptr, src_token, dst_pos, peer_base, disp_row, E_local, recv_rows_cap, cap_status);
   return mgb_host::launch_status();
@@ -598,6 +604,7 @@ __global__ void ep_row_ptrs_kernel(const int* __restrict__ seg_start, const int*
                                    const int* __restrict__ seg_delta, int n_seg, int W,
                                    const long long* __restrict__ peer_base, int row_bytes, int rows_cap,
                                    long long* __restrict__ row_ptr) {
+  mgb::pdl_enter();
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= rows_cap) return;
   int lo = 0, hi = n_seg - 1;  // last segment with start <= q
@@ -614,7 +621,7 @@ __global__ void ep_row_ptrs_kernel(const int* __restrict__ seg_start, const int*
 int mgb_ep_row_ptrs(const int* seg_start, const int* seg_len, const int* seg_delta, int n_seg, int W,
                     const long long* peer_base, int row_bytes, int rows_cap, long long* row_ptr, void* stream) {
   if (n_seg < 1 || W < 1 || n_seg % W || row_bytes < 16 || rows_cap < 1) return MGB_EINVAL;
-  ep_row_ptrs_kernel<<<(rows_cap + 255) / 256, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+  mgb_host::launch(ep_row_ptrs_kernel, dim3((rows_cap + 255) / 256), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream), nullptr,
       seg_start, seg_len, seg_delta, n_seg, W, peer_base, row_bytes, rows_cap, row_ptr);
   return mgb_host::launch_status();
 }
@@ -638,7 +645,7 @@ int mgb_unpermute_combine(const void* y_perm, const int* dst_pos, const float* t
     kern = mgb::combine_kernel<4, 2, 128>;
     nth = 128;
   }
-  kern<<<T, nth, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+  mgb_host::launch(kern, dim3(T), dim3(nth), 0, reinterpret_cast<cudaStream_t>(stream), nullptr,
       reinterpret_cast<const __nv_bfloat16*>(y_perm), dst_pos, topk_w,
       reinterpret_cast<const __nv_bfloat16*>(shared_out), reinterpret_cast<const __nv_bfloat16*>(residual), T, d,
       k, reinterpret_cast<__nv_bfloat16*>(out), reinterpret_cast<const __nv_bfloat16*>(norm_w), eps,
