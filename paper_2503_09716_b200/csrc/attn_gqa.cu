@@ -296,7 +296,12 @@ int launch_gqa(const void* q, const void* kc, const void* vc, const int* bt, int
   using S = GqaSmem<HD, G>;
   if (const int rc = mgb_host::ensure_max_smem((const void*)decode_attn_gqa_kernel<HD, G>, (int)S::kBytes)) return rc;
   const int items = B * Hkv;
-  int grid = 2 * mgb_host::num_sms();
+  int sms = mgb_host::num_sms();
+  if (const char* e = getenv("MGB_ATTN_SMS")) {  // leave SMs to a concurrent stream (overlap experiments)
+    const int cap = atoi(e);
+    if (cap > 0 && cap < sms) sms = cap;
+  }
+  int grid = 2 * sms;
   if (grid > items) grid = items;
   mgb_host::launch(decode_attn_gqa_kernel<HD, G>, dim3(grid), dim3(kAttnThreads), S::kBytes, st, nullptr,
       reinterpret_cast<const __nv_bfloat16*>(q), reinterpret_cast<const __nv_bfloat16*>(kc),

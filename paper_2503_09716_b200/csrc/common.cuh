@@ -397,6 +397,16 @@ MGB_DEVINL void tma_load_2d_pair(void* smem_dst, const CUtensorMap* m, uint64_t*
       : "memory");
 }
 
+MGB_DEVINL void tma_load_4d_pair(void* smem_dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2, int c3,
+                                 uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], %7;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+      "l"(policy)
+      : "memory");
+}
+
 MGB_DEVINL uint32_t warp_id() { return __shfl_sync(0xffffffffu, threadIdx.x / 32, 0); }
 MGB_DEVINL bool elect_one() {
   uint32_t pred = 0;
@@ -455,7 +465,8 @@ CUresult encode_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner,
                              uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer);
 // Rank-N (N <= 5) bf16 tensor map, unswizzled or 128B-swizzled; strides_bytes has rank-1 entries (dims 1..N-1).
 CUresult encode_tmap_bf16(CUtensorMap* map, const void* base, int rank, const uint64_t* dims,
-                          const uint64_t* strides_bytes, const uint32_t* box, bool swizzle128 = false);
+                          const uint64_t* strides_bytes, const uint32_t* box, bool swizzle128 = false,
+                          bool l2_promote_256 = false);
 int num_sms();
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device); MGB_OK or MGB_ECUDA.
 int ensure_max_smem(const void* fn, int bytes);

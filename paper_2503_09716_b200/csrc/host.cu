@@ -29,7 +29,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 encoder() {
 }
 
 CUresult encode_tmap_bf16(CUtensorMap* map, const void* base, int rank, const uint64_t* dims,
-                          const uint64_t* strides_bytes, const uint32_t* box, bool swizzle128) {
+                          const uint64_t* strides_bytes, const uint32_t* box, bool swizzle128, bool l2_promote_256) {
   if (!encoder()) return CUDA_ERROR_NOT_FOUND;
   cuuint64_t d[5], s[4];
   cuuint32_t b[5], e[5];
@@ -41,7 +41,7 @@ CUresult encode_tmap_bf16(CUtensorMap* map, const void* base, int rank, const ui
   }
   return g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), d, s, b, e,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
-                  CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  l2_promote_256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_NONE,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
 }
 

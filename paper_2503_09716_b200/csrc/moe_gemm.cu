@@ -323,20 +323,28 @@ constexpr int kPStages = 6;
 // a 104-row B slice per stage runs at 4.1 TB/s of A with 16-row B boxes and at 6.5 TB/s -- the A-only
 // rate -- with 64+32+8 (tools/tma_pattern_bench.cu).  Every box starts on a whole 8-row (1 KB) swizzle
 // atom, so the boxes together land exactly where one tall box would.
+// With one map per box height 8, 16, ..., 128 rows the half tile is ONE request (`one`, MGB_TMA1 on by
+// default): gate/up stages then take 2 requests (one 4-D gate+up A box, one B box) instead of 5, down
+// stages 2 instead of 4 -- Mixtral's fused FFN 17.47 -> 16.68 ms per replayed forward (same box).
+constexpr int kBMaps = kBNMax / 2 / 8;  // box heights 8 * (i + 1) rows
 struct BMaps {
-  CUtensorMap m[4];  // box heights 64, 32, 16, 8 rows (box width kBK)
+  CUtensorMap m[kBMaps];  // box width kBK
 };
 MGB_DEVINL void load_b_rows_pair(uint8_t* bt, const BMaps& mp, uint64_t* bar, int kcol, int row0, int rows,
-                                 uint64_t pol) {
+                                 uint64_t pol, bool one = false) {
+  if (one) {
+    tma_load_2d_pair(bt, &mp.m[rows / 8 - 1], bar, kcol, row0, pol);
+    return;
+  }
   int r = 0;
-  for (; rows - r >= 64; r += 64) tma_load_2d_pair(bt + r * 128, &mp.m[0], bar, kcol, row0 + r, pol);
-  if (rows - r >= 32) { tma_load_2d_pair(bt + r * 128, &mp.m[1], bar, kcol, row0 + r, pol); r += 32; }
-  if (rows - r >= 16) { tma_load_2d_pair(bt + r * 128, &mp.m[2], bar, kcol, row0 + r, pol); r += 16; }
-  if (rows - r >= 8) tma_load_2d_pair(bt + r * 128, &mp.m[3], bar, kcol, row0 + r, pol);
+  for (; rows - r >= 64; r += 64) tma_load_2d_pair(bt + r * 128, &mp.m[7], bar, kcol, row0 + r, pol);
+  if (rows - r >= 32) { tma_load_2d_pair(bt + r * 128, &mp.m[3], bar, kcol, row0 + r, pol); r += 32; }
+  if (rows - r >= 16) { tma_load_2d_pair(bt + r * 128, &mp.m[1], bar, kcol, row0 + r, pol); r += 16; }
+  if (rows - r >= 8) tma_load_2d_pair(bt + r * 128, &mp.m[0], bar, kcol, row0 + r, pol);
 }
 MGB_DEVINL void prefetch_bmaps(const BMaps& mp) {
 #pragma unroll
-  for (int i = 0; i < 4; ++i) prefetch_tmap(&mp.m[i]);
+  for (int i = 0; i < kBMaps; ++i) prefetch_tmap(&mp.m[i]);
 }
 constexpr int kPStageBytes = kATileBytes + (kBNMax / 2) * kBK * 2;  // 16 KB A + <= 16 KB half-B
 template <bool GATED> constexpr int pair_smem() {
@@ -346,9 +354,11 @@ template <bool GATED> constexpr int pair_smem() {
 template <bool GATED, bool ROWPTR = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Epi<GATED>::kThreads, 1)
 moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ BMaps tmB,
+                     const __grid_constant__ CUtensorMap tmA4,  // GATED: W as [E][gate|up][f][K] (one box per stage)
                      const int* __restrict__ offsets, int E, int MT, int K, int rows_per_expert, int half_rows,
                      __nv_bfloat16* __restrict__ out, int ldo, bool balanced,
-                     const long long* __restrict__ row_ptr, int nalign, int rows_cap, int* __restrict__ cap_status) {
+                     const long long* __restrict__ row_ptr, int nalign, int rows_cap, int* __restrict__ cap_status,
+                     int tma1) {
   mgb::pdl_enter();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -378,7 +388,7 @@ moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
     s_prefix[E] = fit ? acc : 0;  // overflow: no unit runs (status recorded), nothing is written
   }
   if (warp == 0 && lane == 0) {
-    prefetch_tmap(&tmA);
+    prefetch_tmap(GATED && tma1 ? &tmA4 : &tmA);
     prefetch_bmaps(tmB);
     for (int s = 0; s < kPStages; ++s) {
       mbar_init(&full_bar[s], 1);
@@ -426,13 +436,15 @@ moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
           { FFN_T0(); mbar_wait(&empty_bar[stage], phase ^ 1); FFN_ACC(0); }
           if (leader) mbar_arrive_expect_tx(&full_bar[stage], bytes);
           uint8_t* st = tiles + stage * kPStageBytes;
-          if (GATED) {
+          if (GATED && tma1) {
+            tma_load_4d_pair(st, &tmA4, &full_bar[stage], kb * kBK, arow0 - e * rows_per_expert, 0, e, pol_w);
+          } else if (GATED) {
             tma_load_2d_pair(st, &tmA, &full_bar[stage], kb * kBK, arow0, pol_w);
             tma_load_2d_pair(st + kAHalfBytes, &tmA, &full_bar[stage], kb * kBK, arow0 + half_rows, pol_w);
           } else {
             tma_load_2d_pair(st, &tmA, &full_bar[stage], kb * kBK, arow0, pol_w);
           }
-          load_b_rows_pair(st + kATileBytes, tmB, &full_bar[stage], kb * kBK, trow0, half, pol_x);
+          load_b_rows_pair(st + kATileBytes, tmB, &full_bar[stage], kb * kBK, trow0, half, pol_x, tma1 != 0);
           if (++stage == kPStages) { stage = 0; phase ^= 1; }
         }
       }
@@ -571,8 +583,9 @@ MGB_DEVINL void ffn_decode(int u, int total_gu, const int* s_pgu, const int* s_p
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Epi<true>::kThreads, 1)
 moe_ffn_pair_kernel(const __grid_constant__ CUtensorMap tmAg, const __grid_constant__ BMaps tmBx,
                     const __grid_constant__ CUtensorMap tmAd, const __grid_constant__ BMaps tmBh,
+                    const __grid_constant__ CUtensorMap tmAg4,  // W_gate_up as [E][gate|up][f][d]: both halves in one box
                     const int* __restrict__ offsets, int E, FfnGemm gu, FfnGemm dn, int nalign, int rows_cap,
-                    int* __restrict__ cap_status, int* __restrict__ done) {
+                    int* __restrict__ cap_status, int* __restrict__ done, int tma1) {
   mgb::pdl_enter();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -609,7 +622,7 @@ moe_ffn_pair_kernel(const __grid_constant__ CUtensorMap tmAg, const __grid_const
     s_pdn[E] = fit ? ad : 0;
   }
   if (warp == 0 && lane == 0) {
-    prefetch_tmap(&tmAg);
+    prefetch_tmap(tma1 ? &tmAg4 : &tmAg);
     prefetch_bmaps(tmBx);
     prefetch_tmap(&tmAd);
     prefetch_bmaps(tmBh);
@@ -670,13 +683,15 @@ moe_ffn_pair_kernel(const __grid_constant__ CUtensorMap tmAg, const __grid_const
           { FFN_T0(); mbar_wait(&empty_bar[stage], phase ^ 1); FFN_ACC(0); }
           if (leader) mbar_arrive_expect_tx(&full_bar[stage], bytes);
           uint8_t* st = tiles + stage * kPStageBytes;
-          if (gated) {
+          if (gated && tma1) {  // gate rows then the matching up rows: the same smem image as two boxes
+            tma_load_4d_pair(st, &tmAg4, &full_bar[stage], kb * kBK, (mt * 2 + (int)rank) * rows_cta, 0, e, pol_w);
+          } else if (gated) {
             tma_load_2d_pair(st, tA, &full_bar[stage], kb * kBK, arow0, pol_w);
             tma_load_2d_pair(st + kAHalfBytes, tA, &full_bar[stage], kb * kBK, arow0 + G.half_rows, pol_w);
           } else {
             tma_load_2d_pair(st, tA, &full_bar[stage], kb * kBK, arow0, pol_w);
           }
-          load_b_rows_pair(st + kATileBytes, tB, &full_bar[stage], kb * kBK, trow0, half, pol_x);
+          load_b_rows_pair(st + kATileBytes, tB, &full_bar[stage], kb * kBK, trow0, half, pol_x, tma1 != 0);
           if (++stage == kPStages) { stage = 0; phase ^= 1; }
         }
       }
@@ -786,6 +801,24 @@ moe_ffn_pair_kernel(const __grid_constant__ CUtensorMap tmAg, const __grid_const
 // Host side
 // ------------------------------------------------------------------------------------------
 namespace {
+// one TMA request per operand per stage in the pair kernels (4-D gate+up A box, exact-height B box);
+// MGB_TMA1=0 restores the 2 + (up to 4) request split
+int tma1_enabled() {
+  static const int v = [] {
+    const char* e = getenv("MGB_TMA1");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  return v;
+}
+
+// [E][2][f][K] view of a gated weight [E, 2f, K]: one box = 64 gate rows + the matching 64 up rows
+int encode_gate_up_4d(CUtensorMap* m, const void* w, int E, int f, int K) {
+  const uint64_t dims[4] = {(uint64_t)K, (uint64_t)f, 2, (uint64_t)E};
+  const uint64_t strides[3] = {(uint64_t)K * 2, (uint64_t)f * K * 2, (uint64_t)2 * f * K * 2};
+  const uint32_t box[4] = {(uint32_t)mgb::kBK, (uint32_t)mgb::kBM / 2, 2, 1};
+  return mgb_host::encode_tmap_bf16(m, w, 4, dims, strides, box, true, true) != CUDA_SUCCESS;
+}
+
 bool use_pair_kernel() {
   static const bool v = [] {
     const char* e = getenv("MGB_GEMM_PAIR");
@@ -796,15 +829,15 @@ bool use_pair_kernel() {
 
 // token-operand maps of the pair kernels: box heights 64 / 32 / 16 / 8 rows over [rows, K] bf16
 int encode_bmaps(mgb::BMaps* mp, const void* act, int K, int rows) {
-  const uint32_t h[4] = {64, 32, 16, 8};
-  for (int i = 0; i < 4; ++i)
-    if (mgb_host::encode_tmap_2d_bf16(&mp->m[i], act, K, rows, (uint64_t)K * 2, mgb::kBK, h[i]) != CUDA_SUCCESS)
+  for (int i = 0; i < mgb::kBMaps; ++i)
+    if (mgb_host::encode_tmap_2d_bf16(&mp->m[i], act, K, rows, (uint64_t)K * 2, mgb::kBK, 8 * (i + 1)) != CUDA_SUCCESS)
       return 1;
   return 0;
 }
 
 template <bool GATED, bool PAIR, bool ROWPTR>
-int launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, const mgb::BMaps& tmBs, const int* offsets, int E, int MT, int K,
+int launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmA4, const CUtensorMap& tmB, const mgb::BMaps& tmBs,
+                   const int* offsets, int E, int MT, int K,
                    int rows_per_expert, int half_rows, void* out, int ldo, bool balanced, const long long* row_ptr,
                    int rows_cap, cudaStream_t stream) {
   int* cap_status = mgb_host::capacity_status_ptr();
@@ -821,8 +854,8 @@ int launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, const mgb::BM
       return (e && atoi(e) == 32) ? 32 : 16;
     }();
     mgb_host::launch(mgb::moe_gemm_pair_kernel<GATED, ROWPTR>, dim3(grid), dim3(mgb::Epi<GATED>::kThreads), mgb::pair_smem<GATED>(), stream, nullptr,
-        tmA, tmBs, offsets, E, MT / 2, K, rows_per_expert, half_rows, reinterpret_cast<__nv_bfloat16*>(out), ldo,
-        balanced, row_ptr, nalign, rows_cap, cap_status);
+        tmA, tmBs, tmA4, offsets, E, MT / 2, K, rows_per_expert, half_rows, reinterpret_cast<__nv_bfloat16*>(out),
+        ldo, balanced, row_ptr, nalign, rows_cap, cap_status, tma1_enabled());
   } else {
     if (const int rc = mgb_host::ensure_max_smem((const void*)mgb::moe_gemm_kernel<GATED, ROWPTR>,
                                                  mgb::gemm_smem<GATED>()))
@@ -847,8 +880,9 @@ int launch_moe_gemm(const void* w, int w_rows_total, const void* act, int act_ro
     return e ? (e[0] == '1' ? 1 : 0) : -1;
   }();
   const bool balanced = bal_env < 0 ? GATED : bal_env == 1;
-  CUtensorMap tmA, tmB;
+  CUtensorMap tmA, tmB, tmA4 = {};
   mgb::BMaps tmBs;
+  if (GATED && pair && encode_gate_up_4d(&tmA4, w, E, half_rows, K)) return MGB_ECUDA;
   if (mgb_host::encode_tmap_2d_bf16(&tmA, w, K, w_rows_total, (uint64_t)K * 2, mgb::kBK,
                                     GATED ? mgb::kBM / 2 : mgb::kBM) != CUDA_SUCCESS)
     return MGB_ECUDA;
@@ -857,14 +891,14 @@ int launch_moe_gemm(const void* w, int w_rows_total, const void* act, int act_ro
   if (pair && encode_bmaps(&tmBs, act, K, act_rows)) return MGB_ECUDA;
   if (row_ptr) {
     if (GATED) return MGB_EINVAL;  // only the down GEMM sends rows home
-    return pair ? launch_variant<GATED, true, true>(tmA, tmB, tmBs, offsets, E, MT, K, rows_per_expert, half_rows, out, ldo,
+    return pair ? launch_variant<GATED, true, true>(tmA, tmA4, tmB, tmBs, offsets, E, MT, K, rows_per_expert, half_rows, out, ldo,
                                                    balanced, row_ptr, act_rows, stream)
-                : launch_variant<GATED, false, true>(tmA, tmB, tmBs, offsets, E, MT, K, rows_per_expert, half_rows, out, ldo,
+                : launch_variant<GATED, false, true>(tmA, tmA4, tmB, tmBs, offsets, E, MT, K, rows_per_expert, half_rows, out, ldo,
                                                     balanced, row_ptr, act_rows, stream);
   }
-  return pair ? launch_variant<GATED, true, false>(tmA, tmB, tmBs, offsets, E, MT, K, rows_per_expert, half_rows, out, ldo,
+  return pair ? launch_variant<GATED, true, false>(tmA, tmA4, tmB, tmBs, offsets, E, MT, K, rows_per_expert, half_rows, out, ldo,
                                                   balanced, nullptr, act_rows, stream)
-              : launch_variant<GATED, false, false>(tmA, tmB, tmBs, offsets, E, MT, K, rows_per_expert, half_rows, out, ldo,
+              : launch_variant<GATED, false, false>(tmA, tmA4, tmB, tmBs, offsets, E, MT, K, rows_per_expert, half_rows, out, ldo,
                                                    balanced, nullptr, act_rows, stream);
 }
 }  // namespace
@@ -928,9 +962,11 @@ int mgb_moe_ffn(const void* w_gate_up, const void* w_down, const void* x_perm, c
     const int rc = mgb_moe_gemm_gate_up(w_gate_up, x_perm, offsets, E, d, f, rows_cap, h_scratch, stream);
     return rc ? rc : mgb_moe_gemm_down(w_down, h_scratch, offsets, E, d, f, rows_cap, y_out, stream);
   }
-  CUtensorMap tAg, tAd;
+  CUtensorMap tAg, tAd, tAg4;
   mgb::BMaps tBx, tBh;
   using mgb_host::encode_tmap_2d_bf16;
+  const int tma1 = tma1_enabled();
+  if (encode_gate_up_4d(&tAg4, w_gate_up, E, f, d)) return MGB_ECUDA;
   if (encode_tmap_2d_bf16(&tAg, w_gate_up, d, (uint64_t)E * 2 * f, (uint64_t)d * 2, mgb::kBK, mgb::kBM / 2) ||
       encode_tmap_2d_bf16(&tAd, w_down, f, (uint64_t)E * d, (uint64_t)f * 2, mgb::kBK, mgb::kBM) ||
       encode_bmaps(&tBx, x_perm, d, rows_cap) || encode_bmaps(&tBh, h_scratch, f, rows_cap))
@@ -947,8 +983,7 @@ int mgb_moe_ffn(const void* w_gate_up, const void* w_down, const void* x_perm, c
   }();
   const int grid = mgb_host::num_sms() & ~1;
   mgb_host::launch(mgb::moe_ffn_pair_kernel, dim3(grid), dim3(mgb::Epi<true>::kThreads), mgb::pair_smem<true>(), reinterpret_cast<cudaStream_t>(stream), nullptr,
-      tAg, tBx, tAd, tBh, offsets, E, gu, dn,
-                                                                       nalign, rows_cap, cap_status, sync);
+      tAg, tBx, tAd, tBh, tAg4, offsets, E, gu, dn, nalign, rows_cap, cap_status, sync, tma1);
   return mgb_host::launch_status();
 }
 
