@@ -581,11 +581,12 @@ MGB_DEVINL void ffn_decode(int u, int total_gu, const int* s_pgu, const int* s_p
 }
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Epi<true>::kThreads, 1)
-moe_ffn_pair_kernel(const __grid_constant__ CUtensorMap tmAg, const __grid_constant__ BMaps tmBx,
-                    const __grid_constant__ CUtensorMap tmAd, const __grid_constant__ BMaps tmBh,
-                    const __grid_constant__ CUtensorMap tmAg4,  // W_gate_up as [E][gate|up][f][d]: both halves in one box
+moe_ffn_pair_kernel(const __grid_constant__ CUtensorMap tmAg,  // W_gate_up [E][gate|up][f][K/64][64], 5-D
+                    const __grid_constant__ BMaps tmBx,        // x_perm [rows][K/64][64], 3-D
+                    const __grid_constant__ CUtensorMap tmAd,  // W_down [E*d][f/64][64], 3-D
+                    const __grid_constant__ BMaps tmBh,        // h [rows][f/64][64], 3-D
                     const int* __restrict__ offsets, int E, FfnGemm gu, FfnGemm dn, int nalign, int rows_cap,
-                    int* __restrict__ cap_status, int* __restrict__ done, int tma1) {
+                    int* __restrict__ cap_status, int* __restrict__ done, int kps) {
   mgb::pdl_enter();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -605,6 +606,7 @@ moe_ffn_pair_kernel(const __grid_constant__ CUtensorMap tmAg, const __grid_const
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
+  const int nst = kPStages / kps;  // ring stages of kps K-blocks each
 
   if (threadIdx.x == 0) {
     const bool fit = segments_fit(offsets, E, rows_cap, cap_status, kCapGateUp);
@@ -622,7 +624,7 @@ moe_ffn_pair_kernel(const __grid_constant__ CUtensorMap tmAg, const __grid_const
     s_pdn[E] = fit ? ad : 0;
   }
   if (warp == 0 && lane == 0) {
-    prefetch_tmap(tma1 ? &tmAg4 : &tmAg);
+    prefetch_tmap(&tmAg);
     prefetch_bmaps(tmBx);
     prefetch_tmap(&tmAd);
     prefetch_bmaps(tmBh);
@@ -661,7 +663,6 @@ moe_ffn_pair_kernel(const __grid_constant__ CUtensorMap tmAg, const __grid_const
         int e, mt, tok0, n;
         ffn_decode(u, total_gu, s_pgu, s_pdn, E, offsets, gu, dn, gated, e, mt, tok0, n);
         const FfnGemm& G = gated ? gu : dn;
-        const CUtensorMap* tA = gated ? &tmAg : &tmAd;
         const BMaps& tB = gated ? tmBx : tmBh;
         if (!gated) {  // h rows of expert e: every gate/up unit of e has stored and counted them
           const int need = s_need[e];
@@ -676,23 +677,21 @@ moe_ffn_pair_kernel(const __grid_constant__ CUtensorMap tmAg, const __grid_const
         const uint64_t pol_w = token_tiles(offsets[e + 1] - offsets[e], gated) > 1 ? pol_shared : pol_once;
         const int N = (n + nalign - 1) & ~(nalign - 1);
         const int half = N / 2;
-        const uint32_t bytes = 2u * (kATileBytes + half * kBK * 2);
+        const uint32_t bytes = 2u * kps * (kATileBytes + half * kBK * 2);
         const int arow0 = e * G.rows_per_expert + mt * 2 * rows_cta + rank * rows_cta;
         const int trow0 = tok0 + rank * half;
-        for (int kb = 0; kb < G.KB; ++kb) {
+        const CUtensorMap* tBm = &tB.m[half / 8 - 1];
+        // one stage = kps K-blocks: [A kb0 | A kb1 | B kb0 | B kb1], ONE request per operand
+        for (int kb = 0; kb < G.KB; kb += kps) {
           { FFN_T0(); mbar_wait(&empty_bar[stage], phase ^ 1); FFN_ACC(0); }
           if (leader) mbar_arrive_expect_tx(&full_bar[stage], bytes);
-          uint8_t* st = tiles + stage * kPStageBytes;
-          if (gated && tma1) {  // gate rows then the matching up rows: the same smem image as two boxes
-            tma_load_4d_pair(st, &tmAg4, &full_bar[stage], kb * kBK, (mt * 2 + (int)rank) * rows_cta, 0, e, pol_w);
-          } else if (gated) {
-            tma_load_2d_pair(st, tA, &full_bar[stage], kb * kBK, arow0, pol_w);
-            tma_load_2d_pair(st + kAHalfBytes, tA, &full_bar[stage], kb * kBK, arow0 + G.half_rows, pol_w);
-          } else {
-            tma_load_2d_pair(st, tA, &full_bar[stage], kb * kBK, arow0, pol_w);
-          }
-          load_b_rows_pair(st + kATileBytes, tB, &full_bar[stage], kb * kBK, trow0, half, pol_x, tma1 != 0);
-          if (++stage == kPStages) { stage = 0; phase ^= 1; }
+          uint8_t* st = tiles + stage * kps * kPStageBytes;
+          if (gated)  // gate rows then the matching up rows of every K-block
+            tma_load_5d_pair(st, &tmAg, &full_bar[stage], 0, (mt * 2 + (int)rank) * rows_cta, 0, e, kb, pol_w);
+          else
+            tma_load_3d_pair(st, &tmAd, &full_bar[stage], 0, arow0, kb, pol_w);
+          tma_load_3d_pair(st + kps * kATileBytes, tBm, &full_bar[stage], 0, trow0, kb, pol_x);
+          if (++stage == nst) { stage = 0; phase ^= 1; }
         }
       }
     }
@@ -713,17 +712,20 @@ moe_ffn_pair_kernel(const __grid_constant__ CUtensorMap tmAg, const __grid_const
         { FFN_T0(); mbar_wait(&tempty_bar[acc], acc_phase ^ 1); FFN_ACC(2); }
         tc_fence_after();
         const uint32_t d0 = tmem_base + acc * kBNMax;
-        for (int kb = 0; kb < KB; ++kb) {
+        const uint32_t bstride = (N / 2) * kBK * 2;  // B bytes of one K-block (this CTA's half)
+        for (int kb = 0; kb < KB; kb += kps) {
           { FFN_T0(); mbar_wait(&full_bar[stage], phase); FFN_ACC(1); }
           tc_fence_after();
-          const uint32_t st = smem_u32(tiles + stage * kPStageBytes);
-          const uint64_t a0 = make_sdesc_sw128(st);
-          const uint64_t b0 = make_sdesc_sw128(st + kATileBytes);
+          const uint32_t st = smem_u32(tiles + stage * kps * kPStageBytes);
+          for (int j = 0; j < kps; ++j) {
+            const uint64_t a0 = make_sdesc_sw128(st + j * kATileBytes);
+            const uint64_t b0 = make_sdesc_sw128(st + kps * kATileBytes + j * bstride);
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k)
-            umma_bf16_pair(d0, a0 + 2 * k, b0 + 2 * k, idesc, (kb | k) ? 1u : 0u);
+            for (int k = 0; k < kBK / 16; ++k)
+              umma_bf16_pair(d0, a0 + 2 * k, b0 + 2 * k, idesc, ((kb + j) | k) ? 1u : 0u);
+          }
           umma_commit_pair(&empty_bar[stage], 0x3);
-          if (++stage == kPStages) { stage = 0; phase ^= 1; }
+          if (++stage == nst) { stage = 0; phase ^= 1; }
         }
         umma_commit_pair(&tfull_bar[acc], 0x3);
         if (++acc == kAccStages) { acc = 0; acc_phase ^= 1; }
@@ -832,6 +834,18 @@ int encode_bmaps(mgb::BMaps* mp, const void* act, int K, int rows) {
   for (int i = 0; i < mgb::kBMaps; ++i)
     if (mgb_host::encode_tmap_2d_bf16(&mp->m[i], act, K, rows, (uint64_t)K * 2, mgb::kBK, 8 * (i + 1)) != CUDA_SUCCESS)
       return 1;
+  return 0;
+}
+
+// K-blocked token maps of the fused FFN kernel: [rows][K/64][64] with boxes of 8 * (i + 1) rows x kps
+// K-blocks (smem image: kps consecutive [rows][64] swizzled tiles)
+int encode_bmaps_kb(mgb::BMaps* mp, const void* act, int K, int rows, int kps) {
+  const uint64_t dims[3] = {(uint64_t)mgb::kBK, (uint64_t)rows, (uint64_t)K / mgb::kBK};
+  const uint64_t strides[2] = {(uint64_t)K * 2, (uint64_t)mgb::kBK * 2};
+  for (int i = 0; i < mgb::kBMaps; ++i) {
+    const uint32_t box[3] = {(uint32_t)mgb::kBK, (uint32_t)(8 * (i + 1)), (uint32_t)kps};
+    if (mgb_host::encode_tmap_bf16(&mp->m[i], act, 3, dims, strides, box, true, true) != CUDA_SUCCESS) return 1;
+  }
   return 0;
 }
 
@@ -962,14 +976,32 @@ int mgb_moe_ffn(const void* w_gate_up, const void* w_down, const void* x_perm, c
     const int rc = mgb_moe_gemm_gate_up(w_gate_up, x_perm, offsets, E, d, f, rows_cap, h_scratch, stream);
     return rc ? rc : mgb_moe_gemm_down(w_down, h_scratch, offsets, E, d, f, rows_cap, y_out, stream);
   }
-  CUtensorMap tAg, tAd, tAg4;
+  // K-blocked maps: a box covers kps consecutive 64-column K-blocks, one request per operand per stage.
+  // kps = 1 (6 stages); MGB_FFN_KPS=2 takes 2 K-blocks per request in 3 stages of twice the size: half
+  // the requests again, but slower (same box, Mixtral: 17.17 vs 16.84 ms per replayed forward) -- the
+  // coarser ring costs more than the requests it saves once there are two per stage.
+  static const int kps_env = [] {
+    const char* e = getenv("MGB_FFN_KPS");
+    return (e && e[0] == '2') ? 2 : 1;
+  }();
+  const int kps = (kps_env == 2 && (d / mgb::kBK) % 2 == 0 && (f / mgb::kBK) % 2 == 0) ? 2 : 1;
+  CUtensorMap tAg, tAd;
   mgb::BMaps tBx, tBh;
-  using mgb_host::encode_tmap_2d_bf16;
-  const int tma1 = tma1_enabled();
-  if (encode_gate_up_4d(&tAg4, w_gate_up, E, f, d)) return MGB_ECUDA;
-  if (encode_tmap_2d_bf16(&tAg, w_gate_up, d, (uint64_t)E * 2 * f, (uint64_t)d * 2, mgb::kBK, mgb::kBM / 2) ||
-      encode_tmap_2d_bf16(&tAd, w_down, f, (uint64_t)E * d, (uint64_t)f * 2, mgb::kBK, mgb::kBM) ||
-      encode_bmaps(&tBx, x_perm, d, rows_cap) || encode_bmaps(&tBh, h_scratch, f, rows_cap))
+  {
+    const uint64_t dims[5] = {(uint64_t)mgb::kBK, (uint64_t)f, 2, (uint64_t)E, (uint64_t)d / mgb::kBK};
+    const uint64_t strides[4] = {(uint64_t)d * 2, (uint64_t)f * d * 2, (uint64_t)2 * f * d * 2, (uint64_t)mgb::kBK * 2};
+    const uint32_t box[5] = {(uint32_t)mgb::kBK, (uint32_t)mgb::kBM / 2, 2, 1, (uint32_t)kps};
+    if (mgb_host::encode_tmap_bf16(&tAg, w_gate_up, 5, dims, strides, box, true, true) != CUDA_SUCCESS)
+      return MGB_ECUDA;
+  }
+  {
+    const uint64_t dims[3] = {(uint64_t)mgb::kBK, (uint64_t)E * d, (uint64_t)f / mgb::kBK};
+    const uint64_t strides[2] = {(uint64_t)f * 2, (uint64_t)mgb::kBK * 2};
+    const uint32_t box[3] = {(uint32_t)mgb::kBK, (uint32_t)mgb::kBM, (uint32_t)kps};
+    if (mgb_host::encode_tmap_bf16(&tAd, w_down, 3, dims, strides, box, true, true) != CUDA_SUCCESS)
+      return MGB_ECUDA;
+  }
+  if (encode_bmaps_kb(&tBx, x_perm, d, rows_cap, kps) || encode_bmaps_kb(&tBh, h_scratch, f, rows_cap, kps))
     return MGB_ECUDA;
   int* cap_status = mgb_host::capacity_status_ptr();
   if (!cap_status) return MGB_ECUDA;
@@ -983,7 +1015,7 @@ int mgb_moe_ffn(const void* w_gate_up, const void* w_down, const void* x_perm, c
   }();
   const int grid = mgb_host::num_sms() & ~1;
   mgb_host::launch(mgb::moe_ffn_pair_kernel, dim3(grid), dim3(mgb::Epi<true>::kThreads), mgb::pair_smem<true>(), reinterpret_cast<cudaStream_t>(stream), nullptr,
-      tAg, tBx, tAd, tBh, tAg4, offsets, E, gu, dn, nalign, rows_cap, cap_status, sync, tma1);
+      tAg, tBx, tAd, tBh, offsets, E, gu, dn, nalign, rows_cap, cap_status, sync, kps);
   return mgb_host::launch_status();
 }
 
