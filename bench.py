@@ -36,6 +36,17 @@ sys.path.insert(0, ROOT)
 
 METRIC = "decode tokens/sec at prompt 512/gen 256"
 UNIT = "tokens/s"
+# HBM the planner keeps free beside weights + paged KV when sizing the resident batch: the engine's
+# measured non-weight, non-KV peak (tools/mem_probe.py, profiles/r2_mem_probe.json: step buffers,
+# graph pool, cuBLAS workspaces, the batched-prefill buffers, CUDA context) plus a 2 GB margin.
+# Mixtral-8x7B holds 4.2 GB there; DeepSeek-V2-Lite 10.7 GB (B x 102400 logits, MLA scratch) keeps
+# the round-1 14 GB.
+RESERVE_GB = {"mixtral-8x7b": 6.25}
+
+
+def reserve_bytes(args, arch) -> int:
+    gb = args.reserve_gb if args.reserve_gb is not None else RESERVE_GB.get(arch.name, 14.0)
+    return int(gb * 2**30)
 
 
 def _ncu_traffic(config: str, gemm: str):
@@ -219,7 +230,7 @@ def _workload_config(args, arch, world: int, ep: bool = False) -> dict:
     """The workload both arms are quoted on (the GPU arm's batch: the planner's largest resident B)."""
     from paper_2503_09716_b200.engine import resident_plan
 
-    plan = resident_plan(arch, args.prompt_len, args.decode_len, B=args.batch, reserve_bytes=args.reserve_gb << 30)
+    plan = resident_plan(arch, args.prompt_len, args.decode_len, B=args.batch, reserve_bytes=reserve_bytes(args, arch))
     where = (f"{world} B200 expert-parallel" if ep else "1 B200 resident")
     par = (f"ep{world}: experts {arch.n_experts // world} per rank, each rank's B sequences data-parallel, token "
            f"dispatch/combine fused into the permutation / down-GEMM kernels over NVLink peer memory (torch symmetric "
@@ -228,6 +239,7 @@ def _workload_config(args, arch, world: int, ep: bool = False) -> dict:
                         f"({_BASELINE_CFG.get(arch.name, 'not a BASELINE config')});"
                         f" step = {args.decode_len} decode forwards of B={plan.B} sequences per GPU",
             "batch": plan.B, "b_a": plan.b_a, "b_e": plan.b_e, "kv_policy": "resident (paged, HBM)",
+            "hbm_reserve_gb": reserve_bytes(args, arch) / 2**30,
             "parallelism": par, "l2": "inputs larger than L2 (all weights stream from HBM every forward)"}
 
 
@@ -347,7 +359,7 @@ def measure(args, arch, dist, rank, world, steps: int, warmup: int, main: bool, 
     job's ranks (PeerExpertParallel over symmetric memory), each rank decoding its own B sequences."""
     from paper_2503_09716_b200.engine import Engine, resident_plan
 
-    plan = resident_plan(arch, args.prompt_len, args.decode_len, B=args.batch, reserve_bytes=args.reserve_gb << 30)
+    plan = resident_plan(arch, args.prompt_len, args.decode_len, B=args.batch, reserve_bytes=reserve_bytes(args, arch))
     pep = None
     if ep:
         from paper_2503_09716_b200.ep import PeerExpertParallel
@@ -524,7 +536,8 @@ def main():
     ap.add_argument("--batch", type=int, default=None, help="sequences per GPU (default: planner's largest)")
     ap.add_argument("--prompt-len", type=int, default=512)
     ap.add_argument("--decode-len", type=int, default=256)
-    ap.add_argument("--reserve-gb", type=int, default=14)
+    ap.add_argument("--reserve-gb", type=float, default=None,
+                    help="HBM kept free beside weights + KV when sizing B (default: measured per model, RESERVE_GB)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-batch", type=int, default=None, help="CPU arm batch (default: the GPU arm's B)")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")

@@ -26,3 +26,15 @@ def test_workload_config_is_the_planners_resident_batch():
 
 def test_workload_config_batch_cap():
     assert bench._workload_config(_args(batch=64), get_arch("mixtral-8x7b"), 1)["batch"] == 64
+
+
+def test_measured_reserve_sizes_the_mixtral_batch():
+    """Without --reserve-gb the planner keeps the measured per-model reserve (bench.RESERVE_GB):
+    Mixtral's 6.25 GiB admits more sequences than the flat 14 GiB; DeepSeek-V2-Lite keeps 14 GiB."""
+    mix, ds = get_arch("mixtral-8x7b"), get_arch("deepseek-v2-lite")
+    cfg = bench._workload_config(_args(reserve_gb=None), mix, 1)
+    assert cfg["hbm_reserve_gb"] == bench.RESERVE_GB["mixtral-8x7b"]
+    assert cfg["batch"] == resident_plan(mix, 512, 256, reserve_bytes=int(6.25 * 2**30)).B
+    assert cfg["batch"] > resident_plan(mix, 512, 256, reserve_bytes=14 << 30).B
+    assert bench._workload_config(_args(reserve_gb=None), ds, 1)["batch"] == \
+        resident_plan(ds, 512, 256, reserve_bytes=14 << 30).B
