@@ -1,7 +1,7 @@
 """Parity on the exact configurations the bench and BASELINE.json quote (VERDICT r1 "next" #1).
 
-  - Mixtral-8x7B at the bench's batch (the planner's largest resident B on this GPU, 827 on a
-    180 GB B200: 207 tokens per expert) and DeepSeek-V2-Lite at its bench batch (6058: 568 tokens
+  - Mixtral-8x7B at the bench's batch (the planner's largest resident B on this GPU with the bench's
+    measured HBM reserve, 909 on a 180 GB B200: 227 tokens per expert) and DeepSeek-V2-Lite at its bench batch (6058: 568 tokens
     per expert), at the bench's decode context (synthetic 512-token prefill state, position 639 =
     the average context of a 512 / 256 run), full layer width, depth-truncated to 2 and 3 layers
     (DeepSeek: the dense layer 0 plus two MoE layers) so the CPU oracle finishes in about a minute.
@@ -35,7 +35,9 @@ def _bench_batch(name: str) -> int:
     from paper_2503_09716_b200.configs import get_arch
     from paper_2503_09716_b200.engine import resident_plan
 
-    return resident_plan(get_arch(name), 512, 256, reserve_bytes=14 << 30).B
+    import bench
+
+    return resident_plan(get_arch(name), 512, 256, reserve_bytes=int(bench.RESERVE_GB.get(name, 14.0) * 2**30)).B
 
 
 @pytest.mark.parametrize("name,layers", [("mixtral-8x7b", 2), ("deepseek-v2-lite", 3)])
