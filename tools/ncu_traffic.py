@@ -4,6 +4,8 @@ counts as the bench configs).  bench.py reports them as roofline.traffic.
 
   ncu --set full --clock-control none -k regex:moe_gemm -c 2 -o gpurun_out/gemm_mixtral python tools/gemm_check.py mixtral
   ncu --set full --clock-control none -k regex:moe_gemm -c 2 -o gpurun_out/gemm_dsv2 python tools/gemm_check.py dsv2
+  ncu --set full --clock-control none -k regex:moe_ffn -c 1 -o gpurun_out/ffn_mixtral_r2b \
+      python tools/gemm_prefill_bench.py mixtral-8x7b 227 ffn
   python tools/ncu_traffic.py
 """
 import csv
@@ -13,6 +15,8 @@ import subprocess
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CASES = {"mixtral-8x7b": "gpurun_out/gemm_mixtral.ncu-rep", "deepseek-v2-lite": "gpurun_out/gemm_dsv2.ncu-rep"}
+# the fused FFN launch (Mixtral-family default) at the bench's tokens per expert (B = 909: 227)
+FFN = {"mixtral-8x7b": ("gpurun_out/ffn_mixtral_r2b.ncu-rep", "tools/gemm_prefill_bench.py mixtral-8x7b 227 ffn")}
 
 
 def launches(path):
@@ -39,6 +43,12 @@ for cfg, rep in CASES.items():
         key = "gate_up" if targs.split(",")[0].strip() in ("1", "true") else "down"
         out.setdefault(cfg, {})[key] = {"dram_bytes": b, "kernel": name.split("(")[0],
                                         "source": f"ncu --set full of tools/gemm_check.py ({os.path.basename(rep)})"}
+for cfg, (rep, cmd) in FFN.items():
+    path = os.path.join(ROOT, rep)
+    if os.path.exists(path):
+        for name, b in launches(path):
+            out.setdefault(cfg, {})["ffn"] = {"dram_bytes": b, "kernel": name.split("(")[0],
+                                              "source": f"ncu --set full of {cmd} ({os.path.basename(rep)})"}
 with open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w") as f:
     json.dump(out, f, indent=1)
 print(json.dumps(out, indent=1))

@@ -13,10 +13,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="mixtral-8x7b")
 ap.add_argument("--batch", type=int, default=None)
 ap.add_argument("--steps", type=int, default=2)
-ap.add_argument("--reserve-gb", type=int, default=14)
+ap.add_argument("--reserve-gb", type=float, default=None, help="default: bench.py's measured per-model reserve")
 args = ap.parse_args()
 arch = get_arch(args.config)
-plan = resident_plan(arch, 512, 256, B=args.batch, reserve_bytes=args.reserve_gb << 30)
+import bench  # noqa: E402
+
+plan = resident_plan(arch, 512, 256, B=args.batch, reserve_bytes=bench.reserve_bytes(args, arch))
 eng = Engine(arch, plan, prompt_len=512, decode_len=256, use_graph=False)
 eng.synthetic_prefill()
 eng.reset(640)
