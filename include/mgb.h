@@ -120,6 +120,16 @@ int mgb_decode_attn_gqa_sched(const void* q, const void* k_cache, const void* v_
                               int max_pages, const int* seq_lens, int B, int Hq, int Hkv, int head_dim, float scale,
                               void* out, int* sched, void* stream);
 
+/* ... with the step's RoPE + KV append fused in (resident paged KV): qkv [B, (Hq + 2 Hkv) * head_dim]
+ * raw projections of the new tokens, positions [B]; rotates q / k (HF rotate_half, cos_t / sin_t
+ * [max_pos, head_dim / 2] fp32), writes k / v into each token's page slot and seq_lens[b] =
+ * positions[b] + 1, then attends over positions 0..positions[b].  Equals mgb_rope_append_gqa followed
+ * by mgb_decode_attn_gqa_sched bit for bit.  Covers PRE_ATTENTION's KV write + ATTN_MECH_GPU
+ * (offload_dag.py:359-402).  sched as for mgb_decode_attn_gqa_sched (may be NULL). */
+int mgb_decode_attn_gqa_rope(const void* qkv, const int* positions, const float* cos_t, const float* sin_t,
+                             void* k_cache, void* v_cache, const int* block_table, int max_pages, int* seq_lens, int B,
+                             int Hq, int Hkv, int head_dim, float scale, void* out, int* sched, void* stream);
+
 /* ---- ATTN_MECH_GPU for MLA models (DeepSeek-V2; model_catalog.py:242-295 prices it) -------
  * Absorbed latent attention: q_lat [H,B,R], q_pe [B,H,RP], latent pages of mgb_mla_page_size()
  * tokens and mgb_mla_page_elems(R, RP) bf16 elements, laid out as 64-dim blocks

@@ -46,6 +46,7 @@ SIGNATURES: dict[str, list] = {
     # attention (attn_gqa.cu)
     "mgb_decode_attn_gqa": [P, P, P, P, I, P, I, I, I, I, F, P, P],
     "mgb_decode_attn_gqa_sched": [P, P, P, P, I, P, I, I, I, I, F, P, P, P],
+    "mgb_decode_attn_gqa_rope": [P, P, P, P, P, P, P, I, P, I, I, I, I, F, P, P, P],
     # elementwise.cu
     "mgb_add_rmsnorm": [P, P, P, F, I, I, P, P, P],
     "mgb_rope_append_gqa": [P, I, I, P, P, P, I, I, I, P, I, P, P, P, P, P],

@@ -71,6 +71,21 @@ MGB_DEVINL void mma_bf16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t
 }
 MGB_DEVINL void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
+// Fused RoPE + KV append (mgb_decode_attn_gqa_rope): the kernel takes the raw fused qkv rows
+// [Hq | Hkv | Hkv] x HD instead of RoPE'd q, rotates the item's G query heads while loading them,
+// and its producer warp rotates the item's new k row, copies its v row into the token's slot of
+// the last K / V page (same arithmetic as rope_append_gqa_kernel, mgb::rope_rot8) and fences the
+// stores into the async proxy before it issues that item's page loads.  Cache length = position + 1.
+struct GqaRope {
+  const __nv_bfloat16* qkv;  // [B, (Hq + 2 Hkv) * HD]; null: plain decode (q RoPE'd, KV appended)
+  const int* positions;      // [B] position of the new token
+  const float* cos_t;        // [max_pos, HD / 2]
+  const float* sin_t;
+  __nv_bfloat16* k_cache;    // the same pages as k_cache / v_cache, written at the new token's slot
+  __nv_bfloat16* v_cache;
+  int* seq_lens;             // [B] written = position + 1 (by the kv-head-0 item)
+};
+
 template <int HD, int G>
 __global__ void __launch_bounds__(kAttnThreads, 2)
 decode_attn_gqa_kernel(const __nv_bfloat16* __restrict__ q,       // [B, Hkv*G, HD]
@@ -79,7 +94,8 @@ decode_attn_gqa_kernel(const __nv_bfloat16* __restrict__ q,       // [B, Hkv*G, 
                        const int* __restrict__ block_table, int max_pages,
                        const int* __restrict__ seq_lens, int B, int Hkv, float scale_log2,
                        __nv_bfloat16* __restrict__ out,            // [B, Hkv*G*HD]
-                       int* __restrict__ sched) {  // optional {next item, exit ticket}
+                       int* __restrict__ sched,   // optional {next item, exit ticket}
+                       const GqaRope rp) {
   mgb::pdl_enter();
   static_assert(G <= 8 && HD % 16 == 0, "GQA tile: G <= 8 query heads per kv head");
   using S = GqaSmem<HD, G>;
@@ -95,7 +111,7 @@ decode_attn_gqa_kernel(const __nv_bfloat16* __restrict__ q,       // [B, Hkv*G, 
   // work runs out, instead of the static share of 22-23 items leaving the last wave part-idle); without
   // it, the static round-robin share.  Item -1 ends the CTA.
   __shared__ int s_item[4];
-  __shared__ __align__(8) uint64_t item_full[4], item_empty[4];
+  __shared__ __align__(8) uint64_t item_full[4], item_empty[4], appended[4];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_items = B * Hkv;
@@ -107,6 +123,7 @@ decode_attn_gqa_kernel(const __nv_bfloat16* __restrict__ q,       // [B, Hkv*G, 
     for (int s = 0; s < 4; ++s) {
       mbar_init(&item_full[s], 1);
       mbar_init(&item_empty[s], kConsumerWarps);
+      mbar_init(&appended[s], 1);
     }
     fence_mbar_init();
   }
@@ -126,9 +143,19 @@ decode_attn_gqa_kernel(const __nv_bfloat16* __restrict__ q,       // [B, Hkv*G, 
         mbar_arrive(&item_full[k & 3]);
         if (it < 0) break;
         const int b = it / Hkv, h = it - b * Hkv;
-        const int np = (seq_lens[b] + kPage - 1) / kPage;
+        int len;
+        if (rp.qkv) {
+          const int pos = rp.positions[b];
+          len = pos < 0 ? 0 : min(pos + 1, max_pages * kPage);
+        } else {
+          len = seq_lens[b];
+        }
+        const int np = (len + kPage - 1) / kPage;
         const int* bt = block_table + (size_t)b * max_pages;
         for (int p = 0; p < np; ++p) {
+          // fused append: the last page holds the new token, which the consumers store at the item's
+          // start -- by then this producer is normally still a few pages behind
+          if (rp.qkv && p == np - 1) mbar_wait(&appended[k & 3], (k >> 2) & 1);
           mbar_wait(&empty[stage], phase ^ 1);
           gqa_trace(0, gp++);  // 0: stage free, page load issued
           const size_t blk = ((size_t)bt[p] * Hkv + h) * S::kTileElems;
@@ -153,16 +180,80 @@ decode_attn_gqa_kernel(const __nv_bfloat16* __restrict__ q,       // [B, Hkv*G, 
     const int it = s_item[item & 3];
     if (it < 0) break;
     const int b = it / Hkv, h = it - b * Hkv;
-    const int len = seq_lens[b];
+    int len;
+    if (rp.qkv) {
+      const int pos = rp.positions[b];
+      len = pos < 0 ? 0 : min(pos + 1, max_pages * kPage);
+    } else {
+      len = seq_lens[b];
+    }
     if (threadIdx.x == 0) gqa_trace(4, item);  // 4: item start (consumers)
+    if (rp.qkv && warp == 0) {
+      // the item's new token: k rotated, v copied into its slot of the last K / V page (lanes
+      // 0..HD/16-1: one k rotation pair of 8-dim chunks each, the next HD/16 lanes: v), fenced into
+      // the async proxy, then the producer may load that page
+      const int pos = rp.positions[b];
+      if (pos >= 0 && pos < max_pages * kPage) {
+        constexpr int half = HD / 16;
+        if (lane < 2 * half) {
+          const int Hq = Hkv * G;
+          const bool is_k = lane < half;
+          const int j = is_k ? lane : lane - half;
+          const uint4* src = reinterpret_cast<const uint4*>(rp.qkv + (size_t)b * (Hq + 2 * Hkv) * HD +
+                                                            (size_t)(Hq + (is_k ? 0 : Hkv) + h) * HD);
+          uint4 ol = src[j], oh = src[j + half];
+          const int page = block_table[(size_t)b * max_pages + pos / kPage], slot = pos % kPage;
+          if (is_k)
+            rope_rot8(ol, oh, rp.cos_t + (size_t)pos * (HD / 2) + j * 8, rp.sin_t + (size_t)pos * (HD / 2) + j * 8,
+                      ol, oh);
+          __nv_bfloat16* blk = (is_k ? rp.k_cache : rp.v_cache) + ((size_t)page * Hkv + h) * HD * kPage;
+          *reinterpret_cast<uint4*>(blk + ((size_t)j * kPage + slot) * 8) = ol;
+          *reinterpret_cast<uint4*>(blk + ((size_t)(j + half) * kPage + slot) * 8) = oh;
+          asm volatile("fence.proxy.async.global;" ::: "memory");  // generic stores -> the page's bulk copy
+        }
+        if (h == 0 && lane == 0) rp.seq_lens[b] = pos + 1;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&appended[item & 3]);
+    }
     const int np = (len + kPage - 1) / kPage;
     // Q A-fragments (rows = the G query heads of this kv head; rows >= G are zero)
     uint32_t qa[KSTEPS][2];
-    const __nv_bfloat16* qrow = q + ((size_t)b * Hkv * G + (size_t)h * G + (row_ok ? g : 0)) * HD;
+    if (rp.qkv) {
+      // raw q rows, rotated here: fragment dims d and d + HD/2 (k-steps ks and ks + KSTEPS/2) are one
+      // rotation pair, so every lane holds both halves it needs
+      const int Hq = Hkv * G;
+      const int pos = min(max(rp.positions[b], 0), max_pages * kPage - 1);
+      const __nv_bfloat16* qrow = rp.qkv + (size_t)b * (Hq + 2 * Hkv) * HD + ((size_t)h * G + (row_ok ? g : 0)) * HD;
+      const float* cr = rp.cos_t + (size_t)pos * (HD / 2);
+      const float* sr = rp.sin_t + (size_t)pos * (HD / 2);
 #pragma unroll
-    for (int ks = 0; ks < KSTEPS; ++ks) {
-      qa[ks][0] = row_ok ? *reinterpret_cast<const uint32_t*>(qrow + ks * 16 + 2 * t) : 0u;
-      qa[ks][1] = row_ok ? *reinterpret_cast<const uint32_t*>(qrow + ks * 16 + 8 + 2 * t) : 0u;
+      for (int ks = 0; ks < KSTEPS / 2; ++ks) {
+#pragma unroll
+        for (int hv = 0; hv < 2; ++hv) {
+          const int dd = ks * 16 + 8 * hv + 2 * t;  // dims dd, dd + 1 (< HD/2) and their partners + HD/2
+          if (row_ok) {
+            const uint32_t lo = *reinterpret_cast<const uint32_t*>(qrow + dd);
+            const uint32_t hi = *reinterpret_cast<const uint32_t*>(qrow + dd + HD / 2);
+            const float2 c = *reinterpret_cast<const float2*>(cr + dd), sn = *reinterpret_cast<const float2*>(sr + dd);
+            const float a0 = bf16lo(lo), a1 = bf16hi(lo), b0 = bf16lo(hi), b1 = bf16hi(hi);
+            qa[ks][hv] = pack_bf16x2(bf16_round(a0 * c.x) + bf16_round(-b0 * sn.x),
+                                     bf16_round(a1 * c.y) + bf16_round(-b1 * sn.y));
+            qa[ks + KSTEPS / 2][hv] = pack_bf16x2(bf16_round(b0 * c.x) + bf16_round(a0 * sn.x),
+                                                  bf16_round(b1 * c.y) + bf16_round(a1 * sn.y));
+          } else {
+            qa[ks][hv] = 0u;
+            qa[ks + KSTEPS / 2][hv] = 0u;
+          }
+        }
+      }
+    } else {
+      const __nv_bfloat16* qrow = q + ((size_t)b * Hkv * G + (size_t)h * G + (row_ok ? g : 0)) * HD;
+#pragma unroll
+      for (int ks = 0; ks < KSTEPS; ++ks) {
+        qa[ks][0] = row_ok ? *reinterpret_cast<const uint32_t*>(qrow + ks * 16 + 2 * t) : 0u;
+        qa[ks][1] = row_ok ? *reinterpret_cast<const uint32_t*>(qrow + ks * 16 + 8 + 2 * t) : 0u;
+      }
     }
     float o[NT][4];
 #pragma unroll
@@ -292,7 +383,7 @@ decode_attn_gqa_kernel(const __nv_bfloat16* __restrict__ q,       // [B, Hkv*G, 
 
 template <int HD, int G>
 int launch_gqa(const void* q, const void* kc, const void* vc, const int* bt, int max_pages, const int* lens, int B,
-               int Hkv, float scale, void* out, cudaStream_t st, int* sched) {
+               int Hkv, float scale, void* out, cudaStream_t st, int* sched, const GqaRope& rp) {
   using S = GqaSmem<HD, G>;
   if (const int rc = mgb_host::ensure_max_smem((const void*)decode_attn_gqa_kernel<HD, G>, (int)S::kBytes)) return rc;
   const int items = B * Hkv;
@@ -306,11 +397,30 @@ int launch_gqa(const void* q, const void* kc, const void* vc, const int* bt, int
   mgb_host::launch(decode_attn_gqa_kernel<HD, G>, dim3(grid), dim3(kAttnThreads), S::kBytes, st, nullptr,
       reinterpret_cast<const __nv_bfloat16*>(q), reinterpret_cast<const __nv_bfloat16*>(kc),
       reinterpret_cast<const __nv_bfloat16*>(vc), bt, max_pages, lens, B, Hkv, scale * 1.4426950408889634f,
-      reinterpret_cast<__nv_bfloat16*>(out), sched);
+      reinterpret_cast<__nv_bfloat16*>(out), sched, rp);
   return mgb_host::launch_status();
 }
 
 }  // namespace mgb
+
+namespace {
+int gqa_dispatch(const void* q, const void* k_cache, const void* v_cache, const int* block_table, int max_pages,
+                 const int* seq_lens, int B, int Hq, int Hkv, int head_dim, float scale, void* out, int* sched,
+                 const mgb::GqaRope& rp, cudaStream_t st) {
+  const int G = Hq / Hkv;
+#define MGB_GQA_CASE(HD_, G_) \
+  if (head_dim == HD_ && G == G_)                                                                                  \
+    return mgb::launch_gqa<HD_, G_>(q, k_cache, v_cache, block_table, max_pages, seq_lens, B, Hkv, scale, out, st, \
+                                    sched, rp);
+  MGB_GQA_CASE(128, 4)
+  MGB_GQA_CASE(128, 6)
+  MGB_GQA_CASE(128, 8)
+  MGB_GQA_CASE(64, 4)
+  MGB_GQA_CASE(32, 4)
+#undef MGB_GQA_CASE
+  return MGB_EINVAL;
+}
+}  // namespace
 
 extern "C" {
 
@@ -345,17 +455,23 @@ int mgb_decode_attn_gqa_sched(const void* q, const void* k_cache, const void* v_
                               int max_pages, const int* seq_lens, int B, int Hq, int Hkv, int head_dim, float scale,
                               void* out, int* sched, void* stream) {
   if (B < 1 || Hkv < 1 || Hq % Hkv) return MGB_EINVAL;
-  const int G = Hq / Hkv;
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-#define MGB_GQA_CASE(HD_, G_) \
-  if (head_dim == HD_ && G == G_) return mgb::launch_gqa<HD_, G_>(q, k_cache, v_cache, block_table, max_pages, seq_lens, B, Hkv, scale, out, st, sched);
-  MGB_GQA_CASE(128, 4)
-  MGB_GQA_CASE(128, 6)
-  MGB_GQA_CASE(128, 8)
-  MGB_GQA_CASE(64, 4)
-  MGB_GQA_CASE(32, 4)
-#undef MGB_GQA_CASE
-  return MGB_EINVAL;
+  return gqa_dispatch(q, k_cache, v_cache, block_table, max_pages, seq_lens, B, Hq, Hkv, head_dim, scale, out, sched,
+                      mgb::GqaRope{}, reinterpret_cast<cudaStream_t>(stream));
+}
+
+// Decode attention with the step's RoPE + KV append fused in (replaces mgb_rope_append_gqa +
+// mgb_decode_attn_gqa_sched for resident paged KV): qkv [B, (Hq + 2 Hkv) * head_dim] are the raw
+// projections of the B new tokens, positions[b] their positions; the new k (rotated) and v land in
+// the token's slot of its page, seq_lens[b] = positions[b] + 1, out = attention over positions
+// 0..positions[b].  Same numerics as the two-launch path (tests/test_kernels_gpu.py).
+int mgb_decode_attn_gqa_rope(const void* qkv, const int* positions, const float* cos_t, const float* sin_t,
+                             void* k_cache, void* v_cache, const int* block_table, int max_pages, int* seq_lens, int B,
+                             int Hq, int Hkv, int head_dim, float scale, void* out, int* sched, void* stream) {
+  if (B < 1 || Hkv < 1 || Hq % Hkv || !qkv || !positions || !cos_t || !sin_t || !seq_lens) return MGB_EINVAL;
+  const mgb::GqaRope rp{reinterpret_cast<const __nv_bfloat16*>(qkv), positions, cos_t, sin_t,
+                        reinterpret_cast<__nv_bfloat16*>(k_cache), reinterpret_cast<__nv_bfloat16*>(v_cache), seq_lens};
+  return gqa_dispatch(nullptr, k_cache, v_cache, block_table, max_pages, seq_lens, B, Hq, Hkv, head_dim, scale, out,
+                      sched, rp, reinterpret_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

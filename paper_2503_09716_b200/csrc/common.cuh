@@ -31,6 +31,25 @@ MGB_DEVINL uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&h);
 }
+// HF rotate_half RoPE of one rotation pair of 8-dim chunks (lo = dims j..j+7, hi = dims j+hd/2..):
+// lo' = bf16(lo*cos) + bf16(-hi*sin), hi' = bf16(hi*cos) + bf16(lo*sin), each rounded to bf16
+// (modeling_mixtral.py apply_rotary_pos_emb in bf16).  cr / sr: the 8 fp32 cos / sin of the chunk.
+MGB_DEVINL void rope_rot8(const uint4& xl, const uint4& xh, const float* cr, const float* sr, uint4& ol, uint4& oh) {
+  const float4 c0 = *reinterpret_cast<const float4*>(cr), c1 = *reinterpret_cast<const float4*>(cr + 4);
+  const float4 s0 = *reinterpret_cast<const float4*>(sr), s1 = *reinterpret_cast<const float4*>(sr + 4);
+  const float cs[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+  const float sn[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+  const float a[8] = {bf16lo(xl.x), bf16hi(xl.x), bf16lo(xl.y), bf16hi(xl.y), bf16lo(xl.z), bf16hi(xl.z), bf16lo(xl.w), bf16hi(xl.w)};
+  const float b[8] = {bf16lo(xh.x), bf16hi(xh.x), bf16lo(xh.y), bf16hi(xh.y), bf16lo(xh.z), bf16hi(xh.z), bf16lo(xh.w), bf16hi(xh.w)};
+  float rl[8], rh[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    rl[k] = bf16_round(a[k] * cs[k]) + bf16_round(-b[k] * sn[k]);
+    rh[k] = bf16_round(b[k] * cs[k]) + bf16_round(a[k] * sn[k]);
+  }
+  ol = make_uint4(pack_bf16x2(rl[0], rl[1]), pack_bf16x2(rl[2], rl[3]), pack_bf16x2(rl[4], rl[5]), pack_bf16x2(rl[6], rl[7]));
+  oh = make_uint4(pack_bf16x2(rh[0], rh[1]), pack_bf16x2(rh[2], rh[3]), pack_bf16x2(rh[4], rh[5]), pack_bf16x2(rh[6], rh[7]));
+}
 
 // ----------------------------------------------------------------------------------------
 // shared-memory addressing, mbarriers

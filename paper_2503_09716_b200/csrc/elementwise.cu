@@ -196,24 +196,8 @@ __global__ void rope_append_gqa_kernel(const __nv_bfloat16* __restrict__ qkv, in
   const int slot = pos % kPageTok;
   if (seq_lens && i == 0) seq_lens[seq] = pos + 1;  // cache length after the append
   uint4 ol = xl, oh = xh;
-  if (hh < Hq + Hkv) {
-    const float* cr = cos_t + (size_t)pos * (hd / 2) + j * 8;
-    const float* sr = sin_t + (size_t)pos * (hd / 2) + j * 8;
-    const float4 c0 = *reinterpret_cast<const float4*>(cr), c1 = *reinterpret_cast<const float4*>(cr + 4);
-    const float4 s0 = *reinterpret_cast<const float4*>(sr), s1 = *reinterpret_cast<const float4*>(sr + 4);
-    const float cs[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-    const float sn[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
-    const float a[8] = {bf16lo(xl.x), bf16hi(xl.x), bf16lo(xl.y), bf16hi(xl.y), bf16lo(xl.z), bf16hi(xl.z), bf16lo(xl.w), bf16hi(xl.w)};
-    const float b[8] = {bf16lo(xh.x), bf16hi(xh.x), bf16lo(xh.y), bf16hi(xh.y), bf16lo(xh.z), bf16hi(xh.z), bf16lo(xh.w), bf16hi(xh.w)};
-    float rl[8], rh[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {  // HF rotate_half: lo' = lo*cos - hi*sin, hi' = hi*cos + lo*sin (bf16 products)
-      rl[k] = bf16_round(a[k] * cs[k]) + bf16_round(-b[k] * sn[k]);
-      rh[k] = bf16_round(b[k] * cs[k]) + bf16_round(a[k] * sn[k]);
-    }
-    ol = make_uint4(pack_bf16x2(rl[0], rl[1]), pack_bf16x2(rl[2], rl[3]), pack_bf16x2(rl[4], rl[5]), pack_bf16x2(rl[6], rl[7]));
-    oh = make_uint4(pack_bf16x2(rh[0], rh[1]), pack_bf16x2(rh[2], rh[3]), pack_bf16x2(rh[4], rh[5]), pack_bf16x2(rh[6], rh[7]));
-  }
+  if (hh < Hq + Hkv)
+    rope_rot8(xl, xh, cos_t + (size_t)pos * (hd / 2) + j * 8, sin_t + (size_t)pos * (hd / 2) + j * 8, ol, oh);
   if (hh < Hq) {
     uint4* dst = reinterpret_cast<uint4*>(q_out + ((size_t)t * Hq + hh) * hd);
     dst[j] = ol;

@@ -301,6 +301,12 @@ class Engine:
         # stays on the unfused kernels, whose cuBLAS logits GEMM and wide top-k grid win there)
         self.fused_route = (os.environ.get("MGB_FUSED_ROUTE", "1") != "0" and not self.offload and self.ep is None
                             and a.n_experts <= 16 and ops.moe_route_supported(B, a.hidden, a.n_experts))
+        # GQA decode: the step's RoPE + KV append inside the attention launch (mgb_decode_attn_gqa_rope,
+        # MGB_FUSED_ROPE=1) when the pages are the resident store and no CPU share reads the RoPE'd q.
+        # Off by default: bit-identical and faster eagerly (12.47 vs 12.29 + 0.41 ms per Mixtral forward),
+        # but the graph-replayed step measured 0.3-0.4 ms SLOWER in same-box A/Bs
+        self.fused_rope = (os.environ.get("MGB_FUSED_ROPE", "0") == "1" and not self.mla
+                           and kv_policy == "resident" and self.n_cpu == 0)
         self.kernel_launches_per_step = self._count_launches()
         self.host_pos = 0
 
@@ -804,14 +810,20 @@ class Engine:
             if l == 0:  # later layers get h from the previous layer's fused combine+norm
                 ops.add_rmsnorm(b.x[s0:s1], W["ln1"], a.rms_eps, b.h[s0:s1])
             torch.mm(b.h[s0:s1], W["wqkv"].t(), out=b.qkv[s0:s1])
-            (kc, vc), table = self._kv_views(l, j, 0, s1, "append")
-            ops.rope_append_gqa(b.qkv[s0:s1], s0, b.positions, self.cos_t, self.sin_t, Hq, Hkv, hd,
-                                table, kc, vc, b.q[s0:s1], b.seq_lens)
+            if not self.fused_rope:  # else the attention launch rotates and appends
+                (kc, vc), table = self._kv_views(l, j, 0, s1, "append")
+                ops.rope_append_gqa(b.qkv[s0:s1], s0, b.positions, self.cos_t, self.sin_t, Hq, Hkv, hd,
+                                    table, kc, vc, b.q[s0:s1], b.seq_lens)
         elif j.kind == "attn_mech_gpu":
             s0, s1 = self._mb_range(j)
             (kc, vc), table = self._kv_views(l, j, s0, s1, "attend")
-            ops.decode_attn_gqa(b.q[s0:s1], kc, vc, table[:s1 - s0], b.seq_lens[s0:s1], Hq, Hkv, hd,
-                                b.attn[s0:s1], sched=self.attn_sched)
+            if self.fused_rope:
+                ops.decode_attn_gqa_rope(b.qkv[s0:s1], b.positions[s0:s1], self.cos_t, self.sin_t, kc, vc,
+                                         table[:s1 - s0], b.seq_lens[s0:s1], Hq, Hkv, hd, b.attn[s0:s1],
+                                         sched=self.attn_sched)
+            else:
+                ops.decode_attn_gqa(b.q[s0:s1], kc, vc, table[:s1 - s0], b.seq_lens[s0:s1], Hq, Hkv, hd,
+                                    b.attn[s0:s1], sched=self.attn_sched)
         elif j.kind == "post_attention":
             torch.mm(b.attn, W["wo"].t(), out=b.o)
             if not self._route_fused(l):  # else the router job's fused kernel adds + normalises
@@ -863,7 +875,8 @@ class Engine:
         for l in range(self.arch.layers):
             fused = self._route_fused(l)  # one mgb_moe_route instead of add_rmsnorm + router_topk + permute
             for j in self.layer_jobs[l]:
-                n += {"pre_attention": 2 if l == 0 else 1, "attn_mech_gpu": 1, "post_attention": 0 if fused else 1,
+                pre = (1 if l == 0 else 0) + (0 if getattr(self, "fused_rope", False) else 1)
+                n += {"pre_attention": pre, "attn_mech_gpu": 1, "post_attention": 0 if fused else 1,
                       "router": 1 if fused else 2}.get(j.kind, 0)
             n += 3  # gate_up, down, combine
         return n + 2  # argmax, advance  (cuBLAS GEMMs are library launches, not counted)

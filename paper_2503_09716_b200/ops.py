@@ -183,6 +183,20 @@ def decode_attn_gqa(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tenso
                  _p(seq_lens), B, Hq, Hkv, hd, scale, _p(out), _p(sched), _s())
 
 
+def decode_attn_gqa_rope(qkv: torch.Tensor, positions: torch.Tensor, cos_t: torch.Tensor, sin_t: torch.Tensor,
+                         k_cache: torch.Tensor, v_cache: torch.Tensor, block_table: torch.Tensor,
+                         seq_lens: torch.Tensor, Hq: int, Hkv: int, hd: int, out: torch.Tensor,
+                         scale: float | None = None, sched: torch.Tensor | None = None) -> None:
+    """Decode attention with the step's RoPE + KV append fused in: qkv [B, (Hq + 2 Hkv) hd] raw
+    projections, positions [B]; appends the rotated k / the v row at each position, writes
+    seq_lens = positions + 1 and out = attention over positions 0..pos (= rope_append_gqa followed by
+    decode_attn_gqa, bit-identical)."""
+    B = qkv.shape[0]
+    scale = hd ** -0.5 if scale is None else scale
+    nat.call("mgb_decode_attn_gqa_rope", _p(qkv), _p(positions), _p(cos_t), _p(sin_t), _p(k_cache), _p(v_cache),
+             _p(block_table), block_table.shape[1], _p(seq_lens), B, Hq, Hkv, hd, scale, _p(out), _p(sched), _s())
+
+
 def prefill_attn_supported(hd_qk: int, hd_v: int) -> bool:
     return bool(nat.value("mgb_prefill_attn_supported", hd_qk, hd_v))
 

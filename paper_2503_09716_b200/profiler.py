@@ -227,6 +227,7 @@ def profile_engine(arch: ModelArch | str, token_grid: Sequence[int] | None = Non
     spec = ModelSpec.from_document(one.model_spec_document())
     plan = BatchingPlan(Tmax, Tmax, 1 << 20, 0.0, 0, spec.model_bytes)
     eng = Engine(one, plan, prompt_len=max(1, ctx_max - 1), decode_len=1, use_graph=False)
+    eng.fused_rope = False  # pre_attention's RoPE/append and the attention are timed as separate modules
     eng.synthetic_prefill()
     a, b, l = eng.arch, eng.buf, first_moe
     W = eng._layer_weights(l)

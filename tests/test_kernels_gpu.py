@@ -262,6 +262,49 @@ def test_rope_append_matches_oracle():
     assert torch.equal(lens.cpu(), torch.full((B,), pos + 1, dtype=torch.int32))
 
 
+@pytest.mark.parametrize("B,Hq,Hkv,hd", [(37, 32, 8, 128), (300, 32, 8, 128), (9, 8, 2, 32), (5, 16, 4, 64)])
+def test_decode_attn_gqa_rope_fused_matches_two_launches(B, Hq, Hkv, hd):
+    """mgb_decode_attn_gqa_rope (RoPE + KV append inside the attention launch) against
+    mgb_rope_append_gqa followed by mgb_decode_attn_gqa_sched on copies of the same cache: ragged
+    positions (first slot of a page, page boundaries, the last planned slot), pages holding garbage
+    past each sequence's end -> identical attention output, K / V pages and seq_lens, bit for bit."""
+    ops = _ops()
+    page = ops.kv_page_size()
+    pps = 5
+    g = torch.Generator().manual_seed(B + hd)
+    positions = torch.randint(0, pps * page, (B,), generator=g, dtype=torch.int32)
+    positions[:4] = torch.tensor([0, page, page - 1, pps * page - 1], dtype=torch.int32)[:min(4, B)]
+    qkv = uniform_bf16((B, (Hq + 2 * Hkv) * hd), 9, B, 1.0).cuda()
+    theta = 1e6
+    inv = 1.0 / (theta ** (torch.arange(0, hd, 2, dtype=torch.int64).float() / hd))
+    fr = torch.arange(pps * page).float()[:, None] * inv[None]
+    cos_t, sin_t = fr.cos().to(BF16).float().cuda(), fr.sin().to(BF16).float().cuda()
+    kc = uniform_bf16((B * pps * Hkv * hd * page,), 10, B, 1.0).cuda()
+    vc = uniform_bf16((B * pps * Hkv * hd * page,), 11, B, 1.0).cuda()
+    perm = torch.randperm(B * pps, generator=g).to(torch.int32)
+    bt = perm.view(B, pps).cuda()
+    pos_d = positions.cuda()
+    # two launches
+    k1, v1 = kc.clone(), vc.clone()
+    q1 = torch.zeros(B, Hq * hd, dtype=BF16, device="cuda")
+    lens1 = torch.zeros(B, dtype=torch.int32, device="cuda")
+    out1 = torch.zeros(B, Hq * hd, dtype=BF16, device="cuda")
+    ops.rope_append_gqa(qkv, 0, pos_d, cos_t, sin_t, Hq, Hkv, hd, bt, k1, v1, q1, lens1)
+    ops.decode_attn_gqa(q1, k1, v1, bt, lens1, Hq, Hkv, hd, out1, sched=torch.zeros(2, dtype=torch.int32, device="cuda"))
+    # fused, twice (the scheduler counter returns to zero)
+    sched = torch.zeros(2, dtype=torch.int32, device="cuda")
+    for _ in range(2):
+        k2, v2 = kc.clone(), vc.clone()
+        lens2 = torch.zeros(B, dtype=torch.int32, device="cuda")
+        out2 = torch.zeros(B, Hq * hd, dtype=BF16, device="cuda")
+        ops.decode_attn_gqa_rope(qkv, pos_d, cos_t, sin_t, k2, v2, bt, lens2, Hq, Hkv, hd, out2, sched=sched)
+    torch.cuda.synchronize()
+    assert torch.equal(lens2, lens1) and torch.equal(lens1.cpu(), positions + 1)
+    assert torch.equal(k2, k1) and torch.equal(v2, v1)
+    assert torch.equal(out2, out1)
+    assert int(sched.abs().sum()) == 0
+
+
 def test_argmax_first_index():
     ops = _ops()
     lg = torch.randn(9, 32000).to(BF16)
