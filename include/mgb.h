@@ -56,8 +56,10 @@ int mgb_router_topk(const void* x, const void* w_gate, const float* logits_in, i
  * h = RMSNorm(x) * ln_w), router logits on the tensor cores, softmax / top-k, counts / offsets and
  * the stable expert-major permutation of h into x_perm -- one launch for ROUTER + the grouping in
  * front of EXPERT_COMPUTE (offload_dag.py:418-463).  chunk_hist: mgb_moe_route_chunks(T) x E ints;
- * sync: 2 ints zeroed once.  -1 (and no launch) when T is beyond one co-resident grid
- * (mgb_moe_route_supported); the unfused entry points cover every T. */
+ * sync: 2 ints zeroed once (left reusable).  -1 (and no launch) when T is beyond one co-resident
+ * grid (mgb_moe_route_supported); the unfused entry points cover every T.
+ * mgb_moe_route_supported: 0 = not covered, 1 = covered, 2 = covered in one pass (one chunk per CTA);
+ * h_out may then be NULL (the normalised rows land only in x_perm). */
 int mgb_moe_route_chunks(int T);
 int mgb_moe_route_stamps(long long* stamps); /* profiling: per-CTA phase globaltimer stamps [G][16], NULL = off */
 int mgb_moe_route_supported(int T, int d, int E);

@@ -179,6 +179,17 @@ MGB_DEVINL void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint
       : "memory");
 }
 
+// 1-D bulk copy shared -> global (TMA engine; bulk-group completion, per issuing thread).  The smem
+// source must have been fenced into the async proxy (fence_proxy_async_smem) by its writers.
+MGB_DEVINL void bulk_store(void* gdst, const void* smem_src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"(smem_u32(smem_src)), "r"(bytes)
+               : "memory");
+}
+MGB_DEVINL void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// this thread's bulk stores have finished READING smem (the buffer may be reused / the CTA may exit)
+MGB_DEVINL void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+
 // 1-D bulk copy global -> the same smem offset of every CTA in ctaMask (cluster multicast); each
 // destination CTA's mbarrier at bar's offset receives complete_tx for the bytes landing there
 MGB_DEVINL void bulk_load_multicast(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar, uint16_t mask,

@@ -11,12 +11,12 @@
 //
 // Structure: a persistent grid of G co-resident CTAs (G <= half the device's resident capacity, so
 // two such kernels on different streams can never starve each other), each owning <= kMaxOwn
-// 16-token chunks:
+// 8-token chunks:
 //   phase 1 (per chunk): residual add + RMSNorm (warp per token, the normalised rows stay in smem),
 //            logits = H_chunk W_r^T on mma.sync m16n8k16 (16 tokens x 8 experts per tile, K split
 //            across warps when E is small), softmax + top-k (warp per token), chunk histogram and
 //            stable in-chunk ranks;
-//   grid barrier (the only one);
+//   grid barrier (the only one; one atomic per CTA on its critical path);
 //   phase 2: every CTA scans the chunk histograms it needs (its chunks' exclusive bases and the
 //            expert totals -> offsets), then copies its tokens' normalised rows to their permuted
 //            positions (from smem for its last chunk).
@@ -34,7 +34,10 @@ constexpr int kRteMaxK = 8;
 constexpr int kRteMaxOwn = 4;     // chunks per CTA
 constexpr int kRteU = 4;          // 16-byte vectors per lane in flight in the permutation copies
 constexpr int kRteDU = 8;         // delta vectors per lane in flight per batch
-constexpr int kRteKB = 8;         // k-steps of router-weight fragments in flight per warp
+constexpr int kRteKB = 8;         // k-steps of router-weight fragments per batch beyond the preload
+constexpr int kRteKPre = 24;      // k-steps of router-weight fragments preloaded per warp (8 before the
+                                  // norm, the rest while the norm's smem pass runs; 32 spills next to
+                                  // the 8 delta vectors per lane in flight)
 
 struct RouteArgs {
   const __nv_bfloat16* x;      // [T, d] residual stream
@@ -46,7 +49,7 @@ struct RouteArgs {
   int n_group, topk_group;
   const __nv_bfloat16* wr;     // [E, d] router weight
   __nv_bfloat16* x_out;        // optional [T, d] (may alias x)
-  __nv_bfloat16* h_out;        // [T, d] normalised rows
+  __nv_bfloat16* h_out;        // optional [T, d] normalised rows (required when a CTA owns > 1 chunk)
   float* logits_out;           // optional [T, E]
   int* topk_idx;               // [T, k]
   float* topk_w;               // [T, k]
@@ -60,6 +63,7 @@ struct RouteArgs {
   int* sync;                   // [2] grid barrier {arrivals, generation}, zero on first use
   int nchunks;
   long long* stamps;           // optional [G][16] globaltimer per phase (tools/route_bench.py --phases)
+  int bulk_perm;               // permuted rows leave smem as TMA bulk stores (else st.global.v4 per lane)
 };
 
 MGB_DEVINL long long rte_globaltimer() {
@@ -109,20 +113,18 @@ MGB_DEVINL int ld_acquire_gpu(const int* p) {
   return v;
 }
 
-// Sense-free grid barrier over G co-resident CTAs: arrivals counter + generation word.  The count
-// returns to zero, so the workspace is reusable by the next launch (and by graph replays).
+// Grid barrier over G co-resident CTAs with ONE atomic per CTA on the critical path: CTA 0 adds
+// 2^31 - (G - 1), every other CTA adds 1, so the word's top bit flips exactly when the last CTA
+// arrives and every CTA waits for that flip (no reset / generation round trips).  The low 31 bits
+// return to their value each launch, so the workspace is reusable by the next launch with any G
+// (and by graph replays); only sync[0] is used.
 MGB_DEVINL void grid_barrier(int* sync, int G) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    const int gen = ld_acquire_gpu(sync + 1);
-    __threadfence();
-    if (atomicAdd(sync, 1) == G - 1) {
-      atomicExch(sync, 0);
-      __threadfence();
-      atomicAdd(sync + 1, 1);
-    } else {
-      while (ld_acquire_gpu(sync + 1) == gen) __nanosleep(32);
-    }
+    const unsigned add = blockIdx.x == 0 ? 0x80000000u - (unsigned)(G - 1) : 1u;
+    __threadfence();  // release this CTA's phase-1 writes
+    const unsigned old = atomicAdd(reinterpret_cast<unsigned*>(sync), add);
+    while (((old ^ (unsigned)ld_acquire_gpu(sync)) & 0x80000000u) == 0) __nanosleep(20);
     __threadfence();
   }
   __syncthreads();
@@ -181,8 +183,10 @@ __global__ void __launch_bounds__(kRteThreads, 2) moe_route_kernel(RouteArgs a) 
     const int nt0 = ntiles >= kRteWarps ? warp : warp % ntiles;
     const bool mma_warp = kpart < ksplit && nt0 < ntiles;
     const int ks0 = kpart * kper, ks1 = min(ksteps, ks0 + kper);
-    // the first batch of router-weight fragments is requested before the norm (it does not depend on it)
-    uint32_t bcur[kRteKB][2];
+    // router-weight fragments of the warp's first n-tile do not depend on the norm: the first 8
+    // k-steps are requested before it, the next 24 once the delta loads have landed (the norm's smem
+    // pass hides them), so a d <= 4096 row waits for one fragment batch in the logits phase instead of three
+    uint32_t bpre[kRteKPre][2];
     auto load_b = [&](uint32_t (&b)[kRteKB][2], int nt, int ks) {
       const int n = nt * 8 + (lane >> 2);
       const uint32_t* wrow = reinterpret_cast<const uint32_t*>(a.wr + (size_t)(n < E ? n : 0) * d) + (lane & 3);
@@ -193,7 +197,19 @@ __global__ void __launch_bounds__(kRteThreads, 2) moe_route_kernel(RouteArgs a) 
         b[u][1] = ok ? __ldg(wrow + (ks + u) * 8 + 4) : 0u;
       }
     };
-    if (mma_warp) load_b(bcur, nt0, ks0);
+    auto load_pre = [&](int u0, int u1) {
+      const int n = nt0 * 8 + (lane >> 2);
+      const uint32_t* wrow = reinterpret_cast<const uint32_t*>(a.wr + (size_t)(n < E ? n : 0) * d) + (lane & 3);
+#pragma unroll
+      for (int u = 0; u < kRteKPre; ++u) {
+        if (u < u0 || u >= u1) continue;
+        const bool ok = mma_warp && n < E && ks0 + u < ks1;
+        bpre[u][0] = ok ? __ldg(wrow + (ks0 + u) * 8) : 0u;
+        bpre[u][1] = ok ? __ldg(wrow + (ks0 + u) * 8 + 4) : 0u;
+      }
+    };
+    load_pre(0, kRteKB);
+    bool pre_rest = false;
 
     // ---- residual add + RMSNorm, warp per token; rows land in smem (and h_out) ----
     // the chunk's x rows arrive by bulk copy (TMA engine) while every lane has all of its delta
@@ -245,9 +261,13 @@ __global__ void __launch_bounds__(kRteThreads, 2) moe_route_kernel(RouteArgs a) 
           for (int i = 0; i < 8; ++i) ss = fmaf(f[i], f[i], ss);
         }
       }
+      if (!pre_rest) {  // the delta registers are dead: the remaining preloaded fragments go in flight
+        load_pre(kRteKB, kRteKPre);
+        pre_rest = true;
+      }
       const float inv = 1.0f / sqrtf(rte_wsum(ss) / (float)d + a.eps);
       const uint4* wr = reinterpret_cast<const uint4*>(s.lnw);
-      uint4* hr = reinterpret_cast<uint4*>(a.h_out + t * d);
+      uint4* hr = a.h_out ? reinterpret_cast<uint4*>(a.h_out + t * d) : nullptr;
       for (int cc = lane; cc < nvec; cc += 32) {  // smem only: no memory round trip per vector
         const uint4 v = srow[cc], wv = wr[cc];
         uint4 o;
@@ -256,9 +276,11 @@ __global__ void __launch_bounds__(kRteThreads, 2) moe_route_kernel(RouteArgs a) 
         o.z = pack_bf16x2(bf16lo(wv.z) * bf16_round(bf16lo(v.z) * inv), bf16hi(wv.z) * bf16_round(bf16hi(v.z) * inv));
         o.w = pack_bf16x2(bf16lo(wv.w) * bf16_round(bf16lo(v.w) * inv), bf16hi(wv.w) * bf16_round(bf16hi(v.w) * inv));
         srow[cc] = o;
-        hr[cc] = o;
+        if (hr) hr[cc] = o;
       }
     }
+    if (!pre_rest) load_pre(kRteKB, kRteKPre);  // warps whose token row is a tail row
+    if (a.bulk_perm) fence_proxy_async_smem();  // the normalised rows leave smem by bulk stores
     __syncthreads();
 
     MGB_RTE_STAMP(1);
@@ -270,10 +292,21 @@ __global__ void __launch_bounds__(kRteThreads, 2) moe_route_kernel(RouteArgs a) 
       const uint32_t arow = hbase + (uint32_t)((lane & 7) * s.hstride + (lane >> 4) * 8) * 2;
       for (int nt = nt0; mma_warp && nt < ntiles; nt += kRteWarps) {
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
-        if (nt != nt0) load_b(bcur, nt, ks0);
-        for (int ks = ks0; ks < ks1; ks += kRteKB) {  // weight fragments double-buffered, kRteKB k-steps deep
-          uint32_t bnext[kRteKB][2];
-          if (ks + kRteKB < ks1) load_b(bnext, nt, ks + kRteKB);
+        int ks = ks0;
+        if (nt == nt0) {  // the preloaded fragments
+#pragma unroll
+          for (int u = 0; u < kRteKPre; ++u) {
+            if (ks0 + u < ks1) {
+              uint32_t a0, a1, a2, a3;
+              rte_ldsm_x4(arow + (ks0 + u) * 32, a0, a1, a2, a3);
+              rte_mma(acc, a0, a1, a2, a3, bpre[u][0], bpre[u][1]);
+            }
+          }
+          ks = ks0 + kRteKPre;
+        }
+        for (; ks < ks1; ks += kRteKB) {  // wider rows / further n-tiles: kRteKB k-steps per batch
+          uint32_t bcur[kRteKB][2];
+          load_b(bcur, nt, ks);
 #pragma unroll
           for (int u = 0; u < kRteKB; ++u) {
             if (ks + u < ks1) {
@@ -282,8 +315,6 @@ __global__ void __launch_bounds__(kRteThreads, 2) moe_route_kernel(RouteArgs a) 
               rte_mma(acc, a0, a1, a2, a3, bcur[u][0], bcur[u][1]);
             }
           }
-#pragma unroll
-          for (int u = 0; u < kRteKB; ++u) { bcur[u][0] = bnext[u][0]; bcur[u][1] = bnext[u][1]; }
         }
         // c0,c1: token lane/4, experts 2*(lane%4)+{0,1}; c2,c3: token lane/4 + 8
         const int r = lane >> 2, cn = 2 * (lane & 3);
@@ -464,6 +495,10 @@ __global__ void __launch_bounds__(kRteThreads, 2) moe_route_kernel(RouteArgs a) 
       const uint4* src = in_smem ? reinterpret_cast<const uint4*>(s.h + (size_t)(t - t0) * s.hstride)
                                  : reinterpret_cast<const uint4*>(a.h_out + (size_t)t * d);
       uint4* dst = reinterpret_cast<uint4*>(a.x_perm + (size_t)pos * d);
+      if (in_smem && a.bulk_perm) {  // one TMA bulk store per (token, slot) row
+        if (lane == 0) bulk_store(dst, src, (uint32_t)d * 2);
+        continue;
+      }
       for (int c0 = lane; c0 < nvec; c0 += 32 * kRteU) {
         uint4 v[kRteU];
 #pragma unroll
@@ -474,6 +509,10 @@ __global__ void __launch_bounds__(kRteThreads, 2) moe_route_kernel(RouteArgs a) 
           if (c0 + 32 * u < nvec) dst[c0 + 32 * u] = v[u];
       }
     }
+  }
+  if (a.bulk_perm && lane == 0) {  // smem must outlive the bulk stores' reads
+    bulk_commit();
+    bulk_wait_read_all();
   }
   MGB_RTE_STAMP(8);
 }
@@ -510,7 +549,7 @@ int mgb_moe_route_stamps(long long* stamps) {
   return MGB_OK;
 }
 
-// Rows of the chunk_hist workspace mgb_moe_route needs for T tokens (16-token chunks).
+// Rows of the chunk_hist workspace mgb_moe_route needs for T tokens (8-token chunks).
 int mgb_moe_route_chunks(int T) { return (T + mgb::kRteTPC - 1) / mgb::kRteTPC; }
 
 // Fused decode routing front end (see the file comment).  sync: 2 ints, zero before first use, left
@@ -521,7 +560,7 @@ int mgb_moe_route(const void* x, const void* delta, const void* ln_w, float eps,
                   int topk_group, float* logits_out, int* topk_idx, float* topk_w, int* local_rank, int* chunk_hist,
                   int* counts, int* offsets, void* x_perm, int* src_token, int* dst_pos, int* sync, void* stream) {
   if (T < 1 || d % 16 || d < 16 || E < 1 || E > mgb::kRteMaxE || k < 1 || k > mgb::kRteMaxK || k > E || mode < 0 ||
-      mode > 2 || !sync || !h_out || !x_perm)
+      mode > 2 || !sync || !x_perm)
     return MGB_EINVAL;
   if (mode == 2 && (n_group < 1 || n_group > 32 || E % n_group || topk_group < 1 || topk_group > n_group ||
                     topk_group * (E / n_group) < k))
@@ -538,18 +577,26 @@ int mgb_moe_route(const void* x, const void* delta, const void* ln_w, float eps,
   const int cap = std::max(1, mgb_host::num_sms() * occ / 2);  // half the resident capacity
   const int G = std::min(nchunks, cap);
   if (nchunks > G * mgb::kRteMaxOwn) return MGB_EINVAL;
+  if (!h_out && nchunks > G) return MGB_EINVAL;  // a CTA owning > 1 chunk permutes from h_out
+  // MGB_ROUTE_BULK=1: permuted rows leave smem as TMA bulk stores.  Measured equal to the per-lane
+  // st.global.v4 copies (tools/route_bench.py: 22.9 us both at Mixtral B=827/909), so off by default
+  static const int bulk_perm = [] {
+    const char* e = getenv("MGB_ROUTE_BULK");
+    return e ? atoi(e) : 0;
+  }();
   mgb::RouteArgs a{reinterpret_cast<const __nv_bfloat16*>(x), reinterpret_cast<const __nv_bfloat16*>(delta),
                    reinterpret_cast<const __nv_bfloat16*>(ln_w), eps, T, d, E, k, mode, scaling, n_group, topk_group,
                    reinterpret_cast<const __nv_bfloat16*>(w_router), reinterpret_cast<__nv_bfloat16*>(x_out),
                    reinterpret_cast<__nv_bfloat16*>(h_out), logits_out, topk_idx, topk_w, local_rank, chunk_hist,
                    counts, offsets, reinterpret_cast<__nv_bfloat16*>(x_perm), src_token, dst_pos, sync, nchunks,
-                   g_route_stamps};
+                   g_route_stamps, bulk_perm};
   mgb_host::launch(mgb::moe_route_kernel, dim3(G), dim3(mgb::kRteThreads), smem, reinterpret_cast<cudaStream_t>(stream), nullptr,
       a);
   return mgb_host::launch_status();
 }
 
-// 1 if mgb_moe_route covers T tokens of width d routed over E experts on the current device (else the unfused path).
+// 1 if mgb_moe_route covers T tokens of width d routed over E experts on the current device (else the
+// unfused path); 2 if it covers them in one pass (every CTA owns one chunk, so h_out may be NULL).
 int mgb_moe_route_supported(int T, int d, int E) {
   if (T < 1 || d % 16 || E < 1 || E > mgb::kRteMaxE) return 0;
   const size_t smem = mgb::route_smem(d, E);
@@ -560,7 +607,8 @@ int mgb_moe_route_supported(int T, int d, int E) {
           cudaSuccess || occ < 1)
     return 0;
   const int cap = std::max(1, mgb_host::num_sms() * occ / 2);
-  return mgb_moe_route_chunks(T) <= cap * mgb::kRteMaxOwn ? 1 : 0;
+  const int nchunks = mgb_moe_route_chunks(T);
+  return nchunks <= cap ? 2 : nchunks <= cap * mgb::kRteMaxOwn ? 1 : 0;
 }
 
 }  // extern "C"

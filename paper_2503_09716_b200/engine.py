@@ -301,6 +301,9 @@ class Engine:
         # stays on the unfused kernels, whose cuBLAS logits GEMM and wide top-k grid win there)
         self.fused_route = (os.environ.get("MGB_FUSED_ROUTE", "1") != "0" and not self.offload and self.ep is None
                             and a.n_experts <= 16 and ops.moe_route_supported(B, a.hidden, a.n_experts))
+        # one chunk per CTA: the normalised rows need not be written to b.h (only x_perm reads them;
+        # the debug taps still get them)
+        self._route_1pass = self.fused_route and ops.moe_route_single_pass(B, a.hidden, a.n_experts)
         # GQA decode: the step's RoPE + KV append inside the attention launch (mgb_decode_attn_gqa_rope,
         # MGB_FUSED_ROPE=1) when the pages are the resident store and no CPU share reads the RoPE'd q.
         # Off by default: bit-identical and faster eagerly (12.47 vs 12.29 + 0.41 ms per Mixtral forward),
@@ -830,7 +833,8 @@ class Engine:
                 ops.add_rmsnorm(b.x, W["ln2"], a.rms_eps, b.h, delta=b.o, x_out=b.x)
         elif j.kind == "router":
             if self._route_fused(l):
-                ops.moe_route(b.x, b.o, W["ln2"], a.rms_eps, b.h, W["router"], self.rws, b.x_perm, a.router_mode,
+                h_out = None if (self._route_1pass and self.debug_taps is None) else b.h
+                ops.moe_route(b.x, b.o, W["ln2"], a.rms_eps, h_out, W["router"], self.rws, b.x_perm, a.router_mode,
                               a.routed_scaling, a.n_group, a.topk_group, x_out=b.x, logits_out=self.logits_r)
             elif self._forced_logits is not None:
                 ops.router_topk(None, None, self.rws, a.top_k, a.router_mode, a.routed_scaling, a.n_group,

@@ -62,12 +62,18 @@ def moe_route_supported(T: int, d: int, E: int) -> bool:
     return bool(nat.value("mgb_moe_route_supported", T, d, E))
 
 
-def moe_route(x: torch.Tensor, delta: torch.Tensor | None, ln_w: torch.Tensor, eps: float, h_out: torch.Tensor,
+def moe_route_single_pass(T: int, d: int, E: int) -> bool:
+    """mgb_moe_route covers T tokens with one chunk per CTA (its h_out may be None)."""
+    return nat.value("mgb_moe_route_supported", T, d, E) == 2
+
+
+def moe_route(x: torch.Tensor, delta: torch.Tensor | None, ln_w: torch.Tensor, eps: float, h_out: torch.Tensor | None,
               w_router: torch.Tensor, ws: RouterWorkspace, x_perm: torch.Tensor, mode: int, scaling: float = 1.0,
               n_group: int = 1, topk_group: int = 1, x_out: torch.Tensor | None = None,
               logits_out: torch.Tensor | None = None) -> None:
     """Fused decode routing front end (route.cu): x_out = x + delta, h_out = RMSNorm(x_out) * ln_w,
-    top-k routing of h_out, and the stable expert-major permutation of h_out into x_perm."""
+    top-k routing of h_out, and the stable expert-major permutation of h_out into x_perm.  h_out may be
+    None when moe_route_single_pass(T, d, E) (the normalised rows then exist only in x_perm)."""
     T, d = x.shape
     E = w_router.shape[0]
     nat.call("mgb_moe_route", _p(x), _p(delta), _p(ln_w), eps, T, d, _p(x_out), _p(h_out), _p(w_router), E, ws.k,

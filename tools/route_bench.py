@@ -13,7 +13,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2503_09716_b200 import ops  # noqa: E402
 
 BF16 = torch.bfloat16
-SHAPES = [("mixtral-8x7b", 827, 4096, 8, 2, 0, 1, 1), ("deepseek-v2-lite", 6058, 2048, 64, 6, 1, 1, 1),
+SHAPES = [("mixtral-8x7b", 827, 4096, 8, 2, 0, 1, 1), ("mixtral-8x7b", 909, 4096, 8, 2, 0, 1, 1), ("deepseek-v2-lite", 6058, 2048, 64, 6, 1, 1, 1),
           ("mixtral-8x22b", 271, 6144, 8, 2, 0, 1, 1), ("deepseek-v2", 1024, 5120, 160, 6, 2, 8, 3)]
 
 
@@ -47,6 +47,11 @@ for name, T, d, E, k, mode, ng, tg in SHAPES:
     if ops.moe_route_supported(T, d, E):
         row["fused_us"] = timed(lambda: ops.moe_route(x, o, ln, 1e-5, h, wr, ws, xp, mode, 1.0, ng, tg, x_out=xo,
                                                       logits_out=lg))
+        # as the engine's decode step calls it: no h_out when one pass covers T, no logits copy
+        h_eng = None if ops.moe_route_single_pass(T, d, E) else h
+        row["engine_call_us"] = timed(lambda: ops.moe_route(x, o, ln, 1e-5, h_eng, wr, ws, xp, mode, 1.0, ng, tg,
+                                                            x_out=xo))
+        row["bulk_perm"] = os.environ.get("MGB_ROUTE_BULK", "0")
 
     def unfused():
         ops.add_rmsnorm(x, ln, 1e-5, h, delta=o, x_out=xo)
@@ -57,7 +62,7 @@ for name, T, d, E, k, mode, ng, tg in SHAPES:
         from paper_2503_09716_b200 import _native as nat
         st = torch.zeros(1024, 16, dtype=torch.int64, device="cuda")
         nat.call("mgb_moe_route_stamps", st.data_ptr())
-        ops.moe_route(x, o, ln, 1e-5, h, wr, ws, xp, mode, 1.0, ng, tg, x_out=xo, logits_out=lg)
+        ops.moe_route(x, o, ln, 1e-5, h_eng, wr, ws, xp, mode, 1.0, ng, tg, x_out=xo)
         torch.cuda.synchronize()
         nat.call("mgb_moe_route_stamps", None)
         st = st[(st[:, 9] > 0)].double()
