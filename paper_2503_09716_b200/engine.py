@@ -280,6 +280,16 @@ class Engine:
         if self.n_cpu > 0:
             self._init_cpu_attention()
         self._fork, self._join = torch.cuda.Event(), torch.cuda.Event()
+        # DeepSeek shared experts on a side stream (MGB_SHARED_STREAM=0: in line): they read only the
+        # post-attention norm's rows, so they overlap the router chain (logits GEMM, top-k, scan,
+        # permute) and the routed GEMMs' tails, and join before the combine that adds their output.
+        # HBM-resident, non-EP engines only (offloaded shared experts live in the dense buffer, which is
+        # handed to the next layer's copy right after them, offload_dag.py:308-321)
+        self.shared_stream = (torch.cuda.Stream(device=device)
+                              if (self.mla and a.n_shared > 0 and not self.offload and self.ep is None
+                                  and os.environ.get("MGB_SHARED_STREAM", "1") != "0") else None)
+        self._sh_fork, self._sh_join = torch.cuda.Event(), torch.cuda.Event()
+        self._sh_pending = False
         self.events = {i: torch.cuda.Event() for i in self.need_event}
         self.trace_events: dict | None = None  # job id -> (start, end) timing events (eager trace mode)
         self._trace_counts: torch.Tensor | None = None  # [layers, E] routed rows per expert (trace mode)
@@ -675,10 +685,21 @@ class Engine:
                 return  # residual add + norm, routing and the shared experts run in the router job
             ops.add_rmsnorm(b.x, W["ln2"], a.rms_eps, b.h, delta=b.o, x_out=b.x)
             if l >= a.first_k_dense:
-                # shared experts on every token (DeepseekV2Moe.shared_experts): dense -> cuBLAS.  They are
-                # part of the layer's dense modules (dense_bytes_per_layer), so they run before the
-                # single dense buffer is handed to the next layer's copy (offload_dag.py:308-321)
-                self._dense_mlp(W["sh_gate_up"], W["sh_down"], b.h, m["sh_h"], m["sh_out"], m["offsets_all"])
+                # shared experts on every token (DeepseekV2Moe.shared_experts) as one grouped-GEMM
+                # segment.  They are part of the layer's dense modules (dense_bytes_per_layer), so with
+                # offloaded weights they run before the single dense buffer is handed to the next
+                # layer's copy (offload_dag.py:308-321); resident, they run on the side stream
+                if self.shared_stream is not None and self.trace_events is None:
+                    cur = torch.cuda.current_stream()
+                    self._sh_fork.record(cur)
+                    with torch.cuda.stream(self.shared_stream):
+                        self.shared_stream.wait_event(self._sh_fork)
+                        self._dense_mlp(W["sh_gate_up"], W["sh_down"], b.h, m["sh_h"], m["sh_out"],
+                                        m["offsets_all"])
+                        self._sh_join.record(self.shared_stream)
+                    self._sh_pending = True
+                else:
+                    self._dense_mlp(W["sh_gate_up"], W["sh_down"], b.h, m["sh_h"], m["sh_out"], m["offsets_all"])
         elif j.kind == "router":
             if self._route_fused(l):
                 ops.moe_route(b.x, b.o, W["ln2"], a.rms_eps, b.h, W["router"], self.rws, b.x_perm, a.router_mode,
@@ -766,6 +787,9 @@ class Engine:
         if j.id == self.last_expert_job[l]:
             nxt = self.w.layers[l + 1]["ln1"] if l + 1 < a.layers else self.w.final_norm
             y_perm = self.ep.yperm if self.peer_ep else b.y_perm
+            if self._sh_pending:  # the shared experts' side stream joins before their output is added
+                torch.cuda.current_stream().wait_event(self._sh_join)
+                self._sh_pending = False
             ops.unpermute_combine(y_perm, self.rws, b.x, self.B, residual=b.x, shared_out=shared_out,
                                   norm_w=nxt, eps=a.rms_eps, norm_out=b.h)
 
