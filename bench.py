@@ -230,7 +230,8 @@ def _workload_config(args, arch, world: int, ep: bool = False) -> dict:
     """The workload both arms are quoted on (the GPU arm's batch: the planner's largest resident B)."""
     from paper_2503_09716_b200.engine import resident_plan
 
-    plan = resident_plan(arch, args.prompt_len, args.decode_len, B=args.batch, reserve_bytes=reserve_bytes(args, arch))
+    plan = resident_plan(arch, args.prompt_len, args.decode_len, B=args.batch, reserve_bytes=reserve_bytes(args, arch),
+                         ep_world=world if ep else 1)
     where = (f"{world} B200 expert-parallel" if ep else "1 B200 resident")
     par = (f"ep{world}: experts {arch.n_experts // world} per rank, each rank's B sequences data-parallel, token "
            f"dispatch/combine fused into the permutation / down-GEMM kernels over NVLink peer memory (torch symmetric "
@@ -320,6 +321,21 @@ def kernel_breakdown(eng, reps: int = 2) -> dict:
             for n, v in recs.items()}
 
 
+def use_ep(args, arch, world: int) -> bool:
+    """Experts shard across the job's ranks for DeepSeek-V2 models (configs[2], [4]) and
+    for any model whose weights do not fit one GPU (Mixtral-8x22B EP8, configs[3]); Mixtral-8x7B runs
+    replicas.  --ep force: the EP path on a one-rank group; --ep off: never."""
+    from paper_2503_09716_b200.engine import b200_hardware
+    from paper_2503_09716_b200.planner import ModelSpec
+
+    if args.ep == "off" or (world == 1 and args.ep != "force"):
+        return False
+    if arch.family == "deepseek_v2" or args.ep == "force":
+        return True
+    hbm = b200_hardware().m_g if torch.cuda.is_available() else 183_359 << 20
+    return ModelSpec.from_document(arch.model_spec_document()).model_bytes > hbm - reserve_bytes(args, arch)
+
+
 def run_ours(args, dist, rank, world) -> None:
     import gc
 
@@ -327,7 +343,7 @@ def run_ours(args, dist, rank, world) -> None:
 
     torch.cuda.set_device(rank % torch.cuda.device_count())
     arch0 = get_arch(args.config)
-    ep0 = (world > 1 or args.ep == "force") and args.ep != "off" and arch0.family == "deepseek_v2"
+    ep0 = use_ep(args, arch0, world)
     line = measure(args, arch0, dist, rank, world, args.steps, args.warmup, main=True, ep=ep0)
     # the other 1-GPU BASELINE configuration (configs[2], DeepSeek-V2-Lite) measured in the same run, so
     # the driver's bench records it too; same contract (device-timed decode steps, e2e through the
@@ -337,7 +353,7 @@ def run_ours(args, dist, rank, world) -> None:
         gc.collect()
         torch.cuda.empty_cache()
         # DeepSeek-V2-Lite is BASELINE configs[2]: expert-parallel across the job's GPUs (1 GPU: plain)
-        ep = (world > 1 or args.ep == "force") and args.ep != "off" and get_arch(name).family == "deepseek_v2"
+        ep = use_ep(args, get_arch(name), world)
         try:
             sub = measure(args, get_arch(name), dist, rank, world, args.also_steps, max(3, min(args.warmup, 3)),
                           main=False, ep=ep)
@@ -359,7 +375,8 @@ def measure(args, arch, dist, rank, world, steps: int, warmup: int, main: bool, 
     job's ranks (PeerExpertParallel over symmetric memory), each rank decoding its own B sequences."""
     from paper_2503_09716_b200.engine import Engine, resident_plan
 
-    plan = resident_plan(arch, args.prompt_len, args.decode_len, B=args.batch, reserve_bytes=reserve_bytes(args, arch))
+    plan = resident_plan(arch, args.prompt_len, args.decode_len, B=args.batch, reserve_bytes=reserve_bytes(args, arch),
+                         ep_world=world if ep else 1)
     pep = None
     if ep:
         from paper_2503_09716_b200.ep import PeerExpertParallel

@@ -220,6 +220,9 @@ int mgb_decode_advance(const int* next, int B, long long* out_tokens, int ld, in
 /* ---- synthetic random-init weights (counter-based, mirrored by oracle/rng.py) ------------ */
 int mgb_fill_uniform_bf16(void* out, long long n, unsigned long long seed, unsigned long long tensor_id, float std,
                           float constant, int mode, void* stream);
+/* elements [first, first + n) of the same stream (a rank's expert shard, generated in place) */
+int mgb_fill_uniform_bf16_range(void* out, long long n, long long first, unsigned long long seed,
+                                unsigned long long tensor_id, float std, void* stream);
 
 #ifdef __cplusplus
 }

@@ -56,6 +56,7 @@ SIGNATURES: dict[str, list] = {
     "mgb_argmax": [P, I, I, P, P],
     "mgb_decode_advance": [P, I, P, I, P, P, P],
     "mgb_fill_uniform_bf16": [P, L, ctypes.c_uint64, ctypes.c_uint64, F, F, I, P],
+    "mgb_fill_uniform_bf16_range": [P, L, L, ctypes.c_uint64, ctypes.c_uint64, F, P],
     # attn_mla.cu
     "mgb_mla_page_size": [],
     "mgb_mla_page_elems": [I, I],

@@ -349,14 +349,14 @@ MGB_DEVINL uint64_t splitmix64_mix(uint64_t z) {
   return z ^ (z >> 31);
 }
 __global__ void fill_uniform_kernel(__nv_bfloat16* __restrict__ out, size_t n, uint64_t seed, uint64_t tensor_id,
-                                    float scale, float constant, int mode) {
+                                    float scale, float constant, int mode, uint64_t first) {
   mgb::pdl_enter();
   const uint64_t base = (seed * 0x9E3779B97F4A7C15ull + tensor_id) * 0xD1B54A32D192ED03ull;
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     if (mode == 1) {
       out[i] = __float2bfloat16_rn(constant);
     } else {
-      const uint64_t z = splitmix64_mix(base + i);
+      const uint64_t z = splitmix64_mix(base + first + i);  // element first + i of the tensor's stream
       const int u = (int)(z >> 40) - (1 << 23);
       out[i] = __float2bfloat16_rn(__fmul_rn((float)u, scale));
     }
@@ -459,7 +459,23 @@ int mgb_fill_uniform_bf16(void* out, long long n, unsigned long long seed, unsig
   long long blocks = (n + threads - 1) / threads;
   if (blocks > 148 * 64) blocks = 148 * 64;
   mgb_host::launch(mgb::fill_uniform_kernel, dim3((int)blocks), dim3(threads), 0, reinterpret_cast<cudaStream_t>(stream), nullptr,
-      reinterpret_cast<__nv_bfloat16*>(out), (size_t)n, seed, tensor_id, scale, constant, mode);
+      reinterpret_cast<__nv_bfloat16*>(out), (size_t)n, seed, tensor_id, scale, constant, mode, (uint64_t)0);
+  return mgb_host::launch_status();
+}
+
+// Elements [first, first + n) of tensor `tensor_id`'s counter-based stream (the same values
+// mgb_fill_uniform_bf16 writes at those indices of the whole tensor): a rank's expert shard is
+// generated in place without materialising the other ranks' experts.
+int mgb_fill_uniform_bf16_range(void* out, long long n, long long first, unsigned long long seed,
+                                unsigned long long tensor_id, float std, void* stream) {
+  if (n < 0 || first < 0) return MGB_EINVAL;
+  if (n == 0) return MGB_OK;
+  const float scale = (float)((double)std * 1.7320508075688772 / 8388608.0);
+  const int threads = 256;
+  long long blocks = (n + threads - 1) / threads;
+  if (blocks > 148 * 64) blocks = 148 * 64;
+  mgb_host::launch(mgb::fill_uniform_kernel, dim3((int)blocks), dim3(threads), 0, reinterpret_cast<cudaStream_t>(stream), nullptr,
+      reinterpret_cast<__nv_bfloat16*>(out), (size_t)n, seed, tensor_id, scale, 0.0f, 0, (uint64_t)first);
   return mgb_host::launch_status();
 }
 

@@ -49,15 +49,23 @@ def _unit_latency(kind: str, tokens: int, ctx: int) -> float:
     return 1e-6 * tokens
 
 
+def routed_expert_bytes(arch: ModelArch) -> int:
+    """Bytes of all routed experts of all MoE layers (bf16 gate, up and down)."""
+    return (arch.layers - arch.first_k_dense) * arch.n_experts * 3 * arch.hidden * arch.moe_ffn * 2
+
+
 def resident_plan(arch: ModelArch, prompt_len: int, decode_len: int, B: int | None = None,
                   b_a: int | None = None, b_e: int = 4096, reserve_bytes: int = 12 << 30,
-                  hbm_bytes: int | None = None) -> BatchingPlan:
+                  hbm_bytes: int | None = None, ep_world: int = 1) -> BatchingPlan:
     """Plan for an HBM-resident model (s_params = whole model, no expert slots): B is the largest
     batch whose paged KV fits next to the weights (reference max_feasible_B with the resident KV
-    policy), capped by `B` if given."""
+    policy), capped by `B` if given.  ep_world > 1: one rank of an expert-parallel group, which
+    holds 1/ep_world of the routed experts; the planner sees the whole model next to an HBM enlarged
+    by the other ranks' expert bytes, so B is this rank's KV capacity."""
     spec = ModelSpec.from_document(arch.model_spec_document())
     hw = b200_hardware(hbm_bytes=hbm_bytes)
-    hw = Hardware(**{**hw.__dict__, "m_g": hw.m_g - reserve_bytes})
+    others = routed_expert_bytes(arch) * (ep_world - 1) // ep_world
+    hw = Hardware(**{**hw.__dict__, "m_g": hw.m_g - reserve_bytes + others})
     wl = WorkloadSpec(prompt_len, decode_len, 1, "decode")
     tmpl = BatchingPlan(1, 1, b_e, 0.0, 0, spec.model_bytes)
     from .planner import footprint
@@ -178,17 +186,12 @@ class Engine:
             self.w = OffloadedWeights(a, self.spec, self.plan.s_params, self.plan.s_expert, seed=seed,
                                       extra_slots=self.lookahead_expert_slots, extra_dense=len(self.dense_buf_of),
                                       device=device, source=self.source)
-        elif self.mla:
-            self.w = DeepseekDeviceWeights(a, seed=seed, device=device, source=self.source)
         else:
-            self.w = MixtralDeviceWeights(a, seed=seed, device=device, source=self.source)
-        if self.ep is not None:  # this rank holds only its expert range [first, first + E_local)
-            lo, nl = self.ep.first, self.ep.E_local
-            for W_ in self.w.layers:
-                if W_.get("w_gate_up") is not None:
-                    W_["w_gate_up"] = W_["w_gate_up"][lo:lo + nl].clone()
-                    W_["w_down"] = W_["w_down"][lo:lo + nl].clone()
-            torch.cuda.empty_cache()
+            # an expert-parallel rank generates (or loads) only its expert range [first, first + E_local):
+            # DeepSeek-V2 236B EP8 holds 20 of 160 experts per layer, never the 453 GB of all of them
+            shard = (self.ep.first, self.ep.E_local) if self.ep is not None else None
+            cls = DeepseekDeviceWeights if self.mla else MixtralDeviceWeights
+            self.w = cls(a, seed=seed, device=device, source=self.source, experts=shard)
         d, k, f = a.hidden, a.top_k, a.moe_ffn
         bf = dict(dtype=BF16, device=device)
         i32 = dict(dtype=torch.int32, device=device)

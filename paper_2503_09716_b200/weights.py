@@ -22,11 +22,36 @@ def tid(layer: int, name: str) -> int:
     return LAYER_BASE + LAYER_STRIDE * layer + SLOT[name]
 
 
-def fill_uniform_(t: torch.Tensor, seed: int, tensor_id: int, std: float) -> torch.Tensor:
+def fill_uniform_(t: torch.Tensor, seed: int, tensor_id: int, std: float, first: int = 0) -> torch.Tensor:
+    """t <- elements [first, first + t.numel()) of tensor `tensor_id`'s counter-based stream."""
     assert t.dtype == torch.bfloat16 and t.is_cuda and t.is_contiguous()
-    nat.call("mgb_fill_uniform_bf16", t.data_ptr(), t.numel(), seed, tensor_id, std, 0.0, 0,
-             torch.cuda.current_stream().cuda_stream)
+    if first:
+        nat.call("mgb_fill_uniform_bf16_range", t.data_ptr(), t.numel(), first, seed, tensor_id, std,
+                 torch.cuda.current_stream().cuda_stream)
+    else:
+        nat.call("mgb_fill_uniform_bf16", t.data_ptr(), t.numel(), seed, tensor_id, std, 0.0, 0,
+                 torch.cuda.current_stream().cuda_stream)
     return t
+
+
+def routed_experts_(a: ModelArch, seed: int, tid_gate_up: int, tid_down: int, device: str,
+                    experts: tuple[int, int] | None) -> tuple[torch.Tensor, torch.Tensor]:
+    """Routed expert weights [n, 2f, d] / [n, d, f] of experts [lo, lo + n) (all when experts is None),
+    generated in place: an expert-parallel rank never holds the other ranks' experts."""
+    lo, n = experts if experts is not None else (0, a.n_experts)
+    f, d = a.moe_ffn, a.hidden
+    bf = dict(dtype=torch.bfloat16, device=device)
+    gu = fill_uniform_(torch.empty(n, 2 * f, d, **bf), seed, tid_gate_up, a.init_std, first=lo * 2 * f * d)
+    dn = fill_uniform_(torch.empty(n, d, f, **bf), seed, tid_down, a.init_std, first=lo * d * f)
+    return gu, dn
+
+
+def _shard_source(L: dict, experts: tuple[int, int] | None) -> dict:
+    """A checkpoint layer restricted to the rank's routed experts (before it moves to the device)."""
+    if experts is not None and L.get("w_gate_up") is not None:
+        lo, n = experts
+        L = dict(L, w_gate_up=L["w_gate_up"][lo:lo + n], w_down=L["w_down"][lo:lo + n])
+    return L
 
 
 def fill_const_(t: torch.Tensor, value: float) -> torch.Tensor:
@@ -36,13 +61,15 @@ def fill_const_(t: torch.Tensor, value: float) -> torch.Tensor:
     return t
 
 
-def mixtral_layer(a: ModelArch, l: int, seed: int, device: str = "cuda", source=None) -> dict:
+def mixtral_layer(a: ModelArch, l: int, seed: int, device: str = "cuda", source=None,
+                  experts: tuple[int, int] | None = None) -> dict:
     """Layer l of a Mixtral-family model in the engine's layout.  q/k/v projections are stored
     fused as one [Hq*hd + 2*Hkv*hd, d] matrix (rows = wq | wk | wv), each part generated with its
     own tensor id so it equals the oracle's separate wq/wk/wv.  `source` (checkpoint.Checkpoint)
-    loads the layer from a safetensors checkpoint instead of generating it."""
+    loads the layer from a safetensors checkpoint instead of generating it.  experts=(lo, n): only
+    routed experts [lo, lo + n) (an expert-parallel rank's shard)."""
     if source is not None:
-        return {k: v.to(device) for k, v in source.layer(l).items()}
+        return {k: v.to(device) for k, v in _shard_source(source.layer(l), experts).items()}
     d, hd = a.hidden, a.head_dim
     qd, kvd = a.n_heads * hd, a.n_kv_heads * hd
     std = a.init_std
@@ -51,27 +78,29 @@ def mixtral_layer(a: ModelArch, l: int, seed: int, device: str = "cuda", source=
     fill_uniform_(wqkv[:qd], seed, tid(l, "wq"), std)
     fill_uniform_(wqkv[qd:qd + kvd], seed, tid(l, "wk"), std)
     fill_uniform_(wqkv[qd + kvd:], seed, tid(l, "wv"), std)
+    w_gate_up, w_down = routed_experts_(a, seed, tid(l, "w_gate_up"), tid(l, "w_down"), device, experts)
     return dict(
         ln1=fill_const_(torch.empty(d, **bf), 1.0),
         wqkv=wqkv,
         wo=fill_uniform_(torch.empty(d, qd, **bf), seed, tid(l, "wo"), std),
         ln2=fill_const_(torch.empty(d, **bf), 1.0),
         router=fill_uniform_(torch.empty(a.n_experts, d, **bf), seed, tid(l, "router"), std),
-        w_gate_up=fill_uniform_(torch.empty(a.n_experts, 2 * a.moe_ffn, d, **bf), seed, tid(l, "w_gate_up"), std),
-        w_down=fill_uniform_(torch.empty(a.n_experts, d, a.moe_ffn, **bf), seed, tid(l, "w_down"), std),
+        w_gate_up=w_gate_up,
+        w_down=w_down,
     )
 
 
 class _DeviceWeights:
     """All weights HBM-resident, generated layer by layer by the family's layer builder."""
 
-    def __init__(self, arch: ModelArch, seed: int = 0, device: str = "cuda", source=None):
+    def __init__(self, arch: ModelArch, seed: int = 0, device: str = "cuda", source=None,
+                 experts: tuple[int, int] | None = None):
         a = arch
-        bf = dict(dtype=torch.bfloat16, device=device)
         self.arch = a
+        self.experts = experts  # (lo, n): this rank's routed-expert shard; None = all experts
         self.embed, self.final_norm, self.lm_head = global_tensors(a, seed, device, source)
         build = deepseek_layer if a.is_mla else mixtral_layer
-        self.layers = [build(a, l, seed, device, source) for l in range(a.layers)]
+        self.layers = [build(a, l, seed, device, source, experts) for l in range(a.layers)]
 
     def nbytes(self) -> int:
         n = self.embed.nbytes + self.final_norm.nbytes + self.lm_head.nbytes
@@ -106,12 +135,14 @@ def ds_tid(layer: int, name: str) -> int:
     return LAYER_BASE + LAYER_STRIDE * layer + DS_SLOT[name]
 
 
-def deepseek_layer(a: ModelArch, l: int, seed: int, device: str = "cuda", source=None) -> dict:
+def deepseek_layer(a: ModelArch, l: int, seed: int, device: str = "cuda", source=None,
+                   experts: tuple[int, int] | None = None) -> dict:
     """Layer l of a DeepSeek-V2-family model in HF layouts (q_proj or q_a/q_b, kv_a_proj_with_mqa,
     kv_b_proj, o_proj; routed experts [E,2f,d]/[E,d,f]; shared experts and the dense first layers
-    as fused gate|up [2f,d] + down [d,f]).  Tensor ids mirror oracle/moe_ref.py DS_SLOT."""
+    as fused gate|up [2f,d] + down [d,f]).  Tensor ids mirror oracle/moe_ref.py DS_SLOT.
+    experts=(lo, n): only routed experts [lo, lo + n) (an expert-parallel rank's shard)."""
     if source is not None:
-        return derive_views(a, {k: v.to(device) for k, v in source.layer(l).items()})
+        return derive_views(a, {k: v.to(device) for k, v in _shard_source(source.layer(l), experts).items()})
     d, H = a.hidden, a.n_heads
     qk = a.qk_nope_dim + a.qk_rope_dim
     std = a.init_std
@@ -130,9 +161,9 @@ def deepseek_layer(a: ModelArch, l: int, seed: int, device: str = "cuda", source
                  dense_down=U((1, d, a.dense_ffn), "dense_down"))
     else:
         fs = a.moe_ffn * a.n_shared
-        L.update(router=U((a.n_experts, d), "router"), w_gate_up=U((a.n_experts, 2 * a.moe_ffn, d), "w_gate_up"),
-                 w_down=U((a.n_experts, d, a.moe_ffn), "w_down"), sh_gate_up=U((1, 2 * fs, d), "sh_gate_up"),
-                 sh_down=U((1, d, fs), "sh_down"))
+        w_gate_up, w_down = routed_experts_(a, seed, ds_tid(l, "w_gate_up"), ds_tid(l, "w_down"), device, experts)
+        L.update(router=U((a.n_experts, d), "router"), w_gate_up=w_gate_up, w_down=w_down,
+                 sh_gate_up=U((1, 2 * fs, d), "sh_gate_up"), sh_down=U((1, d, fs), "sh_down"))
     derive_views(a, L)
     return L
 
