@@ -304,6 +304,7 @@ def kernel_breakdown(eng, reps: int = 2) -> dict:
                          f"{a[0]}[E={a[4]}]" if a[0].startswith("mgb_moe_gemm") else a[0], orig_call)
         torch.mm = timed("cublas_gemm", mm)
         torch.bmm = timed("cublas_bmm", bmm)
+        eng.serial_jobs = True  # one stream: concurrent side-stream kernels would blur the attribution
         saved = [t.clone() for t in (eng.buf.positions, eng.buf.step, eng.buf.next_ids, eng.buf.seq_lens)]
         for _ in range(reps):
             with torch.cuda.stream(st):
@@ -314,6 +315,7 @@ def kernel_breakdown(eng, reps: int = 2) -> dict:
             t.copy_(s)
     finally:
         nat.call, torch.mm, torch.bmm = orig_call, mm, bmm
+        eng.serial_jobs = False
     recs: dict[str, list[float]] = {}
     for name, e0, e1 in pend:
         recs.setdefault(name.replace("mgb_", ""), []).append(e0.elapsed_time(e1))

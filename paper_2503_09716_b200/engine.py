@@ -293,6 +293,7 @@ class Engine:
                                   and os.environ.get("MGB_SHARED_STREAM", "1") != "0") else None)
         self._sh_fork, self._sh_join = torch.cuda.Event(), torch.cuda.Event()
         self._sh_pending = False
+        self.serial_jobs = False  # measurement: every job in line on one stream (per-kernel breakdowns)
         self.events = {i: torch.cuda.Event() for i in self.need_event}
         self.trace_events: dict | None = None  # job id -> (start, end) timing events (eager trace mode)
         self._trace_counts: torch.Tensor | None = None  # [layers, E] routed rows per expert (trace mode)
@@ -692,7 +693,7 @@ class Engine:
                 # segment.  They are part of the layer's dense modules (dense_bytes_per_layer), so with
                 # offloaded weights they run before the single dense buffer is handed to the next
                 # layer's copy (offload_dag.py:308-321); resident, they run on the side stream
-                if self.shared_stream is not None and self.trace_events is None:
+                if self.shared_stream is not None and self.trace_events is None and not self.serial_jobs:
                     cur = torch.cuda.current_stream()
                     self._sh_fork.record(cur)
                     with torch.cuda.stream(self.shared_stream):
