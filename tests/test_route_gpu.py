@@ -17,7 +17,8 @@ BF16 = torch.bfloat16
 @pytest.mark.parametrize("T,d,E,k,mode,ng,tg", [
     (1, 256, 8, 2, 0, 1, 1), (33, 256, 8, 2, 0, 1, 1), (827, 4096, 8, 2, 0, 1, 1),
     (6058, 2048, 64, 6, 1, 1, 1), (257, 5120, 160, 6, 2, 8, 3), (300, 2048, 64, 6, 1, 1, 1),
-    (1000, 6144, 8, 2, 0, 1, 1)])
+    (1000, 6144, 8, 2, 0, 1, 1),
+    (2000, 4096, 8, 2, 0, 1, 1), (3001, 1024, 8, 2, 0, 1, 1)])  # > 1 chunk per CTA (rows via h_out)
 def test_moe_route_matches_unfused(T, d, E, k, mode, ng, tg):
     from paper_2503_09716_b200 import ops
 
