@@ -63,6 +63,10 @@ MGB_DEVINL float warp_sum(float v) {
   return v;
 }
 
+// GEMV = false: the logits come from the caller (a.logits_in); the kernel then carries none of the
+// GEMV's registers (74 -> fewer per thread, so a DeepSeek-V2-Lite decode batch's 758 CTAs are one
+// wave instead of 1.7)
+template <bool GEMV>
 __global__ void __launch_bounds__(kRouterThreads) router_topk_kernel(RouterArgs a) {
   mgb::pdl_enter();
   extern __shared__ __align__(16) uint8_t smem[];
@@ -77,7 +81,7 @@ __global__ void __launch_bounds__(kRouterThreads) router_topk_kernel(RouterArgs 
   const int E = a.E, d = a.d, k = a.k;
 
   // ---------------- phase 1: logits ----------------
-  if (a.logits_in) {
+  if (!GEMV) {
     // given fp32 logits (e.g. a cuBLAS bf16 GEMM with fp32 output); Mixtral's router linear is a
     // bf16 GEMM (modeling_mixtral.py:111), i.e. the fp32 accumulator rounded once to bf16
     for (int t = warp; t < ntok; t += kRouterThreads / 32)
@@ -85,7 +89,7 @@ __global__ void __launch_bounds__(kRouterThreads) router_topk_kernel(RouterArgs 
         const float v = a.logits_in[(size_t)(t0 + t) * E + e];
         s_logit[t * kMaxE + e] = (a.mode == 0) ? bf16_round(v) : v;
       }
-  } else {
+  } else if constexpr (GEMV) {
     // stage the CTA's (contiguous) token rows in smem with one bulk copy (TMA engine)
     const int vec_per_row = d / 8;
     __shared__ __align__(8) uint64_t s_bar;
@@ -326,11 +330,15 @@ __global__ void __launch_bounds__(256) router_scan_kernel(int* __restrict__ bloc
   __syncthreads();
   if (!s_last) return;
   __threadfence();
+  // every expert's count in flight at once (a serial loop waited for E dependent L2 round trips)
+  __shared__ int s_cnt[kMaxE];
+  for (int i = tid; i < E; i += 256) s_cnt[i] = __ldcg(counts + i);
+  __syncthreads();
   if (tid == 0) {
     int run = 0;
     for (int i = 0; i < E; ++i) {
       offsets[i] = run;
-      run += __ldcg(counts + i);
+      run += s_cnt[i];
     }
     offsets[E] = run;
     *ticket = 0;
@@ -544,12 +552,12 @@ int mgb_router_topk(const void* x, const void* w_gate, const float* logits_in, i
   const int nblk = mgb_router_num_blocks(T);
   const size_t smem = sizeof(float) * mgb::kRouterTPB * mgb::kMaxE + sizeof(int) * mgb::kRouterTPB * mgb::kMaxK +
                       (logits_in ? 0 : (size_t)mgb::kRouterTPB * d * 2);
+  auto kern = logits_in ? mgb::router_topk_kernel<false> : mgb::router_topk_kernel<true>;
   if (smem > 48 * 1024) {
-    if (cudaFuncSetAttribute(mgb::router_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return MGB_ECUDA;
   }
-  mgb_host::launch(mgb::router_topk_kernel, dim3(nblk), dim3(mgb::kRouterThreads), smem, reinterpret_cast<cudaStream_t>(stream), nullptr,
+  mgb_host::launch(kern, dim3(nblk), dim3(mgb::kRouterThreads), smem, reinterpret_cast<cudaStream_t>(stream), nullptr,
       a);
   if (nblk > mgb::kFusedScanMaxBlocks)
     mgb_host::launch(mgb::router_scan_kernel, dim3(E), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream), nullptr,
