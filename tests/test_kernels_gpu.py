@@ -230,9 +230,10 @@ def test_decode_attn_gqa_dynamic_schedule(B, ctx):
         assert int(sched.abs().sum()) == 0
 
 
-def test_rope_append_matches_oracle():
+@pytest.mark.parametrize("B", [3, 301, 1001])  # 301 / 1001: several tokens per CTA (decode batches)
+def test_rope_append_matches_oracle(B):
     ops = _ops()
-    B, Hq, Hkv, hd, pos = 3, 8, 2, 32, 70
+    Hq, Hkv, hd, pos = 8, 2, 32, 70
     page = ops.kv_page_size()
     pps = 2
     qkv = uniform_bf16((B, (Hq + 2 * Hkv) * hd), 6, 1, 1.0)
@@ -244,10 +245,11 @@ def test_rope_append_matches_oracle():
     vc = torch.zeros_like(kc)
     qo = torch.zeros(B, Hq * hd, dtype=BF16, device="cuda")
     bt = torch.arange(B * pps, dtype=torch.int32, device="cuda").view(B, pps)
-    positions = torch.full((B,), pos, dtype=torch.int32, device="cuda")
+    pos_h = pos + torch.arange(B, dtype=torch.int32) % 7  # ragged: pages 1, slots 6..12
+    positions = pos_h.cuda()
     lens = torch.zeros(B, dtype=torch.int32, device="cuda")
     ops.rope_append_gqa(qkv.cuda(), 0, positions, cos_t.cuda(), sin_t.cuda(), Hq, Hkv, hd, bt, kc, vc, qo, lens)
-    cos, sin = R.rope_cos_sin(theta, hd, torch.full((B,), pos))
+    cos, sin = R.rope_cos_sin(theta, hd, pos_h.long())
     q = qkv[:, :Hq * hd].view(B, Hq, hd)
     k = qkv[:, Hq * hd:(Hq + Hkv) * hd].view(B, Hkv, hd)
     v = qkv[:, (Hq + Hkv) * hd:].view(B, Hkv, hd)
@@ -256,10 +258,11 @@ def test_rope_append_matches_oracle():
     kp = kc.cpu().view(B * pps, Hkv, hd // 8, page, 8)
     vp = vc.cpu().view(B * pps, Hkv, hd // 8, page, 8)
     for b in range(B):
-        pg, s = b * pps + pos // page, pos % page
+        pb = int(pos_h[b])
+        pg, s = b * pps + pb // page, pb % page
         assert torch.equal(kp[pg, :, :, s, :].reshape(Hkv, hd), kref[b])
         assert torch.equal(vp[pg, :, :, s, :].reshape(Hkv, hd), v[b])
-    assert torch.equal(lens.cpu(), torch.full((B,), pos + 1, dtype=torch.int32))
+    assert torch.equal(lens.cpu(), pos_h + 1)
 
 
 @pytest.mark.parametrize("B,Hq,Hkv,hd", [(37, 32, 8, 128), (300, 32, 8, 128), (9, 8, 2, 32), (5, 16, 4, 64)])
