@@ -240,8 +240,13 @@ class _SymmComm:
         dist.all_gather_into_tensor(self.counts_all, counts, group=self.group)
         return self.counts_all
 
+    # a peer that died must not leave the others spinning on the signal pad forever (a stuck GPU):
+    # the barrier kernel traps after this long (ranks that are merely slower -- engine set-up of a
+    # large model -- stay well inside it)
+    BARRIER_TIMEOUT_MS = 300_000
+
     def barrier(self) -> None:
-        self.handle.barrier()
+        self.handle.barrier(timeout_ms=self.BARRIER_TIMEOUT_MS)
 
 
 class VirtualPeerGroup:
