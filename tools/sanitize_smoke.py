@@ -31,6 +31,19 @@ ws = ops.RouterWorkspace(T, E, k)
 h = torch.zeros(T, d, dtype=BF, device=dev)
 xp = torch.zeros(T * k, d, dtype=BF, device=dev)
 ops.moe_route(x, o, ln, 1e-5, h, wr, ws, xp, 0, x_out=torch.zeros_like(x))
+ops.moe_route(x, o, ln, 1e-5, None, wr, ops.RouterWorkspace(T, E, k), torch.zeros_like(xp), 0,
+              x_out=torch.zeros_like(x))  # one pass without h_out (decode batches)
+# > 1 chunk per CTA (rows re-read from h_out) on a wider batch
+T2 = 3001
+x2 = uniform_bf16((T2, d), 0, 6, 1.0).to(dev)
+ops.moe_route(x2, None, ln, 1e-5, torch.zeros_like(x2), wr, ops.RouterWorkspace(T2, E, k),
+              torch.zeros(T2 * k, d, dtype=BF, device=dev), 0)
+# DeepSeek-width router over given logits (many CTAs: separate column scan)
+lg2 = torch.randn(T2, 64, device=dev)
+ops.router_topk(None, None, ops.RouterWorkspace(T2, 64, 6), 6, 1, logits_in=lg2)
+# an expert-parallel rank's weight shard generated in place
+from paper_2503_09716_b200.weights import fill_uniform_  # noqa: E402
+fill_uniform_(torch.empty(4097, dtype=BF, device=dev), 0, 7, 0.02, first=123)
 # (cuBLAS writes its output with TMA stores, which initcheck does not count as initialisation: copy it
 # through a plain kernel so the router's reads are not reported)
 lg = torch.mm(h, wr.t(), out_dtype=torch.float32).mul(1.0)
