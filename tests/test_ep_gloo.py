@@ -64,6 +64,35 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
+def _run_world(target, world, attempts: int = 3):
+    """Spawn `world` gloo ranks on a fresh port and return rank 0's result.  A rendezvous that fails
+    (the free port taken between probe and bind, a slow spawn on a loaded host) is retried on a new
+    port; a rank that runs and fails its checks fails the test on the last attempt."""
+    import queue as _queue
+
+    ctx = mp.get_context("spawn")
+    err = None
+    for _ in range(attempts):
+        q = ctx.Queue()
+        port = _free_port()
+        procs = [ctx.Process(target=target, args=(r, world, port, q)) for r in range(world)]
+        for p in procs:
+            p.start()
+        try:
+            got = q.get(timeout=300)
+        except _queue.Empty:
+            got, err = None, "rank 0 returned nothing within 300 s"
+        for p in procs:
+            p.join(timeout=120)
+            if p.exitcode is None:
+                p.kill()
+        codes = [p.exitcode for p in procs]
+        if got is not None and all(c == 0 for c in codes):
+            return got
+        err = err or f"rank exit codes {codes}"
+    raise AssertionError(f"gloo world {world} failed {attempts} times: {err}")
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -74,16 +103,7 @@ def _free_port():
 
 @pytest.mark.parametrize("world", [2, 4])
 def test_ep_dispatch_combine_matches_single_process(world):
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
-    for p in procs:
-        p.start()
-    got = q.get(timeout=120)
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
+    got = _run_world(_worker, world)
     wr, wgu, wd = _weights()
     x = _tokens(world)
     ref = R.moe_block(x, wr, wgu, wd, K, 0)
